@@ -1,0 +1,200 @@
+/* pipeplan_b200.h — C-ABI of the B200 micro-batch planner.
+ *
+ * This is the drop-in boundary underneath the reference planner's C++ API
+ * (include/pipeplan/microbatch.h, cost_model.h).  Every signature uses plain
+ * pointers, sizes and POD descriptors — no C++ or torch types — so a ctypes /
+ * cgo / JNI stub can bind it directly (INTEGRATION.md shows the bindings).
+ *
+ * What each entry point replaces in the reference (/root/reference/proj):
+ *
+ *   pp_order_samples     order_samples(mb, OrderMethod::Sort)
+ *                          src/microbatch.cpp:97-105, include/pipeplan/microbatch.h:59-63
+ *   pp_plan_grid         order_samples(Sort) -> make_slice_cost(grid, cfg, ordered, r)
+ *                          -> dp_partition(ordered, cost, opts), batched over
+ *                          independent mini-batches (the run_plan worker pool,
+ *                          src/driver.cpp:222-242).  Slice costing is
+ *                          estimate()/ProfileGrid::per_layer (src/cost_model.cpp:126-150,
+ *                          294-319) evaluated on the device, bit-exact.
+ *                          include/pipeplan/microbatch.h:64-95
+ *   pp_plan_grid_device  same, device-resident inputs/outputs on a caller stream
+ *   pp_plan_tables       dp_partition() with an arbitrary SliceCostFn: the caller
+ *                          evaluates the callback into the triangular tables the
+ *                          reference builds at src/microbatch.cpp:228-243.
+ *
+ * Errors: a C-ABI cannot throw.  Every call returns a pp_status; per
+ * mini-batch results carry their own status.  The C++ wrapper
+ * (pipeplan::dp_partition) re-throws the reference's exception types with the
+ * reference's messages (src/microbatch.cpp:98,222-226,248-250,320).
+ *
+ * Threading: a pp_ctx owns a CUDA stream and scratch buffers.  Calls on one
+ * ctx are serialised by the caller; use one ctx per host thread (the C++
+ * wrapper keeps a thread_local ctx), which matches the reference's reentrant,
+ * thread-pooled use (src/driver.cpp:222-242).
+ */
+#ifndef PIPEPLAN_B200_H_
+#define PIPEPLAN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PP_ABI_VERSION 1
+
+typedef enum pp_status {
+  PP_OK = 0,
+  PP_ERR_INVALID = 1,          /* std::invalid_argument in the reference     */
+  PP_ERR_INFEASIBLE_SAMPLE = 2,/* InfeasibleError(sample_id, -1), :248-250   */
+  PP_ERR_INFEASIBLE = 3,       /* InfeasibleError(-1, -1), :320              */
+  PP_ERR_CUDA = 4,             /* device error (distinct from domain errors) */
+  PP_ERR_NO_DEVICE = 5,        /* no CUDA device: the product never falls back to CPU */
+  PP_ERR_OUT_OF_RANGE = 6      /* std::out_of_range (cost_model.cpp:297-298) */
+} pp_status;
+
+/* Same layout as pipeplan::Sample (include/pipeplan/workload.h:27-33). */
+typedef struct pp_sample {
+  int64_t id;
+  int64_t input_len;
+  int64_t target_len;
+} pp_sample;
+
+/* A profile grid (reference ProfileGrid, cost_model.h:74-105).  cells holds
+ * [kind(2)][recompute(3)][n_mbs][n_seq][3] doubles, fields (t_f, t_b, act_mem),
+ * in the reference's cell_index order (src/cost_model.cpp:69-73). */
+typedef struct pp_grid_desc {
+  int32_t n_mbs;
+  int32_t n_seq;
+  const int64_t* mbs_axis;
+  const int64_t* seq_axis;
+  const double* cells;
+} pp_grid_desc;
+
+/* Reference ModelConfig (cost_model.h:113-127) reduced to what costing reads,
+ * plus the recompute strategy passed to make_slice_cost. */
+typedef struct pp_model_desc {
+  int32_t n_stages;
+  const int32_t* encoder_layers; /* [n_stages] */
+  const int32_t* decoder_layers; /* [n_stages] */
+  int32_t is_encoder_decoder;
+  int32_t recompute;             /* 0 None, 1 Selective, 2 Full */
+} pp_model_desc;
+
+/* Reference DpOptions (microbatch.h:79-86). */
+typedef struct pp_dp_options {
+  int32_t stage_count;
+  int32_t replica_count;
+  double per_mb_mem_cap;   /* +inf = no cap */
+  double t_max_interval;   /* 0 = exact candidate set */
+} pp_dp_options;
+
+/* Planner knobs that never change results, only the schedule of work. */
+typedef struct pp_tuning {
+  int32_t first_wave;      /* t_max candidates evaluated in the first wave (>=1) */
+  int32_t max_wave;        /* cap on a wave's candidates per mini-batch */
+  int32_t reserved[6];
+} pp_tuning;
+
+/* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are
+ * indexed like the input (segment s occupies [seg_offsets[s], seg_offsets[s+1])).
+ *   ordered   : the order_samples(Sort) permutation of the segment (may be NULL)
+ *   splits    : exclusive end of each micro-batch, relative to the segment start
+ *               (the reference's Best::splits, microbatch.cpp:284); first
+ *               count[s] entries valid
+ *   mb_times  : slice time of each chosen micro-batch (microbatch.cpp:328)
+ *   count, t_max_used, objective, status, err_sample_id : per segment
+ *   (objective is eval_objective over mb_times, microbatch.cpp:333-334;
+ *    t_max_used follows microbatch.cpp:335). */
+typedef struct pp_plan_out {
+  pp_sample* ordered;
+  int32_t* splits;
+  double* mb_times;
+  int32_t* count;
+  double* t_max_used;
+  double* objective;
+  int32_t* status;
+  int64_t* err_sample_id;
+} pp_plan_out;
+
+/* Work counters for the last call (for benchmarks / rooflines). */
+typedef struct pp_stats {
+  int64_t candidates_generated;   /* sum over segments of |unique candidates| */
+  int64_t candidates_evaluated;   /* DP passes actually run on the device      */
+  int64_t transitions_executed;   /* DP transitions visited on the device      */
+  int64_t transitions_reference;  /* n(n+1)/2 x passes the reference would run */
+  int64_t slices_costed;          /* fused slice-cost evaluations              */
+  int64_t waves;                  /* candidate waves launched                  */
+  double  ms_sort, ms_cost, ms_dp, ms_total;  /* device time per phase          */
+} pp_stats;
+
+typedef struct pp_ctx pp_ctx;
+
+int pp_abi_version(void);
+int pp_ctx_create(int device, pp_ctx** out);
+int pp_ctx_destroy(pp_ctx* ctx);
+const char* pp_ctx_last_error(const pp_ctx* ctx);
+int pp_ctx_set_tuning(pp_ctx* ctx, const pp_tuning* tuning);
+int pp_ctx_get_stats(const pp_ctx* ctx, pp_stats* out);
+/* Optional: let the planner run on a caller-owned cudaStream_t. */
+int pp_ctx_set_stream(pp_ctx* ctx, void* cuda_stream);
+
+/* Segmented order_samples(Sort): host in, host out. */
+int pp_order_samples(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets,
+                     int32_t n_seg, pp_sample* out);
+
+/* order_samples(Sort) + make_slice_cost + dp_partition for n_seg independent
+ * mini-batches.  Host buffers in and out.  presorted != 0 skips the sort and
+ * treats each segment as already ordered (the dp_partition(span) entry). */
+int pp_plan_grid(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets,
+                 int32_t n_seg, int32_t presorted, const pp_grid_desc* grid,
+                 const pp_model_desc* model, const pp_dp_options* opts, pp_plan_out* out);
+
+/* Same computation; samples / seg_offsets / every pp_plan_out array are
+ * DEVICE pointers.  grid / model / opts descriptors are host structs. */
+int pp_plan_grid_device(pp_ctx* ctx, const pp_sample* d_samples, const int64_t* d_seg_offsets,
+                        const int64_t* h_seg_offsets, int32_t n_seg, int32_t presorted,
+                        const pp_grid_desc* grid, const pp_model_desc* model,
+                        const pp_dp_options* opts, pp_plan_out* d_out);
+
+/* dp_partition over host-evaluated triangular slice tables: row i holds
+ * slices [i, j) for j in (i, n] at index row_offset(i) + (j - i - 1)
+ * (src/microbatch.cpp:228-243).  On PP_ERR_INFEASIBLE_SAMPLE, *err_index is
+ * the ordered index of the offending sample. */
+int pp_plan_tables(pp_ctx* ctx, const double* slice_time, const double* slice_mem, int64_t n,
+                   const pp_dp_options* opts, int32_t* splits, double* mb_times, int32_t* count,
+                   double* t_max_used, double* objective, int64_t* err_index);
+
+/* Per segment: min / max slice time over memory-feasible slices (the
+ * unquantized candidate range, microbatch.cpp:260-266 with I = 0), computed by
+ * the device cost pass.  Used to map "K candidates" onto t_max_interval. */
+int pp_candidate_range(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets,
+                       int32_t n_seg, int32_t presorted, const pp_grid_desc* grid,
+                       const pp_model_desc* model, double per_mb_mem_cap, double* t_min,
+                       double* t_max);
+
+/* ---- host helpers (no device work): the drop-in C++ API exposed to C ---- */
+/* eval_objective (microbatch.cpp:109-120) */
+int pp_eval_objective(const double* times, int64_t m, int32_t stage_count, int32_t replica_count,
+                      double* out);
+/* ProfileGrid::synthetic (cost_model.cpp:91-124).  params = {alpha, beta, gamma,
+ * full_mem_factor, selective_mem_factor, full_tb_penalty, selective_tb_penalty};
+ * empty axes (n = 0) select the defaults.  out_mbs/out_seq need 64 entries,
+ * out_cells 2*3*n_mbs*n_seq*3; out_sizes receives (n_mbs, n_seq). */
+int pp_synthetic_grid(const double* params, int32_t tp_degree, const int64_t* mbs_axis,
+                      int32_t n_mbs, const int64_t* seq_axis, int32_t n_seq, int64_t* out_mbs,
+                      int64_t* out_seq, int32_t* out_sizes, double* out_cells);
+/* load_dataset with a synthetic descriptor (workload.cpp:50-63,109-127).
+ * dist = {family(0 lognormal,1 uniform,2 mixture), log_mean, log_sigma,
+ *         uniform_lo, uniform_hi, lognormal_weight}; tgt_dist may be NULL. */
+int pp_synthetic_dataset(int64_t n, const double* in_dist, const double* tgt_dist,
+                         int64_t max_seq_len, uint64_t seed, pp_sample* out);
+/* The make_slice_cost lambda on the host for one slice [begin, end). */
+int pp_slice_cost_host(const pp_grid_desc* grid, const pp_model_desc* model,
+                       const pp_sample* ordered, int64_t begin, int64_t end, double* time,
+                       double* act_mem);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPEPLAN_B200_H_ */

@@ -1,0 +1,306 @@
+"""ctypes bindings of the CHECKERS (test infrastructure only).
+
+* ``Oracle``    — liboracle.so, the plain-C restatement (pp_oracle.c).
+* ``Reference`` — _ref/libpipeplan_ref.so, the unmodified reference planner
+  (/root/reference/proj/src/*.cpp) behind ref_shim.cpp.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm import this module.  Both expose ``plan(samples, grid, model, ...)`` and
+``plan_tables(T, M, n, ...)`` returning the same ``Plan`` record the product
+binding returns, so parity checks compare like with like.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libpipeplan_ref.so")
+REF_SRC = "/root/reference/proj"
+
+PP_OK, PP_ERR_INVALID, PP_ERR_INFEASIBLE_SAMPLE, PP_ERR_INFEASIBLE = 0, 1, 2, 3
+
+
+def build(ref: bool = True) -> None:
+    """make liboracle.so (always) and _ref/ (when the reference tree exists)."""
+    subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+    if ref and os.path.isdir(REF_SRC):
+        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class _GridDesc(C.Structure):
+    _fields_ = [("n_mbs", C.c_int32), ("n_seq", C.c_int32), ("mbs_axis", C.c_void_p),
+                ("seq_axis", C.c_void_p), ("cells", C.c_void_p)]
+
+
+class _ModelDesc(C.Structure):
+    _fields_ = [("n_stages", C.c_int32), ("encoder_layers", C.c_void_p),
+                ("decoder_layers", C.c_void_p), ("is_encoder_decoder", C.c_int32),
+                ("recompute", C.c_int32)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("stage_count", C.c_int32), ("replica_count", C.c_int32),
+                ("per_mb_mem_cap", C.c_double), ("t_max_interval", C.c_double)]
+
+
+def grid_desc(grid):
+    mb = np.ascontiguousarray(grid.mbs_axis, np.int64)
+    sq = np.ascontiguousarray(grid.seq_axis, np.int64)
+    ce = np.ascontiguousarray(grid.cells, np.float64)
+    return _GridDesc(len(mb), len(sq), _p(mb), _p(sq), _p(ce)), (mb, sq, ce)
+
+
+def model_desc(model):
+    enc = np.ascontiguousarray(model.encoder_layers, np.int32)
+    dec = np.ascontiguousarray(model.decoder_layers, np.int32)
+    return _ModelDesc(len(enc), _p(enc), _p(dec), int(model.is_encoder_decoder),
+                      int(model.recompute)), (enc, dec)
+
+
+class CheckerPlan:
+    def __init__(self, status, splits=None, mb_times=None, t_max_used=math.nan,
+                 objective=math.nan, err_sample_id=-1, ordered=None, n_candidates=-1,
+                 n_evaluated=-1, replica=None, max_load=math.nan):
+        self.status = status
+        self.splits = splits
+        self.mb_times = mb_times
+        self.t_max_used = t_max_used
+        self.objective = objective
+        self.err_sample_id = err_sample_id
+        self.ordered = ordered
+        self.n_candidates = n_candidates
+        self.n_evaluated = n_evaluated
+        self.replica = replica
+        self.max_load = max_load
+
+
+class Oracle:
+    """The C restatement."""
+
+    def __init__(self):
+        if not os.path.exists(ORACLE_SO):
+            build(ref=False)
+        L = C.CDLL(ORACLE_SO)
+        vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.orc_order_samples.argtypes = [vp, i64, vp]
+        L.orc_per_layer.argtypes = [C.POINTER(_GridDesc), i32, i32, dbl, dbl, vp]
+        L.orc_slice_cost.argtypes = [C.POINTER(_GridDesc), C.POINTER(_ModelDesc), vp, i64, i64, vp, vp]
+        L.orc_dp_tables.argtypes = [vp, vp, i64, C.POINTER(_Opts), vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_plan_grid.argtypes = [vp, i64, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc),
+                                    C.POINTER(_Opts), vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_eval_objective.argtypes = [vp, i64, i32, i32, vp]
+        L.orc_slice_extrema.argtypes = [vp, i64, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), dbl,
+                                        vp, vp]
+        self.L = L
+
+    def slice_extrema(self, ordered, grid, model, mem_cap=math.inf):
+        """(max memory-feasible slice time, max singleton act_mem)."""
+        o = np.ascontiguousarray(ordered, np.int64).reshape(-1, 3)
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        t, a = np.zeros(1), np.zeros(1)
+        self.L.orc_slice_extrema(_p(o), len(o), C.byref(g), C.byref(m), mem_cap, _p(t), _p(a))
+        return float(t[0]), float(a[0])
+
+    def order_samples(self, samples):
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        out = np.empty_like(s)
+        rc = self.L.orc_order_samples(_p(s), len(s), _p(out))
+        if rc != PP_OK:
+            raise ValueError("mini-batch is empty")
+        return out
+
+    def per_layer(self, grid, kind, r, mbs, seq):
+        g, keep = grid_desc(grid)
+        out = np.zeros(3)
+        self.L.orc_per_layer(C.byref(g), kind, r, float(mbs), float(seq), _p(out))
+        return out
+
+    def slice_cost(self, grid, model, ordered, begin, end):
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        o = np.ascontiguousarray(ordered, np.int64)
+        t, a = np.zeros(1), np.zeros(1)
+        self.L.orc_slice_cost(C.byref(g), C.byref(m), _p(o), begin, end, _p(t), _p(a))
+        return float(t[0]), float(a[0])
+
+    def eval_objective(self, times, c, d):
+        t = np.ascontiguousarray(times, np.float64)
+        out = np.zeros(1)
+        rc = self.L.orc_eval_objective(_p(t), len(t), c, d, _p(out))
+        if rc != PP_OK:
+            raise ValueError("bad objective arguments")
+        return float(out[0])
+
+    def plan_tables(self, T, M, n, stage_count, replica_count=1, mem_cap=math.inf,
+                    t_max_interval=5.0):
+        T = np.ascontiguousarray(T, np.float64)
+        M = np.ascontiguousarray(M, np.float64)
+        sp = np.zeros(max(n, 1), np.int32)
+        tt = np.zeros(max(n, 1))
+        cnt = np.zeros(1, np.int32)
+        tm, ob = np.zeros(1), np.zeros(1)
+        err = np.full(1, -1, np.int64)
+        nc = np.zeros(1, np.int64)
+        ne = np.zeros(1, np.int64)
+        o = _Opts(stage_count, replica_count, mem_cap, t_max_interval)
+        rc = self.L.orc_dp_tables(_p(T), _p(M), n, C.byref(o), _p(sp), _p(tt), _p(cnt), _p(tm),
+                                  _p(ob), _p(err), _p(nc), _p(ne))
+        if rc != PP_OK:
+            return CheckerPlan(rc, err_sample_id=int(err[0]))
+        m = int(cnt[0])
+        return CheckerPlan(PP_OK, sp[:m].copy(), tt[:m].copy(), float(tm[0]), float(ob[0]),
+                           n_candidates=int(nc[0]), n_evaluated=int(ne[0]))
+
+    def plan(self, samples, grid, model, stage_count, replica_count=1, mem_cap=math.inf,
+             t_max_interval=5.0, presorted=False):
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        n = len(s)
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        o = _Opts(stage_count, replica_count, mem_cap, t_max_interval)
+        ordered = np.empty_like(s)
+        sp = np.zeros(max(n, 1), np.int32)
+        tt = np.zeros(max(n, 1))
+        cnt = np.zeros(1, np.int32)
+        tm, ob = np.zeros(1), np.zeros(1)
+        err = np.full(1, -1, np.int64)
+        nc = np.zeros(1, np.int64)
+        ne = np.zeros(1, np.int64)
+        rc = self.L.orc_plan_grid(_p(s), n, int(presorted), C.byref(g), C.byref(m), C.byref(o),
+                                  _p(ordered), _p(sp), _p(tt), _p(cnt), _p(tm), _p(ob), _p(err),
+                                  _p(nc), _p(ne))
+        if rc != PP_OK:
+            return CheckerPlan(rc, err_sample_id=int(err[0]), ordered=ordered)
+        k = int(cnt[0])
+        return CheckerPlan(PP_OK, sp[:k].copy(), tt[:k].copy(), float(tm[0]), float(ob[0]),
+                           ordered=ordered, n_candidates=int(nc[0]), n_evaluated=int(ne[0]))
+
+
+class Reference:
+    """The unmodified reference planner (compiled from /root/reference)."""
+
+    def __init__(self):
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference at build time)")
+        L = C.CDLL(REF_SO)
+        vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.ref_order_samples.argtypes = [vp, i64, vp]
+        L.ref_per_layer.argtypes = [C.POINTER(_GridDesc), i32, i32, dbl, dbl, vp]
+        L.ref_synthetic_grid.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp]
+        L.ref_load_dataset.argtypes = [i64, vp, vp, i64, C.c_uint64, vp]
+        L.ref_plan_grid.argtypes = [vp, i64, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc),
+                                    C.POINTER(_Opts), vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.ref_plan_tables.argtypes = [vp, vp, i64, C.POINTER(_Opts), vp, vp, vp, vp, vp, vp, vp, vp]
+        L.ref_plan_batch.argtypes = [vp, vp, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc),
+                                     C.POINTER(_Opts), i32, vp, vp, vp, vp]
+        L.ref_plan_batch.restype = dbl
+        self.L = L
+
+    def order_samples(self, samples):
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        out = np.empty_like(s)
+        rc = self.L.ref_order_samples(_p(s), len(s), _p(out))
+        if rc != PP_OK:
+            raise ValueError("mini-batch is empty")
+        return out
+
+    def per_layer(self, grid, kind, r, mbs, seq):
+        g, keep = grid_desc(grid)
+        out = np.zeros(3)
+        self.L.ref_per_layer(C.byref(g), kind, r, float(mbs), float(seq), _p(out))
+        return out
+
+    def synthetic_grid_cells(self, params7, tp, mbs_axis=(), seq_axis=()):
+        par = np.asarray(params7, np.float64)
+        ma = np.asarray(mbs_axis, np.int64)
+        sa = np.asarray(seq_axis, np.int64)
+        om, os_ = np.zeros(64, np.int64), np.zeros(64, np.int64)
+        sizes = np.zeros(2, np.int32)
+        cells = np.zeros(18 * 64 * 64)
+        rc = self.L.ref_synthetic_grid(_p(par), tp, _p(ma), len(ma), _p(sa), len(sa), _p(om),
+                                       _p(os_), _p(sizes), _p(cells))
+        if rc != PP_OK:
+            raise ValueError("invalid synthetic grid")
+        nm, ns = int(sizes[0]), int(sizes[1])
+        return om[:nm].copy(), os_[:ns].copy(), cells[:18 * nm * ns].reshape(2, 3, nm, ns, 3).copy()
+
+    def load_dataset(self, n, max_seq_len, seed, input_dist, target_dist=None):
+        out = np.zeros((n, 3), np.int64)
+        ind = np.asarray(input_dist, np.float64)
+        tgd = None if target_dist is None else np.asarray(target_dist, np.float64)
+        rc = self.L.ref_load_dataset(n, _p(ind), _p(tgd), max_seq_len, seed, _p(out))
+        if rc != PP_OK:
+            raise ValueError("invalid dataset spec")
+        return out
+
+    def plan(self, samples, grid, model, stage_count, replica_count=1, mem_cap=math.inf,
+             t_max_interval=5.0, presorted=False):
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        n = len(s)
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        o = _Opts(stage_count, replica_count, mem_cap, t_max_interval)
+        ordered = np.empty_like(s)
+        sp = np.zeros(max(n, 1), np.int32)
+        tt = np.zeros(max(n, 1))
+        rep = np.zeros(max(n, 1), np.int32)
+        cnt = np.zeros(1, np.int32)
+        tm, ob, ml = np.zeros(1), np.zeros(1), np.zeros(1)
+        err = np.full(1, -1, np.int64)
+        rc = self.L.ref_plan_grid(_p(s), n, int(presorted), C.byref(g), C.byref(m), C.byref(o),
+                                  _p(ordered), _p(sp), _p(tt), _p(cnt), _p(tm), _p(ob), _p(ml),
+                                  _p(rep), _p(err))
+        if rc != PP_OK:
+            return CheckerPlan(rc, err_sample_id=int(err[0]))
+        k = int(cnt[0])
+        return CheckerPlan(PP_OK, sp[:k].copy(), tt[:k].copy(), float(tm[0]), float(ob[0]),
+                           ordered=ordered, replica=rep[:k].copy(), max_load=float(ml[0]))
+
+    def plan_tables(self, T, M, n, stage_count, replica_count=1, mem_cap=math.inf,
+                    t_max_interval=5.0):
+        T = np.ascontiguousarray(T, np.float64)
+        M = np.ascontiguousarray(M, np.float64)
+        sp = np.zeros(max(n, 1), np.int32)
+        tt = np.zeros(max(n, 1))
+        rep = np.zeros(max(n, 1), np.int32)
+        cnt = np.zeros(1, np.int32)
+        tm, ob, ml = np.zeros(1), np.zeros(1), np.zeros(1)
+        err = np.full(1, -1, np.int64)
+        o = _Opts(stage_count, replica_count, mem_cap, t_max_interval)
+        rc = self.L.ref_plan_tables(_p(T), _p(M), n, C.byref(o), _p(sp), _p(tt), _p(cnt), _p(tm),
+                                    _p(ob), _p(ml), _p(rep), _p(err))
+        if rc != PP_OK:
+            return CheckerPlan(rc, err_sample_id=int(err[0]))
+        k = int(cnt[0])
+        return CheckerPlan(PP_OK, sp[:k].copy(), tt[:k].copy(), float(tm[0]), float(ob[0]),
+                           replica=rep[:k].copy(), max_load=float(ml[0]))
+
+    def plan_batch_timed(self, samples, seg_offsets, grid, model, stage_count, replica_count=1,
+                         mem_cap=math.inf, t_max_interval=5.0, threads=1):
+        """run_plan-style worker pool; returns (wall seconds, t_max, objective, count, status)."""
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        off = np.ascontiguousarray(seg_offsets, np.int64)
+        S = len(off) - 1
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        o = _Opts(stage_count, replica_count, mem_cap, t_max_interval)
+        tm, ob = np.zeros(S), np.zeros(S)
+        cnt, st = np.zeros(S, np.int32), np.zeros(S, np.int32)
+        secs = self.L.ref_plan_batch(_p(s), _p(off), S, C.byref(g), C.byref(m), C.byref(o), threads,
+                                     _p(tm), _p(ob), _p(cnt), _p(st))
+        return secs, tm, ob, cnt, st

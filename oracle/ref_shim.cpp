@@ -1,0 +1,317 @@
+// ref_shim.cpp — C-ABI shim over the UNMODIFIED reference planner.
+//
+// TEST INFRASTRUCTURE ONLY.  Linked with /root/reference/proj/src/{workload,
+// cost_model,microbatch}.cpp into oracle/_ref/libpipeplan_ref.so by
+// oracle/Makefile.  It lets pytest (ctypes) and bench.py's reference arm call
+// the reference's own public API — order_samples, make_slice_cost,
+// dp_partition, ProfileGrid, load_dataset — with no code of ours on the
+// planning path.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+#include <stdexcept>
+#include <thread>
+#include <atomic>
+#include <vector>
+
+#include "pipeplan/cost_model.h"
+#include "pipeplan/errors.h"
+#include "pipeplan/microbatch.h"
+#include "pipeplan/workload.h"
+#include "pipeplan_b200.h"
+
+using namespace pipeplan;
+
+namespace {
+
+// ProfileGrid has no public cell setter; round-trip the descriptor through
+// the reference's own text loader (cost_model.cpp:193-271) at %.17g.
+ProfileGrid grid_from_desc(const pp_grid_desc* g) {
+  static const char* kinds[2] = {"encoder", "decoder"};
+  static const char* strats[3] = {"none", "selective", "full"};
+  std::ostringstream os;
+  os.precision(17);
+  os << "pipeplan-grid 1\nmbs_axis";
+  for (int i = 0; i < g->n_mbs; ++i) os << ' ' << g->mbs_axis[i];
+  os << "\nseq_axis";
+  for (int i = 0; i < g->n_seq; ++i) os << ' ' << g->seq_axis[i];
+  os << '\n';
+  std::size_t c = 0;
+  for (int k = 0; k < 2; ++k)
+    for (int r = 0; r < 3; ++r)
+      for (int mi = 0; mi < g->n_mbs; ++mi)
+        for (int si = 0; si < g->n_seq; ++si, c += 3)
+          os << "row " << kinds[k] << ' ' << strats[r] << ' ' << g->mbs_axis[mi] << ' '
+             << g->seq_axis[si] << ' ' << g->cells[c] << ' ' << g->cells[c + 1] << ' '
+             << g->cells[c + 2] << '\n';
+  os << "end\n";
+  std::istringstream is(os.str());
+  return ProfileGrid::load(is);
+}
+
+ModelConfig model_from_desc(const pp_model_desc* m) {
+  ModelConfig cfg;
+  cfg.is_encoder_decoder = m->is_encoder_decoder != 0;
+  cfg.stages.resize(static_cast<std::size_t>(m->n_stages));
+  for (int j = 0; j < m->n_stages; ++j)
+    cfg.stages[static_cast<std::size_t>(j)] = {m->encoder_layers[j], m->decoder_layers[j]};
+  return cfg;
+}
+
+DpOptions opts_from_desc(const pp_dp_options* o) {
+  DpOptions d;
+  d.stage_count = o->stage_count;
+  d.replica_count = o->replica_count;
+  d.per_mb_mem_cap = o->per_mb_mem_cap;
+  d.t_max_interval = o->t_max_interval;
+  return d;
+}
+
+struct PlanResult {
+  int status = PP_OK;
+  std::int64_t err_id = -1;
+  std::vector<Sample> ordered;
+  MicroBatchPartition part;
+};
+
+PlanResult plan_one(const Sample* s, std::int64_t n, int presorted, const ProfileGrid& grid,
+                    const ModelConfig& cfg, Recompute r, const DpOptions& opt) {
+  PlanResult res;
+  try {
+    MiniBatch mb;
+    mb.samples.assign(s, s + n);
+    res.ordered = presorted ? mb.samples : order_samples(mb, OrderMethod::Sort);
+    SliceCostFn cost = make_slice_cost(grid, cfg, res.ordered, r);
+    res.part = dp_partition(res.ordered, cost, opt);
+  } catch (const InfeasibleError& e) {
+    res.status = e.sample_id() >= 0 ? PP_ERR_INFEASIBLE_SAMPLE : PP_ERR_INFEASIBLE;
+    res.err_id = e.sample_id();
+  } catch (const std::out_of_range&) {
+    res.status = PP_ERR_OUT_OF_RANGE;
+  } catch (const std::invalid_argument&) {
+    res.status = PP_ERR_INVALID;
+  }
+  return res;
+}
+
+void write_result(const PlanResult& res, std::int64_t n, pp_sample* ordered, int32_t* splits,
+                  double* mb_times, int32_t* count, double* t_max_used, double* objective,
+                  double* max_load, int32_t* replica, int64_t* err_id,
+                  const std::vector<double>* times) {
+  if (err_id) *err_id = res.err_id;
+  if (res.status != PP_OK) return;
+  if (ordered) std::memcpy(ordered, res.ordered.data(), sizeof(pp_sample) * n);
+  int32_t end = 0;
+  for (std::size_t k = 0; k < res.part.micro_batches.size(); ++k) {
+    end += static_cast<int32_t>(res.part.micro_batches[k].sample_ids.size());
+    splits[k] = end;
+    if (replica) replica[k] = res.part.replica_assignment[k];
+    if (mb_times && times) mb_times[k] = (*times)[k];
+  }
+  *count = static_cast<int32_t>(res.part.micro_batches.size());
+  *t_max_used = res.part.t_max_used;
+  *objective = res.part.objective_value;
+  if (max_load) *max_load = res.part.max_replica_load;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_order_samples(const pp_sample* in, int64_t n, pp_sample* out) {
+  try {
+    MiniBatch mb;
+    mb.samples.assign(reinterpret_cast<const Sample*>(in), reinterpret_cast<const Sample*>(in) + n);
+    auto o = order_samples(mb, OrderMethod::Sort);
+    std::memcpy(out, o.data(), sizeof(pp_sample) * o.size());
+    return PP_OK;
+  } catch (const std::invalid_argument&) {
+    return PP_ERR_INVALID;
+  }
+}
+
+int ref_per_layer(const pp_grid_desc* g, int32_t kind, int32_t r, double mbs, double seq,
+                  double out[3]) {
+  ProfileGrid grid = grid_from_desc(g);
+  GridCell c = grid.per_layer(static_cast<StageKind>(kind), static_cast<Recompute>(r), mbs, seq);
+  out[0] = c.t_f;
+  out[1] = c.t_b;
+  out[2] = c.act_mem;
+  return PP_OK;
+}
+
+// ProfileGrid::synthetic (cost_model.cpp:91-124) exported as raw cells.
+int ref_synthetic_grid(const double* params8, int32_t tp_degree, const int64_t* mbs_axis,
+                       int32_t n_mbs, const int64_t* seq_axis, int32_t n_seq, int64_t* out_mbs,
+                       int64_t* out_seq, int32_t* out_sizes, double* out_cells) {
+  try {
+    SyntheticGridParams p;
+    p.alpha = params8[0];
+    p.beta = params8[1];
+    p.gamma = params8[2];
+    p.full_mem_factor = params8[3];
+    p.selective_mem_factor = params8[4];
+    p.full_tb_penalty = params8[5];
+    p.selective_tb_penalty = params8[6];
+    p.tp_degree = tp_degree;
+    std::vector<std::int64_t> ma(mbs_axis, mbs_axis + n_mbs), sa(seq_axis, seq_axis + n_seq);
+    ProfileGrid g = ProfileGrid::synthetic(p, ma, sa);
+    out_sizes[0] = static_cast<int32_t>(g.mbs_axis().size());
+    out_sizes[1] = static_cast<int32_t>(g.seq_axis().size());
+    std::memcpy(out_mbs, g.mbs_axis().data(), sizeof(int64_t) * g.mbs_axis().size());
+    std::memcpy(out_seq, g.seq_axis().data(), sizeof(int64_t) * g.seq_axis().size());
+    std::size_t c = 0;
+    for (int k = 0; k < 2; ++k)
+      for (int r = 0; r < 3; ++r)
+        for (std::size_t mi = 0; mi < g.mbs_axis().size(); ++mi)
+          for (std::size_t si = 0; si < g.seq_axis().size(); ++si) {
+            // per_layer at a knot returns the knot value exactly (t = 0 blend)
+            GridCell cell = g.per_layer(static_cast<StageKind>(k), static_cast<Recompute>(r),
+                                        static_cast<double>(g.mbs_axis()[mi]),
+                                        static_cast<double>(g.seq_axis()[si]));
+            out_cells[c++] = cell.t_f;
+            out_cells[c++] = cell.t_b;
+            out_cells[c++] = cell.act_mem;
+          }
+    return PP_OK;
+  } catch (const std::invalid_argument&) {
+    return PP_ERR_INVALID;
+  }
+}
+
+// load_dataset with a synthetic descriptor (workload.cpp:50-63,109-127).
+// dist = {family, log_mean, log_sigma, uniform_lo, uniform_hi, lognormal_weight}
+int ref_load_dataset(int64_t n, const double* in_dist, const double* tgt_dist, int64_t max_seq_len,
+                     uint64_t seed, pp_sample* out) {
+  try {
+    auto mk = [](const double* d) {
+      LengthDistribution l;
+      l.family = static_cast<LengthFamily>(static_cast<int>(d[0]));
+      l.log_mean = d[1];
+      l.log_sigma = d[2];
+      l.uniform_lo = static_cast<std::int64_t>(d[3]);
+      l.uniform_hi = static_cast<std::int64_t>(d[4]);
+      l.lognormal_weight = d[5];
+      return l;
+    };
+    DatasetSpec spec;
+    SyntheticSpec syn;
+    syn.n = n;
+    syn.input = mk(in_dist);
+    if (tgt_dist) syn.target = mk(tgt_dist);
+    spec.synthetic = syn;
+    spec.max_seq_len = max_seq_len;
+    spec.seed = seed;
+    auto s = load_dataset(spec);
+    std::memcpy(out, s.data(), sizeof(pp_sample) * s.size());
+    return PP_OK;
+  } catch (const std::invalid_argument&) {
+    return PP_ERR_INVALID;
+  }
+}
+
+// One mini-batch through the reference's production path.
+int ref_plan_grid(const pp_sample* samples, int64_t n, int32_t presorted, const pp_grid_desc* g,
+                  const pp_model_desc* m, const pp_dp_options* o, pp_sample* ordered,
+                  int32_t* splits, double* mb_times, int32_t* count, double* t_max_used,
+                  double* objective, double* max_load, int32_t* replica, int64_t* err_id) {
+  ProfileGrid grid = grid_from_desc(g);
+  ModelConfig cfg = model_from_desc(m);
+  const Recompute r = static_cast<Recompute>(m->recompute);
+  PlanResult res = plan_one(reinterpret_cast<const Sample*>(samples), n, presorted, grid, cfg, r,
+                            opts_from_desc(o));
+  std::vector<double> times;
+  if (res.status == PP_OK) {
+    SliceCostFn cost = make_slice_cost(grid, cfg, res.ordered, r);
+    std::size_t b = 0;
+    for (const auto& mb : res.part.micro_batches) {
+      times.push_back(cost(b, b + mb.sample_ids.size()).time);
+      b += mb.sample_ids.size();
+    }
+  }
+  write_result(res, n, ordered, splits, mb_times, count, t_max_used, objective, max_load, replica,
+               err_id, &times);
+  return res.status;
+}
+
+// dp_partition over given triangular tables (a generic SliceCostFn).
+int ref_plan_tables(const double* T, const double* M, int64_t n, const pp_dp_options* o,
+                    int32_t* splits, double* mb_times, int32_t* count, double* t_max_used,
+                    double* objective, double* max_load, int32_t* replica, int64_t* err_index) {
+  std::vector<std::int64_t> row_off(static_cast<std::size_t>(n));
+  std::int64_t tot = 0;
+  for (std::int64_t i = 0; i < n; ++i) {
+    row_off[static_cast<std::size_t>(i)] = tot;
+    tot += n - i;
+  }
+  std::vector<Sample> s(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) s[static_cast<std::size_t>(i)] = {i, 1, 0};
+  SliceCostFn cost = [&](std::size_t b, std::size_t e) {
+    const std::size_t idx = static_cast<std::size_t>(row_off[b]) + (e - b - 1);
+    return SliceCost{T[idx], M[idx]};
+  };
+  PlanResult res;
+  try {
+    res.part = dp_partition(s, cost, opts_from_desc(o));
+  } catch (const InfeasibleError& e) {
+    res.status = e.sample_id() >= 0 ? PP_ERR_INFEASIBLE_SAMPLE : PP_ERR_INFEASIBLE;
+    res.err_id = e.sample_id();
+  } catch (const std::invalid_argument&) {
+    res.status = PP_ERR_INVALID;
+  }
+  std::vector<double> times;
+  if (res.status == PP_OK) {
+    std::size_t b = 0;
+    for (const auto& mb : res.part.micro_batches) {
+      times.push_back(cost(b, b + mb.sample_ids.size()).time);
+      b += mb.sample_ids.size();
+    }
+  }
+  write_result(res, n, nullptr, splits, mb_times, count, t_max_used, objective, max_load, replica,
+               err_index, &times);
+  return res.status;
+}
+
+// The reference's batch-planning parallelism model (run_plan's worker pool,
+// driver.cpp:222-242): `threads` std::threads pull mini-batch indices from an
+// atomic counter; each runs order_samples(Sort) + make_slice_cost +
+// dp_partition.  Returns wall seconds; per-segment t_max/objective/count out.
+double ref_plan_batch(const pp_sample* samples, const int64_t* seg_off, int32_t n_seg,
+                      const pp_grid_desc* g, const pp_model_desc* m, const pp_dp_options* o,
+                      int32_t threads, double* t_max_used, double* objective, int32_t* count,
+                      int32_t* status) {
+  ProfileGrid grid = grid_from_desc(g);
+  ModelConfig cfg = model_from_desc(m);
+  const Recompute r = static_cast<Recompute>(m->recompute);
+  const DpOptions opt = opts_from_desc(o);
+  std::atomic<int> next{0};
+  auto t0 = std::chrono::steady_clock::now();
+  auto work = [&]() {
+    for (;;) {
+      const int s = next.fetch_add(1);
+      if (s >= n_seg) return;
+      PlanResult res =
+          plan_one(reinterpret_cast<const Sample*>(samples) + seg_off[s], seg_off[s + 1] - seg_off[s],
+                   0, grid, cfg, r, opt);
+      status[s] = res.status;
+      if (res.status == PP_OK) {
+        t_max_used[s] = res.part.t_max_used;
+        objective[s] = res.part.objective_value;
+        count[s] = static_cast<int32_t>(res.part.micro_batches.size());
+      }
+    }
+  };
+  const int nt = threads < 1 ? 1 : threads;
+  if (nt == 1) {
+    work();
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // extern "C"

@@ -1,0 +1,377 @@
+"""ctypes binding of the B200 planner C-ABI (include/pipeplan_b200.h).
+
+This is the Python face of the drop-in boundary: the same entry points a
+cgo / JNI / ctypes caller of the reference planner would bind (see
+INTEGRATION.md).  Arrays are numpy; samples are an (n, 3) int64 array of
+(id, input_len, target_len) rows — the memory layout of pipeplan::Sample.
+
+There is no CPU fallback anywhere below: if the shared library is missing the
+import fails, and if no CUDA device is present ``Planner()`` raises
+``NoDeviceError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpipeplan_b200.so")
+
+PP_OK, PP_ERR_INVALID, PP_ERR_INFEASIBLE_SAMPLE, PP_ERR_INFEASIBLE = 0, 1, 2, 3
+PP_ERR_CUDA, PP_ERR_NO_DEVICE, PP_ERR_OUT_OF_RANGE = 4, 5, 6
+
+# Every symbol include/pipeplan_b200.h declares (checked by the CPU tests).
+EXPORTED = [
+    "pp_abi_version", "pp_ctx_create", "pp_ctx_destroy", "pp_ctx_last_error", "pp_ctx_set_tuning",
+    "pp_ctx_get_stats", "pp_ctx_set_stream", "pp_order_samples", "pp_plan_grid",
+    "pp_plan_grid_device", "pp_plan_tables", "pp_candidate_range", "pp_eval_objective",
+    "pp_synthetic_grid", "pp_synthetic_dataset", "pp_slice_cost_host",
+]
+
+
+class PlannerError(RuntimeError):
+    pass
+
+
+class NoDeviceError(PlannerError):
+    pass
+
+
+class InvalidArgument(PlannerError, ValueError):
+    pass
+
+
+class InfeasibleError(PlannerError):
+    """Mirror of pipeplan::InfeasibleError (errors.h:43-56)."""
+
+    def __init__(self, msg: str, sample_id: int = -1, stage: int = -1):
+        super().__init__(msg)
+        self.sample_id = sample_id
+        self.stage = stage
+
+
+# ----------------------------------------------------------------- structs
+class GridDesc(C.Structure):
+    _fields_ = [("n_mbs", C.c_int32), ("n_seq", C.c_int32), ("mbs_axis", C.c_void_p),
+                ("seq_axis", C.c_void_p), ("cells", C.c_void_p)]
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("n_stages", C.c_int32), ("encoder_layers", C.c_void_p),
+                ("decoder_layers", C.c_void_p), ("is_encoder_decoder", C.c_int32),
+                ("recompute", C.c_int32)]
+
+
+class DpOptions(C.Structure):
+    _fields_ = [("stage_count", C.c_int32), ("replica_count", C.c_int32),
+                ("per_mb_mem_cap", C.c_double), ("t_max_interval", C.c_double)]
+
+
+class Tuning(C.Structure):
+    _fields_ = [("first_wave", C.c_int32), ("max_wave", C.c_int32), ("reserved", C.c_int32 * 6)]
+
+
+class PlanOut(C.Structure):
+    _fields_ = [("ordered", C.c_void_p), ("splits", C.c_void_p), ("mb_times", C.c_void_p),
+                ("count", C.c_void_p), ("t_max_used", C.c_void_p), ("objective", C.c_void_p),
+                ("status", C.c_void_p), ("err_sample_id", C.c_void_p)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("candidates_generated", C.c_int64), ("candidates_evaluated", C.c_int64),
+                ("transitions_executed", C.c_int64), ("transitions_reference", C.c_int64),
+                ("slices_costed", C.c_int64), ("waves", C.c_int64), ("ms_sort", C.c_double),
+                ("ms_cost", C.c_double), ("ms_dp", C.c_double), ("ms_total", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(the planner has no CPU fallback)")
+    lib = C.CDLL(_LIB_PATH)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    lib.pp_ctx_last_error.restype = C.c_char_p
+    lib.pp_ctx_last_error.argtypes = [vp]
+    lib.pp_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
+    lib.pp_ctx_destroy.argtypes = [vp]
+    lib.pp_ctx_set_tuning.argtypes = [vp, C.POINTER(Tuning)]
+    lib.pp_ctx_get_stats.argtypes = [vp, C.POINTER(Stats)]
+    lib.pp_ctx_set_stream.argtypes = [vp, vp]
+    lib.pp_order_samples.argtypes = [vp, vp, vp, i32, vp]
+    lib.pp_plan_grid.argtypes = [vp, vp, vp, i32, i32, C.POINTER(GridDesc), C.POINTER(ModelDesc),
+                                 C.POINTER(DpOptions), C.POINTER(PlanOut)]
+    lib.pp_plan_grid_device.argtypes = [vp, vp, vp, vp, i32, i32, C.POINTER(GridDesc),
+                                        C.POINTER(ModelDesc), C.POINTER(DpOptions),
+                                        C.POINTER(PlanOut)]
+    lib.pp_plan_tables.argtypes = [vp, vp, vp, i64, C.POINTER(DpOptions), vp, vp, vp, vp, vp, vp]
+    lib.pp_candidate_range.argtypes = [vp, vp, vp, i32, i32, C.POINTER(GridDesc),
+                                       C.POINTER(ModelDesc), dbl, vp, vp]
+    lib.pp_eval_objective.argtypes = [vp, i64, i32, i32, vp]
+    lib.pp_synthetic_grid.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp]
+    lib.pp_synthetic_dataset.argtypes = [i64, vp, vp, i64, C.c_uint64, vp]
+    lib.pp_slice_cost_host.argtypes = [C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, i64, i64, vp, vp]
+    return lib
+
+
+lib = _load()
+
+
+def _p(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ------------------------------------------------------------ host objects
+@dataclass
+class Grid:
+    """A ProfileGrid as flat arrays (cost_model.h:74-105 layout)."""
+    mbs_axis: np.ndarray
+    seq_axis: np.ndarray
+    cells: np.ndarray  # (2, 3, n_mbs, n_seq, 3) float64
+
+    def desc(self) -> GridDesc:
+        self.mbs_axis = np.ascontiguousarray(self.mbs_axis, dtype=np.int64)
+        self.seq_axis = np.ascontiguousarray(self.seq_axis, dtype=np.int64)
+        self.cells = np.ascontiguousarray(self.cells, dtype=np.float64)
+        return GridDesc(len(self.mbs_axis), len(self.seq_axis), _p(self.mbs_axis),
+                        _p(self.seq_axis), _p(self.cells))
+
+
+@dataclass
+class Model:
+    """ModelConfig (cost_model.h:113-127) + the Recompute passed to make_slice_cost."""
+    encoder_layers: np.ndarray
+    decoder_layers: np.ndarray
+    is_encoder_decoder: bool = False
+    recompute: int = 0
+
+    @staticmethod
+    def uniform(n_stages: int, layers_per_stage: int, encoder_decoder: bool, recompute: int = 0):
+        """ModelConfig::uniform (cost_model.cpp:273-292)."""
+        if n_stages < 1 or layers_per_stage < 1:
+            raise InvalidArgument("stage and layer counts must be >= 1")
+        enc = np.zeros(n_stages, np.int32)
+        dec = np.full(n_stages, layers_per_stage, np.int32)
+        if encoder_decoder:
+            if n_stages == 1:
+                enc[0] = layers_per_stage
+            else:
+                ne = (n_stages + 1) // 2
+                enc[:ne] = layers_per_stage
+                dec[:ne] = 0
+        return Model(enc, dec, encoder_decoder, recompute)
+
+    def desc(self) -> ModelDesc:
+        self.encoder_layers = np.ascontiguousarray(self.encoder_layers, dtype=np.int32)
+        self.decoder_layers = np.ascontiguousarray(self.decoder_layers, dtype=np.int32)
+        return ModelDesc(len(self.encoder_layers), _p(self.encoder_layers), _p(self.decoder_layers),
+                         int(self.is_encoder_decoder), int(self.recompute))
+
+
+SYNTH_DEFAULTS = dict(alpha=0.4, beta=2e-4, gamma=0.02, full_mem_factor=0.2,
+                      selective_mem_factor=0.6, full_tb_penalty=1.0, selective_tb_penalty=0.5)
+
+
+def synthetic_grid(mbs_axis=(), seq_axis=(), tp_degree: int = 1, **params) -> Grid:
+    """ProfileGrid::synthetic via the library's host implementation."""
+    p = dict(SYNTH_DEFAULTS)
+    p.update(params)
+    par = np.array([p[k] for k in ("alpha", "beta", "gamma", "full_mem_factor",
+                                   "selective_mem_factor", "full_tb_penalty",
+                                   "selective_tb_penalty")], np.float64)
+    ma = np.asarray(mbs_axis, np.int64)
+    sa = np.asarray(seq_axis, np.int64)
+    om = np.zeros(64, np.int64)
+    os_ = np.zeros(64, np.int64)
+    sizes = np.zeros(2, np.int32)
+    cells = np.zeros(18 * 64 * 64, np.float64)
+    rc = lib.pp_synthetic_grid(_p(par), tp_degree, _p(ma), len(ma), _p(sa), len(sa), _p(om), _p(os_),
+                               _p(sizes), _p(cells))
+    if rc != PP_OK:
+        raise InvalidArgument("synthetic grid coefficients must be positive")
+    nm, ns = int(sizes[0]), int(sizes[1])
+    return Grid(om[:nm].copy(), os_[:ns].copy(), cells[:18 * nm * ns].reshape(2, 3, nm, ns, 3).copy())
+
+
+LOGNORMAL, UNIFORM, MIXTURE = 0, 1, 2
+
+
+def synthetic_dataset(n: int, max_seq_len: int, seed: int, input_dist=(LOGNORMAL, 5.0, 1.5, 1, 1, 0.8),
+                      target_dist=None) -> np.ndarray:
+    """load_dataset(DatasetSpec{synthetic}) — byte-identical to the reference generator."""
+    out = np.zeros((n, 3), np.int64)
+    ind = np.asarray(input_dist, np.float64)
+    tgd = None if target_dist is None else np.asarray(target_dist, np.float64)
+    rc = lib.pp_synthetic_dataset(n, _p(ind), _p(tgd), max_seq_len, seed, _p(out))
+    if rc != PP_OK:
+        raise InvalidArgument("invalid synthetic dataset spec")
+    return out
+
+
+def slice_cost_host(grid: Grid, model: Model, ordered: np.ndarray, begin: int, end: int):
+    t = np.zeros(1)
+    m = np.zeros(1)
+    ordered = np.ascontiguousarray(ordered, np.int64)
+    rc = lib.pp_slice_cost_host(C.byref(grid.desc()), C.byref(model.desc()), _p(ordered), begin, end,
+                                _p(t), _p(m))
+    if rc != PP_OK:
+        raise InvalidArgument("slice cost failed")
+    return float(t[0]), float(m[0])
+
+
+def eval_objective(times, stage_count: int, replica_count: int) -> float:
+    t = np.ascontiguousarray(times, np.float64)
+    out = np.zeros(1)
+    rc = lib.pp_eval_objective(_p(t), len(t), stage_count, replica_count, _p(out))
+    if rc != PP_OK:
+        raise InvalidArgument("objective needs at least one micro-batch and counts >= 1")
+    return float(out[0])
+
+
+@dataclass
+class Plan:
+    """One mini-batch's plan: what dp_partition returns, in flat form."""
+    status: int
+    splits: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    mb_times: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    t_max_used: float = math.nan
+    objective: float = math.nan
+    err_sample_id: int = -1
+    ordered: np.ndarray | None = None
+
+
+def _raise_status(status: int, err_id: int, msg: str = ""):
+    if status == PP_ERR_INFEASIBLE_SAMPLE:
+        raise InfeasibleError(f"sample {err_id} does not fit the per-micro-batch memory cap alone",
+                              err_id, -1)
+    if status == PP_ERR_INFEASIBLE:
+        raise InfeasibleError("no feasible partition under the memory cap", -1, -1)
+    if status == PP_ERR_INVALID:
+        raise InvalidArgument(msg or "invalid argument")
+    if status == PP_ERR_NO_DEVICE:
+        raise NoDeviceError("no CUDA device: the B200 planner has no CPU fallback")
+    raise PlannerError(f"planner error {status}: {msg}")
+
+
+class Planner:
+    """A pp_ctx: one CUDA stream + scratch on one device."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        rc = lib.pp_ctx_create(device, C.byref(h))
+        if rc != PP_OK:
+            _raise_status(rc, -1, "cannot create context")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.pp_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _err(self) -> str:
+        return (lib.pp_ctx_last_error(self._h) or b"").decode()
+
+    def set_tuning(self, first_wave: int = 1, max_wave: int = 16):
+        t = Tuning(first_wave, max_wave)
+        rc = lib.pp_ctx_set_tuning(self._h, C.byref(t))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+
+    def set_stream(self, stream_ptr: int):
+        lib.pp_ctx_set_stream(self._h, C.c_void_p(stream_ptr))
+
+    def stats(self) -> dict:
+        s = Stats()
+        lib.pp_ctx_get_stats(self._h, C.byref(s))
+        return s.as_dict()
+
+    def order_samples(self, samples: np.ndarray, seg_offsets=None) -> np.ndarray:
+        samples = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        off = np.asarray([0, len(samples)] if seg_offsets is None else seg_offsets, np.int64)
+        out = np.empty_like(samples)
+        rc = lib.pp_order_samples(self._h, _p(samples), _p(off), len(off) - 1, _p(out))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return out
+
+    def plan_batch(self, samples: np.ndarray, seg_offsets, grid: Grid, model: Model, stage_count: int,
+                   replica_count: int = 1, mem_cap: float = math.inf, t_max_interval: float = 5.0,
+                   presorted: bool = False) -> dict:
+        """pp_plan_grid over independent mini-batches; returns flat arrays."""
+        samples = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        off = np.ascontiguousarray(seg_offsets, np.int64)
+        S = len(off) - 1
+        n = len(samples)
+        res = dict(ordered=np.empty_like(samples), splits=np.zeros(max(n, 1), np.int32),
+                   mb_times=np.zeros(max(n, 1)), count=np.zeros(S, np.int32),
+                   t_max_used=np.zeros(S), objective=np.zeros(S), status=np.zeros(S, np.int32),
+                   err_sample_id=np.zeros(S, np.int64))
+        out = PlanOut(*(_p(res[k]) for k in ("ordered", "splits", "mb_times", "count", "t_max_used",
+                                            "objective", "status", "err_sample_id")))
+        g, m = grid.desc(), model.desc()
+        o = DpOptions(stage_count, replica_count, mem_cap, t_max_interval)
+        rc = lib.pp_plan_grid(self._h, _p(samples), _p(off), S, int(presorted), C.byref(g), C.byref(m),
+                              C.byref(o), C.byref(out))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        res["seg_offsets"] = off
+        return res
+
+    def plan(self, samples: np.ndarray, grid: Grid, model: Model, stage_count: int,
+             replica_count: int = 1, mem_cap: float = math.inf, t_max_interval: float = 5.0,
+             presorted: bool = False) -> Plan:
+        """order_samples(Sort) + make_slice_cost + dp_partition for one mini-batch;
+        raises like the reference does."""
+        r = self.plan_batch(samples, [0, len(samples)], grid, model, stage_count, replica_count,
+                            mem_cap, t_max_interval, presorted)
+        st = int(r["status"][0])
+        if st != PP_OK:
+            _raise_status(st, int(r["err_sample_id"][0]), self._err())
+        m = int(r["count"][0])
+        return Plan(st, r["splits"][:m].copy(), r["mb_times"][:m].copy(), float(r["t_max_used"][0]),
+                    float(r["objective"][0]), -1, r["ordered"])
+
+    def plan_tables(self, T: np.ndarray, M: np.ndarray, n: int, stage_count: int,
+                    replica_count: int = 1, mem_cap: float = math.inf,
+                    t_max_interval: float = 5.0) -> Plan:
+        """dp_partition with a generic SliceCostFn given as triangular tables."""
+        T = np.ascontiguousarray(T, np.float64)
+        M = np.ascontiguousarray(M, np.float64)
+        splits = np.zeros(max(n, 1), np.int32)
+        times = np.zeros(max(n, 1))
+        cnt = np.zeros(1, np.int32)
+        tm = np.zeros(1)
+        ob = np.zeros(1)
+        err = np.full(1, -1, np.int64)
+        o = DpOptions(stage_count, replica_count, mem_cap, t_max_interval)
+        rc = lib.pp_plan_tables(self._h, _p(T), _p(M), n, C.byref(o), _p(splits), _p(times), _p(cnt),
+                                _p(tm), _p(ob), _p(err))
+        if rc != PP_OK:
+            _raise_status(rc, int(err[0]), self._err())
+        m = int(cnt[0])
+        return Plan(PP_OK, splits[:m].copy(), times[:m].copy(), float(tm[0]), float(ob[0]))
+
+    def candidate_range(self, samples, seg_offsets, grid: Grid, model: Model,
+                        mem_cap: float = math.inf, presorted: bool = False):
+        samples = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        off = np.ascontiguousarray(seg_offsets, np.int64)
+        S = len(off) - 1
+        lo = np.zeros(S)
+        hi = np.zeros(S)
+        rc = lib.pp_candidate_range(self._h, _p(samples), _p(off), S, int(presorted),
+                                    C.byref(grid.desc()), C.byref(model.desc()), mem_cap, _p(lo),
+                                    _p(hi))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return lo, hi

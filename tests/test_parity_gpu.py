@@ -1,0 +1,210 @@
+"""GPU parity: the sm_100a planner through the C-ABI against the golden
+fixtures (generated from the unmodified reference) and the C restatement.
+Bit-exact on splits, per-micro-batch times, ordering and t_max_used;
+objective within 1e-6 relative (BASELINE.json north_star), in practice equal."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import assert_plan_matches, load_golden, record, toy_tables, unhex
+from oracle.bind import Oracle, Reference, reference_available
+from paper_2311_10418_b200 import capi
+from paper_2311_10418_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def planner():
+    p = capi.Planner(0)
+    yield p
+    p.close()
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+def _plan_or_status(fn):
+    try:
+        return fn()
+    except capi.InfeasibleError as e:
+        return capi.Plan(capi.PP_ERR_INFEASIBLE_SAMPLE if e.sample_id >= 0 else capi.PP_ERR_INFEASIBLE,
+                         err_sample_id=e.sample_id)
+
+
+def test_golden_toy_tables(planner):
+    for case in load_golden("toy"):
+        T, M = toy_tables(case["lens"], case["mem_per_sample"], case["heavy"])
+        p = _plan_or_status(lambda: planner.plan_tables(
+            T, M, len(case["lens"]), case["stage_count"], case["replica_count"],
+            unhex(case["mem_cap"]), unhex(case["t_max_interval"])))
+        assert_plan_matches(p, case["expect"], case["name"])
+
+
+def test_golden_grid(planner):
+    grid = capi.synthetic_grid()
+    for case in load_golden("grid"):
+        model = capi.Model.uniform(case["stages"], 2, case["encdec"])
+        s = np.array(case["samples"], np.int64)
+        p = _plan_or_status(lambda: planner.plan(s, grid, model, case["stages"], case["replica_count"],
+                                                 unhex(case["mem_cap"]), unhex(case["t_max_interval"])))
+        assert_plan_matches(p, case["expect"], case["name"])
+
+
+def test_golden_grid_batched(planner):
+    """All golden grid cases with equal options in ONE call (segments)."""
+    grid = capi.synthetic_grid()
+    cases = [c for c in load_golden("grid") if c["stages"] == 4 and not c["encdec"]
+             and c["replica_count"] == 1 and c["t_max_interval"] == (5.0).hex() and c["mem_cap"] == "inf"]
+    assert len(cases) >= 5
+    samples = np.concatenate([np.array(c["samples"], np.int64) for c in cases])
+    off = np.concatenate([[0], np.cumsum([c["n"] for c in cases])]).astype(np.int64)
+    r = planner.plan_batch(samples, off, grid, capi.Model.uniform(4, 2, False), 4, 1, math.inf, 5.0)
+    for s, c in enumerate(cases):
+        m = int(r["count"][s])
+        got = capi.Plan(int(r["status"][s]), r["splits"][off[s]:off[s] + m], r["mb_times"][off[s]:off[s] + m],
+                        float(r["t_max_used"][s]), float(r["objective"][s]), int(r["err_sample_id"][s]),
+                        r["ordered"][off[s]:off[s + 1]])
+        assert_plan_matches(got, c["expect"], c["name"])
+
+
+def test_golden_c1(planner):
+    case = load_golden("c1")
+    cfg = W.CONFIGS["C1"]
+    p = planner.plan(W.dataset(cfg, 1), W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    assert_plan_matches(p, case["expect"], "C1")
+
+
+def test_golden_c3(planner):
+    case = load_golden("c3")
+    cfg = W.CONFIGS["C3"]
+    p = planner.plan(W.dataset(cfg, 1), W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    assert_plan_matches(p, case["expect"], "C3")
+    assert len(p.splits) == 4168
+
+
+def test_c2_matches_oracle(planner, orc):
+    cfg = W.CONFIGS["C2"]
+    s = W.dataset(cfg, 1)
+    a = orc.plan(s, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    b = planner.plan(s, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    assert_plan_matches(b, record(a), "C2")
+
+
+def test_c4_subset_matches_oracle(planner, orc):
+    cfg = W.CONFIGS["C4"]
+    M = 6
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    r = planner.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    for k in (0, 5):
+        a = orc.plan(s[off[k]:off[k + 1]], W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+        m = int(r["count"][k])
+        got = capi.Plan(int(r["status"][k]), r["splits"][off[k]:off[k] + m], r["mb_times"][off[k]:off[k] + m],
+                        float(r["t_max_used"][k]), float(r["objective"][k]), -1,
+                        r["ordered"][off[k]:off[k + 1]])
+        assert_plan_matches(got, record(a), f"C4[{k}]")
+
+
+def test_random_grid_vs_oracle(planner, orc):
+    grid = capi.synthetic_grid()
+    rng = np.random.default_rng(7)
+    for k in range(60):
+        n = int(rng.integers(1, 300))
+        encdec = bool(rng.integers(0, 2))
+        C = int(rng.choice([1, 2, 4, 7, 16]))
+        L = int(rng.choice([64, 1024, 8192]))
+        s = capi.synthetic_dataset(n, L, 900 + k, W.INPUT_DIST, W.T5_TARGET_DIST if encdec else None)
+        s[:, 0] = rng.permutation(n) * 3 + 11
+        model = capi.Model.uniform(C, int(rng.integers(1, 4)), encdec, recompute=int(rng.integers(0, 3)))
+        o = orc.order_samples(s)
+        act = max(orc.slice_cost(grid, model, o, i, i + 1)[1] for i in range(n))
+        cap = float(rng.choice([math.inf, 1.0 * act, 2.5 * act, 0.9 * act]))
+        interval = float(rng.choice([0.0, 5.0, 100.0, 2000.0, 1e5]))
+        d = int(rng.integers(1, 3))
+        a = orc.plan(s, grid, model, C, d, cap, interval)
+        b = _plan_or_status(lambda: planner.plan(s, grid, model, C, d, cap, interval))
+        assert_plan_matches(b, record(a), f"random {k}: n={n} C={C} I={interval} cap={cap}")
+
+
+def test_random_tables_vs_oracle(planner, orc):
+    """Generic SliceCostFn path with non-monotone, tie-heavy and negative costs."""
+    rng = np.random.default_rng(11)
+    for k in range(80):
+        n = int(rng.integers(1, 60))
+        tri = n * (n + 1) // 2
+        kind = k % 4
+        if kind == 0:
+            T = rng.integers(0, 5, tri).astype(float)         # many ties
+        elif kind == 1:
+            T = rng.random(tri) * 100.0                       # non-monotone
+        elif kind == 2:
+            T = rng.integers(-3, 10, tri).astype(float)       # negative times
+        else:
+            T = np.round(rng.random(tri) * 20.0, 1)
+        M = rng.random(tri) * 10.0
+        cap = float(rng.choice([math.inf, 5.0, 9.0]))
+        # keep singletons feasible most of the time
+        idx = 0
+        for i in range(n):
+            if rng.random() < 0.97:
+                M[idx] = min(M[idx], 1.0)
+            idx += n - i
+        C = int(rng.choice([1, 2, 3, 6]))
+        d = int(rng.integers(1, 3))
+        interval = float(rng.choice([0.0, 0.5, 3.0]))
+        a = orc.plan_tables(T, M, n, C, d, cap, interval)
+        b = _plan_or_status(lambda: planner.plan_tables(T, M, n, C, d, cap, interval))
+        if a.status == 2:  # plan_tables reports the ordered index
+            assert b.status == 2 and b.err_sample_id == a.err_sample_id, k
+            continue
+        assert_plan_matches(b, record(a, False), f"tables {k}")
+
+
+def test_sort_matches_oracle(planner, orc):
+    rng = np.random.default_rng(3)
+    for k in range(12):
+        n = int(rng.integers(1, 20000))
+        s = np.stack([rng.permutation(n), rng.integers(1, 9000, n), rng.integers(0, 300, n)], 1)
+        if k % 3 == 1:  # wide fields -> three-word key path
+            s[:, 0] = rng.integers(-(1 << 62), 1 << 62, n)
+            s[:, 1] = rng.integers(-(1 << 40), 1 << 40, n)
+        assert np.array_equal(planner.order_samples(s), orc.order_samples(s)), k
+    # segmented: many segments in one call
+    s = np.stack([np.arange(5000), rng.integers(1, 100, 5000), rng.integers(0, 3, 5000)], 1)
+    off = np.array([0, 1, 2, 500, 501, 4000, 5000], np.int64)
+    got = planner.order_samples(s, off)
+    for a, b in zip(off[:-1], off[1:]):
+        assert np.array_equal(got[a:b], orc.order_samples(s[a:b]))
+
+
+def test_invalid_arguments(planner):
+    grid = capi.synthetic_grid()
+    model = capi.Model.uniform(2, 2, False)
+    s = capi.synthetic_dataset(10, 100, 1)
+    with pytest.raises(capi.InvalidArgument):
+        planner.plan(s, grid, model, 0)
+    with pytest.raises(capi.InvalidArgument):
+        planner.plan(s, grid, model, 2, 0)
+    with pytest.raises(capi.InvalidArgument):
+        planner.plan(s, grid, model, 2, 1, math.inf, -1.0)
+    with pytest.raises(capi.InvalidArgument):
+        planner.plan_tables(np.zeros(0), np.zeros(0), 0, 2)
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not shipped")
+def test_random_vs_reference(planner):
+    ref = Reference()
+    grid = capi.synthetic_grid()
+    rng = np.random.default_rng(21)
+    for k in range(15):
+        n = int(rng.integers(2, 400))
+        encdec = bool(k % 2)
+        s = capi.synthetic_dataset(n, 8192, 40 + k, W.INPUT_DIST, W.T5_TARGET_DIST if encdec else None)
+        model = capi.Model.uniform(4, 2, encdec)
+        a = ref.plan(s, grid, model, 4, 1, math.inf, 5000.0)
+        b = planner.plan(s, grid, model, 4, 1, math.inf, 5000.0)
+        assert_plan_matches(b, record(a), f"ref {k}")
