@@ -1,0 +1,342 @@
+"""Benchmark: micro-batch plans/sec on 8192-sequence mini-batches (BASELINE.json
+config C3: GPT cost model, 16 stages, binding activation-memory cap, 128-candidate
+t_max sweep), at N GPUs of one node (weak scaling: every rank plans its own
+M mini-batches per step, one final NCCL gather of the plans per step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A "step" = planning M independent mini-batches (order_samples(Sort) +
+make_slice_cost + dp_partition each) through pp_plan_grid_device with the
+inputs already resident in HBM; distinct mini-batches every step, and the
+per-step band traffic (~21 MB per plan) exceeds L2.  `e2e` repeats the
+measurement through the host-buffer C-ABI call pp_plan_grid (pinned samples in,
+plans out).  `--impl reference` times the unmodified reference planner
+(oracle/_ref) on the host cores with run_plan's worker-pool model.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "micro-batch plans/sec (8192-seq mini-batch, t_max sweep)"
+UNIT = "plans/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for k, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline_sample(cfg, threads, plans):
+    """The unmodified reference (oracle/_ref) on the host cores: `plans`
+    8192-seq mini-batches (one per thread) through order_samples +
+    make_slice_cost + dp_partition in run_plan's worker pool."""
+    from oracle.bind import Reference, reference_available
+    from paper_2311_10418_b200 import workloads as W
+
+    if not reference_available():
+        return None
+    ref = Reference()
+    s = W.dataset(cfg, plans)
+    off = W.seg_offsets(cfg, plans)
+    secs, tm, ob, cnt, st = ref.plan_batch_timed(s, off, W.grid(), W.model(cfg), cfg.stages, 1,
+                                                 cfg.mem_cap, cfg.interval, threads)
+    return {"value": plans / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{plans} x {cfg.n}-seq mini-batches of {cfg.name}, one per std::thread "
+                      f"(run_plan pool), wall {secs:.1f} s",
+            "t_max_first": float(tm[0]), "status_ok": int((st == 0).sum())}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: rank 0 times the reference CPU planner; others exit."""
+    if rank != 0:
+        return
+    from paper_2311_10418_b200 import workloads as W
+
+    cfg = W.CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    from oracle.bind import Reference, reference_available
+
+    if not reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    ref = Reference()
+    # warm-up steps: bounded C1 plans through the same code path (page-in)
+    c1 = W.CONFIGS["C1"]
+    s1 = W.dataset(c1, max(args.warmup, 1))
+    ref.plan_batch_timed(s1, W.seg_offsets(c1, max(args.warmup, 1)), W.grid(), W.model(c1), c1.stages,
+                         1, c1.mem_cap, c1.interval, min(cores, max(args.warmup, 1)))
+    # timed: K steps = K 8192-seq mini-batches, on min(K, cores) threads
+    K = args.steps
+    s = W.dataset(cfg, K)
+    secs, tm, ob, cnt, st = ref.plan_batch_timed(s, W.seg_offsets(cfg, K), W.grid(), W.model(cfg),
+                                                 cfg.stages, 1, cfg.mem_cap, cfg.interval, min(K, cores))
+    value = K / secs
+    threads = min(K, cores)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": secs * 1e3 / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name + ": " + cfg.desc, "minibatch_seqs": cfg.n,
+                       "stages": cfg.stages, "t_max_candidates": cfg.K,
+                       "t_max_interval": cfg.interval, "per_mb_mem_cap": cfg.mem_cap},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{K} x {cfg.n}-seq mini-batches, one per std::thread, "
+                                       f"wall {secs:.1f} s"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "status_ok": int((st == 0).sum())}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--per-gpu", type=int, default=0, help="mini-batches per GPU per step")
+    ap.add_argument("--cpu-plans", type=int, default=0, help="cpu_baseline sample size (0: cores)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_10418_b200 import capi
+    from paper_2311_10418_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = W.CONFIGS[args.config]
+    M = args.per_gpu or {"C3": 32, "C4": 512, "C1": 1024, "C2": 128, "C5": 1}.get(cfg.name, 8)
+    steps, warm = args.steps, args.warmup
+    n = cfg.n
+    # distinct mini-batches for every (rank, step): rank r owns groups
+    # [r*(W+K), (r+1)*(W+K)) of M consecutive mini-batches of one dataset
+    groups = warm + steps
+    total_mb = world * groups * M
+    data = W.dataset(cfg, total_mb)
+    mine = data[rank * groups * M * n:(rank + 1) * groups * M * n]
+    d_samples = torch.from_numpy(mine).cuda()
+    seg = W.seg_offsets(cfg, M)
+    d_seg = torch.from_numpy(seg).cuda()
+    grid, model = W.grid(), W.model(cfg)
+    planner = capi.Planner(local)
+    stream = torch.cuda.Stream()
+    planner.set_stream(stream.cuda_stream)
+    tot = M * n
+    dev = torch.device("cuda", local)
+    out = {"ordered": torch.empty((tot, 3), dtype=torch.int64, device=dev),
+           "splits": torch.empty(tot, dtype=torch.int32, device=dev),
+           "mb_times": torch.empty(tot, dtype=torch.float64, device=dev),
+           "count": torch.empty(M, dtype=torch.int32, device=dev),
+           "t_max_used": torch.empty(M, dtype=torch.float64, device=dev),
+           "objective": torch.empty(M, dtype=torch.float64, device=dev),
+           "status": torch.empty(M, dtype=torch.int32, device=dev),
+           "err_sample_id": torch.empty(M, dtype=torch.int64, device=dev)}
+    # plan slot per mini-batch for the gather: [count, status, t_max, objective, splits...]
+    slot_words = 4 + n // 2 + 1  # 64-bit words
+    gather_buf = torch.empty((world, M, slot_words), dtype=torch.int64, device=dev) if world > 1 else None
+
+    def step(g):
+        base = g * M * n
+        planner.plan_batch_device(d_samples[base:base + tot], d_seg, seg, out, grid, model, cfg.stages,
+                                  1, cfg.mem_cap, cfg.interval)
+        if world > 1:
+            with torch.cuda.stream(stream):
+                slot = torch.zeros((M, slot_words), dtype=torch.int64, device=dev)
+                slot[:, 0] = out["count"].to(torch.int64)
+                slot[:, 1] = out["status"].to(torch.int64)
+                slot[:, 2] = out["t_max_used"].view(torch.int64)
+                slot[:, 3] = out["objective"].view(torch.int64)
+                sp = out["splits"].view(M, n)
+                slot[:, 4:4 + n // 2] = sp.contiguous().view(torch.int64).view(M, n // 2)
+                dist.all_gather_into_tensor(gather_buf.view(world * M, slot_words), slot)
+
+    stats = []
+    for g in range(warm):
+        step(g)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for g in range(warm, warm + steps):
+            step(g)
+            stats.append(planner.stats())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * M * steps / (ms_max / 1e3)
+    status_ok = int((out["status"] == 0).sum().item())
+
+    # ---- e2e: host buffers through pp_plan_grid (pinned in, plans out)
+    pin = torch.from_numpy(mine).pin_memory()
+    pin_np = pin.numpy()
+    h2d = tot * 24 + seg.nbytes
+    d2h = tot * (24 + 4 + 8) + M * (4 + 8 + 8 + 4 + 8)
+    for g in range(warm):
+        planner.plan_batch(pin_np[g * tot:(g + 1) * tot], seg, grid, model, cfg.stages, 1, cfg.mem_cap,
+                           cfg.interval)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for g in range(warm, warm + steps):
+        planner.plan_batch(pin_np[g * tot:(g + 1) * tot], seg, grid, model, cfg.stages, 1, cfg.mem_cap,
+                           cfg.interval)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * M * steps / float(te.item())
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        agg = {k: 0.0 for k in ("ms_dp", "ms_cost", "ms_sort", "bytes", "tr", "ref_tr", "evals", "gen")}
+        kern = np.zeros(4)
+        launches = np.zeros(4, np.int64)
+        for s in stats:
+            kern += np.array(s["ms_kernel"])
+            launches += np.array(s["launches"], np.int64)
+            agg["bytes"] += s["dp_band_bytes"]
+            agg["tr"] += s["transitions_executed"]
+            agg["ref_tr"] += s["transitions_reference"]
+            agg["evals"] += s["candidates_evaluated"]
+            agg["gen"] += s["candidates_generated"]
+        names = ["segmented sort", "fused slice costing", "DP pass (suffix DP per (mini-batch, t_max))",
+                 "selection / assembly"]
+        dom = int(np.argmax(kern))
+        if dom == 2:
+            achieved = agg["bytes"] / (kern[2] / 1e3) / 1e9
+        else:
+            achieved = None
+        roof = None
+        if achieved is not None:
+            roof = {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": pk["hbm_gbs"],
+                    "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                    "peak_source": pk_kind + " (MEASURED_PEAKS.json hbm_gbs, burst)",
+                    "algorithmic": "8 B band entry per DP transition visited",
+                    "avg_launch_ms": kern[2] / max(launches[2], 1)}
+        else:
+            roof = {"bound": "hbm", "kernel": names[dom], "achieved": None, "peak": pk["hbm_gbs"],
+                    "unit": "GB/s", "frac": None, "traffic": None}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            cpu = cpu_baseline_sample(cfg, cores, args.cpu_plans or cores)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warm, "ms_per_step": ms_max / steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name + ": " + cfg.desc, "minibatches_per_gpu_per_step": M,
+                       "minibatch_seqs": n, "stages": cfg.stages, "t_max_candidates": cfg.K,
+                       "t_max_interval": cfg.interval, "per_mb_mem_cap": cfg.mem_cap,
+                       "parallelism": f"mini-batch sharding x{world}, NCCL plan gather",
+                       "l2": "distinct mini-batches every step; per-step band traffic > L2 (126 MB)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches.sum()),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "work": {"dp_transitions_per_s": agg["tr"] / (ms_max / 1e3),
+                     "reference_equivalent_transitions_per_s": agg["ref_tr"] / (ms_max / 1e3),
+                     "candidates_generated": agg["gen"], "dp_passes": agg["evals"],
+                     "kernel_ms": {nm: float(v) for nm, v in zip(names, kern)},
+                     "kernel_launches": {nm: int(v) for nm, v in zip(names, launches)}},
+            "status_ok": status_ok,
+        }
+        print(json.dumps(line), flush=True)
+    planner.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -126,6 +126,12 @@ typedef struct pp_stats {
   int64_t slices_costed;          /* fused slice-cost evaluations              */
   int64_t waves;                  /* candidate waves launched                  */
   double  ms_sort, ms_cost, ms_dp, ms_total;  /* device time per phase          */
+  /* per-kernel device time (CUDA events around each launch, on the ctx
+   * stream) and launch counts: [0] sort, [1] slice costing, [2] DP passes,
+   * [3] selection / assembly / candidate compaction */
+  double  ms_kernel[4];
+  int64_t launches[4];
+  int64_t dp_band_bytes;          /* band bytes the DP passes read (8 B / transition) */
 } pp_stats;
 
 typedef struct pp_ctx pp_ctx;

@@ -231,6 +231,9 @@ int orc_dp_tables(const double* T, const double* M, int64_t n, const pp_dp_optio
       if (M[idx] > cap) continue;
       double t = T[idx];
       if (o->t_max_interval > 0) t = ceil(t / o->t_max_interval) * o->t_max_interval;
+      /* std::sort leaves the order of -0.0 and +0.0 unspecified, so which zero
+       * std::unique keeps is too; the checker (and the device) keep +0.0. */
+      if (t == 0.0) t = 0.0;
       cand[nc++] = t;
     }
     qsort(cand, (size_t)nc, sizeof(double), cmp_double);

@@ -84,10 +84,16 @@ class Stats(C.Structure):
     _fields_ = [("candidates_generated", C.c_int64), ("candidates_evaluated", C.c_int64),
                 ("transitions_executed", C.c_int64), ("transitions_reference", C.c_int64),
                 ("slices_costed", C.c_int64), ("waves", C.c_int64), ("ms_sort", C.c_double),
-                ("ms_cost", C.c_double), ("ms_dp", C.c_double), ("ms_total", C.c_double)]
+                ("ms_cost", C.c_double), ("ms_dp", C.c_double), ("ms_total", C.c_double),
+                ("ms_kernel", C.c_double * 4), ("launches", C.c_int64 * 4),
+                ("dp_band_bytes", C.c_int64)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        out = {}
+        for k, _ in self._fields_:
+            v = getattr(self, k)
+            out[k] = list(v) if k in ("ms_kernel", "launches") else v
+        return out
 
 
 def _load():
@@ -327,6 +333,26 @@ class Planner:
             _raise_status(rc, -1, self._err())
         res["seg_offsets"] = off
         return res
+
+    def plan_batch_device(self, d_samples, d_seg_offsets, h_seg_offsets, d_out: dict, grid: Grid,
+                          model: Model, stage_count: int, replica_count: int = 1,
+                          mem_cap: float = math.inf, t_max_interval: float = 5.0,
+                          presorted: bool = False) -> None:
+        """pp_plan_grid_device: inputs and outputs are device tensors (torch),
+        already resident in HBM.  d_out maps the pp_plan_out field names to
+        device tensors."""
+        h_off = np.ascontiguousarray(h_seg_offsets, np.int64)
+        S = len(h_off) - 1
+        out = PlanOut(*(C.c_void_p(d_out[k].data_ptr()) if d_out.get(k) is not None else None
+                        for k in ("ordered", "splits", "mb_times", "count", "t_max_used", "objective",
+                                  "status", "err_sample_id")))
+        g, m = grid.desc(), model.desc()
+        o = DpOptions(stage_count, replica_count, mem_cap, t_max_interval)
+        rc = lib.pp_plan_grid_device(self._h, C.c_void_p(d_samples.data_ptr()),
+                                     C.c_void_p(d_seg_offsets.data_ptr()), _p(h_off), S, int(presorted),
+                                     C.byref(g), C.byref(m), C.byref(o), C.byref(out))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
 
     def plan(self, samples: np.ndarray, grid: Grid, model: Model, stage_count: int,
              replica_count: int = 1, mem_cap: float = math.inf, t_max_interval: float = 5.0,

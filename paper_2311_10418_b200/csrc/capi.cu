@@ -5,17 +5,17 @@
 // -> dp_partition, src/planner.cpp:42,64-65; batches come from run_plan's
 // worker pool, src/driver.cpp:222-242):
 //
-//   1. segmented sort                       (sort.cu)     order_samples(Sort)
-//   2. cost pass A: Rm(i), singleton check,  (cost.cu)     microbatch.cpp:228-251
-//      candidate statistics
-//   3. band offsets, cost pass B: band +     (cost.cu)     microbatch.cpp:237-243,253-269
+//   1. segmented sort                          (sort.cu)  order_samples(Sort)
+//   2. cost pass A: Rm(i), singleton check,     (cost.cu)  microbatch.cpp:228-251
+//      candidate statistics, tile widths
+//   3. tile offsets, cost pass B: band tiles + (cost.cu)  microbatch.cpp:237-243,253-269
 //      candidate bitmap / raw list
-//   4. candidate compaction                  (cost.cu/sort.cu)
-//   5. bound + minimax pass (c > 1)          (dp.cu)       microbatch.cpp:274-279
-//   6. candidate waves: DP per (mb, t) +     (dp.cu)       microbatch.cpp:289-318
+//   4. candidate compaction                     (cost.cu/sort.cu)
+//   5. bound + minimax pass (c > 1)             (dp.cu)    microbatch.cpp:274-279
+//   6. candidate waves: DP per (mb, t) +        (dp.cu)    microbatch.cpp:289-318
 //      in-order selection, until every
 //      mini-batch hit the reference's break
-//   7. assembly                              (dp.cu)       microbatch.cpp:322-335
+//   7. assembly                                 (dp.cu)    microbatch.cpp:322-335
 //
 // The host only sizes buffers and decides wave membership from a few
 // per-segment words read back between phases; all planning arithmetic is on
@@ -47,19 +47,27 @@ cudaError_t launch_segmented_sort_u64(unsigned long long* keys, unsigned long lo
                                       const int* seg_mode, int want_mode, int* in_tmp, int n_seg,
                                       cudaStream_t st);
 // cost.cu
-cudaError_t launch_row_scan(const GridDev& g, const double* tabT, const double* tabM,
-                            const double* in_d, const double* tgt_d, const int64_t* seg_off,
-                            int n_seg, int64_t total_rows, double cap, double interval, int* row_w,
-                            SegStats* stats, cudaStream_t st);
-cudaError_t launch_row_offsets(const int* row_w, const int64_t* seg_off, int n_seg, int64_t* row_off,
-                               SegStats* stats, cudaStream_t st);
-cudaError_t launch_band(const GridDev& g, const double* tabT, const double* tabM, const double* in_d,
-                        const double* tgt_d, const int64_t* seg_off, int n_seg, int64_t total_rows,
-                        double cap, double interval, int* row_w, SegStats* stats,
-                        const int64_t* row_off, const int64_t* seg_band_base, double* band,
-                        unsigned int* bitmap, const int64_t* bitmap_off, const int* seg_mode,
-                        unsigned long long* cand_raw, const int64_t* cand_raw_off,
-                        unsigned long long* cand_raw_cnt, cudaStream_t st);
+cudaError_t launch_brackets(const GridDev& g, int max_n, int* mseg, double* mt, const double* in_d,
+                            const double* tgt_d, int64_t total, int* si_in, double* ts_in, int* si_tg,
+                            double* ts_tg, cudaStream_t st);
+cudaError_t launch_cost_pass(int pass, const GridDev& g, const double* tabT, const double* tabM,
+                             const double* in_d, const double* tgt_d, const int* si_in,
+                             const double* ts_in, const int* si_tg, const double* ts_tg,
+                             const int64_t* seg_off, const int* blk_base, int n_seg,
+                             int total_blocks, int max_n, const int* mb_seg, const double* mb_t,
+                             double cap, double interval, int* row_w, int* blk_W, SegStats* stats,
+                             const int64_t* tile_off, const int64_t* seg_band_base, double* band,
+                             cudaStream_t st);
+cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
+                             int* row_w, int* blk_W, cudaStream_t st);
+cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
+                             const int* blk_W, const int64_t* tile_off, const int64_t* seg_band_base,
+                             const double* band, double interval, const SegStats* stats,
+                             unsigned int* bitmap, const int64_t* bitmap_off, const int* seg_mode,
+                             unsigned long long* cand_raw, const int64_t* cand_raw_off,
+                             unsigned long long* cand_raw_cnt, cudaStream_t st);
+cudaError_t launch_tile_offsets(const int* blk_W, const int* blk_base, int n_seg, int64_t* tile_off,
+                                SegStats* stats, cudaStream_t st);
 cudaError_t launch_cand_bitmap(const unsigned int* bitmap, const int64_t* bitmap_off,
                                const SegStats* stats, const int* seg_mode, int n_seg,
                                double interval, const int64_t* cand_off, double* cand, int* cand_n,
@@ -69,12 +77,14 @@ cudaError_t launch_cand_unique(const unsigned long long* keys_a, const unsigned 
                                const unsigned long long* raw_cnt, const int* seg_mode, int n_seg,
                                const int64_t* cand_off, double* cand, int* cand_n, cudaStream_t st);
 // dp.cu
-size_t dp_smem_bytes(int mode, int n);
-cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t smem,
-                           const int64_t* seg_off, const int* row_w, const int64_t* row_off,
-                           const int64_t* seg_band_base, const double* band, const double* cand,
-                           const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
-                           cudaStream_t st);
+size_t dp_smem_fixed();
+size_t dp_state_bytes(int mode, int entries);
+cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t smem_state,
+                           size_t smem_budget,
+                           const int64_t* seg_off, const int* blk_base, const int* blk_W,
+                           const int64_t* tile_off, const int64_t* seg_band_base, const double* band,
+                           const double* cand, const int64_t* cand_off, ItemResult* res,
+                           int* next_buf, double* gstate, int res_by_seg, cudaStream_t st);
 cudaError_t launch_seg_init(const ItemResult* bound_res, int has_bound, int replicas,
                             const int64_t* cand_off, const int* cand_n, const double* cand,
                             const int* active, SegDP* dp, int n_seg, cudaStream_t st);
@@ -83,7 +93,7 @@ cudaError_t launch_select(const WorkItem* items, const ItemResult* res, const in
                           const int64_t* seg_off, const double* cand, const int64_t* cand_off,
                           int stage_count, int replicas, SegDP* dps, int n_seg, cudaStream_t st);
 cudaError_t launch_finalize(const SegDP* dps, const int* best_next, const int64_t* seg_off,
-                            const int* row_w, const int64_t* row_off, const int64_t* seg_band_base,
+                            const int* blk_base, const int64_t* tile_off, const int64_t* seg_band_base,
                             const double* band, const SegStats* stats, const pp_sample* ordered,
                             int stage_count, int replicas, int max_n, int n_seg, int32_t* splits,
                             double* mb_times, int32_t* count, double* t_max_used, double* objective,
@@ -94,7 +104,7 @@ using namespace ppb;
 
 namespace {
 
-constexpr size_t kDpSmemLimit = 200 * 1024;  // per-CTA state budget before spilling to global
+constexpr size_t kDpSmemLimit = 190 * 1024;  // fixed + state budget before DP state spills to global
 
 // Grow-only device buffer.
 struct DevBuf {
@@ -153,13 +163,27 @@ struct pp_ctx {
   cudaEvent_t ev[4]{};
   // device scratch
   DevBuf samples, seg_off, ordered, in_d, tgt_d, sort_keys, sort_vals, range;
-  DevBuf grid_ax, grid_cells, layouts, tabT, tabM;
-  DevBuf row_w, row_off, stats_d, band_base, band, bitmap, bitmap_off, seg_mode, raw, raw_tmp,
-      raw_off, raw_cnt, raw_in_tmp, cand, cand_off, cand_n, active;
+  DevBuf grid_ax, grid_cells, layouts, tabT, tabM, mb_seg, mb_t, sb_in_s, sb_in_t, sb_tg_s, sb_tg_t;
+  int64_t band_total = 0;
+  DevBuf row_w, blk_base, blk_W, tile_off, stats_d, band_base, band, bitmap, bitmap_off, seg_mode,
+      raw, raw_tmp, raw_off, raw_cnt, raw_in_tmp, cand, cand_off, cand_n, active;
   DevBuf items, results, next_buf, gstate, seg_item_start, seg_item_cnt, segdp, best_next,
       bound_items, bound_res;
   DevBuf out_splits, out_times, out_count, out_tmax, out_obj, out_status, out_err;
-  PinBuf h_range, h_stats, h_segdp, h_misc;
+  PinBuf h_range, h_stats, h_segdp;
+  // per-launch event pairs for kernel timing (pp_stats::ms_kernel)
+  std::vector<cudaEvent_t> kev;
+  std::vector<int> kcat;
+  size_t kused = 0;
+  std::vector<DevBuf*> all_bufs() {
+    return {&samples, &seg_off, &ordered, &in_d, &tgt_d, &sort_keys, &sort_vals, &range, &grid_ax,
+            &grid_cells, &layouts, &tabT, &tabM, &mb_seg, &mb_t, &sb_in_s, &sb_in_t, &sb_tg_s,
+            &sb_tg_t, &row_w, &blk_base, &blk_W, &tile_off,
+            &stats_d, &band_base, &band, &bitmap, &bitmap_off, &seg_mode, &raw, &raw_tmp, &raw_off,
+            &raw_cnt, &raw_in_tmp, &cand, &cand_off, &cand_n, &active, &items, &results, &next_buf,
+            &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
+            &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err};
+  }
 };
 
 namespace {
@@ -171,6 +195,30 @@ namespace {
       ctx->err = std::string(#x) + ": " + cudaGetErrorString(e_);                    \
       return PP_ERR_CUDA;                                                            \
     }                                                                                \
+  } while (0)
+
+// Record an event pair around one kernel launch (category: 0 sort, 1 cost,
+// 2 DP pass, 3 other) so pp_stats reports per-kernel device time measured on
+// the launching stream.
+cudaError_t timed_begin(pp_ctx* ctx, int cat) {
+  if (ctx->kused + 2 > ctx->kev.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return r;
+      ctx->kev.push_back(e);
+    }
+  }
+  ctx->kcat.push_back(cat);
+  return cudaEventRecord(ctx->kev[ctx->kused++], ctx->stream);
+}
+cudaError_t timed_end(pp_ctx* ctx) { return cudaEventRecord(ctx->kev[ctx->kused++], ctx->stream); }
+
+#define PP_TIMED(cat, x)            \
+  do {                              \
+    PP_CUDA(timed_begin(ctx, cat)); \
+    PP_CUDA(x);                     \
+    PP_CUDA(timed_end(ctx));        \
   } while (0)
 
 int fail(pp_ctx* ctx, int code, const std::string& msg) {
@@ -210,7 +258,7 @@ int validate_opts(pp_ctx* ctx, const pp_dp_options& o) {
 }
 
 // Upload the grid restricted to the recompute strategy, plus the distinct
-// stage layouts.  Returns the device descriptor.
+// stage layouts.
 int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, GridDev* out) {
   if (!g || !m) return fail(ctx, PP_ERR_INVALID, "grid and model descriptors are required");
   if (g->n_mbs < 1 || g->n_seq < 1) return fail(ctx, PP_ERR_INVALID, "grid axis is empty");
@@ -263,29 +311,30 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-// The planning pipeline (steps 1-7 above).
-int run_plan(pp_ctx* ctx, const PlanCall& c) {
+double dkey_inv_host(unsigned long long k) {
+  const unsigned long long u = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
+  double d;
+  std::memcpy(&d, &u, 8);
+  return d;
+}
+
+// Steps 1-2 (+ tile offsets): sort, block bookkeeping, cost pass A.  Leaves
+// the per-segment statistics in ctx->h_stats (synchronised) and the block
+// table in host vector `blk_base`.
+int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interval,
+                std::vector<int>& blk_base, int& max_n) {
   cudaStream_t st = ctx->stream;
   const int n_seg = c.n_seg;
-  const int64_t total = c.h_seg_off[n_seg] - c.h_seg_off[0];
-  pp_stats S{};
-  int max_n = 0;
-  for (int s = 0; s < n_seg; ++s)
-    max_n = std::max<int>(max_n, (int)(c.h_seg_off[s + 1] - c.h_seg_off[s]));
-  if (c.h_seg_off[0] != 0) return fail(ctx, PP_ERR_INVALID, "seg_offsets[0] must be 0");
-  for (int s = 0; s < n_seg; ++s)
-    if (c.h_seg_off[s + 1] < c.h_seg_off[s]) return fail(ctx, PP_ERR_INVALID, "seg_offsets must be non-decreasing");
-  if (total >= INT_MAX) return fail(ctx, PP_ERR_INVALID, "too many samples in one call");
-
-  GridDev g{};
+  const int64_t total = c.h_seg_off[n_seg];
   const bool table = c.d_tabT != nullptr;
-  if (!table) {
-    int rc = upload_grid(ctx, c.grid, c.model, &g);
-    if (rc) return rc;
+  blk_base.assign(n_seg + 1, 0);
+  max_n = 0;
+  for (int s = 0; s < n_seg; ++s) {
+    const int n = (int)(c.h_seg_off[s + 1] - c.h_seg_off[s]);
+    max_n = std::max(max_n, n);
+    blk_base[s + 1] = blk_base[s] + (n + kRB - 1) / kRB;
   }
-  PP_CUDA(cudaEventRecord(ctx->ev[0], st));
-
-  // ---- 1. order_samples(Sort)
+  const int total_blocks = blk_base[n_seg];
   PP_CUDA(ctx->in_d.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
   PP_CUDA(ctx->tgt_d.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
   if (!table) {
@@ -294,48 +343,138 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(ctx->sort_keys.ensure(std::max<int64_t>(total, 1) * 6 * sizeof(unsigned long long)));
     PP_CUDA(ctx->sort_vals.ensure(std::max<int64_t>(total, 1) * 2 * sizeof(uint32_t)));
     if (total > 0)
-      PP_CUDA(launch_segmented_sort(c.d_samples, c.d_seg_off, c.h_seg_off, n_seg, total, c.presorted,
-                                    ctx->range.as<unsigned long long>(),
-                                    ctx->h_range.as<unsigned long long>(),
-                                    ctx->sort_keys.as<unsigned long long>(),
-                                    ctx->sort_vals.as<uint32_t>(), c.d_ordered, ctx->in_d.as<double>(),
-                                    ctx->tgt_d.as<double>(), st));
+      PP_TIMED(0, launch_segmented_sort(c.d_samples, c.d_seg_off, c.h_seg_off, n_seg, total, c.presorted,
+                                        ctx->range.as<unsigned long long>(),
+                                        ctx->h_range.as<unsigned long long>(),
+                                        ctx->sort_keys.as<unsigned long long>(),
+                                        ctx->sort_vals.as<uint32_t>(), c.d_ordered,
+                                        ctx->in_d.as<double>(), ctx->tgt_d.as<double>(), st));
+    PP_CUDA(ctx->mb_seg.ensure((size_t)(max_n + 1) * sizeof(int)));
+    PP_CUDA(ctx->mb_t.ensure((size_t)(max_n + 1) * sizeof(double)));
+    PP_CUDA(ctx->sb_in_s.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
+    PP_CUDA(ctx->sb_in_t.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
+    PP_CUDA(ctx->sb_tg_s.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
+    PP_CUDA(ctx->sb_tg_t.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
+    PP_TIMED(1, launch_brackets(g, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(),
+                                ctx->in_d.as<double>(), ctx->tgt_d.as<double>(), total,
+                                ctx->sb_in_s.as<int>(), ctx->sb_in_t.as<double>(), ctx->sb_tg_s.as<int>(),
+                                ctx->sb_tg_t.as<double>(), st));
   }
   PP_CUDA(cudaEventRecord(ctx->ev[1], st));
-
-  // ---- 2. cost pass A
-  const double cap = c.opts.per_mb_mem_cap;
-  const double I = c.opts.t_max_interval;
   PP_CUDA(ctx->row_w.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
-  PP_CUDA(ctx->row_off.ensure(std::max<int64_t>(total, 1) * sizeof(int64_t)));
+  PP_CUDA(ctx->blk_base.ensure((n_seg + 1) * sizeof(int)));
+  PP_CUDA(ctx->blk_W.ensure(std::max(total_blocks, 1) * sizeof(int)));
+  PP_CUDA(ctx->tile_off.ensure(std::max(total_blocks, 1) * sizeof(int64_t)));
   PP_CUDA(ctx->stats_d.ensure(n_seg * sizeof(SegStats)));
   PP_CUDA(ctx->h_stats.ensure(n_seg * sizeof(SegStats)));
-  {
-    SegStats* hs = ctx->h_stats.as<SegStats>();
-    for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0};
-    PP_CUDA(cudaMemcpyAsync(ctx->stats_d.p, hs, n_seg * sizeof(SegStats), cudaMemcpyHostToDevice, st));
-  }
-  SegStats* d_stats = ctx->stats_d.as<SegStats>();
+  PP_CUDA(ctx->band_base.ensure(n_seg * sizeof(int64_t)));
+  SegStats* hs = ctx->h_stats.as<SegStats>();
+  for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0, 0, 0};
+  PP_CUDA(cudaMemcpyAsync(ctx->stats_d.p, hs, n_seg * sizeof(SegStats), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->blk_base.p, blk_base.data(), (n_seg + 1) * sizeof(int),
+                          cudaMemcpyHostToDevice, st));
+  const double cap = c.opts.per_mb_mem_cap;
+  // Pass A (or its closed form when every slice is memory-feasible).
+  const bool full_rows = !table && cap == INFINITY;
   if (total > 0) {
-    PP_CUDA(launch_row_scan(g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
-                            c.d_seg_off, n_seg, total, cap, I, ctx->row_w.as<int>(), d_stats, st));
-    PP_CUDA(launch_row_offsets(ctx->row_w.as<int>(), c.d_seg_off, n_seg, ctx->row_off.as<int64_t>(),
-                               d_stats, st));
+    if (full_rows)
+      PP_TIMED(1, launch_full_rows(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
+                                   ctx->row_w.as<int>(), ctx->blk_W.as<int>(), st));
+    else
+      PP_TIMED(1, launch_cost_pass(0, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
+                                   ctx->sb_in_s.as<int>(), ctx->sb_in_t.as<double>(), ctx->sb_tg_s.as<int>(),
+                                   ctx->sb_tg_t.as<double>(), c.d_seg_off, ctx->blk_base.as<int>(), n_seg,
+                                   total_blocks, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(), cap,
+                                   interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
+                                   ctx->stats_d.as<SegStats>(), nullptr, nullptr, nullptr, st));
+    PP_TIMED(1, launch_tile_offsets(ctx->blk_W.as<int>(), ctx->blk_base.as<int>(), n_seg,
+                                    ctx->tile_off.as<int64_t>(), ctx->stats_d.as<SegStats>(), st));
   }
-  PP_CUDA(cudaMemcpyAsync(ctx->h_stats.p, d_stats, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
   PP_CUDA(cudaStreamSynchronize(st));
+  // Band allocation (tiles are NaN-filled: masked / unused entries).
+  std::vector<int64_t> band_base(n_seg);
+  int64_t band_total = 0;
+  for (int s = 0; s < n_seg; ++s) {
+    band_base[s] = band_total;
+    band_total += hs[s].band;
+  }
+  ctx->band_total = band_total;
+  PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
+  PP_CUDA(cudaMemcpyAsync(ctx->band_base.p, band_base.data(), n_seg * sizeof(int64_t),
+                          cudaMemcpyHostToDevice, st));
+  if (band_total > 0) PP_CUDA(cudaMemsetAsync(ctx->band.p, 0xff, band_total * sizeof(double), st));
+  // Pass B: band + candidate statistics.
+  if (total > 0)
+    PP_TIMED(1, launch_cost_pass(1, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
+                                 ctx->sb_in_s.as<int>(), ctx->sb_in_t.as<double>(), ctx->sb_tg_s.as<int>(),
+                                 ctx->sb_tg_t.as<double>(), c.d_seg_off, ctx->blk_base.as<int>(), n_seg,
+                                 total_blocks, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(), cap,
+                                 interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
+                                 ctx->stats_d.as<SegStats>(), ctx->tile_off.as<int64_t>(),
+                                 ctx->band_base.as<int64_t>(), ctx->band.as<double>(), st));
+  PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaStreamSynchronize(st));
+  return PP_OK;
+}
+
+// DP state placement for one pass over a segment of n samples whose tiles
+// are at most wmax columns wide: a ring of R >= wmax + 64 entries (dp.cu)
+// when that is smaller than the full n + 1.
+// Shared memory per DP CTA: deep chunk rings when the launch has at most one
+// CTA per SM, two CTAs per SM otherwise.
+size_t dp_budget(int n_items) { return n_items <= 148 ? 220 * 1024 : 110 * 1024; }
+
+void state_layout(int mode, int n, int wmax, unsigned& mask, int& entries, size_t& smem) {
+  int R = 64;
+  while (R < wmax + 64) R <<= 1;
+  if (R < n + 1) {
+    mask = (unsigned)(R - 1);
+    entries = R;
+  } else {
+    mask = ~0u;
+    entries = n + 1;
+  }
+  smem = dp_smem_fixed() + dp_state_bytes(mode, entries);
+}
+
+// The planning pipeline (steps 1-7 above).
+int run_plan(pp_ctx* ctx, const PlanCall& c) {
+  cudaStream_t st = ctx->stream;
+  const int n_seg = c.n_seg;
+  if (c.h_seg_off[0] != 0) return fail(ctx, PP_ERR_INVALID, "seg_offsets[0] must be 0");
+  for (int s = 0; s < n_seg; ++s)
+    if (c.h_seg_off[s + 1] < c.h_seg_off[s])
+      return fail(ctx, PP_ERR_INVALID, "seg_offsets must be non-decreasing");
+  const int64_t total = c.h_seg_off[n_seg];
+  if (total >= INT_MAX) return fail(ctx, PP_ERR_INVALID, "too many samples in one call");
+  ctx->kused = 0;
+  ctx->kcat.clear();
+  pp_stats S{};
+
+  GridDev g{};
+  if (!c.d_tabT) {
+    int rc = upload_grid(ctx, c.grid, c.model, &g);
+    if (rc) return rc;
+  }
+  PP_CUDA(cudaEventRecord(ctx->ev[0], st));
+  const double cap = c.opts.per_mb_mem_cap;
+  const double I = c.opts.t_max_interval;
+  std::vector<int> blk_base;
+  int max_n = 0;
+  {
+    int rc = cost_pass_a(ctx, c, g, I, blk_base, max_n);
+    if (rc) return rc;
+  }
+  const int total_blocks = blk_base[n_seg];
 
   // ---- 3. sizing: band, candidate modes
   const SegStats* hs = ctx->h_stats.as<SegStats>();
   const bool single = c.opts.stage_count == 1;  // candidates = {+inf} (microbatch.cpp:255-257)
-  std::vector<int64_t> band_base(n_seg), bm_off(n_seg + 1, 0), raw_off(n_seg + 1, 0),
-      cand_off(n_seg + 1, 0);
+  std::vector<int64_t> bm_off(n_seg + 1, 0), raw_off(n_seg + 1, 0), cand_off(n_seg + 1, 0);
   std::vector<int> mode(n_seg, 2), active(n_seg, 0);
-  int64_t band_total = 0;
   for (int s = 0; s < n_seg; ++s) {
     const int n = (int)(c.h_seg_off[s + 1] - c.h_seg_off[s]);
-    band_base[s] = band_total;
-    band_total += hs[s].band;
     active[s] = (n > 0 && hs[s].err_row == INT_MAX) ? 1 : 0;
     int64_t ncap = 1;
     bm_off[s + 1] = bm_off[s];
@@ -343,14 +482,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     if (!single && active[s]) {
       bool bitmap_ok = false;
       if (I > 0 && hs[s].kmin != ~0ULL) {
-        // host mirror of dkey_inv
-        auto inv = [](unsigned long long k) {
-          unsigned long long u = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
-          double d;
-          std::memcpy(&d, &u, 8);
-          return d;
-        };
-        const double kmn = inv(hs[s].kmin), kmx = inv(hs[s].kmax);
+        const double kmn = dkey_inv_host(hs[s].kmin), kmx = dkey_inv_host(hs[s].kmax);
         if (std::fabs(kmn) < 4.0e15 && std::fabs(kmx) < 4.0e15 && kmx - kmn < (double)(1 << 26)) {
           const int64_t range = (int64_t)(kmx - kmn) + 1;
           bm_off[s + 1] = bm_off[s] + (range + 31) / 32;
@@ -368,13 +500,10 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     }
     cand_off[s + 1] = cand_off[s] + ncap;
   }
-  S.slices_costed = 0;
   for (int s = 0; s < n_seg; ++s) {
     const int64_t n = c.h_seg_off[s + 1] - c.h_seg_off[s];
     S.slices_costed += n * (n + 1) / 2 + hs[s].band;
   }
-  PP_CUDA(ctx->band_base.ensure(n_seg * sizeof(int64_t)));
-  PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
   PP_CUDA(ctx->bitmap_off.ensure((n_seg + 1) * sizeof(int64_t)));
   PP_CUDA(ctx->bitmap.ensure(std::max<int64_t>(bm_off[n_seg], 1) * sizeof(unsigned int)));
   PP_CUDA(ctx->seg_mode.ensure(n_seg * sizeof(int)));
@@ -387,7 +516,6 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   PP_CUDA(ctx->cand_off.ensure((n_seg + 1) * sizeof(int64_t)));
   PP_CUDA(ctx->cand.ensure(std::max<int64_t>(cand_off[n_seg], 1) * sizeof(double)));
   PP_CUDA(ctx->cand_n.ensure(n_seg * sizeof(int)));
-  PP_CUDA(cudaMemcpyAsync(ctx->band_base.p, band_base.data(), n_seg * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   PP_CUDA(cudaMemcpyAsync(ctx->bitmap_off.p, bm_off.data(), (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   PP_CUDA(cudaMemcpyAsync(ctx->seg_mode.p, mode.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
   PP_CUDA(cudaMemcpyAsync(ctx->active.p, active.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -398,14 +526,15 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   PP_CUDA(cudaMemsetAsync(ctx->raw_in_tmp.p, 0, n_seg * sizeof(int), st));
   PP_CUDA(cudaMemsetAsync(ctx->cand_n.p, 0, n_seg * sizeof(int), st));
 
-  if (total > 0)
-    PP_CUDA(launch_band(g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
-                        c.d_seg_off, n_seg, total, cap, I, ctx->row_w.as<int>(), d_stats,
-                        ctx->row_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
-                        ctx->band.as<double>(), ctx->bitmap.as<unsigned int>(),
-                        ctx->bitmap_off.as<int64_t>(), ctx->seg_mode.as<int>(),
-                        ctx->raw.as<unsigned long long>(), ctx->raw_off.as<int64_t>(),
-                        ctx->raw_cnt.as<unsigned long long>(), st));
+  // pass C: candidate values from the band
+  if (total > 0 && !single)
+    PP_TIMED(3, launch_band_cand(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
+                                 ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
+                                 ctx->band_base.as<int64_t>(), ctx->band.as<double>(), I,
+                                 ctx->stats_d.as<SegStats>(), ctx->bitmap.as<unsigned int>(),
+                                 ctx->bitmap_off.as<int64_t>(), ctx->seg_mode.as<int>(),
+                                 ctx->raw.as<unsigned long long>(), ctx->raw_off.as<int64_t>(),
+                                 ctx->raw_cnt.as<unsigned long long>(), st));
   // ---- 4. candidate lists
   if (single) {
     std::vector<double> infs(cand_off[n_seg], INFINITY);
@@ -414,25 +543,26 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(cudaMemcpyAsync(ctx->cand_n.p, ones.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaStreamSynchronize(st));  // host vectors die here
   } else {
-    PP_CUDA(launch_cand_bitmap(ctx->bitmap.as<unsigned int>(), ctx->bitmap_off.as<int64_t>(), d_stats,
-                               ctx->seg_mode.as<int>(), n_seg, I, ctx->cand_off.as<int64_t>(),
-                               ctx->cand.as<double>(), ctx->cand_n.as<int>(), st));
+    PP_TIMED(3, launch_cand_bitmap(ctx->bitmap.as<unsigned int>(), ctx->bitmap_off.as<int64_t>(),
+                                   ctx->stats_d.as<SegStats>(), ctx->seg_mode.as<int>(), n_seg, I,
+                                   ctx->cand_off.as<int64_t>(), ctx->cand.as<double>(),
+                                   ctx->cand_n.as<int>(), st));
     if (raw_off[n_seg] > 0) {
-      PP_CUDA(launch_segmented_sort_u64(ctx->raw.as<unsigned long long>(),
-                                        ctx->raw_tmp.as<unsigned long long>(),
-                                        ctx->raw_off.as<int64_t>(),
-                                        ctx->raw_cnt.as<unsigned long long>(), ctx->seg_mode.as<int>(),
-                                        1, ctx->raw_in_tmp.as<int>(), n_seg, st));
-      PP_CUDA(launch_cand_unique(ctx->raw.as<unsigned long long>(),
-                                 ctx->raw_tmp.as<unsigned long long>(), ctx->raw_in_tmp.as<int>(),
-                                 ctx->raw_off.as<int64_t>(), ctx->raw_cnt.as<unsigned long long>(),
-                                 ctx->seg_mode.as<int>(), n_seg, ctx->cand_off.as<int64_t>(),
-                                 ctx->cand.as<double>(), ctx->cand_n.as<int>(), st));
+      PP_TIMED(3, launch_segmented_sort_u64(ctx->raw.as<unsigned long long>(),
+                                            ctx->raw_tmp.as<unsigned long long>(),
+                                            ctx->raw_off.as<int64_t>(),
+                                            ctx->raw_cnt.as<unsigned long long>(), ctx->seg_mode.as<int>(),
+                                            1, ctx->raw_in_tmp.as<int>(), n_seg, st));
+      PP_TIMED(3, launch_cand_unique(ctx->raw.as<unsigned long long>(),
+                                     ctx->raw_tmp.as<unsigned long long>(), ctx->raw_in_tmp.as<int>(),
+                                     ctx->raw_off.as<int64_t>(), ctx->raw_cnt.as<unsigned long long>(),
+                                     ctx->seg_mode.as<int>(), n_seg, ctx->cand_off.as<int64_t>(),
+                                     ctx->cand.as<double>(), ctx->cand_n.as<int>(), st));
     }
   }
   PP_CUDA(cudaEventRecord(ctx->ev[2], st));
 
-  // ---- 5. bound + minimax pass
+  // ---- 5. bound + minimax pass (one CTA per active segment)
   PP_CUDA(ctx->segdp.ensure(n_seg * sizeof(SegDP)));
   PP_CUDA(ctx->h_segdp.ensure(n_seg * sizeof(SegDP)));
   PP_CUDA(ctx->best_next.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
@@ -441,40 +571,46 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   const double* d_cand = ctx->cand.as<double>();
   int64_t bound_transitions = 0;
   if (!single) {
-    std::vector<WorkItem> bi(n_seg);
+    std::vector<WorkItem> bi;
     int64_t goff = 0;
-    size_t smem_max = 0;
+    size_t smem_max = dp_smem_fixed();
     for (int s = 0; s < n_seg; ++s) {
+      if (!active[s]) continue;
       const int n = (int)(c.h_seg_off[s + 1] - c.h_seg_off[s]);
-      bi[s].seg = s;
-      bi[s].cand = -1;
-      bi[s].next_off = 0;
-      const size_t need = dp_smem_bytes(1, n);
+      WorkItem w{};
+      w.seg = s;
+      w.cand = -1;
+      w.next_off = 0;
+      size_t need;
+      state_layout(1, n, hs[s].wmax, w.state_mask, w.state_entries, need);
       if (need <= kDpSmemLimit) {
-        bi[s].state_off = -1;
+        w.state_off = -1;
         smem_max = std::max(smem_max, need);
       } else {
-        bi[s].state_off = goff;
-        goff += 2 * (int64_t)(n + 1);
+        w.state_off = goff;
+        goff += 2 * (int64_t)w.state_entries;
       }
-      if (active[s]) bound_transitions += hs[s].band;
+      bound_transitions += hs[s].band;
+      bi.push_back(w);
     }
-    // inactive segments still launch (cheap: they walk their band) but
-    // their results are ignored by seg_init.
-    PP_CUDA(ctx->bound_items.ensure(n_seg * sizeof(WorkItem)));
-    PP_CUDA(ctx->gstate.ensure(std::max<int64_t>(goff, 1) * sizeof(double)));
-    PP_CUDA(ctx->next_buf.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
-    PP_CUDA(cudaMemcpyAsync(ctx->bound_items.p, bi.data(), n_seg * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
-    PP_CUDA(launch_dp_pass(1, ctx->bound_items.as<WorkItem>(), n_seg, smem_max, c.d_seg_off,
-                           ctx->row_w.as<int>(), ctx->row_off.as<int64_t>(),
-                           ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
-                           ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
-                           ctx->gstate.as<double>(), st));
-    PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
+    if (!bi.empty()) {
+      PP_CUDA(ctx->bound_items.ensure(bi.size() * sizeof(WorkItem)));
+      PP_CUDA(ctx->gstate.ensure(std::max<int64_t>(goff, 1) * sizeof(double)));
+      PP_CUDA(ctx->next_buf.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
+      PP_CUDA(cudaMemcpyAsync(ctx->bound_items.p, bi.data(), bi.size() * sizeof(WorkItem),
+                              cudaMemcpyHostToDevice, st));
+      PP_TIMED(2, launch_dp_pass(1, ctx->bound_items.as<WorkItem>(), (int)bi.size(),
+                                 smem_max - dp_smem_fixed(), dp_budget((int)bi.size()), c.d_seg_off,
+                                 ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
+                                 ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
+                                 ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
+                                 ctx->gstate.as<double>(), 1, st));
+      PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
+    }
   }
-  PP_CUDA(launch_seg_init(ctx->bound_res.as<ItemResult>(), single ? 0 : 1, c.opts.replica_count,
-                          d_cand_off, ctx->cand_n.as<int>(), d_cand, ctx->active.as<int>(),
-                          ctx->segdp.as<SegDP>(), n_seg, st));
+  PP_TIMED(3, launch_seg_init(ctx->bound_res.as<ItemResult>(), single ? 0 : 1, c.opts.replica_count,
+                              d_cand_off, ctx->cand_n.as<int>(), d_cand, ctx->active.as<int>(),
+                              ctx->segdp.as<SegDP>(), n_seg, st));
 
   // ---- 6. candidate waves
   int wave = std::max(1, ctx->tuning.first_wave);
@@ -488,16 +624,18 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     const SegDP* hd = ctx->h_segdp.as<SegDP>();
     items.clear();
     int64_t noff = 0, goff = 0;
-    size_t smem_max = 0;
+    size_t smem_max = dp_smem_fixed();
     for (int s = 0; s < n_seg; ++s) {
       item_start[s] = (int)items.size();
       item_cnt[s] = 0;
       if (hd[s].done) continue;
       const int n = (int)(c.h_seg_off[s + 1] - c.h_seg_off[s]);
       const int k = std::min(wave, hd[s].n_cand - hd[s].next_cand);
-      const size_t need = dp_smem_bytes(0, n);
+      WorkItem proto{};
+      size_t need;
+      state_layout(0, n, hs[s].wmax, proto.state_mask, proto.state_entries, need);
       for (int q = 0; q < k; ++q) {
-        WorkItem w;
+        WorkItem w = proto;
         w.seg = s;
         w.cand = hd[s].next_cand + q;
         w.next_off = noff;
@@ -507,7 +645,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
           smem_max = std::max(smem_max, need);
         } else {
           w.state_off = goff;
-          goff += 2 * (int64_t)(n + 1);
+          goff += 2 * (int64_t)w.state_entries;
         }
         items.push_back(w);
         transitions += hs[s].band;
@@ -527,27 +665,27 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(cudaMemcpyAsync(ctx->items.p, items.data(), ni * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_start.p, item_start.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_cnt.p, item_cnt.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
-    PP_CUDA(launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_max, c.d_seg_off,
-                           ctx->row_w.as<int>(), ctx->row_off.as<int64_t>(),
-                           ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
-                           ctx->results.as<ItemResult>(), ctx->next_buf.as<int>(),
-                           ctx->gstate.as<double>(), st));
-    PP_CUDA(launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
-                          ctx->seg_item_start.as<int>(), ctx->seg_item_cnt.as<int>(),
-                          ctx->next_buf.as<int>(), ctx->best_next.as<int>(), c.d_seg_off, d_cand,
-                          d_cand_off, c.opts.stage_count, c.opts.replica_count,
-                          ctx->segdp.as<SegDP>(), n_seg, st));
+    PP_TIMED(2, launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_max - dp_smem_fixed(), dp_budget(ni),
+                               c.d_seg_off, ctx->blk_base.as<int>(),
+                               ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
+                               ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
+                               ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, st));
+    PP_TIMED(3, launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
+                              ctx->seg_item_start.as<int>(), ctx->seg_item_cnt.as<int>(),
+                              ctx->next_buf.as<int>(), ctx->best_next.as<int>(), c.d_seg_off, d_cand,
+                              d_cand_off, c.opts.stage_count, c.opts.replica_count,
+                              ctx->segdp.as<SegDP>(), n_seg, st));
     wave = std::min(wave * 2, max_wave);
   }
   PP_CUDA(cudaEventRecord(ctx->ev[3], st));
 
   // ---- 7. assembly
-  PP_CUDA(launch_finalize(ctx->segdp.as<SegDP>(), ctx->best_next.as<int>(), c.d_seg_off,
-                          ctx->row_w.as<int>(), ctx->row_off.as<int64_t>(),
-                          ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_stats, c.d_ordered,
-                          c.opts.stage_count, c.opts.replica_count, std::max(max_n, 1), n_seg,
-                          c.d_splits, c.d_times, c.d_count, c.d_tmax, c.d_obj, c.d_status, c.d_err,
-                          st));
+  PP_TIMED(3, launch_finalize(ctx->segdp.as<SegDP>(), ctx->best_next.as<int>(), c.d_seg_off,
+                              ctx->blk_base.as<int>(), ctx->tile_off.as<int64_t>(),
+                              ctx->band_base.as<int64_t>(), ctx->band.as<double>(),
+                              ctx->stats_d.as<SegStats>(), c.d_ordered, c.opts.stage_count,
+                              c.opts.replica_count, std::max(max_n, 1), n_seg, c.d_splits, c.d_times,
+                              c.d_count, c.d_tmax, c.d_obj, c.d_status, c.d_err, st));
   PP_CUDA(cudaStreamSynchronize(st));
   PP_CUDA(cudaGetLastError());
 
@@ -569,6 +707,11 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   S.ms_cost = elapsed(ctx->ev[1], ctx->ev[2]);
   S.ms_dp = elapsed(ctx->ev[2], ctx->ev[3]);
   S.ms_total = elapsed(ctx->ev[0], ctx->ev[3]);
+  for (size_t k = 0; k < ctx->kcat.size(); ++k) {
+    S.ms_kernel[ctx->kcat[k]] += elapsed(ctx->kev[2 * k], ctx->kev[2 * k + 1]);
+    S.launches[ctx->kcat[k]] += 1;
+  }
+  S.dp_band_bytes = transitions * (int64_t)sizeof(double);
   ctx->stats = S;
   return PP_OK;
 }
@@ -577,6 +720,19 @@ int check_ctx(pp_ctx* ctx) {
   if (!ctx) return PP_ERR_INVALID;
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return fail(ctx, PP_ERR_CUDA, cudaGetErrorString(e));
+  return PP_OK;
+}
+
+// Stage host samples + offsets into the ctx buffers.
+int stage_inputs(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets, int n_seg) {
+  const int64_t total = seg_offsets[n_seg];
+  cudaStream_t st = ctx->stream;
+  PP_CUDA(ctx->samples.ensure(std::max<int64_t>(total, 1) * sizeof(pp_sample)));
+  PP_CUDA(ctx->seg_off.ensure((n_seg + 1) * sizeof(int64_t)));
+  PP_CUDA(ctx->ordered.ensure(std::max<int64_t>(total, 1) * sizeof(pp_sample)));
+  if (total > 0)
+    PP_CUDA(cudaMemcpyAsync(ctx->samples.p, samples, total * sizeof(pp_sample), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->seg_off.p, seg_offsets, (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   return PP_OK;
 }
 
@@ -614,20 +770,11 @@ int pp_ctx_destroy(pp_ctx* ctx) {
   if (!ctx) return PP_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->samples, &ctx->seg_off, &ctx->ordered, &ctx->in_d, &ctx->tgt_d,
-                    &ctx->sort_keys, &ctx->sort_vals, &ctx->range, &ctx->grid_ax, &ctx->grid_cells,
-                    &ctx->layouts, &ctx->tabT, &ctx->tabM, &ctx->row_w, &ctx->row_off, &ctx->stats_d,
-                    &ctx->band_base, &ctx->band, &ctx->bitmap, &ctx->bitmap_off, &ctx->seg_mode,
-                    &ctx->raw, &ctx->raw_tmp, &ctx->raw_off, &ctx->raw_cnt, &ctx->raw_in_tmp,
-                    &ctx->cand, &ctx->cand_off, &ctx->cand_n, &ctx->active, &ctx->items,
-                    &ctx->results, &ctx->next_buf, &ctx->gstate, &ctx->seg_item_start,
-                    &ctx->seg_item_cnt, &ctx->segdp, &ctx->best_next, &ctx->bound_items,
-                    &ctx->bound_res, &ctx->out_splits, &ctx->out_times, &ctx->out_count,
-                    &ctx->out_tmax, &ctx->out_obj, &ctx->out_status, &ctx->out_err})
-    b->release();
-  for (PinBuf* b : {&ctx->h_range, &ctx->h_stats, &ctx->h_segdp, &ctx->h_misc}) b->release();
+  for (DevBuf* b : ctx->all_bufs()) b->release();
+  for (PinBuf* b : {&ctx->h_range, &ctx->h_stats, &ctx->h_segdp}) b->release();
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->kev) cudaEventDestroy(e);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PP_OK;
@@ -694,6 +841,11 @@ int pp_plan_grid_device(pp_ctx* ctx, const pp_sample* d_samples, const int64_t* 
   c.d_obj = d_out->objective;
   c.d_status = d_out->status;
   c.d_err = d_out->err_sample_id;
+  if (!c.d_ordered) {  // the sort output is needed internally
+    const int64_t total = h_seg_offsets[n_seg];
+    PP_CUDA(ctx->ordered.ensure(std::max<int64_t>(total, 1) * sizeof(pp_sample)));
+    c.d_ordered = ctx->ordered.as<pp_sample>();
+  }
   return run_plan(ctx, c);
 }
 
@@ -707,9 +859,7 @@ int pp_plan_grid(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offse
   if ((rc = validate_opts(ctx, *opts))) return rc;
   const int64_t total = seg_offsets[n_seg];
   cudaStream_t st = ctx->stream;
-  PP_CUDA(ctx->samples.ensure(std::max<int64_t>(total, 1) * sizeof(pp_sample)));
-  PP_CUDA(ctx->seg_off.ensure((n_seg + 1) * sizeof(int64_t)));
-  PP_CUDA(ctx->ordered.ensure(std::max<int64_t>(total, 1) * sizeof(pp_sample)));
+  if ((rc = stage_inputs(ctx, samples, seg_offsets, n_seg))) return rc;
   PP_CUDA(ctx->out_splits.ensure(std::max<int64_t>(total, 1) * sizeof(int32_t)));
   PP_CUDA(ctx->out_times.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
   PP_CUDA(ctx->out_count.ensure(n_seg * sizeof(int32_t)));
@@ -717,9 +867,6 @@ int pp_plan_grid(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offse
   PP_CUDA(ctx->out_obj.ensure(n_seg * sizeof(double)));
   PP_CUDA(ctx->out_status.ensure(n_seg * sizeof(int32_t)));
   PP_CUDA(ctx->out_err.ensure(n_seg * sizeof(int64_t)));
-  if (total > 0)
-    PP_CUDA(cudaMemcpyAsync(ctx->samples.p, samples, total * sizeof(pp_sample), cudaMemcpyHostToDevice, st));
-  PP_CUDA(cudaMemcpyAsync(ctx->seg_off.p, seg_offsets, (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   pp_plan_out d{};
   d.ordered = ctx->ordered.as<pp_sample>();
   d.splits = ctx->out_splits.as<int32_t>();
@@ -756,17 +903,13 @@ int pp_order_samples(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_o
     if (seg_offsets[s + 1] <= seg_offsets[s]) return fail(ctx, PP_ERR_INVALID, "mini-batch is empty");
   const int64_t total = seg_offsets[n_seg];
   cudaStream_t st = ctx->stream;
-  PP_CUDA(ctx->samples.ensure(total * sizeof(pp_sample)));
-  PP_CUDA(ctx->seg_off.ensure((n_seg + 1) * sizeof(int64_t)));
-  PP_CUDA(ctx->ordered.ensure(total * sizeof(pp_sample)));
+  if ((rc = stage_inputs(ctx, samples, seg_offsets, n_seg))) return rc;
   PP_CUDA(ctx->in_d.ensure(total * sizeof(double)));
   PP_CUDA(ctx->tgt_d.ensure(total * sizeof(double)));
   PP_CUDA(ctx->range.ensure(6 * sizeof(unsigned long long)));
   PP_CUDA(ctx->h_range.ensure(6 * sizeof(unsigned long long)));
   PP_CUDA(ctx->sort_keys.ensure(total * 6 * sizeof(unsigned long long)));
   PP_CUDA(ctx->sort_vals.ensure(total * 2 * sizeof(uint32_t)));
-  PP_CUDA(cudaMemcpyAsync(ctx->samples.p, samples, total * sizeof(pp_sample), cudaMemcpyHostToDevice, st));
-  PP_CUDA(cudaMemcpyAsync(ctx->seg_off.p, seg_offsets, (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   PP_CUDA(launch_segmented_sort(ctx->samples.as<pp_sample>(), ctx->seg_off.as<int64_t>(), seg_offsets,
                                 n_seg, total, 0, ctx->range.as<unsigned long long>(),
                                 ctx->h_range.as<unsigned long long>(),
@@ -785,50 +928,32 @@ int pp_candidate_range(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg
   if (rc) return rc;
   if (!samples || !seg_offsets || n_seg < 1 || !t_min || !t_max)
     return fail(ctx, PP_ERR_INVALID, "bad arguments");
-  const int64_t total = seg_offsets[n_seg];
-  if (total <= 0) return fail(ctx, PP_ERR_INVALID, "mini-batch is empty");
-  cudaStream_t st = ctx->stream;
+  if (seg_offsets[0] != 0 || seg_offsets[n_seg] <= 0) return fail(ctx, PP_ERR_INVALID, "mini-batch is empty");
+  ctx->kused = 0;
+  ctx->kcat.clear();
   GridDev g{};
   if ((rc = upload_grid(ctx, grid, model, &g))) return rc;
-  PP_CUDA(ctx->samples.ensure(total * sizeof(pp_sample)));
-  PP_CUDA(ctx->seg_off.ensure((n_seg + 1) * sizeof(int64_t)));
-  PP_CUDA(ctx->ordered.ensure(total * sizeof(pp_sample)));
-  PP_CUDA(ctx->in_d.ensure(total * sizeof(double)));
-  PP_CUDA(ctx->tgt_d.ensure(total * sizeof(double)));
-  PP_CUDA(ctx->range.ensure(6 * sizeof(unsigned long long)));
-  PP_CUDA(ctx->h_range.ensure(6 * sizeof(unsigned long long)));
-  PP_CUDA(ctx->sort_keys.ensure(total * 6 * sizeof(unsigned long long)));
-  PP_CUDA(ctx->sort_vals.ensure(total * 2 * sizeof(uint32_t)));
-  PP_CUDA(ctx->row_w.ensure(total * sizeof(int)));
-  PP_CUDA(ctx->stats_d.ensure(n_seg * sizeof(SegStats)));
-  PP_CUDA(ctx->h_stats.ensure(n_seg * sizeof(SegStats)));
-  PP_CUDA(cudaMemcpyAsync(ctx->samples.p, samples, total * sizeof(pp_sample), cudaMemcpyHostToDevice, st));
-  PP_CUDA(cudaMemcpyAsync(ctx->seg_off.p, seg_offsets, (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  PP_CUDA(launch_segmented_sort(ctx->samples.as<pp_sample>(), ctx->seg_off.as<int64_t>(), seg_offsets,
-                                n_seg, total, presorted, ctx->range.as<unsigned long long>(),
-                                ctx->h_range.as<unsigned long long>(),
-                                ctx->sort_keys.as<unsigned long long>(), ctx->sort_vals.as<uint32_t>(),
-                                ctx->ordered.as<pp_sample>(), ctx->in_d.as<double>(),
-                                ctx->tgt_d.as<double>(), st));
-  SegStats* hs = ctx->h_stats.as<SegStats>();
-  for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0};
-  PP_CUDA(cudaMemcpyAsync(ctx->stats_d.p, hs, n_seg * sizeof(SegStats), cudaMemcpyHostToDevice, st));
+  if ((rc = stage_inputs(ctx, samples, seg_offsets, n_seg))) return rc;
+  PlanCall c;
+  c.d_samples = ctx->samples.as<pp_sample>();
+  c.d_seg_off = ctx->seg_off.as<int64_t>();
+  c.h_seg_off = seg_offsets;
+  c.n_seg = n_seg;
+  c.presorted = presorted;
+  c.opts.stage_count = 2;
+  c.opts.replica_count = 1;
+  c.opts.per_mb_mem_cap = cap;
+  c.opts.t_max_interval = 0.0;
+  c.d_ordered = ctx->ordered.as<pp_sample>();
+  std::vector<int> blk_base;
+  int max_n = 0;
   // interval 0: the statistics are over the raw slice times
-  PP_CUDA(launch_row_scan(g, nullptr, nullptr, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
-                          ctx->seg_off.as<int64_t>(), n_seg, total, cap, 0.0, ctx->row_w.as<int>(),
-                          ctx->stats_d.as<SegStats>(), st));
-  PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
-  PP_CUDA(cudaStreamSynchronize(st));
-  auto inv = [](unsigned long long k) {
-    unsigned long long u = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
-    double d;
-    std::memcpy(&d, &u, 8);
-    return d;
-  };
+  if ((rc = cost_pass_a(ctx, c, g, 0.0, blk_base, max_n))) return rc;
+  const SegStats* hs = ctx->h_stats.as<SegStats>();
   for (int s = 0; s < n_seg; ++s) {
     const bool any = hs[s].kmin != ~0ULL;
-    t_min[s] = (hs[s].flags & 2) ? -INFINITY : any ? inv(hs[s].kmin) : (hs[s].flags & 1) ? INFINITY : NAN;
-    t_max[s] = (hs[s].flags & 1) ? INFINITY : any ? inv(hs[s].kmax) : (hs[s].flags & 2) ? -INFINITY : NAN;
+    t_min[s] = (hs[s].flags & 2) ? -INFINITY : any ? dkey_inv_host(hs[s].kmin) : (hs[s].flags & 1) ? INFINITY : NAN;
+    t_max[s] = (hs[s].flags & 1) ? INFINITY : any ? dkey_inv_host(hs[s].kmax) : (hs[s].flags & 2) ? -INFINITY : NAN;
   }
   return PP_OK;
 }

@@ -1,27 +1,29 @@
-// cost.cu — fused slice costing on sm_100a: the triangular slice tables the
-// reference builds with n(n+1)/2 std::function calls (microbatch.cpp:228-243),
-// produced on the device as a compact *band*.
+// cost.cu — fused slice costing on sm_100a.  Produces, on the device, the
+// slice-time table the reference builds with n(n+1)/2 std::function calls
+// (microbatch.cpp:228-243), stored as a compact *band* of 32-row tiles.
 //
-// Pass A (row_scan_kernel): one warp per row i scans every j in (i, n],
-//   prices the slice [i, j) bit-exactly (pp_internal.cuh::slice_cost, the
-//   make_slice_cost lambda microbatch.cpp:136-158 + estimate cost_model.cpp:294-319),
-//   and records
-//     - the last memory-feasible end  Rm(i) = max{ j : !(M[i,j] > cap) }
-//     - singleton infeasibility (microbatch.cpp:245-251)
-//     - candidate statistics (microbatch.cpp:253-269).
-//   The padded maxima are running maxima along the row (warp max-scan), so
-//   unsorted spans are priced exactly like the reference's O(j-i) loop.
-// Row offsets (row_offsets_kernel): per-segment exclusive scan of widths.
-// Pass B (band_kernel): rewrites T for j in (i, Rm(i)] into the band; slices
-//   with M > cap become NaN (never pass `T <= t_max`).  Candidate values are
-//   set in a per-segment bitmap over k = ceil(T / I) or, for the exact mode
-//   (I == 0) or very wide k ranges, appended for a segmented sort.
-// Candidate compaction (cand_bitmap_kernel / cand_unique_kernel): ascending,
-//   unique candidate t_max list per segment.
+// Mapping: one warp per 32-row block, lane r <-> row i = i0 + r, and a
+// warp-uniform loop over tile columns c (slice end j = i0 + c) in chunks of
+// 32.  Per chunk the warp stages in shared memory the 32 padded-length
+// candidates in[j-1], tgt[j-1] with their pre-bracketed sequence-axis
+// positions, and the 63 micro-batch-size brackets the lanes need, so the
+// inner loop issues no global loads.  Each lane keeps its own running maxima
+// of the padded lengths (microbatch.cpp:143-148), so unsorted spans are
+// priced exactly like the reference; tile writes are 256 B coalesced columns.
 //
-// Every slice outside (i, Rm(i)] has M > cap, so the DP never needs it: the
-// band carries every slice the reference's DP can use, nothing is assumed
-// about monotonicity of the cost model.
+// Pass A (cap < +inf): act_mem only, every j in (i, n]:
+//   Rm(i) = max{ j : !(M[i,j] > cap) } (the last memory-feasible end), the
+//   singleton check (microbatch.cpp:245-251) and the tile width
+//   W_b = max_r (r + w_r) + 1.  With cap = +inf every slice is feasible,
+//   Rm(i) = n, and pass A is replaced by full_rows_kernel.
+// Pass B: T for c in [r+1, r+w_r] into the tile (NaN where M > cap: it never
+//   passes `T <= t_max`, exactly like the reference's `continue` at
+//   microbatch.cpp:179), plus the candidate statistics (microbatch.cpp:253-269).
+// Pass C (band_cand_kernel): reads the band back and marks candidate values
+//   k = ceil(T / I) in a per-segment bitmap, or appends raw values for a
+//   segmented sort (exact mode I == 0, or very wide k ranges).
+// Every slice outside (i, Rm(i)] has M > cap, so the DP never needs it; no
+// monotonicity of the cost model is assumed anywhere.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,14 +34,9 @@
 
 namespace ppb {
 
-__device__ __forceinline__ int seg_of_row(const int64_t* seg_off, int n_seg, int64_t r) {
-  int lo = 0, hi = n_seg - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (seg_off[mid] <= r) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
+namespace {
+
+constexpr int kCostWarps = 8;
 
 // Stage the (small) grid tables in shared memory.
 __device__ __forceinline__ GridDev stage_grid(const GridDev& g, double* sm, Layout* sl) {
@@ -57,155 +54,312 @@ __device__ __forceinline__ GridDev stage_grid(const GridDev& g, double* sm, Layo
   return s;
 }
 
-__device__ __forceinline__ double dmax(double a, double b) { return (a < b) ? b : a; }
-
-// Inclusive warp max-scan.
-__device__ __forceinline__ double warp_max_scan(double x, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x = dmax(x, y);
+// bracket() of the mbs axis for every micro-batch size 1..max_n.
+__global__ void mbs_bracket_kernel(GridDev g, int max_n, int* __restrict__ seg,
+                                   double* __restrict__ t) {
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m <= max_n; m += gridDim.x * blockDim.x) {
+    int s;
+    double w;
+    bracket(g.mbs_ax, g.n_mbs, (double)m, s, w);
+    seg[m] = s;
+    t[m] = w;
   }
-  return x;
 }
 
-// kTable: slice costs come from host-evaluated triangular tables (the generic
-// SliceCostFn path, microbatch.cpp:237-243) instead of the fused grid coster.
-template <bool kBand, bool kTable>
-__global__ void __launch_bounds__(256)
-    row_kernel(GridDev g, int stage, const double* __restrict__ tabT, const double* __restrict__ tabM, const double* __restrict__ in_d, const double* __restrict__ tgt_d,
-               const int64_t* __restrict__ seg_off, int n_seg, int64_t total_rows, double cap,
-               double interval, int* __restrict__ row_w, SegStats* __restrict__ stats,
-               const int64_t* __restrict__ row_off, const int64_t* __restrict__ seg_band_base,
-               double* __restrict__ band, unsigned int* __restrict__ bitmap,
-               const int64_t* __restrict__ bitmap_off, const int* __restrict__ seg_mode,
-               unsigned long long* __restrict__ cand_raw, const int64_t* __restrict__ cand_raw_off,
-               unsigned long long* __restrict__ cand_raw_cnt) {
+// bracket() of the sequence axis at every ordered sample's input / target length.
+__global__ void seq_bracket_kernel(GridDev g, const double* __restrict__ in_d,
+                                   const double* __restrict__ tgt_d, int64_t total,
+                                   int* __restrict__ si_in, double* __restrict__ ts_in,
+                                   int* __restrict__ si_tg, double* __restrict__ ts_tg) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int s;
+    double w;
+    bracket(g.seq_ax, g.n_seq, in_d[k], s, w);
+    si_in[k] = s;
+    ts_in[k] = w;
+    bracket(g.seq_ax, g.n_seq, tgt_d[k], s, w);
+    si_tg[k] = s;
+    ts_tg[k] = w;
+  }
+}
+
+struct CostArgs {
+  GridDev g;
+  int stage;
+  const double* tabT;
+  const double* tabM;
+  const double* in_d;
+  const double* tgt_d;
+  const int* si_in;
+  const double* ts_in;
+  const int* si_tg;
+  const double* ts_tg;
+  const int64_t* seg_off;
+  const int* blk_base;
+  int n_seg;
+  int total_blocks;
+  int max_n;
+  const int* mb_seg;
+  const double* mb_t;
+  double cap;
+  double interval;
+  int* row_w;
+  int* blk_W;
+  SegStats* stats;
+  const int64_t* tile_off;
+  const int64_t* seg_band_base;
+  double* band;
+};
+
+// PASS 0 = A (act_mem, Rm, singleton check, W_b); PASS 1 = B (band + stats).
+template <int PASS, bool kTable>
+__global__ void __launch_bounds__(32 * kCostWarps)
+    block_kernel(CostArgs a) {
   extern __shared__ __align__(16) double sm_grid[];
   __shared__ Layout sm_lay[kMaxLayouts];
+  __shared__ double s_x[kCostWarps][32], s_y[kCostWarps][32];
+  __shared__ double s_tx[kCostWarps][32], s_ty[kCostWarps][32];
+  __shared__ int s_sx[kCostWarps][32], s_sy[kCostWarps][32];
+  __shared__ double s_mt[kCostWarps][64];
+  __shared__ int s_ms[kCostWarps][64];
   // Small grids (every realistic profile: 648 cells) are staged in shared
   // memory; oversized ones are read through L1 from global memory.
-  const GridDev G = stage ? stage_grid(g, sm_grid, sm_lay) : g;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < total_rows;
-       r += warps) {
-    const int s = seg_of_row(seg_off, n_seg, r);
-    const int64_t b = seg_off[s];
-    const int n = (int)(seg_off[s + 1] - b);
-    const int i = (int)(r - b);
-    int jend = n;
-    if (kBand) jend = i + row_w[r];
-    double cin = 0.0, ctg = 0.0;  // shape.input_len = 0 / target_len = 0 (:143-144)
+  const GridDev G = (a.stage && !kTable) ? stage_grid(a.g, sm_grid, sm_lay) : a.g;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warps = gridDim.x * kCostWarps;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  const bool need_mem = PASS == 0 || !(a.cap == INF);
+  // bracket of the initial padded length 0.0 (shape.input_len = 0, :143-144)
+  int si0 = 0;
+  double ts0 = 0.0;
+  if (!kTable) bracket(G.seq_ax, G.n_seq, 0.0, si0, ts0);
+  for (int gb = blockIdx.x * kCostWarps + wid; gb < a.total_blocks; gb += warps) {
+    const int s = seg_of(a.blk_base, a.n_seg, gb);
+    const int64_t b0 = a.seg_off[s];
+    const int n = (int)(a.seg_off[s + 1] - b0);
+    const int bl = gb - a.blk_base[s];
+    const int i1 = n - kRB * bl;
+    const int i0 = max(0, i1 - kRB);
+    const int nb = i1 - i0;
+    const int r = lane;
+    const bool rowv = r < nb;
+    const int i = i0 + r;
+    int wr = 0, cend;
+    double* tile = nullptr;
+    if (PASS == 1) {
+      wr = rowv ? a.row_w[b0 + i] : 0;
+      cend = a.blk_W[gb] - 1;
+      tile = a.band + a.seg_band_base[s] + a.tile_off[gb];
+    } else {
+      cend = n - i0;
+    }
+    // running padded maxima and their sequence brackets
+    double pin = 0.0, ptg = 0.0;
+    int si_e = si0, si_d = si0;
+    double ts_e = ts0, ts_d = ts0;
     int last_ok = i;
-    double kmn = __longlong_as_double(0x7ff0000000000000LL), kmx = -kmn;  // +inf / -inf
+    double kmn = INF, kmx = -INF;
     unsigned long long nraw = 0;
     int flags = 0;
-    double* brow = nullptr;
-    int mode = 0;
-    if (kBand) {
-      brow = band + seg_band_base[s] + row_off[r] - (i + 1);
-      mode = seg_mode[s];
-    }
-    for (int j0 = i + 1; j0 <= jend; j0 += 32) {
-      const int j = j0 + lane;
-      const bool valid = j <= jend;
-      double xi = -__longlong_as_double(0x7ff0000000000000LL), xt = xi;
-      if (valid && !kTable) {
-        xi = in_d[b + j - 1];
-        xt = tgt_d[b + j - 1];
+    const int64_t trow = kTable ? (int64_t)i * n - (int64_t)i * (i - 1) / 2 - (i + 1) : 0;
+    for (int c0 = 1; c0 <= cend; c0 += 32) {
+      if (!kTable) {
+        // stage the chunk: column c0 + q reads sample index i0 + c0 + q - 1
+        const int cq = c0 + lane;
+        if (cq <= cend) {
+          const int64_t k = b0 + i0 + cq - 1;
+          s_x[wid][lane] = a.in_d[k];
+          s_y[wid][lane] = a.tgt_d[k];
+          s_sx[wid][lane] = a.si_in[k];
+          s_tx[wid][lane] = a.ts_in[k];
+          s_sy[wid][lane] = a.si_tg[k];
+          s_ty[wid][lane] = a.ts_tg[k];
+        }
+        // micro-batch sizes m = c - r in [c0 - 31, c0 + 31] -> slot m - (c0 - 32)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int p = lane + 32 * h;
+          const int m = min(max(c0 - 32 + p, 1), a.max_n);
+          s_ms[wid][p] = a.mb_seg[m];
+          s_mt[wid][p] = a.mb_t[m];
+        }
+        __syncwarp();
       }
-      const double pin = dmax(cin, warp_max_scan(xi, lane));
-      const double ptg = dmax(ctg, warp_max_scan(xt, lane));
-      cin = __shfl_sync(0xffffffffu, pin, 31);
-      ctg = __shfl_sync(0xffffffffu, ptg, 31);
-      double T = 0.0, M = 0.0;
-      bool ok = false;
-      if (valid) {
+      const int qend = min(32, cend - c0 + 1);
+      for (int q = 0; q < qend; ++q) {
+        const int c = c0 + q;
+        const int j = i0 + c;
+        const bool live = rowv && c >= r + 1 && (PASS == 0 || c <= r + wr);
+        if (!live) continue;
+        double T = 0.0, M = 0.0;
+        bool ok = true;
         if (kTable) {
-          const int64_t idx = (int64_t)i * n - (int64_t)i * (i - 1) / 2 + (j - i - 1);
-          T = tabT[idx];
-          M = tabM[idx];
+          T = a.tabT[trow + j];
+          M = a.tabM[trow + j];
+          ok = !(M > a.cap);
         } else {
-          slice_cost(G, (double)(j - i), pin, ptg, T, M);
+          const double x = s_x[wid][q];
+          if (pin < x) {
+            pin = x;
+            si_e = s_sx[wid][q];
+            ts_e = s_tx[wid][q];
+          }
+          const double y = s_y[wid][q];
+          if (ptg < y) {
+            ptg = y;
+            si_d = s_sy[wid][q];
+            ts_d = s_ty[wid][q];
+          }
+          Query qq;
+          const int p = q - r + 32;
+          qq.mi = s_ms[wid][p];
+          qq.tm = s_mt[wid][p];
+          qq.si_enc = si_e;
+          qq.ts_enc = ts_e;
+          if (G.is_encdec) {
+            qq.si_dec = si_d;
+            qq.ts_dec = ts_d;
+          } else {
+            qq.si_dec = si_e;
+            qq.ts_dec = ts_e;
+          }
+          if (need_mem) {
+            M = slice_mem(G, qq);
+            ok = !(M > a.cap);
+          }
+          if (PASS == 1 && ok) T = slice_time(G, qq);
         }
-        ok = !(M > cap);
-        if (!kBand) {
+        if (PASS == 0) {
           if (ok) last_ok = j;
-          if (j == i + 1 && !ok) atomicMin(&stats[s].err_row, i);
+          if (c == r + 1 && !ok) atomicMin(&a.stats[s].err_row, i);
         } else {
-          brow[j] = ok ? T : masked();
-        }
-      }
-      const bool is_cand = valid && ok && !isnan(T);
-      double q = T;
-      if (is_cand && interval > 0) q = ceil(__ddiv_rn(T, interval));
-      if (!kBand) {
-        if (is_cand) {
-          ++nraw;
-          if (isinf(q)) flags |= (q > 0) ? 1 : 2;
-          else {
-            kmn = (q < kmn) ? q : kmn;
-            kmx = (kmx < q) ? q : kmx;
+          tile[(size_t)c * kRB + r] = ok ? T : masked();
+          if (ok && !isnan(T)) {
+            double qv = T;
+            if (a.interval > 0) qv = ceil(__ddiv_rn(T, a.interval));
+            ++nraw;
+            if (isinf(qv)) {
+              flags |= (qv > 0) ? 1 : 2;
+            } else {
+              kmn = (qv < kmn) ? qv : kmn;
+              kmx = (kmx < qv) ? qv : kmx;
+            }
           }
         }
-      } else if (mode == 0) {  // bitmap over k
-        const bool fin = is_cand && !isinf(q);
-        long long bit = -1;
-        if (fin) bit = (long long)(q - dkey_inv(stats[s].kmin));
-        const long long prev = __shfl_up_sync(0xffffffffu, bit, 1);
-        if (fin && (lane == 0 || prev != bit))
-          atomicOr(&bitmap[bitmap_off[s] + (bit >> 5)], 1u << (bit & 31));
-      } else if (mode == 1) {  // raw list for the segmented sort (mode 2: c == 1, no candidates)
-        const unsigned int m = __ballot_sync(0xffffffffu, is_cand);
-        unsigned long long base = 0;
-        if (lane == 0 && m) base = atomicAdd(&cand_raw_cnt[s], (unsigned long long)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (is_cand) {
-          const double qq = interval > 0 ? __dmul_rn(q, interval) : T;
-          cand_raw[cand_raw_off[s] + base + __popc(m & ((1u << lane) - 1))] = dkey(qq);
-        }
       }
+      if (!kTable) __syncwarp();
     }
-    if (!kBand) {
+    if (PASS == 0) {
+      const int w = rowv ? last_ok - i : 0;
+      if (rowv) a.row_w[b0 + i] = w;
+      int wmax = rowv ? r + w : 0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+      if (lane == 0) a.blk_W[gb] = wmax + 1;
+    } else {
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
-        last_ok = max(last_ok, __shfl_xor_sync(0xffffffffu, last_ok, o));
-        const double a = __shfl_xor_sync(0xffffffffu, kmn, o);
-        const double c = __shfl_xor_sync(0xffffffffu, kmx, o);
-        kmn = (a < kmn) ? a : kmn;
-        kmx = (kmx < c) ? c : kmx;
+        const double x = __shfl_xor_sync(0xffffffffu, kmn, o);
+        const double y = __shfl_xor_sync(0xffffffffu, kmx, o);
+        kmn = (x < kmn) ? x : kmn;
+        kmx = (kmx < y) ? y : kmx;
         nraw += __shfl_xor_sync(0xffffffffu, nraw, o);
         flags |= __shfl_xor_sync(0xffffffffu, flags, o);
       }
       if (lane == 0) {
-        row_w[r] = last_ok - i;
         if (nraw) {
-          atomicAdd(&stats[s].nraw, nraw);
+          atomicAdd(&a.stats[s].nraw, nraw);
           if (!isinf(kmn)) {
-            atomicMin(&stats[s].kmin, dkey(kmn));
-            atomicMax(&stats[s].kmax, dkey(kmx));
+            atomicMin(&a.stats[s].kmin, dkey(kmn));
+            atomicMax(&a.stats[s].kmax, dkey(kmx));
           }
         }
-        if (flags) atomicOr(&stats[s].flags, flags);
+        if (flags) atomicOr(&a.stats[s].flags, flags);
       }
     }
   }
 }
 
-// Per-segment exclusive scan of the row widths -> band offsets.
+// cap = +inf: every slice is memory-feasible (!(M > inf) holds for every M,
+// NaN included), so Rm(i) = n and W_b = n - i0 + 1 without costing anything.
+__global__ void full_rows_kernel(const int64_t* __restrict__ seg_off, const int* __restrict__ blk_base,
+                                 int n_seg, int total_blocks, int* __restrict__ row_w,
+                                 int* __restrict__ blk_W) {
+  for (int gb = blockIdx.x * blockDim.x + threadIdx.x; gb < total_blocks;
+       gb += gridDim.x * blockDim.x) {
+    const int s = seg_of(blk_base, n_seg, gb);
+    const int64_t b0 = seg_off[s];
+    const int n = (int)(seg_off[s + 1] - b0);
+    const int bl = gb - blk_base[s];
+    const int i1 = n - kRB * bl;
+    const int i0 = max(0, i1 - kRB);
+    for (int i = i0; i < i1; ++i) row_w[b0 + i] = n - i;
+    blk_W[gb] = n - i0 + 1;
+  }
+}
+
+// Pass C: candidate values from the band (microbatch.cpp:259-266).
+__global__ void __launch_bounds__(256)
+    band_cand_kernel(const int64_t* __restrict__ seg_off, const int* __restrict__ blk_base, int n_seg,
+                     int total_blocks, const int* __restrict__ blk_W,
+                     const int64_t* __restrict__ tile_off, const int64_t* __restrict__ seg_band_base,
+                     const double* __restrict__ band, double interval,
+                     const SegStats* __restrict__ stats, unsigned int* __restrict__ bitmap,
+                     const int64_t* __restrict__ bitmap_off, const int* __restrict__ seg_mode,
+                     unsigned long long* __restrict__ cand_raw,
+                     const int64_t* __restrict__ cand_raw_off,
+                     unsigned long long* __restrict__ cand_raw_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int gb = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gb < total_blocks; gb += warps) {
+    const int s = seg_of(blk_base, n_seg, gb);
+    const int mode = seg_mode[s];
+    if (mode > 1) continue;
+    const double* tile = band + seg_band_base[s] + tile_off[gb];
+    const int W = blk_W[gb];
+    const double kmin = mode == 0 ? dkey_inv(stats[s].kmin) : 0.0;
+    unsigned int* bm = bitmap + bitmap_off[s];
+    long long last_bit = -1;
+    for (int c = 1; c < W; ++c) {
+      const double T = tile[(size_t)c * kRB + lane];
+      if (isnan(T)) continue;
+      double q = T;
+      if (interval > 0) q = ceil(__ddiv_rn(T, interval));
+      if (mode == 0) {
+        if (isinf(q)) continue;  // +-inf candidates come from the flags
+        const long long bit = (long long)(q - kmin);
+        if (bit != last_bit) {
+          atomicOr(&bm[bit >> 5], 1u << (bit & 31));
+          last_bit = bit;
+        }
+      } else {
+        double qq = interval > 0 ? __dmul_rn(q, interval) : T;
+        if (qq == 0.0) qq = 0.0;  // +0.0: the reference's order of equal +-0 is unspecified
+        const unsigned long long slot = atomicAdd(&cand_raw_cnt[s], 1ULL);
+        cand_raw[cand_raw_off[s] + slot] = dkey(qq);
+      }
+    }
+  }
+}
+
+// Per-segment exclusive scan of tile sizes (32 x W_b doubles) -> tile offsets.
 __global__ void __launch_bounds__(1024)
-    row_offsets_kernel(const int* __restrict__ row_w, const int64_t* __restrict__ seg_off,
-                       int64_t* __restrict__ row_off, SegStats* __restrict__ stats) {
+    tile_offsets_kernel(const int* __restrict__ blk_W, const int* __restrict__ blk_base,
+                        int64_t* __restrict__ tile_off, SegStats* __restrict__ stats) {
   __shared__ long long warp_tot[32];
+  __shared__ int wmax;
   const int s = blockIdx.x;
-  const int64_t b = seg_off[s];
-  const int n = (int)(seg_off[s + 1] - b);
+  const int b = blk_base[s];
+  const int nbk = blk_base[s + 1] - b;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) wmax = 0;
+  __syncthreads();
   long long carry = 0;
-  for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+  for (int t0 = 0; t0 < nbk; t0 += blockDim.x) {
     const int k = t0 + threadIdx.x;
-    const long long v = k < n ? row_w[b + k] : 0;
+    if (k < nbk) atomicMax(&wmax, blk_W[b + k]);
+    const long long v = k < nbk ? (long long)kRB * blk_W[b + k] : 0;
     long long x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -225,11 +379,14 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();
     const long long before = wid ? warp_tot[wid - 1] : 0;
-    if (k < n) row_off[b + k] = carry + before + x - v;
+    if (k < nbk) tile_off[b + k] = carry + before + x - v;
     carry += warp_tot[31];
     __syncthreads();
   }
-  if (threadIdx.x == 0) stats[s].band = carry;
+  if (threadIdx.x == 0) {
+    stats[s].band = carry;
+    stats[s].wmax = wmax;
+  }
 }
 
 // Bitmap -> ascending candidate list (k * I), with the +/-inf flags.
@@ -278,7 +435,9 @@ __global__ void __launch_bounds__(1024)
       const int bit = __ffs(rem) - 1;
       rem &= rem - 1;
       const double kk = kmin + (double)(k * 32 + bit);  // exact: integers < 2^52
-      out[pos++] = __dmul_rn(kk, interval);             // ceil(t / I) * I (:264)
+      double q = __dmul_rn(kk, interval);               // ceil(t / I) * I (:264)
+      if (q == 0.0) q = 0.0;                            // canonical +0.0 (see band_cand_kernel)
+      out[pos++] = q;
     }
     carry += warp_tot[31];
     __syncthreads();
@@ -290,7 +449,7 @@ __global__ void __launch_bounds__(1024)
 }
 
 // After the segmented sort of raw keys: std::unique with operator== on the
-// doubles (so -0.0 and +0.0 collapse, keeping the first), one CTA per segment.
+// doubles, one CTA per segment.
 __global__ void __launch_bounds__(1024)
     cand_unique_kernel(const unsigned long long* __restrict__ keys_a,
                        const unsigned long long* __restrict__ keys_b, const int* __restrict__ in_b,
@@ -339,61 +498,77 @@ __global__ void __launch_bounds__(1024)
   if (threadIdx.x == 0) cand_n[s] = carry;
 }
 
-// ---------------------------------------------------------------- launchers
-static size_t grid_smem(const GridDev& g) {
+size_t grid_smem(const GridDev& g) {
   return sizeof(double) * ((size_t)g.n_mbs + g.n_seq + 2 * (size_t)g.n_mbs * g.n_seq * 3);
 }
-static bool grid_fits(const GridDev& g) {
-  return grid_smem(g) <= 160 * 1024 && g.n_layouts <= kMaxLayouts;
-}
+bool grid_fits(const GridDev& g) { return grid_smem(g) <= 160 * 1024 && g.n_layouts <= kMaxLayouts; }
 
-cudaError_t launch_row_scan(const GridDev& g, const double* tabT, const double* tabM,
-                            const double* in_d, const double* tgt_d,
-                            const int64_t* seg_off, int n_seg, int64_t total_rows, double cap,
-                            double interval, int* row_w, SegStats* stats, cudaStream_t st) {
-  const int stage = grid_fits(g) ? 1 : 0;
-  const size_t sm = stage ? grid_smem(g) : 0;
-  const int64_t blocks = std::max<int64_t>(std::min<int64_t>((total_rows + 7) / 8, 148 * 64), 1);
-  if (tabT) {
-    row_kernel<false, true><<<(int)blocks, 256, 0, st>>>(
-        g, 0, tabT, tabM, in_d, tgt_d, seg_off, n_seg, total_rows, cap, interval, row_w, stats,
-        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
-    return cudaGetLastError();
-  }
-  cudaFuncSetAttribute(row_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  row_kernel<false, false><<<(int)blocks, 256, sm, st>>>(
-      g, stage, nullptr, nullptr, in_d, tgt_d, seg_off, n_seg, total_rows, cap, interval, row_w, stats, nullptr, nullptr,
-      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_brackets(const GridDev& g, int max_n, int* mseg, double* mt, const double* in_d,
+                            const double* tgt_d, int64_t total, int* si_in, double* ts_in, int* si_tg,
+                            double* ts_tg, cudaStream_t st) {
+  mbs_bracket_kernel<<<(max_n + 256) / 256, 256, 0, st>>>(g, max_n, mseg, mt);
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  if (total > 0)
+    seq_bracket_kernel<<<std::max(blocks, 1), 256, 0, st>>>(g, in_d, tgt_d, total, si_in, ts_in, si_tg,
+                                                            ts_tg);
   return cudaGetLastError();
 }
 
-cudaError_t launch_row_offsets(const int* row_w, const int64_t* seg_off, int n_seg, int64_t* row_off,
-                               SegStats* stats, cudaStream_t st) {
-  row_offsets_kernel<<<n_seg, 1024, 0, st>>>(row_w, seg_off, row_off, stats);
+// pass: 0 = A, 1 = B.  tabT != null selects the table source.
+cudaError_t launch_cost_pass(int pass, const GridDev& g, const double* tabT, const double* tabM,
+                             const double* in_d, const double* tgt_d, const int* si_in,
+                             const double* ts_in, const int* si_tg, const double* ts_tg,
+                             const int64_t* seg_off, const int* blk_base, int n_seg,
+                             int total_blocks, int max_n, const int* mb_seg, const double* mb_t,
+                             double cap, double interval, int* row_w, int* blk_W, SegStats* stats,
+                             const int64_t* tile_off, const int64_t* seg_band_base, double* band,
+                             cudaStream_t st) {
+  CostArgs a{g, 0, tabT, tabM, in_d, tgt_d, si_in, ts_in, si_tg, ts_tg, seg_off, blk_base, n_seg,
+             total_blocks, max_n, mb_seg, mb_t, cap, interval, row_w, blk_W, stats, tile_off,
+             seg_band_base, band};
+  a.stage = (!tabT && grid_fits(g)) ? 1 : 0;
+  const size_t sm = a.stage ? grid_smem(g) : 0;
+  const int blocks = std::max(1, std::min((total_blocks + kCostWarps - 1) / kCostWarps, 148 * 32));
+#define PP_COST_LAUNCH(P, T)                                                                        \
+  do {                                                                                              \
+    cudaFuncSetAttribute(block_kernel<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    block_kernel<P, T><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                     \
+  } while (0)
+  if (pass == 0) {
+    if (tabT) PP_COST_LAUNCH(0, true); else PP_COST_LAUNCH(0, false);
+  } else {
+    if (tabT) PP_COST_LAUNCH(1, true); else PP_COST_LAUNCH(1, false);
+  }
+#undef PP_COST_LAUNCH
   return cudaGetLastError();
 }
 
-cudaError_t launch_band(const GridDev& g, const double* tabT, const double* tabM, const double* in_d, const double* tgt_d,
-                        const int64_t* seg_off, int n_seg, int64_t total_rows, double cap,
-                        double interval, int* row_w, SegStats* stats, const int64_t* row_off,
-                        const int64_t* seg_band_base, double* band, unsigned int* bitmap,
-                        const int64_t* bitmap_off, const int* seg_mode,
-                        unsigned long long* cand_raw, const int64_t* cand_raw_off,
-                        unsigned long long* cand_raw_cnt, cudaStream_t st) {
-  const int stage = grid_fits(g) ? 1 : 0;
-  const size_t sm = stage ? grid_smem(g) : 0;
-  const int64_t blocks = std::max<int64_t>(std::min<int64_t>((total_rows + 7) / 8, 148 * 64), 1);
-  if (tabT) {
-    row_kernel<true, true><<<(int)blocks, 256, 0, st>>>(
-        g, 0, tabT, tabM, in_d, tgt_d, seg_off, n_seg, total_rows, cap, interval, row_w, stats,
-        row_off, seg_band_base, band, bitmap, bitmap_off, seg_mode, cand_raw, cand_raw_off,
-        cand_raw_cnt);
-    return cudaGetLastError();
-  }
-  cudaFuncSetAttribute(row_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  row_kernel<true, false><<<(int)blocks, 256, sm, st>>>(
-      g, stage, nullptr, nullptr, in_d, tgt_d, seg_off, n_seg, total_rows, cap, interval, row_w, stats, row_off,
-      seg_band_base, band, bitmap, bitmap_off, seg_mode, cand_raw, cand_raw_off, cand_raw_cnt);
+cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
+                             int* row_w, int* blk_W, cudaStream_t st) {
+  full_rows_kernel<<<std::max(1, (total_blocks + 127) / 128), 128, 0, st>>>(seg_off, blk_base, n_seg,
+                                                                             total_blocks, row_w, blk_W);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
+                             const int* blk_W, const int64_t* tile_off, const int64_t* seg_band_base,
+                             const double* band, double interval, const SegStats* stats,
+                             unsigned int* bitmap, const int64_t* bitmap_off, const int* seg_mode,
+                             unsigned long long* cand_raw, const int64_t* cand_raw_off,
+                             unsigned long long* cand_raw_cnt, cudaStream_t st) {
+  const int blocks = std::max(1, std::min((total_blocks + 7) / 8, 148 * 32));
+  band_cand_kernel<<<blocks, 256, 0, st>>>(seg_off, blk_base, n_seg, total_blocks, blk_W, tile_off,
+                                           seg_band_base, band, interval, stats, bitmap, bitmap_off,
+                                           seg_mode, cand_raw, cand_raw_off, cand_raw_cnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_offsets(const int* blk_W, const int* blk_base, int n_seg, int64_t* tile_off,
+                                SegStats* stats, cudaStream_t st) {
+  tile_offsets_kernel<<<n_seg, 1024, 0, st>>>(blk_W, blk_base, tile_off, stats);
   return cudaGetLastError();
 }
 
@@ -410,7 +585,8 @@ cudaError_t launch_cand_unique(const unsigned long long* keys_a, const unsigned 
                                const int* in_b, const int64_t* raw_off,
                                const unsigned long long* raw_cnt, const int* seg_mode, int n_seg,
                                const int64_t* cand_off, double* cand, int* cand_n, cudaStream_t st) {
-  cand_unique_kernel<<<n_seg, 1024, 0, st>>>(keys_a, keys_b, in_b, raw_off, raw_cnt, seg_mode, cand_off, cand, cand_n);
+  cand_unique_kernel<<<n_seg, 1024, 0, st>>>(keys_a, keys_b, in_b, raw_off, raw_cnt, seg_mode, cand_off,
+                                             cand, cand_n);
   return cudaGetLastError();
 }
 

@@ -62,67 +62,80 @@ __device__ __forceinline__ double blend(double tm, double ts, double c00, double
   return (0.0 < v) ? v : 0.0;
 }
 
-struct Cell3 {
-  double tf, tb, act;
-};
-
-// ProfileGrid::per_layer for one kind given pre-bracketed axes.
-__device__ __forceinline__ Cell3 per_layer(const GridDev& g, int kind, int mi, double tm, int si,
-                                           double ts) {
+// One field (0 t_f, 1 t_b, 2 act_mem) of ProfileGrid::per_layer for one kind
+// given pre-bracketed axes (cost_model.cpp:126-150).
+__device__ __forceinline__ double per_layer_field(const GridDev& g, int kind, int mi, double tm,
+                                                  int si, double ts, int f) {
   const int m1 = min(mi + 1, g.n_mbs - 1);
   const int s1 = min(si + 1, g.n_seq - 1);
-  const double* base = g.cells + (size_t)kind * g.n_mbs * g.n_seq * 3;
-  const double* a = base + ((size_t)mi * g.n_seq + si) * 3;
-  const double* b = base + ((size_t)m1 * g.n_seq + si) * 3;
-  const double* c = base + ((size_t)mi * g.n_seq + s1) * 3;
-  const double* d = base + ((size_t)m1 * g.n_seq + s1) * 3;
-  Cell3 r;
-  r.tf = blend(tm, ts, a[0], b[0], c[0], d[0]);
-  r.tb = blend(tm, ts, a[1], b[1], c[1], d[1]);
-  r.act = blend(tm, ts, a[2], b[2], c[2], d[2]);
-  return r;
+  const double* base = g.cells + (size_t)kind * g.n_mbs * g.n_seq * 3 + f;
+  const double c00 = base[((size_t)mi * g.n_seq + si) * 3];
+  const double c10 = base[((size_t)m1 * g.n_seq + si) * 3];
+  const double c01 = base[((size_t)mi * g.n_seq + s1) * 3];
+  const double c11 = base[((size_t)m1 * g.n_seq + s1) * 3];
+  return blend(tm, ts, c00, c10, c01, c11);
 }
 
-// The make_slice_cost lambda for a padded shape (microbatch.cpp:141-155 with
-// estimate(), cost_model.cpp:294-319).  in_len / tgt_len are the padded
-// maxima as doubles (already max(0, .)).
-__device__ __forceinline__ void slice_cost(const GridDev& g, double mbs, double in_len,
-                                           double tgt_len, double& time, double& act) {
-  int mi, si_in, si_dec;
-  double tm, ts_in, ts_dec;
-  bracket(g.mbs_ax, g.n_mbs, mbs, mi, tm);
-  bracket(g.seq_ax, g.n_seq, in_len, si_in, ts_in);
-  const double dec_len = g.is_encdec ? tgt_len : in_len;
-  if (g.is_encdec) {
-    bracket(g.seq_ax, g.n_seq, dec_len, si_dec, ts_dec);
-  } else {
-    si_dec = si_in;
-    ts_dec = ts_in;
-  }
-  double t_best = 0.0, a_best = 0.0;
+// Pre-bracketed query of one slice: mbs bracket (mi, tm), the encoder's
+// sequence bracket (input length) and the decoder's (target length for
+// encoder-decoder models, else the input length) — estimate(),
+// cost_model.cpp:301-317.
+struct Query {
+  int mi, si_enc, si_dec;
+  double tm, ts_enc, ts_dec;
+};
+
+// act_mem of the slice: max over distinct stage layouts of
+// 0.0 + L_enc * act(enc) + L_dec * act(dec) (microbatch.cpp:154).
+__device__ __forceinline__ double slice_mem(const GridDev& g, const Query& q) {
+  double best = 0.0;
   for (int l = 0; l < g.n_layouts; ++l) {
     const Layout lay = g.layouts[l];
-    double ef = 0.0, eb = 0.0, ea = 0.0;
+    double ea = 0.0;
+    if (lay.enc > 0)
+      ea = __dadd_rn(ea, __dmul_rn((double)lay.enc, per_layer_field(g, 0, q.mi, q.tm, q.si_enc, q.ts_enc, 2)));
+    if (lay.dec > 0)
+      ea = __dadd_rn(ea, __dmul_rn((double)lay.dec, per_layer_field(g, 1, q.mi, q.tm, q.si_dec, q.ts_dec, 2)));
+    best = (best < ea) ? ea : best;
+  }
+  return best;
+}
+
+// time of the slice: max over layouts of (t_f + t_b) (microbatch.cpp:153).
+__device__ __forceinline__ double slice_time(const GridDev& g, const Query& q) {
+  double best = 0.0;
+  for (int l = 0; l < g.n_layouts; ++l) {
+    const Layout lay = g.layouts[l];
+    double ef = 0.0, eb = 0.0;
     if (lay.enc > 0) {
-      const Cell3 c = per_layer(g, 0, mi, tm, si_in, ts_in);
       const double L = (double)lay.enc;
-      ef = __dadd_rn(ef, __dmul_rn(L, c.tf));
-      eb = __dadd_rn(eb, __dmul_rn(L, c.tb));
-      ea = __dadd_rn(ea, __dmul_rn(L, c.act));
+      ef = __dadd_rn(ef, __dmul_rn(L, per_layer_field(g, 0, q.mi, q.tm, q.si_enc, q.ts_enc, 0)));
+      eb = __dadd_rn(eb, __dmul_rn(L, per_layer_field(g, 0, q.mi, q.tm, q.si_enc, q.ts_enc, 1)));
     }
     if (lay.dec > 0) {
-      const Cell3 c = per_layer(g, 1, mi, tm, si_dec, ts_dec);
       const double L = (double)lay.dec;
-      ef = __dadd_rn(ef, __dmul_rn(L, c.tf));
-      eb = __dadd_rn(eb, __dmul_rn(L, c.tb));
-      ea = __dadd_rn(ea, __dmul_rn(L, c.act));
+      ef = __dadd_rn(ef, __dmul_rn(L, per_layer_field(g, 1, q.mi, q.tm, q.si_dec, q.ts_dec, 0)));
+      eb = __dadd_rn(eb, __dmul_rn(L, per_layer_field(g, 1, q.mi, q.tm, q.si_dec, q.ts_dec, 1)));
     }
     const double tt = __dadd_rn(ef, eb);
-    t_best = (t_best < tt) ? tt : t_best;
-    a_best = (a_best < ea) ? ea : a_best;
+    best = (best < tt) ? tt : best;
   }
-  time = t_best;
-  act = a_best;
+  return best;
+}
+
+// Rows per band tile (= rows per DP block).  The band of a segment is stored
+// as one tile per block of 32 rows, top-down (block b holds rows
+// [max(0, n-32(b+1)), n-32b)); tile column c holds the 32 rows' values for
+// slice end j = i0 + c, contiguous (256 B per column).
+constexpr int kRB = 32;
+
+__device__ __forceinline__ int seg_of(const int* __restrict__ base, int n_seg, int g) {
+  int lo = 0, hi = n_seg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (base[mid] <= g) lo = mid; else hi = mid - 1;
+  }
+  return lo;
 }
 
 // Masked band entry for a slice excluded by the memory cap.  NaN makes every
@@ -147,8 +160,52 @@ struct SegStats {
   unsigned long long nraw;   // memory-feasible, non-NaN slices (candidate capacity)
   int err_row;               // lowest ordered index whose singleton violates the cap
   int flags;                 // bit0: +inf candidate, bit1: -inf candidate
-  long long band;            // band entries of the segment
+  long long band;            // band entries of the segment (sum of 32 x W_b)
+  int wmax;                  // max tile width W_b of the segment
+  int pad;
 };
+
+// ---- TMA bulk copies + mbarriers (sm_90+ PTX, used on sm_100a) ----------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion reported on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// Order prior generic-proxy accesses of shared memory before async-proxy (TMA) writes.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Named barrier for a subset of warps.
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 // One DP pass: (mini-batch, t_max candidate).
 struct WorkItem {
@@ -156,6 +213,8 @@ struct WorkItem {
   int cand;            // candidate index within the segment (-1: bound pass, t = +inf)
   long long next_off;  // offset of this item's next[] (rows) in the next buffer
   long long state_off; // offset of global state scratch (or -1: shared memory)
+  unsigned state_mask; // state index = j & mask (ring of mask+1 entries, or ~0u: no ring)
+  int state_entries;   // entries per state array
 };
 
 struct ItemResult {
