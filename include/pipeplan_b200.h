@@ -132,6 +132,8 @@ typedef struct pp_stats {
   double  ms_kernel[4];
   int64_t launches[4];
   int64_t dp_band_bytes;          /* band bytes the DP passes read (8 B / transition) */
+  int64_t slices_pass_a;          /* act_mem-only slices priced by cost pass A        */
+  double  exit_thresh;            /* pass-A certified row-exit threshold (+inf: none) */
 } pp_stats;
 
 typedef struct pp_ctx pp_ctx;

@@ -86,7 +86,8 @@ class Stats(C.Structure):
                 ("slices_costed", C.c_int64), ("waves", C.c_int64), ("ms_sort", C.c_double),
                 ("ms_cost", C.c_double), ("ms_dp", C.c_double), ("ms_total", C.c_double),
                 ("ms_kernel", C.c_double * 4), ("launches", C.c_int64 * 4),
-                ("dp_band_bytes", C.c_int64)]
+                ("dp_band_bytes", C.c_int64), ("slices_pass_a", C.c_int64),
+                ("exit_thresh", C.c_double)]
 
     def as_dict(self):
         out = {}

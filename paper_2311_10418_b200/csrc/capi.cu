@@ -57,7 +57,7 @@ cudaError_t launch_cost_pass(int pass, const GridDev& g, const double* tabT, con
                              int total_blocks, int max_n, const int* mb_seg, const double* mb_t,
                              double cap, double interval, int* row_w, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
-                             cudaStream_t st);
+                             double exit_thresh, unsigned int* small_bm, cudaStream_t st);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
                              int* row_w, int* blk_W, cudaStream_t st);
 cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -70,8 +70,8 @@ cudaError_t launch_tile_offsets(const int* blk_W, const int* blk_base, int n_seg
                                 SegStats* stats, cudaStream_t st);
 cudaError_t launch_cand_bitmap(const unsigned int* bitmap, const int64_t* bitmap_off,
                                const SegStats* stats, const int* seg_mode, int n_seg,
-                               double interval, const int64_t* cand_off, double* cand, int* cand_n,
-                               cudaStream_t st);
+                               const unsigned int* small_bm, double interval,
+                               const int64_t* cand_off, double* cand, int* cand_n, cudaStream_t st);
 cudaError_t launch_cand_unique(const unsigned long long* keys_a, const unsigned long long* keys_b,
                                const int* in_b, const int64_t* raw_off,
                                const unsigned long long* raw_cnt, const int* seg_mode, int n_seg,
@@ -171,6 +171,13 @@ struct pp_ctx {
       bound_items, bound_res;
   DevBuf out_splits, out_times, out_count, out_tmax, out_obj, out_status, out_err;
   PinBuf h_range, h_stats, h_segdp;
+  DevBuf small_bm;
+  // host copy of the uploaded grid (restricted to the recompute strategy)
+  // for the monotonicity certificate of cost pass A
+  std::vector<double> h_ax, h_cells;
+  std::vector<Layout> h_lay;
+  int h_nm = 0, h_ns = 0, h_encdec = 0;
+  double exit_thresh = INFINITY;  // last call's pass-A row-exit threshold
   // per-launch event pairs for kernel timing (pp_stats::ms_kernel)
   std::vector<cudaEvent_t> kev;
   std::vector<int> kcat;
@@ -182,7 +189,8 @@ struct pp_ctx {
             &stats_d, &band_base, &band, &bitmap, &bitmap_off, &seg_mode, &raw, &raw_tmp, &raw_off,
             &raw_cnt, &raw_in_tmp, &cand, &cand_off, &cand_n, &active, &items, &results, &next_buf,
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
-            &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err};
+            &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
+            &small_bm};
   }
 };
 
@@ -292,6 +300,12 @@ int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, Grid
   if (!lay.empty())
     PP_CUDA(cudaMemcpyAsync(ctx->layouts.p, lay.data(), lay.size() * sizeof(Layout),
                             cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h_ax = ax;
+  ctx->h_cells = cells;
+  ctx->h_lay = lay;
+  ctx->h_nm = nm;
+  ctx->h_ns = ns;
+  ctx->h_encdec = m->is_encoder_decoder ? 1 : 0;
   out->n_mbs = nm;
   out->n_seq = ns;
   out->n_layouts = (int)lay.size();
@@ -316,6 +330,123 @@ double dkey_inv_host(unsigned long long k) {
   double d;
   std::memcpy(&d, &u, 8);
   return d;
+}
+
+// ---------------------------------------------------------------------------
+// Row-exit certificate for cost pass A (act_mem only).
+//
+// Pass A needs Rm(i) = the last j with !(M[i,j] > cap).  The reference prices
+// every slice.  For slice [i, j) the padded shape is (mbs = j - i, running max
+// of the lengths), both non-decreasing in j for ANY sample order, so if the
+// exact (real-arithmetic) act_mem surface is non-decreasing in mbs and in the
+// sequence length over the ranges this call can reach, the exact M[i,j] is
+// non-decreasing in j.  The device value M~ differs from the exact M by at
+// most E (bound below), hence once M~[i,j0] > cap + 2E every j >= j0 has
+// M~[i,j] >= M[i,j] - E >= M[i,j0] - E >= M~[i,j0] - 2E > cap: the rest of the
+// row is infeasible and pass A stops scanning it.  No result changes; only
+// slices that provably fail the cap are skipped.
+//
+// Exact surface per field and kind (ProfileGrid::per_layer,
+// cost_model.cpp:126-150): on cell (mi, si) with corners c00, c10 (mbs+1),
+// c01 (seq+1), c11 the blend is bilinear in (tm, ts); tm, ts lie in [0, 1]
+// inside the axes and leave it only in the first / last segment
+// (extrapolation).  It is non-decreasing in tm iff (1-ts)(c10-c00) +
+// ts(c11-c01) >= 0 over the reachable ts, and in ts iff (1-tm)(c01-c00) +
+// tm(c11-c10) >= 0 over the reachable tm; both are linear, so the axis
+// differences (ts, tm in [0, 1]) plus the two extrapolated end points are
+// checked.  Adjacent cells agree on shared edges (continuity), max(0, .),
+// non-negative layer multiples, sums and max over stages preserve order.
+//
+// Rounding bound: every field evaluation is ~10 IEEE operations on values of
+// magnitude <= A (1 + 2|tm|)(1 + 2|ts|), A = max |cell|; a forward error
+// analysis gives |v~ - v| <= 72 u A (1 + |tm|)(1 + |ts|) per weighted field,
+// u = 2^-53; we use 128 u.  Returns +inf (no certificate: full scan) when a
+// condition fails or is within 1e-12 relative of failing.
+double mem_exit_threshold(const pp_ctx* ctx, double cap, int max_n, double seq_lo[2],
+                          double seq_hi[2]) {
+  const double INF = INFINITY;
+  if (!(cap < INF) || std::isnan(cap)) return INF;
+  const int nm = ctx->h_nm, ns = ctx->h_ns;
+  const double* mbs_ax = ctx->h_ax.data();
+  const double* seq_ax = ctx->h_ax.data() + nm;
+  auto tpos = [](const double* ax, int size, double x, int& seg) -> long double {
+    seg = 0;
+    if (size == 1) return 0.0L;
+    while (seg + 2 < size && x >= ax[seg + 1]) ++seg;
+    return ((long double)x - ax[seg]) / ((long double)ax[seg + 1] - ax[seg]);
+  };
+  int sg;
+  const long double tm_lo = tpos(mbs_ax, nm, 1.0, sg);
+  const int tm_lo_seg = sg;
+  const long double tm_hi = tpos(mbs_ax, nm, (double)std::max(max_n, 1), sg);
+  const int tm_hi_seg = sg;
+  const long double tm_abs = std::max({1.0L, std::fabs(tm_lo), std::fabs(tm_hi)});
+  bool used[2] = {false, false};
+  for (const Layout& l : ctx->h_lay) {
+    used[0] |= l.enc > 0;
+    used[1] |= l.dec > 0;
+  }
+  long double A[2] = {0.0L, 0.0L}, ts_abs[2] = {1.0L, 1.0L};
+  const size_t per = (size_t)nm * ns * 3;
+  for (int k = 0; k < 2; ++k) {
+    if (!used[k]) continue;
+    // kind k reads the input length (encoder, or decoder of a decoder-only
+    // model) or the target length (decoder of an encoder-decoder model)
+    const int fld = (k == 1 && ctx->h_encdec) ? 1 : 0;
+    const double lo = std::max(0.0, seq_lo[fld]), hi = std::max(0.0, seq_hi[fld]);
+    const long double ts_lo = tpos(seq_ax, ns, lo, sg);
+    const int ts_lo_seg = sg;
+    const long double ts_hi = tpos(seq_ax, ns, hi, sg);
+    const int ts_hi_seg = sg;
+    ts_abs[k] = std::max({1.0L, std::fabs(ts_lo), std::fabs(ts_hi)});
+    auto c = [&](int mi, int si) -> long double {
+      return ctx->h_cells[k * per + ((size_t)mi * ns + si) * 3 + 2];
+    };
+    auto nonneg = [](long double v, long double scale) { return v >= 1e-12L * scale; };
+    for (int mi = 0; mi < nm; ++mi)
+      for (int si = 0; si < ns; ++si) {
+        const long double v = c(mi, si);
+        if (!std::isfinite((double)v)) return INF;
+        A[k] = std::max(A[k], std::fabs(v));
+        if (mi + 1 < nm && !(c(mi + 1, si) >= v)) return INF;
+        if (si + 1 < ns && !(c(mi, si + 1) >= v)) return INF;
+      }
+    // extrapolated sequence positions: d/dtm >= 0 at ts_lo (first segment)
+    // and ts_hi (last segment), for every mbs segment
+    for (int mi = 0; mi + 1 < nm && ns > 1; ++mi) {
+      for (int e = 0; e < 2; ++e) {
+        const long double ts = e ? ts_hi : ts_lo;
+        if (ts >= 0.0L && ts <= 1.0L) continue;
+        const int si = e ? ts_hi_seg : ts_lo_seg;
+        const long double d0 = c(mi + 1, si) - c(mi, si), d1 = c(mi + 1, si + 1) - c(mi, si + 1);
+        if (!nonneg((1.0L - ts) * d0 + ts * d1, (std::fabs(d0) + std::fabs(d1)) * (1.0L + std::fabs(ts))))
+          return INF;
+      }
+    }
+    // extrapolated micro-batch sizes: d/dts >= 0 at tm_lo / tm_hi
+    for (int si = 0; si + 1 < ns && nm > 1; ++si) {
+      for (int e = 0; e < 2; ++e) {
+        const long double tm = e ? tm_hi : tm_lo;
+        if (tm >= 0.0L && tm <= 1.0L) continue;
+        const int mi = e ? tm_hi_seg : tm_lo_seg;
+        const long double e0 = c(mi, si + 1) - c(mi, si), e1 = c(mi + 1, si + 1) - c(mi + 1, si);
+        if (!nonneg((1.0L - tm) * e0 + tm * e1, (std::fabs(e0) + std::fabs(e1)) * (1.0L + std::fabs(tm))))
+          return INF;
+      }
+    }
+  }
+  long double worst = 0.0L;
+  for (const Layout& l : ctx->h_lay) {
+    long double w = 0.0L;
+    if (l.enc > 0) w += (long double)l.enc * A[0] * ts_abs[0];
+    if (l.dec > 0) w += (long double)l.dec * A[1] * ts_abs[1];
+    worst = std::max(worst, w);
+  }
+  const long double u = std::ldexp(1.0L, -53);
+  const long double E = 128.0L * u * (1.0L + tm_abs) * 2.0L * worst + 1e-300L;
+  double th = (double)((long double)cap + 2.0L * E);
+  th = std::nextafter(std::nextafter(th, INF), INF);
+  return std::isfinite(th) ? th : INF;
 }
 
 // Steps 1-2 (+ tile offsets): sort, block bookkeeping, cost pass A.  Leaves
@@ -369,13 +500,30 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interva
   PP_CUDA(ctx->h_stats.ensure(n_seg * sizeof(SegStats)));
   PP_CUDA(ctx->band_base.ensure(n_seg * sizeof(int64_t)));
   SegStats* hs = ctx->h_stats.as<SegStats>();
-  for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0, 0, 0};
+  for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0, 0, 0, 0ULL};
   PP_CUDA(cudaMemcpyAsync(ctx->stats_d.p, hs, n_seg * sizeof(SegStats), cudaMemcpyHostToDevice, st));
   PP_CUDA(cudaMemcpyAsync(ctx->blk_base.p, blk_base.data(), (n_seg + 1) * sizeof(int),
                           cudaMemcpyHostToDevice, st));
   const double cap = c.opts.per_mb_mem_cap;
   // Pass A (or its closed form when every slice is memory-feasible).
   const bool full_rows = !table && cap == INFINITY;
+  double exit_thresh = INFINITY;
+  if (!table && !full_rows && total > 0) {
+    const unsigned long long* hr = ctx->h_range.as<unsigned long long>();
+    double lo[2], hi[2];
+    for (int q = 0; q < 2; ++q) {
+      lo[q] = (double)(long long)(hr[q] ^ 0x8000000000000000ULL);
+      hi[q] = (double)(long long)(hr[3 + q] ^ 0x8000000000000000ULL);
+    }
+    exit_thresh = mem_exit_threshold(ctx, cap, max_n, lo, hi);
+  }
+  ctx->exit_thresh = exit_thresh;
+  unsigned int* small_bm = nullptr;
+  if (interval > 0 && total > 0) {
+    PP_CUDA(ctx->small_bm.ensure((size_t)n_seg * kSmallBmWords * sizeof(unsigned int)));
+    PP_CUDA(cudaMemsetAsync(ctx->small_bm.p, 0, (size_t)n_seg * kSmallBmWords * sizeof(unsigned int), st));
+    small_bm = ctx->small_bm.as<unsigned int>();
+  }
   if (total > 0) {
     if (full_rows)
       PP_TIMED(1, launch_full_rows(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
@@ -386,7 +534,8 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interva
                                    ctx->sb_tg_t.as<double>(), c.d_seg_off, ctx->blk_base.as<int>(), n_seg,
                                    total_blocks, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(), cap,
                                    interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
-                                   ctx->stats_d.as<SegStats>(), nullptr, nullptr, nullptr, st));
+                                   ctx->stats_d.as<SegStats>(), nullptr, nullptr, nullptr, exit_thresh,
+                                   nullptr, st));
     PP_TIMED(1, launch_tile_offsets(ctx->blk_W.as<int>(), ctx->blk_base.as<int>(), n_seg,
                                     ctx->tile_off.as<int64_t>(), ctx->stats_d.as<SegStats>(), st));
   }
@@ -412,7 +561,8 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interva
                                  total_blocks, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(), cap,
                                  interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
                                  ctx->stats_d.as<SegStats>(), ctx->tile_off.as<int64_t>(),
-                                 ctx->band_base.as<int64_t>(), ctx->band.as<double>(), st));
+                                 ctx->band_base.as<int64_t>(), ctx->band.as<double>(), INFINITY, small_bm,
+                                 st));
   PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
   PP_CUDA(cudaStreamSynchronize(st));
   return PP_OK;
@@ -481,7 +631,16 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     raw_off[s + 1] = raw_off[s];
     if (!single && active[s]) {
       bool bitmap_ok = false;
-      if (I > 0 && hs[s].kmin != ~0ULL) {
+      bool small_ok = false;
+      if (I > 0) {
+        // every finite bin in [0, 32 * kSmallBmWords): pass B marked them all
+        small_ok = hs[s].kmin == ~0ULL ||
+                   (dkey_inv_host(hs[s].kmin) >= 0.0 && dkey_inv_host(hs[s].kmax) < 32.0 * kSmallBmWords);
+      }
+      if (small_ok) {
+        mode[s] = 3;
+        ncap = 32 * kSmallBmWords + 2;
+      } else if (I > 0 && hs[s].kmin != ~0ULL) {
         const double kmn = dkey_inv_host(hs[s].kmin), kmx = dkey_inv_host(hs[s].kmax);
         if (std::fabs(kmn) < 4.0e15 && std::fabs(kmx) < 4.0e15 && kmx - kmn < (double)(1 << 26)) {
           const int64_t range = (int64_t)(kmx - kmn) + 1;
@@ -490,7 +649,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
           bitmap_ok = true;
         }
       }
-      if (bitmap_ok) {
+      if (small_ok) {
+      } else if (bitmap_ok) {
         mode[s] = 0;
       } else {
         mode[s] = 1;
@@ -502,7 +662,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   }
   for (int s = 0; s < n_seg; ++s) {
     const int64_t n = c.h_seg_off[s + 1] - c.h_seg_off[s];
-    S.slices_costed += n * (n + 1) / 2 + hs[s].band;
+    (void)n;
+    S.slices_costed += (int64_t)hs[s].priced + hs[s].band;
   }
   PP_CUDA(ctx->bitmap_off.ensure((n_seg + 1) * sizeof(int64_t)));
   PP_CUDA(ctx->bitmap.ensure(std::max<int64_t>(bm_off[n_seg], 1) * sizeof(unsigned int)));
@@ -526,8 +687,10 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   PP_CUDA(cudaMemsetAsync(ctx->raw_in_tmp.p, 0, n_seg * sizeof(int), st));
   PP_CUDA(cudaMemsetAsync(ctx->cand_n.p, 0, n_seg * sizeof(int), st));
 
-  // pass C: candidate values from the band
-  if (total > 0 && !single)
+  // pass C: candidate values from the band (segments pass B did not cover)
+  bool need_pass_c = false;
+  for (int s = 0; s < n_seg; ++s) need_pass_c |= (mode[s] == 0 || mode[s] == 1);
+  if (total > 0 && !single && need_pass_c)
     PP_TIMED(3, launch_band_cand(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
                                  ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), I,
@@ -544,9 +707,9 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(cudaStreamSynchronize(st));  // host vectors die here
   } else {
     PP_TIMED(3, launch_cand_bitmap(ctx->bitmap.as<unsigned int>(), ctx->bitmap_off.as<int64_t>(),
-                                   ctx->stats_d.as<SegStats>(), ctx->seg_mode.as<int>(), n_seg, I,
-                                   ctx->cand_off.as<int64_t>(), ctx->cand.as<double>(),
-                                   ctx->cand_n.as<int>(), st));
+                                   ctx->stats_d.as<SegStats>(), ctx->seg_mode.as<int>(), n_seg,
+                                   ctx->small_bm.as<unsigned int>(), I, ctx->cand_off.as<int64_t>(),
+                                   ctx->cand.as<double>(), ctx->cand_n.as<int>(), st));
     if (raw_off[n_seg] > 0) {
       PP_TIMED(3, launch_segmented_sort_u64(ctx->raw.as<unsigned long long>(),
                                             ctx->raw_tmp.as<unsigned long long>(),
@@ -712,6 +875,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     S.launches[ctx->kcat[k]] += 1;
   }
   S.dp_band_bytes = transitions * (int64_t)sizeof(double);
+  S.exit_thresh = ctx->exit_thresh;
+  for (int s = 0; s < n_seg; ++s) S.slices_pass_a += (int64_t)hs[s].priced;
   ctx->stats = S;
   return PP_OK;
 }

@@ -110,6 +110,13 @@ struct CostArgs {
   const int64_t* tile_off;
   const int64_t* seg_band_base;
   double* band;
+  // pass A: certified row exit (capi.cu mem_exit_threshold): once a slice's
+  // act_mem exceeds this, every longer slice of the row exceeds the cap
+  // (+inf = no certificate, scan every j like the reference).
+  double exit_thresh;
+  // pass B: 256-bit candidate bitmap per segment for k = ceil(T / I) < 256
+  // (null when I == 0)
+  unsigned int* small_bm;
 };
 
 // PASS 0 = A (act_mem, Rm, singleton check, W_b); PASS 1 = B (band + stats).
@@ -123,6 +130,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
   __shared__ int s_sx[kCostWarps][32], s_sy[kCostWarps][32];
   __shared__ double s_mt[kCostWarps][64];
   __shared__ int s_ms[kCostWarps][64];
+  __shared__ unsigned int s_bm[kCostWarps][kSmallBmWords];
   // Small grids (every realistic profile: 648 cells) are staged in shared
   // memory; oversized ones are read through L1 from global memory.
   const GridDev G = (a.stage && !kTable) ? stage_grid(a.g, sm_grid, sm_lay) : a.g;
@@ -159,9 +167,16 @@ __global__ void __launch_bounds__(32 * kCostWarps)
     int si_e = si0, si_d = si0;
     double ts_e = ts0, ts_d = ts0;
     int last_ok = i;
+    bool done = !rowv;  // pass A: row certified finished (or no row)
     double kmn = INF, kmx = -INF;
     unsigned long long nraw = 0;
     int flags = 0;
+    int last_k = -1;
+    unsigned int npriced = 0;
+    if (PASS == 1 && a.small_bm) {
+      if (lane < kSmallBmWords) s_bm[wid][lane] = 0u;
+      __syncwarp();
+    }
     const int64_t trow = kTable ? (int64_t)i * n - (int64_t)i * (i - 1) / 2 - (i + 1) : 0;
     for (int c0 = 1; c0 <= cend; c0 += 32) {
       if (!kTable) {
@@ -190,7 +205,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
       for (int q = 0; q < qend; ++q) {
         const int c = c0 + q;
         const int j = i0 + c;
-        const bool live = rowv && c >= r + 1 && (PASS == 0 || c <= r + wr);
+        const bool live = rowv && c >= r + 1 && (PASS == 0 ? !done : c <= r + wr);
         if (!live) continue;
         double T = 0.0, M = 0.0;
         bool ok = true;
@@ -231,8 +246,10 @@ __global__ void __launch_bounds__(32 * kCostWarps)
           if (PASS == 1 && ok) T = slice_time(G, qq);
         }
         if (PASS == 0) {
+          ++npriced;
           if (ok) last_ok = j;
           if (c == r + 1 && !ok) atomicMin(&a.stats[s].err_row, i);
+          if (M > a.exit_thresh) done = true;
         } else {
           tile[(size_t)c * kRB + r] = ok ? T : masked();
           if (ok && !isnan(T)) {
@@ -244,11 +261,19 @@ __global__ void __launch_bounds__(32 * kCostWarps)
             } else {
               kmn = (qv < kmn) ? qv : kmn;
               kmx = (kmx < qv) ? qv : kmx;
+              if (a.small_bm && qv >= 0.0 && qv < 32.0 * kSmallBmWords) {
+                const int k = (int)qv;
+                if (k != last_k) {  // a row's bins repeat in runs
+                  atomicOr(&s_bm[wid][k >> 5], 1u << (k & 31));
+                  last_k = k;
+                }
+              }
             }
           }
         }
       }
       if (!kTable) __syncwarp();
+      if (PASS == 0 && !__any_sync(0xffffffffu, !done)) break;  // every row certified done
     }
     if (PASS == 0) {
       const int w = rowv ? last_ok - i : 0;
@@ -256,7 +281,13 @@ __global__ void __launch_bounds__(32 * kCostWarps)
       int wmax = rowv ? r + w : 0;
 #pragma unroll
       for (int o = 16; o; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-      if (lane == 0) a.blk_W[gb] = wmax + 1;
+      unsigned long long np = npriced;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+      if (lane == 0) {
+        a.blk_W[gb] = wmax + 1;
+        atomicAdd(&a.stats[s].priced, np);
+      }
     } else {
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
@@ -276,6 +307,14 @@ __global__ void __launch_bounds__(32 * kCostWarps)
           }
         }
         if (flags) atomicOr(&a.stats[s].flags, flags);
+      }
+      if (a.small_bm) {
+        __syncwarp();
+        if (lane < kSmallBmWords) {
+          const unsigned int w = s_bm[wid][lane];
+          if (w) atomicOr(&a.small_bm[(size_t)s * kSmallBmWords + lane], w);
+        }
+        __syncwarp();
       }
     }
   }
@@ -393,20 +432,24 @@ __global__ void __launch_bounds__(1024)
 __global__ void __launch_bounds__(1024)
     cand_bitmap_kernel(const unsigned int* __restrict__ bitmap, const int64_t* __restrict__ bitmap_off,
                        const SegStats* __restrict__ stats, const int* __restrict__ seg_mode,
-                       double interval, const int64_t* __restrict__ cand_off,
-                       double* __restrict__ cand, int* __restrict__ cand_n) {
+                       const unsigned int* __restrict__ small_bm, double interval,
+                       const int64_t* __restrict__ cand_off, double* __restrict__ cand,
+                       int* __restrict__ cand_n) {
   __shared__ int warp_tot[32];
   const int s = blockIdx.x;
-  if (seg_mode[s] != 0) return;
+  const int mode = seg_mode[s];
+  if (mode != 0 && mode != 3) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t nw = bitmap_off[s + 1] - bitmap_off[s];
-  const unsigned int* bm = bitmap + bitmap_off[s];
+  // mode 0: bitmap over [kmin, kmax] filled by band_cand_kernel;
+  // mode 3: the 256-bit bitmap over [0, 256) filled by cost pass B.
+  const int64_t nw = mode == 3 ? kSmallBmWords : bitmap_off[s + 1] - bitmap_off[s];
+  const unsigned int* bm = mode == 3 ? small_bm + (size_t)s * kSmallBmWords : bitmap + bitmap_off[s];
   double* out = cand + cand_off[s];
   const SegStats st = stats[s];
   int carry = 0;
   if (st.flags & 2) carry = 1;  // -inf first
   if (threadIdx.x == 0 && (st.flags & 2)) out[0] = -__longlong_as_double(0x7ff0000000000000LL);
-  const double kmin = st.nraw && st.kmin != ~0ULL ? dkey_inv(st.kmin) : 0.0;
+  const double kmin = (mode == 0 && st.nraw && st.kmin != ~0ULL) ? dkey_inv(st.kmin) : 0.0;
   for (int64_t t0 = 0; t0 < nw; t0 += blockDim.x) {
     const int64_t k = t0 + threadIdx.x;
     const unsigned int w = k < nw ? bm[k] : 0u;
@@ -525,10 +568,10 @@ cudaError_t launch_cost_pass(int pass, const GridDev& g, const double* tabT, con
                              int total_blocks, int max_n, const int* mb_seg, const double* mb_t,
                              double cap, double interval, int* row_w, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
-                             cudaStream_t st) {
+                             double exit_thresh, unsigned int* small_bm, cudaStream_t st) {
   CostArgs a{g, 0, tabT, tabM, in_d, tgt_d, si_in, ts_in, si_tg, ts_tg, seg_off, blk_base, n_seg,
              total_blocks, max_n, mb_seg, mb_t, cap, interval, row_w, blk_W, stats, tile_off,
-             seg_band_base, band};
+             seg_band_base, band, exit_thresh, small_bm};
   a.stage = (!tabT && grid_fits(g)) ? 1 : 0;
   const size_t sm = a.stage ? grid_smem(g) : 0;
   const int blocks = std::max(1, std::min((total_blocks + kCostWarps - 1) / kCostWarps, 148 * 32));
@@ -574,10 +617,10 @@ cudaError_t launch_tile_offsets(const int* blk_W, const int* blk_base, int n_seg
 
 cudaError_t launch_cand_bitmap(const unsigned int* bitmap, const int64_t* bitmap_off,
                                const SegStats* stats, const int* seg_mode, int n_seg,
-                               double interval, const int64_t* cand_off, double* cand, int* cand_n,
-                               cudaStream_t st) {
-  cand_bitmap_kernel<<<n_seg, 1024, 0, st>>>(bitmap, bitmap_off, stats, seg_mode, interval, cand_off,
-                                             cand, cand_n);
+                               const unsigned int* small_bm, double interval,
+                               const int64_t* cand_off, double* cand, int* cand_n, cudaStream_t st) {
+  cand_bitmap_kernel<<<n_seg, 1024, 0, st>>>(bitmap, bitmap_off, stats, seg_mode, small_bm, interval,
+                                             cand_off, cand, cand_n);
   return cudaGetLastError();
 }
 

@@ -15,6 +15,9 @@ namespace ppb {
 
 constexpr int kWarp = 32;
 constexpr int kMaxLayouts = 64;  // distinct (encoder, decoder) layer layouts
+// Candidate bins k = ceil(T / I) < 32 * kSmallBmWords are marked directly by
+// cost pass B into a per-segment bitmap (segment mode 3, capi.cu).
+constexpr int kSmallBmWords = 8;
 
 // One distinct stage layout; stages with equal layouts yield equal costs and
 // max() over equal values is exact, so dedup is parity-safe
@@ -163,6 +166,7 @@ struct SegStats {
   long long band;            // band entries of the segment (sum of 32 x W_b)
   int wmax;                  // max tile width W_b of the segment
   int pad;
+  unsigned long long priced; // slices priced by cost pass A
 };
 
 // ---- TMA bulk copies + mbarriers (sm_90+ PTX, used on sm_100a) ----------

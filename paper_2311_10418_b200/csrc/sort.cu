@@ -300,16 +300,19 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
                                   unsigned long long* h_range, unsigned long long* d_keys,
                                   uint32_t* d_vals, pp_sample* d_out, double* d_in_len,
                                   double* d_tgt_len, cudaStream_t st) {
-  if (presorted) {
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    copy_soa_kernel<<<blocks, 256, 0, st>>>(d_in, total, d_out, d_in_len, d_tgt_len);
-    return cudaGetLastError();
-  }
+  // Field ranges of the call: they size the sort key and feed the host's
+  // monotonicity certificate for the cost passes (capi.cu), so they are
+  // computed for presorted calls too.
   const unsigned long long init[6] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL};
   cudaMemcpyAsync(d_range, init, sizeof(init), cudaMemcpyHostToDevice, st);
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
   field_range_kernel<<<blocks, 256, 0, st>>>(d_in, total, d_range);
   cudaMemcpyAsync(h_range, d_range, sizeof(init), cudaMemcpyDeviceToHost, st);
+  if (presorted) {
+    const int cb = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    copy_soa_kernel<<<cb, 256, 0, st>>>(d_in, total, d_out, d_in_len, d_tgt_len);
+    return cudaStreamSynchronize(st);
+  }
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
   int bits = 0;

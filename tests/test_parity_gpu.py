@@ -208,3 +208,61 @@ def test_random_vs_reference(planner):
         a = ref.plan(s, grid, model, 4, 1, math.inf, 5000.0)
         b = planner.plan(s, grid, model, 4, 1, math.inf, 5000.0)
         assert_plan_matches(b, record(a), f"ref {k}")
+
+
+def _monotone_grid(rng, nm=5, ns=6, jitter=False):
+    """Random grid whose cells grow along both axes (cumulative sums of
+    positive steps); jitter=True breaks monotonicity of act_mem."""
+    mbs = np.cumsum(rng.integers(1, 4, nm)).astype(np.int64)
+    mbs[0] = 1
+    seq = np.cumsum(rng.integers(8, 200, ns)).astype(np.int64)
+    cells = np.zeros((2, 3, nm, ns, 3))
+    for k in range(2):
+        for r in range(3):
+            for f in range(3):
+                step = rng.random((nm, ns)) * 3.0 + 0.01
+                cells[k, r, :, :, f] = np.cumsum(np.cumsum(step, 0), 1)
+    if jitter:
+        cells[:, :, nm // 2, ns // 2, 2] *= 0.2  # a dip in act_mem
+    return capi.Grid(mbs, seq, cells)
+
+
+def test_pass_a_certificate_engaged_c3(planner):
+    """C3 (binding cap): the certified row exit prices ~the band only, and
+    the batched result still equals the reference's golden plan."""
+    case = load_golden("c3")
+    cfg = W.CONFIGS["C3"]
+    M = 3
+    r = planner.plan_batch(W.dataset(cfg, M), W.seg_offsets(cfg, M), W.grid(), W.model(cfg), cfg.stages,
+                           1, cfg.mem_cap, cfg.interval)
+    st = planner.stats()
+    assert math.isfinite(st["exit_thresh"]) and st["exit_thresh"] > cfg.mem_cap
+    assert st["exit_thresh"] - cfg.mem_cap < 1e-6 * cfg.mem_cap
+    full = M * cfg.n * (cfg.n + 1) // 2
+    assert st["slices_pass_a"] < full // 5, (st["slices_pass_a"], full)
+    m = int(r["count"][0])
+    got = capi.Plan(int(r["status"][0]), r["splits"][:m], r["mb_times"][:m], float(r["t_max_used"][0]),
+                    float(r["objective"][0]), -1, r["ordered"][:cfg.n])
+    assert_plan_matches(got, case["expect"], "C3 batched")
+
+
+@pytest.mark.parametrize("jitter", [False, True])
+def test_pass_a_certificate_random_grids(planner, orc, jitter):
+    rng = np.random.default_rng(5 + jitter)
+    for k in range(12):
+        grid = _monotone_grid(rng, jitter=jitter)
+        n = int(rng.integers(20, 400))
+        encdec = bool(k % 2)
+        s = capi.synthetic_dataset(n, int(rng.choice([300, 2000])), 70 + k, W.INPUT_DIST,
+                                   W.T5_TARGET_DIST if encdec else None)
+        model = capi.Model.uniform(int(rng.choice([2, 4])), 2, encdec)
+        o = orc.order_samples(s)
+        acts = [orc.slice_cost(grid, model, o, i, i + 1)[1] for i in range(n)]
+        cap = float(max(acts) * rng.choice([1.0, 1.7, 3.0]))
+        interval = float(rng.choice([0.0, 5.0, 50.0]))
+        a = orc.plan(s, grid, model, model.encoder_layers.size, 1, cap, interval)
+        b = _plan_or_status(lambda: planner.plan(s, grid, model, model.encoder_layers.size, 1, cap, interval))
+        st = planner.stats()
+        if jitter:
+            assert math.isinf(st["exit_thresh"]), k  # no certificate: full scan
+        assert_plan_matches(b, record(a), f"cert grid {k} jitter={jitter}")
