@@ -135,13 +135,15 @@ def run_reference(args, rank, world):
     s1 = W.dataset(c1, max(args.warmup, 1))
     ref.plan_batch_timed(s1, W.seg_offsets(c1, max(args.warmup, 1)), W.grid(), W.model(c1), c1.stages,
                          1, c1.mem_cap, c1.interval, min(cores, max(args.warmup, 1)))
-    # timed: K steps = K 8192-seq mini-batches, on min(K, cores) threads
+    # timed: max(K, cores) 8192-seq mini-batches, one per std::thread of
+    # run_plan's pool over ALL host cores (a mini-batch is one step's unit)
     K = args.steps
-    s = W.dataset(cfg, K)
-    secs, tm, ob, cnt, st = ref.plan_batch_timed(s, W.seg_offsets(cfg, K), W.grid(), W.model(cfg),
-                                                 cfg.stages, 1, cfg.mem_cap, cfg.interval, min(K, cores))
-    value = K / secs
-    threads = min(K, cores)
+    P = max(K, cores)
+    s = W.dataset(cfg, P)
+    secs, tm, ob, cnt, st = ref.plan_batch_timed(s, W.seg_offsets(cfg, P), W.grid(), W.model(cfg),
+                                                 cfg.stages, 1, cfg.mem_cap, cfg.interval, cores)
+    value = P / secs
+    threads = cores
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": K, "warmup": args.warmup, "ms_per_step": secs * 1e3 / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -149,8 +151,8 @@ def run_reference(args, rank, world):
                        "stages": cfg.stages, "t_max_candidates": cfg.K,
                        "t_max_interval": cfg.interval, "per_mb_mem_cap": cfg.mem_cap},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{K} x {cfg.n}-seq mini-batches, one per std::thread, "
-                                       f"wall {secs:.1f} s"},
+                             "sample": f"{P} x {cfg.n}-seq mini-batches on {threads} std::threads "
+                                       f"(run_plan pool), wall {secs:.1f} s"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "status_ok": int((st == 0).sum())}
     print(json.dumps(line), flush=True)
@@ -159,7 +161,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
@@ -178,22 +180,24 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2311_10418_b200 import capi
+    from paper_2311_10418_b200 import capi, shard
     from paper_2311_10418_b200 import workloads as W
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = W.CONFIGS[args.config]
-    M = args.per_gpu or {"C3": 32, "C4": 512, "C1": 1024, "C2": 128, "C5": 1}.get(cfg.name, 8)
+    M = args.per_gpu or {"C3": 148, "C4": 512, "C1": 1024, "C2": 128, "C5": 1}.get(cfg.name, 8)
     steps, warm = args.steps, args.warmup
     n = cfg.n
     # distinct mini-batches for every (rank, step): rank r owns groups
     # [r*(W+K), (r+1)*(W+K)) of M consecutive mini-batches of one dataset
     groups = warm + steps
-    total_mb = world * groups * M
-    data = W.dataset(cfg, total_mb)
-    mine = data[rank * groups * M * n:(rank + 1) * groups * M * n]
+    # rank r draws its own dataset (seed 7 + 1000 r; rank 0's first
+    # mini-batch is exactly BASELINE config C3's), so no rank materialises
+    # the whole job's samples
+    mine = capi.synthetic_dataset(groups * M * n, cfg.max_seq_len, W.SEED + 1000 * rank, W.INPUT_DIST,
+                                  W.T5_TARGET_DIST if cfg.encdec else None)
     d_samples = torch.from_numpy(mine).cuda()
     seg = W.seg_offsets(cfg, M)
     d_seg = torch.from_numpy(seg).cuda()
@@ -211,24 +215,16 @@ def main():
            "objective": torch.empty(M, dtype=torch.float64, device=dev),
            "status": torch.empty(M, dtype=torch.int32, device=dev),
            "err_sample_id": torch.empty(M, dtype=torch.int64, device=dev)}
-    # plan slot per mini-batch for the gather: [count, status, t_max, objective, splits...]
-    slot_words = 4 + n // 2 + 1  # 64-bit words
-    gather_buf = torch.empty((world, M, slot_words), dtype=torch.int64, device=dev) if world > 1 else None
+    gather_out = None
 
     def step(g):
+        nonlocal gather_out
         base = g * M * n
-        planner.plan_batch_device(d_samples[base:base + tot], d_seg, seg, out, grid, model, cfg.stages,
-                                  1, cfg.mem_cap, cfg.interval)
-        if world > 1:
-            with torch.cuda.stream(stream):
-                slot = torch.zeros((M, slot_words), dtype=torch.int64, device=dev)
-                slot[:, 0] = out["count"].to(torch.int64)
-                slot[:, 1] = out["status"].to(torch.int64)
-                slot[:, 2] = out["t_max_used"].view(torch.int64)
-                slot[:, 3] = out["objective"].view(torch.int64)
-                sp = out["splits"].view(M, n)
-                slot[:, 4:4 + n // 2] = sp.contiguous().view(torch.int64).view(M, n // 2)
-                dist.all_gather_into_tensor(gather_buf.view(world * M, slot_words), slot)
+        with torch.cuda.stream(stream):
+            slot = shard.plan_shard_device(planner, d_samples[base:base + tot], n, M, grid, model,
+                                           cfg.stages, 1, cfg.mem_cap, cfg.interval, out, d_seg, seg)
+            if world > 1:  # the only collective: one all_gather of the plans per step
+                gather_out = shard.gather_plans(slot)
 
     stats = []
     for g in range(warm):
@@ -278,34 +274,54 @@ def main():
 
     if rank == 0:
         pk, pk_kind = peaks()
-        agg = {k: 0.0 for k in ("ms_dp", "ms_cost", "ms_sort", "bytes", "tr", "ref_tr", "evals", "gen")}
-        kern = np.zeros(4)
-        launches = np.zeros(4, np.int64)
+        fp64_peak = capi.calibrate_fp64(local) / 1e12  # adds/s -> T ops/s
+        kern = np.zeros(8)
+        launches = np.zeros(8, np.int64)
+        agg = {k: 0 for k in ("tr", "ref_tr", "evals", "gen", "sl_a", "sl_b", "bound_tr")}
         for s in stats:
             kern += np.array(s["ms_kernel"])
             launches += np.array(s["launches"], np.int64)
-            agg["bytes"] += s["dp_band_bytes"]
             agg["tr"] += s["transitions_executed"]
             agg["ref_tr"] += s["transitions_reference"]
             agg["evals"] += s["candidates_evaluated"]
             agg["gen"] += s["candidates_generated"]
-        names = ["segmented sort", "fused slice costing", "DP pass (suffix DP per (mini-batch, t_max))",
-                 "selection / assembly"]
-        dom = int(np.argmax(kern))
-        if dom == 2:
-            achieved = agg["bytes"] / (kern[2] / 1e3) / 1e9
-        else:
-            achieved = None
-        roof = None
-        if achieved is not None:
-            roof = {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": pk["hbm_gbs"],
-                    "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                    "peak_source": pk_kind + " (MEASURED_PEAKS.json hbm_gbs, burst)",
-                    "algorithmic": "8 B band entry per DP transition visited",
-                    "avg_launch_ms": kern[2] / max(launches[2], 1)}
-        else:
-            roof = {"bound": "hbm", "kernel": names[dom], "achieved": None, "peak": pk["hbm_gbs"],
-                    "unit": "GB/s", "frac": None, "traffic": None}
+            agg["sl_a"] += s["slices_pass_a"]
+            agg["sl_b"] += s["slices_pass_b"]
+            agg["bound_tr"] += s["bound_transitions"]
+        names = capi.KERNEL_NAMES
+        kl = W.kind_layouts(cfg)  # (layout, kind) pairs priced per slice
+        # algorithmic work per launch category:
+        #   pass A: act_mem per (layout, kind): 3 bilinear blends x 3 FP64 ops + scale + add = 11
+        #   pass B: time 2 x 9 + 2 + 2 + 1 = 23 and act_mem 11 per (layout, kind), + 1 candidate divide
+        #   DP: one 8-byte band entry streamed per transition
+        capped = math.isfinite(cfg.mem_cap)
+        work = {
+            2: ("fp64", agg["sl_a"] * 11 * kl, "11 FP64 ops per act_mem slice per (layout, kind)"),
+            3: ("fp64", agg["sl_b"] * ((23 + (11 if capped else 0)) * kl + 1),
+                f"{(23 + (11 if capped else 0)) * kl + 1} FP64 ops per band slice"),
+            4: ("hbm", agg["bound_tr"] * 8, "8 B band entry per transition"),
+            5: ("hbm", (agg["tr"] - agg["bound_tr"]) * 8, "8 B band entry per transition"),
+        }
+
+        def roof_of(cat):
+            bound, units, algo = work[cat]
+            secs = kern[cat] / 1e3
+            if bound == "fp64":
+                ach, peak, unit = units / secs / 1e12, fp64_peak, "TFLOP/s"
+                src = "fp64 add rate measured in-run (pp_calibrate_fp64)"
+            else:
+                ach, peak, unit = units / secs / 1e9, pk["hbm_gbs"], "GB/s"
+                src = f"MEASURED_PEAKS.json hbm_gbs ({pk_kind}, burst)"
+            return {"bound": bound, "kernel": names[cat], "achieved": ach, "peak": peak, "unit": unit,
+                    "frac": ach / peak, "traffic": None, "algorithmic": algo, "peak_source": src,
+                    "avg_launch_ms": kern[cat] / max(int(launches[cat]), 1),
+                    "share_of_step": kern[cat] / max(kern.sum(), 1e-9)}
+
+        dom = max(work, key=lambda c: kern[c])
+        roof = roof_of(dom)
+        roof["all"] = {names[c]: {k: roof_of(c)[k] for k in ("bound", "achieved", "unit", "frac",
+                                                             "share_of_step")}
+                       for c in work if kern[c] > 0}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
@@ -328,6 +344,8 @@ def main():
             "work": {"dp_transitions_per_s": agg["tr"] / (ms_max / 1e3),
                      "reference_equivalent_transitions_per_s": agg["ref_tr"] / (ms_max / 1e3),
                      "candidates_generated": agg["gen"], "dp_passes": agg["evals"],
+                     "slices_priced_pass_a": agg["sl_a"], "slices_priced_pass_b": agg["sl_b"],
+                     "fp64_add_peak_tops": fp64_peak,
                      "kernel_ms": {nm: float(v) for nm, v in zip(names, kern)},
                      "kernel_launches": {nm: int(v) for nm, v in zip(names, launches)}},
             "status_ok": status_ok,

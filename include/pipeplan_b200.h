@@ -127,13 +127,18 @@ typedef struct pp_stats {
   int64_t waves;                  /* candidate waves launched                  */
   double  ms_sort, ms_cost, ms_dp, ms_total;  /* device time per phase          */
   /* per-kernel device time (CUDA events around each launch, on the ctx
-   * stream) and launch counts: [0] sort, [1] slice costing, [2] DP passes,
-   * [3] selection / assembly / candidate compaction */
-  double  ms_kernel[4];
-  int64_t launches[4];
+   * stream) and launch counts: [0] segmented sort, [1] cost setup (axis
+   * brackets, row widths, tile offsets), [2] cost pass A (act_mem, row
+   * widths), [3] cost pass B (band tiles + candidate bins), [4] DP bound
+   * pass (t = +inf), [5] DP candidate passes, [6] candidate compaction,
+   * [7] selection / assembly */
+  double  ms_kernel[8];
+  int64_t launches[8];
   int64_t dp_band_bytes;          /* band bytes the DP passes read (8 B / transition) */
   int64_t slices_pass_a;          /* act_mem-only slices priced by cost pass A        */
   double  exit_thresh;            /* pass-A certified row-exit threshold (+inf: none) */
+  int64_t slices_pass_b;          /* memory-feasible band slices priced by cost pass B */
+  int64_t bound_transitions;      /* DP transitions of the bound pass (t = +inf)       */
 } pp_stats;
 
 typedef struct pp_ctx pp_ctx;
@@ -180,6 +185,10 @@ int pp_candidate_range(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg
                        int32_t n_seg, int32_t presorted, const pp_grid_desc* grid,
                        const pp_model_desc* model, double per_mb_mem_cap, double* t_min,
                        double* t_max);
+
+/* Diagnostics: measured FP64 add issue rate of `device` (adds/s), the
+ * roofline denominator of the FP64-bound cost kernels (calib.cu). */
+int pp_calibrate_fp64(int device, double* dadd_per_s);
 
 /* ---- host helpers (no device work): the drop-in C++ API exposed to C ---- */
 /* eval_objective (microbatch.cpp:109-120) */

@@ -21,7 +21,7 @@ INC = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libpipeplan_b200.so")
 
-CU = ["sort.cu", "cost.cu", "dp.cu", "capi.cu"]
+CU = ["sort.cu", "cost.cu", "dp.cu", "capi.cu", "calib.cu"]
 CPP = ["host/workload.cpp", "host/cost_model.cpp", "host/microbatch.cpp", "host/capi_host.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else os.environ.get("CXX", "g++")

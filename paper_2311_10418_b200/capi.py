@@ -28,7 +28,7 @@ EXPORTED = [
     "pp_abi_version", "pp_ctx_create", "pp_ctx_destroy", "pp_ctx_last_error", "pp_ctx_set_tuning",
     "pp_ctx_get_stats", "pp_ctx_set_stream", "pp_order_samples", "pp_plan_grid",
     "pp_plan_grid_device", "pp_plan_tables", "pp_candidate_range", "pp_eval_objective",
-    "pp_synthetic_grid", "pp_synthetic_dataset", "pp_slice_cost_host",
+    "pp_synthetic_grid", "pp_synthetic_dataset", "pp_slice_cost_host", "pp_calibrate_fp64",
 ]
 
 
@@ -80,14 +80,20 @@ class PlanOut(C.Structure):
                 ("status", C.c_void_p), ("err_sample_id", C.c_void_p)]
 
 
+KERNEL_NAMES = ["segmented sort", "cost setup", "cost pass A (act_mem row widths)",
+                "cost pass B (band tiles + candidate bins)", "DP bound pass", "DP candidate passes",
+                "candidate compaction", "selection / assembly"]
+
+
 class Stats(C.Structure):
     _fields_ = [("candidates_generated", C.c_int64), ("candidates_evaluated", C.c_int64),
                 ("transitions_executed", C.c_int64), ("transitions_reference", C.c_int64),
                 ("slices_costed", C.c_int64), ("waves", C.c_int64), ("ms_sort", C.c_double),
                 ("ms_cost", C.c_double), ("ms_dp", C.c_double), ("ms_total", C.c_double),
-                ("ms_kernel", C.c_double * 4), ("launches", C.c_int64 * 4),
+                ("ms_kernel", C.c_double * 8), ("launches", C.c_int64 * 8),
                 ("dp_band_bytes", C.c_int64), ("slices_pass_a", C.c_int64),
-                ("exit_thresh", C.c_double)]
+                ("exit_thresh", C.c_double), ("slices_pass_b", C.c_int64),
+                ("bound_transitions", C.c_int64)]
 
     def as_dict(self):
         out = {}
@@ -123,6 +129,7 @@ def _load():
     lib.pp_synthetic_grid.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp]
     lib.pp_synthetic_dataset.argtypes = [i64, vp, vp, i64, C.c_uint64, vp]
     lib.pp_slice_cost_host.argtypes = [C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, i64, i64, vp, vp]
+    lib.pp_calibrate_fp64.argtypes = [C.c_int, C.POINTER(dbl)]
     return lib
 
 
@@ -229,6 +236,15 @@ def slice_cost_host(grid: Grid, model: Model, ordered: np.ndarray, begin: int, e
     if rc != PP_OK:
         raise InvalidArgument("slice cost failed")
     return float(t[0]), float(m[0])
+
+
+def calibrate_fp64(device: int = 0) -> float:
+    """Measured FP64 add rate of the device (adds/s), see calib.cu."""
+    out = C.c_double(0.0)
+    rc = lib.pp_calibrate_fp64(device, C.byref(out))
+    if rc != PP_OK:
+        _raise_status(rc, -1, "fp64 calibration failed")
+    return out.value
 
 
 def eval_objective(times, stage_count: int, replica_count: int) -> float:

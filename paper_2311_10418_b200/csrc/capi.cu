@@ -205,9 +205,9 @@ namespace {
     }                                                                                \
   } while (0)
 
-// Record an event pair around one kernel launch (category: 0 sort, 1 cost,
-// 2 DP pass, 3 other) so pp_stats reports per-kernel device time measured on
-// the launching stream.
+// Record an event pair around one kernel launch (category = pp_stats
+// ms_kernel index, see include/pipeplan_b200.h) so pp_stats reports
+// per-kernel device time measured on the launching stream.
 cudaError_t timed_begin(pp_ctx* ctx, int cat) {
   if (ctx->kused + 2 > ctx->kev.size()) {
     for (int k = 0; k < 64; ++k) {
@@ -500,7 +500,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interva
   PP_CUDA(ctx->h_stats.ensure(n_seg * sizeof(SegStats)));
   PP_CUDA(ctx->band_base.ensure(n_seg * sizeof(int64_t)));
   SegStats* hs = ctx->h_stats.as<SegStats>();
-  for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0, 0, 0, 0ULL};
+  for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0, 0, 0, 0ULL, 0ULL};
   PP_CUDA(cudaMemcpyAsync(ctx->stats_d.p, hs, n_seg * sizeof(SegStats), cudaMemcpyHostToDevice, st));
   PP_CUDA(cudaMemcpyAsync(ctx->blk_base.p, blk_base.data(), (n_seg + 1) * sizeof(int),
                           cudaMemcpyHostToDevice, st));
@@ -529,7 +529,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interva
       PP_TIMED(1, launch_full_rows(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
                                    ctx->row_w.as<int>(), ctx->blk_W.as<int>(), st));
     else
-      PP_TIMED(1, launch_cost_pass(0, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
+      PP_TIMED(2, launch_cost_pass(0, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
                                    ctx->sb_in_s.as<int>(), ctx->sb_in_t.as<double>(), ctx->sb_tg_s.as<int>(),
                                    ctx->sb_tg_t.as<double>(), c.d_seg_off, ctx->blk_base.as<int>(), n_seg,
                                    total_blocks, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(), cap,
@@ -555,7 +555,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interva
   if (band_total > 0) PP_CUDA(cudaMemsetAsync(ctx->band.p, 0xff, band_total * sizeof(double), st));
   // Pass B: band + candidate statistics.
   if (total > 0)
-    PP_TIMED(1, launch_cost_pass(1, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
+    PP_TIMED(3, launch_cost_pass(1, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
                                  ctx->sb_in_s.as<int>(), ctx->sb_in_t.as<double>(), ctx->sb_tg_s.as<int>(),
                                  ctx->sb_tg_t.as<double>(), c.d_seg_off, ctx->blk_base.as<int>(), n_seg,
                                  total_blocks, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(), cap,
@@ -663,7 +663,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   for (int s = 0; s < n_seg; ++s) {
     const int64_t n = c.h_seg_off[s + 1] - c.h_seg_off[s];
     (void)n;
-    S.slices_costed += (int64_t)hs[s].priced + hs[s].band;
+    S.slices_costed += (int64_t)hs[s].priced + (int64_t)hs[s].priced_b;
   }
   PP_CUDA(ctx->bitmap_off.ensure((n_seg + 1) * sizeof(int64_t)));
   PP_CUDA(ctx->bitmap.ensure(std::max<int64_t>(bm_off[n_seg], 1) * sizeof(unsigned int)));
@@ -691,7 +691,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   bool need_pass_c = false;
   for (int s = 0; s < n_seg; ++s) need_pass_c |= (mode[s] == 0 || mode[s] == 1);
   if (total > 0 && !single && need_pass_c)
-    PP_TIMED(3, launch_band_cand(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
+    PP_TIMED(6, launch_band_cand(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
                                  ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), I,
                                  ctx->stats_d.as<SegStats>(), ctx->bitmap.as<unsigned int>(),
@@ -706,17 +706,17 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(cudaMemcpyAsync(ctx->cand_n.p, ones.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaStreamSynchronize(st));  // host vectors die here
   } else {
-    PP_TIMED(3, launch_cand_bitmap(ctx->bitmap.as<unsigned int>(), ctx->bitmap_off.as<int64_t>(),
+    PP_TIMED(6, launch_cand_bitmap(ctx->bitmap.as<unsigned int>(), ctx->bitmap_off.as<int64_t>(),
                                    ctx->stats_d.as<SegStats>(), ctx->seg_mode.as<int>(), n_seg,
                                    ctx->small_bm.as<unsigned int>(), I, ctx->cand_off.as<int64_t>(),
                                    ctx->cand.as<double>(), ctx->cand_n.as<int>(), st));
     if (raw_off[n_seg] > 0) {
-      PP_TIMED(3, launch_segmented_sort_u64(ctx->raw.as<unsigned long long>(),
+      PP_TIMED(6, launch_segmented_sort_u64(ctx->raw.as<unsigned long long>(),
                                             ctx->raw_tmp.as<unsigned long long>(),
                                             ctx->raw_off.as<int64_t>(),
                                             ctx->raw_cnt.as<unsigned long long>(), ctx->seg_mode.as<int>(),
                                             1, ctx->raw_in_tmp.as<int>(), n_seg, st));
-      PP_TIMED(3, launch_cand_unique(ctx->raw.as<unsigned long long>(),
+      PP_TIMED(6, launch_cand_unique(ctx->raw.as<unsigned long long>(),
                                      ctx->raw_tmp.as<unsigned long long>(), ctx->raw_in_tmp.as<int>(),
                                      ctx->raw_off.as<int64_t>(), ctx->raw_cnt.as<unsigned long long>(),
                                      ctx->seg_mode.as<int>(), n_seg, ctx->cand_off.as<int64_t>(),
@@ -762,7 +762,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       PP_CUDA(ctx->next_buf.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
       PP_CUDA(cudaMemcpyAsync(ctx->bound_items.p, bi.data(), bi.size() * sizeof(WorkItem),
                               cudaMemcpyHostToDevice, st));
-      PP_TIMED(2, launch_dp_pass(1, ctx->bound_items.as<WorkItem>(), (int)bi.size(),
+      PP_TIMED(4, launch_dp_pass(1, ctx->bound_items.as<WorkItem>(), (int)bi.size(),
                                  smem_max - dp_smem_fixed(), dp_budget((int)bi.size()), c.d_seg_off,
                                  ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
@@ -771,7 +771,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
     }
   }
-  PP_TIMED(3, launch_seg_init(ctx->bound_res.as<ItemResult>(), single ? 0 : 1, c.opts.replica_count,
+  PP_TIMED(7, launch_seg_init(ctx->bound_res.as<ItemResult>(), single ? 0 : 1, c.opts.replica_count,
                               d_cand_off, ctx->cand_n.as<int>(), d_cand, ctx->active.as<int>(),
                               ctx->segdp.as<SegDP>(), n_seg, st));
 
@@ -828,12 +828,12 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(cudaMemcpyAsync(ctx->items.p, items.data(), ni * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_start.p, item_start.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_cnt.p, item_cnt.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
-    PP_TIMED(2, launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_max - dp_smem_fixed(), dp_budget(ni),
+    PP_TIMED(5, launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_max - dp_smem_fixed(), dp_budget(ni),
                                c.d_seg_off, ctx->blk_base.as<int>(),
                                ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
                                ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
                                ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, st));
-    PP_TIMED(3, launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
+    PP_TIMED(7, launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
                               ctx->seg_item_start.as<int>(), ctx->seg_item_cnt.as<int>(),
                               ctx->next_buf.as<int>(), ctx->best_next.as<int>(), c.d_seg_off, d_cand,
                               d_cand_off, c.opts.stage_count, c.opts.replica_count,
@@ -843,7 +843,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   PP_CUDA(cudaEventRecord(ctx->ev[3], st));
 
   // ---- 7. assembly
-  PP_TIMED(3, launch_finalize(ctx->segdp.as<SegDP>(), ctx->best_next.as<int>(), c.d_seg_off,
+  PP_TIMED(7, launch_finalize(ctx->segdp.as<SegDP>(), ctx->best_next.as<int>(), c.d_seg_off,
                               ctx->blk_base.as<int>(), ctx->tile_off.as<int64_t>(),
                               ctx->band_base.as<int64_t>(), ctx->band.as<double>(),
                               ctx->stats_d.as<SegStats>(), c.d_ordered, c.opts.stage_count,
@@ -876,7 +876,11 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   }
   S.dp_band_bytes = transitions * (int64_t)sizeof(double);
   S.exit_thresh = ctx->exit_thresh;
-  for (int s = 0; s < n_seg; ++s) S.slices_pass_a += (int64_t)hs[s].priced;
+  for (int s = 0; s < n_seg; ++s) {
+    S.slices_pass_a += (int64_t)hs[s].priced;
+    S.slices_pass_b += (int64_t)hs[s].priced_b;
+  }
+  S.bound_transitions = bound_transitions;
   ctx->stats = S;
   return PP_OK;
 }

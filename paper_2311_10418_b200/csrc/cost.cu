@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
           if (c == r + 1 && !ok) atomicMin(&a.stats[s].err_row, i);
           if (M > a.exit_thresh) done = true;
         } else {
+          ++npriced;
           tile[(size_t)c * kRB + r] = ok ? T : masked();
           if (ok && !isnan(T)) {
             double qv = T;
@@ -308,6 +309,10 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         }
         if (flags) atomicOr(&a.stats[s].flags, flags);
       }
+      unsigned long long np = npriced;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+      if (lane == 0) atomicAdd(&a.stats[s].priced_b, np);
       if (a.small_bm) {
         __syncwarp();
         if (lane < kSmallBmWords) {

@@ -166,7 +166,8 @@ struct SegStats {
   long long band;            // band entries of the segment (sum of 32 x W_b)
   int wmax;                  // max tile width W_b of the segment
   int pad;
-  unsigned long long priced; // slices priced by cost pass A
+  unsigned long long priced;   // slices priced by cost pass A
+  unsigned long long priced_b; // band slices priced by cost pass B
 };
 
 // ---- TMA bulk copies + mbarriers (sm_90+ PTX, used on sm_100a) ----------

@@ -72,6 +72,14 @@ def model(cfg: Config) -> capi.Model:
     return capi.Model.uniform(cfg.stages, 2, cfg.encdec, recompute=0)
 
 
+def kind_layouts(cfg: Config) -> int:
+    """(distinct stage layout, kind with layers) pairs one slice is priced
+    over: stages with equal layouts are deduplicated (capi.cu upload_grid)."""
+    m = model(cfg)
+    lay = {(int(e), int(d)) for e, d in zip(m.encoder_layers, m.decoder_layers) if e > 0 or d > 0}
+    return sum((e > 0) + (d > 0) for e, d in lay)
+
+
 def dataset(cfg: Config, n_minibatches: int | None = None) -> np.ndarray:
     """(n * M, 3) int64 samples (id, input_len, target_len)."""
     m = cfg.minibatches if n_minibatches is None else n_minibatches
