@@ -145,7 +145,7 @@ def run_reference(args, rank, world):
     value = P / secs
     threads = cores
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": K, "warmup": args.warmup, "ms_per_step": secs * 1e3 / K, "higher_is_better": True,
+            "steps": K, "warmup": args.warmup, "ms_per_step": secs * 1e3 / P, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name + ": " + cfg.desc, "minibatch_seqs": cfg.n,
                        "stages": cfg.stages, "t_max_candidates": cfg.K,
