@@ -47,17 +47,17 @@ cudaError_t launch_segmented_sort_u64(unsigned long long* keys, unsigned long lo
                                       const int* seg_mode, int want_mode, int* in_tmp, int n_seg,
                                       cudaStream_t st);
 // cost.cu
-cudaError_t launch_brackets(const GridDev& g, int max_n, int* mseg, double* mt, const double* in_d,
-                            const double* tgt_d, int64_t total, int* si_in, double* ts_in, int* si_tg,
-                            double* ts_tg, cudaStream_t st);
-cudaError_t launch_cost_pass(int pass, const GridDev& g, const double* tabT, const double* tabM,
-                             const double* in_d, const double* tgt_d, const int* si_in,
-                             const double* ts_in, const int* si_tg, const double* ts_tg,
-                             const int64_t* seg_off, const int* blk_base, int n_seg,
-                             int total_blocks, int max_n, const int* mb_seg, const double* mb_t,
-                             double cap, double interval, int* row_w, int* blk_W, SegStats* stats,
+cudaError_t launch_brackets(const CostGrid& g, int max_n, AxisPos* mbp, const double* in_d,
+                            const double* tgt_d, int64_t total, AxisPos* pin, AxisPos* ptg,
+                            cudaStream_t st);
+cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, const double* tabM,
+                             const double* in_d, const double* tgt_d, const AxisPos* pin,
+                             const AxisPos* ptg, const int64_t* seg_off, const int* blk_base, int n_seg,
+                             int total_blocks, int max_n, const AxisPos* mbp, double cap,
+                             double interval, int* row_w, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
-                             double exit_thresh, unsigned int* small_bm, cudaStream_t st);
+                             double exit_thresh, unsigned int* small_bm, const double* tau,
+                             cudaStream_t st);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
                              int* row_w, int* blk_W, cudaStream_t st);
 cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -163,7 +163,7 @@ struct pp_ctx {
   cudaEvent_t ev[4]{};
   // device scratch
   DevBuf samples, seg_off, ordered, in_d, tgt_d, sort_keys, sort_vals, range;
-  DevBuf grid_ax, grid_cells, layouts, tabT, tabM, mb_seg, mb_t, sb_in_s, sb_in_t, sb_tg_s, sb_tg_t;
+  DevBuf grid_ax, grid_cells, layouts, tabT, tabM, mbp, pin, ptg, tau;
   int64_t band_total = 0;
   DevBuf row_w, blk_base, blk_W, tile_off, stats_d, band_base, band, bitmap, bitmap_off, seg_mode,
       raw, raw_tmp, raw_off, raw_cnt, raw_in_tmp, cand, cand_off, cand_n, active;
@@ -184,8 +184,7 @@ struct pp_ctx {
   size_t kused = 0;
   std::vector<DevBuf*> all_bufs() {
     return {&samples, &seg_off, &ordered, &in_d, &tgt_d, &sort_keys, &sort_vals, &range, &grid_ax,
-            &grid_cells, &layouts, &tabT, &tabM, &mb_seg, &mb_t, &sb_in_s, &sb_in_t, &sb_tg_s,
-            &sb_tg_t, &row_w, &blk_base, &blk_W, &tile_off,
+            &grid_cells, &layouts, &tabT, &tabM, &mbp, &pin, &ptg, &tau, &row_w, &blk_base, &blk_W, &tile_off,
             &stats_d, &band_base, &band, &bitmap, &bitmap_off, &seg_mode, &raw, &raw_tmp, &raw_off,
             &raw_cnt, &raw_in_tmp, &cand, &cand_off, &cand_n, &active, &items, &results, &next_buf,
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
@@ -267,7 +266,7 @@ int validate_opts(pp_ctx* ctx, const pp_dp_options& o) {
 
 // Upload the grid restricted to the recompute strategy, plus the distinct
 // stage layouts.
-int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, GridDev* out) {
+int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, CostGrid* out) {
   if (!g || !m) return fail(ctx, PP_ERR_INVALID, "grid and model descriptors are required");
   if (g->n_mbs < 1 || g->n_seq < 1) return fail(ctx, PP_ERR_INVALID, "grid axis is empty");
   if (m->n_stages < 1) return fail(ctx, PP_ERR_INVALID, "stage and layer counts must be >= 1");
@@ -281,6 +280,21 @@ int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, Grid
   for (int kind = 0; kind < 2; ++kind)
     std::memcpy(&cells[kind * per], g->cells + ((size_t)kind * 3 + m->recompute) * per,
                 per * sizeof(double));
+  // cost-kernel tables: values + mbs-direction differences (see CostGrid)
+  std::vector<double4> tt(2 * (size_t)nm * ns);
+  std::vector<double2> am(2 * (size_t)nm * ns);
+  for (int kind = 0; kind < 2; ++kind)
+    for (int mi = 0; mi < nm; ++mi)
+      for (int si = 0; si < ns; ++si) {
+        const int m1 = std::min(mi + 1, nm - 1);
+        const double* c0 = &cells[kind * per + ((size_t)mi * ns + si) * 3];
+        const double* c1 = &cells[kind * per + ((size_t)m1 * ns + si) * 3];
+        volatile double d[3];  // IEEE subtraction, exactly the reference's c10 - c00
+        for (int f = 0; f < 3; ++f) d[f] = c1[f] - c0[f];
+        const size_t o = (size_t)kind * nm * ns + (size_t)mi * ns + si;
+        tt[o] = make_double4(c0[0], c0[1], d[0], d[1]);
+        am[o] = make_double2(c0[2], d[2]);
+      }
   std::vector<Layout> lay;
   for (int s = 0; s < m->n_stages; ++s) {
     Layout l{m->encoder_layers[s] > 0 ? m->encoder_layers[s] : 0,
@@ -290,15 +304,25 @@ int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, Grid
     for (const auto& x : lay) seen |= (x.enc == l.enc && x.dec == l.dec);
     if (!seen) lay.push_back(l);
   }
+  std::vector<LayoutD> layd;
+  int used = 0;
+  for (const auto& l : lay) {
+    layd.push_back(LayoutD{(double)l.enc, (double)l.dec});
+    used |= (l.enc > 0 ? 1 : 0) | (l.dec > 0 ? 2 : 0);
+  }
   PP_CUDA(ctx->grid_ax.ensure(ax.size() * sizeof(double)));
-  PP_CUDA(ctx->grid_cells.ensure(cells.size() * sizeof(double)));
-  PP_CUDA(ctx->layouts.ensure(std::max<size_t>(lay.size(), 1) * sizeof(Layout)));
+  PP_CUDA(ctx->grid_cells.ensure(tt.size() * sizeof(double4) + am.size() * sizeof(double2)));
+  PP_CUDA(ctx->layouts.ensure(std::max<size_t>(layd.size(), 1) * sizeof(LayoutD)));
+  double4* d_tt = ctx->grid_cells.as<double4>();
+  double2* d_am = reinterpret_cast<double2*>(d_tt + tt.size());
   PP_CUDA(cudaMemcpyAsync(ctx->grid_ax.p, ax.data(), ax.size() * sizeof(double),
                           cudaMemcpyHostToDevice, ctx->stream));
-  PP_CUDA(cudaMemcpyAsync(ctx->grid_cells.p, cells.data(), cells.size() * sizeof(double),
-                          cudaMemcpyHostToDevice, ctx->stream));
-  if (!lay.empty())
-    PP_CUDA(cudaMemcpyAsync(ctx->layouts.p, lay.data(), lay.size() * sizeof(Layout),
+  PP_CUDA(cudaMemcpyAsync(d_tt, tt.data(), tt.size() * sizeof(double4), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  PP_CUDA(cudaMemcpyAsync(d_am, am.data(), am.size() * sizeof(double2), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  if (!layd.empty())
+    PP_CUDA(cudaMemcpyAsync(ctx->layouts.p, layd.data(), layd.size() * sizeof(LayoutD),
                             cudaMemcpyHostToDevice, ctx->stream));
   ctx->h_ax = ax;
   ctx->h_cells = cells;
@@ -306,17 +330,43 @@ int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, Grid
   ctx->h_nm = nm;
   ctx->h_ns = ns;
   ctx->h_encdec = m->is_encoder_decoder ? 1 : 0;
-  out->n_mbs = nm;
-  out->n_seq = ns;
-  out->n_layouts = (int)lay.size();
+  out->nm = nm;
+  out->ns = ns;
+  out->n_lay = (int)layd.size();
   out->is_encdec = m->is_encoder_decoder ? 1 : 0;
+  out->used = used;
+  out->pad = 0;
   out->mbs_ax = ctx->grid_ax.as<double>();
   out->seq_ax = ctx->grid_ax.as<double>() + nm;
-  out->cells = ctx->grid_cells.as<double>();
-  out->layouts = ctx->layouts.as<Layout>();
+  out->tt = d_tt;
+  out->am = d_am;
+  out->lay = ctx->layouts.as<LayoutD>();
   // The host staging vectors die at return: make the copies complete first.
   PP_CUDA(cudaStreamSynchronize(ctx->stream));
   return PP_OK;
+}
+
+// Candidate-bin thresholds for cost pass B: tau[k] = the largest double
+// T >= 0 with fl(T / I) <= k, k < 32 * kSmallBmWords.  Correctly rounded
+// division by I > 0 is monotone in T, so ceil(fl(T / I)) = min{k : T <=
+// tau[k]} for every T in [0, tau[last]] — the device then bins a slice time
+// with compares only (microbatch.cpp:264 quantisation, no division).  Found by
+// bisection over the ordered bit patterns of non-negative doubles, with the
+// host's IEEE division.
+void bin_thresholds(double I, std::vector<double>& tau) {
+  tau.resize(32 * kSmallBmWords);
+  for (int k = 0; k < (int)tau.size(); ++k) {
+    const double kk = (double)k;
+    uint64_t lo = 0, hi = 0x7ff0000000000000ULL;  // P(lo) true (0 / I = 0 <= k), P(+inf) false
+    while (hi - lo > 1) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      double t;
+      std::memcpy(&t, &mid, 8);
+      volatile double q = t / I;
+      if (q <= kk) lo = mid; else hi = mid;
+    }
+    std::memcpy(&tau[k], &lo, 8);
+  }
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -452,7 +502,7 @@ double mem_exit_threshold(const pp_ctx* ctx, double cap, int max_n, double seq_l
 // Steps 1-2 (+ tile offsets): sort, block bookkeeping, cost pass A.  Leaves
 // the per-segment statistics in ctx->h_stats (synchronised) and the block
 // table in host vector `blk_base`.
-int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interval,
+int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interval,
                 std::vector<int>& blk_base, int& max_n) {
   cudaStream_t st = ctx->stream;
   const int n_seg = c.n_seg;
@@ -480,16 +530,12 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interva
                                         ctx->sort_keys.as<unsigned long long>(),
                                         ctx->sort_vals.as<uint32_t>(), c.d_ordered,
                                         ctx->in_d.as<double>(), ctx->tgt_d.as<double>(), st));
-    PP_CUDA(ctx->mb_seg.ensure((size_t)(max_n + 1) * sizeof(int)));
-    PP_CUDA(ctx->mb_t.ensure((size_t)(max_n + 1) * sizeof(double)));
-    PP_CUDA(ctx->sb_in_s.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
-    PP_CUDA(ctx->sb_in_t.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
-    PP_CUDA(ctx->sb_tg_s.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
-    PP_CUDA(ctx->sb_tg_t.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
-    PP_TIMED(1, launch_brackets(g, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(),
-                                ctx->in_d.as<double>(), ctx->tgt_d.as<double>(), total,
-                                ctx->sb_in_s.as<int>(), ctx->sb_in_t.as<double>(), ctx->sb_tg_s.as<int>(),
-                                ctx->sb_tg_t.as<double>(), st));
+    PP_CUDA(ctx->mbp.ensure((size_t)(max_n + 1) * sizeof(AxisPos)));
+    PP_CUDA(ctx->pin.ensure(std::max<int64_t>(total, 1) * sizeof(AxisPos)));
+    PP_CUDA(ctx->ptg.ensure(std::max<int64_t>(total, 1) * sizeof(AxisPos)));
+    PP_TIMED(1, launch_brackets(g, max_n, ctx->mbp.as<AxisPos>(), ctx->in_d.as<double>(),
+                                ctx->tgt_d.as<double>(), total, ctx->pin.as<AxisPos>(),
+                                ctx->ptg.as<AxisPos>(), st));
   }
   PP_CUDA(cudaEventRecord(ctx->ev[1], st));
   PP_CUDA(ctx->row_w.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
@@ -524,18 +570,26 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interva
     PP_CUDA(cudaMemsetAsync(ctx->small_bm.p, 0, (size_t)n_seg * kSmallBmWords * sizeof(unsigned int), st));
     small_bm = ctx->small_bm.as<unsigned int>();
   }
+  const double* tau_d = nullptr;
+  if (interval > 0 && total > 0 && !table) {
+    std::vector<double> tau;
+    bin_thresholds(interval, tau);
+    PP_CUDA(ctx->tau.ensure(tau.size() * sizeof(double)));
+    PP_CUDA(cudaMemcpyAsync(ctx->tau.p, tau.data(), tau.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    PP_CUDA(cudaStreamSynchronize(st));  // tau dies at scope exit
+    tau_d = ctx->tau.as<double>();
+  }
   if (total > 0) {
     if (full_rows)
       PP_TIMED(1, launch_full_rows(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
                                    ctx->row_w.as<int>(), ctx->blk_W.as<int>(), st));
     else
       PP_TIMED(2, launch_cost_pass(0, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
-                                   ctx->sb_in_s.as<int>(), ctx->sb_in_t.as<double>(), ctx->sb_tg_s.as<int>(),
-                                   ctx->sb_tg_t.as<double>(), c.d_seg_off, ctx->blk_base.as<int>(), n_seg,
-                                   total_blocks, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(), cap,
-                                   interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
+                                   ctx->pin.as<AxisPos>(), ctx->ptg.as<AxisPos>(), c.d_seg_off,
+                                   ctx->blk_base.as<int>(), n_seg, total_blocks, max_n, ctx->mbp.as<AxisPos>(),
+                                   cap, interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
                                    ctx->stats_d.as<SegStats>(), nullptr, nullptr, nullptr, exit_thresh,
-                                   nullptr, st));
+                                   nullptr, nullptr, st));
     PP_TIMED(1, launch_tile_offsets(ctx->blk_W.as<int>(), ctx->blk_base.as<int>(), n_seg,
                                     ctx->tile_off.as<int64_t>(), ctx->stats_d.as<SegStats>(), st));
   }
@@ -556,13 +610,12 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const GridDev& g, double interva
   // Pass B: band + candidate statistics.
   if (total > 0)
     PP_TIMED(3, launch_cost_pass(1, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
-                                 ctx->sb_in_s.as<int>(), ctx->sb_in_t.as<double>(), ctx->sb_tg_s.as<int>(),
-                                 ctx->sb_tg_t.as<double>(), c.d_seg_off, ctx->blk_base.as<int>(), n_seg,
-                                 total_blocks, max_n, ctx->mb_seg.as<int>(), ctx->mb_t.as<double>(), cap,
-                                 interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
+                                 ctx->pin.as<AxisPos>(), ctx->ptg.as<AxisPos>(), c.d_seg_off,
+                                 ctx->blk_base.as<int>(), n_seg, total_blocks, max_n, ctx->mbp.as<AxisPos>(),
+                                 cap, interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
                                  ctx->stats_d.as<SegStats>(), ctx->tile_off.as<int64_t>(),
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), INFINITY, small_bm,
-                                 st));
+                                 tau_d, st));
   PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
   PP_CUDA(cudaStreamSynchronize(st));
   return PP_OK;
@@ -602,7 +655,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   ctx->kcat.clear();
   pp_stats S{};
 
-  GridDev g{};
+  CostGrid g{};
   if (!c.d_tabT) {
     int rc = upload_grid(ctx, c.grid, c.model, &g);
     if (rc) return rc;
@@ -1100,7 +1153,7 @@ int pp_candidate_range(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg
   if (seg_offsets[0] != 0 || seg_offsets[n_seg] <= 0) return fail(ctx, PP_ERR_INVALID, "mini-batch is empty");
   ctx->kused = 0;
   ctx->kcat.clear();
-  GridDev g{};
+  CostGrid g{};
   if ((rc = upload_grid(ctx, grid, model, &g))) return rc;
   if ((rc = stage_inputs(ctx, samples, seg_offsets, n_seg))) return rc;
   PlanCall c;

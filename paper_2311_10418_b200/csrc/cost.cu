@@ -38,70 +38,60 @@ namespace {
 
 constexpr int kCostWarps = 8;
 
-// Stage the (small) grid tables in shared memory.
-__device__ __forceinline__ GridDev stage_grid(const GridDev& g, double* sm, Layout* sl) {
-  const int nm = g.n_mbs, ns = g.n_seq, nc = 2 * nm * ns * 3;
-  for (int k = threadIdx.x; k < nm; k += blockDim.x) sm[k] = g.mbs_ax[k];
-  for (int k = threadIdx.x; k < ns; k += blockDim.x) sm[nm + k] = g.seq_ax[k];
-  for (int k = threadIdx.x; k < nc; k += blockDim.x) sm[nm + ns + k] = g.cells[k];
-  for (int k = threadIdx.x; k < g.n_layouts; k += blockDim.x) sl[k] = g.layouts[k];
-  __syncthreads();
-  GridDev s = g;
-  s.mbs_ax = sm;
-  s.seq_ax = sm + nm;
-  s.cells = sm + nm + ns;
-  s.layouts = sl;
-  return s;
+// Shared-memory image of the cost grid + candidate-bin thresholds.
+struct GridSmem {
+  size_t tt, am, lay, tau, bytes;
+};
+__host__ __device__ inline GridSmem grid_smem_layout(int nm, int ns, int n_lay, int n_tau) {
+  GridSmem g;
+  const size_t cells = 2 * (size_t)nm * ns;
+  g.tt = 0;
+  g.am = g.tt + cells * sizeof(double4);
+  g.lay = g.am + cells * sizeof(double2);
+  g.tau = g.lay + (size_t)n_lay * sizeof(LayoutD);
+  g.bytes = g.tau + (size_t)n_tau * sizeof(double);
+  return g;
 }
 
 // bracket() of the mbs axis for every micro-batch size 1..max_n.
-__global__ void mbs_bracket_kernel(GridDev g, int max_n, int* __restrict__ seg,
-                                   double* __restrict__ t) {
+__global__ void mbs_bracket_kernel(CostGrid g, int max_n, AxisPos* __restrict__ out) {
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m <= max_n; m += gridDim.x * blockDim.x) {
-    int s;
-    double w;
-    bracket(g.mbs_ax, g.n_mbs, (double)m, s, w);
-    seg[m] = s;
-    t[m] = w;
+    AxisPos p;
+    bracket(g.mbs_ax, g.nm, (double)m, p.seg, p.t);
+    p.pad = 0;
+    out[m] = p;
   }
 }
 
 // bracket() of the sequence axis at every ordered sample's input / target length.
-__global__ void seq_bracket_kernel(GridDev g, const double* __restrict__ in_d,
+__global__ void seq_bracket_kernel(CostGrid g, const double* __restrict__ in_d,
                                    const double* __restrict__ tgt_d, int64_t total,
-                                   int* __restrict__ si_in, double* __restrict__ ts_in,
-                                   int* __restrict__ si_tg, double* __restrict__ ts_tg) {
+                                   AxisPos* __restrict__ pin, AxisPos* __restrict__ ptg) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
        k += (int64_t)gridDim.x * blockDim.x) {
-    int s;
-    double w;
-    bracket(g.seq_ax, g.n_seq, in_d[k], s, w);
-    si_in[k] = s;
-    ts_in[k] = w;
-    bracket(g.seq_ax, g.n_seq, tgt_d[k], s, w);
-    si_tg[k] = s;
-    ts_tg[k] = w;
+    AxisPos p;
+    p.pad = 0;
+    bracket(g.seq_ax, g.ns, in_d[k], p.seg, p.t);
+    pin[k] = p;
+    bracket(g.seq_ax, g.ns, tgt_d[k], p.seg, p.t);
+    ptg[k] = p;
   }
 }
 
 struct CostArgs {
-  GridDev g;
-  int stage;
+  CostGrid g;
   const double* tabT;
   const double* tabM;
   const double* in_d;
   const double* tgt_d;
-  const int* si_in;
-  const double* ts_in;
-  const int* si_tg;
-  const double* ts_tg;
+  const AxisPos* pin;
+  const AxisPos* ptg;
   const int64_t* seg_off;
   const int* blk_base;
   int n_seg;
   int total_blocks;
   int max_n;
-  const int* mb_seg;
-  const double* mb_t;
+  const AxisPos* mbp;
   double cap;
   double interval;
   int* row_w;
@@ -115,33 +105,60 @@ struct CostArgs {
   // (+inf = no certificate, scan every j like the reference).
   double exit_thresh;
   // pass B: 256-bit candidate bitmap per segment for k = ceil(T / I) < 256
-  // (null when I == 0)
+  // (null when I == 0), and the bin thresholds tau[k] = the largest double T
+  // with fl(T / I) <= k, so k = ceil(fl(T / I)) = min{k : T <= tau[k]} needs
+  // no division (monotone, correctly rounded division; capi.cu bin_thresholds)
   unsigned int* small_bm;
+  const double* tau;
 };
 
-// PASS 0 = A (act_mem, Rm, singleton check, W_b); PASS 1 = B (band + stats).
-template <int PASS, bool kTable>
+// SRC: 0 = fused grid costing, grid staged in shared memory
+//      1 = fused grid costing, grid read from global memory (oversized grids)
+//      2 = host-evaluated triangular tables (generic SliceCostFn)
+// PASS 0 = A (act_mem, Rm, singleton check, W_b); PASS 1 = B (band + candidates).
+template <int PASS, int SRC>
 __global__ void __launch_bounds__(32 * kCostWarps)
     block_kernel(CostArgs a) {
-  extern __shared__ __align__(16) double sm_grid[];
-  __shared__ Layout sm_lay[kMaxLayouts];
+  extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ double s_x[kCostWarps][32], s_y[kCostWarps][32];
-  __shared__ double s_tx[kCostWarps][32], s_ty[kCostWarps][32];
-  __shared__ int s_sx[kCostWarps][32], s_sy[kCostWarps][32];
-  __shared__ double s_mt[kCostWarps][64];
-  __shared__ int s_ms[kCostWarps][64];
+  __shared__ AxisPos s_px[kCostWarps][32], s_py[kCostWarps][32];
+  __shared__ AxisPos s_mb[kCostWarps][64];
   __shared__ unsigned int s_bm[kCostWarps][kSmallBmWords];
-  // Small grids (every realistic profile: 648 cells) are staged in shared
-  // memory; oversized ones are read through L1 from global memory.
-  const GridDev G = (a.stage && !kTable) ? stage_grid(a.g, sm_grid, sm_lay) : a.g;
+  constexpr bool kGrid = SRC != 2;
+  const int nm = a.g.nm, ns = a.g.ns, n_lay = a.g.n_lay, used = a.g.used;
+  const double4* tt = a.g.tt;
+  const double2* am = a.g.am;
+  const LayoutD* lay = a.g.lay;
+  const double* tau = a.tau;
+  if (SRC == 0) {
+    const GridSmem L = grid_smem_layout(nm, ns, n_lay, a.tau ? kSmallBmWords * 32 : 0);
+    double4* stt = reinterpret_cast<double4*>(dsm + L.tt);
+    double2* sam = reinterpret_cast<double2*>(dsm + L.am);
+    LayoutD* slay = reinterpret_cast<LayoutD*>(dsm + L.lay);
+    double* stau = reinterpret_cast<double*>(dsm + L.tau);
+    const int cells = 2 * nm * ns;
+    for (int k = threadIdx.x; k < cells; k += blockDim.x) {
+      stt[k] = a.g.tt[k];
+      sam[k] = a.g.am[k];
+    }
+    for (int k = threadIdx.x; k < n_lay; k += blockDim.x) slay[k] = a.g.lay[k];
+    if (a.tau)
+      for (int k = threadIdx.x; k < kSmallBmWords * 32; k += blockDim.x) stau[k] = a.tau[k];
+    __syncthreads();
+    tt = stt;
+    am = sam;
+    lay = slay;
+    tau = a.tau ? stau : nullptr;
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int warps = gridDim.x * kCostWarps;
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   const bool need_mem = PASS == 0 || !(a.cap == INF);
+  const bool encdec = a.g.is_encdec != 0;
+  constexpr int kTau = kSmallBmWords * 32;
   // bracket of the initial padded length 0.0 (shape.input_len = 0, :143-144)
-  int si0 = 0;
-  double ts0 = 0.0;
-  if (!kTable) bracket(G.seq_ax, G.n_seq, 0.0, si0, ts0);
+  AxisPos p0{0.0, 0, 0};
+  if (kGrid) bracket(a.g.seq_ax, ns, 0.0, p0.seg, p0.t);
   for (int gb = blockIdx.x * kCostWarps + wid; gb < a.total_blocks; gb += warps) {
     const int s = seg_of(a.blk_base, a.n_seg, gb);
     const int64_t b0 = a.seg_off[s];
@@ -164,40 +181,38 @@ __global__ void __launch_bounds__(32 * kCostWarps)
     }
     // running padded maxima and their sequence brackets
     double pin = 0.0, ptg = 0.0;
-    int si_e = si0, si_d = si0;
-    double ts_e = ts0, ts_d = ts0;
+    AxisPos pe = p0, pd = p0;
     int last_ok = i;
     bool done = !rowv;  // pass A: row certified finished (or no row)
     double kmn = INF, kmx = -INF;
     unsigned long long nraw = 0;
     int flags = 0;
-    int last_k = -1;
+    int last_k = -1, kw = 0;
+    int kmn_i = INT_MAX, kmx_i = -1;  // bins found through the thresholds
     unsigned int npriced = 0;
     if (PASS == 1 && a.small_bm) {
       if (lane < kSmallBmWords) s_bm[wid][lane] = 0u;
       __syncwarp();
     }
-    const int64_t trow = kTable ? (int64_t)i * n - (int64_t)i * (i - 1) / 2 - (i + 1) : 0;
+    const int64_t trow = SRC == 2 ? (int64_t)i * n - (int64_t)i * (i - 1) / 2 - (i + 1) : 0;
     for (int c0 = 1; c0 <= cend; c0 += 32) {
-      if (!kTable) {
+      if (kGrid) {
         // stage the chunk: column c0 + q reads sample index i0 + c0 + q - 1
         const int cq = c0 + lane;
         if (cq <= cend) {
           const int64_t k = b0 + i0 + cq - 1;
           s_x[wid][lane] = a.in_d[k];
-          s_y[wid][lane] = a.tgt_d[k];
-          s_sx[wid][lane] = a.si_in[k];
-          s_tx[wid][lane] = a.ts_in[k];
-          s_sy[wid][lane] = a.si_tg[k];
-          s_ty[wid][lane] = a.ts_tg[k];
+          s_px[wid][lane] = a.pin[k];
+          if (encdec) {
+            s_y[wid][lane] = a.tgt_d[k];
+            s_py[wid][lane] = a.ptg[k];
+          }
         }
         // micro-batch sizes m = c - r in [c0 - 31, c0 + 31] -> slot m - (c0 - 32)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int p = lane + 32 * h;
-          const int m = min(max(c0 - 32 + p, 1), a.max_n);
-          s_ms[wid][p] = a.mb_seg[m];
-          s_mt[wid][p] = a.mb_t[m];
+          s_mb[wid][p] = a.mbp[min(max(c0 - 32 + p, 1), a.max_n)];
         }
         __syncwarp();
       }
@@ -209,7 +224,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         if (!live) continue;
         double T = 0.0, M = 0.0;
         bool ok = true;
-        if (kTable) {
+        if (SRC == 2) {
           T = a.tabT[trow + j];
           M = a.tabM[trow + j];
           ok = !(M > a.cap);
@@ -217,52 +232,65 @@ __global__ void __launch_bounds__(32 * kCostWarps)
           const double x = s_x[wid][q];
           if (pin < x) {
             pin = x;
-            si_e = s_sx[wid][q];
-            ts_e = s_tx[wid][q];
+            pe = s_px[wid][q];
           }
-          const double y = s_y[wid][q];
-          if (ptg < y) {
-            ptg = y;
-            si_d = s_sy[wid][q];
-            ts_d = s_ty[wid][q];
+          if (encdec) {
+            const double y = s_y[wid][q];
+            if (ptg < y) {
+              ptg = y;
+              pd = s_py[wid][q];
+            }
           }
-          Query qq;
-          const int p = q - r + 32;
-          qq.mi = s_ms[wid][p];
-          qq.tm = s_mt[wid][p];
-          qq.si_enc = si_e;
-          qq.ts_enc = ts_e;
-          if (G.is_encdec) {
-            qq.si_dec = si_d;
-            qq.ts_dec = ts_d;
-          } else {
-            qq.si_dec = si_e;
-            qq.ts_dec = ts_e;
-          }
-          if (need_mem) {
-            M = slice_mem(G, qq);
+          const AxisPos mb = s_mb[wid][q - r + 32];
+          const AxisPos& pdd = encdec ? pd : pe;  // decoder reads the target length (:301-302)
+          if (PASS == 0) {
+            slice_cost<false, true>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t, pdd.seg,
+                                    pdd.t, T, M);
             ok = !(M > a.cap);
+          } else if (need_mem) {
+            slice_cost<true, true>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t, pdd.seg,
+                                   pdd.t, T, M);
+            ok = !(M > a.cap);
+          } else {
+            slice_cost<true, false>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t, pdd.seg,
+                                    pdd.t, T, M);
           }
-          if (PASS == 1 && ok) T = slice_time(G, qq);
         }
+        ++npriced;
         if (PASS == 0) {
-          ++npriced;
           if (ok) last_ok = j;
           if (c == r + 1 && !ok) atomicMin(&a.stats[s].err_row, i);
           if (M > a.exit_thresh) done = true;
         } else {
-          ++npriced;
           tile[(size_t)c * kRB + r] = ok ? T : masked();
           if (ok && !isnan(T)) {
-            double qv = T;
-            if (a.interval > 0) qv = ceil(__ddiv_rn(T, a.interval));
             ++nraw;
-            if (isinf(qv)) {
+            bool binned = false;
+            if (kGrid && tau && T >= 0.0) {
+              // k = min{k : T <= tau[k]}, walked from the lane's previous bin
+              int k = kw;
+              while (k < kTau && !(T <= tau[k])) ++k;
+              while (k > 0 && T <= tau[k - 1]) --k;
+              kw = min(k, kTau - 1);
+              if (k < kTau) {
+                binned = true;
+                kmn_i = min(kmn_i, k);
+                kmx_i = max(kmx_i, k);
+                if (k != last_k) {  // a row's bins repeat in runs
+                  atomicOr(&s_bm[wid][k >> 5], 1u << (k & 31));
+                  last_k = k;
+                }
+              }
+            }
+            double qv = T;
+            if (!binned && a.interval > 0) qv = ceil(__ddiv_rn(T, a.interval));
+            if (binned) {
+            } else if (isinf(qv)) {
               flags |= (qv > 0) ? 1 : 2;
             } else {
               kmn = (qv < kmn) ? qv : kmn;
               kmx = (kmx < qv) ? qv : kmx;
-              if (a.small_bm && qv >= 0.0 && qv < 32.0 * kSmallBmWords) {
+              if (a.small_bm && qv >= 0.0 && qv < (double)kTau) {
                 const int k = (int)qv;
                 if (k != last_k) {  // a row's bins repeat in runs
                   atomicOr(&s_bm[wid][k >> 5], 1u << (k & 31));
@@ -273,23 +301,27 @@ __global__ void __launch_bounds__(32 * kCostWarps)
           }
         }
       }
-      if (!kTable) __syncwarp();
+      if (kGrid) __syncwarp();
       if (PASS == 0 && !__any_sync(0xffffffffu, !done)) break;  // every row certified done
     }
+    unsigned long long np = npriced;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
     if (PASS == 0) {
       const int w = rowv ? last_ok - i : 0;
       if (rowv) a.row_w[b0 + i] = w;
       int wmax = rowv ? r + w : 0;
 #pragma unroll
       for (int o = 16; o; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-      unsigned long long np = npriced;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
       if (lane == 0) {
         a.blk_W[gb] = wmax + 1;
         atomicAdd(&a.stats[s].priced, np);
       }
     } else {
+      if (kmx_i >= 0) {
+        kmn = ((double)kmn_i < kmn) ? (double)kmn_i : kmn;
+        kmx = (kmx < (double)kmx_i) ? (double)kmx_i : kmx;
+      }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         const double x = __shfl_xor_sync(0xffffffffu, kmn, o);
@@ -300,6 +332,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         flags |= __shfl_xor_sync(0xffffffffu, flags, o);
       }
       if (lane == 0) {
+        atomicAdd(&a.stats[s].priced_b, np);
         if (nraw) {
           atomicAdd(&a.stats[s].nraw, nraw);
           if (!isinf(kmn)) {
@@ -309,10 +342,6 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         }
         if (flags) atomicOr(&a.stats[s].flags, flags);
       }
-      unsigned long long np = npriced;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
-      if (lane == 0) atomicAdd(&a.stats[s].priced_b, np);
       if (a.small_bm) {
         __syncwarp();
         if (lane < kSmallBmWords) {
@@ -546,49 +575,44 @@ __global__ void __launch_bounds__(1024)
   if (threadIdx.x == 0) cand_n[s] = carry;
 }
 
-size_t grid_smem(const GridDev& g) {
-  return sizeof(double) * ((size_t)g.n_mbs + g.n_seq + 2 * (size_t)g.n_mbs * g.n_seq * 3);
-}
-bool grid_fits(const GridDev& g) { return grid_smem(g) <= 160 * 1024 && g.n_layouts <= kMaxLayouts; }
-
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
-cudaError_t launch_brackets(const GridDev& g, int max_n, int* mseg, double* mt, const double* in_d,
-                            const double* tgt_d, int64_t total, int* si_in, double* ts_in, int* si_tg,
-                            double* ts_tg, cudaStream_t st) {
-  mbs_bracket_kernel<<<(max_n + 256) / 256, 256, 0, st>>>(g, max_n, mseg, mt);
+cudaError_t launch_brackets(const CostGrid& g, int max_n, AxisPos* mbp, const double* in_d,
+                            const double* tgt_d, int64_t total, AxisPos* pin, AxisPos* ptg,
+                            cudaStream_t st) {
+  mbs_bracket_kernel<<<(max_n + 256) / 256, 256, 0, st>>>(g, max_n, mbp);
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
   if (total > 0)
-    seq_bracket_kernel<<<std::max(blocks, 1), 256, 0, st>>>(g, in_d, tgt_d, total, si_in, ts_in, si_tg,
-                                                            ts_tg);
+    seq_bracket_kernel<<<std::max(blocks, 1), 256, 0, st>>>(g, in_d, tgt_d, total, pin, ptg);
   return cudaGetLastError();
 }
 
 // pass: 0 = A, 1 = B.  tabT != null selects the table source.
-cudaError_t launch_cost_pass(int pass, const GridDev& g, const double* tabT, const double* tabM,
-                             const double* in_d, const double* tgt_d, const int* si_in,
-                             const double* ts_in, const int* si_tg, const double* ts_tg,
-                             const int64_t* seg_off, const int* blk_base, int n_seg,
-                             int total_blocks, int max_n, const int* mb_seg, const double* mb_t,
-                             double cap, double interval, int* row_w, int* blk_W, SegStats* stats,
+cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, const double* tabM,
+                             const double* in_d, const double* tgt_d, const AxisPos* pin,
+                             const AxisPos* ptg, const int64_t* seg_off, const int* blk_base, int n_seg,
+                             int total_blocks, int max_n, const AxisPos* mbp, double cap,
+                             double interval, int* row_w, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
-                             double exit_thresh, unsigned int* small_bm, cudaStream_t st) {
-  CostArgs a{g, 0, tabT, tabM, in_d, tgt_d, si_in, ts_in, si_tg, ts_tg, seg_off, blk_base, n_seg,
-             total_blocks, max_n, mb_seg, mb_t, cap, interval, row_w, blk_W, stats, tile_off,
-             seg_band_base, band, exit_thresh, small_bm};
-  a.stage = (!tabT && grid_fits(g)) ? 1 : 0;
-  const size_t sm = a.stage ? grid_smem(g) : 0;
+                             double exit_thresh, unsigned int* small_bm, const double* tau,
+                             cudaStream_t st) {
+  CostArgs a{g, tabT, tabM, in_d, tgt_d, pin, ptg, seg_off, blk_base, n_seg, total_blocks, max_n, mbp,
+             cap, interval, row_w, blk_W, stats, tile_off, seg_band_base, band, exit_thresh,
+             small_bm, tau};
+  const GridSmem L = grid_smem_layout(g.nm, g.ns, g.n_lay, tau ? kSmallBmWords * 32 : 0);
+  const int src = tabT ? 2 : (L.bytes <= 160 * 1024 ? 0 : 1);
+  const size_t sm = src == 0 ? L.bytes : 0;
   const int blocks = std::max(1, std::min((total_blocks + kCostWarps - 1) / kCostWarps, 148 * 32));
-#define PP_COST_LAUNCH(P, T)                                                                        \
+#define PP_COST_LAUNCH(P, S)                                                                        \
   do {                                                                                              \
-    cudaFuncSetAttribute(block_kernel<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    block_kernel<P, T><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                     \
+    cudaFuncSetAttribute(block_kernel<P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    block_kernel<P, S><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                     \
   } while (0)
   if (pass == 0) {
-    if (tabT) PP_COST_LAUNCH(0, true); else PP_COST_LAUNCH(0, false);
+    if (src == 0) PP_COST_LAUNCH(0, 0); else if (src == 1) PP_COST_LAUNCH(0, 1); else PP_COST_LAUNCH(0, 2);
   } else {
-    if (tabT) PP_COST_LAUNCH(1, true); else PP_COST_LAUNCH(1, false);
+    if (src == 0) PP_COST_LAUNCH(1, 0); else if (src == 1) PP_COST_LAUNCH(1, 1); else PP_COST_LAUNCH(1, 2);
   }
 #undef PP_COST_LAUNCH
   return cudaGetLastError();

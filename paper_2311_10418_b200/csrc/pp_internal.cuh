@@ -19,25 +19,39 @@ constexpr int kMaxLayouts = 64;  // distinct (encoder, decoder) layer layouts
 // cost pass B into a per-segment bitmap (segment mode 3, capi.cu).
 constexpr int kSmallBmWords = 8;
 
-// One distinct stage layout; stages with equal layouts yield equal costs and
-// max() over equal values is exact, so dedup is parity-safe
-// (microbatch.cpp:150-155).
+// One distinct stage layout as FP64 layer multiples (0 = kind absent).
+// Stages with equal layouts yield equal costs and max() over equal values is
+// exact, so dedup is parity-safe (microbatch.cpp:150-155).  The multiples are
+// converted once on the host, so the slice loops issue no int->double
+// conversions (those run on the narrow XU pipe).
 struct Layout {
   int32_t enc;
   int32_t dec;
 };
+struct LayoutD {
+  double le;
+  double ld;
+};
 
-// Profile grid restricted to the recompute strategy in use
-// (ProfileGrid::per_layer, cost_model.cpp:126-150).
-struct GridDev {
-  int32_t n_mbs;
-  int32_t n_seq;
-  int32_t n_layouts;
+// Profile grid of ONE recompute strategy, prepared on the host (capi.cu
+// upload_grid) for the cost kernels.  Per kind and cell (mi, si):
+//   tt = {t_f, t_b, dt_f, dt_b},  am = {act, dact}
+// where dX(mi, si) = X(min(mi+1, nm-1), si) - X(mi, si) is the mbs-direction
+// difference the reference evaluates inside every blend
+// (cost_model.cpp:138-142: c10 - c00 and c11 - c01).  It depends on the
+// cells only, so computing it once (IEEE subtraction on the host) gives the
+// same double the reference computes per query.
+struct CostGrid {
+  int32_t nm, ns;          // axis sizes
+  int32_t n_lay;           // distinct stage layouts
   int32_t is_encdec;
-  const double* mbs_ax;  // double(axis[k]) — the reference converts at :50-51
+  int32_t used;            // bit0: encoder kind priced, bit1: decoder kind priced
+  int32_t pad;
+  const double* mbs_ax;    // double(axis[k]) — the reference converts at :50-51
   const double* seq_ax;
-  const double* cells;   // [kind 2][n_mbs][n_seq][3]
-  const Layout* layouts; // [n_layouts]
+  const double4* tt;       // [2][nm][ns]
+  const double2* am;       // [2][nm][ns]
+  const LayoutD* lay;      // [n_lay]
 };
 
 // bracket(): linear segment scan + IEEE divide (cost_model.cpp:46-53).
@@ -56,74 +70,95 @@ __device__ __forceinline__ void bracket(const double* ax, int size, double x, in
   t = __ddiv_rn(__dsub_rn(x, x0), __dsub_rn(x1, x0));
 }
 
-// blend + std::max(0.0, v) (cost_model.cpp:138-142).
-__device__ __forceinline__ double blend(double tm, double ts, double c00, double c10, double c01,
-                                        double c11) {
-  const double lo = __dadd_rn(c00, __dmul_rn(tm, __dsub_rn(c10, c00)));
-  const double hi = __dadd_rn(c01, __dmul_rn(tm, __dsub_rn(c11, c01)));
+// A pre-bracketed axis position: segment and interpolation weight.
+struct AxisPos {
+  double t;
+  int32_t seg;
+  int32_t pad;
+};
+
+// blend + std::max(0.0, v) (cost_model.cpp:138-142) with the mbs-direction
+// differences d0 = c10 - c00, d1 = c11 - c01 precomputed (see CostGrid).
+__device__ __forceinline__ double blend_d(double tm, double ts, double c00, double d0, double c01,
+                                          double d1) {
+  const double lo = __dadd_rn(c00, __dmul_rn(tm, d0));
+  const double hi = __dadd_rn(c01, __dmul_rn(tm, d1));
   const double v = __dadd_rn(lo, __dmul_rn(ts, __dsub_rn(hi, lo)));
   return (0.0 < v) ? v : 0.0;
 }
 
-// One field (0 t_f, 1 t_b, 2 act_mem) of ProfileGrid::per_layer for one kind
-// given pre-bracketed axes (cost_model.cpp:126-150).
-__device__ __forceinline__ double per_layer_field(const GridDev& g, int kind, int mi, double tm,
-                                                  int si, double ts, int f) {
-  const int m1 = min(mi + 1, g.n_mbs - 1);
-  const int s1 = min(si + 1, g.n_seq - 1);
-  const double* base = g.cells + (size_t)kind * g.n_mbs * g.n_seq * 3 + f;
-  const double c00 = base[((size_t)mi * g.n_seq + si) * 3];
-  const double c10 = base[((size_t)m1 * g.n_seq + si) * 3];
-  const double c01 = base[((size_t)mi * g.n_seq + s1) * 3];
-  const double c11 = base[((size_t)m1 * g.n_seq + s1) * 3];
-  return blend(tm, ts, c00, c10, c01, c11);
-}
-
-// Pre-bracketed query of one slice: mbs bracket (mi, tm), the encoder's
-// sequence bracket (input length) and the decoder's (target length for
-// encoder-decoder models, else the input length) — estimate(),
-// cost_model.cpp:301-317.
-struct Query {
-  int mi, si_enc, si_dec;
-  double tm, ts_enc, ts_dec;
+// ProfileGrid::per_layer (cost_model.cpp:126-150) of one kind: corners
+// (mi, si) and (mi, s1) carry the mbs-direction differences to (m1, .).
+struct KindCost {
+  double tf, tb, act;
 };
-
-// act_mem of the slice: max over distinct stage layouts of
-// 0.0 + L_enc * act(enc) + L_dec * act(dec) (microbatch.cpp:154).
-__device__ __forceinline__ double slice_mem(const GridDev& g, const Query& q) {
-  double best = 0.0;
-  for (int l = 0; l < g.n_layouts; ++l) {
-    const Layout lay = g.layouts[l];
-    double ea = 0.0;
-    if (lay.enc > 0)
-      ea = __dadd_rn(ea, __dmul_rn((double)lay.enc, per_layer_field(g, 0, q.mi, q.tm, q.si_enc, q.ts_enc, 2)));
-    if (lay.dec > 0)
-      ea = __dadd_rn(ea, __dmul_rn((double)lay.dec, per_layer_field(g, 1, q.mi, q.tm, q.si_dec, q.ts_dec, 2)));
-    best = (best < ea) ? ea : best;
+template <bool TIME, bool MEM>
+__device__ __forceinline__ KindCost kind_cost(const double4* __restrict__ tt,
+                                              const double2* __restrict__ am, int ns, int mi,
+                                              double tm, int si, double ts) {
+  const int s1 = min(si + 1, ns - 1);
+  const int i0 = mi * ns + si, i1 = mi * ns + s1;
+  KindCost v;
+  if (TIME) {
+    const double4 a = tt[i0], b = tt[i1];
+    v.tf = blend_d(tm, ts, a.x, a.z, b.x, b.z);
+    v.tb = blend_d(tm, ts, a.y, a.w, b.y, b.w);
   }
-  return best;
+  if (MEM) {
+    const double2 a = am[i0], b = am[i1];
+    v.act = blend_d(tm, ts, a.x, a.y, b.x, b.y);
+  }
+  return v;
 }
 
-// time of the slice: max over layouts of (t_f + t_b) (microbatch.cpp:153).
-__device__ __forceinline__ double slice_time(const GridDev& g, const Query& q) {
-  double best = 0.0;
-  for (int l = 0; l < g.n_layouts; ++l) {
-    const Layout lay = g.layouts[l];
-    double ef = 0.0, eb = 0.0;
-    if (lay.enc > 0) {
-      const double L = (double)lay.enc;
-      ef = __dadd_rn(ef, __dmul_rn(L, per_layer_field(g, 0, q.mi, q.tm, q.si_enc, q.ts_enc, 0)));
-      eb = __dadd_rn(eb, __dmul_rn(L, per_layer_field(g, 0, q.mi, q.tm, q.si_enc, q.ts_enc, 1)));
+// Slice cost (make_slice_cost lambda, microbatch.cpp:149-155 over estimate,
+// cost_model.cpp:301-317): per distinct stage layout
+//   est.X = 0.0 + L_enc * enc.X (+ L_dec * dec.X)
+// then time = max over stages of t_f + t_b, act_mem = max of act, both from
+// 0.0.  Every per_layer value is in [+0, +inf] (the clamp maps NaN to 0.0),
+// so 0.0 + L * x == L * x bit for bit and the leading add is skipped.
+template <bool TIME, bool MEM>
+__device__ __forceinline__ void slice_cost(const double4* __restrict__ tt,
+                                           const double2* __restrict__ am,
+                                           const LayoutD* __restrict__ lay, int n_lay, int used,
+                                           int nm, int ns, int mi, double tm, int se, double tse,
+                                           int sd, double tsd, double& T, double& M) {
+  KindCost E{0.0, 0.0, 0.0}, D{0.0, 0.0, 0.0};
+  const int per = nm * ns;
+  if (used & 1) E = kind_cost<TIME, MEM>(tt, am, ns, mi, tm, se, tse);
+  if (used & 2) D = kind_cost<TIME, MEM>(tt + per, am + per, ns, mi, tm, sd, tsd);
+  double bt = 0.0, bm = 0.0;
+  for (int l = 0; l < n_lay; ++l) {
+    const LayoutD L = lay[l];
+    if (MEM) {
+      double ea;
+      if (L.le > 0.0) {
+        ea = __dmul_rn(L.le, E.act);
+        if (L.ld > 0.0) ea = __dadd_rn(ea, __dmul_rn(L.ld, D.act));
+      } else {
+        ea = __dmul_rn(L.ld, D.act);
+      }
+      bm = (bm < ea) ? ea : bm;
     }
-    if (lay.dec > 0) {
-      const double L = (double)lay.dec;
-      ef = __dadd_rn(ef, __dmul_rn(L, per_layer_field(g, 1, q.mi, q.tm, q.si_dec, q.ts_dec, 0)));
-      eb = __dadd_rn(eb, __dmul_rn(L, per_layer_field(g, 1, q.mi, q.tm, q.si_dec, q.ts_dec, 1)));
+    if (TIME) {
+      double ef, eb;
+      if (L.le > 0.0) {
+        ef = __dmul_rn(L.le, E.tf);
+        eb = __dmul_rn(L.le, E.tb);
+        if (L.ld > 0.0) {
+          ef = __dadd_rn(ef, __dmul_rn(L.ld, D.tf));
+          eb = __dadd_rn(eb, __dmul_rn(L.ld, D.tb));
+        }
+      } else {
+        ef = __dmul_rn(L.ld, D.tf);
+        eb = __dmul_rn(L.ld, D.tb);
+      }
+      const double t = __dadd_rn(ef, eb);
+      bt = (bt < t) ? t : bt;
     }
-    const double tt = __dadd_rn(ef, eb);
-    best = (best < tt) ? tt : best;
   }
-  return best;
+  T = bt;
+  M = bm;
 }
 
 // Rows per band tile (= rows per DP block).  The band of a segment is stored
