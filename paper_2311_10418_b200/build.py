@@ -20,6 +20,12 @@ CSRC = os.path.join(PKG, "csrc")
 INC = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libpipeplan_b200.so")
+# Development variant: PP_TRACE=1 builds build/trace/libpipeplan_b200_trace.so
+# with clock64 stamps in the DP kernel (tools/dp_trace.py); never shipped.
+TRACE = os.environ.get("PP_TRACE") == "1"
+if TRACE:
+    BUILD = os.path.join(ROOT, "build", "trace")
+    LIB = os.path.join(BUILD, "libpipeplan_b200_trace.so")
 
 CU = ["sort.cu", "cost.cu", "dp.cu", "capi.cu", "calib.cu"]
 CPP = ["host/workload.cpp", "host/cost_model.cpp", "host/microbatch.cpp", "host/capi_host.cpp"]
@@ -27,7 +33,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
-           "-I" + INC] + ARCH
+           "-I" + INC] + ARCH + (["-DPP_DP_TRACE"] if TRACE else [])
 CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall", "-Wextra",
             "-I" + INC, "-I/usr/local/cuda/include"]
 

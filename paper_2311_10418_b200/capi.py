@@ -18,7 +18,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpipeplan_b200.so")
+_LIB_PATH = os.environ.get("PIPEPLAN_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libpipeplan_b200.so")
 
 PP_OK, PP_ERR_INVALID, PP_ERR_INFEASIBLE_SAMPLE, PP_ERR_INFEASIBLE = 0, 1, 2, 3
 PP_ERR_CUDA, PP_ERR_NO_DEVICE, PP_ERR_OUT_OF_RANGE = 4, 5, 6

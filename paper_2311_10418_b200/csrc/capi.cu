@@ -80,11 +80,11 @@ cudaError_t launch_cand_unique(const unsigned long long* keys_a, const unsigned 
 size_t dp_smem_fixed();
 size_t dp_state_bytes(int mode, int entries);
 cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t smem_state,
-                           size_t smem_budget,
-                           const int64_t* seg_off, const int* blk_base, const int* blk_W,
-                           const int64_t* tile_off, const int64_t* seg_band_base, const double* band,
-                           const double* cand, const int64_t* cand_off, ItemResult* res,
-                           int* next_buf, double* gstate, int res_by_seg, cudaStream_t st);
+                           int state_global, int sanitize, size_t smem_budget, const int64_t* seg_off,
+                           const int* blk_base, const int* blk_W, const int64_t* tile_off,
+                           const int64_t* seg_band_base, const double* band, const double* cand,
+                           const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
+                           int res_by_seg, cudaStream_t st);
 cudaError_t launch_seg_init(const ItemResult* bound_res, int has_bound, int replicas,
                             const int64_t* cand_off, const int* cand_n, const double* cand,
                             const int* active, SegDP* dp, int n_seg, cudaStream_t st);
@@ -641,6 +641,27 @@ void state_layout(int mode, int n, int wmax, unsigned& mask, int& entries, size_
   smem = dp_smem_fixed() + dp_state_bytes(mode, entries);
 }
 
+// A DP launch keeps every item's state in shared memory, or (when any
+// item's state does not fit) every item's state in an L2-resident global
+// ring: the kernel is specialised on the placement.
+void place_states(std::vector<WorkItem>& items, int mode, size_t& smem_state, int& state_global,
+                  int64_t& goff) {
+  smem_state = 0;
+  state_global = 0;
+  goff = 0;
+  for (const WorkItem& w : items)
+    if (dp_smem_fixed() + dp_state_bytes(mode, w.state_entries) > kDpSmemLimit) state_global = 1;
+  for (WorkItem& w : items) {
+    if (state_global) {
+      w.state_off = goff;
+      goff += 2 * (int64_t)w.state_entries;
+    } else {
+      w.state_off = -1;
+      smem_state = std::max(smem_state, dp_state_bytes(mode, w.state_entries));
+    }
+  }
+}
+
 // The planning pipeline (steps 1-7 above).
 int run_plan(pp_ctx* ctx, const PlanCall& c) {
   cudaStream_t st = ctx->stream;
@@ -661,8 +682,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     if (rc) return rc;
   }
   PP_CUDA(cudaEventRecord(ctx->ev[0], st));
-  const double cap = c.opts.per_mb_mem_cap;
   const double I = c.opts.t_max_interval;
+  const bool table = c.d_tabT != nullptr;
   std::vector<int> blk_base;
   int max_n = 0;
   {
@@ -789,7 +810,6 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   if (!single) {
     std::vector<WorkItem> bi;
     int64_t goff = 0;
-    size_t smem_max = dp_smem_fixed();
     for (int s = 0; s < n_seg; ++s) {
       if (!active[s]) continue;
       const int n = (int)(c.h_seg_off[s + 1] - c.h_seg_off[s]);
@@ -799,24 +819,20 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       w.next_off = 0;
       size_t need;
       state_layout(1, n, hs[s].wmax, w.state_mask, w.state_entries, need);
-      if (need <= kDpSmemLimit) {
-        w.state_off = -1;
-        smem_max = std::max(smem_max, need);
-      } else {
-        w.state_off = goff;
-        goff += 2 * (int64_t)w.state_entries;
-      }
       bound_transitions += hs[s].band;
       bi.push_back(w);
     }
+    size_t smem_state = 0;
+    int state_global = 0;
+    place_states(bi, 1, smem_state, state_global, goff);
     if (!bi.empty()) {
       PP_CUDA(ctx->bound_items.ensure(bi.size() * sizeof(WorkItem)));
       PP_CUDA(ctx->gstate.ensure(std::max<int64_t>(goff, 1) * sizeof(double)));
       PP_CUDA(ctx->next_buf.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
       PP_CUDA(cudaMemcpyAsync(ctx->bound_items.p, bi.data(), bi.size() * sizeof(WorkItem),
                               cudaMemcpyHostToDevice, st));
-      PP_TIMED(4, launch_dp_pass(1, ctx->bound_items.as<WorkItem>(), (int)bi.size(),
-                                 smem_max - dp_smem_fixed(), dp_budget((int)bi.size()), c.d_seg_off,
+      PP_TIMED(4, launch_dp_pass(1, ctx->bound_items.as<WorkItem>(), (int)bi.size(), smem_state,
+                                 state_global, table ? 1 : 0, dp_budget((int)bi.size()), c.d_seg_off,
                                  ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
                                  ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
@@ -840,7 +856,6 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     const SegDP* hd = ctx->h_segdp.as<SegDP>();
     items.clear();
     int64_t noff = 0, goff = 0;
-    size_t smem_max = dp_smem_fixed();
     for (int s = 0; s < n_seg; ++s) {
       item_start[s] = (int)items.size();
       item_cnt[s] = 0;
@@ -856,19 +871,15 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
         w.cand = hd[s].next_cand + q;
         w.next_off = noff;
         noff += n;
-        if (need <= kDpSmemLimit) {
-          w.state_off = -1;
-          smem_max = std::max(smem_max, need);
-        } else {
-          w.state_off = goff;
-          goff += 2 * (int64_t)w.state_entries;
-        }
         items.push_back(w);
         transitions += hs[s].band;
       }
       item_cnt[s] = k;
     }
     if (items.empty()) break;
+    size_t smem_state = 0;
+    int state_global = 0;
+    place_states(items, 0, smem_state, state_global, goff);
     ++waves;
     evaluated += (int64_t)items.size();
     const int ni = (int)items.size();
@@ -881,8 +892,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(cudaMemcpyAsync(ctx->items.p, items.data(), ni * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_start.p, item_start.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_cnt.p, item_cnt.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
-    PP_TIMED(5, launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_max - dp_smem_fixed(), dp_budget(ni),
-                               c.d_seg_off, ctx->blk_base.as<int>(),
+    PP_TIMED(5, launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_state, state_global, table ? 1 : 0,
+                               dp_budget(ni), c.d_seg_off, ctx->blk_base.as<int>(),
                                ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
                                ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
                                ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, st));
