@@ -329,18 +329,26 @@ class Planner:
             _raise_status(rc, -1, self._err())
         return out
 
+    @staticmethod
+    def plan_buffers(n_samples: int, n_seg: int, alloc=np.zeros) -> dict:
+        """Output arrays for plan_batch; pass e.g. a pinned-memory allocator
+        (bench.py) so the device->host copies run at full PCIe rate."""
+        return dict(ordered=alloc((max(n_samples, 1), 3), np.int64),
+                    splits=alloc(max(n_samples, 1), np.int32), mb_times=alloc(max(n_samples, 1), np.float64),
+                    count=alloc(n_seg, np.int32), t_max_used=alloc(n_seg, np.float64),
+                    objective=alloc(n_seg, np.float64), status=alloc(n_seg, np.int32),
+                    err_sample_id=alloc(n_seg, np.int64))
+
     def plan_batch(self, samples: np.ndarray, seg_offsets, grid: Grid, model: Model, stage_count: int,
                    replica_count: int = 1, mem_cap: float = math.inf, t_max_interval: float = 5.0,
-                   presorted: bool = False) -> dict:
-        """pp_plan_grid over independent mini-batches; returns flat arrays."""
+                   presorted: bool = False, out: dict | None = None) -> dict:
+        """pp_plan_grid over independent mini-batches; returns flat arrays
+        (written into `out` when given, see plan_buffers)."""
         samples = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
         off = np.ascontiguousarray(seg_offsets, np.int64)
         S = len(off) - 1
         n = len(samples)
-        res = dict(ordered=np.empty_like(samples), splits=np.zeros(max(n, 1), np.int32),
-                   mb_times=np.zeros(max(n, 1)), count=np.zeros(S, np.int32),
-                   t_max_used=np.zeros(S), objective=np.zeros(S), status=np.zeros(S, np.int32),
-                   err_sample_id=np.zeros(S, np.int64))
+        res = dict(out) if out is not None else self.plan_buffers(n, S)
         out = PlanOut(*(_p(res[k]) for k in ("ordered", "splits", "mb_times", "count", "t_max_used",
                                             "objective", "status", "err_sample_id")))
         g, m = grid.desc(), model.desc()

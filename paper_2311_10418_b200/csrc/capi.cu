@@ -178,6 +178,9 @@ struct pp_ctx {
   std::vector<Layout> h_lay;
   int h_nm = 0, h_ns = 0, h_encdec = 0;
   double exit_thresh = INFINITY;  // last call's pass-A row-exit threshold
+  CostGrid grid_dev{};            // device view of the uploaded grid
+  bool grid_valid = false;
+  double tau_interval = -1.0;     // interval the device bin thresholds were built for
   // per-launch event pairs for kernel timing (pp_stats::ms_kernel)
   std::vector<cudaEvent_t> kev;
   std::vector<int> kcat;
@@ -280,6 +283,26 @@ int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, Cost
   for (int kind = 0; kind < 2; ++kind)
     std::memcpy(&cells[kind * per], g->cells + ((size_t)kind * 3 + m->recompute) * per,
                 per * sizeof(double));
+  std::vector<Layout> lay0;
+  for (int s = 0; s < m->n_stages; ++s) {
+    Layout l{m->encoder_layers[s] > 0 ? m->encoder_layers[s] : 0,
+             m->decoder_layers[s] > 0 ? m->decoder_layers[s] : 0};
+    if (l.enc == 0 && l.dec == 0) continue;
+    bool seen = false;
+    for (const auto& x : lay0) seen |= (x.enc == l.enc && x.dec == l.dec);
+    if (!seen) lay0.push_back(l);
+  }
+  // Same grid, strategy and layouts as the previous call: the device tables
+  // are current (planning the same model call after call is the common case).
+  const int encdec = m->is_encoder_decoder ? 1 : 0;
+  if (ctx->grid_valid && ctx->h_nm == nm && ctx->h_ns == ns && ctx->h_encdec == encdec &&
+      ctx->h_ax == ax && ctx->h_cells == cells && ctx->h_lay.size() == lay0.size() &&
+      std::equal(lay0.begin(), lay0.end(), ctx->h_lay.begin(),
+                 [](const Layout& a, const Layout& b) { return a.enc == b.enc && a.dec == b.dec; })) {
+    *out = ctx->grid_dev;
+    return PP_OK;
+  }
+  ctx->grid_valid = false;
   // cost-kernel tables: values + mbs-direction differences (see CostGrid)
   std::vector<double4> tt(2 * (size_t)nm * ns);
   std::vector<double2> am(2 * (size_t)nm * ns);
@@ -295,15 +318,7 @@ int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, Cost
         tt[o] = make_double4(c0[0], c0[1], d[0], d[1]);
         am[o] = make_double2(c0[2], d[2]);
       }
-  std::vector<Layout> lay;
-  for (int s = 0; s < m->n_stages; ++s) {
-    Layout l{m->encoder_layers[s] > 0 ? m->encoder_layers[s] : 0,
-             m->decoder_layers[s] > 0 ? m->decoder_layers[s] : 0};
-    if (l.enc == 0 && l.dec == 0) continue;  // contributes (0, 0): max() unaffected
-    bool seen = false;
-    for (const auto& x : lay) seen |= (x.enc == l.enc && x.dec == l.dec);
-    if (!seen) lay.push_back(l);
-  }
+  const std::vector<Layout>& lay = lay0;  // stages with (0, 0) layers contribute nothing to max()
   std::vector<LayoutD> layd;
   int used = 0;
   for (const auto& l : lay) {
@@ -343,6 +358,8 @@ int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, Cost
   out->lay = ctx->layouts.as<LayoutD>();
   // The host staging vectors die at return: make the copies complete first.
   PP_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->grid_dev = *out;
+  ctx->grid_valid = true;
   return PP_OK;
 }
 
@@ -572,11 +589,14 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   }
   const double* tau_d = nullptr;
   if (interval > 0 && total > 0 && !table) {
-    std::vector<double> tau;
-    bin_thresholds(interval, tau);
-    PP_CUDA(ctx->tau.ensure(tau.size() * sizeof(double)));
-    PP_CUDA(cudaMemcpyAsync(ctx->tau.p, tau.data(), tau.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-    PP_CUDA(cudaStreamSynchronize(st));  // tau dies at scope exit
+    if (ctx->tau_interval != interval) {
+      std::vector<double> tau;
+      bin_thresholds(interval, tau);
+      PP_CUDA(ctx->tau.ensure(tau.size() * sizeof(double)));
+      PP_CUDA(cudaMemcpyAsync(ctx->tau.p, tau.data(), tau.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+      PP_CUDA(cudaStreamSynchronize(st));  // tau dies at scope exit
+      ctx->tau_interval = interval;
+    }
     tau_d = ctx->tau.as<double>();
   }
   if (total > 0) {
@@ -606,7 +626,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
   PP_CUDA(cudaMemcpyAsync(ctx->band_base.p, band_base.data(), n_seg * sizeof(int64_t),
                           cudaMemcpyHostToDevice, st));
-  if (band_total > 0) PP_CUDA(cudaMemsetAsync(ctx->band.p, 0xff, band_total * sizeof(double), st));
+  // (no fill: pass B writes every tile entry, NaN where no slice is feasible)
   // Pass B: band + candidate statistics.
   if (total > 0)
     PP_TIMED(3, launch_cost_pass(1, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),

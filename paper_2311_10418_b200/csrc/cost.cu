@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
       __syncwarp();
     }
     const int64_t trow = SRC == 2 ? (int64_t)i * n - (int64_t)i * (i - 1) / 2 - (i + 1) : 0;
+    if (PASS == 1) tile[r] = masked();  // column 0: j = i0 <= i is never a slice
     for (int c0 = 1; c0 <= cend; c0 += 32) {
       if (kGrid) {
         // stage the chunk: column c0 + q reads sample index i0 + c0 + q - 1
@@ -221,7 +222,10 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         const int c = c0 + q;
         const int j = i0 + c;
         const bool live = rowv && c >= r + 1 && (PASS == 0 ? !done : c <= r + wr);
-        if (!live) continue;
+        // pass B writes every tile entry: NaN outside the row's feasible span,
+        // so the band needs no separate fill
+        double outv = masked();
+        if (live) {
         double T = 0.0, M = 0.0;
         bool ok = true;
         if (SRC == 2) {
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
           if (c == r + 1 && !ok) atomicMin(&a.stats[s].err_row, i);
           if (M > a.exit_thresh) done = true;
         } else {
-          tile[(size_t)c * kRB + r] = ok ? T : masked();
+          outv = ok ? T : masked();
           if (ok && !isnan(T)) {
             ++nraw;
             bool binned = false;
@@ -300,6 +304,8 @@ __global__ void __launch_bounds__(32 * kCostWarps)
             }
           }
         }
+        }  // live
+        if (PASS == 1) tile[(size_t)c * kRB + r] = outv;
       }
       if (kGrid) __syncwarp();
       if (PASS == 0 && !__any_sync(0xffffffffu, !done)) break;  // every row certified done
