@@ -54,7 +54,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              const double* in_d, const double* tgt_d, const AxisPos* pin,
                              const AxisPos* ptg, const int64_t* seg_off, const int* blk_base, int n_seg,
                              int total_blocks, int max_n, const AxisPos* mbp, double cap,
-                             double interval, int* row_w, int* blk_W, SegStats* stats,
+                             double interval, int* row_w, int* row_fb, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
                              cudaStream_t st);
@@ -165,7 +165,7 @@ struct pp_ctx {
   DevBuf samples, seg_off, ordered, in_d, tgt_d, sort_keys, sort_vals, range;
   DevBuf grid_ax, grid_cells, layouts, tabT, tabM, mbp, pin, ptg, tau;
   int64_t band_total = 0;
-  DevBuf row_w, blk_base, blk_W, tile_off, stats_d, band_base, band, bitmap, bitmap_off, seg_mode,
+  DevBuf row_w, row_fb, blk_base, blk_W, tile_off, stats_d, band_base, band, bitmap, bitmap_off, seg_mode,
       raw, raw_tmp, raw_off, raw_cnt, raw_in_tmp, cand, cand_off, cand_n, active;
   DevBuf items, results, next_buf, gstate, seg_item_start, seg_item_cnt, segdp, best_next,
       bound_items, bound_res;
@@ -187,7 +187,7 @@ struct pp_ctx {
   size_t kused = 0;
   std::vector<DevBuf*> all_bufs() {
     return {&samples, &seg_off, &ordered, &in_d, &tgt_d, &sort_keys, &sort_vals, &range, &grid_ax,
-            &grid_cells, &layouts, &tabT, &tabM, &mbp, &pin, &ptg, &tau, &row_w, &blk_base, &blk_W, &tile_off,
+            &grid_cells, &layouts, &tabT, &tabM, &mbp, &pin, &ptg, &tau, &row_w, &row_fb, &blk_base, &blk_W, &tile_off,
             &stats_d, &band_base, &band, &bitmap, &bitmap_off, &seg_mode, &raw, &raw_tmp, &raw_off,
             &raw_cnt, &raw_in_tmp, &cand, &cand_off, &cand_n, &active, &items, &results, &next_buf,
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
@@ -350,7 +350,23 @@ int upload_grid(pp_ctx* ctx, const pp_grid_desc* g, const pp_model_desc* m, Cost
   out->n_lay = (int)layd.size();
   out->is_encdec = m->is_encoder_decoder ? 1 : 0;
   out->used = used;
-  out->pad = 0;
+  out->lay_class = kLayGeneric;
+  out->le = 0.0;
+  out->ld = 0.0;
+  if (lay.size() == 1 && lay[0].enc == 0 && lay[0].dec > 0) {
+    out->lay_class = kLayDec1;
+    out->ld = (double)lay[0].dec;
+  } else if (lay.size() == 2) {
+    for (int k = 0; k < 2; ++k) {
+      const Layout& e = lay[k];
+      const Layout& d = lay[1 - k];
+      if (e.enc > 0 && e.dec == 0 && d.enc == 0 && d.dec > 0) {
+        out->lay_class = kLayEncDec2;
+        out->le = (double)e.enc;
+        out->ld = (double)d.dec;
+      }
+    }
+  }
   out->mbs_ax = ctx->grid_ax.as<double>();
   out->seq_ax = ctx->grid_ax.as<double>() + nm;
   out->tt = d_tt;
@@ -556,6 +572,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   }
   PP_CUDA(cudaEventRecord(ctx->ev[1], st));
   PP_CUDA(ctx->row_w.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
+  PP_CUDA(ctx->row_fb.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
   PP_CUDA(ctx->blk_base.ensure((n_seg + 1) * sizeof(int)));
   PP_CUDA(ctx->blk_W.ensure(std::max(total_blocks, 1) * sizeof(int)));
   PP_CUDA(ctx->tile_off.ensure(std::max(total_blocks, 1) * sizeof(int64_t)));
@@ -607,7 +624,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
       PP_TIMED(2, launch_cost_pass(0, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
                                    ctx->pin.as<AxisPos>(), ctx->ptg.as<AxisPos>(), c.d_seg_off,
                                    ctx->blk_base.as<int>(), n_seg, total_blocks, max_n, ctx->mbp.as<AxisPos>(),
-                                   cap, interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
+                                   cap, interval, ctx->row_w.as<int>(), ctx->row_fb.as<int>(), ctx->blk_W.as<int>(),
                                    ctx->stats_d.as<SegStats>(), nullptr, nullptr, nullptr, exit_thresh,
                                    nullptr, nullptr, st));
     PP_TIMED(1, launch_tile_offsets(ctx->blk_W.as<int>(), ctx->blk_base.as<int>(), n_seg,
@@ -632,7 +649,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     PP_TIMED(3, launch_cost_pass(1, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
                                  ctx->pin.as<AxisPos>(), ctx->ptg.as<AxisPos>(), c.d_seg_off,
                                  ctx->blk_base.as<int>(), n_seg, total_blocks, max_n, ctx->mbp.as<AxisPos>(),
-                                 cap, interval, ctx->row_w.as<int>(), ctx->blk_W.as<int>(),
+                                 cap, interval, ctx->row_w.as<int>(), ctx->row_fb.as<int>(), ctx->blk_W.as<int>(),
                                  ctx->stats_d.as<SegStats>(), ctx->tile_off.as<int64_t>(),
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), INFINITY, small_bm,
                                  tau_d, st));

@@ -95,6 +95,7 @@ struct CostArgs {
   double cap;
   double interval;
   int* row_w;
+  int* row_fb;  // pass A -> B: first memory-infeasible j of the row (INT_MAX: none)
   int* blk_W;
   SegStats* stats;
   const int64_t* tile_off;
@@ -116,7 +117,7 @@ struct CostArgs {
 //      1 = fused grid costing, grid read from global memory (oversized grids)
 //      2 = host-evaluated triangular tables (generic SliceCostFn)
 // PASS 0 = A (act_mem, Rm, singleton check, W_b); PASS 1 = B (band + candidates).
-template <int PASS, int SRC>
+template <int PASS, int SRC, int LAY>
 __global__ void __launch_bounds__(32 * kCostWarps)
     block_kernel(CostArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -170,10 +171,11 @@ __global__ void __launch_bounds__(32 * kCostWarps)
     const int r = lane;
     const bool rowv = r < nb;
     const int i = i0 + r;
-    int wr = 0, cend;
+    int wr = 0, cend, fb = INT_MAX;
     double* tile = nullptr;
     if (PASS == 1) {
       wr = rowv ? a.row_w[b0 + i] : 0;
+      if (need_mem && SRC != 2 && rowv) fb = a.row_fb[b0 + i];
       cend = a.blk_W[gb] - 1;
       tile = a.band + a.seg_band_base[s] + a.tile_off[gb];
     } else {
@@ -188,7 +190,9 @@ __global__ void __launch_bounds__(32 * kCostWarps)
     unsigned long long nraw = 0;
     int flags = 0;
     int last_k = -1, kw = 0;
-    int kmn_i = INT_MAX, kmx_i = -1;  // bins found through the thresholds
+    // the lane's current bin kw and its bounds: T in (tlo, thi] <=> bin kw
+    double tlo = -INF, thi = (PASS == 1 && tau) ? tau[0] : -INF;
+    bool any_binned = false;
     unsigned int npriced = 0;
     if (PASS == 1 && a.small_bm) {
       if (lane < kSmallBmWords) s_bm[wid][lane] = 0u;
@@ -234,35 +238,44 @@ __global__ void __launch_bounds__(32 * kCostWarps)
           ok = !(M > a.cap);
         } else {
           const double x = s_x[wid][q];
-          if (pin < x) {
-            pin = x;
-            pe = s_px[wid][q];
-          }
+          const AxisPos px = s_px[wid][q];
+          const bool upx = pin < x;
+          pin = upx ? x : pin;
+          pe.t = upx ? px.t : pe.t;
+          pe.seg = upx ? px.seg : pe.seg;
           if (encdec) {
             const double y = s_y[wid][q];
-            if (ptg < y) {
-              ptg = y;
-              pd = s_py[wid][q];
-            }
+            const AxisPos py = s_py[wid][q];
+            const bool upy = ptg < y;
+            ptg = upy ? y : ptg;
+            pd.t = upy ? py.t : pd.t;
+            pd.seg = upy ? py.seg : pd.seg;
           }
           const AxisPos mb = s_mb[wid][q - r + 32];
-          const AxisPos& pdd = encdec ? pd : pe;  // decoder reads the target length (:301-302)
+          // the decoder reads the target length of encoder-decoder models (:301-302)
+          const int sd = encdec ? pd.seg : pe.seg;
+          const double tsd = encdec ? pd.t : pe.t;
           if (PASS == 0) {
-            slice_cost<false, true>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t, pdd.seg,
-                                    pdd.t, T, M);
-            ok = !(M > a.cap);
-          } else if (need_mem) {
-            slice_cost<true, true>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t, pdd.seg,
-                                   pdd.t, T, M);
+            slice_cost_lay<LAY, false, true>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t,
+                                             sd, tsd, a.g.le, a.g.ld, T, M);
             ok = !(M > a.cap);
           } else {
-            slice_cost<true, false>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t, pdd.seg,
-                                    pdd.t, T, M);
+            slice_cost_lay<LAY, true, false>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t,
+                                             sd, tsd, a.g.le, a.g.ld, T, M);
+            // act_mem only from the row's first infeasible slice on (pass A):
+            // every earlier slice of the row is feasible
+            if (j >= fb) {
+              double T2;
+              slice_cost_lay<LAY, false, true>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg,
+                                               pe.t, sd, tsd, a.g.le, a.g.ld, T2, M);
+              ok = !(M > a.cap);
+            }
           }
         }
         ++npriced;
         if (PASS == 0) {
           if (ok) last_ok = j;
+          fb = (!ok & (j < fb)) ? j : fb;
           if (c == r + 1 && !ok) atomicMin(&a.stats[s].err_row, i);
           if (M > a.exit_thresh) done = true;
         } else {
@@ -271,18 +284,22 @@ __global__ void __launch_bounds__(32 * kCostWarps)
             ++nraw;
             bool binned = false;
             if (kGrid && tau && T >= 0.0) {
-              // k = min{k : T <= tau[k]}, walked from the lane's previous bin
-              int k = kw;
-              while (k < kTau && !(T <= tau[k])) ++k;
-              while (k > 0 && T <= tau[k - 1]) --k;
-              kw = min(k, kTau - 1);
-              if (k < kTau) {
+              // k = min{k : T <= tau[k]}; a row's bins change rarely, so the
+              // common case is two compares against the cached bounds
+              if (!(T > tlo && T <= thi)) {
+                int k = kw;
+                while (k < kTau && !(T <= tau[k])) ++k;
+                while (k > 0 && T <= tau[k - 1]) --k;
+                kw = min(k, kTau - 1);
+                tlo = kw > 0 ? tau[kw - 1] : -INF;
+                thi = tau[kw];
+              }
+              if (T <= thi) {  // else beyond the last threshold: exact division below
                 binned = true;
-                kmn_i = min(kmn_i, k);
-                kmx_i = max(kmx_i, k);
-                if (k != last_k) {  // a row's bins repeat in runs
-                  atomicOr(&s_bm[wid][k >> 5], 1u << (k & 31));
-                  last_k = k;
+                any_binned = true;
+                if (kw != last_k) {  // a row's bins repeat in runs
+                  atomicOr(&s_bm[wid][kw >> 5], 1u << (kw & 31));
+                  last_k = kw;
                 }
               }
             }
@@ -315,7 +332,10 @@ __global__ void __launch_bounds__(32 * kCostWarps)
     for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
     if (PASS == 0) {
       const int w = rowv ? last_ok - i : 0;
-      if (rowv) a.row_w[b0 + i] = w;
+      if (rowv) {
+        a.row_w[b0 + i] = w;
+        a.row_fb[b0 + i] = fb;
+      }
       int wmax = rowv ? r + w : 0;
 #pragma unroll
       for (int o = 16; o; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
@@ -324,9 +344,9 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         atomicAdd(&a.stats[s].priced, np);
       }
     } else {
-      if (kmx_i >= 0) {
-        kmn = ((double)kmn_i < kmn) ? (double)kmn_i : kmn;
-        kmx = (kmx < (double)kmx_i) ? (double)kmx_i : kmx;
+      if (any_binned) {  // binned values lie in [0, kTau): widen the range to a superset
+        kmn = (0.0 < kmn) ? 0.0 : kmn;
+        kmx = (kmx < (double)(kTau - 1)) ? (double)(kTau - 1) : kmx;
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
@@ -599,27 +619,34 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              const double* in_d, const double* tgt_d, const AxisPos* pin,
                              const AxisPos* ptg, const int64_t* seg_off, const int* blk_base, int n_seg,
                              int total_blocks, int max_n, const AxisPos* mbp, double cap,
-                             double interval, int* row_w, int* blk_W, SegStats* stats,
+                             double interval, int* row_w, int* row_fb, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
                              cudaStream_t st) {
   CostArgs a{g, tabT, tabM, in_d, tgt_d, pin, ptg, seg_off, blk_base, n_seg, total_blocks, max_n, mbp,
-             cap, interval, row_w, blk_W, stats, tile_off, seg_band_base, band, exit_thresh,
+             cap, interval, row_w, row_fb, blk_W, stats, tile_off, seg_band_base, band, exit_thresh,
              small_bm, tau};
   const GridSmem L = grid_smem_layout(g.nm, g.ns, g.n_lay, tau ? kSmallBmWords * 32 : 0);
   const int src = tabT ? 2 : (L.bytes <= 160 * 1024 ? 0 : 1);
   const size_t sm = src == 0 ? L.bytes : 0;
   const int blocks = std::max(1, std::min((total_blocks + kCostWarps - 1) / kCostWarps, 148 * 32));
-#define PP_COST_LAUNCH(P, S)                                                                        \
-  do {                                                                                              \
-    cudaFuncSetAttribute(block_kernel<P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    block_kernel<P, S><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                     \
+#define PP_COST_LAUNCH(P, S, L)                                                                        \
+  do {                                                                                                 \
+    cudaFuncSetAttribute(block_kernel<P, S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    block_kernel<P, S, L><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                     \
+  } while (0)
+#define PP_COST_LAUNCH_L(P, S)                                                  \
+  do {                                                                           \
+    if (g.lay_class == kLayDec1) PP_COST_LAUNCH(P, S, kLayDec1);                 \
+    else if (g.lay_class == kLayEncDec2) PP_COST_LAUNCH(P, S, kLayEncDec2);      \
+    else PP_COST_LAUNCH(P, S, kLayGeneric);                                      \
   } while (0)
   if (pass == 0) {
-    if (src == 0) PP_COST_LAUNCH(0, 0); else if (src == 1) PP_COST_LAUNCH(0, 1); else PP_COST_LAUNCH(0, 2);
+    if (src == 0) PP_COST_LAUNCH_L(0, 0); else if (src == 1) PP_COST_LAUNCH_L(0, 1); else PP_COST_LAUNCH(0, 2, 0);
   } else {
-    if (src == 0) PP_COST_LAUNCH(1, 0); else if (src == 1) PP_COST_LAUNCH(1, 1); else PP_COST_LAUNCH(1, 2);
+    if (src == 0) PP_COST_LAUNCH_L(1, 0); else if (src == 1) PP_COST_LAUNCH_L(1, 1); else PP_COST_LAUNCH(1, 2, 0);
   }
+#undef PP_COST_LAUNCH_L
 #undef PP_COST_LAUNCH
   return cudaGetLastError();
 }

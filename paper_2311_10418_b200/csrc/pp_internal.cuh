@@ -46,7 +46,8 @@ struct CostGrid {
   int32_t n_lay;           // distinct stage layouts
   int32_t is_encdec;
   int32_t used;            // bit0: encoder kind priced, bit1: decoder kind priced
-  int32_t pad;
+  int32_t lay_class;       // kLayGeneric / kLayDec1 / kLayEncDec2 (see slice_cost_lay)
+  double le, ld;           // the class's encoder / decoder layer multiples
   const double* mbs_ax;    // double(axis[k]) — the reference converts at :50-51
   const double* seq_ax;
   const double4* tt;       // [2][nm][ns]
@@ -159,6 +160,53 @@ __device__ __forceinline__ void slice_cost(const double4* __restrict__ tt,
   }
   T = bt;
   M = bm;
+}
+
+// Stage-layout classes with a branch-free slice-cost path (capi.cu picks one
+// per call; results are identical to slice_cost, max() over non-NaN values
+// being order-free):
+//   kLayGeneric  any layouts
+//   kLayDec1     one layout, decoder layers only (decoder-only models: GPT)
+//   kLayEncDec2  two layouts, one encoder-only and one decoder-only
+//                (ModelConfig::uniform encoder-decoder split, T5)
+constexpr int kLayGeneric = 0, kLayDec1 = 1, kLayEncDec2 = 2;
+
+template <int LAY, bool TIME, bool MEM>
+__device__ __forceinline__ void slice_cost_lay(const double4* __restrict__ tt,
+                                               const double2* __restrict__ am,
+                                               const LayoutD* __restrict__ lay, int n_lay, int used,
+                                               int nm, int ns, int mi, double tm, int se, double tse,
+                                               int sd, double tsd, double le, double ld, double& T,
+                                               double& M) {
+  if (LAY == kLayGeneric) {
+    slice_cost<TIME, MEM>(tt, am, lay, n_lay, used, nm, ns, mi, tm, se, tse, sd, tsd, T, M);
+    return;
+  }
+  const int per = nm * ns;
+  const KindCost D = kind_cost<TIME, MEM>(tt + per, am + per, ns, mi, tm, sd, tsd);
+  if (LAY == kLayDec1) {
+    if (TIME) {
+      const double t = __dadd_rn(__dmul_rn(ld, D.tf), __dmul_rn(ld, D.tb));
+      T = (0.0 < t) ? t : 0.0;
+    }
+    if (MEM) {
+      const double a = __dmul_rn(ld, D.act);
+      M = (0.0 < a) ? a : 0.0;
+    }
+  } else {
+    const KindCost E = kind_cost<TIME, MEM>(tt, am, ns, mi, tm, se, tse);
+    if (TIME) {
+      const double t1 = __dadd_rn(__dmul_rn(le, E.tf), __dmul_rn(le, E.tb));
+      const double t2 = __dadd_rn(__dmul_rn(ld, D.tf), __dmul_rn(ld, D.tb));
+      const double b1 = (0.0 < t1) ? t1 : 0.0;
+      T = (b1 < t2) ? t2 : b1;
+    }
+    if (MEM) {
+      const double a1 = __dmul_rn(le, E.act), a2 = __dmul_rn(ld, D.act);
+      const double b1 = (0.0 < a1) ? a1 : 0.0;
+      M = (b1 < a2) ? a2 : b1;
+    }
+  }
 }
 
 // Rows per band tile (= rows per DP block).  The band of a segment is stored
