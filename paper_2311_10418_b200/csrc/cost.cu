@@ -380,6 +380,192 @@ __global__ void __launch_bounds__(32 * kCostWarps)
   }
 }
 
+// Pass B, fused grid costing with quantised candidates (I > 0): the lean
+// form of block_kernel<1, SRC, LAY>.  Every lane prices every column of its
+// warp's tile unconditionally and masks the result (no divergence in the
+// column loop); act_mem is priced only where some lane of the warp reaches
+// its row's first infeasible slice (pass A), and candidate bins only leave
+// the two-compare fast path when a lane's slice time crosses into another bin.
+template <int SRC, int LAY>
+__global__ void __launch_bounds__(32 * kCostWarps)
+    band_kernel(CostArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ double s_x[kCostWarps][32], s_y[kCostWarps][32];
+  __shared__ AxisPos s_px[kCostWarps][32], s_py[kCostWarps][32];
+  __shared__ AxisPos s_mb[kCostWarps][64];
+  __shared__ unsigned int s_bm[kCostWarps][kSmallBmWords];
+  const int nm = a.g.nm, ns = a.g.ns, n_lay = a.g.n_lay, used = a.g.used;
+  const double4* tt = a.g.tt;
+  const double2* am = a.g.am;
+  const LayoutD* lay = a.g.lay;
+  const double* tau = a.tau;
+  if (SRC == 0) {
+    const GridSmem L = grid_smem_layout(nm, ns, n_lay, kSmallBmWords * 32);
+    double4* stt = reinterpret_cast<double4*>(dsm + L.tt);
+    double2* sam = reinterpret_cast<double2*>(dsm + L.am);
+    LayoutD* slay = reinterpret_cast<LayoutD*>(dsm + L.lay);
+    double* stau = reinterpret_cast<double*>(dsm + L.tau);
+    const int cells = 2 * nm * ns;
+    for (int k = threadIdx.x; k < cells; k += blockDim.x) {
+      stt[k] = a.g.tt[k];
+      sam[k] = a.g.am[k];
+    }
+    for (int k = threadIdx.x; k < n_lay; k += blockDim.x) slay[k] = a.g.lay[k];
+    for (int k = threadIdx.x; k < kSmallBmWords * 32; k += blockDim.x) stau[k] = a.tau[k];
+    __syncthreads();
+    tt = stt;
+    am = sam;
+    lay = slay;
+    tau = stau;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warps = gridDim.x * kCostWarps;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
+  const bool need_mem = !(a.cap == INF);
+  const bool encdec = a.g.is_encdec != 0;
+  constexpr int kTau = kSmallBmWords * 32;
+  AxisPos p0{0.0, 0, 0};
+  bracket(a.g.seq_ax, ns, 0.0, p0.seg, p0.t);
+  for (int gb = blockIdx.x * kCostWarps + wid; gb < a.total_blocks; gb += warps) {
+    const int s = seg_of(a.blk_base, a.n_seg, gb);
+    const int64_t b0 = a.seg_off[s];
+    const int n = (int)(a.seg_off[s + 1] - b0);
+    const int bl = gb - a.blk_base[s];
+    const int i1 = n - kRB * bl;
+    const int i0 = max(0, i1 - kRB);
+    const int r = lane;
+    const bool rowv = r < i1 - i0;
+    const int i = i0 + r;
+    const int wr = rowv ? a.row_w[b0 + i] : 0;  // 0: never live
+    const int fb = (need_mem && rowv) ? a.row_fb[b0 + i] : INT_MAX;
+    const int W = a.blk_W[gb];
+    double* tile = a.band + a.seg_band_base[s] + a.tile_off[gb];
+    tile[r] = QNAN;  // column 0: j = i0 <= i is never a slice
+    double pin = 0.0, ptg = 0.0;
+    AxisPos pe = p0, pd = p0;
+    // candidate bin of the lane: T in (tlo, thi] <=> bin kw (first slice always misses)
+    int kw = -1;
+    double tlo = INF, thi = -INF;
+    double kmn = INF, kmx = -INF;
+    int flags = 0;
+    bool any_binned = false;
+    unsigned int npriced = 0;
+    if (lane < kSmallBmWords) s_bm[wid][lane] = 0u;
+    __syncwarp();
+    for (int c0 = 1; c0 < W; c0 += 32) {
+      const int cq = c0 + lane;
+      if (cq < W) {
+        const int64_t k = b0 + i0 + cq - 1;
+        s_x[wid][lane] = a.in_d[k];
+        s_px[wid][lane] = a.pin[k];
+        if (encdec) {
+          s_y[wid][lane] = a.tgt_d[k];
+          s_py[wid][lane] = a.ptg[k];
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = lane + 32 * h;
+        s_mb[wid][p] = a.mbp[min(max(c0 - 32 + p, 1), a.max_n)];
+      }
+      __syncwarp();
+      const int qend = min(32, W - c0);
+      for (int q = 0; q < qend; ++q) {
+        const int c = c0 + q;
+        const int j = i0 + c;
+        const bool inrow = c > r;  // sample j-1 belongs to slice [i, j)
+        const bool live = inrow & (c <= r + wr);
+        const double x = s_x[wid][q];
+        const AxisPos px = s_px[wid][q];
+        const bool upx = inrow & (pin < x);
+        pin = upx ? x : pin;
+        pe.t = upx ? px.t : pe.t;
+        pe.seg = upx ? px.seg : pe.seg;
+        if (encdec) {
+          const double y = s_y[wid][q];
+          const AxisPos py = s_py[wid][q];
+          const bool upy = inrow & (ptg < y);
+          ptg = upy ? y : ptg;
+          pd.t = upy ? py.t : pd.t;
+          pd.seg = upy ? py.seg : pd.seg;
+        }
+        const AxisPos mb = s_mb[wid][q - r + 32];
+        const int sd = encdec ? pd.seg : pe.seg;
+        const double tsd = encdec ? pd.t : pe.t;
+        double T, M;
+        slice_cost_lay<LAY, true, false>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t, sd,
+                                         tsd, a.g.le, a.g.ld, T, M);
+        bool ok = true;
+        const bool chk = live & (j >= fb);
+        if (__any_sync(0xffffffffu, chk)) {  // act_mem near the cap (rare)
+          double T2;
+          slice_cost_lay<LAY, false, true>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t,
+                                           sd, tsd, a.g.le, a.g.ld, T2, M);
+          ok = !(chk & (M > a.cap));
+        }
+        const bool feas = live & ok;
+        tile[(size_t)c * kRB + r] = feas ? T : QNAN;
+        npriced += live ? 1u : 0u;
+        // candidate bin k = ceil(fl(T / I)) = min{k : T <= tau[k]} (microbatch.cpp:264)
+        const bool miss = feas & !((T > tlo) & (T <= thi));
+        if (__any_sync(0xffffffffu, miss)) {
+          if (miss) {
+            int k = max(kw, 0);
+            while (k < kTau && !(T <= tau[k])) ++k;
+            while (k > 0 && T <= tau[k - 1]) --k;
+            if (k < kTau) {
+              kw = k;
+              tlo = k > 0 ? tau[k - 1] : -INF;
+              thi = tau[k];
+              any_binned = true;
+              atomicOr(&s_bm[wid][k >> 5], 1u << (k & 31));
+            } else {  // beyond the thresholds (or +inf): exact quantisation
+              const double qv = ceil(__ddiv_rn(T, a.interval));
+              if (isinf(qv)) {
+                flags |= (qv > 0) ? 1 : 2;
+              } else {
+                kmn = (qv < kmn) ? qv : kmn;
+                kmx = (kmx < qv) ? qv : kmx;
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (any_binned) {  // binned values lie in [0, kTau): widen the range to a superset
+      kmn = (0.0 < kmn) ? 0.0 : kmn;
+      kmx = (kmx < (double)(kTau - 1)) ? (double)(kTau - 1) : kmx;
+    }
+    unsigned long long np = npriced;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, kmn, o);
+      const double y = __shfl_xor_sync(0xffffffffu, kmx, o);
+      kmn = (x < kmn) ? x : kmn;
+      kmx = (kmx < y) ? y : kmx;
+      np += __shfl_xor_sync(0xffffffffu, np, o);
+      flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&a.stats[s].priced_b, np);
+      if (np) atomicAdd(&a.stats[s].nraw, np);  // >= the raw count; only sizes the raw fallback
+      if (!isinf(kmn)) {
+        atomicMin(&a.stats[s].kmin, dkey(kmn));
+        atomicMax(&a.stats[s].kmax, dkey(kmx));
+      }
+      if (flags) atomicOr(&a.stats[s].flags, flags);
+    }
+    __syncwarp();
+    if (lane < kSmallBmWords) {
+      const unsigned int w = s_bm[wid][lane];
+      if (w) atomicOr(&a.small_bm[(size_t)s * kSmallBmWords + lane], w);
+    }
+    __syncwarp();
+  }
+}
+
 // cap = +inf: every slice is memory-feasible (!(M > inf) holds for every M,
 // NaN included), so Rm(i) = n and W_b = n - i0 + 1 without costing anything.
 __global__ void full_rows_kernel(const int64_t* __restrict__ seg_off, const int* __restrict__ blk_base,
@@ -641,12 +827,28 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
     else if (g.lay_class == kLayEncDec2) PP_COST_LAUNCH(P, S, kLayEncDec2);      \
     else PP_COST_LAUNCH(P, S, kLayGeneric);                                      \
   } while (0)
+#define PP_BAND_LAUNCH(S, L)                                                                       \
+  do {                                                                                              \
+    cudaFuncSetAttribute(band_kernel<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
+    band_kernel<S, L><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                      \
+  } while (0)
   if (pass == 0) {
     if (src == 0) PP_COST_LAUNCH_L(0, 0); else if (src == 1) PP_COST_LAUNCH_L(0, 1); else PP_COST_LAUNCH(0, 2, 0);
+  } else if (tau && src != 2) {
+    if (src == 0) {
+      if (g.lay_class == kLayDec1) PP_BAND_LAUNCH(0, kLayDec1);
+      else if (g.lay_class == kLayEncDec2) PP_BAND_LAUNCH(0, kLayEncDec2);
+      else PP_BAND_LAUNCH(0, kLayGeneric);
+    } else {
+      if (g.lay_class == kLayDec1) PP_BAND_LAUNCH(1, kLayDec1);
+      else if (g.lay_class == kLayEncDec2) PP_BAND_LAUNCH(1, kLayEncDec2);
+      else PP_BAND_LAUNCH(1, kLayGeneric);
+    }
   } else {
     if (src == 0) PP_COST_LAUNCH_L(1, 0); else if (src == 1) PP_COST_LAUNCH_L(1, 1); else PP_COST_LAUNCH(1, 2, 0);
   }
 #undef PP_COST_LAUNCH_L
+#undef PP_BAND_LAUNCH
 #undef PP_COST_LAUNCH
   return cudaGetLastError();
 }

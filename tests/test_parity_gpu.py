@@ -266,3 +266,26 @@ def test_pass_a_certificate_random_grids(planner, orc, jitter):
         if jitter:
             assert math.isinf(st["exit_thresh"]), k  # no certificate: full scan
         assert_plan_matches(b, record(a), f"cert grid {k} jitter={jitter}")
+
+
+@pytest.mark.parametrize("bad", [math.inf, math.nan])
+def test_nonfinite_grid_cells_match_oracle(planner, orc, bad):
+    """The reference accepts any non-negative cells (cost_model.cpp:86-88; NaN
+    and +inf pass its check).  Blends through such cells produce NaN, which
+    std::max(0.0, v) maps to 0.0 (cost_model.cpp:141) — the device must clamp
+    exactly the same way."""
+    g = capi.synthetic_grid()
+    cells = g.cells.copy()
+    cells[:, :, 3, 4, :] = bad
+    cells[1, 0, 6, 2, 0] = bad
+    grid = capi.Grid(g.mbs_axis, g.seq_axis, cells)
+    rng = np.random.default_rng(17)
+    for k in range(8):
+        n = int(rng.integers(5, 200))
+        encdec = bool(k % 2)
+        s = capi.synthetic_dataset(n, 4096, 300 + k, W.INPUT_DIST, W.T5_TARGET_DIST if encdec else None)
+        model = capi.Model.uniform(4, 2, encdec)
+        interval = float(rng.choice([0.0, 50.0, 5000.0]))
+        a = orc.plan(s, grid, model, 4, 1, math.inf, interval)
+        b = _plan_or_status(lambda: planner.plan(s, grid, model, 4, 1, math.inf, interval))
+        assert_plan_matches(b, record(a), f"nonfinite {bad} {k}")
