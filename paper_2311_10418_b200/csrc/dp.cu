@@ -125,7 +125,7 @@ __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int
 // than the (+inf, 0) identity or any taken value, -inf is taken exactly when
 // the reference takes it.
 template <int MODE, bool SMEM_STATE, bool SANITIZE>
-__global__ void __launch_bounds__(kDpThreads, 1)
+__global__ void __launch_bounds__(kDpThreads, 2)
     dp_pass_kernel(const WorkItem* __restrict__ items, const int64_t* __restrict__ seg_off,
                    const int* __restrict__ blk_base, const int* __restrict__ blk_W,
                    const int64_t* __restrict__ tile_off, const int64_t* __restrict__ seg_band_base,
@@ -284,25 +284,30 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         npm[o] = m1;
       }
     }
-    named_bar(3, kSyncThreads);
-
+    // ---- the chain warp meanwhile loads its own tile and far-far partial
+    const int W = blk_W[gb0 + b];
+    const int r = lane;
+    double as = INF, am = INF;
+    int ac = 0, aj = INT_MAX;
     if (wid == kChainWarp) {
-      // ================= chain warp: block b =================
       PP_TRACE(0);
-      const int W = blk_W[gb0 + b];
-      const int r = lane;
       const int pbuf = (b & 1) * kRB + r;
-      double as = ps[pbuf];
-      int ac = 0, aj = INT_MAX;
-      double am = INF;
+      as = ps[pbuf];
       if (MODE == 0) {
         ac = pc[pbuf];
         aj = pj[pbuf];
       } else {
         am = pm[pbuf];
       }
-      // fold far-far + the 8 near-far partials: a pairwise tree (ILP), lexmin
-      // with j ties is associative
+      mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
+    }
+    named_bar(3, kSyncThreads);
+
+    if (wid == kChainWarp) {
+      // ================= chain warp: block b =================
+      PP_TRACE(1);
+      // fold the 8 near-far partials: a pairwise tree (ILP), lexmin with j
+      // ties is associative
       {
         double s8[kWorkers], m8[kWorkers];
         int c8[kWorkers], j8[kWorkers];
@@ -342,18 +347,6 @@ __global__ void __launch_bounds__(kDpThreads, 1)
           am = (m8[0] < am) ? m8[0] : am;
         }
       }
-      PP_TRACE(1);
-      // in-block triangle: T[i0 + r, i0 + jj] for jj in (r, nb)
-      double tn[kRB];
-      unsigned fm = 0;  // columns this lane may take (x <= t; MODE 1: not masked)
-#pragma unroll
-      for (int jj = 0; jj < kRB; ++jj) {
-        tn[jj] = (jj < W) ? nt[jj * kRB + r] : QNAN;
-        const bool ok = MODE == 0 ? (tn[jj] <= t) : !isnan(tn[jj]);
-        fm |= (ok & (r < jj)) ? (1u << jj) : 0u;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);  // near tile of block b consumed
       PP_TRACE(2);
       if (r >= nb) {
         as = INF;
@@ -364,11 +357,15 @@ __global__ void __launch_bounds__(kDpThreads, 1)
       // T[i0 + r, i0 + jj] + state.  Descending j: equal (sum, count) takes
       // the lower j.  Rows >= nb hold (+inf, 0), which can never be taken, so
       // a full block runs all 32 steps unconditionally.
+      // the triangle's tile column jj is read from shared memory inside its
+      // step (independent of the chain, so its latency hides under the
+      // shuffle) — 32 doubles fewer live registers
       auto tri_step = [&](int jj) {
+        const double x = lds_f64(nt + jj * kRB + r);
         double sj = __shfl_sync(0xffffffffu, as, jj);
         if (SANITIZE) sj = isfinite(sj) ? sj : INF;
-        const double cs = __dadd_rn(tn[jj], sj);
-        const bool ok = (fm >> jj) & 1u;
+        const double cs = __dadd_rn(x, sj);
+        const bool ok = (jj < W) & (r < jj) & (MODE == 0 ? (x <= t) : !isnan(x));
         if (MODE == 0) {
           const int cn = 1 + __shfl_sync(0xffffffffu, ac, jj);
           const bool upd = ok & ((cs < as) | ((cs == as) & (cn <= ac)));
@@ -378,7 +375,6 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         } else {
           const double mj = __shfl_sync(0xffffffffu, am, jj);
           as = (ok & (cs < as)) ? cs : as;
-          const double x = tn[jj];
           const double v = (x < mj) ? mj : x;
           am = (ok & (x < INF) & (mj < INF) & (v < am)) ? v : am;
         }
@@ -391,6 +387,8 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         for (int jj = kRB - 1; jj >= 0; --jj)
           if (jj < nb) tri_step(jj);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);  // near tile of block b consumed
       PP_TRACE(3);
       if (r < nb) {
         const int row = i0 + r;
