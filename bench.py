@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--per-gpu", type=int, default=0, help="mini-batches per GPU per step")
     ap.add_argument("--cpu-plans", type=int, default=0, help="cpu_baseline sample size (0: cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=2, help="concurrent sub-batches per GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -187,7 +188,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = W.CONFIGS[args.config]
-    M = args.per_gpu or {"C3": 148, "C4": 512, "C1": 1024, "C2": 128, "C5": 1}.get(cfg.name, 8)
+    M = args.per_gpu or {"C3": 296, "C4": 1024, "C1": 1024, "C2": 128, "C5": 1}.get(cfg.name, 8)
     steps, warm = args.steps, args.warmup
     n = cfg.n
     # distinct mini-batches for every (rank, step): rank r owns groups
@@ -203,6 +204,9 @@ def main():
     d_seg = torch.from_numpy(seg).cuda()
     grid, model = W.grid(), W.model(cfg)
     planner = capi.Planner(local)
+    # concurrent sub-batches (pp_tuning::streams): one sub-batch's
+    # latency-bound DP overlaps another's cost passes
+    planner.set_tuning(streams=args.streams)
     stream = torch.cuda.Stream()
     planner.set_stream(stream.cuda_stream)
     tot = M * n

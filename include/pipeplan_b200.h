@@ -93,7 +93,11 @@ typedef struct pp_dp_options {
 typedef struct pp_tuning {
   int32_t first_wave;      /* t_max candidates evaluated in the first wave (>=1) */
   int32_t max_wave;        /* cap on a wave's candidates per mini-batch */
-  int32_t reserved[6];
+  int32_t streams;         /* >1: a batched call is split into this many contiguous
+                              sub-batches planned concurrently on their own streams
+                              and host threads (one sub-batch's latency-bound DP
+                              overlaps another's cost passes); 0/1 = one stream */
+  int32_t reserved[5];
 } pp_tuning;
 
 /* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are

@@ -72,7 +72,8 @@ class DpOptions(C.Structure):
 
 
 class Tuning(C.Structure):
-    _fields_ = [("first_wave", C.c_int32), ("max_wave", C.c_int32), ("reserved", C.c_int32 * 6)]
+    _fields_ = [("first_wave", C.c_int32), ("max_wave", C.c_int32), ("streams", C.c_int32),
+                ("reserved", C.c_int32 * 5)]
 
 
 class PlanOut(C.Structure):
@@ -306,8 +307,8 @@ class Planner:
     def _err(self) -> str:
         return (lib.pp_ctx_last_error(self._h) or b"").decode()
 
-    def set_tuning(self, first_wave: int = 1, max_wave: int = 16):
-        t = Tuning(first_wave, max_wave)
+    def set_tuning(self, first_wave: int = 1, max_wave: int = 16, streams: int = 1):
+        t = Tuning(first_wave, max_wave, streams)
         rc = lib.pp_ctx_set_tuning(self._h, C.byref(t))
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())

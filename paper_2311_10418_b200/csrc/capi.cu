@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "pp_internal.cuh"
@@ -181,6 +182,9 @@ struct pp_ctx {
   CostGrid grid_dev{};            // device view of the uploaded grid
   bool grid_valid = false;
   double tau_interval = -1.0;     // interval the device bin thresholds were built for
+  // concurrent sub-batch contexts (pp_tuning::streams), created on demand
+  std::vector<pp_ctx*> subs;
+  cudaEvent_t ev_in = nullptr;
   // per-launch event pairs for kernel timing (pp_stats::ms_kernel)
   std::vector<cudaEvent_t> kev;
   std::vector<int> kcat;
@@ -1006,6 +1010,106 @@ int stage_inputs(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offse
   return PP_OK;
 }
 
+// pp_tuning::streams > 1: contiguous sub-batches of segments, each planned by
+// its own sub-context (stream + scratch) from its own host thread, all on the
+// caller's device.  Sub-streams start after the caller stream's pending work
+// (the inputs) and the caller stream waits for all of them, so the call keeps
+// its single-stream semantics.  Results are written in place (outputs are
+// indexed by sample / segment, so each part writes a disjoint slice).
+int plan_split(pp_ctx* ctx, const PlanCall& c, int parts) {
+  const int n_seg = c.n_seg;
+  parts = std::min(parts, n_seg);
+  while ((int)ctx->subs.size() < parts) {
+    pp_ctx* sub = nullptr;
+    const int rc = pp_ctx_create(ctx->device, &sub);
+    if (rc != PP_OK) return fail(ctx, rc, "cannot create a sub-context");
+    ctx->subs.push_back(sub);
+  }
+  if (!ctx->ev_in) PP_CUDA(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+  PP_CUDA(cudaEventRecord(ctx->ev_in, ctx->stream));
+  // split by sample count
+  const int64_t total = c.h_seg_off[n_seg];
+  std::vector<int> cut(parts + 1, 0);
+  cut[parts] = n_seg;
+  for (int p = 1; p < parts; ++p) {
+    const int64_t target = total * p / parts;
+    int s = cut[p - 1] + 1;
+    while (s < n_seg - (parts - p) && c.h_seg_off[s] < target) ++s;
+    cut[p] = s;
+  }
+  std::vector<int> rcs(parts, PP_OK);
+  std::vector<std::thread> th;
+  for (int p = 0; p < parts; ++p) {
+    th.emplace_back([&, p]() {
+      pp_ctx* sub = ctx->subs[p];
+      cudaSetDevice(sub->device);
+      sub->tuning = ctx->tuning;
+      sub->tuning.streams = 1;
+      const int s0 = cut[p], s1 = cut[p + 1];
+      const int64_t base = c.h_seg_off[s0];
+      std::vector<int64_t> off(s1 - s0 + 1);
+      for (int s = s0; s <= s1; ++s) off[s - s0] = c.h_seg_off[s] - base;
+      int rc = PP_OK;
+      auto cu = [&](cudaError_t e) {
+        if (e != cudaSuccess && rc == PP_OK) {
+          sub->err = cudaGetErrorString(e);
+          rc = PP_ERR_CUDA;
+        }
+      };
+      cu(cudaStreamWaitEvent(sub->stream, ctx->ev_in, 0));
+      cu(sub->seg_off.ensure(off.size() * sizeof(int64_t)));
+      cu(cudaMemcpyAsync(sub->seg_off.p, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                         sub->stream));
+      if (rc == PP_OK) {
+        PlanCall cc = c;
+        cc.d_samples = c.d_samples ? c.d_samples + base : nullptr;
+        cc.d_seg_off = sub->seg_off.as<int64_t>();
+        cc.h_seg_off = off.data();
+        cc.n_seg = s1 - s0;
+        cc.d_ordered = c.d_ordered + base;
+        cc.d_splits = c.d_splits ? c.d_splits + base : nullptr;
+        cc.d_times = c.d_times ? c.d_times + base : nullptr;
+        cc.d_count = c.d_count ? c.d_count + s0 : nullptr;
+        cc.d_tmax = c.d_tmax ? c.d_tmax + s0 : nullptr;
+        cc.d_obj = c.d_obj ? c.d_obj + s0 : nullptr;
+        cc.d_status = c.d_status ? c.d_status + s0 : nullptr;
+        cc.d_err = c.d_err ? c.d_err + s0 : nullptr;
+        rc = run_plan(sub, cc);  // synchronises its stream before returning
+      }
+      rcs[p] = rc;
+    });
+  }
+  for (auto& t : th) t.join();
+  pp_stats S{};
+  S.exit_thresh = INFINITY;
+  for (int p = 0; p < parts; ++p) {
+    pp_ctx* sub = ctx->subs[p];
+    if (rcs[p] != PP_OK) return fail(ctx, rcs[p], sub->err);
+    const pp_stats& t = sub->stats;
+    S.candidates_generated += t.candidates_generated;
+    S.candidates_evaluated += t.candidates_evaluated;
+    S.transitions_executed += t.transitions_executed;
+    S.transitions_reference += t.transitions_reference;
+    S.slices_costed += t.slices_costed;
+    S.waves = std::max(S.waves, t.waves);
+    S.ms_sort = std::max(S.ms_sort, t.ms_sort);
+    S.ms_cost = std::max(S.ms_cost, t.ms_cost);
+    S.ms_dp = std::max(S.ms_dp, t.ms_dp);
+    S.ms_total = std::max(S.ms_total, t.ms_total);
+    for (int k = 0; k < 8; ++k) {
+      S.ms_kernel[k] += t.ms_kernel[k];
+      S.launches[k] += t.launches[k];
+    }
+    S.dp_band_bytes += t.dp_band_bytes;
+    S.slices_pass_a += t.slices_pass_a;
+    S.slices_pass_b += t.slices_pass_b;
+    S.bound_transitions += t.bound_transitions;
+    S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
+  }
+  ctx->stats = S;
+  return PP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1038,7 +1142,10 @@ int pp_ctx_create(int device, pp_ctx** out) {
 
 int pp_ctx_destroy(pp_ctx* ctx) {
   if (!ctx) return PP_OK;
+  for (pp_ctx* sub : ctx->subs) pp_ctx_destroy(sub);
+  ctx->subs.clear();
   cudaSetDevice(ctx->device);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : ctx->all_bufs()) b->release();
   for (PinBuf* b : {&ctx->h_range, &ctx->h_stats, &ctx->h_segdp}) b->release();
@@ -1053,7 +1160,7 @@ int pp_ctx_destroy(pp_ctx* ctx) {
 const char* pp_ctx_last_error(const pp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int pp_ctx_set_tuning(pp_ctx* ctx, const pp_tuning* t) {
-  if (!ctx || !t || t->first_wave < 1) return PP_ERR_INVALID;
+  if (!ctx || !t || t->first_wave < 1 || t->streams < 0 || t->streams > 16) return PP_ERR_INVALID;
   ctx->tuning = *t;
   return PP_OK;
 }
@@ -1115,6 +1222,13 @@ int pp_plan_grid_device(pp_ctx* ctx, const pp_sample* d_samples, const int64_t* 
     const int64_t total = h_seg_offsets[n_seg];
     PP_CUDA(ctx->ordered.ensure(std::max<int64_t>(total, 1) * sizeof(pp_sample)));
     c.d_ordered = ctx->ordered.as<pp_sample>();
+  }
+  if (ctx->tuning.streams > 1 && n_seg > 1) {
+    if (h_seg_offsets[0] != 0) return fail(ctx, PP_ERR_INVALID, "seg_offsets[0] must be 0");
+    for (int s = 0; s < n_seg; ++s)
+      if (h_seg_offsets[s + 1] < h_seg_offsets[s])
+        return fail(ctx, PP_ERR_INVALID, "seg_offsets must be non-decreasing");
+    return plan_split(ctx, c, ctx->tuning.streams);
   }
   return run_plan(ctx, c);
 }

@@ -289,3 +289,32 @@ def test_nonfinite_grid_cells_match_oracle(planner, orc, bad):
         a = orc.plan(s, grid, model, 4, 1, math.inf, interval)
         b = _plan_or_status(lambda: planner.plan(s, grid, model, 4, 1, math.inf, interval))
         assert_plan_matches(b, record(a), f"nonfinite {bad} {k}")
+
+
+def test_concurrent_sub_batches_match_single_stream():
+    """pp_tuning::streams splits a batch over concurrent sub-contexts; the
+    plans must be identical to the single-stream call (and the golden C3)."""
+    cfg = W.CONFIGS["C3"]
+    M = 7
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    a = capi.Planner(0)
+    b = capi.Planner(0)
+    b.set_tuning(streams=3)
+    ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    for k in ("ordered", "count", "t_max_used", "objective", "status"):
+        assert ra[k].tobytes() == rb[k].tobytes(), k
+    for q in range(M):  # only the first count[q] entries of a segment are defined
+        m = int(ra["count"][q])
+        for k in ("splits", "mb_times"):
+            assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
+    st = b.stats()
+    assert st["candidates_evaluated"] == M
+    case = load_golden("c3")
+    m = int(rb["count"][0])
+    got = capi.Plan(int(rb["status"][0]), rb["splits"][:m], rb["mb_times"][:m], float(rb["t_max_used"][0]),
+                    float(rb["objective"][0]), -1, rb["ordered"][:cfg.n])
+    assert_plan_matches(got, case["expect"], "C3 split")
+    a.close()
+    b.close()

@@ -11,12 +11,12 @@ from paper_2311_10418_b200 import capi  # noqa: E402
 from paper_2311_10418_b200 import workloads as W  # noqa: E402
 
 
-def run(name, M, reps=3, first_wave=1, max_wave=16):
+def run(name, M, reps=3, first_wave=1, max_wave=16, streams=1):
     cfg = W.CONFIGS[name]
     s = W.dataset(cfg, M)
     off = W.seg_offsets(cfg, M)
     p = capi.Planner(0)
-    p.set_tuning(first_wave, max_wave)
+    p.set_tuning(first_wave, max_wave, streams)
     r = p.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     best = 1e9
     for _ in range(reps):
@@ -31,5 +31,5 @@ def run(name, M, reps=3, first_wave=1, max_wave=16):
 
 if __name__ == "__main__":
     for spec in sys.argv[1:] or ["C1:1", "C1:64", "C2:1", "C2:16", "C3:1", "C3:8", "C4:64", "C4:512"]:
-        n, m = spec.split(":")
-        run(n, int(m))
+        n, m, *g = spec.split(":")
+        run(n, int(m), streams=int(g[0]) if g else 1)
