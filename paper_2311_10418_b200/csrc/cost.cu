@@ -444,9 +444,12 @@ __global__ void __launch_bounds__(32 * kCostWarps)
     tile[r] = QNAN;  // column 0: j = i0 <= i is never a slice
     double pin = 0.0, ptg = 0.0;
     AxisPos pe = p0, pd = p0;
-    // candidate bin of the lane: T in (tlo, thi] <=> bin kw (first slice always misses)
-    int kw = -1;
-    double tlo = INF, thi = -INF;
+    // candidate bin of the lane: T in (tlo, thi] <=> bin kw (first slice always
+    // misses); bins seen are kept in a 64-bit window [kb, kb + 64) and
+    // flushed to the warp's shared bitmap only when the window moves
+    int kw = -1, kb = 0;
+    double tlo = INF, thi = -INF, tnx = -INF;  // tnx = tau[kw + 1]
+    unsigned long long win = 0ull;
     double kmn = INF, kmx = -INF;
     int flags = 0;
     bool any_binned = false;
@@ -507,7 +510,15 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         const bool feas = live & ok;
         tile[(size_t)c * kRB + r] = feas ? T : QNAN;
         npriced += live ? 1u : 0u;
-        // candidate bin k = ceil(fl(T / I)) = min{k : T <= tau[k]} (microbatch.cpp:264)
+        // candidate bin k = ceil(fl(T / I)) = min{k : T <= tau[k]} (microbatch.cpp:264).
+        // Fast path, branch-free: same bin, or the next one (slice times grow
+        // along a row).
+        const bool step = feas & (T > thi) & (T <= tnx) & (kw + 1 < kb + 64);
+        kw = step ? kw + 1 : kw;
+        tlo = step ? thi : tlo;
+        thi = step ? tnx : thi;
+        win |= step ? (1ull << (kw - kb)) : 0ull;
+        if (step) tnx = (kw + 1 < kTau) ? tau[kw + 1] : INF;
         const bool miss = feas & !((T > tlo) & (T <= thi));
         if (__any_sync(0xffffffffu, miss)) {
           if (miss) {
@@ -515,11 +526,20 @@ __global__ void __launch_bounds__(32 * kCostWarps)
             while (k < kTau && !(T <= tau[k])) ++k;
             while (k > 0 && T <= tau[k - 1]) --k;
             if (k < kTau) {
+              if (k < kb || k >= kb + 64) {  // move the window
+                for (int w = 0; w < 2; ++w) {
+                  const unsigned int part = (unsigned int)(win >> (32 * w));
+                  if (part) atomicOr(&s_bm[wid][(kb >> 5) + w], part);
+                }
+                win = 0ull;
+                kb = k & ~31;
+              }
               kw = k;
               tlo = k > 0 ? tau[k - 1] : -INF;
               thi = tau[k];
+              tnx = (k + 1 < kTau) ? tau[k + 1] : INF;
+              win |= 1ull << (k - kb);
               any_binned = true;
-              atomicOr(&s_bm[wid][k >> 5], 1u << (k & 31));
             } else {  // beyond the thresholds (or +inf): exact quantisation
               const double qv = ceil(__ddiv_rn(T, a.interval));
               if (isinf(qv)) {
@@ -533,6 +553,10 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         }
       }
       __syncwarp();
+    }
+    for (int w = 0; w < 2; ++w) {  // flush the bin window
+      const unsigned int part = (unsigned int)(win >> (32 * w));
+      if (part) atomicOr(&s_bm[wid][(kb >> 5) + w], part);
     }
     if (any_binned) {  // binned values lie in [0, kTau): widen the range to a superset
       kmn = (0.0 < kmn) ? 0.0 : kmn;
