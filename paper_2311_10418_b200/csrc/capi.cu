@@ -58,7 +58,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              double interval, int* row_w, int* row_fb, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
-                             cudaStream_t st);
+                             double lo_thresh, int bisect, cudaStream_t st);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
                              int* row_w, int* blk_W, cudaStream_t st);
 cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -450,8 +450,9 @@ double dkey_inv_host(unsigned long long k) {
 // u = 2^-53; we use 128 u.  Returns +inf (no certificate: full scan) when a
 // condition fails or is within 1e-12 relative of failing.
 double mem_exit_threshold(const pp_ctx* ctx, double cap, int max_n, double seq_lo[2],
-                          double seq_hi[2]) {
+                          double seq_hi[2], double* lo_thresh) {
   const double INF = INFINITY;
+  *lo_thresh = -INF;
   if (!(cap < INF) || std::isnan(cap)) return INF;
   const int nm = ctx->h_nm, ns = ctx->h_ns;
   const double* mbs_ax = ctx->h_ax.data();
@@ -533,7 +534,12 @@ double mem_exit_threshold(const pp_ctx* ctx, double cap, int max_n, double seq_l
   const long double E = 128.0L * u * (1.0L + tm_abs) * 2.0L * worst + 1e-300L;
   double th = (double)((long double)cap + 2.0L * E);
   th = std::nextafter(std::nextafter(th, INF), INF);
-  return std::isfinite(th) ? th : INF;
+  if (!std::isfinite(th)) return INF;
+  // cap - 2E, rounded down: a slice at or below it is certified feasible along
+  // with every shorter slice of its row (rowexit_kernel)
+  double tl = (double)((long double)cap - 2.0L * E);
+  *lo_thresh = std::nextafter(std::nextafter(tl, -INF), -INF);
+  return th;
 }
 
 // Steps 1-2 (+ tile offsets): sort, block bookkeeping, cost pass A.  Leaves
@@ -591,7 +597,8 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   const double cap = c.opts.per_mb_mem_cap;
   // Pass A (or its closed form when every slice is memory-feasible).
   const bool full_rows = !table && cap == INFINITY;
-  double exit_thresh = INFINITY;
+  double exit_thresh = INFINITY, lo_thresh = -INFINITY;
+  int bisect = 0;
   if (!table && !full_rows && total > 0) {
     const unsigned long long* hr = ctx->h_range.as<unsigned long long>();
     double lo[2], hi[2];
@@ -599,7 +606,10 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
       lo[q] = (double)(long long)(hr[q] ^ 0x8000000000000000ULL);
       hi[q] = (double)(long long)(hr[3 + q] ^ 0x8000000000000000ULL);
     }
-    exit_thresh = mem_exit_threshold(ctx, cap, max_n, lo, hi);
+    exit_thresh = mem_exit_threshold(ctx, cap, max_n, lo, hi, &lo_thresh);
+    // bisection needs O(1) slice pricing: every segment sorted by input (our
+    // sort) and every priced kind reading the input length
+    bisect = !c.presorted && std::isfinite(exit_thresh) && (!g.is_encdec || !(g.used & 2));
   }
   ctx->exit_thresh = exit_thresh;
   unsigned int* small_bm = nullptr;
@@ -630,7 +640,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                    ctx->blk_base.as<int>(), n_seg, total_blocks, max_n, ctx->mbp.as<AxisPos>(),
                                    cap, interval, ctx->row_w.as<int>(), ctx->row_fb.as<int>(), ctx->blk_W.as<int>(),
                                    ctx->stats_d.as<SegStats>(), nullptr, nullptr, nullptr, exit_thresh,
-                                   nullptr, nullptr, st));
+                                   nullptr, nullptr, lo_thresh, bisect, st));
     PP_TIMED(1, launch_tile_offsets(ctx->blk_W.as<int>(), ctx->blk_base.as<int>(), n_seg,
                                     ctx->tile_off.as<int64_t>(), ctx->stats_d.as<SegStats>(), st));
   }
@@ -656,7 +666,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                  cap, interval, ctx->row_w.as<int>(), ctx->row_fb.as<int>(), ctx->blk_W.as<int>(),
                                  ctx->stats_d.as<SegStats>(), ctx->tile_off.as<int64_t>(),
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), INFINITY, small_bm,
-                                 tau_d, st));
+                                 tau_d, -INFINITY, 0, st));
   PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
   PP_CUDA(cudaStreamSynchronize(st));
   return PP_OK;

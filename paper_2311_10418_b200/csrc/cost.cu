@@ -380,6 +380,121 @@ __global__ void __launch_bounds__(32 * kCostWarps)
   }
 }
 
+// Pass A by certified bisection.  Applies when every segment is sorted by
+// input length and every priced stage kind reads the input length (decoder-
+// only models, or encoder-decoder models without decoder layers): the padded
+// shape of slice [i, j) is then (j - i, max(0, in[j-1])), so any slice can be
+// priced in O(1).  With the monotonicity certificate (capi.cu
+// mem_exit_threshold: exact act_mem non-decreasing in j, device error <= E):
+//   * a j with M~(i,j) > cap + 2E makes every longer slice infeasible (jx);
+//   * a j with M~(i,j) <= cap - 2E makes every shorter slice feasible (jlo);
+// bisection finds such crossing points in ~2 log2(n) pricings, and only the
+// few slices strictly between them are priced one by one.  Rm(i), the first
+// infeasible end fb(i) and the singleton check come out exactly as from the
+// full scan of block_kernel<0>.
+template <int SRC, int LAY>
+__global__ void __launch_bounds__(32 * kCostWarps)
+    rowexit_kernel(CostArgs a, double lo_thresh) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int nm = a.g.nm, ns = a.g.ns, n_lay = a.g.n_lay, used = a.g.used;
+  const double4* tt = a.g.tt;
+  const double2* am = a.g.am;
+  const LayoutD* lay = a.g.lay;
+  if (SRC == 0) {
+    const GridSmem L = grid_smem_layout(nm, ns, n_lay, 0);
+    double4* stt = reinterpret_cast<double4*>(dsm + L.tt);
+    double2* sam = reinterpret_cast<double2*>(dsm + L.am);
+    LayoutD* slay = reinterpret_cast<LayoutD*>(dsm + L.lay);
+    const int cells = 2 * nm * ns;
+    for (int k = threadIdx.x; k < cells; k += blockDim.x) {
+      stt[k] = a.g.tt[k];
+      sam[k] = a.g.am[k];
+    }
+    for (int k = threadIdx.x; k < n_lay; k += blockDim.x) slay[k] = a.g.lay[k];
+    __syncthreads();
+    tt = stt;
+    am = sam;
+    lay = slay;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warps = gridDim.x * kCostWarps;
+  const double cap = a.cap, hi_thresh = a.exit_thresh;
+  AxisPos p0{0.0, 0, 0};
+  bracket(a.g.seq_ax, ns, 0.0, p0.seg, p0.t);
+  for (int gb = blockIdx.x * kCostWarps + wid; gb < a.total_blocks; gb += warps) {
+    const int s = seg_of(a.blk_base, a.n_seg, gb);
+    const int64_t b0 = a.seg_off[s];
+    const int n = (int)(a.seg_off[s + 1] - b0);
+    const int bl = gb - a.blk_base[s];
+    const int i1 = n - kRB * bl;
+    const int i0 = max(0, i1 - kRB);
+    const int r = lane;
+    const bool rowv = r < i1 - i0;
+    const int i = i0 + r;
+    unsigned int npriced = 0;
+    int w = 0;
+    if (rowv) {
+      // act_mem of slice [i, j): shape (j - i, max(0, in[j-1]))
+      auto mem_of = [&](int j) -> double {
+        ++npriced;
+        const AxisPos mb = a.mbp[min(j - i, a.max_n)];
+        const bool pos = 0.0 < a.in_d[b0 + j - 1];
+        const AxisPos px = a.pin[b0 + j - 1];
+        const int se = pos ? px.seg : p0.seg;
+        const double ts = pos ? px.t : p0.t;
+        double T, M;
+        slice_cost_lay<LAY, false, true>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, se, ts, se, ts,
+                                         a.g.le, a.g.ld, T, M);
+        return M;
+      };
+      const double m1 = mem_of(i + 1);
+      if (m1 > cap) atomicMin(&a.stats[s].err_row, i);  // microbatch.cpp:245-251
+      // jx: every slice [i, j >= jx) is infeasible
+      int jx = n + 1;
+      if (mem_of(n) > hi_thresh) {
+        int lo = i, hi = n;  // mem_of(hi) > hi_thresh; lo: empty or <= hi_thresh
+        while (hi - lo > 1) {
+          const int mid = lo + ((hi - lo) >> 1);
+          if (mem_of(mid) > hi_thresh) hi = mid; else lo = mid;
+        }
+        jx = hi;
+      }
+      // jlo: every slice [i, j <= jlo) is feasible
+      int jlo = i;
+      if (m1 <= lo_thresh) {
+        int lo = i + 1, hi = jx;  // hi: virtual (> lo_thresh) or jx
+        while (hi - lo > 1) {
+          const int mid = lo + ((hi - lo) >> 1);
+          if (mem_of(mid) <= lo_thresh) lo = mid; else hi = mid;
+        }
+        jlo = lo;
+      }
+      int last_ok = jlo, fb = INT_MAX;
+      for (int j = jlo + 1; j < min(jx, n + 1); ++j) {
+        const double m = (j == i + 1) ? m1 : mem_of(j);
+        const bool ok = !(m > cap);
+        last_ok = ok ? j : last_ok;
+        fb = (!ok & (j < fb)) ? j : fb;
+      }
+      if (jx <= n) fb = min(fb, jx);
+      w = last_ok - i;
+      a.row_w[b0 + i] = w;
+      a.row_fb[b0 + i] = fb;
+    }
+    int wmax = rowv ? r + w : 0;
+    unsigned long long np = npriced;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+      np += __shfl_xor_sync(0xffffffffu, np, o);
+    }
+    if (lane == 0) {
+      a.blk_W[gb] = wmax + 1;
+      atomicAdd(&a.stats[s].priced, np);
+    }
+  }
+}
+
 // Pass B, fused grid costing with quantised candidates (I > 0): the lean
 // form of block_kernel<1, SRC, LAY>.  Every lane prices every column of its
 // warp's tile unconditionally and masks the result (no divergence in the
@@ -832,7 +947,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              double interval, int* row_w, int* row_fb, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
-                             cudaStream_t st) {
+                             double lo_thresh, int bisect, cudaStream_t st) {
   CostArgs a{g, tabT, tabM, in_d, tgt_d, pin, ptg, seg_off, blk_base, n_seg, total_blocks, max_n, mbp,
              cap, interval, row_w, row_fb, blk_W, stats, tile_off, seg_band_base, band, exit_thresh,
              small_bm, tau};
@@ -856,7 +971,23 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
     cudaFuncSetAttribute(band_kernel<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
     band_kernel<S, L><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                      \
   } while (0)
-  if (pass == 0) {
+#define PP_ROWEXIT_LAUNCH(S, L)                                                                        \
+  do {                                                                                                 \
+    const size_t smr = S == 0 ? grid_smem_layout(g.nm, g.ns, g.n_lay, 0).bytes : 0;                   \
+    cudaFuncSetAttribute(rowexit_kernel<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr); \
+    rowexit_kernel<S, L><<<blocks, 32 * kCostWarps, smr, st>>>(a, lo_thresh);                          \
+  } while (0)
+  if (pass == 0 && bisect && src != 2) {
+    if (src == 0) {
+      if (g.lay_class == kLayDec1) PP_ROWEXIT_LAUNCH(0, kLayDec1);
+      else if (g.lay_class == kLayEncDec2) PP_ROWEXIT_LAUNCH(0, kLayEncDec2);
+      else PP_ROWEXIT_LAUNCH(0, kLayGeneric);
+    } else {
+      if (g.lay_class == kLayDec1) PP_ROWEXIT_LAUNCH(1, kLayDec1);
+      else if (g.lay_class == kLayEncDec2) PP_ROWEXIT_LAUNCH(1, kLayEncDec2);
+      else PP_ROWEXIT_LAUNCH(1, kLayGeneric);
+    }
+  } else if (pass == 0) {
     if (src == 0) PP_COST_LAUNCH_L(0, 0); else if (src == 1) PP_COST_LAUNCH_L(0, 1); else PP_COST_LAUNCH(0, 2, 0);
   } else if (tau && src != 2) {
     if (src == 0) {
@@ -873,6 +1004,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
   }
 #undef PP_COST_LAUNCH_L
 #undef PP_BAND_LAUNCH
+#undef PP_ROWEXIT_LAUNCH
 #undef PP_COST_LAUNCH
   return cudaGetLastError();
 }
