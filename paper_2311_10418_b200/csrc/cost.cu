@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
 // column loop); act_mem is priced only where some lane of the warp reaches
 // its row's first infeasible slice (pass A), and candidate bins only leave
 // the two-compare fast path when a lane's slice time crosses into another bin.
-template <int SRC, int LAY>
+template <int SRC, int LAY, bool SIN>
 __global__ void __launch_bounds__(32 * kCostWarps)
     band_kernel(CostArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -554,6 +554,14 @@ __global__ void __launch_bounds__(32 * kCostWarps)
     const int i = i0 + r;
     const int wr = rowv ? a.row_w[b0 + i] : 0;  // 0: never live
     const int fb = (need_mem && rowv) ? a.row_fb[b0 + i] : INT_MAX;
+    // first tile column at which any row of the warp reaches its first
+    // infeasible slice: only from there on is act_mem priced (warp-uniform)
+    // (a lane needs it only when an infeasible slice lies INSIDE its feasible
+    // span, i.e. fb <= i + wr: act_mem not monotone along the row)
+    int cfb = (fb != INT_MAX && fb <= i + wr) ? fb - i0 : INT_MAX;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cfb = min(cfb, __shfl_xor_sync(0xffffffffu, cfb, o));
+    const double le = a.g.le, ld = a.g.ld, ival = a.interval;
     const int W = a.blk_W[gb];
     double* tile = a.band + a.seg_band_base[s] + a.tile_off[gb];
     tile[r] = QNAN;  // column 0: j = i0 <= i is never a slice
@@ -594,12 +602,20 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         const int j = i0 + c;
         const bool inrow = c > r;  // sample j-1 belongs to slice [i, j)
         const bool live = inrow & (c <= r + wr);
-        const double x = s_x[wid][q];
-        const AxisPos px = s_px[wid][q];
-        const bool upx = inrow & (pin < x);
-        pin = upx ? x : pin;
-        pe.t = upx ? px.t : pe.t;
-        pe.seg = upx ? px.seg : pe.seg;
+        if (SIN) {
+          // sorted by input: the padded input of [i, j) is max(0, in[j-1])
+          const AxisPos px = s_px[wid][q];
+          const bool pos = 0.0 < s_x[wid][q];
+          pe.t = pos ? px.t : p0.t;
+          pe.seg = pos ? px.seg : p0.seg;
+        } else {
+          const double x = s_x[wid][q];
+          const AxisPos px = s_px[wid][q];
+          const bool upx = inrow & (pin < x);
+          pin = upx ? x : pin;
+          pe.t = upx ? px.t : pe.t;
+          pe.seg = upx ? px.seg : pe.seg;
+        }
         if (encdec) {
           const double y = s_y[wid][q];
           const AxisPos py = s_py[wid][q];
@@ -613,13 +629,13 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         const double tsd = encdec ? pd.t : pe.t;
         double T, M;
         slice_cost_lay<LAY, true, false>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t, sd,
-                                         tsd, a.g.le, a.g.ld, T, M);
+                                         tsd, le, ld, T, M);
         bool ok = true;
-        const bool chk = live & (j >= fb);
-        if (__any_sync(0xffffffffu, chk)) {  // act_mem near the cap (rare)
+        if (c >= cfb) {  // act_mem near the cap: warp-uniform, rare
+          const bool chk = live & (j >= fb);
           double T2;
           slice_cost_lay<LAY, false, true>(tt, am, lay, n_lay, used, nm, ns, mb.seg, mb.t, pe.seg, pe.t,
-                                           sd, tsd, a.g.le, a.g.ld, T2, M);
+                                           sd, tsd, le, ld, T2, M);
           ok = !(chk & (M > a.cap));
         }
         const bool feas = live & ok;
@@ -633,7 +649,10 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         tlo = step ? thi : tlo;
         thi = step ? tnx : thi;
         win |= step ? (1ull << (kw - kb)) : 0ull;
-        if (step) tnx = (kw + 1 < kTau) ? tau[kw + 1] : INF;
+        {
+          const double nx = tau[min(kw + 1, kTau - 1)];  // unconditional: no branch
+          tnx = step ? ((kw + 1 < kTau) ? nx : INF) : tnx;
+        }
         const bool miss = feas & !((T > tlo) & (T <= thi));
         if (__any_sync(0xffffffffu, miss)) {
           if (miss) {
@@ -656,7 +675,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
               win |= 1ull << (k - kb);
               any_binned = true;
             } else {  // beyond the thresholds (or +inf): exact quantisation
-              const double qv = ceil(__ddiv_rn(T, a.interval));
+              const double qv = ceil(__ddiv_rn(T, ival));
               if (isinf(qv)) {
                 flags |= (qv > 0) ? 1 : 2;
               } else {
@@ -947,7 +966,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              double interval, int* row_w, int* row_fb, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
-                             double lo_thresh, int bisect, cudaStream_t st) {
+                             double lo_thresh, int bisect, int sorted_in, cudaStream_t st) {
   CostArgs a{g, tabT, tabM, in_d, tgt_d, pin, ptg, seg_off, blk_base, n_seg, total_blocks, max_n, mbp,
              cap, interval, row_w, row_fb, blk_W, stats, tile_off, seg_band_base, band, exit_thresh,
              small_bm, tau};
@@ -966,10 +985,15 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
     else if (g.lay_class == kLayEncDec2) PP_COST_LAUNCH(P, S, kLayEncDec2);      \
     else PP_COST_LAUNCH(P, S, kLayGeneric);                                      \
   } while (0)
-#define PP_BAND_LAUNCH(S, L)                                                                       \
-  do {                                                                                              \
-    cudaFuncSetAttribute(band_kernel<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
-    band_kernel<S, L><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                      \
+#define PP_BAND_LAUNCH2(S, L, Z)                                                                      \
+  do {                                                                                                 \
+    cudaFuncSetAttribute(band_kernel<S, L, Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
+    band_kernel<S, L, Z><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                      \
+  } while (0)
+#define PP_BAND_LAUNCH(S, L)                                 \
+  do {                                                       \
+    if (sorted_in) PP_BAND_LAUNCH2(S, L, true);              \
+    else PP_BAND_LAUNCH2(S, L, false);                       \
   } while (0)
 #define PP_ROWEXIT_LAUNCH(S, L)                                                                        \
   do {                                                                                                 \
@@ -1004,6 +1028,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
   }
 #undef PP_COST_LAUNCH_L
 #undef PP_BAND_LAUNCH
+#undef PP_BAND_LAUNCH2
 #undef PP_ROWEXIT_LAUNCH
 #undef PP_COST_LAUNCH
   return cudaGetLastError();

@@ -196,21 +196,22 @@ __device__ __forceinline__ void slice_cost_lay(const double4* __restrict__ tt,
   }
   const int per = nm * ns;
   const KindCost D = kind_cost<TIME, MEM>(tt + per, am + per, ns, mi, tm, sd, tsd);
+  // per_layer values are in [+0, +inf] (clamped), so L * x and sums of them
+  // are too (no NaN: L >= 1 is finite): max(0.0, .) of the first layout's
+  // value is the value itself
   if (LAY == kLayDec1) {
-    if (TIME) T = clamp0(__dadd_rn(__dmul_rn(ld, D.tf), __dmul_rn(ld, D.tb)));
-    if (MEM) M = clamp0(__dmul_rn(ld, D.act));
+    if (TIME) T = __dadd_rn(__dmul_rn(ld, D.tf), __dmul_rn(ld, D.tb));
+    if (MEM) M = __dmul_rn(ld, D.act);
   } else {
     const KindCost E = kind_cost<TIME, MEM>(tt, am, ns, mi, tm, se, tse);
     if (TIME) {
       const double t1 = __dadd_rn(__dmul_rn(le, E.tf), __dmul_rn(le, E.tb));
       const double t2 = __dadd_rn(__dmul_rn(ld, D.tf), __dmul_rn(ld, D.tb));
-      const double b1 = clamp0(t1);
-      T = (b1 < t2) ? t2 : b1;
+      T = (t1 < t2) ? t2 : t1;
     }
     if (MEM) {
       const double a1 = __dmul_rn(le, E.act), a2 = __dmul_rn(ld, D.act);
-      const double b1 = clamp0(a1);
-      M = (b1 < a2) ? a2 : b1;
+      M = (a1 < a2) ? a2 : a1;
     }
   }
 }
