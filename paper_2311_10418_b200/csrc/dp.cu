@@ -70,7 +70,7 @@ __device__ long long* g_dp_trace = nullptr;  // [block][16] clock64 stamps of CT
 constexpr int kNearCols = 64;
 constexpr int kChunkCols = 32;
 constexpr int kMaxRing = 24;
-constexpr int kNearBufs = 3;  // near tiles of blocks b and b+1 in use, b+2 in flight
+constexpr int kNearBufs = 2;  // near tile of block b in use, b+1 in flight
 constexpr uint32_t kColBytes = kRB * sizeof(double);  // 256 B
 constexpr size_t kChunkBytes = (size_t)kChunkCols * kColBytes;  // 8 KB
 
