@@ -161,7 +161,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
@@ -188,7 +188,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = W.CONFIGS[args.config]
-    M = args.per_gpu or {"C3": 296, "C4": 1024, "C1": 1024, "C2": 128, "C5": 1}.get(cfg.name, 8)
+    M = args.per_gpu or {"C3": 592, "C4": 1024, "C1": 1024, "C2": 128, "C5": 1}.get(cfg.name, 8)
     steps, warm = args.steps, args.warmup
     n = cfg.n
     # distinct mini-batches for every (rank, step): rank r owns groups
