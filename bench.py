@@ -96,6 +96,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def traffic_record(config_name):
+    """Latest profiles/r*/traffic_<config>.json (per-plan DRAM bytes per kernel
+    from an ncu --set full capture), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"traffic_{config_name.lower()}.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        return json.load(f)
+
+
 def cpu_baseline_sample(cfg, threads, plans):
     """The unmodified reference (oracle/_ref) on the host cores: `plans`
     8192-seq mini-batches (one per thread) through order_samples +
@@ -304,14 +315,13 @@ def main():
         names = capi.KERNEL_NAMES
         kl = W.kind_layouts(cfg)  # (layout, kind) pairs priced per slice
         # algorithmic work per launch category:
-        #   pass A: act_mem per (layout, kind): 3 bilinear blends x 3 FP64 ops + scale + add = 11
-        #   pass B: time 2 x 9 + 2 + 2 + 1 = 23 and act_mem 11 per (layout, kind), + 1 candidate divide
+        #   pass A: act_mem per (layout, kind): 3 bilinear blends (differences precomputed):
+        #           7 FP64 ops + scale = 8 ... counted as 11 with the clamp/compare
+        #   pass B: slice time per (layout, kind): 2 blends x 7 + 2 DMUL + 1 DADD = 17 FP64 ops
         #   DP: one 8-byte band entry streamed per transition
-        capped = math.isfinite(cfg.mem_cap)
         work = {
-            2: ("fp64", agg["sl_a"] * 11 * kl, "11 FP64 ops per act_mem slice per (layout, kind)"),
-            3: ("fp64", agg["sl_b"] * ((23 + (11 if capped else 0)) * kl + 1),
-                f"{(23 + (11 if capped else 0)) * kl + 1} FP64 ops per band slice"),
+            2: ("fp64", agg["sl_a"] * 11 * kl, "11 FP64 ops per act_mem pricing per (layout, kind)"),
+            3: ("fp64", agg["sl_b"] * 17 * kl, f"{17 * kl} FP64 ops per band slice"),
             4: ("hbm", agg["bound_tr"] * 8, "8 B band entry per transition"),
             5: ("hbm", (agg["tr"] - agg["bound_tr"]) * 8, "8 B band entry per transition"),
         }
@@ -332,6 +342,16 @@ def main():
 
         dom = max(work, key=lambda c: kern[c])
         roof = roof_of(dom)
+        # DRAM traffic of the dominant kernel from the committed ncu --set full
+        # capture (profiles/<round>/traffic_<config>.json), per launch
+        tr = traffic_record(cfg.name)
+        if tr and names[dom] in tr["kernels"]:
+            per_plan = tr["kernels"][names[dom]]["dram_bytes_per_plan"]
+            plans_per_launch = M / max(args.streams, 1)
+            roof["traffic"] = per_plan * plans_per_launch
+            roof["traffic_source"] = tr["source"]
+            if work[dom][0] == "hbm":
+                roof["traffic_vs_algorithmic"] = per_plan * M * steps / max(work[dom][1], 1)
         roof["all"] = {names[c]: {k: roof_of(c)[k] for k in ("bound", "achieved", "unit", "frac",
                                                              "share_of_step")}
                        for c in work if kern[c] > 0}
