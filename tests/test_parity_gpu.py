@@ -318,3 +318,52 @@ def test_concurrent_sub_batches_match_single_stream():
     assert_plan_matches(got, case["expect"], "C3 split")
     a.close()
     b.close()
+
+
+def test_presorted_arbitrary_order_matches_oracle(planner, orc):
+    """dp_partition(span) on the caller's order (no sort): running maxima of
+    the padded lengths over unsorted spans, certified scan (no bisection)."""
+    grid = capi.synthetic_grid()
+    rng = np.random.default_rng(31)
+    for k in range(10):
+        n = int(rng.integers(2, 600))
+        encdec = bool(k % 2)
+        s = capi.synthetic_dataset(n, 8192, 500 + k, W.INPUT_DIST, W.T5_TARGET_DIST if encdec else None)
+        s = s[rng.permutation(n)]
+        model = capi.Model.uniform(4, 2, encdec)
+        acts = [orc.slice_cost(grid, model, s, i, i + 1)[1] for i in range(n)]
+        cap = float(rng.choice([math.inf, 3.0 * max(acts)]))
+        interval = float(rng.choice([0.0, 1000.0, 50000.0]))
+        a = orc.plan(s, grid, model, 4, 1, cap, interval, presorted=True)
+        b = _plan_or_status(lambda: planner.plan(s, grid, model, 4, 1, cap, interval, presorted=True))
+        assert_plan_matches(b, record(a), f"presorted {k}")
+
+
+def test_exact_candidate_set_c2_scale(planner, orc):
+    """t_max_interval = 0 (the exact candidate set: segmented u64 sort +
+    unique of every feasible slice time) on a BASELINE-C2-sized T5 batch."""
+    cfg = W.CONFIGS["C2"]
+    s = W.dataset(cfg, 1)
+    a = orc.plan(s, W.grid(), W.model(cfg), cfg.stages, 1, math.inf, 0.0)
+    b = planner.plan(s, W.grid(), W.model(cfg), cfg.stages, 1, math.inf, 0.0)
+    assert_plan_matches(b, record(a), "C2 exact")
+
+
+def test_replicas_and_capped_t5(planner, orc):
+    """D > 1 (balance_replicas on the host, bound / objective divided by D)
+    and a binding cap on an encoder-decoder model (scan pass A, target
+    running maxima)."""
+    grid = capi.synthetic_grid()
+    rng = np.random.default_rng(41)
+    for k in range(6):
+        n = int(rng.integers(50, 900))
+        s = capi.synthetic_dataset(n, 8192, 600 + k, W.INPUT_DIST, W.T5_TARGET_DIST)
+        model = capi.Model.uniform(8, 2, True)
+        o = orc.order_samples(s)
+        acts = [orc.slice_cost(grid, model, o, i, i + 1)[1] for i in range(n)]
+        cap = float(max(acts) * rng.choice([1.5, 4.0]))
+        d = int(rng.integers(2, 5))
+        interval = float(rng.choice([0.0, 2000.0]))
+        a = orc.plan(s, grid, model, 8, d, cap, interval)
+        b = _plan_or_status(lambda: planner.plan(s, grid, model, 8, d, cap, interval))
+        assert_plan_matches(b, record(a), f"D={d} T5 cap {k}")
