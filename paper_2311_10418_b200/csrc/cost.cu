@@ -58,7 +58,7 @@ __global__ void mbs_bracket_kernel(CostGrid g, int max_n, AxisPos* __restrict__ 
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m <= max_n; m += gridDim.x * blockDim.x) {
     AxisPos p;
     bracket(g.mbs_ax, g.nm, (double)m, p.seg, p.t);
-    p.pad = 0;
+    p.pad = p.seg * g.ns;  // row base of the cell table (band_kernel)
     out[m] = p;
   }
 }
@@ -495,6 +495,239 @@ __global__ void __launch_bounds__(32 * kCostWarps)
   }
 }
 
+// Cells of the cost grid the lean band kernel keeps in STATIC shared memory
+// (statically shared addresses: plain LDS with immediate offsets, no generic
+// address conversion in the loop); larger grids take band_kernel.
+constexpr int kBandCells = 512;  // 2 kinds x 256 (mbs x seq) cells: 24 KB
+
+// Pass B, quantised candidates (I > 0), grid staged in static shared memory:
+// the leanest column loop.  ENC: encoder-decoder model (decoder reads the
+// target length; its running maximum is tracked).  SIN: segments sorted by
+// input length (padded input = max(0, in[j-1]), no running maximum).
+// Candidate bins: a lane's slice times grow along its row, so the bins it
+// hits through the fast path form a contiguous run [run_lo, kw]; runs are
+// written to the warp's bitmap only when they end (a miss or the block end).
+template <int LAY, bool SIN, bool ENC>
+__global__ void __launch_bounds__(32 * kCostWarps)
+    band3_kernel(CostArgs a) {
+  __shared__ double4 s_tt[kBandCells];
+  __shared__ double2 s_am[kBandCells];
+  __shared__ double s_tau[kSmallBmWords * 32];
+  __shared__ double s_x[kCostWarps][32], s_y[kCostWarps][32];
+  __shared__ AxisPos s_px[kCostWarps][32], s_py[kCostWarps][32];
+  __shared__ AxisPos s_mb[kCostWarps][64];
+  __shared__ unsigned int s_bm[kCostWarps][kSmallBmWords];
+  const int nm = a.g.nm, ns = a.g.ns;
+  {
+    const int cells = 2 * nm * ns;
+    for (int k = threadIdx.x; k < cells; k += blockDim.x) {
+      s_tt[k] = a.g.tt[k];
+      s_am[k] = a.g.am[k];
+    }
+    for (int k = threadIdx.x; k < kSmallBmWords * 32; k += blockDim.x) s_tau[k] = a.tau[k];
+    __syncthreads();
+  }
+  const int per = nm * ns;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warps = gridDim.x * kCostWarps;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
+  const bool need_mem = !(a.cap == INF);
+  constexpr int kTau = kSmallBmWords * 32;
+  const double le = a.g.le, ld = a.g.ld, ival = a.interval, cap = a.cap;
+  AxisPos p0{0.0, 0, 0};
+  bracket(a.g.seq_ax, ns, 0.0, p0.seg, p0.t);
+  // one kind's (t_f, t_b) at cell row mb (mi * ns) and sequence segment sg
+  auto kind_time = [&](int base, int mb, double tm, int sg, double ts, double& tf, double& tb) {
+    const int s1 = min(sg + 1, ns - 1);
+    const double4 c0 = s_tt[base + mb + sg], c1 = s_tt[base + mb + s1];
+    tf = blend_d(tm, ts, c0.x, c0.z, c1.x, c1.z);
+    tb = blend_d(tm, ts, c0.y, c0.w, c1.y, c1.w);
+  };
+  auto kind_mem = [&](int base, int mb, double tm, int sg, double ts) {
+    const int s1 = min(sg + 1, ns - 1);
+    const double2 c0 = s_am[base + mb + sg], c1 = s_am[base + mb + s1];
+    return blend_d(tm, ts, c0.x, c0.y, c1.x, c1.y);
+  };
+  // bits [lo, hi] of the warp's bin bitmap
+  auto mark_run = [&](int lo, int hi) {
+    for (int w = lo >> 5; w <= (hi >> 5); ++w) {
+      const int b_lo = max(lo - 32 * w, 0), b_hi = min(hi - 32 * w, 31);
+      const unsigned int m = (b_hi == 31 ? 0xffffffffu : ((1u << (b_hi + 1)) - 1u)) & ~((1u << b_lo) - 1u);
+      atomicOr(&s_bm[wid][w], m);
+    }
+  };
+  for (int gb = blockIdx.x * kCostWarps + wid; gb < a.total_blocks; gb += warps) {
+    const int s = seg_of(a.blk_base, a.n_seg, gb);
+    const int64_t b0 = a.seg_off[s];
+    const int n = (int)(a.seg_off[s + 1] - b0);
+    const int bl = gb - a.blk_base[s];
+    const int i1 = n - kRB * bl;
+    const int i0 = max(0, i1 - kRB);
+    const int r = lane;
+    const bool rowv = r < i1 - i0;
+    const int i = i0 + r;
+    const int wr = rowv ? a.row_w[b0 + i] : 0;  // 0: never live
+    const int fb = (need_mem && rowv) ? a.row_fb[b0 + i] : INT_MAX;
+    int cfb = (fb != INT_MAX && fb <= i + wr) ? fb - i0 : INT_MAX;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cfb = min(cfb, __shfl_xor_sync(0xffffffffu, cfb, o));
+    const int W = a.blk_W[gb];
+    double* tile = a.band + a.seg_band_base[s] + a.tile_off[gb];
+    tile[r] = QNAN;  // column 0: j = i0 <= i is never a slice
+    double pin = 0.0, ptg = 0.0;
+    AxisPos pe = p0, pd = p0;
+    int kw = -1, run_lo = -1;
+    double tlo = INF, thi = -INF, tnx = -INF;
+    double kmn = INF, kmx = -INF;
+    int flags = 0;
+    unsigned int npriced = 0;
+    if (lane < kSmallBmWords) s_bm[wid][lane] = 0u;
+    __syncwarp();
+    for (int c0 = 1; c0 < W; c0 += 32) {
+      const int cq = c0 + lane;
+      if (cq < W) {
+        const int64_t k = b0 + i0 + cq - 1;
+        s_x[wid][lane] = a.in_d[k];
+        s_px[wid][lane] = a.pin[k];
+        if (ENC) {
+          s_y[wid][lane] = a.tgt_d[k];
+          s_py[wid][lane] = a.ptg[k];
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = lane + 32 * h;
+        s_mb[wid][p] = a.mbp[min(max(c0 - 32 + p, 1), a.max_n)];
+      }
+      __syncwarp();
+      const int qend = min(32, W - c0);
+      for (int q = 0; q < qend; ++q) {
+        const int c = c0 + q;
+        const bool inrow = c > r;  // sample j-1 belongs to slice [i, j)
+        const bool live = inrow & (c <= r + wr);
+        if (SIN) {
+          const AxisPos px = s_px[wid][q];
+          const bool pos = 0.0 < s_x[wid][q];
+          pe.t = pos ? px.t : p0.t;
+          pe.seg = pos ? px.seg : p0.seg;
+        } else {
+          const double x = s_x[wid][q];
+          const AxisPos px = s_px[wid][q];
+          const bool upx = inrow & (pin < x);
+          pin = upx ? x : pin;
+          pe.t = upx ? px.t : pe.t;
+          pe.seg = upx ? px.seg : pe.seg;
+        }
+        if (ENC) {
+          const double y = s_y[wid][q];
+          const AxisPos py = s_py[wid][q];
+          const bool upy = inrow & (ptg < y);
+          ptg = upy ? y : ptg;
+          pd.t = upy ? py.t : pd.t;
+          pd.seg = upy ? py.seg : pd.seg;
+        }
+        const AxisPos mb = s_mb[wid][q - r + 32];
+        const int sd = ENC ? pd.seg : pe.seg;
+        const double tsd = ENC ? pd.t : pe.t;
+        double T;
+        {
+          double df, db;
+          kind_time(per, mb.pad, mb.t, sd, tsd, df, db);
+          const double t2 = __dadd_rn(__dmul_rn(ld, df), __dmul_rn(ld, db));
+          if (LAY == kLayDec1) {
+            T = t2;
+          } else {  // kLayEncDec2
+            double ef, eb;
+            kind_time(0, mb.pad, mb.t, pe.seg, pe.t, ef, eb);
+            const double t1 = __dadd_rn(__dmul_rn(le, ef), __dmul_rn(le, eb));
+            T = (t1 < t2) ? t2 : t1;
+          }
+        }
+        bool ok = true;
+        if (c >= cfb) {  // act_mem near the cap: warp-uniform, rare
+          const bool chk = live & (i0 + c >= fb);
+          double M = __dmul_rn(ld, kind_mem(per, mb.pad, mb.t, sd, tsd));
+          if (LAY != kLayDec1) {
+            const double a1 = __dmul_rn(le, kind_mem(0, mb.pad, mb.t, pe.seg, pe.t));
+            M = (a1 < M) ? M : a1;
+          }
+          ok = !(chk & (M > cap));
+        }
+        const bool feas = live & ok;
+        tile[(size_t)c * kRB + r] = feas ? T : QNAN;
+        npriced += live ? 1u : 0u;
+        // bin fast path: same bin, or the next one
+        const bool step = feas & (T > thi) & (T <= tnx) & (kw + 1 < kTau);
+        kw += step ? 1 : 0;
+        tlo = step ? thi : tlo;
+        thi = step ? tnx : thi;
+        {
+          const double nx = s_tau[min(kw + 1, kTau - 1)];
+          tnx = step ? ((kw + 1 < kTau) ? nx : INF) : tnx;
+        }
+        const bool miss = feas & !((T > tlo) & (T <= thi));
+        if (__any_sync(0xffffffffu, miss)) {
+          if (miss) {
+            if (run_lo >= 0) mark_run(run_lo, kw);
+            run_lo = -1;
+            int k = max(kw, 0);
+            while (k < kTau && !(T <= s_tau[k])) ++k;
+            while (k > 0 && T <= s_tau[k - 1]) --k;
+            if (k < kTau) {
+              kw = k;
+              run_lo = k;
+              tlo = k > 0 ? s_tau[k - 1] : -INF;
+              thi = s_tau[k];
+              tnx = (k + 1 < kTau) ? s_tau[k + 1] : INF;
+            } else {  // beyond the thresholds (or +inf): exact quantisation
+              const double qv = ceil(__ddiv_rn(T, ival));
+              if (isinf(qv)) {
+                flags |= (qv > 0) ? 1 : 2;
+              } else {
+                kmn = (qv < kmn) ? qv : kmn;
+                kmx = (kmx < qv) ? qv : kmx;
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (run_lo >= 0) mark_run(run_lo, kw);
+    const bool any_binned = __any_sync(0xffffffffu, kw >= 0);
+    if (any_binned) {  // binned values lie in [0, kTau): widen the range to a superset
+      kmn = (0.0 < kmn) ? 0.0 : kmn;
+      kmx = (kmx < (double)(kTau - 1)) ? (double)(kTau - 1) : kmx;
+    }
+    unsigned long long np = npriced;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, kmn, o);
+      const double y = __shfl_xor_sync(0xffffffffu, kmx, o);
+      kmn = (x < kmn) ? x : kmn;
+      kmx = (kmx < y) ? y : kmx;
+      np += __shfl_xor_sync(0xffffffffu, np, o);
+      flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&a.stats[s].priced_b, np);
+      if (np) atomicAdd(&a.stats[s].nraw, np);  // >= the raw count; only sizes the raw fallback
+      if (!isinf(kmn)) {
+        atomicMin(&a.stats[s].kmin, dkey(kmn));
+        atomicMax(&a.stats[s].kmax, dkey(kmx));
+      }
+      if (flags) atomicOr(&a.stats[s].flags, flags);
+    }
+    __syncwarp();
+    if (lane < kSmallBmWords) {
+      const unsigned int w = s_bm[wid][lane];
+      if (w) atomicOr(&a.small_bm[(size_t)s * kSmallBmWords + lane], w);
+    }
+    __syncwarp();
+  }
+}
+
 // Pass B, fused grid costing with quantised candidates (I > 0): the lean
 // form of block_kernel<1, SRC, LAY>.  Every lane prices every column of its
 // warp's tile unconditionally and masks the result (no divergence in the
@@ -597,6 +830,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
       }
       __syncwarp();
       const int qend = min(32, W - c0);
+#pragma unroll 2
       for (int q = 0; q < qend; ++q) {
         const int c = c0 + q;
         const int j = i0 + c;
@@ -644,7 +878,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         // candidate bin k = ceil(fl(T / I)) = min{k : T <= tau[k]} (microbatch.cpp:264).
         // Fast path, branch-free: same bin, or the next one (slice times grow
         // along a row).
-        const bool step = feas & (T > thi) & (T <= tnx) & (kw + 1 < kb + 64);
+        const bool step = feas & (T > thi) & (T <= tnx) & (kw + 1 < kb + 64) & (kw + 1 < kTau);
         kw = step ? kw + 1 : kw;
         tlo = step ? thi : tlo;
         thi = step ? tnx : thi;
@@ -1013,6 +1247,19 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
     }
   } else if (pass == 0) {
     if (src == 0) PP_COST_LAUNCH_L(0, 0); else if (src == 1) PP_COST_LAUNCH_L(0, 1); else PP_COST_LAUNCH(0, 2, 0);
+  } else if (tau && src != 2 && 2 * g.nm * g.ns <= kBandCells &&
+             (g.lay_class == kLayDec1 || g.lay_class == kLayEncDec2)) {
+#define PP_BAND3(L, Z, E)                                              \
+  band3_kernel<L, Z, E><<<blocks, 32 * kCostWarps, 0, st>>>(a)
+    const bool enc = g.is_encdec != 0;
+    if (g.lay_class == kLayDec1) {
+      if (sorted_in) { if (enc) PP_BAND3(kLayDec1, true, true); else PP_BAND3(kLayDec1, true, false); }
+      else { if (enc) PP_BAND3(kLayDec1, false, true); else PP_BAND3(kLayDec1, false, false); }
+    } else {
+      if (sorted_in) { if (enc) PP_BAND3(kLayEncDec2, true, true); else PP_BAND3(kLayEncDec2, true, false); }
+      else { if (enc) PP_BAND3(kLayEncDec2, false, true); else PP_BAND3(kLayEncDec2, false, false); }
+    }
+#undef PP_BAND3
   } else if (tau && src != 2) {
     if (src == 0) {
       if (g.lay_class == kLayDec1) PP_BAND_LAUNCH(0, kLayDec1);

@@ -367,3 +367,16 @@ def test_replicas_and_capped_t5(planner, orc):
         a = orc.plan(s, grid, model, 8, d, cap, interval)
         b = _plan_or_status(lambda: planner.plan(s, grid, model, 8, d, cap, interval))
         assert_plan_matches(b, record(a), f"D={d} T5 cap {k}")
+
+
+def test_candidate_bins_past_the_threshold_table(planner, orc):
+    """Slice times far beyond the 256 binned candidates (I = 5, the paper's
+    interval): every bin past the threshold table takes the exact-division
+    path; batches of heavy-tailed lengths up to 8192 tokens."""
+    grid = capi.synthetic_grid()
+    for k, L in enumerate([512, 8192]):
+        s = capi.synthetic_dataset(700, L, 77 + k, (capi.LOGNORMAL, 4.0, 2.0, 1, 1, 0.8))
+        model = capi.Model.uniform(4, 2, False)
+        a = orc.plan(s, grid, model, 4, 1, math.inf, 5.0)
+        b = planner.plan(s, grid, model, 4, 1, math.inf, 5.0)
+        assert_plan_matches(b, record(a), f"I=5 L={L}")
