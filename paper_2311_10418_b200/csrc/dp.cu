@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         npm[o] = m1;
       }
     }
-    // ---- the chain warp meanwhile loads its own tile and far-far partial
+    // ---- the chain warp meanwhile loads its far-far partial, waits for its tile
     const int W = blk_W[gb0 + b];
     const int r = lane;
     double as = INF, am = INF;
@@ -387,8 +387,11 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         for (int jj = kRB - 1; jj >= 0; --jj)
           if (jj < nb) tri_step(jj);
       }
+      // near tile of block b consumed: order this warp's generic-proxy reads
+      // before the producer's next async-proxy (TMA) write into the buffer
+      fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);  // near tile of block b consumed
+      if (lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);
       PP_TRACE(3);
       if (r < nb) {
         const int row = i0 + r;
@@ -449,6 +452,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
               m_ = (ok & (x < INF) & (mj < INF) & (v < m_)) ? v : m_;
             }
           }
+          fence_proxy_async();  // generic reads before the next TMA write of the slot
           __syncwarp();
           if (lane == 0) mbar_arrive(&ring_empty[cslot]);  // this warp is done with the chunk
           if (++cslot == kRing) {
