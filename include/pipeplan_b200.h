@@ -97,7 +97,10 @@ typedef struct pp_tuning {
                               sub-batches planned concurrently on their own streams
                               and host threads (one sub-batch's latency-bound DP
                               overlaps another's cost passes); 0/1 = one stream */
-  int32_t reserved[5];
+  int32_t coop_min_n;      /* a DP launch of <= 8 passes whose mini-batches all have at
+                              least this many samples runs each pass as one cooperative
+                              kernel over the whole GPU; 0 = default (16384) */
+  int32_t reserved[4];
 } pp_tuning;
 
 /* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are

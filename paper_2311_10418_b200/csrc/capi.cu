@@ -86,6 +86,13 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int64_t* seg_band_base, const double* band, const double* cand,
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, cudaStream_t st);
+size_t dp_coop_parts_bytes(int grid);
+int dp_coop_grid(int device);
+cudaError_t launch_dp_coop(int mode, int sanitize, const WorkItem& it, int grid, const int64_t* seg_off,
+                           const int* blk_base, const int* blk_W, const int64_t* tile_off,
+                           const int64_t* seg_band_base, const double* band, const double* cand,
+                           const int64_t* cand_off, ItemResult* res, int res_slot, int* next_buf,
+                           double* gstate, void* parts, cudaStream_t st);
 cudaError_t launch_seg_init(const ItemResult* bound_res, int has_bound, int replicas,
                             const int64_t* cand_off, const int* cand_n, const double* cand,
                             const int* active, SegDP* dp, int n_seg, cudaStream_t st);
@@ -172,7 +179,7 @@ struct pp_ctx {
       bound_items, bound_res;
   DevBuf out_splits, out_times, out_count, out_tmax, out_obj, out_status, out_err;
   PinBuf h_range, h_stats, h_segdp;
-  DevBuf small_bm;
+  DevBuf small_bm, coop_state, coop_parts;
   // host copy of the uploaded grid (restricted to the recompute strategy)
   // for the monotonicity certificate of cost pass A
   std::vector<double> h_ax, h_cells;
@@ -196,7 +203,7 @@ struct pp_ctx {
             &raw_cnt, &raw_in_tmp, &cand, &cand_off, &cand_n, &active, &items, &results, &next_buf,
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
             &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
-            &small_bm};
+            &small_bm, &coop_state, &coop_parts};
   }
 };
 
@@ -713,6 +720,39 @@ void place_states(std::vector<WorkItem>& items, int mode, size_t& smem_state, in
   }
 }
 
+// A DP launch over few, very long mini-batches (C5: 65,536 samples, rows up
+// to n wide) runs each pass as one cooperative kernel over the whole GPU
+// (dp_coop.cu) instead of one CTA per pass.
+constexpr int kCoopMinN = 16384;
+constexpr int kCoopMaxItems = 8;
+
+bool use_coop(const pp_ctx* ctx, const std::vector<WorkItem>& items, const int64_t* h_seg_off) {
+  if (items.empty() || (int)items.size() > kCoopMaxItems) return false;
+  const int64_t min_n = ctx->tuning.coop_min_n > 0 ? ctx->tuning.coop_min_n : kCoopMinN;
+  for (const WorkItem& w : items)
+    if (h_seg_off[w.seg + 1] - h_seg_off[w.seg] < min_n) return false;
+  return true;
+}
+
+int run_coop(pp_ctx* ctx, int mode, int sanitize, const std::vector<WorkItem>& items, const PlanCall& c,
+             ItemResult* res, int res_by_seg, cudaStream_t st) {
+  const int grid = dp_coop_grid(ctx->device);
+  int64_t nmax = 0;
+  for (const WorkItem& w : items) nmax = std::max<int64_t>(nmax, c.h_seg_off[w.seg + 1] - c.h_seg_off[w.seg]);
+  PP_CUDA(ctx->coop_state.ensure((size_t)2 * (nmax + 1) * sizeof(double)));
+  PP_CUDA(ctx->coop_parts.ensure(dp_coop_parts_bytes(grid)));
+  for (size_t k = 0; k < items.size(); ++k) {
+    WorkItem w = items[k];
+    w.state_off = 0;  // passes run one after another on the stream: one state array
+    PP_CUDA(launch_dp_coop(mode, sanitize, w, grid, c.d_seg_off, ctx->blk_base.as<int>(), ctx->blk_W.as<int>(),
+                           ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(), ctx->band.as<double>(),
+                           ctx->cand.as<double>(), ctx->cand_off.as<int64_t>(), res,
+                           res_by_seg ? w.seg : (int)k, ctx->next_buf.as<int>(), ctx->coop_state.as<double>(),
+                           ctx->coop_parts.p, st));
+  }
+  return PP_OK;
+}
+
 // The planning pipeline (steps 1-7 above).
 int run_plan(pp_ctx* ctx, const PlanCall& c) {
   cudaStream_t st = ctx->stream;
@@ -882,12 +922,19 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       PP_CUDA(ctx->next_buf.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
       PP_CUDA(cudaMemcpyAsync(ctx->bound_items.p, bi.data(), bi.size() * sizeof(WorkItem),
                               cudaMemcpyHostToDevice, st));
-      PP_TIMED(4, launch_dp_pass(1, ctx->bound_items.as<WorkItem>(), (int)bi.size(), smem_state,
-                                 state_global, table ? 1 : 0, dp_budget((int)bi.size()), c.d_seg_off,
-                                 ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
-                                 ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
-                                 ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
-                                 ctx->gstate.as<double>(), 1, st));
+      if (use_coop(ctx, bi, c.h_seg_off)) {
+        PP_CUDA(timed_begin(ctx, 4));
+        int rc = run_coop(ctx, 1, table ? 1 : 0, bi, c, ctx->bound_res.as<ItemResult>(), 1, st);
+        if (rc) return rc;
+        PP_CUDA(timed_end(ctx));
+      } else {
+        PP_TIMED(4, launch_dp_pass(1, ctx->bound_items.as<WorkItem>(), (int)bi.size(), smem_state,
+                                   state_global, table ? 1 : 0, dp_budget((int)bi.size()), c.d_seg_off,
+                                   ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
+                                   ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
+                                   ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
+                                   ctx->gstate.as<double>(), 1, st));
+      }
       PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
     }
   }
@@ -943,11 +990,18 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(cudaMemcpyAsync(ctx->items.p, items.data(), ni * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_start.p, item_start.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_cnt.p, item_cnt.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
-    PP_TIMED(5, launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_state, state_global, table ? 1 : 0,
-                               dp_budget(ni), c.d_seg_off, ctx->blk_base.as<int>(),
-                               ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
-                               ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
-                               ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, st));
+    if (use_coop(ctx, items, c.h_seg_off)) {
+      PP_CUDA(timed_begin(ctx, 5));
+      int rc = run_coop(ctx, 0, table ? 1 : 0, items, c, ctx->results.as<ItemResult>(), 0, st);
+      if (rc) return rc;
+      PP_CUDA(timed_end(ctx));
+    } else {
+      PP_TIMED(5, launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_state, state_global, table ? 1 : 0,
+                                 dp_budget(ni), c.d_seg_off, ctx->blk_base.as<int>(),
+                                 ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
+                                 ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
+                                 ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, st));
+    }
     PP_TIMED(7, launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
                               ctx->seg_item_start.as<int>(), ctx->seg_item_cnt.as<int>(),
                               ctx->next_buf.as<int>(), ctx->best_next.as<int>(), c.d_seg_off, d_cand,

@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
 // Cells of the cost grid the lean band kernel keeps in STATIC shared memory
 // (statically shared addresses: plain LDS with immediate offsets, no generic
 // address conversion in the loop); larger grids take band_kernel.
-constexpr int kBandCells = 512;  // 2 kinds x 256 (mbs x seq) cells: 24 KB
+constexpr int kBandCells = 384;  // 2 kinds x 192 (mbs x seq) cells: 18 KB
 
 // Pass B, quantised candidates (I > 0), grid staged in static shared memory:
 // the leanest column loop.  ENC: encoder-decoder model (decoder reads the

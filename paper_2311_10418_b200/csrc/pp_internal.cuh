@@ -17,7 +17,7 @@ constexpr int kWarp = 32;
 constexpr int kMaxLayouts = 64;  // distinct (encoder, decoder) layer layouts
 // Candidate bins k = ceil(T / I) < 32 * kSmallBmWords are marked directly by
 // cost pass B into a per-segment bitmap (segment mode 3, capi.cu).
-constexpr int kSmallBmWords = 8;
+constexpr int kSmallBmWords = 16;
 
 // One distinct stage layout as FP64 layer multiples (0 = kind absent).
 // Stages with equal layouts yield equal costs and max() over equal values is

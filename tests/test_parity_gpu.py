@@ -380,3 +380,59 @@ def test_candidate_bins_past_the_threshold_table(planner, orc):
         a = orc.plan(s, grid, model, 4, 1, math.inf, 5.0)
         b = planner.plan(s, grid, model, 4, 1, math.inf, 5.0)
         assert_plan_matches(b, record(a), f"I=5 L={L}")
+
+
+def test_cooperative_dp_pass_matches_oracle(orc):
+    """The whole-GPU cooperative DP pass (dp_coop.cu, used for very long
+    mini-batches such as C5), forced onto small mini-batches with
+    coop_min_n, against the C restatement: capped and uncapped, GPT and T5,
+    quantised and exact candidate sets, and the table path."""
+    p = capi.Planner(0)
+    p.set_tuning(coop_min_n=1)
+    grid = capi.synthetic_grid()
+    rng = np.random.default_rng(57)
+    for k in range(8):
+        n = int(rng.integers(40, 700))
+        encdec = bool(k % 2)
+        s = capi.synthetic_dataset(n, 8192, 800 + k, W.INPUT_DIST, W.T5_TARGET_DIST if encdec else None)
+        model = capi.Model.uniform(4, 2, encdec)
+        o = orc.order_samples(s)
+        acts = [orc.slice_cost(grid, model, o, i, i + 1)[1] for i in range(n)]
+        cap = float(rng.choice([math.inf, 3.0 * max(acts)]))
+        interval = float(rng.choice([0.0, 500.0, 20000.0]))
+        a = orc.plan(s, grid, model, 4, 1, cap, interval)
+        b = _plan_or_status(lambda: p.plan(s, grid, model, 4, 1, cap, interval))
+        assert_plan_matches(b, record(a), f"coop {k}")
+    for case in load_golden("toy")[:40]:
+        T, M = toy_tables(case["lens"], case["mem_per_sample"], case["heavy"])
+        got = _plan_or_status(lambda: p.plan_tables(
+            T, M, len(case["lens"]), case["stage_count"], case["replica_count"],
+            unhex(case["mem_cap"]), unhex(case["t_max_interval"])))
+        assert_plan_matches(got, case["expect"], "coop " + case["name"])
+    p.close()
+
+
+@pytest.mark.timeout(900)
+def test_c5_long_tail_full_scale():
+    """BASELINE config C5 (65,536 T5 sequences up to 65,536 tokens, no cap,
+    256 candidates) at full scale — the reference needs ~9 h, so parity here
+    is (a) the whole-GPU cooperative DP against the one-CTA DP kernel, two
+    independent device implementations of run_suffix_dp, bit for bit, and
+    (b) plan invariants: splits partition [0, n), every micro-batch time is
+    at most t_max_used, objective == eval_objective(times)."""
+    cfg = W.CONFIGS["C5"]
+    s = W.dataset(cfg, 1)
+    coop = capi.Planner(0)
+    single = capi.Planner(0)
+    single.set_tuning(coop_min_n=1 << 30)  # never cooperative
+    a = coop.plan(s, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    b = single.plan(s, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    assert np.array_equal(a.splits, b.splits)
+    assert a.mb_times.tobytes() == b.mb_times.tobytes()
+    assert a.t_max_used == b.t_max_used and a.objective == b.objective
+    sp = a.splits
+    assert sp[-1] == cfg.n and np.all(np.diff(np.concatenate([[0], sp])) > 0)
+    assert np.all(a.mb_times <= a.t_max_used)
+    assert a.objective == capi.eval_objective(a.mb_times, cfg.stages, 1)
+    coop.close()
+    single.close()
