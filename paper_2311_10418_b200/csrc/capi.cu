@@ -29,6 +29,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <string>
 #include <thread>
 #include <vector>
@@ -1297,16 +1298,18 @@ int pp_plan_grid_device(pp_ctx* ctx, const pp_sample* d_samples, const int64_t* 
   return run_plan(ctx, c);
 }
 
-int pp_plan_grid(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets, int32_t n_seg,
-                 int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
-                 const pp_dp_options* opts, pp_plan_out* out) {
-  int rc = check_ctx(ctx);
-  if (rc) return rc;
-  if (!samples || !seg_offsets || n_seg < 1 || !opts || !out)
-    return fail(ctx, PP_ERR_INVALID, "bad arguments");
-  if ((rc = validate_opts(ctx, *opts))) return rc;
+}  // extern "C"
+
+namespace {
+
+// One host-buffer planning call on one context: stage the samples, plan on
+// the device, copy the plans back (caller's buffers), synchronise.
+int plan_host(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets, int32_t n_seg,
+              int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
+              const pp_dp_options* opts, const pp_plan_out* out) {
   const int64_t total = seg_offsets[n_seg];
   cudaStream_t st = ctx->stream;
+  int rc;
   if ((rc = stage_inputs(ctx, samples, seg_offsets, n_seg))) return rc;
   PP_CUDA(ctx->out_splits.ensure(std::max<int64_t>(total, 1) * sizeof(int32_t)));
   PP_CUDA(ctx->out_times.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
@@ -1340,6 +1343,133 @@ int pp_plan_grid(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offse
   PP_CUDA(d2h(out->err_sample_id, d.err_sample_id, n_seg * sizeof(int64_t)));
   PP_CUDA(cudaStreamSynchronize(st));
   return PP_OK;
+}
+
+// pp_tuning::streams > 1 with host buffers: the batch is cut into 2 x streams
+// contiguous chunks that `streams` host threads (each with its own
+// sub-context and stream) take from a queue; a chunk is staged, planned and
+// copied back on its own stream, so one chunk's copies overlap another's
+// planning.
+int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets, int32_t n_seg,
+                    int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
+                    const pp_dp_options* opts, const pp_plan_out* out, int workers) {
+  workers = std::min(workers, (int)n_seg);
+  const int chunks = std::min((int)n_seg, 2 * workers);
+  while ((int)ctx->subs.size() < workers) {
+    pp_ctx* sub = nullptr;
+    const int rc = pp_ctx_create(ctx->device, &sub);
+    if (rc != PP_OK) return fail(ctx, rc, "cannot create a sub-context");
+    ctx->subs.push_back(sub);
+  }
+  const int64_t total = seg_offsets[n_seg];
+  std::vector<int> cut(chunks + 1, 0);
+  cut[chunks] = n_seg;
+  for (int p = 1; p < chunks; ++p) {
+    const int64_t target = total * p / chunks;
+    int s = cut[p - 1] + 1;
+    while (s < n_seg - (chunks - p) && seg_offsets[s] < target) ++s;
+    cut[p] = s;
+  }
+  std::atomic<int> next{0};
+  std::vector<int> rcs(workers, PP_OK);
+  std::vector<pp_stats> acc(workers);
+  std::vector<std::thread> th;
+  for (int w = 0; w < workers; ++w) {
+    th.emplace_back([&, w]() {
+      pp_ctx* sub = ctx->subs[w];
+      cudaSetDevice(sub->device);
+      sub->tuning = ctx->tuning;
+      sub->tuning.streams = 1;
+      pp_stats S{};
+      S.exit_thresh = INFINITY;
+      for (int k = next++; k < chunks && rcs[w] == PP_OK; k = next++) {
+        const int s0 = cut[k], s1 = cut[k + 1];
+        const int64_t base = seg_offsets[s0];
+        std::vector<int64_t> off(s1 - s0 + 1);
+        for (int s = s0; s <= s1; ++s) off[s - s0] = seg_offsets[s] - base;
+        pp_plan_out o{};
+        o.ordered = out->ordered ? out->ordered + base : nullptr;
+        o.splits = out->splits ? out->splits + base : nullptr;
+        o.mb_times = out->mb_times ? out->mb_times + base : nullptr;
+        o.count = out->count ? out->count + s0 : nullptr;
+        o.t_max_used = out->t_max_used ? out->t_max_used + s0 : nullptr;
+        o.objective = out->objective ? out->objective + s0 : nullptr;
+        o.status = out->status ? out->status + s0 : nullptr;
+        o.err_sample_id = out->err_sample_id ? out->err_sample_id + s0 : nullptr;
+        rcs[w] = plan_host(sub, samples + base, off.data(), s1 - s0, presorted, grid, model, opts, &o);
+        const pp_stats& t = sub->stats;
+        S.candidates_generated += t.candidates_generated;
+        S.candidates_evaluated += t.candidates_evaluated;
+        S.transitions_executed += t.transitions_executed;
+        S.transitions_reference += t.transitions_reference;
+        S.slices_costed += t.slices_costed;
+        S.waves = std::max(S.waves, t.waves);
+        S.ms_sort += t.ms_sort;
+        S.ms_cost += t.ms_cost;
+        S.ms_dp += t.ms_dp;
+        S.ms_total += t.ms_total;
+        for (int q = 0; q < 8; ++q) {
+          S.ms_kernel[q] += t.ms_kernel[q];
+          S.launches[q] += t.launches[q];
+        }
+        S.dp_band_bytes += t.dp_band_bytes;
+        S.slices_pass_a += t.slices_pass_a;
+        S.slices_pass_b += t.slices_pass_b;
+        S.bound_transitions += t.bound_transitions;
+        S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
+      }
+      acc[w] = S;
+    });
+  }
+  for (auto& t : th) t.join();
+  pp_stats S{};
+  S.exit_thresh = INFINITY;
+  for (int w = 0; w < workers; ++w) {
+    if (rcs[w] != PP_OK) return fail(ctx, rcs[w], ctx->subs[w]->err);
+    const pp_stats& t = acc[w];
+    S.candidates_generated += t.candidates_generated;
+    S.candidates_evaluated += t.candidates_evaluated;
+    S.transitions_executed += t.transitions_executed;
+    S.transitions_reference += t.transitions_reference;
+    S.slices_costed += t.slices_costed;
+    S.waves = std::max(S.waves, t.waves);
+    S.ms_sort = std::max(S.ms_sort, t.ms_sort);
+    S.ms_cost = std::max(S.ms_cost, t.ms_cost);
+    S.ms_dp = std::max(S.ms_dp, t.ms_dp);
+    S.ms_total = std::max(S.ms_total, t.ms_total);
+    for (int q = 0; q < 8; ++q) {
+      S.ms_kernel[q] += t.ms_kernel[q];
+      S.launches[q] += t.launches[q];
+    }
+    S.dp_band_bytes += t.dp_band_bytes;
+    S.slices_pass_a += t.slices_pass_a;
+    S.slices_pass_b += t.slices_pass_b;
+    S.bound_transitions += t.bound_transitions;
+    S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
+  }
+  ctx->stats = S;
+  return PP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pp_plan_grid(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets, int32_t n_seg,
+                 int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
+                 const pp_dp_options* opts, pp_plan_out* out) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (!samples || !seg_offsets || n_seg < 1 || !opts || !out)
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  if ((rc = validate_opts(ctx, *opts))) return rc;
+  if (seg_offsets[0] != 0) return fail(ctx, PP_ERR_INVALID, "seg_offsets[0] must be 0");
+  for (int s = 0; s < n_seg; ++s)
+    if (seg_offsets[s + 1] < seg_offsets[s]) return fail(ctx, PP_ERR_INVALID, "seg_offsets must be non-decreasing");
+  if (ctx->tuning.streams > 1 && n_seg > 1)
+    return plan_host_split(ctx, samples, seg_offsets, n_seg, presorted, grid, model, opts, out,
+                           ctx->tuning.streams);
+  return plan_host(ctx, samples, seg_offsets, n_seg, presorted, grid, model, opts, out);
 }
 
 int pp_order_samples(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets, int32_t n_seg,
