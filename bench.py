@@ -179,7 +179,7 @@ def main():
     ap.add_argument("--per-gpu", type=int, default=0, help="mini-batches per GPU per step")
     ap.add_argument("--cpu-plans", type=int, default=0, help="cpu_baseline sample size (0: cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=2, help="concurrent sub-batches per GPU")
+    ap.add_argument("--streams", type=int, default=3, help="concurrent sub-batches per GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -199,7 +199,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = W.CONFIGS[args.config]
-    M = args.per_gpu or {"C3": 592, "C4": 1024, "C1": 1024, "C2": 128, "C5": 1}.get(cfg.name, 8)
+    M = args.per_gpu or {"C3": 888, "C4": 1536, "C1": 1024, "C2": 192, "C5": 1}.get(cfg.name, 8)
     steps, warm = args.steps, args.warmup
     n = cfg.n
     # distinct mini-batches for every (rank, step): rank r owns groups
