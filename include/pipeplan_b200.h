@@ -81,6 +81,13 @@ typedef struct pp_model_desc {
   int32_t recompute;             /* 0 None, 1 Selective, 2 Full */
 } pp_model_desc;
 
+/* Reference PaddedShape (cost_model.h:52-56). */
+typedef struct pp_padded_shape {
+  int64_t mbs;
+  int64_t input_len;
+  int64_t target_len;
+} pp_padded_shape;
+
 /* Reference DpOptions (microbatch.h:79-86). */
 typedef struct pp_dp_options {
   int32_t stage_count;
@@ -192,6 +199,26 @@ int pp_candidate_range(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg
                        int32_t n_seg, int32_t presorted, const pp_grid_desc* grid,
                        const pp_model_desc* model, double per_mb_mem_cap, double* t_min,
                        double* t_max);
+
+/* OpCostTable::from_shapes (src/cost_model.cpp:360-382, per shape and stage
+ * estimate(), :294-319): t_f / t_b / act_mem of every (shape, stage) at
+ * [shape * n_stages + stage], priced on the device, bit-exact.  Host buffers.
+ * model->recompute selects the strategy (the planner may price a replica
+ * with a different one than it partitioned with, planner.cpp:73-130). */
+int pp_op_costs(pp_ctx* ctx, const pp_padded_shape* shapes, int64_t n, const pp_grid_desc* grid,
+                const pp_model_desc* model, double* t_f, double* t_b, double* act_mem);
+
+/* The same table for every micro-batch of plans already on the device
+ * (pp_plan_grid_device outputs: ordered samples, splits, count): micro-batch
+ * k of segment s is row mb_offset[s] + k at its padded shape (microbatch_cost
+ * over the micro-batch's samples, cost_model.cpp:331-341).  mb_offset (host,
+ * n_seg + 1 entries) is filled; the d_* tables are device arrays of
+ * capacity x n_stages doubles (PP_ERR_INVALID if capacity is too small). */
+int pp_plan_op_costs_device(pp_ctx* ctx, const pp_sample* d_ordered, const int64_t* d_seg_offsets,
+                            const int64_t* h_seg_offsets, int32_t n_seg, const int32_t* d_splits,
+                            const int32_t* d_count, const pp_grid_desc* grid,
+                            const pp_model_desc* model, int64_t capacity, int64_t* mb_offset,
+                            double* d_t_f, double* d_t_b, double* d_act_mem);
 
 /* Diagnostics: measured FP64 add issue rate of `device` (adds/s), the
  * roofline denominator of the FP64-bound cost kernels (calib.cu). */

@@ -209,6 +209,7 @@ class Reference:
         L.ref_plan_batch.argtypes = [vp, vp, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc),
                                      C.POINTER(_Opts), i32, vp, vp, vp, vp]
         L.ref_plan_batch.restype = dbl
+        L.ref_op_costs.argtypes = [vp, i64, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), vp, vp, vp]
         self.L = L
 
     def order_samples(self, samples):
@@ -224,6 +225,18 @@ class Reference:
         out = np.zeros(3)
         self.L.ref_per_layer(C.byref(g), kind, r, float(mbs), float(seq), _p(out))
         return out
+
+    def op_costs(self, shapes, grid, model):
+        """The reference's OpCostTable::from_shapes -> (t_f, t_b, act), (n, stages)."""
+        sh = np.ascontiguousarray(shapes, np.int64).reshape(-1, 3)
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        C_ = len(model.encoder_layers)
+        tf, tb, act = (np.zeros((len(sh), C_)) for _ in range(3))
+        rc = self.L.ref_op_costs(_p(sh), len(sh), C.byref(g), C.byref(m), _p(tf), _p(tb), _p(act))
+        if rc != PP_OK:
+            raise ValueError(f"reference from_shapes failed: {rc}")
+        return tf, tb, act
 
     def synthetic_grid_cells(self, params7, tp, mbs_axis=(), seq_axis=()):
         par = np.asarray(params7, np.float64)

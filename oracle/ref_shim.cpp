@@ -314,4 +314,30 @@ double ref_plan_batch(const pp_sample* samples, const int64_t* seg_off, int32_t 
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+
+// OpCostTable::from_shapes (src/cost_model.cpp:360-382): the reference's own
+// op-cost table, [shape * stages + stage].
+int ref_op_costs(const pp_padded_shape* shapes, int64_t n, const pp_grid_desc* g, const pp_model_desc* m,
+                 double* t_f, double* t_b, double* act) {
+  try {
+    ProfileGrid grid = grid_from_desc(g);
+    ModelConfig cfg = model_from_desc(m);
+    std::vector<PaddedShape> sh(n);
+    for (int64_t k = 0; k < n; ++k) {
+      sh[k].mbs = shapes[k].mbs;
+      sh[k].input_len = shapes[k].input_len;
+      sh[k].target_len = shapes[k].target_len;
+    }
+    OpCostTable t = OpCostTable::from_shapes(grid, cfg, sh, static_cast<Recompute>(m->recompute));
+    std::memcpy(t_f, t.t_f.data(), t.t_f.size() * sizeof(double));
+    std::memcpy(t_b, t.t_b.data(), t.t_b.size() * sizeof(double));
+    std::memcpy(act, t.act_mem.data(), t.act_mem.size() * sizeof(double));
+    return PP_OK;
+  } catch (const std::invalid_argument&) {
+    return PP_ERR_INVALID;
+  } catch (const std::out_of_range&) {
+    return PP_ERR_OUT_OF_RANGE;
+  }
+}
+
 }  // extern "C"

@@ -30,6 +30,7 @@ EXPORTED = [
     "pp_ctx_get_stats", "pp_ctx_set_stream", "pp_order_samples", "pp_plan_grid",
     "pp_plan_grid_device", "pp_plan_tables", "pp_candidate_range", "pp_eval_objective",
     "pp_synthetic_grid", "pp_synthetic_dataset", "pp_slice_cost_host", "pp_calibrate_fp64",
+    "pp_op_costs", "pp_plan_op_costs_device",
 ]
 
 
@@ -132,6 +133,9 @@ def _load():
     lib.pp_synthetic_dataset.argtypes = [i64, vp, vp, i64, C.c_uint64, vp]
     lib.pp_slice_cost_host.argtypes = [C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, i64, i64, vp, vp]
     lib.pp_calibrate_fp64.argtypes = [C.c_int, C.POINTER(dbl)]
+    lib.pp_op_costs.argtypes = [vp, vp, i64, C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, vp, vp]
+    lib.pp_plan_op_costs_device.argtypes = [vp, vp, vp, vp, i32, vp, vp, C.POINTER(GridDesc),
+                                            C.POINTER(ModelDesc), i64, vp, vp, vp, vp]
     return lib
 
 
@@ -414,6 +418,35 @@ class Planner:
             _raise_status(rc, int(err[0]), self._err())
         m = int(cnt[0])
         return Plan(PP_OK, splits[:m].copy(), times[:m].copy(), float(tm[0]), float(ob[0]))
+
+    def op_costs(self, shapes, grid: Grid, model: Model):
+        """OpCostTable::from_shapes: (t_f, t_b, act_mem), each (n, n_stages);
+        shapes is an (n, 3) int64 array of (mbs, input_len, target_len)."""
+        sh = np.ascontiguousarray(shapes, np.int64).reshape(-1, 3)
+        n, C_ = len(sh), len(model.encoder_layers)
+        tf, tb, act = (np.zeros((n, C_)) for _ in range(3))
+        rc = lib.pp_op_costs(self._h, _p(sh), n, C.byref(grid.desc()), C.byref(model.desc()), _p(tf),
+                             _p(tb), _p(act))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return tf, tb, act
+
+    def plan_op_costs_device(self, d_ordered, d_seg_offsets, h_seg_offsets, d_splits, d_count,
+                             grid: Grid, model: Model, d_tf, d_tb, d_act) -> np.ndarray:
+        """Op-cost tables of every planned micro-batch (device tensors);
+        returns mb_offset (host)."""
+        h_off = np.ascontiguousarray(h_seg_offsets, np.int64)
+        S = len(h_off) - 1
+        mb_off = np.zeros(S + 1, np.int64)
+        cap = d_tf.numel() // len(model.encoder_layers)
+        rc = lib.pp_plan_op_costs_device(
+            self._h, C.c_void_p(d_ordered.data_ptr()), C.c_void_p(d_seg_offsets.data_ptr()), _p(h_off), S,
+            C.c_void_p(d_splits.data_ptr()), C.c_void_p(d_count.data_ptr()), C.byref(grid.desc()),
+            C.byref(model.desc()), cap, _p(mb_off), C.c_void_p(d_tf.data_ptr()),
+            C.c_void_p(d_tb.data_ptr()), C.c_void_p(d_act.data_ptr()))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return mb_off
 
     def candidate_range(self, samples, seg_offsets, grid: Grid, model: Model,
                         mem_cap: float = math.inf, presorted: bool = False):

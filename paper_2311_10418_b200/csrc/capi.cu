@@ -87,6 +87,12 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int64_t* seg_band_base, const double* band, const double* cand,
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, cudaStream_t st);
+cudaError_t launch_mb_shapes(const pp_sample* ordered, const int64_t* seg_off, const int32_t* splits,
+                             const int64_t* mb_off, int n_seg, int64_t n_mb, pp_padded_shape* shapes,
+                             cudaStream_t st);
+cudaError_t launch_op_costs(const CostGrid& g, const double* le_st, const double* ld_st, int stages,
+                            const pp_padded_shape* shapes, int64_t n, double* t_f, double* t_b,
+                            double* act, cudaStream_t st);
 size_t dp_coop_parts_bytes(int grid);
 int dp_coop_grid(int device);
 cudaError_t launch_dp_coop(int mode, int sanitize, const WorkItem& it, int grid, const int64_t* seg_off,
@@ -180,7 +186,7 @@ struct pp_ctx {
       bound_items, bound_res;
   DevBuf out_splits, out_times, out_count, out_tmax, out_obj, out_status, out_err;
   PinBuf h_range, h_stats, h_segdp;
-  DevBuf small_bm, coop_state, coop_parts;
+  DevBuf small_bm, coop_state, coop_parts, shapes, stage_lay, mb_off, oc_tf, oc_tb, oc_act;
   // host copy of the uploaded grid (restricted to the recompute strategy)
   // for the monotonicity certificate of cost pass A
   std::vector<double> h_ax, h_cells;
@@ -204,7 +210,7 @@ struct pp_ctx {
             &raw_cnt, &raw_in_tmp, &cand, &cand_off, &cand_n, &active, &items, &results, &next_buf,
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
             &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
-            &small_bm, &coop_state, &coop_parts};
+            &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act};
   }
 };
 
@@ -1600,6 +1606,80 @@ int pp_plan_tables(pp_ctx* ctx, const double* slice_time, const double* slice_me
     return fail(ctx, status, "sample does not fit the per-micro-batch memory cap alone");
   if (status == PP_ERR_INFEASIBLE) return fail(ctx, status, "no feasible partition under the memory cap");
   return status;
+}
+
+
+int pp_op_costs(pp_ctx* ctx, const pp_padded_shape* shapes, int64_t n, const pp_grid_desc* grid,
+                const pp_model_desc* model, double* t_f, double* t_b, double* act_mem) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!shapes || !t_f || !t_b || !act_mem))) return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  for (int64_t k = 0; k < n; ++k)
+    if (shapes[k].mbs < 1) return fail(ctx, PP_ERR_INVALID, "micro-batch size must be >= 1");  // :299
+  CostGrid g{};
+  if ((rc = upload_grid(ctx, grid, model, &g))) return rc;
+  if (n == 0) return PP_OK;
+  const int C = model->n_stages;
+  cudaStream_t st = ctx->stream;
+  std::vector<double> lay(2 * (size_t)C);
+  for (int j = 0; j < C; ++j) {
+    lay[j] = model->encoder_layers[j] > 0 ? (double)model->encoder_layers[j] : 0.0;
+    lay[C + j] = model->decoder_layers[j] > 0 ? (double)model->decoder_layers[j] : 0.0;
+  }
+  PP_CUDA(ctx->stage_lay.ensure(lay.size() * sizeof(double)));
+  PP_CUDA(ctx->shapes.ensure(n * sizeof(pp_padded_shape)));
+  PP_CUDA(ctx->oc_tf.ensure(n * C * sizeof(double)));
+  PP_CUDA(ctx->oc_tb.ensure(n * C * sizeof(double)));
+  PP_CUDA(ctx->oc_act.ensure(n * C * sizeof(double)));
+  PP_CUDA(cudaMemcpyAsync(ctx->stage_lay.p, lay.data(), lay.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->shapes.p, shapes, n * sizeof(pp_padded_shape), cudaMemcpyHostToDevice, st));
+  PP_CUDA(launch_op_costs(g, ctx->stage_lay.as<double>(), ctx->stage_lay.as<double>() + C, C,
+                          ctx->shapes.as<pp_padded_shape>(), n, ctx->oc_tf.as<double>(), ctx->oc_tb.as<double>(),
+                          ctx->oc_act.as<double>(), st));
+  PP_CUDA(cudaMemcpyAsync(t_f, ctx->oc_tf.p, n * C * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaMemcpyAsync(t_b, ctx->oc_tb.p, n * C * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaMemcpyAsync(act_mem, ctx->oc_act.p, n * C * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaStreamSynchronize(st));  // lay dies here
+  return PP_OK;
+}
+
+int pp_plan_op_costs_device(pp_ctx* ctx, const pp_sample* d_ordered, const int64_t* d_seg_offsets,
+                            const int64_t* h_seg_offsets, int32_t n_seg, const int32_t* d_splits,
+                            const int32_t* d_count, const pp_grid_desc* grid,
+                            const pp_model_desc* model, int64_t capacity, int64_t* mb_offset,
+                            double* d_t_f, double* d_t_b, double* d_act_mem) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n_seg < 1 || !d_ordered || !d_seg_offsets || !h_seg_offsets || !d_splits || !d_count || !mb_offset)
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  CostGrid g{};
+  if ((rc = upload_grid(ctx, grid, model, &g))) return rc;
+  cudaStream_t st = ctx->stream;
+  std::vector<int32_t> cnt(n_seg);
+  PP_CUDA(cudaMemcpyAsync(cnt.data(), d_count, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaStreamSynchronize(st));
+  mb_offset[0] = 0;
+  for (int s = 0; s < n_seg; ++s) mb_offset[s + 1] = mb_offset[s] + std::max(cnt[s], 0);
+  const int64_t n_mb = mb_offset[n_seg];
+  if (n_mb > capacity) return fail(ctx, PP_ERR_INVALID, "op-cost table capacity too small");
+  if (n_mb == 0) return PP_OK;
+  const int C = model->n_stages;
+  std::vector<double> lay(2 * (size_t)C);
+  for (int j = 0; j < C; ++j) {
+    lay[j] = model->encoder_layers[j] > 0 ? (double)model->encoder_layers[j] : 0.0;
+    lay[C + j] = model->decoder_layers[j] > 0 ? (double)model->decoder_layers[j] : 0.0;
+  }
+  PP_CUDA(ctx->stage_lay.ensure(lay.size() * sizeof(double)));
+  PP_CUDA(ctx->mb_off.ensure((n_seg + 1) * sizeof(int64_t)));
+  PP_CUDA(ctx->shapes.ensure(n_mb * sizeof(pp_padded_shape)));
+  PP_CUDA(cudaMemcpyAsync(ctx->stage_lay.p, lay.data(), lay.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->mb_off.p, mb_offset, (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  PP_CUDA(launch_mb_shapes(d_ordered, d_seg_offsets, d_splits, ctx->mb_off.as<int64_t>(), n_seg, n_mb,
+                           ctx->shapes.as<pp_padded_shape>(), st));
+  PP_CUDA(launch_op_costs(g, ctx->stage_lay.as<double>(), ctx->stage_lay.as<double>() + C, C,
+                          ctx->shapes.as<pp_padded_shape>(), n_mb, d_t_f, d_t_b, d_act_mem, st));
+  PP_CUDA(cudaStreamSynchronize(st));  // lay and the offsets die here
+  return PP_OK;
 }
 
 }  // extern "C"

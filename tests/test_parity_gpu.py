@@ -436,3 +436,71 @@ def test_c5_long_tail_full_scale():
     assert a.objective == capi.eval_objective(a.mb_times, cfg.stages, 1)
     coop.close()
     single.close()
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not shipped")
+def test_op_cost_tables_match_reference(planner):
+    """OpCostTable::from_shapes on the device (SURVEY.md §8f row 2) against
+    the unmodified reference's from_shapes: every recompute strategy, GPT and
+    T5 layouts, shapes inside, below and beyond the grid axes."""
+    ref = Reference()
+    grid = capi.synthetic_grid()
+    rng = np.random.default_rng(63)
+    for encdec in (False, True):
+        for r in range(3):
+            model = capi.Model.uniform(int(rng.choice([1, 4, 8])), int(rng.integers(1, 4)), encdec, recompute=r)
+            sh = np.stack([rng.integers(1, 600, 400), rng.integers(0, 90000, 400),
+                           rng.integers(0, 9000, 400)], 1)
+            a = ref.op_costs(sh, grid, model)
+            b = planner.op_costs(sh, grid, model)
+            for x, y, nm in zip(a, b, ("t_f", "t_b", "act_mem")):
+                assert x.tobytes() == y.tobytes(), (nm, encdec, r)
+
+
+def test_plan_op_costs_device_match_reference_shapes(planner):
+    """Op-cost tables of device-resident C3 plans (padded shape of every planned
+    micro-batch) equal the reference's from_shapes over the same shapes."""
+    import torch
+
+    cfg = W.CONFIGS["C3"]
+    M = 3
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    d_s = torch.from_numpy(s).cuda()
+    d_off = torch.from_numpy(off).cuda()
+    tot = M * cfg.n
+    out = {"ordered": torch.empty((tot, 3), dtype=torch.int64, device="cuda"),
+           "splits": torch.empty(tot, dtype=torch.int32, device="cuda"),
+           "mb_times": torch.empty(tot, dtype=torch.float64, device="cuda"),
+           "count": torch.empty(M, dtype=torch.int32, device="cuda"),
+           "t_max_used": torch.empty(M, dtype=torch.float64, device="cuda"),
+           "objective": torch.empty(M, dtype=torch.float64, device="cuda"),
+           "status": torch.empty(M, dtype=torch.int32, device="cuda"),
+           "err_sample_id": torch.empty(M, dtype=torch.int64, device="cuda")}
+    planner.plan_batch_device(d_s, d_off, off, out, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap,
+                              cfg.interval)
+    C_ = cfg.stages
+    cap = tot
+    tf, tb, act = (torch.empty(cap * C_, dtype=torch.float64, device="cuda") for _ in range(3))
+    model = capi.Model.uniform(cfg.stages, 2, False, recompute=2)  # a replica may price another strategy
+    mb_off = planner.plan_op_costs_device(out["ordered"], d_off, off, out["splits"], out["count"],
+                                          W.grid(), model, tf, tb, act)
+    ordered = out["ordered"].cpu().numpy()
+    splits = out["splits"].cpu().numpy()
+    count = out["count"].cpu().numpy()
+    shapes = []
+    for q in range(M):
+        sp = splits[off[q]:off[q] + count[q]]
+        lo = 0
+        for e in sp:
+            blk = ordered[off[q] + lo:off[q] + e]
+            shapes.append((e - lo, max(0, blk[:, 1].max()), max(0, blk[:, 2].max())))
+            lo = e
+    assert mb_off[-1] == len(shapes)
+    host = planner.op_costs(np.array(shapes, np.int64), W.grid(), model)
+    n_mb = len(shapes)
+    for x, y in zip(host, (tf, tb, act)):
+        assert x.reshape(-1).tobytes() == y[:n_mb * C_].cpu().numpy().tobytes()
+    if reference_available():
+        ref = Reference().op_costs(np.array(shapes, np.int64), W.grid(), model)
+        assert ref[0].tobytes() == host[0].tobytes() and ref[2].tobytes() == host[2].tobytes()
