@@ -296,22 +296,39 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * M * steps / float(te.item())
 
+    # ---- isolated kernel durations: the timed region runs `streams` concurrent
+    # sub-batches, so a kernel's event-timed duration there includes the SMs it
+    # shares with the other streams' kernels.  A few untimed 1-stream steps give
+    # each kernel's duration alone on the GPU (the roofline's isolated figures).
+    solo_stats = []
+    if args.streams > 1:
+        planner.set_tuning(streams=1)
+        for g in range(warm, warm + min(steps, 4)):
+            step(g)
+            solo_stats.append(planner.stats())
+        torch.cuda.synchronize()
+        planner.set_tuning(streams=args.streams)
+
     if rank == 0:
         pk, pk_kind = peaks()
         fp64_peak = capi.calibrate_fp64(local) / 1e12  # adds/s -> T ops/s
-        kern = np.zeros(8)
-        launches = np.zeros(8, np.int64)
-        agg = {k: 0 for k in ("tr", "ref_tr", "evals", "gen", "sl_a", "sl_b", "bound_tr")}
-        for s in stats:
-            kern += np.array(s["ms_kernel"])
-            launches += np.array(s["launches"], np.int64)
-            agg["tr"] += s["transitions_executed"]
-            agg["ref_tr"] += s["transitions_reference"]
-            agg["evals"] += s["candidates_evaluated"]
-            agg["gen"] += s["candidates_generated"]
-            agg["sl_a"] += s["slices_pass_a"]
-            agg["sl_b"] += s["slices_pass_b"]
-            agg["bound_tr"] += s["bound_transitions"]
+        def aggregate(sts):
+            kern = np.zeros(8)
+            launches = np.zeros(8, np.int64)
+            agg = {k: 0 for k in ("tr", "ref_tr", "evals", "gen", "sl_a", "sl_b", "bound_tr")}
+            for s in sts:
+                kern += np.array(s["ms_kernel"])
+                launches += np.array(s["launches"], np.int64)
+                agg["tr"] += s["transitions_executed"]
+                agg["ref_tr"] += s["transitions_reference"]
+                agg["evals"] += s["candidates_evaluated"]
+                agg["gen"] += s["candidates_generated"]
+                agg["sl_a"] += s["slices_pass_a"]
+                agg["sl_b"] += s["slices_pass_b"]
+                agg["bound_tr"] += s["bound_transitions"]
+            return kern, launches, agg
+
+        kern, launches, agg = aggregate(stats)
         names = capi.KERNEL_NAMES
         kl = W.kind_layouts(cfg)  # (layout, kind) pairs priced per slice
         # algorithmic work per launch category:
@@ -319,14 +336,17 @@ def main():
         #           7 FP64 ops + scale = 8 ... counted as 11 with the clamp/compare
         #   pass B: slice time per (layout, kind): 2 blends x 7 + 2 DMUL + 1 DADD = 17 FP64 ops
         #   DP: one 8-byte band entry streamed per transition
-        work = {
-            2: ("fp64", agg["sl_a"] * 11 * kl, "11 FP64 ops per act_mem pricing per (layout, kind)"),
-            3: ("fp64", agg["sl_b"] * 17 * kl, f"{17 * kl} FP64 ops per band slice"),
-            4: ("hbm", agg["bound_tr"] * 8, "8 B band entry per transition"),
-            5: ("hbm", (agg["tr"] - agg["bound_tr"]) * 8, "8 B band entry per transition"),
-        }
+        def work_of(agg):
+            return {
+                2: ("fp64", agg["sl_a"] * 11 * kl, "11 FP64 ops per act_mem pricing per (layout, kind)"),
+                3: ("fp64", agg["sl_b"] * 17 * kl, f"{17 * kl} FP64 ops per band slice"),
+                4: ("hbm", agg["bound_tr"] * 8, "8 B band entry per transition"),
+                5: ("hbm", (agg["tr"] - agg["bound_tr"]) * 8, "8 B band entry per transition"),
+            }
 
-        def roof_of(cat):
+        work = work_of(agg)
+
+        def roof_of(cat, work=work, kern=kern, launches=launches):
             bound, units, algo = work[cat]
             secs = kern[cat] / 1e3
             if bound == "fp64":
@@ -355,6 +375,20 @@ def main():
         roof["all"] = {names[c]: {k: roof_of(c)[k] for k in ("bound", "achieved", "unit", "frac",
                                                              "share_of_step")}
                        for c in work if kern[c] > 0}
+        if solo_stats:
+            s_kern, s_launch, s_agg = aggregate(solo_stats)
+            s_work = work_of(s_agg)
+            iso = {names[c]: {k: roof_of(c, s_work, s_kern, s_launch)[k]
+                              for k in ("achieved", "frac", "avg_launch_ms", "share_of_step")}
+                   for c in s_work if s_kern[c] > 0}
+            roof["isolated"] = {
+                "note": (f"the timed region runs {args.streams} concurrent sub-batches, so each kernel's "
+                         "event-timed duration includes SMs shared with the other streams; these are the "
+                         f"same kernels timed alone ({len(solo_stats)} untimed 1-stream steps, "
+                         f"{M} mini-batches each)"),
+                "kernels": iso}
+            if names[dom] in iso:
+                roof["frac_isolated"] = iso[names[dom]]["frac"]
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1

@@ -107,7 +107,10 @@ typedef struct pp_tuning {
   int32_t coop_min_n;      /* a DP launch of <= 8 passes whose mini-batches all have at
                               least this many samples runs each pass as one cooperative
                               kernel over the whole GPU; 0 = default (16384) */
-  int32_t reserved[4];
+  int32_t no_slice_reuse;  /* 1: price every band slice; 0 (default): sorted single-input
+                              mini-batches price each distinct (micro-batch size, padded
+                              length) pair once and copy it along the band's diagonal */
+  int32_t reserved[3];
 } pp_tuning;
 
 /* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are

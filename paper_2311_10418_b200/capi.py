@@ -74,7 +74,7 @@ class DpOptions(C.Structure):
 
 class Tuning(C.Structure):
     _fields_ = [("first_wave", C.c_int32), ("max_wave", C.c_int32), ("streams", C.c_int32),
-                ("coop_min_n", C.c_int32), ("reserved", C.c_int32 * 4)]
+                ("coop_min_n", C.c_int32), ("no_slice_reuse", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 class PlanOut(C.Structure):
@@ -311,8 +311,9 @@ class Planner:
     def _err(self) -> str:
         return (lib.pp_ctx_last_error(self._h) or b"").decode()
 
-    def set_tuning(self, first_wave: int = 1, max_wave: int = 16, streams: int = 1, coop_min_n: int = 0):
-        t = Tuning(first_wave, max_wave, streams, coop_min_n)
+    def set_tuning(self, first_wave: int = 1, max_wave: int = 16, streams: int = 1, coop_min_n: int = 0,
+                   slice_reuse: bool = True):
+        t = Tuning(first_wave, max_wave, streams, coop_min_n, 0 if slice_reuse else 1)
         rc = lib.pp_ctx_set_tuning(self._h, C.byref(t))
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())

@@ -59,7 +59,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              double interval, int* row_w, int* row_fb, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
-                             double lo_thresh, int bisect, int sorted_in, cudaStream_t st);
+                             double lo_thresh, int bisect, int sorted_in, int reuse, cudaStream_t st);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
                              int* row_w, int* blk_W, cudaStream_t st);
 cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -654,7 +654,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                    ctx->blk_base.as<int>(), n_seg, total_blocks, max_n, ctx->mbp.as<AxisPos>(),
                                    cap, interval, ctx->row_w.as<int>(), ctx->row_fb.as<int>(), ctx->blk_W.as<int>(),
                                    ctx->stats_d.as<SegStats>(), nullptr, nullptr, nullptr, exit_thresh,
-                                   nullptr, nullptr, lo_thresh, bisect, 0, st));
+                                   nullptr, nullptr, lo_thresh, bisect, 0, 0, st));
     PP_TIMED(1, launch_tile_offsets(ctx->blk_W.as<int>(), ctx->blk_base.as<int>(), n_seg,
                                     ctx->tile_off.as<int64_t>(), ctx->stats_d.as<SegStats>(), st));
   }
@@ -680,7 +680,8 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                  cap, interval, ctx->row_w.as<int>(), ctx->row_fb.as<int>(), ctx->blk_W.as<int>(),
                                  ctx->stats_d.as<SegStats>(), ctx->tile_off.as<int64_t>(),
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), INFINITY, small_bm,
-                                 tau_d, -INFINITY, 0, c.presorted ? 0 : 1, st));
+                                 tau_d, -INFINITY, 0, c.presorted ? 0 : 1,
+                                 ctx->tuning.no_slice_reuse ? 0 : 1, st));
   PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
   PP_CUDA(cudaStreamSynchronize(st));
   return PP_OK;

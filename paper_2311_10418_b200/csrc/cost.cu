@@ -728,6 +728,270 @@ __global__ void __launch_bounds__(32 * kCostWarps)
   }
 }
 
+// Pass B for segments sorted by input length with one sequence input (GPT):
+// the slice [i, j) pads to in[j-1], so its time and act_mem depend only on
+// (d = j - i, in[j-1]).  Sorted mini-batches repeat lengths (C3: ~1550
+// distinct lengths in 8192 samples, and the wide rows are the short, dense
+// ones), so along a diagonal of the band the same value recurs for every
+// column of a run of equal lengths: only ~11% of C3's band slices are
+// distinct (d, run) pairs.  Each pair is priced ONCE, with exactly the
+// operations of band3_kernel, into a per-warp ring indexed by d, and every
+// column of the run reads its 32 entries back (lane r: d = c - r):
+//   * a column chunk splits into pieces of equal length (a ballot over the
+//     staged lengths); a piece prices the diagonals it reaches that the run
+//     has not priced yet, 32 per batch (lane l: d = next + l), then stores
+//     its columns (one coalesced 256 B column per step);
+//   * the ring holds the last 128 priced diagonals, enough for a piece of up
+//     to 32 columns (needs d in [cs - 31, ce]) after a batch overshoot.
+// Feasibility is (live) & !(act_mem > cap) per entry: act_mem > cap implies
+// j >= the row's first infeasible j (pass A), which is exactly band3's test.
+// A pair's candidate bin is recorded iff some LIVE slice of the tile carries
+// it (a range-max over the tile's row widths: rows r' with d <= w_r' whose
+// column r' + d lies in the run), so the candidate set is the reference's
+// exactly.  The store stream is the kernel's bound rather than FP64 issue.
+template <int LAY>
+__global__ void __launch_bounds__(32 * kCostWarps)
+    band_run_kernel(CostArgs a) {
+  __shared__ double4 s_tt[kBandCells];
+  __shared__ double2 s_am[kBandCells];
+  __shared__ double s_tau[kSmallBmWords * 32];
+  __shared__ double s_x[kCostWarps][32];
+  __shared__ AxisPos s_px[kCostWarps][32];
+  __shared__ double s_ring[kCostWarps][128];
+  __shared__ int s_rmq[kCostWarps][5][32];
+  __shared__ unsigned int s_bm[kCostWarps][kSmallBmWords];
+  const int nm = a.g.nm, ns = a.g.ns;
+  {
+    const int cells = 2 * nm * ns;
+    for (int k = threadIdx.x; k < cells; k += blockDim.x) {
+      s_tt[k] = a.g.tt[k];
+      s_am[k] = a.g.am[k];
+    }
+    for (int k = threadIdx.x; k < kSmallBmWords * 32; k += blockDim.x) s_tau[k] = a.tau[k];
+    __syncthreads();
+  }
+  const int per = nm * ns;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warps = gridDim.x * kCostWarps;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
+  const bool need_mem = !(a.cap == INF);
+  constexpr int kTau = kSmallBmWords * 32;
+  const double le = a.g.le, ld = a.g.ld, ival = a.interval, cap = a.cap;
+  AxisPos p0{0.0, 0, 0};
+  bracket(a.g.seq_ax, ns, 0.0, p0.seg, p0.t);
+  auto kind_time = [&](int base, int mb, double tm, int sg, double ts, double& tf, double& tb) {
+    const int s1 = min(sg + 1, ns - 1);
+    const double4 c0 = s_tt[base + mb + sg], c1 = s_tt[base + mb + s1];
+    tf = blend_d(tm, ts, c0.x, c0.z, c1.x, c1.z);
+    tb = blend_d(tm, ts, c0.y, c0.w, c1.y, c1.w);
+  };
+  auto kind_mem = [&](int base, int mb, double tm, int sg, double ts) {
+    const int s1 = min(sg + 1, ns - 1);
+    const double2 c0 = s_am[base + mb + sg], c1 = s_am[base + mb + s1];
+    return blend_d(tm, ts, c0.x, c0.y, c1.x, c1.y);
+  };
+  // slice time, NaN where act_mem exceeds the cap (band3_kernel's operations)
+  auto price = [&](const AxisPos& mb, const AxisPos& pe) {
+    double df, db;
+    kind_time(per, mb.pad, mb.t, pe.seg, pe.t, df, db);
+    const double t2 = __dadd_rn(__dmul_rn(ld, df), __dmul_rn(ld, db));
+    double T = t2;
+    if (LAY != kLayDec1) {
+      double ef, eb;
+      kind_time(0, mb.pad, mb.t, pe.seg, pe.t, ef, eb);
+      const double t1 = __dadd_rn(__dmul_rn(le, ef), __dmul_rn(le, eb));
+      T = (t1 < t2) ? t2 : t1;
+    }
+    if (need_mem) {
+      double M = __dmul_rn(ld, kind_mem(per, mb.pad, mb.t, pe.seg, pe.t));
+      if (LAY != kLayDec1) {
+        const double a1 = __dmul_rn(le, kind_mem(0, mb.pad, mb.t, pe.seg, pe.t));
+        M = (a1 < M) ? M : a1;
+      }
+      T = (M > cap) ? QNAN : T;
+    }
+    return T;
+  };
+  for (int gb = blockIdx.x * kCostWarps + wid; gb < a.total_blocks; gb += warps) {
+    const int s = seg_of(a.blk_base, a.n_seg, gb);
+    const int64_t b0 = a.seg_off[s];
+    const int n = (int)(a.seg_off[s + 1] - b0);
+    const int bl = gb - a.blk_base[s];
+    const int i1 = n - kRB * bl;
+    const int i0 = max(0, i1 - kRB);
+    const int r = lane;
+    const bool rowv = r < i1 - i0;
+    const int wr = rowv ? a.row_w[b0 + i0 + r] : 0;  // 0: never live
+    // range-max table over the tile's row widths (levels 0..4: windows of 2^L rows)
+    {
+      int m = wr;
+      s_rmq[wid][0][lane] = m;
+#pragma unroll
+      for (int L = 1; L < 5; ++L) {
+        m = max(m, __shfl_down_sync(0xffffffffu, m, 1 << (L - 1)));
+        s_rmq[wid][L][lane] = m;
+      }
+    }
+    if (lane < kSmallBmWords) s_bm[wid][lane] = 0u;
+    __syncwarp();
+    auto rmq = [&](int lo, int hi) {  // max of the row widths r' in [lo, hi], 0 <= lo <= hi <= 31
+      const int L = min(31 - __clz(hi - lo + 1), 4);  // two windows of 2^L cover the range
+      return max(s_rmq[wid][L][lo], s_rmq[wid][L][hi - (1 << L) + 1]);
+    };
+    // candidate bins of the priced pairs: k = ceil(T / I) exactly as the
+    // reference computes it, one division per bin change of the lane (its bin
+    // (tlo, thi] = (tau[k-1], tau[k]] is cached); bits gather in one register
+    // word until the word changes
+    double tlo = INF, thi = -INF;
+    int cw = -1;
+    unsigned int cbits = 0u;
+    double kmn = INF, kmx = -INF;
+    int flags = 0;
+    bool any_binned = false;
+    auto bin = [&](double T) {
+      if ((T > tlo) & (T <= thi)) return;  // the lane's current bin: already marked
+      const double qv = ceil(__ddiv_rn(T, ival));
+      if (qv < (double)kTau) {  // T >= +0: qv in [0, kTau)
+        const int k = (int)qv;
+        tlo = k > 0 ? s_tau[k - 1] : -INF;
+        thi = s_tau[k];
+        any_binned = true;
+        if ((k >> 5) != cw) {
+          if (cbits) atomicOr(&s_bm[wid][cw], cbits);
+          cw = k >> 5;
+          cbits = 0u;
+        }
+        cbits |= 1u << (k & 31);
+      } else if (isinf(qv)) {
+        flags |= (qv > 0) ? 1 : 2;
+      } else {
+        kmn = (qv < kmn) ? qv : kmn;
+        kmx = (kmx < qv) ? qv : kmx;
+      }
+    };
+    const int W = a.blk_W[gb];
+    double* tile = a.band + a.seg_band_base[s] + a.tile_off[gb];
+    tile[r] = QNAN;  // column 0: j = i0 <= i is never a slice
+    double* ring = s_ring[wid];
+    double prev_x = QNAN;  // NaN: the first column starts a run
+    AxisPos pe = p0;       // sequence bracket of the current run
+    int ca = 0, cb = 0;    // the run's first and last column (within the tile)
+    int done = 0;          // the run's diagonals up to `done` are in the ring
+    for (int c0 = 1; c0 < W; c0 += 32) {
+      const int cq = c0 + lane;
+      double xq = QNAN;
+      if (cq < W) {
+        const int64_t k = b0 + i0 + cq - 1;
+        xq = a.in_d[k];
+        s_x[wid][lane] = xq;
+        s_px[wid][lane] = a.pin[k];
+      }
+      // bit q: column c0 + q ends its run (the next column differs or is past the tile)
+      double xn = __shfl_down_sync(0xffffffffu, xq, 1);
+      if (lane == 31) xn = (cq + 1 < W) ? a.in_d[b0 + i0 + cq] : QNAN;
+      const unsigned int run_end = __ballot_sync(0xffffffffu, !(xn == xq));
+      __syncwarp();
+      const int qend = min(32, W - c0);
+      for (int q = 0; q < qend;) {
+        const unsigned int e = run_end >> q;
+        const int qe = min(e ? q + __ffs(e) - 1 : 31, qend - 1);
+        const int cs = c0 + q, ce = c0 + qe;
+        const double x = s_x[wid][q];
+        if (!(x == prev_x)) {  // warp-uniform: column cs starts a run of equal lengths
+          prev_x = x;
+          const AxisPos px = s_px[wid][q];
+          const bool pos = 0.0 < x;
+          pe.t = pos ? px.t : p0.t;
+          pe.seg = pos ? px.seg : p0.seg;
+          ca = cs;
+          if (e) {
+            cb = c0 + q + __ffs(e) - 1;
+          } else {  // the run continues past this chunk
+            cb = W - 1;
+            for (int base = c0 + 32; base < W; base += 32) {
+              const int cc = base + lane;
+              const bool same = (cc < W) && (a.in_d[b0 + i0 + cc - 1] == x);
+              const unsigned int diff = __ballot_sync(0xffffffffu, !same);
+              if (diff) {
+                cb = base + __ffs(diff) - 2;
+                break;
+              }
+            }
+          }
+          if (cb == cs) {  // a one-column run: lane r prices its own slice (r, cs), d = cs - r
+            const int d = cs - r;
+            const double F = price(a.mbp[min(max(d, 1), a.max_n)], pe);
+            const bool live = (unsigned)(d - 1) < (unsigned)wr;
+            tile[(size_t)cs * kRB + r] = live ? F : QNAN;
+            if (live && !isnan(F)) bin(F);
+            q = qe + 1;
+            continue;
+          }
+          done = cs - 32;
+        }
+        // price the run's diagonals (done, ce] (d <= 0 entries are never live)
+        while (done < ce) {
+          const int d = done + 1 + lane;
+          const double F = price(a.mbp[min(max(d, 1), a.max_n)], pe);
+          ring[d & 127] = F;
+          // live slices carrying (d, run): rows r' in [ca - d, cb - d] with w_r' >= d
+          const int lo = max(ca - d, 0), hi = min(cb - d, 31);
+          if ((d >= 1) && (lo <= hi) && !isnan(F) && rmq(lo, hi) >= d) bin(F);
+          done += 32;
+        }
+        __syncwarp();
+        {
+          // column c: lane r stores ring[d = c - r], live iff 1 <= d <= w_r
+          double* out = tile + (size_t)cs * kRB + r;
+          int d = cs - r;
+#pragma unroll 2
+          for (int c = cs; c <= ce; ++c) {
+            const double v = ring[d & 127];
+            *out = ((unsigned)(d - 1) < (unsigned)wr) ? v : QNAN;
+            out += kRB;
+            ++d;
+          }
+        }
+        __syncwarp();
+        q = qe + 1;
+      }
+    }
+    const unsigned int npriced = (unsigned int)wr;  // live slices of the row: columns r+1 .. r+wr
+    if (cbits) atomicOr(&s_bm[wid][cw], cbits);
+    const bool any_b = __any_sync(0xffffffffu, any_binned);
+    if (any_b) {  // binned values lie in [0, kTau): widen the range to a superset
+      kmn = (0.0 < kmn) ? 0.0 : kmn;
+      kmx = (kmx < (double)(kTau - 1)) ? (double)(kTau - 1) : kmx;
+    }
+    unsigned long long np = npriced;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, kmn, o);
+      const double y = __shfl_xor_sync(0xffffffffu, kmx, o);
+      kmn = (x < kmn) ? x : kmn;
+      kmx = (kmx < y) ? y : kmx;
+      np += __shfl_xor_sync(0xffffffffu, np, o);
+      flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&a.stats[s].priced_b, np);
+      if (np) atomicAdd(&a.stats[s].nraw, np);  // >= the raw count; only sizes the raw fallback
+      if (!isinf(kmn)) {
+        atomicMin(&a.stats[s].kmin, dkey(kmn));
+        atomicMax(&a.stats[s].kmax, dkey(kmx));
+      }
+      if (flags) atomicOr(&a.stats[s].flags, flags);
+    }
+    __syncwarp();
+    if (lane < kSmallBmWords) {
+      const unsigned int w = s_bm[wid][lane];
+      if (w) atomicOr(&a.small_bm[(size_t)s * kSmallBmWords + lane], w);
+    }
+    __syncwarp();
+  }
+}
+
 // Pass B, fused grid costing with quantised candidates (I > 0): the lean
 // form of block_kernel<1, SRC, LAY>.  Every lane prices every column of its
 // warp's tile unconditionally and masks the result (no divergence in the
@@ -1200,7 +1464,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              double interval, int* row_w, int* row_fb, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
-                             double lo_thresh, int bisect, int sorted_in, cudaStream_t st) {
+                             double lo_thresh, int bisect, int sorted_in, int reuse, cudaStream_t st) {
   CostArgs a{g, tabT, tabM, in_d, tgt_d, pin, ptg, seg_off, blk_base, n_seg, total_blocks, max_n, mbp,
              cap, interval, row_w, row_fb, blk_W, stats, tile_off, seg_band_base, band, exit_thresh,
              small_bm, tau};
@@ -1210,7 +1474,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
   const int blocks = std::max(1, std::min((total_blocks + kCostWarps - 1) / kCostWarps, 148 * 32));
 #define PP_COST_LAUNCH(P, S, L)                                                                        \
   do {                                                                                                 \
-    cudaFuncSetAttribute(block_kernel<P, S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    ensure_dyn_smem((const void*)block_kernel<P, S, L>, sm);                                           \
     block_kernel<P, S, L><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                     \
   } while (0)
 #define PP_COST_LAUNCH_L(P, S)                                                  \
@@ -1221,7 +1485,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
   } while (0)
 #define PP_BAND_LAUNCH2(S, L, Z)                                                                      \
   do {                                                                                                 \
-    cudaFuncSetAttribute(band_kernel<S, L, Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
+    ensure_dyn_smem((const void*)band_kernel<S, L, Z>, sm);                                            \
     band_kernel<S, L, Z><<<blocks, 32 * kCostWarps, sm, st>>>(a);                                      \
   } while (0)
 #define PP_BAND_LAUNCH(S, L)                                 \
@@ -1232,7 +1496,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
 #define PP_ROWEXIT_LAUNCH(S, L)                                                                        \
   do {                                                                                                 \
     const size_t smr = S == 0 ? grid_smem_layout(g.nm, g.ns, g.n_lay, 0).bytes : 0;                   \
-    cudaFuncSetAttribute(rowexit_kernel<S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr); \
+    ensure_dyn_smem((const void*)rowexit_kernel<S, L>, smr);                                           \
     rowexit_kernel<S, L><<<blocks, 32 * kCostWarps, smr, st>>>(a, lo_thresh);                          \
   } while (0)
   if (pass == 0 && bisect && src != 2) {
@@ -1247,6 +1511,10 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
     }
   } else if (pass == 0) {
     if (src == 0) PP_COST_LAUNCH_L(0, 0); else if (src == 1) PP_COST_LAUNCH_L(0, 1); else PP_COST_LAUNCH(0, 2, 0);
+  } else if (reuse && tau && src != 2 && 2 * g.nm * g.ns <= kBandCells && sorted_in && !g.is_encdec &&
+             (g.lay_class == kLayDec1 || g.lay_class == kLayEncDec2)) {
+    if (g.lay_class == kLayDec1) band_run_kernel<kLayDec1><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+    else band_run_kernel<kLayEncDec2><<<blocks, 32 * kCostWarps, 0, st>>>(a);
   } else if (tau && src != 2 && 2 * g.nm * g.ns <= kBandCells &&
              (g.lay_class == kLayDec1 || g.lay_class == kLayEncDec2)) {
 #define PP_BAND3(L, Z, E)                                              \

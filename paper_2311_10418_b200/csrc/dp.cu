@@ -780,8 +780,7 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
   const size_t smem = ring_off + (size_t)ring * kChunkBytes;
 #define PP_DP_LAUNCH(M, S, Z)                                                                         \
   do {                                                                                                \
-    cudaFuncSetAttribute(dp_pass_kernel<M, S, Z>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                         (int)smem);                                                                  \
+    ensure_dyn_smem((const void*)dp_pass_kernel<M, S, Z>, smem);                                      \
     dp_pass_kernel<M, S, Z><<<n_items, kDpThreads, smem, st>>>(                                       \
         items, seg_off, blk_base, blk_W, tile_off, seg_band_base, band, cand, cand_off, res, next_buf, \
         gstate, res_by_seg, (int)ring_off, ring);                                                     \
@@ -826,7 +825,7 @@ cudaError_t launch_finalize(const SegDP* dps, const int* best_next, const int64_
                             int32_t* status, int64_t* err_id, cudaStream_t st) {
   const int in_smem = (size_t)max_n * sizeof(int) <= 200 * 1024 ? 1 : 0;
   const size_t smem = in_smem ? (size_t)max_n * sizeof(int) : 0;
-  cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_dyn_smem((const void*)finalize_kernel, smem);
   finalize_kernel<<<n_seg, 256, smem, st>>>(dps, best_next, seg_off, blk_base, tile_off, seg_band_base,
                                             band, stats, ordered, in_smem, stage_count, replicas,
                                             splits, mb_times, count, t_max_used, objective, status,

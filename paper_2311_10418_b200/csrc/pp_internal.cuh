@@ -11,7 +11,29 @@
 
 #include "pipeplan_b200.h"
 
+#include <mutex>
+#include <unordered_map>
+
 namespace ppb {
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is process-wide per (function,
+// device) while contexts plan on many host threads at once (the reference's
+// run_plan pool, driver.cpp:222-242): a thread that LOWERED the limit for its
+// small launch would fail another thread's larger launch in flight with
+// "invalid argument".  So the limit only ever rises, under a lock.
+inline cudaError_t ensure_dyn_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> lim[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = lim[dev & 63][fn];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
 
 constexpr int kWarp = 32;
 constexpr int kMaxLayouts = 64;  // distinct (encoder, decoder) layer layouts

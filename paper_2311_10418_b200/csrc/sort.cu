@@ -328,13 +328,11 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
   const int use_smem = smem_need <= 200 * 1024 ? 1 : 0;
   const size_t smem = use_smem ? smem_need : 0;
   if (W == 1) {
-    cudaFuncSetAttribute(seg_sort_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max<size_t>(smem, 1));
+    ensure_dyn_smem((const void*)seg_sort_kernel<1>, smem);
     seg_sort_kernel<1><<<n_seg, kSortThreads, smem, st>>>(d_in, d_seg_off, d_range, d_keys, d_vals,
                                                           use_smem, d_out, d_in_len, d_tgt_len);
   } else {
-    cudaFuncSetAttribute(seg_sort_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max<size_t>(smem, 1));
+    ensure_dyn_smem((const void*)seg_sort_kernel<3>, smem);
     seg_sort_kernel<3><<<n_seg, kSortThreads, smem, st>>>(d_in, d_seg_off, d_range, d_keys, d_vals,
                                                           use_smem, d_out, d_in_len, d_tgt_len);
   }

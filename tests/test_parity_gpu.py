@@ -130,6 +130,57 @@ def test_random_grid_vs_oracle(planner, orc):
         assert_plan_matches(b, record(a), f"random {k}: n={n} C={C} I={interval} cap={cap}")
 
 
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_slice_reuse_matches_per_slice_pricing(name):
+    """Pass B's diagonal reuse (band_run_kernel: each distinct (micro-batch
+    size, padded length) pair priced once) against pricing every slice
+    (band3_kernel): identical plans, candidate counts and slice counts."""
+    cfg = W.CONFIGS[name]
+    M = {"C1": 64, "C3": 6, "C4": 24}[name]
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    a = capi.Planner(0)
+    b = capi.Planner(0)
+    b.set_tuning(slice_reuse=False)
+    ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    for k in ("ordered", "count", "t_max_used", "objective", "status"):
+        assert ra[k].tobytes() == rb[k].tobytes(), k
+    for q in range(M):
+        m = int(ra["count"][q])
+        for k in ("splits", "mb_times"):
+            assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
+    sa, sb = a.stats(), b.stats()
+    for k in ("candidates_generated", "candidates_evaluated", "slices_pass_b", "transitions_executed"):
+        assert sa[k] == sb[k], k
+    a.close()
+    b.close()
+
+
+def test_slice_reuse_duplicate_heavy_vs_oracle(planner, orc):
+    """Few distinct lengths (long runs), ragged sizes, binding and loose caps,
+    fine and coarse intervals: the reuse path against the C restatement."""
+    grid = capi.synthetic_grid()
+    rng = np.random.default_rng(23)
+    for k in range(40):
+        n = int(rng.integers(1, 1500))
+        distinct = int(rng.choice([1, 2, 5, 30, 200]))
+        vals = rng.choice(np.arange(1, 4097), size=distinct, replace=False)
+        s = np.zeros((n, 3), np.int64)
+        s[:, 0] = rng.permutation(n) * 5 + 3
+        s[:, 1] = rng.choice(vals, size=n)
+        C = int(rng.choice([1, 4, 16]))
+        model = capi.Model.uniform(C, int(rng.integers(1, 4)), False, recompute=int(rng.integers(0, 3)))
+        o = orc.order_samples(s)
+        act = max(orc.slice_cost(grid, model, o, i, i + 1)[1] for i in range(0, n, max(1, n // 50)))
+        act = max(act, orc.slice_cost(grid, model, o, n - 1, n)[1])
+        cap = float(rng.choice([math.inf, 1.0 * act, 3.0 * act, 20.0 * act]))
+        interval = float(rng.choice([1.0, 50.0, 1000.0, 1e5]))
+        a = orc.plan(s, grid, model, C, 1, cap, interval)
+        b = _plan_or_status(lambda: planner.plan(s, grid, model, C, 1, cap, interval))
+        assert_plan_matches(b, record(a), f"dup-heavy {k}: n={n} distinct={distinct} C={C} I={interval}")
+
+
 def test_random_tables_vs_oracle(planner, orc):
     """Generic SliceCostFn path with non-monotone, tie-heavy and negative costs."""
     rng = np.random.default_rng(11)
@@ -318,6 +369,45 @@ def test_concurrent_sub_batches_match_single_stream():
     assert_plan_matches(got, case["expect"], "C3 split")
     a.close()
     b.close()
+
+
+def test_threads_with_own_contexts_mixed_sizes():
+    """Many host threads, one context each, planning small and large
+    mini-batches at once (the reference's run_plan pool, driver.cpp:222-242):
+    every plan equals the single-threaded one.  Regression: per-launch
+    shared-memory limits set by one thread used to fail another thread's
+    larger launch in flight."""
+    import threading
+
+    cfg = W.CONFIGS["C3"]
+    big = W.dataset(cfg, 1)
+    grid, model = W.grid(), W.model(cfg)
+    rng = np.random.default_rng(5)
+    smalls = [big[rng.choice(len(big), int(k), replace=False)] for k in rng.integers(8, 600, 6)]
+    jobs = [big] + smalls
+    ref_p = capi.Planner(0)
+    want = [record(ref_p.plan(s, grid, model, cfg.stages, 1, cfg.mem_cap, cfg.interval)) for s in jobs]
+    ref_p.close()
+    errors = []
+
+    def worker(t):
+        p = capi.Planner(0)
+        try:
+            for it in range(6):
+                k = (t + it) % len(jobs)
+                got = p.plan(jobs[k], grid, model, cfg.stages, 1, cfg.mem_cap, cfg.interval)
+                assert_plan_matches(got, want[k], f"thread {t} job {k}")
+        except BaseException as e:  # noqa: BLE001 - surfaced below
+            errors.append(e)
+        finally:
+            p.close()
+
+    ts = [threading.Thread(target=worker, args=(t,)) for t in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[0]
 
 
 def test_presorted_arbitrary_order_matches_oracle(planner, orc):
