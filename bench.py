@@ -315,7 +315,7 @@ def main():
         def aggregate(sts):
             kern = np.zeros(8)
             launches = np.zeros(8, np.int64)
-            agg = {k: 0 for k in ("tr", "ref_tr", "evals", "gen", "sl_a", "sl_b", "bound_tr")}
+            agg = {k: 0 for k in ("tr", "ref_tr", "evals", "gen", "sl_a", "sl_b", "bound_tr", "band_b")}
             for s in sts:
                 kern += np.array(s["ms_kernel"])
                 launches += np.array(s["launches"], np.int64)
@@ -326,6 +326,7 @@ def main():
                 agg["sl_a"] += s["slices_pass_a"]
                 agg["sl_b"] += s["slices_pass_b"]
                 agg["bound_tr"] += s["bound_transitions"]
+                agg["band_b"] += s["band_bytes"]
             return kern, launches, agg
 
         kern, launches, agg = aggregate(stats)
@@ -336,10 +337,16 @@ def main():
         #           7 FP64 ops + scale = 8 ... counted as 11 with the clamp/compare
         #   pass B: slice time per (layout, kind): 2 blends x 7 + 2 DMUL + 1 DADD = 17 FP64 ops
         #   DP: one 8-byte band entry streamed per transition
+        # pass B on sorted single-input (GPT) mini-batches prices each distinct
+        # (micro-batch size, padded length) pair once and streams the band out:
+        # bound by the band bytes it writes; otherwise by FP64 pricing per slice
+        reuse = not cfg.encdec
+
         def work_of(agg):
             return {
                 2: ("fp64", agg["sl_a"] * 11 * kl, "11 FP64 ops per act_mem pricing per (layout, kind)"),
-                3: ("fp64", agg["sl_b"] * 17 * kl, f"{17 * kl} FP64 ops per band slice"),
+                3: (("hbm", agg["band_b"], "8 B per band entry written (32-row tiles incl. masked entries)")
+                    if reuse else ("fp64", agg["sl_b"] * 17 * kl, f"{17 * kl} FP64 ops per band slice")),
                 4: ("hbm", agg["bound_tr"] * 8, "8 B band entry per transition"),
                 5: ("hbm", (agg["tr"] - agg["bound_tr"]) * 8, "8 B band entry per transition"),
             }

@@ -110,7 +110,15 @@ typedef struct pp_tuning {
   int32_t no_slice_reuse;  /* 1: price every band slice; 0 (default): sorted single-input
                               mini-batches price each distinct (micro-batch size, padded
                               length) pair once and copy it along the band's diagonal */
-  int32_t reserved[3];
+  int32_t no_band_trunc;   /* 1: candidate DP passes stream every tile column; 0 (default):
+                              on certified length-sorted tiles they stop at the first
+                              32-column chunk whose slices all exceed the candidate */
+  int32_t compact_band;    /* 1: length-sorted single-input mini-batches get compact far
+                              chunk records (the distinct diagonal windows, ~1/4 of the
+                              DP's band traffic) instead of the dense band; 0 (default):
+                              dense — the DP passes are issue-bound on a B200, and the
+                              record indirection costs more than the bytes it saves */
+  int32_t reserved[1];
 } pp_tuning;
 
 /* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are
@@ -156,6 +164,7 @@ typedef struct pp_stats {
   double  exit_thresh;            /* pass-A certified row-exit threshold (+inf: none) */
   int64_t slices_pass_b;          /* memory-feasible band slices priced by cost pass B */
   int64_t bound_transitions;      /* DP transitions of the bound pass (t = +inf)       */
+  int64_t band_bytes;             /* band written by cost pass B (32-row tiles, 8 B/entry) */
 } pp_stats;
 
 typedef struct pp_ctx pp_ctx;

@@ -74,7 +74,8 @@ class DpOptions(C.Structure):
 
 class Tuning(C.Structure):
     _fields_ = [("first_wave", C.c_int32), ("max_wave", C.c_int32), ("streams", C.c_int32),
-                ("coop_min_n", C.c_int32), ("no_slice_reuse", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("coop_min_n", C.c_int32), ("no_slice_reuse", C.c_int32), ("no_band_trunc", C.c_int32),
+                ("compact_band", C.c_int32), ("reserved", C.c_int32 * 1)]
 
 
 class PlanOut(C.Structure):
@@ -96,7 +97,7 @@ class Stats(C.Structure):
                 ("ms_kernel", C.c_double * 8), ("launches", C.c_int64 * 8),
                 ("dp_band_bytes", C.c_int64), ("slices_pass_a", C.c_int64),
                 ("exit_thresh", C.c_double), ("slices_pass_b", C.c_int64),
-                ("bound_transitions", C.c_int64)]
+                ("bound_transitions", C.c_int64), ("band_bytes", C.c_int64)]
 
     def as_dict(self):
         out = {}
@@ -312,8 +313,9 @@ class Planner:
         return (lib.pp_ctx_last_error(self._h) or b"").decode()
 
     def set_tuning(self, first_wave: int = 1, max_wave: int = 16, streams: int = 1, coop_min_n: int = 0,
-                   slice_reuse: bool = True):
-        t = Tuning(first_wave, max_wave, streams, coop_min_n, 0 if slice_reuse else 1)
+                   slice_reuse: bool = True, band_trunc: bool = True, compact_band: bool = False):
+        t = Tuning(first_wave, max_wave, streams, coop_min_n, 0 if slice_reuse else 1, 0 if band_trunc else 1,
+                   1 if compact_band else 0)
         rc = lib.pp_ctx_set_tuning(self._h, C.byref(t))
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())

@@ -59,7 +59,8 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              double interval, int* row_w, int* row_fb, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
-                             double lo_thresh, int bisect, int sorted_in, int reuse, cudaStream_t st);
+                             double lo_thresh, int bisect, int sorted_in, int reuse, double* cmin,
+                             short* colbase, int* chunk_nv, int* wrote_cmin, cudaStream_t st);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
                              int* row_w, int* blk_W, cudaStream_t st);
 cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -67,7 +68,8 @@ cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_
                              const double* band, double interval, const SegStats* stats,
                              unsigned int* bitmap, const int64_t* bitmap_off, const int* seg_mode,
                              unsigned long long* cand_raw, const int64_t* cand_raw_off,
-                             unsigned long long* cand_raw_cnt, cudaStream_t st);
+                             unsigned long long* cand_raw_cnt, const short* colbase, const int* row_w,
+                             cudaStream_t st);
 cudaError_t launch_tile_offsets(const int* blk_W, const int* blk_base, int n_seg, int64_t* tile_off,
                                 SegStats* stats, cudaStream_t st);
 cudaError_t launch_cand_bitmap(const unsigned int* bitmap, const int64_t* bitmap_off,
@@ -86,7 +88,9 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int* blk_base, const int* blk_W, const int64_t* tile_off,
                            const int64_t* seg_band_base, const double* band, const double* cand,
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
-                           int res_by_seg, cudaStream_t st);
+                           int res_by_seg, const double* cmin, double t_margin,
+                           unsigned long long* cols_streamed, const short* colbase, const int* chunk_nv,
+                           const int* row_w, cudaStream_t st);
 cudaError_t launch_mb_shapes(const pp_sample* ordered, const int64_t* seg_off, const int32_t* splits,
                              const int64_t* mb_off, int n_seg, int64_t n_mb, pp_padded_shape* shapes,
                              cudaStream_t st);
@@ -109,10 +113,10 @@ cudaError_t launch_select(const WorkItem* items, const ItemResult* res, const in
                           int stage_count, int replicas, SegDP* dps, int n_seg, cudaStream_t st);
 cudaError_t launch_finalize(const SegDP* dps, const int* best_next, const int64_t* seg_off,
                             const int* blk_base, const int64_t* tile_off, const int64_t* seg_band_base,
-                            const double* band, const SegStats* stats, const pp_sample* ordered,
-                            int stage_count, int replicas, int max_n, int n_seg, int32_t* splits,
-                            double* mb_times, int32_t* count, double* t_max_used, double* objective,
-                            int32_t* status, int64_t* err_id, cudaStream_t st);
+                            const double* band, const SegStats* stats, const short* colbase,
+                            const pp_sample* ordered, int stage_count, int replicas, int max_n, int n_seg,
+                            int32_t* splits, double* mb_times, int32_t* count, double* t_max_used,
+                            double* objective, int32_t* status, int64_t* err_id, cudaStream_t st);
 }  // namespace ppb
 
 using namespace ppb;
@@ -186,13 +190,16 @@ struct pp_ctx {
       bound_items, bound_res;
   DevBuf out_splits, out_times, out_count, out_tmax, out_obj, out_status, out_err;
   PinBuf h_range, h_stats, h_segdp;
-  DevBuf small_bm, coop_state, coop_parts, shapes, stage_lay, mb_off, oc_tf, oc_tb, oc_act;
+  DevBuf small_bm, coop_state, coop_parts, shapes, stage_lay, mb_off, oc_tf, oc_tb, oc_act, cmin, dp_cols,
+      colbase, chunk_nv;
   // host copy of the uploaded grid (restricted to the recompute strategy)
   // for the monotonicity certificate of cost pass A
   std::vector<double> h_ax, h_cells;
   std::vector<Layout> h_lay;
   int h_nm = 0, h_ns = 0, h_encdec = 0;
   double exit_thresh = INFINITY;  // last call's pass-A row-exit threshold
+  double trunc_margin = INFINITY; // candidate-pass truncation margin 2E (+inf: off)
+  bool compact = false;           // the band holds compact chunk records (pp_internal.cuh)
   CostGrid grid_dev{};            // device view of the uploaded grid
   bool grid_valid = false;
   double tau_interval = -1.0;     // interval the device bin thresholds were built for
@@ -210,7 +217,8 @@ struct pp_ctx {
             &raw_cnt, &raw_in_tmp, &cand, &cand_off, &cand_n, &active, &items, &results, &next_buf,
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
             &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
-            &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act};
+            &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act,
+            &cmin, &dp_cols, &colbase, &chunk_nv};
   }
 };
 
@@ -463,11 +471,18 @@ double dkey_inv_host(unsigned long long k) {
 // analysis gives |v~ - v| <= 72 u A (1 + |tm|)(1 + |ts|) per weighted field,
 // u = 2^-53; we use 128 u.  Returns +inf (no certificate: full scan) when a
 // condition fails or is within 1e-12 relative of failing.
-double mem_exit_threshold(const pp_ctx* ctx, double cap, int max_n, double seq_lo[2],
-                          double seq_hi[2], double* lo_thresh) {
-  const double INF = INFINITY;
-  *lo_thresh = -INF;
-  if (!(cap < INF) || std::isnan(cap)) return INF;
+// Certified forward error bound of a slice value priced on the grid: the sum
+// over `fields` [f0, f1] of the cell surfaces (0 t_f, 1 t_b, 2 act), scaled
+// by the layer multiples of every stage layout.  Returns E with
+// |computed - exact| <= E for every slice of the call, PROVIDED each used
+// kind's surfaces are nondecreasing along both grid axes (checked here,
+// including the extrapolated ends the call's micro-batch sizes and lengths
+// reach) — so the exact value is nondecreasing in the slice end j of a row of
+// a length-sorted segment.  +inf when not certified.  `k_ulp` sizes the
+// per-value rounding budget (the blends, the layer products and the sums).
+long double surface_error_bound(const pp_ctx* ctx, int max_n, const double seq_lo[2], const double seq_hi[2],
+                                int f0, int f1, long double k_ulp) {
+  const long double BAD = INFINITY;
   const int nm = ctx->h_nm, ns = ctx->h_ns;
   const double* mbs_ax = ctx->h_ax.data();
   const double* seq_ax = ctx->h_ax.data() + nm;
@@ -501,39 +516,43 @@ double mem_exit_threshold(const pp_ctx* ctx, double cap, int max_n, double seq_l
     const long double ts_hi = tpos(seq_ax, ns, hi, sg);
     const int ts_hi_seg = sg;
     ts_abs[k] = std::max({1.0L, std::fabs(ts_lo), std::fabs(ts_hi)});
-    auto c = [&](int mi, int si) -> long double {
-      return ctx->h_cells[k * per + ((size_t)mi * ns + si) * 3 + 2];
-    };
-    auto nonneg = [](long double v, long double scale) { return v >= 1e-12L * scale; };
-    for (int mi = 0; mi < nm; ++mi)
-      for (int si = 0; si < ns; ++si) {
-        const long double v = c(mi, si);
-        if (!std::isfinite((double)v)) return INF;
-        A[k] = std::max(A[k], std::fabs(v));
-        if (mi + 1 < nm && !(c(mi + 1, si) >= v)) return INF;
-        if (si + 1 < ns && !(c(mi, si + 1) >= v)) return INF;
+    for (int f = f0; f <= f1; ++f) {
+      auto c = [&](int mi, int si) -> long double {
+        return ctx->h_cells[k * per + ((size_t)mi * ns + si) * 3 + f];
+      };
+      auto nonneg = [](long double v, long double scale) { return v >= 1e-12L * scale; };
+      long double af = 0.0L;
+      for (int mi = 0; mi < nm; ++mi)
+        for (int si = 0; si < ns; ++si) {
+          const long double v = c(mi, si);
+          if (!std::isfinite((double)v)) return BAD;
+          af = std::max(af, std::fabs(v));
+          if (mi + 1 < nm && !(c(mi + 1, si) >= v)) return BAD;
+          if (si + 1 < ns && !(c(mi, si + 1) >= v)) return BAD;
+        }
+      A[k] += af;
+      // extrapolated sequence positions: d/dtm >= 0 at ts_lo (first segment)
+      // and ts_hi (last segment), for every mbs segment
+      for (int mi = 0; mi + 1 < nm && ns > 1; ++mi) {
+        for (int e = 0; e < 2; ++e) {
+          const long double ts = e ? ts_hi : ts_lo;
+          if (ts >= 0.0L && ts <= 1.0L) continue;
+          const int si = e ? ts_hi_seg : ts_lo_seg;
+          const long double d0 = c(mi + 1, si) - c(mi, si), d1 = c(mi + 1, si + 1) - c(mi, si + 1);
+          if (!nonneg((1.0L - ts) * d0 + ts * d1, (std::fabs(d0) + std::fabs(d1)) * (1.0L + std::fabs(ts))))
+            return BAD;
+        }
       }
-    // extrapolated sequence positions: d/dtm >= 0 at ts_lo (first segment)
-    // and ts_hi (last segment), for every mbs segment
-    for (int mi = 0; mi + 1 < nm && ns > 1; ++mi) {
-      for (int e = 0; e < 2; ++e) {
-        const long double ts = e ? ts_hi : ts_lo;
-        if (ts >= 0.0L && ts <= 1.0L) continue;
-        const int si = e ? ts_hi_seg : ts_lo_seg;
-        const long double d0 = c(mi + 1, si) - c(mi, si), d1 = c(mi + 1, si + 1) - c(mi, si + 1);
-        if (!nonneg((1.0L - ts) * d0 + ts * d1, (std::fabs(d0) + std::fabs(d1)) * (1.0L + std::fabs(ts))))
-          return INF;
-      }
-    }
-    // extrapolated micro-batch sizes: d/dts >= 0 at tm_lo / tm_hi
-    for (int si = 0; si + 1 < ns && nm > 1; ++si) {
-      for (int e = 0; e < 2; ++e) {
-        const long double tm = e ? tm_hi : tm_lo;
-        if (tm >= 0.0L && tm <= 1.0L) continue;
-        const int mi = e ? tm_hi_seg : tm_lo_seg;
-        const long double e0 = c(mi, si + 1) - c(mi, si), e1 = c(mi + 1, si + 1) - c(mi + 1, si);
-        if (!nonneg((1.0L - tm) * e0 + tm * e1, (std::fabs(e0) + std::fabs(e1)) * (1.0L + std::fabs(tm))))
-          return INF;
+      // extrapolated micro-batch sizes: d/dts >= 0 at tm_lo / tm_hi
+      for (int si = 0; si + 1 < ns && nm > 1; ++si) {
+        for (int e = 0; e < 2; ++e) {
+          const long double tm = e ? tm_hi : tm_lo;
+          if (tm >= 0.0L && tm <= 1.0L) continue;
+          const int mi = e ? tm_hi_seg : tm_lo_seg;
+          const long double e0 = c(mi, si + 1) - c(mi, si), e1 = c(mi + 1, si + 1) - c(mi + 1, si);
+          if (!nonneg((1.0L - tm) * e0 + tm * e1, (std::fabs(e0) + std::fabs(e1)) * (1.0L + std::fabs(tm))))
+            return BAD;
+        }
       }
     }
   }
@@ -545,7 +564,16 @@ double mem_exit_threshold(const pp_ctx* ctx, double cap, int max_n, double seq_l
     worst = std::max(worst, w);
   }
   const long double u = std::ldexp(1.0L, -53);
-  const long double E = 128.0L * u * (1.0L + tm_abs) * 2.0L * worst + 1e-300L;
+  return k_ulp * u * (1.0L + tm_abs) * 2.0L * worst + 1e-300L;
+}
+
+double mem_exit_threshold(const pp_ctx* ctx, double cap, int max_n, double seq_lo[2],
+                          double seq_hi[2], double* lo_thresh) {
+  const double INF = INFINITY;
+  *lo_thresh = -INF;
+  if (!(cap < INF) || std::isnan(cap)) return INF;
+  const long double E = surface_error_bound(ctx, max_n, seq_lo, seq_hi, 2, 2, 128.0L);
+  if (!std::isfinite((double)E)) return INF;
   double th = (double)((long double)cap + 2.0L * E);
   th = std::nextafter(std::nextafter(th, INF), INF);
   if (!std::isfinite(th)) return INF;
@@ -554,6 +582,19 @@ double mem_exit_threshold(const pp_ctx* ctx, double cap, int max_n, double seq_l
   double tl = (double)((long double)cap - 2.0L * E);
   *lo_thresh = std::nextafter(std::nextafter(tl, -INF), -INF);
   return th;
+}
+
+// Margin 2E of the candidate passes' band truncation (dp.cu): a far chunk
+// whose first column prices above t + 2E on every live row has, on a
+// length-sorted segment, only slices above t from there on.  +inf: not
+// certified (no truncation).
+double time_trunc_margin(const pp_ctx* ctx, int max_n, const double seq_lo[2], const double seq_hi[2]) {
+  // the slice time sums two blends per kind (t_f, t_b) through the layer
+  // products: a doubled rounding budget over the act_mem certificate's
+  const long double E = surface_error_bound(ctx, max_n, seq_lo, seq_hi, 0, 1, 256.0L);
+  if (!std::isfinite((double)E)) return INFINITY;
+  const double m = std::nextafter((double)(2.0L * E), (double)INFINITY);
+  return std::isfinite(m) ? m : INFINITY;
 }
 
 // Steps 1-2 (+ tile offsets): sort, block bookkeeping, cost pass A.  Leaves
@@ -654,7 +695,8 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                    ctx->blk_base.as<int>(), n_seg, total_blocks, max_n, ctx->mbp.as<AxisPos>(),
                                    cap, interval, ctx->row_w.as<int>(), ctx->row_fb.as<int>(), ctx->blk_W.as<int>(),
                                    ctx->stats_d.as<SegStats>(), nullptr, nullptr, nullptr, exit_thresh,
-                                   nullptr, nullptr, lo_thresh, bisect, 0, 0, st));
+                                   nullptr, nullptr, lo_thresh, bisect, 0, 0, nullptr, nullptr, nullptr,
+                                   nullptr, st));
     PP_TIMED(1, launch_tile_offsets(ctx->blk_W.as<int>(), ctx->blk_base.as<int>(), n_seg,
                                     ctx->tile_off.as<int64_t>(), ctx->stats_d.as<SegStats>(), st));
   }
@@ -672,6 +714,23 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   PP_CUDA(cudaMemcpyAsync(ctx->band_base.p, band_base.data(), n_seg * sizeof(int64_t),
                           cudaMemcpyHostToDevice, st));
   // (no fill: pass B writes every tile entry, NaN where no slice is feasible)
+  // Per-chunk minimum slice times for the candidate passes' truncation (dp.cu):
+  // one slot per 1024 band entries plus one per block bounds every tile's chunks.
+  double* cmin = nullptr;
+  short* colbase = nullptr;
+  int* chunk_nv = nullptr;
+  if (!table && total > 0) {
+    const int64_t ids = (band_total >> 10) + 2 * (int64_t)total_blocks + 64;  // chunk_id0 range
+    PP_CUDA(ctx->cmin.ensure(ids * sizeof(double)));
+    cmin = ctx->cmin.as<double>();
+    if (ctx->tuning.compact_band) {
+      PP_CUDA(ctx->colbase.ensure(ids * 32 * sizeof(short)));
+      PP_CUDA(ctx->chunk_nv.ensure(ids * sizeof(int)));
+      colbase = ctx->colbase.as<short>();
+      chunk_nv = ctx->chunk_nv.as<int>();
+    }
+  }
+  int wrote_cmin = 0;
   // Pass B: band + candidate statistics.
   if (total > 0)
     PP_TIMED(3, launch_cost_pass(1, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
@@ -681,7 +740,19 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                  ctx->stats_d.as<SegStats>(), ctx->tile_off.as<int64_t>(),
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), INFINITY, small_bm,
                                  tau_d, -INFINITY, 0, c.presorted ? 0 : 1,
-                                 ctx->tuning.no_slice_reuse ? 0 : 1, st));
+                                 ctx->tuning.no_slice_reuse ? 0 : 1, cmin, colbase, chunk_nv, &wrote_cmin,
+                                 st));
+  ctx->trunc_margin = INFINITY;
+  ctx->compact = (wrote_cmin & 2) != 0;
+  if ((wrote_cmin & 1) && !ctx->tuning.no_band_trunc) {
+    const unsigned long long* hr = ctx->h_range.as<unsigned long long>();
+    double lo[2], hi[2];
+    for (int q = 0; q < 2; ++q) {
+      lo[q] = (double)(long long)(hr[q] ^ 0x8000000000000000ULL);
+      hi[q] = (double)(long long)(hr[3 + q] ^ 0x8000000000000000ULL);
+    }
+    ctx->trunc_margin = time_trunc_margin(ctx, max_n, lo, hi);
+  }
   PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
   PP_CUDA(cudaStreamSynchronize(st));
   return PP_OK;
@@ -736,6 +807,7 @@ constexpr int kCoopMaxItems = 8;
 
 bool use_coop(const pp_ctx* ctx, const std::vector<WorkItem>& items, const int64_t* h_seg_off) {
   if (items.empty() || (int)items.size() > kCoopMaxItems) return false;
+  if (ctx->compact) return false;  // the cooperative pass reads the dense band
   const int64_t min_n = ctx->tuning.coop_min_n > 0 ? ctx->tuning.coop_min_n : kCoopMinN;
   for (const WorkItem& w : items)
     if (h_seg_off[w.seg + 1] - h_seg_off[w.seg] < min_n) return false;
@@ -870,7 +942,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                  ctx->stats_d.as<SegStats>(), ctx->bitmap.as<unsigned int>(),
                                  ctx->bitmap_off.as<int64_t>(), ctx->seg_mode.as<int>(),
                                  ctx->raw.as<unsigned long long>(), ctx->raw_off.as<int64_t>(),
-                                 ctx->raw_cnt.as<unsigned long long>(), st));
+                                 ctx->raw_cnt.as<unsigned long long>(),
+                                 ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->row_w.as<int>(), st));
   // ---- 4. candidate lists
   if (single) {
     std::vector<double> infs(cand_off[n_seg], INFINITY);
@@ -941,7 +1014,9 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                    ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
                                    ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
                                    ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
-                                   ctx->gstate.as<double>(), 1, st));
+                                   ctx->gstate.as<double>(), 1, nullptr, 0.0, nullptr,
+                                   ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
+                                   ctx->row_w.as<int>(), st));
       }
       PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
     }
@@ -954,6 +1029,12 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   int wave = std::max(1, ctx->tuning.first_wave);
   const int max_wave = std::max(wave, ctx->tuning.max_wave > 0 ? ctx->tuning.max_wave : 16);
   int64_t transitions = bound_transitions, evaluated = 0, waves = 0;
+  // candidate passes on certified tiles stream only the chunks that can hold
+  // a slice <= t: their transitions are counted on the device
+  const bool trunc = std::isfinite(ctx->trunc_margin);
+  PP_CUDA(ctx->dp_cols.ensure(sizeof(unsigned long long)));
+  PP_CUDA(cudaMemsetAsync(ctx->dp_cols.p, 0, sizeof(unsigned long long), st));
+  bool counted = false;
   std::vector<WorkItem> items;
   std::vector<int> item_start(n_seg), item_cnt(n_seg);
   for (;;) {
@@ -978,7 +1059,6 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
         w.next_off = noff;
         noff += n;
         items.push_back(w);
-        transitions += hs[s].band;
       }
       item_cnt[s] = k;
     }
@@ -1003,12 +1083,18 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       int rc = run_coop(ctx, 0, table ? 1 : 0, items, c, ctx->results.as<ItemResult>(), 0, st);
       if (rc) return rc;
       PP_CUDA(timed_end(ctx));
+      for (const WorkItem& w : items) transitions += hs[w.seg].band;
     } else {
       PP_TIMED(5, launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_state, state_global, table ? 1 : 0,
                                  dp_budget(ni), c.d_seg_off, ctx->blk_base.as<int>(),
                                  ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
                                  ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
-                                 ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, st));
+                                 ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0,
+                                 trunc ? ctx->cmin.as<double>() : nullptr, ctx->trunc_margin,
+                                 ctx->dp_cols.as<unsigned long long>(),
+                                 ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
+                                 ctx->row_w.as<int>(), st));
+      counted = true;
     }
     PP_TIMED(7, launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
                               ctx->seg_item_start.as<int>(), ctx->seg_item_cnt.as<int>(),
@@ -1023,11 +1109,16 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   PP_TIMED(7, launch_finalize(ctx->segdp.as<SegDP>(), ctx->best_next.as<int>(), c.d_seg_off,
                               ctx->blk_base.as<int>(), ctx->tile_off.as<int64_t>(),
                               ctx->band_base.as<int64_t>(), ctx->band.as<double>(),
-                              ctx->stats_d.as<SegStats>(), c.d_ordered, c.opts.stage_count,
+                              ctx->stats_d.as<SegStats>(), ctx->compact ? ctx->colbase.as<short>() : nullptr,
+                              c.d_ordered, c.opts.stage_count,
                               c.opts.replica_count, std::max(max_n, 1), n_seg, c.d_splits, c.d_times,
                               c.d_count, c.d_tmax, c.d_obj, c.d_status, c.d_err, st));
+  unsigned long long dp_cols = 0;
+  if (counted)
+    PP_CUDA(cudaMemcpyAsync(&dp_cols, ctx->dp_cols.p, sizeof(dp_cols), cudaMemcpyDeviceToHost, st));
   PP_CUDA(cudaStreamSynchronize(st));
   PP_CUDA(cudaGetLastError());
+  transitions += (int64_t)dp_cols * kRB;
 
   // stats
   const SegDP* hd = ctx->h_segdp.as<SegDP>();
@@ -1052,6 +1143,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     S.launches[ctx->kcat[k]] += 1;
   }
   S.dp_band_bytes = transitions * (int64_t)sizeof(double);
+  S.band_bytes = ctx->band_total * (int64_t)sizeof(double);
   S.exit_thresh = ctx->exit_thresh;
   for (int s = 0; s < n_seg; ++s) {
     S.slices_pass_a += (int64_t)hs[s].priced;
@@ -1175,6 +1267,7 @@ int plan_split(pp_ctx* ctx, const PlanCall& c, int parts) {
     S.dp_band_bytes += t.dp_band_bytes;
     S.slices_pass_a += t.slices_pass_a;
     S.slices_pass_b += t.slices_pass_b;
+    S.band_bytes += t.band_bytes;
     S.bound_transitions += t.bound_transitions;
     S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
   }
@@ -1422,6 +1515,7 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
         S.dp_band_bytes += t.dp_band_bytes;
         S.slices_pass_a += t.slices_pass_a;
         S.slices_pass_b += t.slices_pass_b;
+        S.band_bytes += t.band_bytes;
         S.bound_transitions += t.bound_transitions;
         S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
       }
@@ -1451,6 +1545,7 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
     S.dp_band_bytes += t.dp_band_bytes;
     S.slices_pass_a += t.slices_pass_a;
     S.slices_pass_b += t.slices_pass_b;
+    S.band_bytes += t.band_bytes;
     S.bound_transitions += t.bound_transitions;
     S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
   }

@@ -111,6 +111,16 @@ struct CostArgs {
   // no division (monotone, correctly rounded division; capi.cu bin_thresholds)
   unsigned int* small_bm;
   const double* tau;
+  // pass B (band_run_kernel): per far chunk k of a tile (the DP's columns
+  // [64 + 32k, 96 + 32k)), the least slice time (act_mem ignored) over the
+  // live rows at its first column; slot ((tile base) >> 10) + k.  Lets the DP
+  // candidate passes stop streaming a tile where every row has passed t
+  // (dp.cu; capi.cu time_trunc_margin).  Null: not recorded.
+  double* cmin;
+  // pass B (band_run_kernel<.., true>): compact chunk records instead of the
+  // dense band (pp_internal.cuh "compact band"); null: dense band
+  short* colbase;
+  int* chunk_nv;
 };
 
 // SRC: 0 = fused grid costing, grid staged in shared memory
@@ -749,7 +759,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
 // it (a range-max over the tile's row widths: rows r' with d <= w_r' whose
 // column r' + d lies in the run), so the candidate set is the reference's
 // exactly.  The store stream is the kernel's bound rather than FP64 issue.
-template <int LAY>
+template <int LAY, bool COMPACT>
 __global__ void __launch_bounds__(32 * kCostWarps)
     band_run_kernel(CostArgs a) {
   __shared__ double4 s_tt[kBandCells];
@@ -758,6 +768,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
   __shared__ double s_x[kCostWarps][32];
   __shared__ AxisPos s_px[kCostWarps][32];
   __shared__ double s_ring[kCostWarps][128];
+  __shared__ short s_cb[kCostWarps][32];
   __shared__ int s_rmq[kCostWarps][5][32];
   __shared__ unsigned int s_bm[kCostWarps][kSmallBmWords];
   const int nm = a.g.nm, ns = a.g.ns;
@@ -791,8 +802,8 @@ __global__ void __launch_bounds__(32 * kCostWarps)
     const double2 c0 = s_am[base + mb + sg], c1 = s_am[base + mb + s1];
     return blend_d(tm, ts, c0.x, c0.y, c1.x, c1.y);
   };
-  // slice time, NaN where act_mem exceeds the cap (band3_kernel's operations)
-  auto price = [&](const AxisPos& mb, const AxisPos& pe) {
+  // slice time (band3_kernel's operations)
+  auto price_t = [&](const AxisPos& mb, const AxisPos& pe) {
     double df, db;
     kind_time(per, mb.pad, mb.t, pe.seg, pe.t, df, db);
     const double t2 = __dadd_rn(__dmul_rn(ld, df), __dmul_rn(ld, db));
@@ -803,6 +814,11 @@ __global__ void __launch_bounds__(32 * kCostWarps)
       const double t1 = __dadd_rn(__dmul_rn(le, ef), __dmul_rn(le, eb));
       T = (t1 < t2) ? t2 : t1;
     }
+    return T;
+  };
+  // ... NaN where act_mem exceeds the cap
+  auto price = [&](const AxisPos& mb, const AxisPos& pe) {
+    double T = price_t(mb, pe);
     if (need_mem) {
       double M = __dmul_rn(ld, kind_mem(per, mb.pad, mb.t, pe.seg, pe.t));
       if (LAY != kLayDec1) {
@@ -872,27 +888,38 @@ __global__ void __launch_bounds__(32 * kCostWarps)
     };
     const int W = a.blk_W[gb];
     double* tile = a.band + a.seg_band_base[s] + a.tile_off[gb];
-    tile[r] = QNAN;  // column 0: j = i0 <= i is never a slice
+    const int64_t cid = chunk_id0(a.seg_band_base[s] + a.tile_off[gb], gb);  // record of column chunk 0
     double* ring = s_ring[wid];
     double prev_x = QNAN;  // NaN: the first column starts a run
     AxisPos pe = p0;       // sequence bracket of the current run
     int ca = 0, cb = 0;    // the run's first and last column (within the tile)
     int done = 0;          // the run's diagonals up to `done` are in the ring
-    for (int c0 = 1; c0 < W; c0 += 32) {
+    // 32-column chunks aligned with the DP's (column 0 = the never-live
+    // diagonal, a one-column run of its own)
+    for (int c0 = 0; c0 < W; c0 += 32) {
+      const int kk = c0 >> 5;
       const int cq = c0 + lane;
       double xq = QNAN;
-      if (cq < W) {
+      AxisPos pxq = p0;
+      if (cq < W && cq > 0) {
         const int64_t k = b0 + i0 + cq - 1;
         xq = a.in_d[k];
-        s_x[wid][lane] = xq;
-        s_px[wid][lane] = a.pin[k];
+        pxq = a.pin[k];
       }
+      s_x[wid][lane] = xq;
+      s_px[wid][lane] = pxq;
       // bit q: column c0 + q ends its run (the next column differs or is past the tile)
       double xn = __shfl_down_sync(0xffffffffu, xq, 1);
       if (lane == 31) xn = (cq + 1 < W) ? a.in_d[b0 + i0 + cq] : QNAN;
       const unsigned int run_end = __ballot_sync(0xffffffffu, !(xn == xq));
       __syncwarp();
       const int qend = min(32, W - c0);
+      // far chunks (kk >= 2) of a COMPACT band hold records; the near tile
+      // (columns [0, 64), the DP's serial triangle) stays dense
+      const bool rec = COMPACT && kk >= 2;
+      double* vals = tile + (size_t)c0 * kRB;  // the chunk's region: its record
+      int voff = 0;                            // values written to the record
+      double vfirst = QNAN;                    // the lane's entry at the chunk's first column
       for (int q = 0; q < qend;) {
         const unsigned int e = run_end >> q;
         const int qe = min(e ? q + __ffs(e) - 1 : 31, qend - 1);
@@ -923,8 +950,15 @@ __global__ void __launch_bounds__(32 * kCostWarps)
             const int d = cs - r;
             const double F = price(a.mbp[min(max(d, 1), a.max_n)], pe);
             const bool live = (unsigned)(d - 1) < (unsigned)wr;
-            tile[(size_t)cs * kRB + r] = live ? F : QNAN;
+            if (rec) {
+              vals[voff + 31 - r] = F;  // window d in [cs - 31, cs]
+              if (lane == 0) s_cb[wid][q] = (short)(voff + 31);
+              voff += 32;
+            } else {
+              tile[(size_t)cs * kRB + r] = live ? F : QNAN;
+            }
             if (live && !isnan(F)) bin(F);
+            if (q == 0) vfirst = F;
             q = qe + 1;
             continue;
           }
@@ -941,7 +975,14 @@ __global__ void __launch_bounds__(32 * kCostWarps)
           done += 32;
         }
         __syncwarp();
-        {
+        if (q == 0) vfirst = ring[(cs - r) & 127];
+        if (rec) {
+          // the piece's window d in [cs - 31, ce]; column c reads it at c - cs + 31 - r
+          const int L = ce - cs + 32;
+          for (int idx = lane; idx < L; idx += 32) vals[voff + idx] = ring[(cs - 31 + idx) & 127];
+          if (lane <= qe - q) s_cb[wid][q + lane] = (short)(voff + lane + 31);
+          voff += L;
+        } else {
           // column c: lane r stores ring[d = c - r], live iff 1 <= d <= w_r
           double* out = tile + (size_t)cs * kRB + r;
           int d = cs - r;
@@ -956,6 +997,27 @@ __global__ void __launch_bounds__(32 * kCostWarps)
         __syncwarp();
         q = qe + 1;
       }
+      if (rec) {
+        __syncwarp();
+        a.colbase[(cid + kk) * 32 + lane] = lane < qend ? s_cb[wid][lane] : (short)0;
+        if (lane == 0) a.chunk_nv[cid + kk] = voff;
+      }
+      // far chunk (kk >= 2): least slice time over the live rows at its first
+      // column (act_mem-masked entries re-priced), for the DP's truncation
+      if (a.cmin && kk >= 2) {
+        const int d = c0 - r;
+        double v = vfirst;
+        const bool live = (unsigned)(d - 1) < (unsigned)wr;
+        if (live && isnan(v)) v = price_t(a.mbp[min(max(d, 1), a.max_n)], pe);
+        v = live ? v : INF;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const double y = __shfl_xor_sync(0xffffffffu, v, o);
+          v = (y < v) ? y : v;
+        }
+        if (lane == 0) a.cmin[cid + kk] = v;
+      }
+      __syncwarp();
     }
     const unsigned int npriced = (unsigned int)wr;  // live slices of the row: columns r+1 .. r+wr
     if (cbits) atomicOr(&s_bm[wid][cw], cbits);
@@ -1250,7 +1312,8 @@ __global__ void __launch_bounds__(256)
                      const int64_t* __restrict__ bitmap_off, const int* __restrict__ seg_mode,
                      unsigned long long* __restrict__ cand_raw,
                      const int64_t* __restrict__ cand_raw_off,
-                     unsigned long long* __restrict__ cand_raw_cnt) {
+                     unsigned long long* __restrict__ cand_raw_cnt, const short* __restrict__ colbase,
+                     const int* __restrict__ row_w) {
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (blockDim.x >> 5);
   for (int gb = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gb < total_blocks; gb += warps) {
@@ -1262,8 +1325,27 @@ __global__ void __launch_bounds__(256)
     const double kmin = mode == 0 ? dkey_inv(stats[s].kmin) : 0.0;
     unsigned int* bm = bitmap + bitmap_off[s];
     long long last_bit = -1;
+    // compact band (pp_internal.cuh): entry (lane, c) of a live slice is
+    // record value colbase[c] - lane; other entries are masked here
+    int wr = 0;
+    int64_t cid = 0;
+    if (colbase) {
+      const int n = (int)(seg_off[s + 1] - seg_off[s]);
+      const int i1 = n - kRB * (gb - blk_base[s]);
+      const int i0 = max(0, i1 - kRB);
+      wr = lane < i1 - i0 ? row_w[seg_off[s] + i0 + lane] : 0;
+      cid = chunk_id0(seg_band_base[s] + tile_off[gb], gb);
+    }
     for (int c = 1; c < W; ++c) {
-      const double T = tile[(size_t)c * kRB + lane];
+      double T;
+      if (colbase && c >= 64) {
+        const int kk = c >> 5;
+        T = (unsigned)(c - lane - 1) < (unsigned)wr
+                ? tile[(size_t)kk * (32 * kRB) + colbase[(cid + kk) * 32 + (c & 31)] - lane]
+                : __longlong_as_double(0x7ff8000000000000LL);
+      } else {
+        T = tile[(size_t)c * kRB + lane];
+      }
       if (isnan(T)) continue;
       double q = T;
       if (interval > 0) q = ceil(__ddiv_rn(T, interval));
@@ -1464,10 +1546,12 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              double interval, int* row_w, int* row_fb, int* blk_W, SegStats* stats,
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
-                             double lo_thresh, int bisect, int sorted_in, int reuse, cudaStream_t st) {
+                             double lo_thresh, int bisect, int sorted_in, int reuse, double* cmin,
+                             short* colbase, int* chunk_nv, int* wrote_cmin, cudaStream_t st) {
   CostArgs a{g, tabT, tabM, in_d, tgt_d, pin, ptg, seg_off, blk_base, n_seg, total_blocks, max_n, mbp,
              cap, interval, row_w, row_fb, blk_W, stats, tile_off, seg_band_base, band, exit_thresh,
-             small_bm, tau};
+             small_bm, tau, cmin, colbase, chunk_nv};
+  if (wrote_cmin) *wrote_cmin = 0;
   const GridSmem L = grid_smem_layout(g.nm, g.ns, g.n_lay, tau ? kSmallBmWords * 32 : 0);
   const int src = tabT ? 2 : (L.bytes <= 160 * 1024 ? 0 : 1);
   const size_t sm = src == 0 ? L.bytes : 0;
@@ -1513,8 +1597,19 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
     if (src == 0) PP_COST_LAUNCH_L(0, 0); else if (src == 1) PP_COST_LAUNCH_L(0, 1); else PP_COST_LAUNCH(0, 2, 0);
   } else if (reuse && tau && src != 2 && 2 * g.nm * g.ns <= kBandCells && sorted_in && !g.is_encdec &&
              (g.lay_class == kLayDec1 || g.lay_class == kLayEncDec2)) {
-    if (g.lay_class == kLayDec1) band_run_kernel<kLayDec1><<<blocks, 32 * kCostWarps, 0, st>>>(a);
-    else band_run_kernel<kLayEncDec2><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+    const bool compact = colbase != nullptr;
+    if (!compact) {
+      a.colbase = nullptr;
+      a.chunk_nv = nullptr;
+    }
+    if (g.lay_class == kLayDec1) {
+      if (compact) band_run_kernel<kLayDec1, true><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+      else band_run_kernel<kLayDec1, false><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+    } else {
+      if (compact) band_run_kernel<kLayEncDec2, true><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+      else band_run_kernel<kLayEncDec2, false><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+    }
+    if (wrote_cmin) *wrote_cmin = (cmin ? 1 : 0) | (compact ? 2 : 0);
   } else if (tau && src != 2 && 2 * g.nm * g.ns <= kBandCells &&
              (g.lay_class == kLayDec1 || g.lay_class == kLayEncDec2)) {
 #define PP_BAND3(L, Z, E)                                              \
@@ -1561,11 +1656,12 @@ cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_
                              const double* band, double interval, const SegStats* stats,
                              unsigned int* bitmap, const int64_t* bitmap_off, const int* seg_mode,
                              unsigned long long* cand_raw, const int64_t* cand_raw_off,
-                             unsigned long long* cand_raw_cnt, cudaStream_t st) {
+                             unsigned long long* cand_raw_cnt, const short* colbase, const int* row_w,
+                             cudaStream_t st) {
   const int blocks = std::max(1, std::min((total_blocks + 7) / 8, 148 * 32));
   band_cand_kernel<<<blocks, 256, 0, st>>>(seg_off, blk_base, n_seg, total_blocks, blk_W, tile_off,
                                            seg_band_base, band, interval, stats, bitmap, bitmap_off,
-                                           seg_mode, cand_raw, cand_raw_off, cand_raw_cnt);
+                                           seg_mode, cand_raw, cand_raw_off, cand_raw_cnt, colbase, row_w);
   return cudaGetLastError();
 }
 

@@ -89,7 +89,12 @@ struct DpSmem {
   static constexpr size_t npx = nps + kWorkers * kRB * 8;             // [8][32] double / int
   static constexpr size_t npj = npx + kWorkers * kRB * 8;             // [8][32] int
   static constexpr size_t row0 = npj + kWorkers * kRB * 4;            // raw state[0] (sum, aux)
-  static constexpr size_t bars = (row0 + 16 + 15) / 16 * 16;          // mbarriers: near full/empty
+  // compact band: column -> window index tables of the near tiles and the
+  // ring chunks (int16), and the row widths of the current / next block
+  static constexpr size_t cbn = (row0 + 16 + 15) / 16 * 16;           // [2][64] short
+  static constexpr size_t cbr = cbn + kNearBufs * kNearCols * 2;      // [kMaxRing][32] short
+  static constexpr size_t wrs = cbr + kMaxRing * kChunkCols * 2;      // [2][32] int
+  static constexpr size_t bars = (wrs + 2 * kRB * 4 + 15) / 16 * 16;  // mbarriers: near full/empty
   static constexpr size_t state = (bars + 8 * (2 * kNearBufs + 2 * kMaxRing) + 127) / 128 * 128;  // + ring
 };
 
@@ -102,6 +107,22 @@ int dp_max_ring() { return kMaxRing; }
 // chunks of up to 32 columns starting at column 64.
 __device__ __forceinline__ int n_chunks(int W) {
   return W > kNearCols ? (W - kNearCols + kChunkCols - 1) / kChunkCols : 0;
+}
+
+// Far-far chunks of a tile that a candidate pass (MODE 0, threshold t) needs:
+// all nc of them, or those before the first chunk k whose opening column
+// prices above thr = t + 2E on every live row (cost.cu band_run_kernel's
+// cmin; capi.cu time_trunc_margin): on a length-sorted segment the exact
+// slice time is nondecreasing along a row, so every slice from that column
+// on exceeds t and can never pass `x <= t`.  Warp-cooperative (all lanes).
+__device__ __forceinline__ int far_chunks_needed(int nc, const double* __restrict__ cmin_blk, double thr,
+                                                 int lane) {
+  for (int base = 0; base < nc; base += 32) {
+    const bool over = (base + lane < nc) && (cmin_blk[base + lane] > thr);
+    const unsigned int m = __ballot_sync(0xffffffffu, over);
+    if (m) return base + __ffs(m) - 1;
+  }
+  return nc;
 }
 
 // (s, c, j) lexmin with lowest-j ties.
@@ -124,7 +145,7 @@ __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int
 // finiteness test on the sum is needed: +inf or NaN never compares smaller
 // than the (+inf, 0) identity or any taken value, -inf is taken exactly when
 // the reference takes it.
-template <int MODE, bool SMEM_STATE, bool SANITIZE>
+template <int MODE, bool SMEM_STATE, bool SANITIZE, bool COMPACT>
 __global__ void __launch_bounds__(kDpThreads, 2)
     dp_pass_kernel(const WorkItem* __restrict__ items, const int64_t* __restrict__ seg_off,
                    const int* __restrict__ blk_base, const int* __restrict__ blk_W,
@@ -132,7 +153,9 @@ __global__ void __launch_bounds__(kDpThreads, 2)
                    const double* __restrict__ band, const double* __restrict__ cand,
                    const int64_t* __restrict__ cand_off, ItemResult* __restrict__ res,
                    int* __restrict__ next_buf, double* __restrict__ gstate, int res_by_seg,
-                   int ring_off, int kRing) {
+                   int ring_off, int kRing, const double* __restrict__ cmin, double t_margin,
+                   unsigned long long* __restrict__ cols_streamed, const short* __restrict__ colbase,
+                   const int* __restrict__ chunk_nv, const int* __restrict__ row_w) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* near = reinterpret_cast<double*>(smem + DpSmem::near);
   double* ring = reinterpret_cast<double*>(smem + ring_off);
@@ -149,6 +172,9 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   double* npm = reinterpret_cast<double*>(smem + DpSmem::npx);  // MODE 1
   int* npj = reinterpret_cast<int*>(smem + DpSmem::npj);
   double* row0 = reinterpret_cast<double*>(smem + DpSmem::row0);
+  short* cbn = reinterpret_cast<short*>(smem + DpSmem::cbn);
+  short* cbr = reinterpret_cast<short*>(smem + DpSmem::cbr);
+  int* wrs = reinterpret_cast<int*>(smem + DpSmem::wrs);
   uint64_t* near_full = reinterpret_cast<uint64_t*>(smem + DpSmem::bars);
   uint64_t* near_empty = near_full + kNearBufs;
   uint64_t* ring_full = near_full + 2 * kNearBufs;
@@ -162,6 +188,16 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   const int nblk = blk_base[s + 1] - gb0;
   const double t = item_t(it, cand, cand_off);
   const double* bseg = band + seg_band_base[s];
+  // candidate passes on certified tiles stream only the far chunks that can
+  // hold a slice time <= t (thr = +inf or cmin == null: all of them)
+  const bool trunc = MODE == 0 && cmin != nullptr;
+  const double thr = trunc ? __dadd_ru(t, t_margin) : __longlong_as_double(0x7ff0000000000000LL);
+  auto far_nc = [&](int gb, int W) {
+    const int nc = n_chunks(W);
+    return trunc ? far_chunks_needed(nc, cmin + chunk_id0(seg_band_base[s] + tile_off[gb], gb) + 2, thr,
+                                     threadIdx.x & 31)
+                 : nc;
+  };
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
@@ -207,25 +243,58 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   // released through the matching "empty" mbarrier.  It never joins the
   // block barrier, so it runs ahead by up to the ring depth.
   if (wid == kProducerWarp) {
-    if (lane == 0) {
-      int islot = 0, iround = 0;
-      for (int b = 0; b < nblk; ++b) {
-        const int gb = gb0 + b;
-        const int W = blk_W[gb];
-        const int nsl = b % kNearBufs;
+    // Issue order = consumption order: near tile of block b (used during
+    // block b), then the far-far chunks of block b+1 (used by the workers
+    // during block b), so far chunks never queue behind a near-buffer wait.
+    int islot = 0, iround = 0;
+    long long ncols_total = 0;  // tile columns streamed (the transitions this pass visits / 32)
+    for (int b = 0; b < nblk; ++b) {
+      const int gb = gb0 + b;
+      const int W = blk_W[gb];
+      const int nsl = b % kNearBufs;
+      const int ncols = min(kNearCols, W);
+      ncols_total += ncols;
+      if (lane == 0) {
         if (b >= kNearBufs) mbar_wait(&near_empty[nsl], ((b / kNearBufs) - 1) & 1);
-        const int ncols = min(kNearCols, W);
         mbar_expect_tx(&near_full[nsl], ncols * kColBytes);
         tma_load_1d(near + (size_t)nsl * kNearCols * kRB, bseg + tile_off[gb], ncols * kColBytes,
                     &near_full[nsl]);
-        if (b == 0) continue;  // block 0's far-far is never needed
-        const int nc = n_chunks(W);
+      }
+      if (b + 1 >= nblk) break;
+      const int gn = gb + 1;
+      const int Wn = blk_W[gn];
+      // (the whole warp: far_nc is warp-cooperative; lane 0 issues)
+      const int nc = far_nc(gn, Wn);
+      ncols_total += nc > 0 ? min(Wn, kNearCols + nc * kChunkCols) - kNearCols : 0;
+      if (COMPACT) {
+        // far chunks kk = 2 .. nc + 1 are records (pp_internal.cuh); their
+        // sizes are read 32 at a time by the whole warp
+        const int64_t cid = chunk_id0(seg_band_base[s] + tile_off[gn], gn) + kNearCols / kChunkCols;
+        const double* tb = bseg + tile_off[gn] + (size_t)kNearCols * kRB;
+        int mynv = 0;
+        for (int k = 0; k < nc; ++k) {
+          if ((k & 31) == 0) mynv = k + lane < nc ? chunk_nv[cid + k + lane] : 0;
+          const int nv = __shfl_sync(0xffffffffu, mynv, k & 31);
+          const uint32_t vbytes = (uint32_t)((nv + 1) & ~1) * 8u;  // a multiple of 16 B
+          if (lane == 0) {
+            if (iround > 0) mbar_wait(&ring_empty[islot], (iround - 1) & 1);
+            mbar_expect_tx(&ring_full[islot], vbytes + 64u);
+            tma_load_1d(ring + (size_t)islot * kChunkCols * kRB, tb + (size_t)k * kChunkCols * kRB, vbytes,
+                        &ring_full[islot]);
+            tma_load_1d(cbr + islot * kChunkCols, colbase + (cid + k) * kChunkCols, 64u, &ring_full[islot]);
+          }
+          if (++islot == kRing) {
+            islot = 0;
+            ++iround;
+          }
+        }
+      } else if (lane == 0) {
         for (int k = 0; k < nc; ++k) {
           const int c0 = kNearCols + k * kChunkCols;
-          const int cols = min(kChunkCols, W - c0);
+          const int cols = min(kChunkCols, Wn - c0);
           if (iround > 0) mbar_wait(&ring_empty[islot], (iround - 1) & 1);
           mbar_expect_tx(&ring_full[islot], cols * kColBytes);
-          tma_load_1d(ring + (size_t)islot * kChunkCols * kRB, bseg + tile_off[gb] + (size_t)c0 * kRB,
+          tma_load_1d(ring + (size_t)islot * kChunkCols * kRB, bseg + tile_off[gn] + (size_t)c0 * kRB,
                       cols * kColBytes, &ring_full[islot]);
           if (++islot == kRing) {
             islot = 0;
@@ -234,6 +303,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         }
       }
     }
+    if (lane == 0 && cols_streamed) atomicAdd(cols_streamed, (unsigned long long)ncols_total);
     return;
   }
   int cslot = 0;
@@ -417,10 +487,11 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         const int j1 = n - kRB * bn;
         const int k0 = max(0, j1 - kRB);  // i0 of block b+1
         const int Wn = blk_W[gb0 + bn];
-        const int nc = n_chunks(Wn);
+        const int nc = far_nc(gb0 + bn, Wn);
         double as = INF, am = INF, as2 = INF, am2 = INF;
         int ac = 0, aj = INT_MAX, ac2 = 0, aj2 = INT_MAX;
         const int r = lane;
+
         for (int k = 0; k < nc; ++k) {
           mbar_wait(&ring_full[cslot], cphase);
           const double* ch = ring + (size_t)cslot * kChunkCols * kRB;
@@ -431,7 +502,12 @@ __global__ void __launch_bounds__(kDpThreads, 2)
             const int q = q0 + w;
             const int j = min(k0 + c0 + q, n);
             // columns past the chunk are masked (NaN never passes x <= t)
-            const double x = (q < cols) ? ch[q * kRB + r] : QNAN;
+            double x;
+            if (COMPACT) {  // record of a far chunk (pp_internal.cuh: no masking needed)
+              x = (q < cols) ? ch[cbr[cslot * kChunkCols + q] - r] : QNAN;
+            } else {
+              x = (q < cols) ? ch[q * kRB + r] : QNAN;
+            }
             const double cs = __dadd_rn(x, st_s[j & mask]);
             // two accumulators (even / odd q0 step) for ILP; ascending j in each
             double& s_ = (q0 / kWorkers) & 1 ? as2 : as;
@@ -676,7 +752,8 @@ __global__ void __launch_bounds__(256)
                     const int64_t* __restrict__ seg_off, const int* __restrict__ blk_base,
                     const int64_t* __restrict__ tile_off, const int64_t* __restrict__ seg_band_base,
                     const double* __restrict__ band, const SegStats* __restrict__ stats,
-                    const pp_sample* __restrict__ ordered, int chain_in_smem, int stage_count,
+                    const short* __restrict__ colbase, const pp_sample* __restrict__ ordered,
+                    int chain_in_smem, int stage_count,
                     int replicas, int32_t* __restrict__ splits, double* __restrict__ mb_times,
                     int32_t* __restrict__ count, double* __restrict__ t_max_used,
                     double* __restrict__ objective, int32_t* __restrict__ status,
@@ -720,7 +797,41 @@ __global__ void __launch_bounds__(256)
     ch = chain;
   }
   int32_t* sp = splits + b;
-  if (threadIdx.x == 0) {
+  if (chain_in_smem == 2) {
+    // hop tables next^2, next^3, next^4 (built in parallel): the walk then
+    // issues four independent shared-memory loads per four splits instead of
+    // one dependent load per split
+    int* h1 = chain;
+    int* h2 = chain + n;
+    int* h3 = chain + 2 * n;
+    int* h4 = chain + 3 * n;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+      const int a = h1[q];
+      h2[q] = a < n ? h1[a] : n;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+      const int a = h2[q];
+      h3[q] = a < n ? h1[a] : n;
+      h4[q] = a < n ? h2[a] : n;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int i = 0, m = 0;
+      while (i < n) {
+        const int a = h1[i], c2 = h2[i], c3 = h3[i], c4 = h4[i];
+        sp[m++] = a;
+        if (a >= n) break;
+        sp[m++] = c2;
+        if (c2 >= n) break;
+        sp[m++] = c3;
+        if (c3 >= n) break;
+        sp[m++] = c4;
+        i = c4;
+      }
+      m_sh = m;
+    }
+  } else if (threadIdx.x == 0) {  // one dependent load per split
     int i = 0, m = 0;
     while (i < n) {
       const int j = ch[i];
@@ -734,21 +845,56 @@ __global__ void __launch_bounds__(256)
   const double* bseg = band + seg_band_base[s];
   const int gb0 = blk_base[s];
   double* tt = mb_times + b;
+  // slice times of the chosen micro-batches, fetched in parallel; staged in
+  // shared memory (over the chain, which is no longer needed) when they fit
+  double* tsh = chain_in_smem ? reinterpret_cast<double*>(chain) : nullptr;
+  const bool t_in_smem = chain_in_smem && (size_t)m * sizeof(double) <= (size_t)n * sizeof(int) * (chain_in_smem == 2 ? 4 : 1);
+  double mx = 0.0;
   for (int k = threadIdx.x; k < m; k += blockDim.x) {
     const int j = sp[k];
     const int i = k ? sp[k - 1] : 0;
     const int bl = (n - 1 - i) / kRB;  // block of row i
     const int i0 = max(0, n - kRB * (bl + 1));
-    tt[k] = bseg[tile_off[gb0 + bl] + (int64_t)(j - i0) * kRB + (i - i0)];
+    const int64_t to = tile_off[gb0 + bl];
+    double v;
+    if (colbase && j - i0 >= 64) {  // compact band: the record of far column chunk (j - i0) / 32
+      const int c = j - i0, kk = c >> 5;
+      const int64_t id = chunk_id0(seg_band_base[s] + to, gb0 + bl) + kk;
+      v = bseg[to + (int64_t)kk * (32 * kRB) + colbase[id * 32 + (c & 31)] - (i - i0)];
+    } else {
+      v = bseg[to + (int64_t)(j - i0) * kRB + (i - i0)];
+    }
+    tt[k] = v;
+    mx = (mx < v) ? v : mx;
   }
+  __syncthreads();  // every thread is past its last chain read
+  if (t_in_smem)
+    for (int k = threadIdx.x; k < m; k += blockDim.x) tsh[k] = tt[k];
+  // max slice time (order-free) ...
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double y = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (mx < y) ? y : mx;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double max_t = 0.0, sum = 0.0;
-    for (int k = 0; k < m; ++k) {
-      const double v = tt[k];
-      max_t = (max_t < v) ? v : max_t;
-      sum = __dadd_rn(sum, v);
+    double max_t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) max_t = (max_t < red[w]) ? red[w] : max_t;
+    // ... and the front-to-back sum of eval_objective (microbatch.cpp:109-120):
+    // one dependent add per micro-batch, loads issued ahead of the chain
+    const double* src = t_in_smem ? tsh : tt;
+    double sum = 0.0;
+    int k = 0;
+    for (; k + 8 <= m; k += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = src[k + q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sum = __dadd_rn(sum, v[q]);
     }
+    for (; k < m; ++k) sum = __dadd_rn(sum, src[k]);
     count[s] = m;
     objective[s] = __dadd_rn(__dmul_rn((double)(stage_count - 1), max_t),
                              __ddiv_rn(sum, (double)replicas));
@@ -772,23 +918,28 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int* blk_base, const int* blk_W, const int64_t* tile_off,
                            const int64_t* seg_band_base, const double* band, const double* cand,
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
-                           int res_by_seg, cudaStream_t st) {
+                           int res_by_seg, const double* cmin, double t_margin,
+                           unsigned long long* cols_streamed, const short* colbase, const int* chunk_nv,
+                           const int* row_w, cudaStream_t st) {
   if (n_items == 0) return cudaSuccess;
   const size_t ring_off = (DpSmem::state + (state_global ? 0 : smem_state) + 127) / 128 * 128;
   int ring = (int)std::min<size_t>(kMaxRing, (smem_budget - std::min(smem_budget, ring_off)) / kChunkBytes);
   ring = std::max(ring, 4);
   const size_t smem = ring_off + (size_t)ring * kChunkBytes;
-#define PP_DP_LAUNCH(M, S, Z)                                                                         \
+  const bool compact = colbase != nullptr;
+#define PP_DP_LAUNCH(M, S, Z, C)                                                                      \
   do {                                                                                                \
-    ensure_dyn_smem((const void*)dp_pass_kernel<M, S, Z>, smem);                                      \
-    dp_pass_kernel<M, S, Z><<<n_items, kDpThreads, smem, st>>>(                                       \
+    ensure_dyn_smem((const void*)dp_pass_kernel<M, S, Z, C>, smem);                                   \
+    dp_pass_kernel<M, S, Z, C><<<n_items, kDpThreads, smem, st>>>(                                    \
         items, seg_off, blk_base, blk_W, tile_off, seg_band_base, band, cand, cand_off, res, next_buf, \
-        gstate, res_by_seg, (int)ring_off, ring);                                                     \
+        gstate, res_by_seg, (int)ring_off, ring, cmin, t_margin, cols_streamed, colbase, chunk_nv,    \
+        row_w);                                                                                       \
   } while (0)
-#define PP_DP_LAUNCH_Z(M, S)              \
-  do {                                    \
-    if (sanitize) PP_DP_LAUNCH(M, S, true); \
-    else PP_DP_LAUNCH(M, S, false);       \
+#define PP_DP_LAUNCH_Z(M, S)                                   \
+  do {                                                         \
+    if (compact) PP_DP_LAUNCH(M, S, false, true);              \
+    else if (sanitize) PP_DP_LAUNCH(M, S, true, false);        \
+    else PP_DP_LAUNCH(M, S, false, false);                     \
   } while (0)
   if (mode == 0) {
     if (state_global) PP_DP_LAUNCH_Z(0, false); else PP_DP_LAUNCH_Z(0, true);
@@ -819,15 +970,18 @@ cudaError_t launch_select(const WorkItem* items, const ItemResult* res, const in
 
 cudaError_t launch_finalize(const SegDP* dps, const int* best_next, const int64_t* seg_off,
                             const int* blk_base, const int64_t* tile_off, const int64_t* seg_band_base,
-                            const double* band, const SegStats* stats, const pp_sample* ordered,
-                            int stage_count, int replicas, int max_n, int n_seg, int32_t* splits,
+                            const double* band, const SegStats* stats, const short* colbase,
+                            const pp_sample* ordered, int stage_count, int replicas, int max_n, int n_seg,
+                            int32_t* splits,
                             double* mb_times, int32_t* count, double* t_max_used, double* objective,
                             int32_t* status, int64_t* err_id, cudaStream_t st) {
-  const int in_smem = (size_t)max_n * sizeof(int) <= 200 * 1024 ? 1 : 0;
-  const size_t smem = in_smem ? (size_t)max_n * sizeof(int) : 0;
+  // 2: the chain and its three hop tables in shared memory; 1: the chain only
+  const int in_smem = (size_t)max_n * 4 * sizeof(int) <= 200 * 1024 ? 2
+                      : (size_t)max_n * sizeof(int) <= 200 * 1024 ? 1 : 0;
+  const size_t smem = (size_t)max_n * sizeof(int) * (in_smem == 2 ? 4 : in_smem);
   ensure_dyn_smem((const void*)finalize_kernel, smem);
   finalize_kernel<<<n_seg, 256, smem, st>>>(dps, best_next, seg_off, blk_base, tile_off, seg_band_base,
-                                            band, stats, ordered, in_smem, stage_count, replicas,
+                                            band, stats, colbase, ordered, in_smem, stage_count, replicas,
                                             splits, mb_times, count, t_max_used, objective, status,
                                             err_id);
   return cudaGetLastError();

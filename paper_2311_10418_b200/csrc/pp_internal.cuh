@@ -244,6 +244,26 @@ __device__ __forceinline__ void slice_cost_lay(const double4* __restrict__ tt,
 // slice end j = i0 + c, contiguous (256 B per column).
 constexpr int kRB = 32;
 
+// Compact band (length-sorted single-input mini-batches: cost.cu
+// band_run_kernel<.., true> writes it, dp.cu dp_pass_kernel<.., .., .., true>
+// and finalize read it).  A tile's near tile (columns [0, 64): the DP's
+// serial triangle) stays dense; each far 32-column chunk kk >= 2 keeps, IN
+// PLACE of its dense region (columns [32 kk, 32 kk + 32) x 32 rows), a record: the values
+// of the distinct (micro-batch size d, padded length) pairs its columns use —
+// one window d in [cs - 31, ce] per run of equal lengths [cs, ce] — nv =
+// chunk_nv[id] doubles (nv <= 32 x columns, so the record fits the region),
+// and colbase[id][q] (int16) with
+//     T(row r, column 32 kk + q) = vals[colbase[q] - r]
+// for every slice of an existing row r: far columns have d = column - r >= 33,
+// and d > w_r reads NaN exactly like the dense band (past the row's last
+// feasible j every act_mem exceeds the cap; with no cap every d fits).
+// Readers mask rows past the top tile's last row and d <= 0 (band_cand).
+// NaN values: act_mem > cap.
+// Record ids: chunk kk of the tile at band offset `off` (doubles) of block gb
+// is chunk_id0(off, gb) + kk — disjoint across tiles (ceil(W / 32) <=
+// floor(32 W / 1024) + 1).  Also indexes the per-chunk minima (cmin).
+__host__ __device__ inline int64_t chunk_id0(int64_t off, int gb) { return (off >> 10) + gb; }
+
 __device__ __forceinline__ int seg_of(const int* __restrict__ base, int n_seg, int g) {
   int lo = 0, hi = n_seg - 1;
   while (lo < hi) {

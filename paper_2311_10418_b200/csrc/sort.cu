@@ -170,14 +170,51 @@ __global__ void __launch_bounds__(kSortThreads)
   const int64_t b = seg_off[s];
   const int n = (int)(seg_off[s + 1] - b);
   if (n <= 0) return;
+  // field ranges of THIS segment (each is within the call's range, so the
+  // key still fits the word count the launcher chose from the call's range):
+  // ids of a mini-batch usually span far fewer bits than the call's ids
+  __shared__ long long s_rng[kSortThreads / 32][6];
+  {
+    long long lo[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
+    long long hi[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const pp_sample v = in[b + k];
+      const long long f[3] = {v.input_len, v.target_len, v.id};
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        lo[q] = min(lo[q], f[q]);
+        hi[q] = max(hi[q], f[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      for (int o = 16; o; o >>= 1) {
+        lo[q] = min(lo[q], __shfl_xor_sync(0xffffffffu, lo[q], o));
+        hi[q] = max(hi[q], __shfl_xor_sync(0xffffffffu, hi[q], o));
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        s_rng[threadIdx.x >> 5][q] = lo[q];
+        s_rng[threadIdx.x >> 5][3 + q] = hi[q];
+      }
+    }
+    __syncthreads();
+  }
   long long mn[3];
   int bits[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
-    mn[q] = (long long)(range[q] ^ 0x8000000000000000ULL);
-    const long long mx = (long long)(range[3 + q] ^ 0x8000000000000000ULL);
-    bits[q] = bit_width((unsigned long long)mx - (unsigned long long)mn[q]);
+    long long lo = s_rng[0][q], hi = s_rng[0][3 + q];
+    for (int w = 1; w < kSortThreads / 32; ++w) {
+      lo = min(lo, s_rng[w][q]);
+      hi = max(hi, s_rng[w][3 + q]);
+    }
+    mn[q] = lo;
+    bits[q] = bit_width((unsigned long long)hi - (unsigned long long)lo);
   }
+  (void)range;
   unsigned long long *k0, *k1;
   uint32_t *v0, *v1;
   if (use_smem) {

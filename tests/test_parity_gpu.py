@@ -151,7 +151,62 @@ def test_slice_reuse_matches_per_slice_pricing(name):
         for k in ("splits", "mb_times"):
             assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
     sa, sb = a.stats(), b.stats()
-    for k in ("candidates_generated", "candidates_evaluated", "slices_pass_b", "transitions_executed"):
+    for k in ("candidates_generated", "candidates_evaluated", "slices_pass_b"):
+        assert sa[k] == sb[k], k
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_band_truncation_matches_full_stream(name):
+    """Candidate passes that stop streaming a tile at the first chunk whose
+    slices all exceed t (certified monotone slice times on length-sorted
+    segments) against streaming every column: identical plans, fewer
+    transitions."""
+    cfg = W.CONFIGS[name]
+    M = {"C1": 64, "C3": 6, "C4": 24}[name]
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    a = capi.Planner(0)
+    b = capi.Planner(0)
+    b.set_tuning(band_trunc=False)
+    ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    for k in ("ordered", "count", "t_max_used", "objective", "status"):
+        assert ra[k].tobytes() == rb[k].tobytes(), k
+    for q in range(M):
+        m = int(ra["count"][q])
+        for k in ("splits", "mb_times"):
+            assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
+    sa, sb = a.stats(), b.stats()
+    assert sa["candidates_evaluated"] == sb["candidates_evaluated"]
+    assert sa["transitions_executed"] < sb["transitions_executed"]
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_compact_band_matches_dense_band(name):
+    """DP passes and assembly reading compact chunk records (the distinct
+    diagonal windows of each 32-column chunk) against the dense band:
+    identical plans and candidate sets."""
+    cfg = W.CONFIGS[name]
+    M = {"C1": 64, "C3": 6, "C4": 24}[name]
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    a = capi.Planner(0)
+    b = capi.Planner(0)
+    a.set_tuning(compact_band=True)
+    ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    for k in ("ordered", "count", "t_max_used", "objective", "status"):
+        assert ra[k].tobytes() == rb[k].tobytes(), k
+    for q in range(M):
+        m = int(ra["count"][q])
+        for k in ("splits", "mb_times"):
+            assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
+    sa, sb = a.stats(), b.stats()
+    for k in ("candidates_generated", "candidates_evaluated", "transitions_executed"):
         assert sa[k] == sb[k], k
     a.close()
     b.close()

@@ -11,6 +11,7 @@
 from __future__ import annotations
 
 import argparse
+import json
 import collections
 import csv
 import io
@@ -86,12 +87,47 @@ def full(rep: str):
     return "\n".join(out)
 
 
+CATEGORY = [("band_run_kernel", "cost pass B (band tiles + candidate bins)"),
+            ("band3_kernel", "cost pass B (band tiles + candidate bins)"),
+            ("band_kernel", "cost pass B (band tiles + candidate bins)"),
+            ("dp_pass_kernel<0", "DP bound pass"),
+            ("dp_pass_kernel<1", "DP candidate passes")]
+
+
+def traffic(rep: str, plans: int, source: str) -> dict:
+    """Per-plan DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of
+    the bench's roofline kernels, averaged over the captured launches (the
+    record bench.py reads as roofline.traffic)."""
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    h, units = rows[0], rows[1]
+    ki, ri, wi = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+    acc = {}
+    for r in rows[2:]:
+        cat = next((c for k, c in CATEGORY if short(r[ki]).startswith(k)), None)
+        if cat is None:
+            continue
+        b = float(r[ri]) * BYTES.get(units[ri], 1) + float(r[wi]) * BYTES.get(units[wi], 1)
+        n, t = acc.get(cat, (0, 0.0))
+        acc[cat] = (n + 1, t + b)
+    return {"source": source,
+            "kernels": {c: {"dram_bytes_per_plan": t / n / plans, "launches_captured": n}
+                        for c, (n, t) in acc.items()}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
     ap.add_argument("--rep")
     ap.add_argument("--title", default="ncu summary")
+    ap.add_argument("--traffic", help="write the per-plan DRAM traffic record here (needs --rep)")
+    ap.add_argument("--plans", type=int, default=148, help="mini-batches per captured launch")
+    ap.add_argument("--source", default="")
     a = ap.parse_args()
+    if a.traffic:
+        with open(a.traffic, "w") as f:
+            json.dump(traffic(a.rep, a.plans, a.source), f, indent=1)
     print(f"# {a.title}\n")
     if a.launches:
         print("## Launch list (`--metrics gpu__time_duration.sum --clock-control none`; cold, serialised)\n")

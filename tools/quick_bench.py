@@ -16,7 +16,9 @@ def run(name, M, reps=3, first_wave=1, max_wave=16, streams=1):
     s = W.dataset(cfg, M)
     off = W.seg_offsets(cfg, M)
     p = capi.Planner(0)
-    p.set_tuning(first_wave, max_wave, streams, slice_reuse=os.environ.get("QB_NO_REUSE") is None)
+    # QB_TUNE="compact_band=0,band_trunc=0,slice_reuse=0": A/B switches
+    tune = {k: bool(int(v)) for k, v in (kv.split("=") for kv in os.environ.get("QB_TUNE", "").split(",") if kv)}
+    p.set_tuning(first_wave, max_wave, streams, **tune)
     r = p.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     best = 1e9
     for _ in range(reps):

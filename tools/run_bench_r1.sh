@@ -10,6 +10,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --
     --log-file $OUT/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --streams 1 --per-gpu 296 > $OUT/ncu_bench_$TAG.log 2>&1
 echo "ncu list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"band3_kernel|band_kernel|block_kernel|dp_pass_kernel" -s 6 -c 4 -o $OUT/prof_$TAG -f \
+    -k regex:"band_run_kernel|band3_kernel|band_kernel|block_kernel|dp_pass_kernel" -s 6 -c 4 -o $OUT/prof_$TAG -f \
     python tools/quick_bench.py C3:148 > $OUT/ncu_full_$TAG.log 2>&1
 echo "ncu full rc=$?"
