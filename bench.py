@@ -278,9 +278,11 @@ def main():
         pinned.append(t)
         return t.numpy()
 
-    host_out = capi.Planner.plan_buffers(tot, M, pinned_alloc)
+    # the plan read back: the ordering as per-segment sample indices (4 B per
+    # sample; pp_plan_out.order), splits, micro-batch times and the per-plan scalars
+    host_out = capi.Planner.plan_buffers(tot, M, pinned_alloc, order_only=True)
     h2d = tot * 24 + seg.nbytes
-    d2h = tot * (24 + 4 + 8) + M * (4 + 8 + 8 + 4 + 8)
+    d2h = tot * (4 + 4 + 8) + M * (4 + 8 + 8 + 4 + 8)
     for g in range(warm):
         planner.plan_batch(pin_np[g * tot:(g + 1) * tot], seg, grid, model, cfg.stages, 1, cfg.mem_cap,
                            cfg.interval, out=host_out)

@@ -140,6 +140,9 @@ typedef struct pp_plan_out {
   double* objective;
   int32_t* status;
   int64_t* err_sample_id;
+  int32_t* order;  /* optional (may be NULL): the same ordering as `ordered`, as the
+                      index (within the segment) of the input sample placed at each
+                      position — 4 bytes per sample instead of a 24-byte copy */
 } pp_plan_out;
 
 /* Work counters for the last call (for benchmarks / rooflines). */

@@ -81,7 +81,7 @@ class Tuning(C.Structure):
 class PlanOut(C.Structure):
     _fields_ = [("ordered", C.c_void_p), ("splits", C.c_void_p), ("mb_times", C.c_void_p),
                 ("count", C.c_void_p), ("t_max_used", C.c_void_p), ("objective", C.c_void_p),
-                ("status", C.c_void_p), ("err_sample_id", C.c_void_p)]
+                ("status", C.c_void_p), ("err_sample_id", C.c_void_p), ("order", C.c_void_p)]
 
 
 KERNEL_NAMES = ["segmented sort", "cost setup", "cost pass A (act_mem row widths)",
@@ -338,10 +338,16 @@ class Planner:
         return out
 
     @staticmethod
-    def plan_buffers(n_samples: int, n_seg: int, alloc=np.zeros) -> dict:
+    def plan_buffers(n_samples: int, n_seg: int, alloc=np.zeros, order_only: bool = False) -> dict:
         """Output arrays for plan_batch; pass e.g. a pinned-memory allocator
-        (bench.py) so the device->host copies run at full PCIe rate."""
-        return dict(ordered=alloc((max(n_samples, 1), 3), np.int64),
+        (bench.py) so the device->host copies run at full PCIe rate.
+        order_only: return the ordering as per-segment sample indices
+        (`order`, 4 B per sample) instead of the ordered sample records."""
+        if order_only:
+            o = dict(ordered=None, order=alloc(max(n_samples, 1), np.int32))
+        else:
+            o = dict(ordered=alloc((max(n_samples, 1), 3), np.int64), order=None)
+        return dict(**o,
                     splits=alloc(max(n_samples, 1), np.int32), mb_times=alloc(max(n_samples, 1), np.float64),
                     count=alloc(n_seg, np.int32), t_max_used=alloc(n_seg, np.float64),
                     objective=alloc(n_seg, np.float64), status=alloc(n_seg, np.int32),
@@ -357,8 +363,8 @@ class Planner:
         S = len(off) - 1
         n = len(samples)
         res = dict(out) if out is not None else self.plan_buffers(n, S)
-        out = PlanOut(*(_p(res[k]) for k in ("ordered", "splits", "mb_times", "count", "t_max_used",
-                                            "objective", "status", "err_sample_id")))
+        out = PlanOut(*(_p(res.get(k)) for k in ("ordered", "splits", "mb_times", "count", "t_max_used",
+                                                "objective", "status", "err_sample_id", "order")))
         g, m = grid.desc(), model.desc()
         o = DpOptions(stage_count, replica_count, mem_cap, t_max_interval)
         rc = lib.pp_plan_grid(self._h, _p(samples), _p(off), S, int(presorted), C.byref(g), C.byref(m),
@@ -379,7 +385,7 @@ class Planner:
         S = len(h_off) - 1
         out = PlanOut(*(C.c_void_p(d_out[k].data_ptr()) if d_out.get(k) is not None else None
                         for k in ("ordered", "splits", "mb_times", "count", "t_max_used", "objective",
-                                  "status", "err_sample_id")))
+                                  "status", "err_sample_id", "order")))
         g, m = grid.desc(), model.desc()
         o = DpOptions(stage_count, replica_count, mem_cap, t_max_interval)
         rc = lib.pp_plan_grid_device(self._h, C.c_void_p(d_samples.data_ptr()),

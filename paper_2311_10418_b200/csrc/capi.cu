@@ -43,7 +43,7 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
                                   int presorted, unsigned long long* d_range,
                                   unsigned long long* h_range, unsigned long long* d_keys,
                                   uint32_t* d_vals, pp_sample* d_out, double* d_in_len,
-                                  double* d_tgt_len, cudaStream_t st);
+                                  double* d_tgt_len, int32_t* d_perm, cudaStream_t st);
 cudaError_t launch_segmented_sort_u64(unsigned long long* keys, unsigned long long* tmp,
                                       const int64_t* off, const unsigned long long* cnt,
                                       const int* seg_mode, int want_mode, int* in_tmp, int n_seg,
@@ -83,6 +83,7 @@ cudaError_t launch_cand_unique(const unsigned long long* keys_a, const unsigned 
 // dp.cu
 size_t dp_smem_fixed();
 size_t dp_state_bytes(int mode, int entries);
+int dp_state_stride(int entries);
 cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t smem_state,
                            int state_global, int sanitize, size_t smem_budget, const int64_t* seg_off,
                            const int* blk_base, const int* blk_W, const int64_t* tile_off,
@@ -191,7 +192,7 @@ struct pp_ctx {
   DevBuf out_splits, out_times, out_count, out_tmax, out_obj, out_status, out_err;
   PinBuf h_range, h_stats, h_segdp;
   DevBuf small_bm, coop_state, coop_parts, shapes, stage_lay, mb_off, oc_tf, oc_tb, oc_act, cmin, dp_cols,
-      colbase, chunk_nv;
+      colbase, chunk_nv, perm;
   // host copy of the uploaded grid (restricted to the recompute strategy)
   // for the monotonicity certificate of cost pass A
   std::vector<double> h_ax, h_cells;
@@ -218,7 +219,7 @@ struct pp_ctx {
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
             &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
             &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act,
-            &cmin, &dp_cols, &colbase, &chunk_nv};
+            &cmin, &dp_cols, &colbase, &chunk_nv, &perm};
   }
 };
 
@@ -276,6 +277,7 @@ struct PlanCall {
   pp_dp_options opts{};
   // outputs (device)
   pp_sample* d_ordered = nullptr;
+  int32_t* d_order = nullptr;
   int32_t* d_splits = nullptr;
   double* d_times = nullptr;
   int32_t* d_count = nullptr;
@@ -627,7 +629,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                         ctx->h_range.as<unsigned long long>(),
                                         ctx->sort_keys.as<unsigned long long>(),
                                         ctx->sort_vals.as<uint32_t>(), c.d_ordered,
-                                        ctx->in_d.as<double>(), ctx->tgt_d.as<double>(), st));
+                                        ctx->in_d.as<double>(), ctx->tgt_d.as<double>(), c.d_order, st));
     PP_CUDA(ctx->mbp.ensure((size_t)(max_n + 1) * sizeof(AxisPos)));
     PP_CUDA(ctx->pin.ensure(std::max<int64_t>(total, 1) * sizeof(AxisPos)));
     PP_CUDA(ctx->ptg.ensure(std::max<int64_t>(total, 1) * sizeof(AxisPos)));
@@ -791,7 +793,7 @@ void place_states(std::vector<WorkItem>& items, int mode, size_t& smem_state, in
   for (WorkItem& w : items) {
     if (state_global) {
       w.state_off = goff;
-      goff += 2 * (int64_t)w.state_entries;
+      goff += 2 * (int64_t)dp_state_stride(w.state_entries);
     } else {
       w.state_off = -1;
       smem_state = std::max(smem_state, dp_state_bytes(mode, w.state_entries));
@@ -1231,6 +1233,7 @@ int plan_split(pp_ctx* ctx, const PlanCall& c, int parts) {
         cc.h_seg_off = off.data();
         cc.n_seg = s1 - s0;
         cc.d_ordered = c.d_ordered + base;
+        cc.d_order = c.d_order ? c.d_order + base : nullptr;
         cc.d_splits = c.d_splits ? c.d_splits + base : nullptr;
         cc.d_times = c.d_times ? c.d_times + base : nullptr;
         cc.d_count = c.d_count ? c.d_count + s0 : nullptr;
@@ -1376,6 +1379,7 @@ int pp_plan_grid_device(pp_ctx* ctx, const pp_sample* d_samples, const int64_t* 
   c.model = model;
   c.opts = *opts;
   c.d_ordered = d_out->ordered;
+  c.d_order = d_out->order;
   c.d_splits = d_out->splits;
   c.d_times = d_out->mb_times;
   c.d_count = d_out->count;
@@ -1420,6 +1424,10 @@ int plan_host(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets,
   PP_CUDA(ctx->out_err.ensure(n_seg * sizeof(int64_t)));
   pp_plan_out d{};
   d.ordered = ctx->ordered.as<pp_sample>();
+  if (out->order) {
+    PP_CUDA(ctx->perm.ensure(std::max<int64_t>(total, 1) * sizeof(int32_t)));
+    d.order = ctx->perm.as<int32_t>();
+  }
   d.splits = ctx->out_splits.as<int32_t>();
   d.mb_times = ctx->out_times.as<double>();
   d.count = ctx->out_count.as<int32_t>();
@@ -1434,6 +1442,7 @@ int plan_host(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets,
     return dst && bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
   };
   PP_CUDA(d2h(out->ordered, d.ordered, total * sizeof(pp_sample)));
+  PP_CUDA(d2h(out->order, d.order, total * sizeof(int32_t)));
   PP_CUDA(d2h(out->splits, d.splits, total * sizeof(int32_t)));
   PP_CUDA(d2h(out->mb_times, d.mb_times, total * sizeof(double)));
   PP_CUDA(d2h(out->count, d.count, n_seg * sizeof(int32_t)));
@@ -1489,6 +1498,7 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
         for (int s = s0; s <= s1; ++s) off[s - s0] = seg_offsets[s] - base;
         pp_plan_out o{};
         o.ordered = out->ordered ? out->ordered + base : nullptr;
+        o.order = out->order ? out->order + base : nullptr;
         o.splits = out->splits ? out->splits + base : nullptr;
         o.mb_times = out->mb_times ? out->mb_times + base : nullptr;
         o.count = out->count ? out->count + s0 : nullptr;
@@ -1595,7 +1605,7 @@ int pp_order_samples(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_o
                                 ctx->h_range.as<unsigned long long>(),
                                 ctx->sort_keys.as<unsigned long long>(), ctx->sort_vals.as<uint32_t>(),
                                 ctx->ordered.as<pp_sample>(), ctx->in_d.as<double>(),
-                                ctx->tgt_d.as<double>(), st));
+                                ctx->tgt_d.as<double>(), nullptr, st));
   PP_CUDA(cudaMemcpyAsync(out, ctx->ordered.p, total * sizeof(pp_sample), cudaMemcpyDeviceToHost, st));
   PP_CUDA(cudaStreamSynchronize(st));
   return PP_OK;

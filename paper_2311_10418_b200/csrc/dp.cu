@@ -99,7 +99,15 @@ struct DpSmem {
 };
 
 size_t dp_smem_fixed() { return DpSmem::state; }
-size_t dp_state_bytes(int mode, int entries) { return (size_t)entries * (mode == 0 ? 12 : 16); }
+// DP state arrays (sum; count or minimax) of E = entries + kStatePad slots:
+// a ring (R = mask + 1 entries) mirrors its first kStatePad entries after its
+// end, so the far-far loop reads a chunk's 32 states at base + q with no
+// per-column wrap or clamp; a full array (mask = ~0) just gets the slack.
+constexpr int kStatePad = 32;
+int dp_state_stride(int entries) { return entries + kStatePad; }
+size_t dp_state_bytes(int mode, int entries) {
+  return (size_t)(entries + kStatePad) * (mode == 0 ? 12 : 16);
+}
 size_t dp_chunk_bytes() { return kChunkBytes; }
 int dp_max_ring() { return kMaxRing; }
 
@@ -206,8 +214,9 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   const unsigned mask = it.state_mask;
   const int entries = it.state_entries;
   double* st_s = SMEM_STATE ? reinterpret_cast<double*>(smem + DpSmem::state) : gstate + it.state_off;
-  int* st_c = reinterpret_cast<int*>(st_s + entries);     // MODE 0
-  double* st_m = st_s + entries;                          // MODE 1
+  int* st_c = reinterpret_cast<int*>(st_s + entries + kStatePad);  // MODE 0
+  double* st_m = st_s + entries + kStatePad;                        // MODE 1
+  const bool ring_state = mask != ~0u;
   int* nxt = next_buf + it.next_off;
 
   // ---- prologue
@@ -221,8 +230,12 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       mbar_init(&ring_empty[k], kWorkers);  // every worker warp releases a chunk
     }
     mbar_fence_init();
-    st_s[n & mask] = 0.0;  // state[n] = {0.0, 0} (microbatch.cpp:174)
-    if (MODE == 0) st_c[n & mask] = 0; else st_m[n & mask] = -INF;
+    // state[n] = {0.0, 0} (microbatch.cpp:174), and its ring mirror
+    for (int e = (int)(n & mask); ; e += entries) {
+      st_s[e] = 0.0;
+      if (MODE == 0) st_c[e] = 0; else st_m[e] = -INF;
+      if (!(ring_state && e < kStatePad)) break;
+    }
     row0[0] = INF;
     row0[1] = MODE == 0 ? 0.0 : INF;
   }
@@ -338,11 +351,11 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           c1 = upd ? cn : c1;
           j1 = upd ? j : j1;
         } else {
-          const bool ok = !isnan(x);
-          s1 = (ok & (cs < s1)) ? cs : s1;
+          // (NaN / +inf entries never pass the compares: see the far-far loop)
+          s1 = (cs < s1) ? cs : s1;
           const double mj = st_m[j & mask];
           const double v = (x < mj) ? mj : x;
-          m1 = (ok & (x < INF) & (mj < INF) & (v < m1)) ? v : m1;
+          m1 = (v < m1) ? v : m1;
         }
       }
       const int o = wid * kRB + r;
@@ -435,7 +448,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         double sj = __shfl_sync(0xffffffffu, as, jj);
         if (SANITIZE) sj = isfinite(sj) ? sj : INF;
         const double cs = __dadd_rn(x, sj);
-        const bool ok = (jj < W) & (r < jj) & (MODE == 0 ? (x <= t) : !isnan(x));
+        const bool ok = (jj < W) & (r < jj) & (MODE == 0 ? (x <= t) : true);  // (NaN: fails the `<`s)
         if (MODE == 0) {
           const int cn = 1 + __shfl_sync(0xffffffffu, ac, jj);
           const bool upd = ok & ((cs < as) | ((cs == as) & (cn <= ac)));
@@ -446,7 +459,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           const double mj = __shfl_sync(0xffffffffu, am, jj);
           as = (ok & (cs < as)) ? cs : as;
           const double v = (x < mj) ? mj : x;
-          am = (ok & (x < INF) & (mj < INF) & (v < am)) ? v : am;
+          am = (ok & (v < am)) ? v : am;
         }
       };
       if (nb == kRB) {  // every block but the top one of a segment
@@ -457,21 +470,27 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         for (int jj = kRB - 1; jj >= 0; --jj)
           if (jj < nb) tri_step(jj);
       }
-      // near tile of block b consumed: order this warp's generic-proxy reads
-      // before the producer's next async-proxy (TMA) write into the buffer
-      fence_proxy_async();
+      // near tile of block b consumed: the warp's reads are ordered before the
+      // release (__syncwarp + mbarrier arrive), and the producer's next TMA
+      // write into the buffer waits for it (the TMA pipeline WAR pattern)
       __syncwarp();
       if (lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);
       PP_TRACE(3);
       if (r < nb) {
         const int row = i0 + r;
         const bool f = isfinite(as);
-        st_s[row & mask] = (SANITIZE && !f) ? INF : as;
+        const int e = (int)(row & mask);
+        const int em = (ring_state && e < kStatePad) ? e + entries : e;  // the ring mirror
+        const double sv = (SANITIZE && !f) ? INF : as;
+        st_s[e] = sv;
+        st_s[em] = sv;
         if (MODE == 0) {
-          st_c[row & mask] = f ? ac : 0;
+          st_c[e] = f ? ac : 0;
+          st_c[em] = f ? ac : 0;
           nxt[row] = f ? aj : -1;
         } else {
-          st_m[row & mask] = am;
+          st_m[e] = am;
+          st_m[em] = am;
         }
         if (row == 0) {
           row0[0] = as;
@@ -497,10 +516,15 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           const double* ch = ring + (size_t)cslot * kChunkCols * kRB;
           const int c0 = kNearCols + k * kChunkCols;
           const int cols = min(kChunkCols, Wn - c0);
+          // the chunk's states: slots jb .. jb + 31 (ring mirror / slack: no wrap)
+          const int jb = (int)((k0 + c0) & mask) + w;
+          const double* ss = st_s + jb;
+          const int* sc = st_c + jb;
+          const double* sm = st_m + jb;
 #pragma unroll
           for (int q0 = 0; q0 < kChunkCols; q0 += kWorkers) {
             const int q = q0 + w;
-            const int j = min(k0 + c0 + q, n);
+            const int j = k0 + c0 + q;
             // columns past the chunk are masked (NaN never passes x <= t)
             double x;
             if (COMPACT) {  // record of a far chunk (pp_internal.cuh: no masking needed)
@@ -508,28 +532,29 @@ __global__ void __launch_bounds__(kDpThreads, 2)
             } else {
               x = (q < cols) ? ch[q * kRB + r] : QNAN;
             }
-            const double cs = __dadd_rn(x, st_s[j & mask]);
+            const double cs = __dadd_rn(x, ss[q0]);
             // two accumulators (even / odd q0 step) for ILP; ascending j in each
             double& s_ = (q0 / kWorkers) & 1 ? as2 : as;
             int& c_ = (q0 / kWorkers) & 1 ? ac2 : ac;
             int& j_ = (q0 / kWorkers) & 1 ? aj2 : aj;
             double& m_ = (q0 / kWorkers) & 1 ? am2 : am;
             if (MODE == 0) {
-              const int cn = 1 + st_c[j & mask];
+              const int cn = 1 + sc[q0];
               const bool upd = (x <= t) & ((cs < s_) | ((cs == s_) & (cn < c_)));
               s_ = upd ? cs : s_;
               c_ = upd ? cn : c_;
               j_ = upd ? j : j_;
             } else {
-              const bool ok = !isnan(x);
-              s_ = (ok & (cs < s_)) ? cs : s_;
-              const double mj = st_m[j & mask];
+              // an infeasible entry (x NaN) gives cs = NaN and v = NaN, which
+              // fail every `<`; x = +inf or state = +inf gives v = +inf, which
+              // never beats the running minimum (<= +inf): no separate tests
+              s_ = (cs < s_) ? cs : s_;
+              const double mj = sm[q0];
               const double v = (x < mj) ? mj : x;
-              m_ = (ok & (x < INF) & (mj < INF) & (v < m_)) ? v : m_;
+              m_ = (v < m_) ? v : m_;
             }
           }
-          fence_proxy_async();  // generic reads before the next TMA write of the slot
-          __syncwarp();
+          __syncwarp();  // the warp's reads of the slot, then its release
           if (lane == 0) mbar_arrive(&ring_empty[cslot]);  // this warp is done with the chunk
           if (++cslot == kRing) {
             cslot = 0;
@@ -798,13 +823,15 @@ __global__ void __launch_bounds__(256)
   }
   int32_t* sp = splits + b;
   if (chain_in_smem == 2) {
-    // hop tables next^2, next^3, next^4 (built in parallel): the walk then
-    // issues four independent shared-memory loads per four splits instead of
-    // one dependent load per split
+    // hop tables next^2, next^4, next^8 (built in parallel); one thread walks
+    // the chain 8 splits per dependent shared-memory load, leaving a
+    // checkpoint every 8 splits, and the block expands the checkpoints in
+    // parallel (8 dependent loads each)
     int* h1 = chain;
     int* h2 = chain + n;
-    int* h3 = chain + 2 * n;
-    int* h4 = chain + 3 * n;
+    int* h4 = chain + 2 * n;
+    int* h8 = chain + 3 * n;
+    int* ck = chain + 4 * n;  // checkpoints: the node before splits 8k .. 8k + 7
     for (int q = threadIdx.x; q < n; q += blockDim.x) {
       const int a = h1[q];
       h2[q] = a < n ? h1[a] : n;
@@ -812,24 +839,37 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     for (int q = threadIdx.x; q < n; q += blockDim.x) {
       const int a = h2[q];
-      h3[q] = a < n ? h1[a] : n;
       h4[q] = a < n ? h2[a] : n;
     }
     __syncthreads();
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+      const int a = h4[q];
+      h8[q] = a < n ? h4[a] : n;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-      int i = 0, m = 0;
+      int i = 0, k = 0;
       while (i < n) {
-        const int a = h1[i], c2 = h2[i], c3 = h3[i], c4 = h4[i];
-        sp[m++] = a;
-        if (a >= n) break;
-        sp[m++] = c2;
-        if (c2 >= n) break;
-        sp[m++] = c3;
-        if (c3 >= n) break;
-        sp[m++] = c4;
-        i = c4;
+        ck[k++] = i;
+        i = h8[i];
       }
-      m_sh = m;
+      m_sh = k;  // checkpoint count for now
+    }
+    __syncthreads();
+    const int K = m_sh;
+    __syncthreads();
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+      int node = ck[k];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int nx = h1[node];
+        sp[8 * k + q] = nx;
+        if (nx >= n) {
+          m_sh = 8 * k + q + 1;  // only the last checkpoint reaches n
+          break;
+        }
+        node = nx;
+      }
     }
   } else if (threadIdx.x == 0) {  // one dependent load per split
     int i = 0, m = 0;
@@ -850,22 +890,40 @@ __global__ void __launch_bounds__(256)
   double* tsh = chain_in_smem ? reinterpret_cast<double*>(chain) : nullptr;
   const bool t_in_smem = chain_in_smem && (size_t)m * sizeof(double) <= (size_t)n * sizeof(int) * (chain_in_smem == 2 ? 4 : 1);
   double mx = 0.0;
-  for (int k = threadIdx.x; k < m; k += blockDim.x) {
-    const int j = sp[k];
-    const int i = k ? sp[k - 1] : 0;
-    const int bl = (n - 1 - i) / kRB;  // block of row i
-    const int i0 = max(0, n - kRB * (bl + 1));
-    const int64_t to = tile_off[gb0 + bl];
-    double v;
-    if (colbase && j - i0 >= 64) {  // compact band: the record of far column chunk (j - i0) / 32
-      const int c = j - i0, kk = c >> 5;
-      const int64_t id = chunk_id0(seg_band_base[s] + to, gb0 + bl) + kk;
-      v = bseg[to + (int64_t)kk * (32 * kRB) + colbase[id * 32 + (c & 31)] - (i - i0)];
-    } else {
-      v = bseg[to + (int64_t)(j - i0) * kRB + (i - i0)];
+  // four micro-batches per thread and step: their band loads are independent
+  constexpr int kU = 4;
+  for (int kb = threadIdx.x; kb < m; kb += kU * blockDim.x) {
+    int64_t at[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int k = kb + u * blockDim.x;
+      at[u] = -1;
+      if (k < m) {
+        const int j = sp[k];
+        const int i = k ? sp[k - 1] : 0;
+        const int bl = (n - 1 - i) / kRB;  // block of row i
+        const int i0 = max(0, n - kRB * (bl + 1));
+        const int64_t to = __ldg(tile_off + gb0 + bl);
+        if (colbase && j - i0 >= 64) {  // compact band: the record of far column chunk (j - i0) / 32
+          const int c = j - i0, kk = c >> 5;
+          const int64_t id = chunk_id0(seg_band_base[s] + to, gb0 + bl) + kk;
+          at[u] = to + (int64_t)kk * (32 * kRB) + __ldg(colbase + id * 32 + (c & 31)) - (i - i0);
+        } else {
+          at[u] = to + (int64_t)(j - i0) * kRB + (i - i0);
+        }
+      }
     }
-    tt[k] = v;
-    mx = (mx < v) ? v : mx;
+    double v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) v[u] = at[u] >= 0 ? __ldg(bseg + at[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int k = kb + u * blockDim.x;
+      if (k < m) {
+        tt[k] = v[u];
+        mx = (mx < v[u]) ? v[u] : mx;
+      }
+    }
   }
   __syncthreads();  // every thread is past its last chain read
   if (t_in_smem)
@@ -976,9 +1034,9 @@ cudaError_t launch_finalize(const SegDP* dps, const int* best_next, const int64_
                             double* mb_times, int32_t* count, double* t_max_used, double* objective,
                             int32_t* status, int64_t* err_id, cudaStream_t st) {
   // 2: the chain and its three hop tables in shared memory; 1: the chain only
-  const int in_smem = (size_t)max_n * 4 * sizeof(int) <= 200 * 1024 ? 2
-                      : (size_t)max_n * sizeof(int) <= 200 * 1024 ? 1 : 0;
-  const size_t smem = (size_t)max_n * sizeof(int) * (in_smem == 2 ? 4 : in_smem);
+  const size_t hop_bytes = ((size_t)max_n * 4 + (size_t)max_n / 8 + 2) * sizeof(int);
+  const int in_smem = hop_bytes <= 200 * 1024 ? 2 : (size_t)max_n * sizeof(int) <= 200 * 1024 ? 1 : 0;
+  const size_t smem = in_smem == 2 ? hop_bytes : in_smem ? (size_t)max_n * sizeof(int) : 0;
   ensure_dyn_smem((const void*)finalize_kernel, smem);
   finalize_kernel<<<n_seg, 256, smem, st>>>(dps, best_next, seg_off, blk_base, tile_off, seg_band_base,
                                             band, stats, colbase, ordered, in_smem, stage_count, replicas,

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kSortThreads)
     seg_sort_kernel(const pp_sample* __restrict__ in, const int64_t* __restrict__ seg_off,
                     const unsigned long long* __restrict__ range, unsigned long long* gkeys,
                     uint32_t* gvals, int use_smem, pp_sample* __restrict__ out,
-                    double* __restrict__ in_d, double* __restrict__ tgt_d) {
+                    double* __restrict__ in_d, double* __restrict__ tgt_d, int32_t* __restrict__ perm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long warp_tot[kSortThreads / 32];
   __shared__ int bucket[4];
@@ -262,10 +262,12 @@ __global__ void __launch_bounds__(kSortThreads)
       }
   }
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    const pp_sample v = in[b + v0[k]];
+    const uint32_t src = v0[k];
+    const pp_sample v = in[b + src];
     out[b + k] = v;
     in_d[b + k] = (double)v.input_len;
     tgt_d[b + k] = (double)v.target_len;
+    if (perm) perm[b + k] = (int32_t)src;
   }
 }
 
@@ -305,6 +307,12 @@ __global__ void __launch_bounds__(kSortThreads)
 }
 
 // presorted path: copy + SoA lengths.
+// presorted order: position k of a segment holds its sample k
+__global__ void iota_seg_kernel(const int64_t* __restrict__ seg_off, int32_t* __restrict__ perm) {
+  const int64_t b = seg_off[blockIdx.x], e = seg_off[blockIdx.x + 1];
+  for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) perm[k] = (int32_t)(k - b);
+}
+
 __global__ void copy_soa_kernel(const pp_sample* __restrict__ in, int64_t n, pp_sample* out,
                                 double* in_d, double* tgt_d) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
@@ -336,7 +344,7 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
                                   int presorted, unsigned long long* d_range,
                                   unsigned long long* h_range, unsigned long long* d_keys,
                                   uint32_t* d_vals, pp_sample* d_out, double* d_in_len,
-                                  double* d_tgt_len, cudaStream_t st) {
+                                  double* d_tgt_len, int32_t* d_perm, cudaStream_t st) {
   // Field ranges of the call: they size the sort key and feed the host's
   // monotonicity certificate for the cost passes (capi.cu), so they are
   // computed for presorted calls too.
@@ -348,6 +356,7 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
   if (presorted) {
     const int cb = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     copy_soa_kernel<<<cb, 256, 0, st>>>(d_in, total, d_out, d_in_len, d_tgt_len);
+    if (d_perm && n_seg > 0) iota_seg_kernel<<<n_seg, 256, 0, st>>>(d_seg_off, d_perm);
     return cudaStreamSynchronize(st);
   }
   cudaError_t e = cudaStreamSynchronize(st);
@@ -367,11 +376,11 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
   if (W == 1) {
     ensure_dyn_smem((const void*)seg_sort_kernel<1>, smem);
     seg_sort_kernel<1><<<n_seg, kSortThreads, smem, st>>>(d_in, d_seg_off, d_range, d_keys, d_vals,
-                                                          use_smem, d_out, d_in_len, d_tgt_len);
+                                                          use_smem, d_out, d_in_len, d_tgt_len, d_perm);
   } else {
     ensure_dyn_smem((const void*)seg_sort_kernel<3>, smem);
     seg_sort_kernel<3><<<n_seg, kSortThreads, smem, st>>>(d_in, d_seg_off, d_range, d_keys, d_vals,
-                                                          use_smem, d_out, d_in_len, d_tgt_len);
+                                                          use_smem, d_out, d_in_len, d_tgt_len, d_perm);
   }
   return cudaGetLastError();
 }

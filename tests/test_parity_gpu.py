@@ -465,6 +465,28 @@ def test_threads_with_own_contexts_mixed_sizes():
     assert not errors, errors[0]
 
 
+def test_order_output_matches_ordered_samples(planner):
+    """pp_plan_out.order (per-segment sample indices) is the ordering the
+    `ordered` records carry, for sorted, split-stream and presorted calls."""
+    cfg = W.CONFIGS["C3"]
+    M = 5
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    for streams, presorted in ((1, False), (3, False), (1, True)):
+        p = capi.Planner(0)
+        p.set_tuning(streams=streams)
+        a = p.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval,
+                         presorted=presorted)
+        b = p.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval,
+                         presorted=presorted, out=capi.Planner.plan_buffers(len(s), M, order_only=True))
+        for q in range(M):
+            seg = s[off[q]:off[q + 1]]
+            assert np.array_equal(seg[b["order"][off[q]:off[q + 1]]], a["ordered"][off[q]:off[q + 1]]), q
+            m = int(a["count"][q])
+            assert np.array_equal(a["splits"][off[q]:off[q] + m], b["splits"][off[q]:off[q] + m])
+        p.close()
+
+
 def test_presorted_arbitrary_order_matches_oracle(planner, orc):
     """dp_partition(span) on the caller's order (no sort): running maxima of
     the padded lengths over unsorted spans, certified scan (no bisection)."""
