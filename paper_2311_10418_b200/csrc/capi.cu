@@ -31,6 +31,7 @@
 #include <cstring>
 #include <atomic>
 #include <string>
+#include <chrono>
 #include <thread>
 #include <vector>
 
@@ -171,6 +172,16 @@ struct PinBuf {
   }
 };
 
+// One staging set of a pipelined host-buffer worker (plan_host_chunks):
+// device inputs and outputs of one chunk, the pinned segment offsets, and the
+// events that order its copies against the compute stream.
+struct HostSet {
+  DevBuf samples, seg, ordered, order, splits, times, count, tmax, obj, status, err;
+  PinBuf hoff;
+  cudaEvent_t h2d = nullptr, d2h = nullptr;
+  bool d2h_pending = false;
+};
+
 }  // namespace
 
 struct pp_ctx {
@@ -201,6 +212,9 @@ struct pp_ctx {
   double exit_thresh = INFINITY;  // last call's pass-A row-exit threshold
   double trunc_margin = INFINITY; // candidate-pass truncation margin 2E (+inf: off)
   bool compact = false;           // the band holds compact chunk records (pp_internal.cuh)
+  // pipelined host-buffer worker (plan_host_chunks): copy stream + two sets
+  cudaStream_t cstream = nullptr;
+  HostSet hset[2];
   CostGrid grid_dev{};            // device view of the uploaded grid
   bool grid_valid = false;
   double tau_interval = -1.0;     // interval the device bin thresholds were built for
@@ -219,7 +233,11 @@ struct pp_ctx {
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
             &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
             &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act,
-            &cmin, &dp_cols, &colbase, &chunk_nv, &perm};
+            &cmin, &dp_cols, &colbase, &chunk_nv, &perm,
+            &hset[0].samples, &hset[0].seg, &hset[0].ordered, &hset[0].order, &hset[0].splits,
+            &hset[0].times, &hset[0].count, &hset[0].tmax, &hset[0].obj, &hset[0].status, &hset[0].err,
+            &hset[1].samples, &hset[1].seg, &hset[1].ordered, &hset[1].order, &hset[1].splits,
+            &hset[1].times, &hset[1].count, &hset[1].tmax, &hset[1].obj, &hset[1].status, &hset[1].err};
   }
 };
 
@@ -1315,6 +1333,15 @@ int pp_ctx_destroy(pp_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->cstream) {
+    cudaStreamSynchronize(ctx->cstream);
+    cudaStreamDestroy(ctx->cstream);
+  }
+  for (HostSet& h : ctx->hset) {
+    if (h.h2d) cudaEventDestroy(h.h2d);
+    if (h.d2h) cudaEventDestroy(h.d2h);
+    h.hoff.release();
+  }
   for (DevBuf* b : ctx->all_bufs()) b->release();
   for (PinBuf* b : {&ctx->h_range, &ctx->h_stats, &ctx->h_segdp}) b->release();
   for (auto& e : ctx->ev)
@@ -1459,11 +1486,114 @@ int plan_host(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets,
 // sub-context and stream) take from a queue; a chunk is staged, planned and
 // copied back on its own stream, so one chunk's copies overlap another's
 // planning.
+// A worker's chunk queue with its copies overlapped: while the compute stream
+// plans chunk k, the copy stream stages chunk k+1's samples and drains chunk
+// k-1's plans, through two alternating sets of device buffers (each set's
+// outputs are reused only after their device->host copy completed).
+// `claim` hands out chunk indices (-1: none left); chunk q covers segments
+// [cut[q], cut[q + 1]).
+template <class Claim, class Done>
+int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_offsets, const int* cut,
+                     int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
+                     const pp_dp_options* opts, const pp_plan_out* out, Claim claim, Done done) {
+  pp_ctx* ctx = sub;  // (PP_CUDA reports on ctx)
+  if (!sub->cstream) PP_CUDA(cudaStreamCreateWithFlags(&sub->cstream, cudaStreamNonBlocking));
+  for (HostSet& h : sub->hset) {
+    if (!h.h2d) PP_CUDA(cudaEventCreateWithFlags(&h.h2d, cudaEventDisableTiming));
+    if (!h.d2h) PP_CUDA(cudaEventCreateWithFlags(&h.d2h, cudaEventDisableTiming));
+    h.d2h_pending = false;
+  }
+  cudaStream_t cs = sub->cstream;
+  auto stage = [&](int set, int q) -> int {
+    HostSet& h = sub->hset[set];
+    const int s0 = cut[q], s1 = cut[q + 1], ns = s1 - s0;
+    const int64_t base = seg_offsets[s0], n = seg_offsets[s1] - base;
+    PP_CUDA(h.hoff.ensure((ns + 1) * sizeof(int64_t)));
+    int64_t* ho = h.hoff.as<int64_t>();
+    for (int s = s0; s <= s1; ++s) ho[s - s0] = seg_offsets[s] - base;
+    PP_CUDA(h.samples.ensure(std::max<int64_t>(n, 1) * sizeof(pp_sample)));
+    PP_CUDA(h.seg.ensure((ns + 1) * sizeof(int64_t)));
+    if (n > 0) PP_CUDA(cudaMemcpyAsync(h.samples.p, samples + base, n * sizeof(pp_sample), cudaMemcpyHostToDevice, cs));
+    PP_CUDA(cudaMemcpyAsync(h.seg.p, ho, (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, cs));
+    PP_CUDA(cudaEventRecord(h.h2d, cs));
+    return PP_OK;
+  };
+  int rc = PP_OK;
+  int q = claim(), set = 0;
+  if (q >= 0 && (rc = stage(set, q))) return rc;
+  while (q >= 0) {
+    const int qn = claim();
+    // prefetch the next chunk's inputs — after this chunk's arrived, so the
+    // first chunks of all workers cross PCIe ahead of any prefetch
+    PP_CUDA(cudaEventSynchronize(sub->hset[set].h2d));
+    if (qn >= 0 && (rc = stage(set ^ 1, qn))) return rc;
+    HostSet& h = sub->hset[set];
+    const int s0 = cut[q], s1 = cut[q + 1], ns = s1 - s0;
+    const int64_t base = seg_offsets[s0], n = seg_offsets[s1] - base;
+    PP_CUDA(cudaStreamWaitEvent(sub->stream, h.h2d, 0));
+    if (h.d2h_pending) PP_CUDA(cudaStreamWaitEvent(sub->stream, h.d2h, 0));
+    const size_t nn = (size_t)std::max<int64_t>(n, 1);
+    PP_CUDA(h.splits.ensure(nn * sizeof(int32_t)));
+    PP_CUDA(h.times.ensure(nn * sizeof(double)));
+    PP_CUDA(h.count.ensure(ns * sizeof(int32_t)));
+    PP_CUDA(h.tmax.ensure(ns * sizeof(double)));
+    PP_CUDA(h.obj.ensure(ns * sizeof(double)));
+    PP_CUDA(h.status.ensure(ns * sizeof(int32_t)));
+    PP_CUDA(h.err.ensure(ns * sizeof(int64_t)));
+    pp_plan_out d{};
+    if (out->ordered) {
+      PP_CUDA(h.ordered.ensure(nn * sizeof(pp_sample)));
+      d.ordered = h.ordered.as<pp_sample>();
+    }
+    if (out->order) {
+      PP_CUDA(h.order.ensure(nn * sizeof(int32_t)));
+      d.order = h.order.as<int32_t>();
+    }
+    d.splits = h.splits.as<int32_t>();
+    d.mb_times = h.times.as<double>();
+    d.count = h.count.as<int32_t>();
+    d.t_max_used = h.tmax.as<double>();
+    d.objective = h.obj.as<double>();
+    d.status = h.status.as<int32_t>();
+    d.err_sample_id = h.err.as<int64_t>();
+    rc = pp_plan_grid_device(sub, h.samples.as<pp_sample>(), h.seg.as<int64_t>(), h.hoff.as<int64_t>(), ns,
+                             presorted, grid, model, opts, &d);
+    if (rc) {
+      cudaStreamSynchronize(cs);  // no copy into the caller's buffers after the call
+      return rc;
+    }
+    done(q);
+    // drain this chunk's plans on the copy stream (the compute stream is idle:
+    // the planning call synchronised it)
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      return dst && bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs) : cudaSuccess;
+    };
+    PP_CUDA(d2h(out->ordered ? out->ordered + base : nullptr, d.ordered, n * sizeof(pp_sample)));
+    PP_CUDA(d2h(out->order ? out->order + base : nullptr, d.order, n * sizeof(int32_t)));
+    PP_CUDA(d2h(out->splits ? out->splits + base : nullptr, d.splits, n * sizeof(int32_t)));
+    PP_CUDA(d2h(out->mb_times ? out->mb_times + base : nullptr, d.mb_times, n * sizeof(double)));
+    PP_CUDA(d2h(out->count ? out->count + s0 : nullptr, d.count, ns * sizeof(int32_t)));
+    PP_CUDA(d2h(out->t_max_used ? out->t_max_used + s0 : nullptr, d.t_max_used, ns * sizeof(double)));
+    PP_CUDA(d2h(out->objective ? out->objective + s0 : nullptr, d.objective, ns * sizeof(double)));
+    PP_CUDA(d2h(out->status ? out->status + s0 : nullptr, d.status, ns * sizeof(int32_t)));
+    PP_CUDA(d2h(out->err_sample_id ? out->err_sample_id + s0 : nullptr, d.err_sample_id, ns * sizeof(int64_t)));
+    PP_CUDA(cudaEventRecord(h.d2h, cs));
+    h.d2h_pending = true;
+    q = qn;
+    set ^= 1;
+  }
+  PP_CUDA(cudaStreamSynchronize(cs));
+  return PP_OK;
+}
+
 int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets, int32_t n_seg,
                     int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
                     const pp_dp_options* opts, const pp_plan_out* out, int workers) {
   workers = std::min(workers, (int)n_seg);
-  const int chunks = std::min((int)n_seg, 2 * workers);
+  // two chunks per worker: one is planned while the other's inputs / plans
+  // cross PCIe (plan_host_chunks)
+  std::vector<int> wts(std::min<int>(n_seg, 2 * workers), 1);
+  const int chunks = (int)wts.size();
   while ((int)ctx->subs.size() < workers) {
     pp_ctx* sub = nullptr;
     const int rc = pp_ctx_create(ctx->device, &sub);
@@ -1473,8 +1603,11 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
   const int64_t total = seg_offsets[n_seg];
   std::vector<int> cut(chunks + 1, 0);
   cut[chunks] = n_seg;
+  int64_t wsum = 0, wacc = 0;
+  for (int wt : wts) wsum += wt;
   for (int p = 1; p < chunks; ++p) {
-    const int64_t target = total * p / chunks;
+    wacc += wts[p - 1];
+    const int64_t target = total * wacc / wsum;
     int s = cut[p - 1] + 1;
     while (s < n_seg - (chunks - p) && seg_offsets[s] < target) ++s;
     cut[p] = s;
@@ -1491,22 +1624,11 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
       sub->tuning.streams = 1;
       pp_stats S{};
       S.exit_thresh = INFINITY;
-      for (int k = next++; k < chunks && rcs[w] == PP_OK; k = next++) {
-        const int s0 = cut[k], s1 = cut[k + 1];
-        const int64_t base = seg_offsets[s0];
-        std::vector<int64_t> off(s1 - s0 + 1);
-        for (int s = s0; s <= s1; ++s) off[s - s0] = seg_offsets[s] - base;
-        pp_plan_out o{};
-        o.ordered = out->ordered ? out->ordered + base : nullptr;
-        o.order = out->order ? out->order + base : nullptr;
-        o.splits = out->splits ? out->splits + base : nullptr;
-        o.mb_times = out->mb_times ? out->mb_times + base : nullptr;
-        o.count = out->count ? out->count + s0 : nullptr;
-        o.t_max_used = out->t_max_used ? out->t_max_used + s0 : nullptr;
-        o.objective = out->objective ? out->objective + s0 : nullptr;
-        o.status = out->status ? out->status + s0 : nullptr;
-        o.err_sample_id = out->err_sample_id ? out->err_sample_id + s0 : nullptr;
-        rcs[w] = plan_host(sub, samples + base, off.data(), s1 - s0, presorted, grid, model, opts, &o);
+      auto claim = [&]() {
+        const int k = next++;
+        return k < chunks ? k : -1;
+      };
+      auto done = [&](int) {
         const pp_stats& t = sub->stats;
         S.candidates_generated += t.candidates_generated;
         S.candidates_evaluated += t.candidates_evaluated;
@@ -1528,7 +1650,9 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
         S.band_bytes += t.band_bytes;
         S.bound_transitions += t.bound_transitions;
         S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
-      }
+      };
+      rcs[w] = plan_host_chunks(sub, samples, seg_offsets, cut.data(), presorted, grid, model, opts, out,
+                                claim, done);
       acc[w] = S;
     });
   }
