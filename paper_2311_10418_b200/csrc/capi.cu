@@ -108,7 +108,8 @@ cudaError_t launch_dp_coop(int mode, int sanitize, const WorkItem& it, int grid,
                            double* gstate, void* parts, cudaStream_t st);
 cudaError_t launch_seg_init(const ItemResult* bound_res, int has_bound, int replicas,
                             const int64_t* cand_off, const int* cand_n, const double* cand,
-                            const int* active, SegDP* dp, int n_seg, cudaStream_t st);
+                            const int* active, const SegStats* tsingle, double margin, SegDP* dp,
+                            int n_seg, cudaStream_t st);
 cudaError_t launch_select(const WorkItem* items, const ItemResult* res, const int* seg_item_start,
                           const int* seg_item_cnt, const int* next_buf, int* best_next,
                           const int64_t* seg_off, const double* cand, const int64_t* cand_off,
@@ -665,7 +666,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   PP_CUDA(ctx->h_stats.ensure(n_seg * sizeof(SegStats)));
   PP_CUDA(ctx->band_base.ensure(n_seg * sizeof(int64_t)));
   SegStats* hs = ctx->h_stats.as<SegStats>();
-  for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0, 0, 0, 0ULL, 0ULL};
+  for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0, 0, 0, 0ULL, 0ULL, 0ULL};
   PP_CUDA(cudaMemcpyAsync(ctx->stats_d.p, hs, n_seg * sizeof(SegStats), cudaMemcpyHostToDevice, st));
   PP_CUDA(cudaMemcpyAsync(ctx->blk_base.p, blk_base.data(), (n_seg + 1) * sizeof(int),
                           cudaMemcpyHostToDevice, st));
@@ -999,6 +1000,10 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   const int64_t* d_cand_off = ctx->cand_off.as<int64_t>();
   const double* d_cand = ctx->cand.as<double>();
   int64_t bound_transitions = 0;
+  // with a certified slice-time surface (pass B's truncation certificate), t*
+  // is bounded below by the singleton slices: the bound pass then skips the
+  // minimax (MODE 2) and the first wave starts at that bound
+  const double* t_lo = nullptr;  // (non-null: the margin 2E; the bound is pass B's singleton maximum)
   if (!single) {
     std::vector<WorkItem> bi;
     int64_t goff = 0;
@@ -1029,7 +1034,10 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
         if (rc) return rc;
         PP_CUDA(timed_end(ctx));
       } else {
-        PP_TIMED(4, launch_dp_pass(1, ctx->bound_items.as<WorkItem>(), (int)bi.size(), smem_state,
+        // (pass B recorded the largest singleton time per segment, SegStats::tsingle)
+        const int bmode = std::isfinite(ctx->trunc_margin) && !table ? 2 : 1;
+        if (bmode == 2) t_lo = &ctx->trunc_margin;
+        PP_TIMED(4, launch_dp_pass(bmode, ctx->bound_items.as<WorkItem>(), (int)bi.size(), smem_state,
                                    state_global, table ? 1 : 0, dp_budget((int)bi.size()), c.d_seg_off,
                                    ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
                                    ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
@@ -1043,6 +1051,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   }
   PP_TIMED(7, launch_seg_init(ctx->bound_res.as<ItemResult>(), single ? 0 : 1, c.opts.replica_count,
                               d_cand_off, ctx->cand_n.as<int>(), d_cand, ctx->active.as<int>(),
+                              t_lo ? ctx->stats_d.as<SegStats>() : nullptr, t_lo ? *t_lo : 0.0,
                               ctx->segdp.as<SegDP>(), n_seg, st));
 
   // ---- 6. candidate waves

@@ -1019,6 +1019,19 @@ __global__ void __launch_bounds__(32 * kCostWarps)
       }
       __syncwarp();
     }
+    {
+      // the tile's singleton slices [i, i+1) (column r + 1 <= 32, in the dense
+      // near tile, written by this lane): their largest feasible time bounds
+      // t* from below (dp.cu seg_init_kernel)
+      double v = (r + 1 < W) ? tile[(size_t)(r + 1) * kRB + r] : QNAN;
+      v = (wr > 0 && !isnan(v)) ? v : -INF;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = (v < y) ? y : v;
+      }
+      if (lane == 0 && v > -INF) atomicMax(&a.stats[s].tsingle, dkey(v));
+    }
     const unsigned int npriced = (unsigned int)wr;  // live slices of the row: columns r+1 .. r+wr
     if (cbits) atomicOr(&s_bm[wid][cw], cbits);
     const bool any_b = __any_sync(0xffffffffu, any_binned);

@@ -141,6 +141,8 @@ __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int
 // MODE 0: DP pass of one t_max candidate: (sum, count, next) per row.
 // MODE 1: bound pass (t = +inf): min sum (microbatch.cpp:274-279) and the
 //         minimax slice time t* per row (the feasibility threshold).
+// MODE 2: the bound pass without the minimax, when a certified lower bound of
+//         t* comes from the singleton slices instead (seg_init_kernel).
 // SMEM_STATE: DP state in shared memory (else an L2-resident global ring).
 // SANITIZE: slice times may be -inf (generic SliceCostFn tables).  The
 //   reference skips non-finite state[j] (microbatch.cpp:180); states are stored
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     // state[n] = {0.0, 0} (microbatch.cpp:174), and its ring mirror
     for (int e = (int)(n & mask); ; e += entries) {
       st_s[e] = 0.0;
-      if (MODE == 0) st_c[e] = 0; else st_m[e] = -INF;
+      if (MODE == 0) st_c[e] = 0; else if (MODE == 1) st_m[e] = -INF;
       if (!(ring_state && e < kStatePad)) break;
     }
     row0[0] = INF;
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       pc[lane] = 0;
       pj[lane] = INT_MAX;
     } else {
-      pm[lane] = INF;
+      if (MODE == 1) pm[lane] = INF;
     }
   }
   __syncthreads();
@@ -353,9 +355,9 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         } else {
           // (NaN / +inf entries never pass the compares: see the far-far loop)
           s1 = (cs < s1) ? cs : s1;
-          const double mj = st_m[j & mask];
+          const double mj = MODE == 1 ? st_m[j & mask] : 0.0;
           const double v = (x < mj) ? mj : x;
-          m1 = (v < m1) ? v : m1;
+          if (MODE == 1) m1 = (v < m1) ? v : m1;
         }
       }
       const int o = wid * kRB + r;
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         npc[o] = c1;
         npj[o] = j1;
       } else {
-        npm[o] = m1;
+        if (MODE == 1) npm[o] = m1;
       }
     }
     // ---- the chain warp meanwhile loads its far-far partial, waits for its tile
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         ac = pc[pbuf];
         aj = pj[pbuf];
       } else {
-        am = pm[pbuf];
+        if (MODE == 1) am = pm[pbuf];
       }
       mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
     }
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
             c8[v] = npc[o];
             j8[v] = npj[o];
           } else {
-            m8[v] = npm[o];
+            m8[v] = MODE == 1 ? npm[o] : INF;
           }
         }
 #pragma unroll
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
               j8[v] = tk ? j8[v + h] : j8[v];
             } else {
               s8[v] = (s8[v + h] < s8[v]) ? s8[v + h] : s8[v];
-              m8[v] = (m8[v + h] < m8[v]) ? m8[v + h] : m8[v];
+              if (MODE == 1) m8[v] = (m8[v + h] < m8[v]) ? m8[v + h] : m8[v];
             }
           }
         }
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           aj = tk ? j8[0] : aj;
         } else {
           as = (s8[0] < as) ? s8[0] : as;
-          am = (m8[0] < am) ? m8[0] : am;
+          if (MODE == 1) am = (m8[0] < am) ? m8[0] : am;
         }
       }
       PP_TRACE(2);
@@ -456,10 +458,10 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           ac = upd ? cn : ac;
           aj = upd ? i0 + jj : aj;
         } else {
-          const double mj = __shfl_sync(0xffffffffu, am, jj);
+          const double mj = MODE == 1 ? __shfl_sync(0xffffffffu, am, jj) : 0.0;
           as = (ok & (cs < as)) ? cs : as;
           const double v = (x < mj) ? mj : x;
-          am = (ok & (v < am)) ? v : am;
+          if (MODE == 1) am = (ok & (v < am)) ? v : am;
         }
       };
       if (nb == kRB) {  // every block but the top one of a segment
@@ -489,8 +491,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           st_c[em] = f ? ac : 0;
           nxt[row] = f ? aj : -1;
         } else {
-          st_m[e] = am;
-          st_m[em] = am;
+          if (MODE == 1) st_m[e] = am;
+          if (MODE == 1) st_m[em] = am;
         }
         if (row == 0) {
           row0[0] = as;
@@ -549,9 +551,9 @@ __global__ void __launch_bounds__(kDpThreads, 2)
               // fail every `<`; x = +inf or state = +inf gives v = +inf, which
               // never beats the running minimum (<= +inf): no separate tests
               s_ = (cs < s_) ? cs : s_;
-              const double mj = sm[q0];
+              const double mj = MODE == 1 ? sm[q0] : 0.0;
               const double v = (x < mj) ? mj : x;
-              m_ = (v < m_) ? v : m_;
+              if (MODE == 1) m_ = (v < m_) ? v : m_;
             }
           }
           __syncwarp();  // the warp's reads of the slot, then its release
@@ -568,7 +570,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           aj = tk ? aj2 : aj;
         } else {
           as = (as2 < as) ? as2 : as;
-          am = (am2 < am) ? am2 : am;
+          if (MODE == 1) am = (am2 < am) ? am2 : am;
         }
         if (w == 0) PP_TRACE(9);
         const int o = w * kRB + r;
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           wpc[o] = ac;
           wpj[o] = aj;
         } else {
-          wpm[o] = am;
+          if (MODE == 1) wpm[o] = am;
         }
         named_bar(2, 32 * kWorkers);
         if (w == 0) {  // fold the 8 worker partials for the chain
@@ -592,7 +594,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
               }
             } else {
               as = (wps[p] < as) ? wps[p] : as;
-              am = (wpm[p] < am) ? wpm[p] : am;
+              if (MODE == 1) am = (wpm[p] < am) ? wpm[p] : am;
             }
           }
           const int pb2 = (bn & 1) * kRB + r;
@@ -601,7 +603,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
             pc[pb2] = ac;
             pj[pb2] = aj;
           } else {
-            pm[pb2] = am;
+            if (MODE == 1) pm[pb2] = am;
           }
         }
       }
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     rr.sum0 = row0[0];
     rr.count0 = MODE == 0 ? (int)row0[1] : 0;
     rr.feasible = isfinite(row0[0]) ? 1 : 0;
-    rr.aux = MODE == 1 ? row0[1] : 0.0;
+    rr.aux = MODE == 1 ? row0[1] : -__longlong_as_double(0x7ff0000000000000LL);  // (MODE 2: no t*)
     res[res_by_seg ? s : blockIdx.x] = rr;
   }
 }
@@ -625,6 +627,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
 __global__ void seg_init_kernel(const ItemResult* __restrict__ bound_res, int has_bound, int replicas,
                                 const int64_t* __restrict__ cand_off, const int* __restrict__ cand_n,
                                 const double* __restrict__ cand, const int* __restrict__ active,
+                                const SegStats* __restrict__ tsingle, double margin,
                                 SegDP* __restrict__ dp, int n_seg) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_seg) return;
@@ -648,7 +651,12 @@ __global__ void seg_init_kernel(const ItemResult* __restrict__ bound_res, int ha
   if (has_bound) {
     const ItemResult r = bound_res[s];
     d.bound = r.sum0 / (double)replicas;  // microbatch.cpp:278
-    d.tstar = r.aux;
+    // t*, or (MODE 2 bound pass) its certified lower bound: on a length-sorted
+    // segment with a certified slice-time surface every slice [a, b) costs at
+    // least (exactly) the singleton [i, i+1) of any sample it holds, so
+    // t* >= max_i T(i, i+1) exactly and >= (computed max) - 2E as computed;
+    // candidates below it are infeasible just the same
+    d.tstar = tsingle ? __dsub_rd(dkey_inv(tsingle[s].tsingle), margin) : r.aux;
     // first candidate >= t*: every candidate below it is infeasible (no
     // partition keeps all slices <= t), so the reference only `continue`s
     // there (microbatch.cpp:292) before any best exists.
@@ -1001,8 +1009,10 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
   } while (0)
   if (mode == 0) {
     if (state_global) PP_DP_LAUNCH_Z(0, false); else PP_DP_LAUNCH_Z(0, true);
-  } else {
+  } else if (mode == 1) {
     if (state_global) PP_DP_LAUNCH_Z(1, false); else PP_DP_LAUNCH_Z(1, true);
+  } else {
+    if (state_global) PP_DP_LAUNCH_Z(2, false); else PP_DP_LAUNCH_Z(2, true);
   }
 #undef PP_DP_LAUNCH_Z
 #undef PP_DP_LAUNCH
@@ -1011,11 +1021,13 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
 
 cudaError_t launch_seg_init(const ItemResult* bound_res, int has_bound, int replicas,
                             const int64_t* cand_off, const int* cand_n, const double* cand,
-                            const int* active, SegDP* dp, int n_seg, cudaStream_t st) {
+                            const int* active, const SegStats* tsingle, double margin, SegDP* dp,
+                            int n_seg, cudaStream_t st) {
   seg_init_kernel<<<(n_seg + 127) / 128, 128, 0, st>>>(bound_res, has_bound, replicas, cand_off,
-                                                       cand_n, cand, active, dp, n_seg);
+                                                       cand_n, cand, active, tsingle, margin, dp, n_seg);
   return cudaGetLastError();
 }
+
 
 cudaError_t launch_select(const WorkItem* items, const ItemResult* res, const int* seg_item_start,
                           const int* seg_item_cnt, const int* next_buf, int* best_next,

@@ -300,6 +300,7 @@ struct SegStats {
   int pad;
   unsigned long long priced;   // slices priced by cost pass A
   unsigned long long priced_b; // band slices priced by cost pass B
+  unsigned long long tsingle;  // dkey of the largest feasible singleton slice time (band_run_kernel; 0: none)
 };
 
 // ---- TMA bulk copies + mbarriers (sm_90+ PTX, used on sm_100a) ----------
