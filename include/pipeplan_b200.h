@@ -158,7 +158,8 @@ typedef struct pp_stats {
    * stream) and launch counts: [0] segmented sort, [1] cost setup (axis
    * brackets, row widths, tile offsets), [2] cost pass A (act_mem, row
    * widths), [3] cost pass B (band tiles + candidate bins), [4] DP bound
-   * pass (t = +inf), [5] DP candidate passes, [6] candidate compaction,
+   * pass (t = +inf; fused with the first candidate pass on certified sorted
+   * GPT mini-batches), [5] DP candidate passes, [6] candidate compaction,
    * [7] selection / assembly */
   double  ms_kernel[8];
   int64_t launches[8];

@@ -85,7 +85,7 @@ class PlanOut(C.Structure):
 
 
 KERNEL_NAMES = ["segmented sort", "cost setup", "cost pass A (act_mem row widths)",
-                "cost pass B (band tiles + candidate bins)", "DP bound pass", "DP candidate passes",
+                "cost pass B (band tiles + candidate bins)", "DP bound pass (+ first candidate, fused)", "DP candidate passes",
                 "candidate compaction", "selection / assembly"]
 
 

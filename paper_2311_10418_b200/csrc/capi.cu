@@ -92,7 +92,9 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, const double* cmin, double t_margin,
                            unsigned long long* cols_streamed, const short* colbase, const int* chunk_nv,
-                           const int* row_w, cudaStream_t st);
+                           const int* row_w, ItemResult* res2, cudaStream_t st);
+cudaError_t launch_seg_set_bound(const ItemResult* bound_res, int replicas, SegDP* dp, int n_seg,
+                                 cudaStream_t st);
 cudaError_t launch_mb_shapes(const pp_sample* ordered, const int64_t* seg_off, const int32_t* splits,
                              const int64_t* mb_off, int n_seg, int64_t n_mb, pp_padded_shape* shapes,
                              cudaStream_t st);
@@ -812,7 +814,7 @@ void place_states(std::vector<WorkItem>& items, int mode, size_t& smem_state, in
   for (WorkItem& w : items) {
     if (state_global) {
       w.state_off = goff;
-      goff += 2 * (int64_t)dp_state_stride(w.state_entries);
+      goff += (int64_t)((dp_state_bytes(mode, w.state_entries) + 7) / 8);
     } else {
       w.state_off = -1;
       smem_state = std::max(smem_state, dp_state_bytes(mode, w.state_entries));
@@ -1004,6 +1006,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   // is bounded below by the singleton slices: the bound pass then skips the
   // minimax (MODE 2) and the first wave starts at that bound
   const double* t_lo = nullptr;  // (non-null: the margin 2E; the bound is pass B's singleton maximum)
+  bool fused = false;
   if (!single) {
     std::vector<WorkItem> bi;
     int64_t goff = 0;
@@ -1028,15 +1031,19 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       PP_CUDA(ctx->next_buf.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
       PP_CUDA(cudaMemcpyAsync(ctx->bound_items.p, bi.data(), bi.size() * sizeof(WorkItem),
                               cudaMemcpyHostToDevice, st));
-      if (use_coop(ctx, bi, c.h_seg_off)) {
+      const bool coop = use_coop(ctx, bi, c.h_seg_off);
+      // (pass B recorded the largest singleton time per segment, SegStats::tsingle)
+      const int bmode = std::isfinite(ctx->trunc_margin) && !table ? 2 : 1;
+      if (bmode == 2 && !coop) t_lo = &ctx->trunc_margin;
+      // the first wave's candidate is then known before the bound: one fused
+      // pass runs both (MODE 3, in the wave loop below)
+      fused = t_lo != nullptr && std::max(1, ctx->tuning.first_wave) == 1;
+      if (coop) {
         PP_CUDA(timed_begin(ctx, 4));
         int rc = run_coop(ctx, 1, table ? 1 : 0, bi, c, ctx->bound_res.as<ItemResult>(), 1, st);
         if (rc) return rc;
         PP_CUDA(timed_end(ctx));
-      } else {
-        // (pass B recorded the largest singleton time per segment, SegStats::tsingle)
-        const int bmode = std::isfinite(ctx->trunc_margin) && !table ? 2 : 1;
-        if (bmode == 2) t_lo = &ctx->trunc_margin;
+      } else if (!fused) {
         PP_TIMED(4, launch_dp_pass(bmode, ctx->bound_items.as<WorkItem>(), (int)bi.size(), smem_state,
                                    state_global, table ? 1 : 0, dp_budget((int)bi.size()), c.d_seg_off,
                                    ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
@@ -1044,12 +1051,12 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                    ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
                                    ctx->gstate.as<double>(), 1, nullptr, 0.0, nullptr,
                                    ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                   ctx->row_w.as<int>(), st));
+                                   ctx->row_w.as<int>(), nullptr, st));
       }
       PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
     }
   }
-  PP_TIMED(7, launch_seg_init(ctx->bound_res.as<ItemResult>(), single ? 0 : 1, c.opts.replica_count,
+  PP_TIMED(7, launch_seg_init(ctx->bound_res.as<ItemResult>(), single ? 0 : fused ? 2 : 1, c.opts.replica_count,
                               d_cand_off, ctx->cand_n.as<int>(), d_cand, ctx->active.as<int>(),
                               t_lo ? ctx->stats_d.as<SegStats>() : nullptr, t_lo ? *t_lo : 0.0,
                               ctx->segdp.as<SegDP>(), n_seg, st));
@@ -1077,10 +1084,10 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       item_cnt[s] = 0;
       if (hd[s].done) continue;
       const int n = (int)(c.h_seg_off[s + 1] - c.h_seg_off[s]);
-      const int k = std::min(wave, hd[s].n_cand - hd[s].next_cand);
+      const int k = std::min(fused ? 1 : wave, hd[s].n_cand - hd[s].next_cand);
       WorkItem proto{};
       size_t need;
-      state_layout(0, n, hs[s].wmax, proto.state_mask, proto.state_entries, need);
+      state_layout(fused ? 3 : 0, n, hs[s].wmax, proto.state_mask, proto.state_entries, need);
       for (int q = 0; q < k; ++q) {
         WorkItem w = proto;
         w.seg = s;
@@ -1094,7 +1101,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     if (items.empty()) break;
     size_t smem_state = 0;
     int state_global = 0;
-    place_states(items, 0, smem_state, state_global, goff);
+    place_states(items, fused ? 3 : 0, smem_state, state_global, goff);
     ++waves;
     evaluated += (int64_t)items.size();
     const int ni = (int)items.size();
@@ -1107,7 +1114,19 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(cudaMemcpyAsync(ctx->items.p, items.data(), ni * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_start.p, item_start.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
     PP_CUDA(cudaMemcpyAsync(ctx->seg_item_cnt.p, item_cnt.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
-    if (use_coop(ctx, items, c.h_seg_off)) {
+    if (fused) {
+      // the bound pass and the first wave in one band stream (MODE 3): the
+      // candidate results per item, the bounds per segment
+      PP_TIMED(4, launch_dp_pass(3, ctx->items.as<WorkItem>(), ni, smem_state, state_global, 0, dp_budget(ni),
+                                 c.d_seg_off, ctx->blk_base.as<int>(), ctx->blk_W.as<int>(),
+                                 ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
+                                 ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
+                                 ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, nullptr, 0.0, nullptr,
+                                 ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
+                                 ctx->row_w.as<int>(), ctx->bound_res.as<ItemResult>(), st));
+      PP_TIMED(7, launch_seg_set_bound(ctx->bound_res.as<ItemResult>(), c.opts.replica_count,
+                                       ctx->segdp.as<SegDP>(), n_seg, st));
+    } else if (use_coop(ctx, items, c.h_seg_off)) {
       PP_CUDA(timed_begin(ctx, 5));
       int rc = run_coop(ctx, 0, table ? 1 : 0, items, c, ctx->results.as<ItemResult>(), 0, st);
       if (rc) return rc;
@@ -1122,7 +1141,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                  trunc ? ctx->cmin.as<double>() : nullptr, ctx->trunc_margin,
                                  ctx->dp_cols.as<unsigned long long>(),
                                  ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                 ctx->row_w.as<int>(), st));
+                                 ctx->row_w.as<int>(), nullptr, st));
       counted = true;
     }
     PP_TIMED(7, launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
@@ -1130,6 +1149,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                               ctx->next_buf.as<int>(), ctx->best_next.as<int>(), c.d_seg_off, d_cand,
                               d_cand_off, c.opts.stage_count, c.opts.replica_count,
                               ctx->segdp.as<SegDP>(), n_seg, st));
+    if (fused) fused = false;  // (wave 1 done; the doubling goes on from it)
     wave = std::min(wave * 2, max_wave);
   }
   PP_CUDA(cudaEventRecord(ctx->ev[3], st));

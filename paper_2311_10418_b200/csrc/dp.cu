@@ -88,10 +88,14 @@ struct DpSmem {
   static constexpr size_t nps = pj + 2 * kRB * 4;                     // [8][32] double  near-far partials
   static constexpr size_t npx = nps + kWorkers * kRB * 8;             // [8][32] double / int
   static constexpr size_t npj = npx + kWorkers * kRB * 8;             // [8][32] int
-  static constexpr size_t row0 = npj + kWorkers * kRB * 4;            // raw state[0] (sum, aux)
+  // MODE 3 (fused bound + candidate): the bound sums' partials
+  static constexpr size_t npb = npj + kWorkers * kRB * 4;             // [8][32] double  near-far
+  static constexpr size_t wpb = npb + kWorkers * kRB * 8;             // [8][32] double  worker
+  static constexpr size_t pb = wpb + kWorkers * kRB * 8;              // [2][32] double  folded
+  static constexpr size_t row0 = pb + 2 * kRB * 8;                    // raw state[0] (sum, aux, bound)
   // compact band: column -> window index tables of the near tiles and the
   // ring chunks (int16), and the row widths of the current / next block
-  static constexpr size_t cbn = (row0 + 16 + 15) / 16 * 16;           // [2][64] short
+  static constexpr size_t cbn = (row0 + 32 + 15) / 16 * 16;           // [2][64] short
   static constexpr size_t cbr = cbn + kNearBufs * kNearCols * 2;      // [kMaxRing][32] short
   static constexpr size_t wrs = cbr + kMaxRing * kChunkCols * 2;      // [2][32] int
   static constexpr size_t bars = (wrs + 2 * kRB * 4 + 15) / 16 * 16;  // mbarriers: near full/empty
@@ -106,7 +110,7 @@ size_t dp_smem_fixed() { return DpSmem::state; }
 constexpr int kStatePad = 32;
 int dp_state_stride(int entries) { return entries + kStatePad; }
 size_t dp_state_bytes(int mode, int entries) {
-  return (size_t)(entries + kStatePad) * (mode == 0 ? 12 : 16);
+  return (size_t)(entries + kStatePad) * (mode == 0 ? 12 : mode == 3 ? 20 : 16);
 }
 size_t dp_chunk_bytes() { return kChunkBytes; }
 int dp_max_ring() { return kMaxRing; }
@@ -143,6 +147,11 @@ __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int
 //         minimax slice time t* per row (the feasibility threshold).
 // MODE 2: the bound pass without the minimax, when a certified lower bound of
 //         t* comes from the singleton slices instead (seg_init_kernel).
+// MODE 3: MODE 2 fused with the first candidate pass (MODE 0): that candidate
+//         (the first >= the singleton bound) is known before the bound, so
+//         one pass streams the band once and runs both recurrences — two
+//         independent chains interleaved in the same triangle steps.  The
+//         candidate result goes to res[item], the bound to res2[segment].
 // SMEM_STATE: DP state in shared memory (else an L2-resident global ring).
 // SANITIZE: slice times may be -inf (generic SliceCostFn tables).  The
 //   reference skips non-finite state[j] (microbatch.cpp:180); states are stored
@@ -165,7 +174,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
                    int* __restrict__ next_buf, double* __restrict__ gstate, int res_by_seg,
                    int ring_off, int kRing, const double* __restrict__ cmin, double t_margin,
                    unsigned long long* __restrict__ cols_streamed, const short* __restrict__ colbase,
-                   const int* __restrict__ chunk_nv, const int* __restrict__ row_w) {
+                   const int* __restrict__ chunk_nv, const int* __restrict__ row_w,
+                   ItemResult* __restrict__ res2) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* near = reinterpret_cast<double*>(smem + DpSmem::near);
   double* ring = reinterpret_cast<double*>(smem + ring_off);
@@ -181,6 +191,9 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   int* npc = reinterpret_cast<int*>(smem + DpSmem::npx);        // MODE 0
   double* npm = reinterpret_cast<double*>(smem + DpSmem::npx);  // MODE 1
   int* npj = reinterpret_cast<int*>(smem + DpSmem::npj);
+  double* npb = reinterpret_cast<double*>(smem + DpSmem::npb);  // MODE 3
+  double* wpb = reinterpret_cast<double*>(smem + DpSmem::wpb);  // MODE 3
+  double* pb = reinterpret_cast<double*>(smem + DpSmem::pb);    // MODE 3
   double* row0 = reinterpret_cast<double*>(smem + DpSmem::row0);
   short* cbn = reinterpret_cast<short*>(smem + DpSmem::cbn);
   short* cbr = reinterpret_cast<short*>(smem + DpSmem::cbr);
@@ -211,13 +224,18 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
+  // CAND: the candidate recurrence (lexmin of (sum, count, j) over T <= t);
+  // BSUM: MODE 3's extra bound recurrence (min sum, t = +inf)
+  constexpr bool CAND = MODE == 0 || MODE == 3;
+  constexpr bool BSUM = MODE == 3;
 
   // state: ring of R = mask + 1 entries (mask = ~0 when not a ring)
   const unsigned mask = it.state_mask;
   const int entries = it.state_entries;
   double* st_s = SMEM_STATE ? reinterpret_cast<double*>(smem + DpSmem::state) : gstate + it.state_off;
-  int* st_c = reinterpret_cast<int*>(st_s + entries + kStatePad);  // MODE 0
-  double* st_m = st_s + entries + kStatePad;                        // MODE 1
+  int* st_c = reinterpret_cast<int*>(st_s + (BSUM ? 2 : 1) * (entries + kStatePad));  // CAND
+  double* st_m = st_s + entries + kStatePad;                                         // MODE 1
+  double* st_b = st_s + entries + kStatePad;                                         // MODE 3
   const bool ring_state = mask != ~0u;
   int* nxt = next_buf + it.next_off;
 
@@ -235,15 +253,18 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     // state[n] = {0.0, 0} (microbatch.cpp:174), and its ring mirror
     for (int e = (int)(n & mask); ; e += entries) {
       st_s[e] = 0.0;
-      if (MODE == 0) st_c[e] = 0; else if (MODE == 1) st_m[e] = -INF;
+      if (CAND) st_c[e] = 0; else if (MODE == 1) st_m[e] = -INF;
+      if (BSUM) st_b[e] = 0.0;
       if (!(ring_state && e < kStatePad)) break;
     }
     row0[0] = INF;
-    row0[1] = MODE == 0 ? 0.0 : INF;
+    row0[1] = CAND ? 0.0 : INF;
+    row0[2] = INF;
   }
   if (wid == 0) {  // block 0 has no far-far columns (j <= n < i0 + 64)
     ps[lane] = INF;
-    if (MODE == 0) {
+    if (BSUM) pb[lane] = INF;
+    if (CAND) {
       pc[lane] = 0;
       pj[lane] = INT_MAX;
     } else {
@@ -339,14 +360,18 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       const int W = blk_W[gb0 + b];
       const int r = lane;
       mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
-      double s1 = INF, m1 = INF;
+      double s1 = INF, m1 = INF, b1 = INF;
       int c1 = 0, j1 = INT_MAX;
       const int cnf = min(kNearCols, W);
       for (int c = nb + wid; c < cnf; c += kWorkers) {
         const double x = nt[c * kRB + r];
         const int j = i0 + c;
         const double cs = __dadd_rn(x, st_s[j & mask]);
-        if (MODE == 0) {
+        if (BSUM) {
+          const double cb = __dadd_rn(x, st_b[j & mask]);
+          b1 = (cb < b1) ? cb : b1;
+        }
+        if (CAND) {
           const int cn = 1 + st_c[j & mask];
           const bool upd = (x <= t) & ((cs < s1) | ((cs == s1) & (cn < c1)));
           s1 = upd ? cs : s1;
@@ -362,7 +387,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       }
       const int o = wid * kRB + r;
       nps[o] = s1;
-      if (MODE == 0) {
+      if (BSUM) npb[o] = b1;
+      if (CAND) {
         npc[o] = c1;
         npj[o] = j1;
       } else {
@@ -372,13 +398,14 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     // ---- the chain warp meanwhile loads its far-far partial, waits for its tile
     const int W = blk_W[gb0 + b];
     const int r = lane;
-    double as = INF, am = INF;
+    double as = INF, am = INF, ab = INF;
     int ac = 0, aj = INT_MAX;
     if (wid == kChainWarp) {
       PP_TRACE(0);
       const int pbuf = (b & 1) * kRB + r;
       as = ps[pbuf];
-      if (MODE == 0) {
+      if (BSUM) ab = pb[pbuf];
+      if (CAND) {
         ac = pc[pbuf];
         aj = pj[pbuf];
       } else {
@@ -394,13 +421,14 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       // fold the 8 near-far partials: a pairwise tree (ILP), lexmin with j
       // ties is associative
       {
-        double s8[kWorkers], m8[kWorkers];
+        double s8[kWorkers], m8[kWorkers], b8[kWorkers];
         int c8[kWorkers], j8[kWorkers];
 #pragma unroll
         for (int v = 0; v < kWorkers; ++v) {
           const int o = v * kRB + r;
           s8[v] = nps[o];
-          if (MODE == 0) {
+          b8[v] = BSUM ? npb[o] : INF;
+          if (CAND) {
             c8[v] = npc[o];
             j8[v] = npj[o];
           } else {
@@ -411,7 +439,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         for (int h = kWorkers / 2; h >= 1; h /= 2) {
 #pragma unroll
           for (int v = 0; v < h; ++v) {
-            if (MODE == 0) {
+            if (BSUM) b8[v] = (b8[v + h] < b8[v]) ? b8[v + h] : b8[v];
+            if (CAND) {
               const bool tk = better(s8[v + h], c8[v + h], j8[v + h], s8[v], c8[v], j8[v]);
               s8[v] = tk ? s8[v + h] : s8[v];
               c8[v] = tk ? c8[v + h] : c8[v];
@@ -422,7 +451,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
             }
           }
         }
-        if (MODE == 0) {
+        if (BSUM) ab = (b8[0] < ab) ? b8[0] : ab;
+        if (CAND) {
           const bool tk = better(s8[0], c8[0], j8[0], as, ac, aj);
           as = tk ? s8[0] : as;
           ac = tk ? c8[0] : ac;
@@ -437,6 +467,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         as = INF;
         ac = 0;
         am = INF;
+        ab = INF;
       }
       // Step jj: lane jj's row is final; broadcast it, the lanes below absorb
       // T[i0 + r, i0 + jj] + state.  Descending j: equal (sum, count) takes
@@ -450,8 +481,14 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         double sj = __shfl_sync(0xffffffffu, as, jj);
         if (SANITIZE) sj = isfinite(sj) ? sj : INF;
         const double cs = __dadd_rn(x, sj);
-        const bool ok = (jj < W) & (r < jj) & (MODE == 0 ? (x <= t) : true);  // (NaN: fails the `<`s)
-        if (MODE == 0) {
+        const bool okb = (jj < W) & (r < jj);
+        const bool ok = okb & (CAND ? (x <= t) : true);  // (NaN: fails the `<`s)
+        if (BSUM) {  // the bound chain, independent of the candidate chain
+          const double bj = __shfl_sync(0xffffffffu, ab, jj);
+          const double cb = __dadd_rn(x, bj);
+          ab = (okb & (cb < ab)) ? cb : ab;
+        }
+        if (CAND) {
           const int cn = 1 + __shfl_sync(0xffffffffu, ac, jj);
           const bool upd = ok & ((cs < as) | ((cs == as) & (cn <= ac)));
           as = upd ? cs : as;
@@ -486,7 +523,11 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         const double sv = (SANITIZE && !f) ? INF : as;
         st_s[e] = sv;
         st_s[em] = sv;
-        if (MODE == 0) {
+        if (BSUM) {
+          st_b[e] = ab;
+          st_b[em] = ab;
+        }
+        if (CAND) {
           st_c[e] = f ? ac : 0;
           st_c[em] = f ? ac : 0;
           nxt[row] = f ? aj : -1;
@@ -496,7 +537,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         }
         if (row == 0) {
           row0[0] = as;
-          row0[1] = MODE == 0 ? (double)ac : am;
+          row0[1] = CAND ? (double)ac : am;
+          row0[2] = ab;
         }
       }
     } else {
@@ -509,7 +551,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         const int k0 = max(0, j1 - kRB);  // i0 of block b+1
         const int Wn = blk_W[gb0 + bn];
         const int nc = far_nc(gb0 + bn, Wn);
-        double as = INF, am = INF, as2 = INF, am2 = INF;
+        double as = INF, am = INF, as2 = INF, am2 = INF, ab = INF, ab2 = INF;
         int ac = 0, aj = INT_MAX, ac2 = 0, aj2 = INT_MAX;
         const int r = lane;
 
@@ -523,6 +565,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           const double* ss = st_s + jb;
           const int* sc = st_c + jb;
           const double* sm = st_m + jb;
+          const double* sb = st_b + jb;
 #pragma unroll
           for (int q0 = 0; q0 < kChunkCols; q0 += kWorkers) {
             const int q = q0 + w;
@@ -540,7 +583,12 @@ __global__ void __launch_bounds__(kDpThreads, 2)
             int& c_ = (q0 / kWorkers) & 1 ? ac2 : ac;
             int& j_ = (q0 / kWorkers) & 1 ? aj2 : aj;
             double& m_ = (q0 / kWorkers) & 1 ? am2 : am;
-            if (MODE == 0) {
+            if (BSUM) {
+              double& b_ = (q0 / kWorkers) & 1 ? ab2 : ab;
+              const double cb = __dadd_rn(x, sb[q0]);
+              b_ = (cb < b_) ? cb : b_;
+            }
+            if (CAND) {
               const int cn = 1 + sc[q0];
               const bool upd = (x <= t) & ((cs < s_) | ((cs == s_) & (cn < c_)));
               s_ = upd ? cs : s_;
@@ -563,7 +611,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
             cphase ^= 1u;
           }
         }
-        if (MODE == 0) {
+        if (BSUM) ab = (ab2 < ab) ? ab2 : ab;
+        if (CAND) {
           const bool tk = better(as2, ac2, aj2, as, ac, aj);
           as = tk ? as2 : as;
           ac = tk ? ac2 : ac;
@@ -575,7 +624,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         if (w == 0) PP_TRACE(9);
         const int o = w * kRB + r;
         wps[o] = as;
-        if (MODE == 0) {
+        if (BSUM) wpb[o] = ab;
+        if (CAND) {
           wpc[o] = ac;
           wpj[o] = aj;
         } else {
@@ -586,7 +636,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
 #pragma unroll
           for (int v = 1; v < kWorkers; ++v) {
             const int p = v * kRB + r;
-            if (MODE == 0) {
+            if (BSUM) ab = (wpb[p] < ab) ? wpb[p] : ab;
+            if (CAND) {
               if (better(wps[p], wpc[p], wpj[p], as, ac, aj)) {
                 as = wps[p];
                 ac = wpc[p];
@@ -599,7 +650,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           }
           const int pb2 = (bn & 1) * kRB + r;
           ps[pb2] = as;
-          if (MODE == 0) {
+          if (BSUM) pb[pb2] = ab;
+          if (CAND) {
             pc[pb2] = ac;
             pj[pb2] = aj;
           } else {
@@ -616,10 +668,18 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   if (threadIdx.x == 0) {  // after the last block barrier: row0 is final
     ItemResult rr;
     rr.sum0 = row0[0];
-    rr.count0 = MODE == 0 ? (int)row0[1] : 0;
+    rr.count0 = CAND ? (int)row0[1] : 0;
     rr.feasible = isfinite(row0[0]) ? 1 : 0;
     rr.aux = MODE == 1 ? row0[1] : -__longlong_as_double(0x7ff0000000000000LL);  // (MODE 2: no t*)
     res[res_by_seg ? s : blockIdx.x] = rr;
+    if (BSUM) {  // the fused bound pass's result, by segment
+      ItemResult rb;
+      rb.sum0 = row0[2];
+      rb.count0 = 0;
+      rb.feasible = isfinite(row0[2]) ? 1 : 0;
+      rb.aux = -__longlong_as_double(0x7ff0000000000000LL);
+      res2[s] = rb;
+    }
   }
 }
 
@@ -649,7 +709,9 @@ __global__ void seg_init_kernel(const ItemResult* __restrict__ bound_res, int ha
   }
   d.done = 0;
   if (has_bound) {
-    const ItemResult r = bound_res[s];
+    // has_bound 2: before a fused (MODE 3) pass — the bound arrives with the
+    // first wave's results (seg_set_bound_kernel); t* comes from the singletons
+    const ItemResult r = has_bound == 1 ? bound_res[s] : ItemResult{};
     d.bound = r.sum0 / (double)replicas;  // microbatch.cpp:278
     // t*, or (MODE 2 bound pass) its certified lower bound: on a length-sorted
     // segment with a certified slice-time surface every slice [a, b) costs at
@@ -677,6 +739,14 @@ __global__ void seg_init_kernel(const ItemResult* __restrict__ bound_res, int ha
     d.ref_evals = d.n_cand;
   }
   dp[s] = d;
+}
+
+// After a fused (MODE 3) pass: the bound of every segment still in the loop.
+__global__ void seg_set_bound_kernel(const ItemResult* __restrict__ bound_res, int replicas,
+                                     SegDP* __restrict__ dp, int n_seg) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_seg || dp[s].done) return;
+  dp[s].bound = bound_res[s].sum0 / (double)replicas;  // microbatch.cpp:278
 }
 
 // Lexicographic compare of two split vectors given as next[] chains from 0
@@ -986,7 +1056,7 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, const double* cmin, double t_margin,
                            unsigned long long* cols_streamed, const short* colbase, const int* chunk_nv,
-                           const int* row_w, cudaStream_t st) {
+                           const int* row_w, ItemResult* res2, cudaStream_t st) {
   if (n_items == 0) return cudaSuccess;
   const size_t ring_off = (DpSmem::state + (state_global ? 0 : smem_state) + 127) / 128 * 128;
   int ring = (int)std::min<size_t>(kMaxRing, (smem_budget - std::min(smem_budget, ring_off)) / kChunkBytes);
@@ -999,7 +1069,7 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
     dp_pass_kernel<M, S, Z, C><<<n_items, kDpThreads, smem, st>>>(                                    \
         items, seg_off, blk_base, blk_W, tile_off, seg_band_base, band, cand, cand_off, res, next_buf, \
         gstate, res_by_seg, (int)ring_off, ring, cmin, t_margin, cols_streamed, colbase, chunk_nv,    \
-        row_w);                                                                                       \
+        row_w, res2);                                                                                 \
   } while (0)
 #define PP_DP_LAUNCH_Z(M, S)                                   \
   do {                                                         \
@@ -1011,8 +1081,10 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
     if (state_global) PP_DP_LAUNCH_Z(0, false); else PP_DP_LAUNCH_Z(0, true);
   } else if (mode == 1) {
     if (state_global) PP_DP_LAUNCH_Z(1, false); else PP_DP_LAUNCH_Z(1, true);
-  } else {
+  } else if (mode == 2) {
     if (state_global) PP_DP_LAUNCH_Z(2, false); else PP_DP_LAUNCH_Z(2, true);
+  } else {
+    if (state_global) PP_DP_LAUNCH_Z(3, false); else PP_DP_LAUNCH_Z(3, true);
   }
 #undef PP_DP_LAUNCH_Z
 #undef PP_DP_LAUNCH
@@ -1028,6 +1100,12 @@ cudaError_t launch_seg_init(const ItemResult* bound_res, int has_bound, int repl
   return cudaGetLastError();
 }
 
+
+cudaError_t launch_seg_set_bound(const ItemResult* bound_res, int replicas, SegDP* dp, int n_seg,
+                                 cudaStream_t st) {
+  seg_set_bound_kernel<<<(n_seg + 127) / 128, 128, 0, st>>>(bound_res, replicas, dp, n_seg);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_select(const WorkItem* items, const ItemResult* res, const int* seg_item_start,
                           const int* seg_item_cnt, const int* next_buf, int* best_next,

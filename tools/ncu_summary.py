@@ -90,8 +90,10 @@ def full(rep: str):
 CATEGORY = [("band_run_kernel", "cost pass B (band tiles + candidate bins)"),
             ("band3_kernel", "cost pass B (band tiles + candidate bins)"),
             ("band_kernel", "cost pass B (band tiles + candidate bins)"),
-            ("dp_pass_kernel<0", "DP bound pass"),
-            ("dp_pass_kernel<1", "DP candidate passes")]
+            ("dp_pass_kernel<1", "DP bound pass (+ first candidate, fused)"),
+            ("dp_pass_kernel<2", "DP bound pass (+ first candidate, fused)"),
+            ("dp_pass_kernel<3", "DP bound pass (+ first candidate, fused)"),
+            ("dp_pass_kernel<0", "DP candidate passes")]
 
 
 def traffic(rep: str, plans: int, source: str) -> dict:
