@@ -174,11 +174,17 @@ __global__ void __launch_bounds__(kSortThreads)
   // key still fits the word count the launcher chose from the call's range):
   // ids of a mini-batch usually span far fewer bits than the call's ids
   __shared__ long long s_rng[kSortThreads / 32][6];
+  // ids strictly increasing in input order (the common case: ids are indices):
+  // a stable sort on (input, target) alone then yields the (input, target, id)
+  // order, with the id bits out of the key
+  bool ids_in_order;
   {
     long long lo[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
     long long hi[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+    int unordered = 0;  // some id is not above its predecessor's
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
       const pp_sample v = in[b + k];
+      if (k + 1 < n) unordered |= in[b + k + 1].id <= v.id;
       const long long f[3] = {v.input_len, v.target_len, v.id};
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(kSortThreads)
         s_rng[threadIdx.x >> 5][3 + q] = hi[q];
       }
     }
-    __syncthreads();
+    ids_in_order = !__syncthreads_or(unordered);
   }
   long long mn[3];
   int bits[3];
@@ -214,6 +220,7 @@ __global__ void __launch_bounds__(kSortThreads)
     mn[q] = lo;
     bits[q] = bit_width((unsigned long long)hi - (unsigned long long)lo);
   }
+  if (ids_in_order) bits[2] = 0;
   (void)range;
   unsigned long long *k0, *k1;
   uint32_t *v0, *v1;
@@ -232,7 +239,7 @@ __global__ void __launch_bounds__(kSortThreads)
     const pp_sample v = in[b + k];
     const unsigned long long fi = (unsigned long long)v.input_len - (unsigned long long)mn[0];
     const unsigned long long ft = (unsigned long long)v.target_len - (unsigned long long)mn[1];
-    const unsigned long long fd = (unsigned long long)v.id - (unsigned long long)mn[2];
+    const unsigned long long fd = ids_in_order ? 0ULL : (unsigned long long)v.id - (unsigned long long)mn[2];
     if (W == 1) {
       // caller checked bits[0]+bits[1]+bits[2] <= 64; guard the 64-bit shifts
       const int s1 = bits[1] + bits[2];
