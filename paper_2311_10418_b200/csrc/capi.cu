@@ -789,10 +789,10 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
 size_t dp_budget(int n_items) { return n_items <= 148 ? 220 * 1024 : 110 * 1024; }
 
 void state_layout(int mode, int n, int wmax, unsigned& mask, int& entries, size_t& smem) {
-  int R = 64;
-  while (R < wmax + 64) R <<= 1;
+  // a ring of R >= W_max + 64 slots (a multiple of 32; dp.cu indexes it mod R)
+  const int R = (wmax + 64 + 31) / 32 * 32;
   if (R < n + 1) {
-    mask = (unsigned)(R - 1);
+    mask = (unsigned)(R - 1);  // (any value but ~0: "a ring")
     entries = R;
   } else {
     mask = ~0u;

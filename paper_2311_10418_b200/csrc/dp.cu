@@ -237,6 +237,11 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   double* st_m = st_s + entries + kStatePad;                                         // MODE 1
   double* st_b = st_s + entries + kStatePad;                                         // MODE 3
   const bool ring_state = mask != ~0u;
+  // state slot of row j: j mod R on a ring of R = entries slots (R is only a
+  // multiple of 32 sized to the widest tile, not a power of two): one modulo
+  // per block and role; offsets below R from a block's base wrap once
+  auto slot = [&](int j) { return ring_state ? j % entries : j; };
+  auto wrap = [&](int e) { return (ring_state && e >= entries) ? e - entries : e; };
   int* nxt = next_buf + it.next_off;
 
   // ---- prologue
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     }
     mbar_fence_init();
     // state[n] = {0.0, 0} (microbatch.cpp:174), and its ring mirror
-    for (int e = (int)(n & mask); ; e += entries) {
+    for (int e = slot(n); ; e += entries) {
       st_s[e] = 0.0;
       if (CAND) st_c[e] = 0; else if (MODE == 1) st_m[e] = -INF;
       if (BSUM) st_b[e] = 0.0;
@@ -356,6 +361,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     // partials.  A few hundred cycles instead of a serial 32-column loop on
     // the chain.
     const double* nt = near + (size_t)(b % kNearBufs) * kNearCols * kRB;
+    const int si0 = slot(i0);  // state slot of the block's first row
     if (wid < kWorkers) {
       const int W = blk_W[gb0 + b];
       const int r = lane;
@@ -366,13 +372,14 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       for (int c = nb + wid; c < cnf; c += kWorkers) {
         const double x = nt[c * kRB + r];
         const int j = i0 + c;
-        const double cs = __dadd_rn(x, st_s[j & mask]);
+        const int sj = wrap(si0 + c);  // (c < 64 < R)
+        const double cs = __dadd_rn(x, st_s[sj]);
         if (BSUM) {
-          const double cb = __dadd_rn(x, st_b[j & mask]);
+          const double cb = __dadd_rn(x, st_b[sj]);
           b1 = (cb < b1) ? cb : b1;
         }
         if (CAND) {
-          const int cn = 1 + st_c[j & mask];
+          const int cn = 1 + st_c[sj];
           const bool upd = (x <= t) & ((cs < s1) | ((cs == s1) & (cn < c1)));
           s1 = upd ? cs : s1;
           c1 = upd ? cn : c1;
@@ -380,7 +387,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         } else {
           // (NaN / +inf entries never pass the compares: see the far-far loop)
           s1 = (cs < s1) ? cs : s1;
-          const double mj = MODE == 1 ? st_m[j & mask] : 0.0;
+          const double mj = MODE == 1 ? st_m[sj] : 0.0;
           const double v = (x < mj) ? mj : x;
           if (MODE == 1) m1 = (v < m1) ? v : m1;
         }
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       if (r < nb) {
         const int row = i0 + r;
         const bool f = isfinite(as);
-        const int e = (int)(row & mask);
+        const int e = wrap(si0 + r);
         const int em = (ring_state && e < kStatePad) ? e + entries : e;  // the ring mirror
         const double sv = (SANITIZE && !f) ? INF : as;
         st_s[e] = sv;
@@ -551,6 +558,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         const int k0 = max(0, j1 - kRB);  // i0 of block b+1
         const int Wn = blk_W[gb0 + bn];
         const int nc = far_nc(gb0 + bn, Wn);
+        const int sk0 = slot(k0);  // state slot of block b+1's first row
         double as = INF, am = INF, as2 = INF, am2 = INF, ab = INF, ab2 = INF;
         int ac = 0, aj = INT_MAX, ac2 = 0, aj2 = INT_MAX;
         const int r = lane;
@@ -561,7 +569,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           const int c0 = kNearCols + k * kChunkCols;
           const int cols = min(kChunkCols, Wn - c0);
           // the chunk's states: slots jb .. jb + 31 (ring mirror / slack: no wrap)
-          const int jb = (int)((k0 + c0) & mask) + w;
+          const int jb = wrap(sk0 + c0) + w;  // (c0 < W <= R - 63)
           const double* ss = st_s + jb;
           const int* sc = st_c + jb;
           const double* sm = st_m + jb;
