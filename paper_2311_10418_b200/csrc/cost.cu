@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(32 * kCostWarps)
 // column r' + d lies in the run), so the candidate set is the reference's
 // exactly.  The store stream is the kernel's bound rather than FP64 issue.
 template <int LAY, bool COMPACT>
-__global__ void __launch_bounds__(32 * kCostWarps)
+__global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per SM: more stores in flight
     band_run_kernel(CostArgs a) {
   __shared__ double4 s_tt[kBandCells];
   __shared__ double2 s_am[kBandCells];
