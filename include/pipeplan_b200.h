@@ -50,7 +50,9 @@ typedef enum pp_status {
   PP_ERR_INFEASIBLE = 3,       /* InfeasibleError(-1, -1), :320              */
   PP_ERR_CUDA = 4,             /* device error (distinct from domain errors) */
   PP_ERR_NO_DEVICE = 5,        /* no CUDA device: the product never falls back to CPU */
-  PP_ERR_OUT_OF_RANGE = 6      /* std::out_of_range (cost_model.cpp:297-298) */
+  PP_ERR_OUT_OF_RANGE = 6,     /* std::out_of_range (cost_model.cpp:297-298) */
+  PP_ERR_NOT_CONVERGED = 7,    /* std::logic_error, schedule.cpp:81-82        */
+  PP_ERR_NOT_EXECUTABLE = 8    /* std::logic_error, schedule.cpp:155-156      */
 } pp_status;
 
 /* Same layout as pipeplan::Sample (include/pipeplan/workload.h:27-33). */
@@ -235,6 +237,40 @@ int pp_plan_op_costs_device(pp_ctx* ctx, const pp_sample* d_ordered, const int64
                             const int32_t* d_count, const pp_grid_desc* grid,
                             const pp_model_desc* model, int64_t capacity, int64_t* mb_offset,
                             double* d_t_f, double* d_t_b, double* d_act_mem);
+
+/* Injection-order search of the per-replica planner:
+ * order_microbatches(predicted, costs, limits, n_clusters, evaluator)
+ * (src/schedule.cpp:277-317, include/pipeplan/schedule.h:101-108) with the
+ * evaluator plan_iteration passes (src/planner.cpp:94-105): the makespan of
+ * simulate(plan_communication(schedule_adaptive(costs, limits, order)),
+ * costs, {noise_sigma 0, comm_latency}) (schedule.cpp:55-122,
+ * comm_plan.cpp:115-233, simulate.cpp:78-213).  Batched over n_seg
+ * independent op-cost tables (mini-batches / replicas): table s holds rows
+ * [mb_offset[s], mb_offset[s+1]) of t_f / t_b / act_mem, [row * n_stages +
+ * stage] (OpCostTable layout, cost_model.h:148-171; pp_op_costs output);
+ * predicted times are OpCostTable::scalar_time (cost_model.cpp:344-348).
+ * Outputs per table: order (n_s entries at mb_offset[s], the chosen
+ * injection order; all -1 when no order is selectable, where the reference
+ * returns an empty vector), makespan, bubble_ratio and deadlock of the chosen
+ * order's SimReport (simulate.cpp:186-197), device_stats (optional,
+ * [s][stage][5] = busy, idle, blocked, peak_mem, final_mem: DeviceStats,
+ * simulate.h:30-36), status (PP_ERR_INVALID: no micro-batch or a negative /
+ * NaN duration; PP_ERR_NOT_CONVERGED / PP_ERR_NOT_EXECUTABLE: the
+ * reference's logic_errors).  Device limits: n_stages <= 32, n_clusters <= 8.
+ * Host buffers. */
+int pp_order_search(pp_ctx* ctx, const double* t_f, const double* t_b, const double* act_mem,
+                    const int64_t* mb_offset, int32_t n_seg, int32_t n_stages, const double* limits,
+                    int32_t n_clusters, double comm_latency, int32_t* order, double* makespan,
+                    double* bubble_ratio, int32_t* deadlock, double* device_stats, int32_t* status);
+
+/* The same on device-resident tables (e.g. pp_plan_op_costs_device output)
+ * on the ctx stream: d_* are device pointers, h_mb_offset / limits host. */
+int pp_order_search_device(pp_ctx* ctx, const double* d_t_f, const double* d_t_b,
+                           const double* d_act_mem, const int64_t* d_mb_offset,
+                           const int64_t* h_mb_offset, int32_t n_seg, int32_t n_stages,
+                           const double* limits, int32_t n_clusters, double comm_latency,
+                           int32_t* d_order, double* d_makespan, double* d_bubble_ratio,
+                           int32_t* d_deadlock, double* d_device_stats, int32_t* d_status);
 
 /* Diagnostics: measured FP64 add issue rate of `device` (adds/s), the
  * roofline denominator of the FP64-bound cost kernels (calib.cu). */

@@ -210,6 +210,8 @@ class Reference:
                                      C.POINTER(_Opts), i32, vp, vp, vp, vp]
         L.ref_plan_batch.restype = dbl
         L.ref_op_costs.argtypes = [vp, i64, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), vp, vp, vp]
+        L.ref_order_search.argtypes = [vp, vp, vp, vp, i32, i32, vp, i32, dbl, i32, vp, vp, vp, vp, vp, vp]
+        L.ref_order_search.restype = dbl
         self.L = L
 
     def order_samples(self, samples):
@@ -237,6 +239,25 @@ class Reference:
         if rc != PP_OK:
             raise ValueError(f"reference from_shapes failed: {rc}")
         return tf, tb, act
+
+    def order_search(self, t_f, t_b, act_mem, mb_offset, limits, n_clusters=3, comm_latency=0.0,
+                     threads=1):
+        """The reference's order_microbatches + the chosen order's SimReport
+        (planner.cpp:94-108) per table; returns (wall seconds, dict)."""
+        tf = np.ascontiguousarray(t_f, np.float64)
+        tb = np.ascontiguousarray(t_b, np.float64)
+        ac = np.ascontiguousarray(act_mem, np.float64)
+        off = np.ascontiguousarray(mb_offset, np.int64)
+        lim = np.ascontiguousarray(limits, np.float64)
+        S, C_ = len(off) - 1, tf.shape[1]
+        out = {"order": np.full(len(tf), -1, np.int32), "makespan": np.zeros(S), "bubble_ratio": np.zeros(S),
+               "deadlock": np.zeros(S, np.int32), "device_stats": np.zeros((S, C_, 5)),
+               "status": np.zeros(S, np.int32)}
+        secs = self.L.ref_order_search(_p(tf), _p(tb), _p(ac), _p(off), S, C_, _p(lim), n_clusters,
+                                       float(comm_latency), threads, _p(out["order"]), _p(out["makespan"]),
+                                       _p(out["bubble_ratio"]), _p(out["deadlock"]), _p(out["device_stats"]),
+                                       _p(out["status"]))
+        return secs, out
 
     def synthetic_grid_cells(self, params7, tp, mbs_axis=(), seq_axis=()):
         par = np.asarray(params7, np.float64)

@@ -20,6 +20,9 @@
 #include "pipeplan/errors.h"
 #include "pipeplan/microbatch.h"
 #include "pipeplan/workload.h"
+#include "pipeplan/comm_plan.h"
+#include "pipeplan/schedule.h"
+#include "pipeplan/simulate.h"
 #include "pipeplan_b200.h"
 
 using namespace pipeplan;
@@ -338,6 +341,78 @@ int ref_op_costs(const pp_padded_shape* shapes, int64_t n, const pp_grid_desc* g
   } catch (const std::out_of_range&) {
     return PP_ERR_OUT_OF_RANGE;
   }
+}
+
+
+// order_microbatches with plan_iteration's evaluator (planner.cpp:94-108)
+// over n_seg op-cost tables, then the chosen order's schedule_adaptive ->
+// plan_communication -> simulate report, exactly as plan_iteration builds
+// rep.report.  `threads` std::threads pull tables from an atomic counter
+// (run_plan's pool model).  Returns wall seconds.
+double ref_order_search(const double* t_f, const double* t_b, const double* act, const int64_t* mb_off,
+                        int32_t n_seg, int32_t C, const double* limits, int32_t k, double comm_latency,
+                        int32_t threads, int32_t* order, double* makespan, double* bubble,
+                        int32_t* deadlock, double* dev_stats, int32_t* status) {
+  std::vector<double> lim(limits, limits + C);
+  std::atomic<int> next{0};
+  auto t0 = std::chrono::steady_clock::now();
+  auto work = [&]() {
+    for (;;) {
+      const int s = next.fetch_add(1);
+      if (s >= n_seg) return;
+      const int64_t b = mb_off[s], M = mb_off[s + 1] - b;
+      try {
+        OpCostTable costs;
+        costs.micro_batches = static_cast<int>(M);
+        costs.stages = C;
+        costs.t_f.assign(t_f + b * C, t_f + (b + M) * C);
+        costs.t_b.assign(t_b + b * C, t_b + (b + M) * C);
+        costs.act_mem.assign(act + b * C, act + (b + M) * C);
+        PlanMeta meta;
+        meta.shape_table.assign(static_cast<std::size_t>(M), MbShapeEntry{1, 1, 0});
+        SimConfig zero_noise;
+        zero_noise.comm_latency = comm_latency;
+        std::vector<double> predicted(static_cast<std::size_t>(M));
+        for (int i = 0; i < M; ++i) predicted[static_cast<std::size_t>(i)] = costs.scalar_time(i);
+        auto evaluator = [&](const PipelineSchedule& sched) {
+          ExecutionPlan candidate = plan_communication(sched, costs, meta);
+          return simulate(candidate, costs, zero_noise).makespan;
+        };
+        std::vector<int> best = order_microbatches(predicted, costs, lim, k, evaluator);
+        status[s] = PP_OK;
+        if (best.empty()) {
+          for (int64_t i = 0; i < M; ++i) order[b + i] = -1;
+          makespan[s] = std::nan("");
+          continue;
+        }
+        for (int64_t i = 0; i < M; ++i) order[b + i] = best[static_cast<std::size_t>(i)];
+        PipelineSchedule sched = schedule_adaptive(costs, lim, best);
+        ExecutionPlan plan = plan_communication(sched, costs, meta);
+        SimReport rep = simulate(plan, costs, zero_noise);
+        makespan[s] = rep.makespan;
+        bubble[s] = rep.bubble_ratio;
+        deadlock[s] = rep.deadlock ? 1 : 0;
+        for (int j = 0; j < C; ++j) {
+          const DeviceStats& d = rep.devices[static_cast<std::size_t>(j)];
+          double* o = dev_stats + (static_cast<int64_t>(s) * C + j) * 5;
+          o[0] = d.busy; o[1] = d.idle; o[2] = d.blocked; o[3] = d.peak_mem; o[4] = d.final_mem;
+        }
+      } catch (const std::invalid_argument&) {
+        status[s] = PP_ERR_INVALID;
+      } catch (const std::logic_error& e) {
+        status[s] = std::strstr(e.what(), "converge") ? PP_ERR_NOT_CONVERGED : PP_ERR_NOT_EXECUTABLE;
+      }
+    }
+  };
+  const int nt = threads < 1 ? 1 : threads;
+  if (nt == 1) {
+    work();
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 }  // extern "C"

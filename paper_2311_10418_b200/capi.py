@@ -23,6 +23,7 @@ _LIB_PATH = os.environ.get("PIPEPLAN_B200_LIB") or os.path.join(
 
 PP_OK, PP_ERR_INVALID, PP_ERR_INFEASIBLE_SAMPLE, PP_ERR_INFEASIBLE = 0, 1, 2, 3
 PP_ERR_CUDA, PP_ERR_NO_DEVICE, PP_ERR_OUT_OF_RANGE = 4, 5, 6
+PP_ERR_NOT_CONVERGED, PP_ERR_NOT_EXECUTABLE = 7, 8
 
 # Every symbol include/pipeplan_b200.h declares (checked by the CPU tests).
 EXPORTED = [
@@ -30,7 +31,7 @@ EXPORTED = [
     "pp_ctx_get_stats", "pp_ctx_set_stream", "pp_order_samples", "pp_plan_grid",
     "pp_plan_grid_device", "pp_plan_tables", "pp_candidate_range", "pp_eval_objective",
     "pp_synthetic_grid", "pp_synthetic_dataset", "pp_slice_cost_host", "pp_calibrate_fp64",
-    "pp_op_costs", "pp_plan_op_costs_device",
+    "pp_op_costs", "pp_plan_op_costs_device", "pp_order_search", "pp_order_search_device",
 ]
 
 
@@ -137,6 +138,9 @@ def _load():
     lib.pp_op_costs.argtypes = [vp, vp, i64, C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, vp, vp]
     lib.pp_plan_op_costs_device.argtypes = [vp, vp, vp, vp, i32, vp, vp, C.POINTER(GridDesc),
                                             C.POINTER(ModelDesc), i64, vp, vp, vp, vp]
+    lib.pp_order_search.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, i32, dbl, vp, vp, vp, vp, vp, vp]
+    lib.pp_order_search_device.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, dbl, vp, vp, vp, vp,
+                                           vp, vp]
     return lib
 
 
@@ -456,6 +460,45 @@ class Planner:
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())
         return mb_off
+
+    def order_search(self, t_f, t_b, act_mem, mb_offset, limits, n_clusters: int = 3,
+                     comm_latency: float = 0.0) -> dict:
+        """order_microbatches with the planner's simulate(plan_communication(...))
+        evaluator over every op-cost table [mb_offset[s], mb_offset[s+1]) of the
+        (rows, n_stages) arrays.  Returns a dict of per-table arrays: order
+        (rows), makespan, bubble_ratio, deadlock, device_stats (n_seg, C, 5),
+        status."""
+        tf = np.ascontiguousarray(t_f, np.float64)
+        tb = np.ascontiguousarray(t_b, np.float64)
+        ac = np.ascontiguousarray(act_mem, np.float64)
+        off = np.ascontiguousarray(mb_offset, np.int64)
+        lim = np.ascontiguousarray(limits, np.float64)
+        S, C_ = len(off) - 1, tf.shape[1]
+        out = {"order": np.full(len(tf), -1, np.int32), "makespan": np.zeros(S), "bubble_ratio": np.zeros(S),
+               "deadlock": np.zeros(S, np.int32), "device_stats": np.zeros((S, C_, 5)),
+               "status": np.zeros(S, np.int32)}
+        rc = lib.pp_order_search(self._h, _p(tf), _p(tb), _p(ac), _p(off), S, C_, _p(lim), n_clusters,
+                                 float(comm_latency), _p(out["order"]), _p(out["makespan"]),
+                                 _p(out["bubble_ratio"]), _p(out["deadlock"]), _p(out["device_stats"]),
+                                 _p(out["status"]))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return out
+
+    def order_search_device(self, d_tf, d_tb, d_act, d_mb_offset, h_mb_offset, limits, d_out: dict,
+                            n_clusters: int = 3, comm_latency: float = 0.0) -> None:
+        """Device-resident variant (torch tensors); d_out holds order, makespan,
+        bubble_ratio, deadlock, device_stats (may be None), status."""
+        off = np.ascontiguousarray(h_mb_offset, np.int64)
+        lim = np.ascontiguousarray(limits, np.float64)
+        S, C_ = len(off) - 1, len(lim)
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        rc = lib.pp_order_search_device(
+            self._h, ptr(d_tf), ptr(d_tb), ptr(d_act), ptr(d_mb_offset), _p(off), S, C_, _p(lim), n_clusters,
+            float(comm_latency), ptr(d_out["order"]), ptr(d_out["makespan"]), ptr(d_out.get("bubble_ratio")),
+            ptr(d_out.get("deadlock")), ptr(d_out.get("device_stats")), ptr(d_out["status"]))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
 
     def candidate_range(self, samples, seg_offsets, grid: Grid, model: Model,
                         mem_cap: float = math.inf, presorted: bool = False):

@@ -102,6 +102,16 @@ cudaError_t launch_op_costs(const CostGrid& g, const double* le_st, const double
                             const pp_padded_shape* shapes, int64_t n, double* t_f, double* t_b,
                             double* act, cudaStream_t st);
 size_t dp_coop_parts_bytes(int grid);
+size_t order_search_slot_bytes(int64_t max_m, int C);
+int order_search_warps(int64_t n_items, size_t slot_bytes, size_t budget);
+size_t order_search_item_bytes();
+cudaError_t launch_order_search(const double* tf, const double* tb, const double* act,
+                                const int64_t* mb_off, int n_seg, int C, const double* limits,
+                                int k, int kfact, double comm_latency, int64_t max_m, double* pred,
+                                int* assign, int* cl_idx, int* cl_off, int* cl_k, char* scratch,
+                                size_t slot_bytes, int warps, void* items, double* item_stats,
+                                int* order, double* makespan, double* bubble, int* deadlock,
+                                double* dev_stats, int* status, cudaStream_t st);
 int dp_coop_grid(int device);
 cudaError_t launch_dp_coop(int mode, int sanitize, const WorkItem& it, int grid, const int64_t* seg_off,
                            const int* blk_base, const int* blk_W, const int64_t* tile_off,
@@ -207,6 +217,9 @@ struct pp_ctx {
   PinBuf h_range, h_stats, h_segdp;
   DevBuf small_bm, coop_state, coop_parts, shapes, stage_lay, mb_off, oc_tf, oc_tb, oc_act, cmin, dp_cols,
       colbase, chunk_nv, perm;
+  // injection-order search (sched.cu)
+  DevBuf os_tf, os_tb, os_act, os_off, os_lim, os_pred, os_assign, os_idx, os_cloff, os_clk, os_scratch,
+      os_items, os_istats, os_order, os_ms, os_bub, os_dl, os_ds, os_status;
   // host copy of the uploaded grid (restricted to the recompute strategy)
   // for the monotonicity certificate of cost pass A
   std::vector<double> h_ax, h_cells;
@@ -237,6 +250,8 @@ struct pp_ctx {
             &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
             &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act,
             &cmin, &dp_cols, &colbase, &chunk_nv, &perm,
+            &os_tf, &os_tb, &os_act, &os_off, &os_lim, &os_pred, &os_assign, &os_idx, &os_cloff, &os_clk,
+            &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status,
             &hset[0].samples, &hset[0].seg, &hset[0].ordered, &hset[0].order, &hset[0].splits,
             &hset[0].times, &hset[0].count, &hset[0].tmax, &hset[0].obj, &hset[0].status, &hset[0].err,
             &hset[1].samples, &hset[1].seg, &hset[1].ordered, &hset[1].order, &hset[1].splits,
@@ -1939,6 +1954,140 @@ int pp_plan_op_costs_device(pp_ctx* ctx, const pp_sample* d_ordered, const int64
                           ctx->shapes.as<pp_padded_shape>(), n_mb, d_t_f, d_t_b, d_act_mem, st));
   PP_CUDA(cudaStreamSynchronize(st));  // lay and the offsets die here
   return PP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Shared body of pp_order_search{,_device}: every pointer is device memory
+// except h_off and limits.
+int order_search_run(pp_ctx* ctx, const double* d_tf, const double* d_tb, const double* d_act,
+                     const int64_t* d_off, const int64_t* h_off, int32_t n_seg, int32_t C,
+                     const double* limits, int32_t k, double comm_latency, int32_t* d_order,
+                     double* d_ms, double* d_bub, int32_t* d_dl, double* d_ds, int32_t* d_status) {
+  cudaStream_t st = ctx->stream;
+  int64_t max_m = 1;
+  std::vector<int32_t> stat(n_seg, PP_OK);
+  for (int s = 0; s < n_seg; ++s) {
+    const int64_t m = h_off[s + 1] - h_off[s];
+    if (m < 1) stat[s] = PP_ERR_INVALID;  // "need at least one micro-batch" (schedule.cpp:281)
+    if (m >= (int64_t)1 << 26) return fail(ctx, PP_ERR_INVALID, "micro-batch count too large");
+    max_m = std::max(max_m, m);
+  }
+  int kfact = 1;
+  for (int q = 2; q <= k; ++q) kfact *= q;
+  const int64_t n_mb = h_off[n_seg] - h_off[0];
+  const int64_t n_items = (int64_t)n_seg * kfact;
+  const size_t slot = order_search_slot_bytes(max_m, C);
+  // scratch budget: a quarter of the free memory, at most 8 GB
+  size_t free_b = 0, total_b = 0;
+  PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t budget = std::min<size_t>(free_b / 4, (size_t)8 << 30);
+  const int warps = order_search_warps(n_items, slot, budget);
+  PP_CUDA(ctx->os_lim.ensure(C * sizeof(double)));
+  PP_CUDA(ctx->os_pred.ensure(std::max<int64_t>(n_mb + h_off[0], 1) * sizeof(double)));
+  PP_CUDA(ctx->os_assign.ensure(std::max<int64_t>(n_mb + h_off[0], 1) * sizeof(int)));
+  PP_CUDA(ctx->os_idx.ensure(std::max<int64_t>(n_mb + h_off[0], 1) * sizeof(int)));
+  PP_CUDA(ctx->os_cloff.ensure((size_t)n_seg * (k + 1) * sizeof(int)));
+  PP_CUDA(ctx->os_clk.ensure(n_seg * sizeof(int)));
+  PP_CUDA(ctx->os_scratch.ensure((size_t)warps * slot));
+  PP_CUDA(ctx->os_items.ensure(n_items * order_search_item_bytes()));
+  PP_CUDA(ctx->os_istats.ensure(n_items * 5 * C * sizeof(double)));
+  PP_CUDA(cudaMemcpyAsync(ctx->os_lim.p, limits, C * sizeof(double), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(d_status, stat.data(), n_seg * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  // tables with no micro-batch are skipped by the kernels (cl_k = 0)
+  PP_CUDA(ctx->os_off.ensure((n_seg + 1) * sizeof(int64_t)));
+  PP_CUDA(cudaMemcpyAsync(ctx->os_off.p, d_off, (n_seg + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  PP_CUDA(launch_order_search(d_tf, d_tb, d_act, ctx->os_off.as<int64_t>(), n_seg, C, ctx->os_lim.as<double>(), k,
+                              kfact, comm_latency, max_m, ctx->os_pred.as<double>(), ctx->os_assign.as<int>(),
+                              ctx->os_idx.as<int>(), ctx->os_cloff.as<int>(), ctx->os_clk.as<int>(),
+                              ctx->os_scratch.as<char>(), slot, warps, ctx->os_items.p,
+                              d_ds ? ctx->os_istats.as<double>() : nullptr, d_order, d_ms, d_bub, d_dl, d_ds,
+                              d_status, st));
+  PP_CUDA(cudaStreamSynchronize(st));  // stat / limits die here
+  return PP_OK;
+}
+
+int order_search_check(pp_ctx* ctx, const int64_t* h_off, int32_t n_seg, int32_t C, const double* limits,
+                       int32_t k) {
+  if (n_seg < 0 || (n_seg > 0 && (!h_off || !limits))) return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  if (C < 1 || C > 32) return fail(ctx, PP_ERR_INVALID, "the device order search supports 1..32 stages");
+  if (k < 1) return fail(ctx, PP_ERR_INVALID, "n_clusters must be >= 1");  // schedule.cpp:284
+  if (k > 8) return fail(ctx, PP_ERR_INVALID, "the device order search supports n_clusters <= 8");
+  for (int s = 0; s < n_seg; ++s)
+    if (h_off[s + 1] < h_off[s]) return fail(ctx, PP_ERR_INVALID, "mb_offset must be non-decreasing");
+  return PP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pp_order_search(pp_ctx* ctx, const double* t_f, const double* t_b, const double* act_mem,
+                    const int64_t* mb_offset, int32_t n_seg, int32_t n_stages, const double* limits,
+                    int32_t n_clusters, double comm_latency, int32_t* order, double* makespan,
+                    double* bubble_ratio, int32_t* deadlock, double* device_stats, int32_t* status) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = order_search_check(ctx, mb_offset, n_seg, n_stages, limits, n_clusters))) return rc;
+  if (n_seg == 0) return PP_OK;
+  if (!t_f || !t_b || !act_mem || !order || !makespan || !status) return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  const int C = n_stages;
+  const int64_t o0 = mb_offset[0], n_mb = mb_offset[n_seg] - o0;
+  std::vector<int64_t> off(n_seg + 1);
+  for (int s = 0; s <= n_seg; ++s) off[s] = mb_offset[s] - o0;
+  cudaStream_t st = ctx->stream;
+  const size_t tb_bytes = std::max<int64_t>(n_mb, 1) * C * sizeof(double);
+  PP_CUDA(ctx->os_tf.ensure(tb_bytes));
+  PP_CUDA(ctx->os_tb.ensure(tb_bytes));
+  PP_CUDA(ctx->os_act.ensure(tb_bytes));
+  PP_CUDA(ctx->mb_off.ensure((n_seg + 1) * sizeof(int64_t)));
+  PP_CUDA(ctx->os_order.ensure(std::max<int64_t>(n_mb, 1) * sizeof(int32_t)));
+  PP_CUDA(ctx->os_ms.ensure(n_seg * sizeof(double)));
+  PP_CUDA(ctx->os_bub.ensure(n_seg * sizeof(double)));
+  PP_CUDA(ctx->os_dl.ensure(n_seg * sizeof(int32_t)));
+  PP_CUDA(ctx->os_ds.ensure((size_t)n_seg * 5 * C * sizeof(double)));
+  PP_CUDA(ctx->os_status.ensure(n_seg * sizeof(int32_t)));
+  PP_CUDA(cudaMemcpyAsync(ctx->os_tf.p, t_f + o0 * C, n_mb * C * sizeof(double), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->os_tb.p, t_b + o0 * C, n_mb * C * sizeof(double), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->os_act.p, act_mem + o0 * C, n_mb * C * sizeof(double), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->mb_off.p, off.data(), (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if ((rc = order_search_run(ctx, ctx->os_tf.as<double>(), ctx->os_tb.as<double>(), ctx->os_act.as<double>(),
+                             ctx->mb_off.as<int64_t>(), off.data(), n_seg, C, limits, n_clusters, comm_latency,
+                             ctx->os_order.as<int32_t>(), ctx->os_ms.as<double>(), ctx->os_bub.as<double>(),
+                             ctx->os_dl.as<int32_t>(), device_stats ? ctx->os_ds.as<double>() : nullptr,
+                             ctx->os_status.as<int32_t>())))
+    return rc;
+  PP_CUDA(cudaMemcpyAsync(order + o0, ctx->os_order.p, n_mb * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaMemcpyAsync(makespan, ctx->os_ms.p, n_seg * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (bubble_ratio)
+    PP_CUDA(cudaMemcpyAsync(bubble_ratio, ctx->os_bub.p, n_seg * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (deadlock)
+    PP_CUDA(cudaMemcpyAsync(deadlock, ctx->os_dl.p, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (device_stats)
+    PP_CUDA(cudaMemcpyAsync(device_stats, ctx->os_ds.p, (size_t)n_seg * 5 * C * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaMemcpyAsync(status, ctx->os_status.p, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaStreamSynchronize(st));
+  return PP_OK;
+}
+
+int pp_order_search_device(pp_ctx* ctx, const double* d_t_f, const double* d_t_b,
+                           const double* d_act_mem, const int64_t* d_mb_offset,
+                           const int64_t* h_mb_offset, int32_t n_seg, int32_t n_stages,
+                           const double* limits, int32_t n_clusters, double comm_latency,
+                           int32_t* d_order, double* d_makespan, double* d_bubble_ratio,
+                           int32_t* d_deadlock, double* d_device_stats, int32_t* d_status) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = order_search_check(ctx, h_mb_offset, n_seg, n_stages, limits, n_clusters))) return rc;
+  if (n_seg == 0) return PP_OK;
+  if (!d_t_f || !d_t_b || !d_act_mem || !d_mb_offset || !d_order || !d_makespan || !d_status)
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  return order_search_run(ctx, d_t_f, d_t_b, d_act_mem, d_mb_offset, h_mb_offset, n_seg, n_stages, limits,
+                          n_clusters, comm_latency, d_order, d_makespan, d_bubble_ratio, d_deadlock,
+                          d_device_stats, d_status);
 }
 
 }  // extern "C"
