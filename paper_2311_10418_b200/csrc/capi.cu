@@ -103,7 +103,7 @@ cudaError_t launch_op_costs(const CostGrid& g, const double* le_st, const double
                             double* act, cudaStream_t st);
 size_t dp_coop_parts_bytes(int grid);
 size_t order_search_slot_bytes(int64_t max_m, int C);
-int order_search_warps(int64_t n_items, size_t slot_bytes, size_t budget);
+int order_search_warps(int64_t n_items, int C, size_t slot_bytes, size_t budget);
 size_t order_search_item_bytes();
 cudaError_t launch_order_search(const double* tf, const double* tb, const double* act,
                                 const int64_t* mb_off, int n_seg, int C, const double* limits,
@@ -1980,18 +1980,21 @@ int order_search_run(pp_ctx* ctx, const double* d_tf, const double* d_tb, const 
   const int64_t n_mb = h_off[n_seg] - h_off[0];
   const int64_t n_items = (int64_t)n_seg * kfact;
   const size_t slot = order_search_slot_bytes(max_m, C);
-  // scratch budget: a quarter of the free memory, at most 8 GB
+  // scratch budget: half the free memory, at most 32 GB (one slot per
+  // resident (mini-batch, permutation) evaluation; L2-resident when small)
   size_t free_b = 0, total_b = 0;
   PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const size_t budget = std::min<size_t>(free_b / 4, (size_t)8 << 30);
-  const int warps = order_search_warps(n_items, slot, budget);
+  const size_t budget = std::min<size_t>(free_b / 2, (size_t)32 << 30);
+  const int warps = order_search_warps(n_items, C, slot, budget);
+  int G = 1;
+  while (G < C) G *= 2;
   PP_CUDA(ctx->os_lim.ensure(C * sizeof(double)));
   PP_CUDA(ctx->os_pred.ensure(std::max<int64_t>(n_mb + h_off[0], 1) * sizeof(double)));
   PP_CUDA(ctx->os_assign.ensure(std::max<int64_t>(n_mb + h_off[0], 1) * sizeof(int)));
   PP_CUDA(ctx->os_idx.ensure(std::max<int64_t>(n_mb + h_off[0], 1) * sizeof(int)));
   PP_CUDA(ctx->os_cloff.ensure((size_t)n_seg * (k + 1) * sizeof(int)));
   PP_CUDA(ctx->os_clk.ensure(n_seg * sizeof(int)));
-  PP_CUDA(ctx->os_scratch.ensure((size_t)warps * slot));
+  PP_CUDA(ctx->os_scratch.ensure((size_t)warps * (32 / G) * slot));
   PP_CUDA(ctx->os_items.ensure(n_items * order_search_item_bytes()));
   PP_CUDA(ctx->os_istats.ensure(n_items * 5 * C * sizeof(double)));
   PP_CUDA(cudaMemcpyAsync(ctx->os_lim.p, limits, C * sizeof(double), cudaMemcpyHostToDevice, st));

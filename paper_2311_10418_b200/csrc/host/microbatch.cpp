@@ -20,10 +20,11 @@
 #include "pipeplan_b200.h"
 
 namespace pipeplan {
-namespace {
+namespace detail {
 
 // One device context per host thread: the reference planner is called
-// concurrently from run_plan's workers (driver.cpp:222-242).
+// concurrently from run_plan's workers (driver.cpp:222-242).  Shared with
+// order_search.cpp.
 pp_ctx* device_ctx() {
   struct Holder {
     pp_ctx* ctx = nullptr;
@@ -43,6 +44,10 @@ pp_ctx* device_ctx() {
   }
   return h.ctx;
 }
+
+}  // namespace detail
+namespace {
+using detail::device_ctx;
 
 [[noreturn]] void raise(pp_ctx* ctx, int rc, std::int64_t sample_id) {
   switch (rc) {

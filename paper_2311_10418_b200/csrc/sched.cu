@@ -55,10 +55,6 @@ enum : int {
   kRecvGradStart = 5, kWaitSendAct = 6, kWaitRecvAct = 7, kWaitSendGrad = 8, kWaitRecvGrad = 9
 };
 
-__device__ __forceinline__ double vld(const double* p) { return *(const volatile double*)p; }
-__device__ __forceinline__ void vst(double* p, double v) { *(volatile double*)p = v; }
-__device__ __forceinline__ int vldi(const int* p) { return *(const volatile int*)p; }
-
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000LL); }
 
 }  // namespace
@@ -278,100 +274,127 @@ struct ItemOut {
   int32_t pad;
 };
 
+// Lanes are packed in groups of G = next power of two >= C: 32 / G
+// (mini-batch, permutation) items per warp, lane j of a group = device j.
+// Loop exits are warp-wide (every group steps until all groups are done);
+// per-group conditions (convergence, no progress) use ballots masked to the
+// group.  Cross-lane data goes through global scratch written and read with
+// CTA-scope relaxed accesses (coherent in the SM's L1: every lane of a group
+// is in the same CTA), ordered by __syncwarp between rounds.
+__device__ __forceinline__ double ld_cta(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.cta.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cta(double* p, double v) {
+  asm volatile("st.relaxed.cta.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(128) perm_eval_kernel(
     const double* __restrict__ tf, const double* __restrict__ tb, const double* __restrict__ act,
-    const int64_t* __restrict__ mb_off, const double* __restrict__ limits, int C, int k, int kfact,
+    const int64_t* __restrict__ mb_off, const double* __restrict__ limits, int C, int G, int k, int kfact,
     double comm_latency, int n_seg, const int* __restrict__ cl_idx, const int* __restrict__ cl_off,
     const int* __restrict__ cl_k, char* __restrict__ scratch, size_t slot_bytes, int64_t Mcap,
     ItemOut* __restrict__ items, double* __restrict__ dev_stats) {
   __shared__ int sqn_s[4][64], rqn_s[4][64];
-  __shared__ int perm_s[4][16];
+  __shared__ int perm_s[4][32][8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int IPW = 32 / G;                 // items per warp
+  const int grp = lane / G, j = lane % G;  // item slot in the warp, device
+  const unsigned gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (grp * G);
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  SchedSlot S = carve(scratch + gw * slot_bytes, Mcap, C);
-  int* sqn = sqn_s[wib];
-  int* rqn = rqn_s[wib];
-  const int j = lane;
-  const bool active = j < C;
+  SchedSlot S = carve(scratch + (gw * IPW + grp) * slot_bytes, Mcap, C);
+  int* sqn = sqn_s[wib] + grp * 2 * G;
+  int* rqn = rqn_s[wib] + grp * 2 * G;
+  int* perm = perm_s[wib][grp];
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
-  const double lim = active ? limits[j] : 0.0;
+  const double lim = j < C ? limits[j] : 0.0;
+  const int64_t n_items = (int64_t)n_seg * kfact;
 
-  for (int64_t item = gw; item < (int64_t)n_seg * kfact; item += nw) {
-    const int s = (int)(item / kfact);
-    const int r = (int)(item - (int64_t)s * kfact);
-    const int kk = cl_k[s];
-    int kkf = 1;
-    for (int q = 2; q <= kk; ++q) kkf *= q;
-    if (kk == 0 || r >= kkf) continue;  // (kk == 0: bad input, status set by cluster_kernel)
-    const int64_t base = mb_off[s];
-    const int M = (int)(mb_off[s + 1] - base);
+  for (int64_t ib = gw * IPW; ib < n_items; ib += nw * IPW) {
+    const int64_t item = ib + grp;
+    int s = 0, r = 0, kk = 0, kkf = 0;
+    if (item < n_items) {
+      s = (int)(item / kfact);
+      r = (int)(item - (int64_t)s * kfact);
+      kk = cl_k[s];
+      kkf = 1;
+      for (int q = 2; q <= kk; ++q) kkf *= q;
+    }
+    // (kk == 0: no micro-batch or bad input, status set by cluster_kernel)
+    const bool valid = item < n_items && kk > 0 && r < kkf;
+    const bool active = valid && j < C;
+    const int64_t base = valid ? mb_off[s] : 0;
+    const int M = valid ? (int)(mb_off[s + 1] - base) : 0;
     const int M2 = 2 * M;
     const double* TF = tf + base * C;
     const double* TB = tb + base * C;
     const double* AC = act + base * C;
-    const int* idx = cl_idx + base;
-    const int* off = cl_off + (int64_t)s * (k + 1);
 
     // injection order = clusters concatenated in permutation order, written
     // straight into device 0's forward queue
-    if (lane == 0) nth_perm(r, kk, perm_s[wib]);
+    if (valid && j == 0) nth_perm(r, kk, perm);
     __syncwarp();
-    {
+    bool ident = true;
+    if (valid) {
+      const int* idx = cl_idx + base;
+      const int* off = cl_off + (int64_t)s * (k + 1);
       int pos = 0;
-      bool ident = true;
       for (int q = 0; q < kk; ++q) {
-        const int c = perm_s[wib][q];
+        const int c = perm[q];
         const int a = off[c], n = off[c + 1] - off[c];
-        for (int t = lane; t < n; t += 32) {
+        for (int t = j; t < n; t += G) {
           const int mb = idx[a + t];
           S.fq[pos + t] = mb;
           ident &= (mb == pos + t);
         }
         pos += n;
       }
-      ident = __all_sync(kFull, ident);
-      if (lane == 0) items[item].flags = ident ? 1 : 0;
     }
+    ident = (__ballot_sync(kFull, !ident) & gmask) == 0;
     __syncwarp();
-    int err = 0;
+    int err = 0;  // group-uniform
 
     // ---- phase 1: schedule_adaptive (schedule.cpp:55-122) ----
-    int n_ord = 0;
     {
-      int fh = 0, ft = (j == 0) ? M : 0, bh = 0, bt = 0;
+      int n_ord = 0, fh = 0, ft = (j == 0) ? M : 0, bh = 0, bt = 0;
       double mem = 0.0;
       int* FQ = S.fq + (int64_t)j * M;
       int* BQ = S.bq + (int64_t)j * M;
       int* ORD = S.ord + (int64_t)j * M2;
       const long long cap = 4LL * M * C;
       long long cycle = 0;
+      bool gdone = !valid;
       while (true) {
-        if (__all_sync(kFull, !active || n_ord == M2)) break;
-        if (cycle > cap) { err = 3; break; }  // logic_error: failed to converge
-        ++cycle;
+        if (!gdone) gdone = (__ballot_sync(gmask, active && n_ord != M2) & gmask) == 0;
+        if (__all_sync(kFull, gdone)) break;
+        if (!gdone && cycle > cap) { err = 3; gdone = true; }  // logic_error: failed to converge
         int fo = -1, bo = -1, selfb = -1;
-        if (active) {
-          if (bh < bt) {
-            const int i = BQ[bh++];
-            mem = __dsub_rn(mem, AC[(int64_t)i * C + j]);
-            ORD[n_ord++] = 2 * i + 1;
-            if (j > 0) bo = i;
-          }
-          if (fh < ft) {
-            const int i = FQ[fh];
-            const double a = AC[(int64_t)i * C + j];
-            if (__dadd_rn(mem, a) < lim) {
-              ++fh;
-              mem = __dadd_rn(mem, a);
-              ORD[n_ord++] = 2 * i;
-              if (j + 1 < C) fo = i; else selfb = i;
+        if (!gdone) {
+          ++cycle;
+          if (active) {
+            if (bh < bt) {
+              const int i = BQ[bh++];
+              mem = __dsub_rn(mem, AC[(int64_t)i * C + j]);
+              ORD[n_ord++] = 2 * i + 1;
+              if (j > 0) bo = i;
+            }
+            if (fh < ft) {
+              const int i = FQ[fh];
+              const double a = AC[(int64_t)i * C + j];
+              if (__dadd_rn(mem, a) < lim) {
+                ++fh;
+                mem = __dadd_rn(mem, a);
+                ORD[n_ord++] = 2 * i;
+                if (j + 1 < C) fo = i; else selfb = i;
+              }
             }
           }
         }
-        const int in_f = __shfl_up_sync(kFull, fo, 1);
-        const int in_b = __shfl_down_sync(kFull, bo, 1);
-        if (active) {
+        const int in_f = __shfl_up_sync(kFull, fo, 1, G);
+        const int in_b = __shfl_down_sync(kFull, bo, 1, G);
+        if (active && !gdone) {
           if (j > 0 && in_f >= 0) FQ[ft++] = in_f;
           const int nb = (j == C - 1) ? selfb : in_b;
           if (nb >= 0) BQ[bt++] = nb;
@@ -381,37 +404,42 @@ __global__ void __launch_bounds__(128) perm_eval_kernel(
     __syncwarp();
 
     // ---- phase 2: replay_schedule (schedule.cpp:124-183) ----
-    if (!err) {
-      for (int64_t q = lane; q < (int64_t)M * C; q += 32) { S.fend[q] = qnan(); S.bend[q] = qnan(); }
+    {
+      if (valid && !err)
+        for (int64_t q = j; q < (int64_t)M * C; q += G) { S.fend[q] = qnan(); S.bend[q] = qnan(); }
       __syncwarp();
       int p = 0;
       double dev_free = 0.0;
       const int* ORD = S.ord + (int64_t)j * M2;
       double* ST = S.st + (int64_t)j * M2;
       double* EN = S.en + (int64_t)j * M2;
+      bool gdone = !valid || err;
       while (true) {
         bool prog = false;
-        if (active)
+        if (active && !gdone)
           while (p < M2) {
             const int o = ORD[p];
             const int mb = o >> 1;
             const bool bwd = o & 1;
             double ready;
-            if (!bwd) ready = j == 0 ? -INF : vld(S.fend + (int64_t)mb * C + j - 1);
-            else ready = j == C - 1 ? vld(S.fend + (int64_t)mb * C + j) : vld(S.bend + (int64_t)mb * C + j + 1);
+            if (!bwd) ready = j == 0 ? -INF : ld_cta(S.fend + (int64_t)mb * C + j - 1);
+            else ready = j == C - 1 ? ld_cta(S.fend + (int64_t)mb * C + j) : ld_cta(S.bend + (int64_t)mb * C + j + 1);
             if (ready != ready) break;
             const double start = dev_free < ready ? ready : dev_free;  // std::max(dev_free, ready)
             const double end = __dadd_rn(start, bwd ? TB[(int64_t)mb * C + j] : TF[(int64_t)mb * C + j]);
             ST[p] = start;
             EN[p] = end;
-            vst((bwd ? S.bend : S.fend) + (int64_t)mb * C + j, end);
+            st_cta((bwd ? S.bend : S.fend) + (int64_t)mb * C + j, end);
             dev_free = end;
             ++p;
             prog = true;
           }
         __syncwarp();
-        if (__all_sync(kFull, !active || p == M2)) break;
-        if (!__any_sync(kFull, prog)) { err = 4; break; }  // logic_error: not executable
+        const unsigned pend = __ballot_sync(kFull, active && !gdone && p != M2) & gmask;
+        const unsigned anyp = __ballot_sync(kFull, prog) & gmask;
+        if (!gdone && pend == 0) gdone = true;
+        if (!gdone && anyp == 0) { err = 4; gdone = true; }  // logic_error: not executable
+        if (__all_sync(kFull, gdone)) break;
       }
     }
     __syncwarp();
@@ -446,6 +474,8 @@ __global__ void __launch_bounds__(128) perm_eval_kernel(
         return q;
       };
       int po = adv_own(0), pp = adv_prev(0), pn = adv_next(0);
+      // stream heads cached in registers (end time, +inf sentinel via flags)
+      double ep = pp < M2 ? ENP[pp] : 0.0, eo = po < M2 ? EN[po] : 0.0, en_ = pn < M2 ? ENN[pn] : 0.0;
       // lazily placed send Waits: channel 0 = (j+1, SendAct), 1 = (j-1, SendGrad)
       bool pend[2] = {false, false};
       int pend_mb[2] = {0, 0}, stamp[2] = {0, 0}, ctr = 0;
@@ -453,21 +483,28 @@ __global__ void __launch_bounds__(128) perm_eval_kernel(
       // next pending Start in (end, device, op_index) order: 0 prev, 1 own, 2 next, -1 none
       auto head = [&](double& e) {
         int w = -1;
-        if (pp < M2) { w = 0; e = ENP[pp]; }
-        if (po < M2 && (w < 0 || EN[po] < e)) { w = 1; e = EN[po]; }
-        if (pn < M2 && (w < 0 || ENN[pn] < e)) { w = 2; e = ENN[pn]; }
+        if (pp < M2) { w = 0; e = ep; }
+        if (po < M2 && (w < 0 || eo < e)) { w = 1; e = eo; }
+        if (pn < M2 && (w < 0 || en_ < e)) { w = 2; e = en_; }
         return w;
       };
       auto emit_head = [&](int w) {
-        if (w == 0) { emit(kRecvActStart, ORDP[pp] >> 1); pp = adv_prev(pp + 1); }
-        else if (w == 2) { emit(kRecvGradStart, ORDN[pn] >> 1); pn = adv_next(pn + 1); }
-        else {
+        if (w == 0) {
+          emit(kRecvActStart, ORDP[pp] >> 1);
+          pp = adv_prev(pp + 1);
+          if (pp < M2) ep = ENP[pp];
+        } else if (w == 2) {
+          emit(kRecvGradStart, ORDN[pn] >> 1);
+          pn = adv_next(pn + 1);
+          if (pn < M2) en_ = ENN[pn];
+        } else {
           const int o = ORD[po];
           const int ch = (o & 1) ? 1 : 0;
           if (pend[ch]) { emit(ch ? kWaitSendGrad : kWaitSendAct, pend_mb[ch]); pend[ch] = false; }
           emit(ch ? kSendGradStart : kSendActStart, o >> 1);
           pend[ch] = true; pend_mb[ch] = o >> 1; stamp[ch] = ++ctr;
           po = adv_own(po + 1);
+          if (po < M2) eo = EN[po];
         }
       };
       for (int p = 0; p < M2; ++p) {
@@ -499,10 +536,13 @@ __global__ void __launch_bounds__(128) perm_eval_kernel(
     // ---- phase 4: simulate at zero noise (simulate.cpp:78-213) ----
     double clock = 0.0, busy = 0.0, blocked = 0.0, mem = 0.0, peak = 0.0;
     bool deadlock = false;
-    if (!err) {
-      const int nch = 2 * (C - 1);
-      for (int64_t q = lane; q < (int64_t)nch * M; q += 32) S.comp[q] = qnan();
-      for (int q = lane; q < 64; q += 32) { sqn[q] = 0; rqn[q] = 0; }
+    {
+      const bool run = valid && !err;
+      if (run) {
+        const int nch = 2 * (C - 1);
+        for (int64_t q = j; q < (int64_t)nch * M; q += G) S.comp[q] = qnan();
+        for (int q = j; q < 2 * G; q += G) { sqn[q] = 0; rqn[q] = 0; }
+      }
       __syncwarp();
       const int* INS = S.ins + (int64_t)j * 10 * M;
       // queues this lane appends to: send (j, act), send (j-1, grad), recv (j-1, act), recv (j, grad)
@@ -510,22 +550,24 @@ __global__ void __launch_bounds__(128) perm_eval_kernel(
       int matched[2] = {0, 0};
       double free_at[2] = {0.0, 0.0};
       int ip = 0;
+      bool gdone = !run;
       while (true) {
         bool prog = false;
-        if (active)
+        if (active && !gdone)
           while (ip < n_ins) {
             const int w = INS[ip];
             const int kind = w & 15, mb = w >> 4;
             if (kind <= kBwd) {
               const bool fwd = kind == kFwd;
               const double dur = fwd ? TF[(int64_t)mb * C + j] : TB[(int64_t)mb * C + j];
+              const double a = AC[(int64_t)mb * C + j];
               clock = __dadd_rn(clock, dur);
               busy = __dadd_rn(busy, dur);
               if (fwd) {
-                mem = __dadd_rn(mem, AC[(int64_t)mb * C + j]);
+                mem = __dadd_rn(mem, a);
                 peak = peak < mem ? mem : peak;
               } else {
-                mem = __dsub_rn(mem, AC[(int64_t)mb * C + j]);
+                mem = __dsub_rn(mem, a);
               }
             } else if (kind <= kRecvGradStart) {
               int ch, q;
@@ -542,7 +584,7 @@ __global__ void __launch_bounds__(128) perm_eval_kernel(
               else if (kind == kWaitRecvAct) ch = 2 * (j - 1);
               else if (kind == kWaitSendGrad) ch = 2 * (j - 1) + 1;
               else ch = 2 * j + 1;
-              const double c = vld(S.comp + (int64_t)ch * M + mb);
+              const double c = ld_cta(S.comp + (int64_t)ch * M + mb);
               if (c != c) break;  // blocked until the transfer lands
               if (c > clock) {
                 blocked = __dadd_rn(blocked, __dsub_rn(c, clock));
@@ -553,17 +595,17 @@ __global__ void __launch_bounds__(128) perm_eval_kernel(
             prog = true;
           }
         // publish queue lengths, then resolve channels (lane l owns link l)
-        if (active) {
+        if (active && !gdone) {
           if (j + 1 < C) sqn[2 * j] = n_sa;
           if (j > 0) sqn[2 * (j - 1) + 1] = n_sg;
           if (j > 0) rqn[2 * (j - 1)] = n_ra;
           if (j + 1 < C) rqn[2 * j + 1] = n_rg;
         }
         __syncwarp();
-        if (active && j + 1 < C)
+        if (active && !gdone && j + 1 < C)
           for (int a = 0; a < 2; ++a) {
             const int ch = 2 * j + a;
-            const int ns = vldi(sqn + ch), nr = vldi(rqn + ch);
+            const int ns = sqn[ch], nr = rqn[ch];
             while (matched[a] < ns && matched[a] < nr &&
                    S.sq_mb[(int64_t)ch * M + matched[a]] == S.rq_mb[(int64_t)ch * M + matched[a]]) {
               const int mb = S.sq_mb[(int64_t)ch * M + matched[a]];
@@ -572,38 +614,44 @@ __global__ void __launch_bounds__(128) perm_eval_kernel(
               if (st < rt) st = rt;
               if (st < free_at[a]) st = free_at[a];  // std::max({send, recv, free_at})
               const double en = __dadd_rn(st, comm_latency);
-              vst(S.comp + (int64_t)ch * M + mb, en);
+              st_cta(S.comp + (int64_t)ch * M + mb, en);
               free_at[a] = en;
               ++matched[a];
               prog = true;
             }
           }
         __syncwarp();
-        if (__all_sync(kFull, !active || ip == n_ins)) break;
-        if (!__any_sync(kFull, prog)) { deadlock = true; break; }
+        const unsigned pendm = __ballot_sync(kFull, active && !gdone && ip != n_ins) & gmask;
+        const unsigned anyp = __ballot_sync(kFull, prog) & gmask;
+        if (!gdone && pendm == 0) gdone = true;
+        if (!gdone && anyp == 0) { deadlock = true; gdone = true; }
+        if (__all_sync(kFull, gdone)) break;
       }
     }
-    // report (simulate.cpp:186-197): device order j = 0..C-1 on lane 0
+    // report (simulate.cpp:186-197): device order j = 0..C-1 on lane 0 of the group
     double makespan = 0.0, non_busy = 0.0;
     for (int q = 0; q < C; ++q) {
-      const double c = __shfl_sync(kFull, clock, q);
+      const double c = __shfl_sync(kFull, clock, q, G);
       makespan = makespan < c ? c : makespan;
     }
-    double* ds = dev_stats ? dev_stats + item * 5 * C : nullptr;
+    double* ds = (dev_stats && valid) ? dev_stats + item * 5 * C : nullptr;
     for (int q = 0; q < C; ++q) {
-      const double bz = __shfl_sync(kFull, busy, q), bl = __shfl_sync(kFull, blocked, q);
-      const double pk = __shfl_sync(kFull, peak, q), fm = __shfl_sync(kFull, mem, q);
+      const double bz = __shfl_sync(kFull, busy, q, G), bl = __shfl_sync(kFull, blocked, q, G);
+      const double pk = __shfl_sync(kFull, peak, q, G), fm = __shfl_sync(kFull, mem, q, G);
       const double idle = __dsub_rn(__dsub_rn(makespan, bz), bl);
       non_busy = __dadd_rn(non_busy, __dadd_rn(idle, bl));
-      if (ds && lane == 0) {
+      if (ds && j == 0) {
         ds[5 * q + 0] = bz; ds[5 * q + 1] = idle; ds[5 * q + 2] = bl;
         ds[5 * q + 3] = pk; ds[5 * q + 4] = fm;
       }
     }
-    if (lane == 0) {
-      items[item].makespan = makespan;
-      items[item].bubble = makespan > 0 ? __ddiv_rn(non_busy, __dmul_rn((double)C, makespan)) : 0.0;
-      items[item].flags |= (deadlock ? 2 : 0) | (err << 8);
+    if (valid && j == 0) {
+      ItemOut o;
+      o.makespan = makespan;
+      o.bubble = makespan > 0 ? __ddiv_rn(non_busy, __dmul_rn((double)C, makespan)) : 0.0;
+      o.flags = (ident ? 1 : 0) | (deadlock ? 2 : 0) | (err << 8);
+      o.pad = 0;
+      items[item] = o;
     }
     __syncwarp();
   }
@@ -677,9 +725,13 @@ __global__ void order_select_kernel(const int64_t* __restrict__ mb_off, int k, i
 
 size_t order_search_slot_bytes(int64_t max_m, int C) { return sched_slot_bytes(max_m, C); }
 
-int order_search_warps(int64_t n_items, size_t slot_bytes, size_t budget) {
-  int64_t w = std::min<int64_t>(n_items, (int64_t)148 * 64);
-  const int64_t by_mem = std::max<int64_t>(4, (int64_t)(budget / std::max<size_t>(slot_bytes, 1)));
+// warps for the evaluation grid; the scratch holds warps * (32 / G) slots
+int order_search_warps(int64_t n_items, int C, size_t slot_bytes, size_t budget) {
+  int G = 1;
+  while (G < C) G *= 2;
+  const int ipw = 32 / G;
+  int64_t w = std::min<int64_t>((n_items + ipw - 1) / ipw, (int64_t)148 * 64);
+  const int64_t by_mem = std::max<int64_t>(4, (int64_t)(budget / std::max<size_t>(slot_bytes * ipw, 1)));
   w = std::max<int64_t>(std::min(w, by_mem), 1);
   return (int)((w + 3) / 4 * 4);  // whole 4-warp CTAs: every warp owns a slot
 }
@@ -693,8 +745,10 @@ cudaError_t launch_order_search(const double* tf, const double* tb, const double
                                 double* dev_stats, int* status, cudaStream_t st) {
   if (n_seg <= 0) return cudaSuccess;
   cluster_kernel<<<n_seg, 256, 0, st>>>(tf, tb, mb_off, C, k, pred, assign, cl_idx, cl_off, cl_k, status);
+  int G = 1;
+  while (G < C) G *= 2;
   const int blocks = (warps + 3) / 4;
-  perm_eval_kernel<<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, limits, C, k, kfact, comm_latency, n_seg,
+  perm_eval_kernel<<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, limits, C, G, k, kfact, comm_latency, n_seg,
                                            cl_idx, cl_off, cl_k, scratch, slot_bytes, max_m,
                                            (ItemOut*)items, item_stats);
   order_select_kernel<<<n_seg, 128, 0, st>>>(mb_off, k, kfact, C, cl_idx, cl_off, cl_k, (const ItemOut*)items,

@@ -53,3 +53,18 @@ def test_reference_acceptance_suite_on_b200(tmp_path):
     dp_partition through the reference's own callers."""
     r = subprocess.run([ACC], capture_output=True, text=True, timeout=900, cwd=tmp_path)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+
+
+ORD = os.path.join(ROOT, "oracle", "_ref", "order_dropin")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(ORD), reason="order_dropin not built")
+def test_injection_order_search_matches_reference_planner(tmp_path):
+    """tests/cpp/order_dropin.cpp: pipeplan::b200::search_injection_order(s)
+    against the reference's order_microbatches + plan_communication +
+    simulate on random tables, and against the injection orders / reports of
+    the reference's own plan_iteration."""
+    r = subprocess.run([ORD], capture_output=True, text=True, timeout=600, cwd=tmp_path)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert "order dropin: OK" in r.stdout, r.stdout
