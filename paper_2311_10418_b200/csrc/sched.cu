@@ -290,7 +290,7 @@ __device__ __forceinline__ void st_cta(double* p, double v) {
   asm volatile("st.relaxed.cta.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(128) perm_eval_kernel(
+__global__ void __launch_bounds__(128, 6) perm_eval_kernel(
     const double* __restrict__ tf, const double* __restrict__ tb, const double* __restrict__ act,
     const int64_t* __restrict__ mb_off, const double* __restrict__ limits, int C, int G, int k, int kfact,
     double comm_latency, int n_seg, const int* __restrict__ cl_idx, const int* __restrict__ cl_off,
