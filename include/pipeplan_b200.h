@@ -52,8 +52,16 @@ typedef enum pp_status {
   PP_ERR_NO_DEVICE = 5,        /* no CUDA device: the product never falls back to CPU */
   PP_ERR_OUT_OF_RANGE = 6,     /* std::out_of_range (cost_model.cpp:297-298) */
   PP_ERR_NOT_CONVERGED = 7,    /* std::logic_error, schedule.cpp:81-82        */
-  PP_ERR_NOT_EXECUTABLE = 8    /* std::logic_error, schedule.cpp:155-156      */
+  PP_ERR_NOT_EXECUTABLE = 8,   /* std::logic_error, schedule.cpp:155-156      */
+  PP_ERR_PARSE = 9             /* ParseError (errors.h:25-40), workload.cpp:77-98 */
 } pp_status;
+
+/* ParseError kinds of load_record_file (src/workload.cpp:79-97), in the
+ * reference's check order; the messages are the reference's. */
+#define PP_PARSE_MISSING_TAB 0   /* "dataset record missing tab separator"     */
+#define PP_PARSE_NOT_INTEGERS 1  /* "dataset record is not a pair of integers" */
+#define PP_PARSE_INPUT_LT_1 2    /* "dataset record has input_len < 1"         */
+#define PP_PARSE_TARGET_LT_0 3   /* "dataset record has target_len < 0"        */
 
 /* Same layout as pipeplan::Sample (include/pipeplan/workload.h:27-33). */
 typedef struct pp_sample {
@@ -120,7 +128,9 @@ typedef struct pp_tuning {
                               DP's band traffic) instead of the dense band; 0 (default):
                               dense — the DP passes are issue-bound on a B200, and the
                               record indirection costs more than the bytes it saves */
-  int32_t reserved[1];
+  int32_t host_chunks;     /* host-buffer calls with streams > 1: chunks per worker (0 =
+                              default 2; 1 = no intra-worker prefetch).  Inputs of all
+                              chunks cross PCIe on one in-order stream, in claim order */
 } pp_tuning;
 
 /* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are
@@ -271,6 +281,33 @@ int pp_order_search_device(pp_ctx* ctx, const double* d_t_f, const double* d_t_b
                            const double* limits, int32_t n_clusters, double comm_latency,
                            int32_t* d_order, double* d_makespan, double* d_bubble_ratio,
                            int32_t* d_deadlock, double* d_device_stats, int32_t* d_status);
+
+/* Dataset ingest on the device: load_dataset over a
+ * record file (src/workload.cpp:65-103 load_record_file + :109-127
+ * truncation to max_seq_len), given the file's bytes.  out receives the
+ * samples (id = record index) when capacity allows; *n_records is set either
+ * way.  PP_ERR_PARSE: the first malformed line, *err_line 1-based,
+ * *err_byte its offset, *err_kind a PP_PARSE_* kind.  PP_ERR_INVALID:
+ * max_seq_len < 1, "dataset is empty" (no record), or capacity too small.
+ * Host buffers (the bytes are copied to the device). */
+int pp_load_records(pp_ctx* ctx, const char* bytes, int64_t n_bytes, int64_t max_seq_len, pp_sample* out,
+                    int64_t capacity, int64_t* n_records, int64_t* err_line, int64_t* err_byte,
+                    int32_t* err_kind);
+/* The same with the bytes and the output on the device (ctx stream). */
+int pp_load_records_device(pp_ctx* ctx, const char* d_bytes, int64_t n_bytes, int64_t max_seq_len,
+                           pp_sample* d_out, int64_t capacity, int64_t* n_records, int64_t* err_line,
+                           int64_t* err_byte, int32_t* err_kind);
+
+/* The mini-batches run_plan draws over a sample stream (src/driver.cpp:211,
+ * draw_minibatch src/workload.cpp:129-146, cursor 0 onwards): consecutive
+ * samples until the running total_tokens reaches token_budget, the crossing
+ * sample included.  seg_offsets (capacity n + 1) receives the n_seg + 1
+ * boundaries, directly usable as pp_plan_grid's seg_offsets.
+ * PP_ERR_INVALID: token_budget < 1. */
+int pp_draw_minibatches(pp_ctx* ctx, const pp_sample* samples, int64_t n, int64_t token_budget,
+                        int64_t* seg_offsets, int64_t* n_seg);
+int pp_draw_minibatches_device(pp_ctx* ctx, const pp_sample* d_samples, int64_t n, int64_t token_budget,
+                               int64_t* d_seg_offsets, int64_t* n_seg);
 
 /* Diagnostics: measured FP64 add issue rate of `device` (adds/s), the
  * roofline denominator of the FP64-bound cost kernels (calib.cu). */

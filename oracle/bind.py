@@ -212,6 +212,8 @@ class Reference:
         L.ref_op_costs.argtypes = [vp, i64, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), vp, vp, vp]
         L.ref_order_search.argtypes = [vp, vp, vp, vp, i32, i32, vp, i32, dbl, i32, vp, vp, vp, vp, vp, vp]
         L.ref_order_search.restype = dbl
+        L.ref_load_record_file.argtypes = [C.c_char_p, i64, vp, i64, vp, vp, vp, vp]
+        L.ref_draw_all.argtypes = [vp, i64, i64, vp, vp]
         self.L = L
 
     def order_samples(self, samples):
@@ -258,6 +260,25 @@ class Reference:
                                        _p(out["bubble_ratio"]), _p(out["deadlock"]), _p(out["device_stats"]),
                                        _p(out["status"]))
         return secs, out
+
+    def load_record_file(self, path, max_seq_len, cap=None):
+        """The reference's load_dataset(DatasetSpec{path}) -> (status, samples,
+        err_line, err_byte, err_kind)."""
+        if cap is None:
+            cap = os.path.getsize(path) // 2 + 1
+        out = np.zeros((cap, 3), np.int64)
+        n, el, eb = (np.zeros(1, np.int64) for _ in range(3))
+        ek = np.zeros(1, np.int32)
+        rc = self.L.ref_load_record_file(str(path).encode(), max_seq_len, _p(out), cap, _p(n), _p(el), _p(eb),
+                                         _p(ek))
+        return rc, out[:min(int(n[0]), cap)].copy(), int(el[0]), int(eb[0]), int(ek[0])
+
+    def draw_all(self, samples, budget):
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        off = np.zeros(len(s) + 1, np.int64)
+        m = np.zeros(1, np.int64)
+        rc = self.L.ref_draw_all(_p(s), len(s), budget, _p(off), _p(m))
+        return rc, off[:int(m[0]) + 1].copy()
 
     def synthetic_grid_cells(self, params7, tp, mbs_axis=(), seq_axis=()):
         par = np.asarray(params7, np.float64)

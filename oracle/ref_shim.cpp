@@ -415,4 +415,55 @@ double ref_order_search(const double* t_f, const double* t_b, const double* act,
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+
+// load_dataset over a record file (workload.cpp:65-127): samples out (up to
+// cap), *n set; PP_ERR_PARSE with line / byte / message kind, PP_ERR_INVALID.
+int ref_load_record_file(const char* path, int64_t max_seq_len, pp_sample* out, int64_t cap, int64_t* n,
+                         int64_t* err_line, int64_t* err_byte, int32_t* err_kind) {
+  *n = 0;
+  *err_line = -1;
+  *err_byte = 0;
+  *err_kind = -1;
+  try {
+    DatasetSpec spec;
+    spec.path = path;
+    spec.max_seq_len = max_seq_len;
+    std::vector<Sample> v = load_dataset(spec);
+    *n = static_cast<int64_t>(v.size());
+    for (int64_t k = 0; k < *n && k < cap; ++k) out[k] = pp_sample{v[k].id, v[k].input_len, v[k].target_len};
+    return PP_OK;
+  } catch (const ParseError& e) {
+    *err_line = e.line();
+    *err_byte = e.byte_offset();
+    const std::string w = e.what();
+    *err_kind = w.find("missing tab") != std::string::npos    ? PP_PARSE_MISSING_TAB
+                : w.find("pair of integers") != std::string::npos ? PP_PARSE_NOT_INTEGERS
+                : w.find("input_len < 1") != std::string::npos    ? PP_PARSE_INPUT_LT_1
+                                                                  : PP_PARSE_TARGET_LT_0;
+    return PP_ERR_PARSE;
+  } catch (const std::invalid_argument&) {
+    return PP_ERR_INVALID;
+  }
+}
+
+// run_plan's draw loop (driver.cpp:209-215): seg offsets of every mini-batch
+// draw_minibatch yields from cursor 0.
+int ref_draw_all(const pp_sample* s, int64_t n, int64_t budget, int64_t* offsets, int64_t* n_seg) {
+  try {
+    std::vector<Sample> v(n);
+    for (int64_t k = 0; k < n; ++k) v[k] = Sample{s[k].id, s[k].input_len, s[k].target_len};
+    std::size_t cursor = 0;
+    int64_t m = 0;
+    offsets[0] = 0;
+    while (auto d = draw_minibatch(v, budget, cursor)) {
+      cursor = d->next_cursor;
+      offsets[++m] = static_cast<int64_t>(cursor);
+    }
+    *n_seg = m;
+    return PP_OK;
+  } catch (const std::invalid_argument&) {
+    return PP_ERR_INVALID;
+  }
+}
+
 }  // extern "C"

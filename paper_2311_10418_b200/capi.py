@@ -23,7 +23,7 @@ _LIB_PATH = os.environ.get("PIPEPLAN_B200_LIB") or os.path.join(
 
 PP_OK, PP_ERR_INVALID, PP_ERR_INFEASIBLE_SAMPLE, PP_ERR_INFEASIBLE = 0, 1, 2, 3
 PP_ERR_CUDA, PP_ERR_NO_DEVICE, PP_ERR_OUT_OF_RANGE = 4, 5, 6
-PP_ERR_NOT_CONVERGED, PP_ERR_NOT_EXECUTABLE = 7, 8
+PP_ERR_NOT_CONVERGED, PP_ERR_NOT_EXECUTABLE, PP_ERR_PARSE = 7, 8, 9
 
 # Every symbol include/pipeplan_b200.h declares (checked by the CPU tests).
 EXPORTED = [
@@ -32,6 +32,7 @@ EXPORTED = [
     "pp_plan_grid_device", "pp_plan_tables", "pp_candidate_range", "pp_eval_objective",
     "pp_synthetic_grid", "pp_synthetic_dataset", "pp_slice_cost_host", "pp_calibrate_fp64",
     "pp_op_costs", "pp_plan_op_costs_device", "pp_order_search", "pp_order_search_device",
+    "pp_load_records", "pp_load_records_device", "pp_draw_minibatches", "pp_draw_minibatches_device",
 ]
 
 
@@ -45,6 +46,14 @@ class NoDeviceError(PlannerError):
 
 class InvalidArgument(PlannerError, ValueError):
     pass
+
+
+class ParseError(PlannerError, ValueError):
+    """pipeplan::ParseError (errors.h:25-40): line (1-based), byte offset."""
+
+    def __init__(self, msg: str, line: int, byte_offset: int, kind: int = -1):
+        super().__init__(msg)
+        self.line, self.byte_offset, self.kind = line, byte_offset, kind
 
 
 class InfeasibleError(PlannerError):
@@ -76,7 +85,7 @@ class DpOptions(C.Structure):
 class Tuning(C.Structure):
     _fields_ = [("first_wave", C.c_int32), ("max_wave", C.c_int32), ("streams", C.c_int32),
                 ("coop_min_n", C.c_int32), ("no_slice_reuse", C.c_int32), ("no_band_trunc", C.c_int32),
-                ("compact_band", C.c_int32), ("reserved", C.c_int32 * 1)]
+                ("compact_band", C.c_int32), ("host_chunks", C.c_int32)]
 
 
 class PlanOut(C.Structure):
@@ -138,6 +147,10 @@ def _load():
     lib.pp_op_costs.argtypes = [vp, vp, i64, C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, vp, vp]
     lib.pp_plan_op_costs_device.argtypes = [vp, vp, vp, vp, i32, vp, vp, C.POINTER(GridDesc),
                                             C.POINTER(ModelDesc), i64, vp, vp, vp, vp]
+    lib.pp_load_records.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp]
+    lib.pp_load_records_device.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp]
+    lib.pp_draw_minibatches.argtypes = [vp, vp, i64, i64, vp, vp]
+    lib.pp_draw_minibatches_device.argtypes = [vp, vp, i64, i64, vp, vp]
     lib.pp_order_search.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, i32, dbl, vp, vp, vp, vp, vp, vp]
     lib.pp_order_search_device.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, dbl, vp, vp, vp, vp,
                                            vp, vp]
@@ -317,9 +330,10 @@ class Planner:
         return (lib.pp_ctx_last_error(self._h) or b"").decode()
 
     def set_tuning(self, first_wave: int = 1, max_wave: int = 16, streams: int = 1, coop_min_n: int = 0,
-                   slice_reuse: bool = True, band_trunc: bool = True, compact_band: bool = False):
+                   slice_reuse: bool = True, band_trunc: bool = True, compact_band: bool = False,
+                   host_chunks: int = 0):
         t = Tuning(first_wave, max_wave, streams, coop_min_n, 0 if slice_reuse else 1, 0 if band_trunc else 1,
-                   1 if compact_band else 0)
+                   1 if compact_band else 0, host_chunks)
         rc = lib.pp_ctx_set_tuning(self._h, C.byref(t))
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())
@@ -460,6 +474,52 @@ class Planner:
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())
         return mb_off
+
+    def load_records(self, data: bytes, max_seq_len: int, capacity: int | None = None):
+        """load_dataset over a record file's bytes on the device -> (n, 3)
+        int64 samples.  Raises ParseError (line, byte) / InvalidArgument."""
+        buf = np.frombuffer(data, np.uint8)
+        cap = len(buf) // 2 + 1 if capacity is None else capacity
+        out = np.zeros((cap, 3), np.int64)
+        n, el, eb = (np.zeros(1, np.int64) for _ in range(3))
+        ek = np.zeros(1, np.int32)
+        rc = lib.pp_load_records(self._h, _p(buf) if len(buf) else None, len(buf), max_seq_len, _p(out), cap,
+                                 _p(n), _p(el), _p(eb), _p(ek))
+        if rc == PP_ERR_PARSE:
+            raise ParseError(self._err(), int(el[0]), int(eb[0]), int(ek[0]))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return out[:int(n[0])].copy()
+
+    def load_records_device(self, d_bytes, n_bytes: int, max_seq_len: int, d_out) -> int:
+        n, el, eb = (np.zeros(1, np.int64) for _ in range(3))
+        ek = np.zeros(1, np.int32)
+        rc = lib.pp_load_records_device(self._h, C.c_void_p(d_bytes.data_ptr()), n_bytes, max_seq_len,
+                                        C.c_void_p(d_out.data_ptr()), d_out.shape[0], _p(n), _p(el), _p(eb),
+                                        _p(ek))
+        if rc == PP_ERR_PARSE:
+            raise ParseError(self._err(), int(el[0]), int(eb[0]), int(ek[0]))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return int(n[0])
+
+    def draw_minibatches(self, samples, token_budget: int) -> np.ndarray:
+        """run_plan's draw_minibatch loop -> seg_offsets (n_seg + 1)."""
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        off = np.zeros(len(s) + 1, np.int64)
+        m = np.zeros(1, np.int64)
+        rc = lib.pp_draw_minibatches(self._h, _p(s) if len(s) else None, len(s), token_budget, _p(off), _p(m))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return off[:int(m[0]) + 1].copy()
+
+    def draw_minibatches_device(self, d_samples, n: int, token_budget: int, d_offsets) -> int:
+        m = np.zeros(1, np.int64)
+        rc = lib.pp_draw_minibatches_device(self._h, C.c_void_p(d_samples.data_ptr()), n, token_budget,
+                                            C.c_void_p(d_offsets.data_ptr()), _p(m))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return int(m[0])
 
     def order_search(self, t_f, t_b, act_mem, mb_offset, limits, n_clusters: int = 3,
                      comm_latency: float = 0.0) -> dict:

@@ -105,6 +105,14 @@ size_t dp_coop_parts_bytes(int grid);
 size_t order_search_slot_bytes(int64_t max_m, int C);
 int order_search_warps(int64_t n_items, int C, size_t slot_bytes, size_t budget);
 size_t order_search_item_bytes();
+size_t ingest_scratch_bytes(int64_t n_bytes);
+cudaError_t launch_load_records(const unsigned char* d_bytes, int64_t n, long long max_seq_len, char* scratch,
+                                size_t scratch_bytes, pp_sample* d_out, int64_t capacity, int64_t* n_records,
+                                int64_t* n_lines_out, int64_t* err_line, int32_t* err_kind, int64_t* err_byte,
+                                cudaStream_t st);
+size_t draw_scratch_bytes(int64_t n);
+cudaError_t launch_draw_minibatches(const pp_sample* d_samples, int64_t n, long long budget, char* scratch,
+                                    size_t scratch_bytes, int64_t* d_seg_offsets, int64_t* n_seg, cudaStream_t st);
 cudaError_t launch_order_search(const double* tf, const double* tb, const double* act,
                                 const int64_t* mb_off, int n_seg, int C, const double* limits,
                                 int k, int kfact, double comm_latency, int64_t max_m, double* pred,
@@ -220,6 +228,8 @@ struct pp_ctx {
   // injection-order search (sched.cu)
   DevBuf os_tf, os_tb, os_act, os_off, os_lim, os_pred, os_assign, os_idx, os_cloff, os_clk, os_scratch,
       os_items, os_istats, os_order, os_ms, os_bub, os_dl, os_ds, os_status;
+  // dataset ingest (ingest.cu)
+  DevBuf ing_bytes, ing_scratch, ing_out, ing_off;
   // host copy of the uploaded grid (restricted to the recompute strategy)
   // for the monotonicity certificate of cost pass A
   std::vector<double> h_ax, h_cells;
@@ -231,6 +241,8 @@ struct pp_ctx {
   // pipelined host-buffer worker (plan_host_chunks): copy stream + two sets
   cudaStream_t cstream = nullptr;
   HostSet hset[2];
+  cudaStream_t h2d_stream = nullptr;  // shared in-order input stream of plan_host_split
+  std::mutex h2d_mu;
   CostGrid grid_dev{};            // device view of the uploaded grid
   bool grid_valid = false;
   double tau_interval = -1.0;     // interval the device bin thresholds were built for
@@ -252,6 +264,7 @@ struct pp_ctx {
             &cmin, &dp_cols, &colbase, &chunk_nv, &perm,
             &os_tf, &os_tb, &os_act, &os_off, &os_lim, &os_pred, &os_assign, &os_idx, &os_cloff, &os_clk,
             &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status,
+            &ing_bytes, &ing_scratch, &ing_out, &ing_off,
             &hset[0].samples, &hset[0].seg, &hset[0].ordered, &hset[0].order, &hset[0].splits,
             &hset[0].times, &hset[0].count, &hset[0].tmax, &hset[0].obj, &hset[0].status, &hset[0].err,
             &hset[1].samples, &hset[1].seg, &hset[1].ordered, &hset[1].order, &hset[1].splits,
@@ -1377,6 +1390,10 @@ int pp_ctx_destroy(pp_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->h2d_stream) {
+    cudaStreamSynchronize(ctx->h2d_stream);
+    cudaStreamDestroy(ctx->h2d_stream);
+  }
   if (ctx->cstream) {
     cudaStreamSynchronize(ctx->cstream);
     cudaStreamDestroy(ctx->cstream);
@@ -1539,7 +1556,8 @@ int plan_host(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets,
 template <class Claim, class Done>
 int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_offsets, const int* cut,
                      int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
-                     const pp_dp_options* opts, const pp_plan_out* out, Claim claim, Done done) {
+                     const pp_dp_options* opts, const pp_plan_out* out, Claim claim, Done done,
+                     cudaStream_t h2d_stream, std::mutex* h2d_mu) {
   pp_ctx* ctx = sub;  // (PP_CUDA reports on ctx)
   if (!sub->cstream) PP_CUDA(cudaStreamCreateWithFlags(&sub->cstream, cudaStreamNonBlocking));
   for (HostSet& h : sub->hset) {
@@ -1557,20 +1575,27 @@ int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_o
     for (int s = s0; s <= s1; ++s) ho[s - s0] = seg_offsets[s] - base;
     PP_CUDA(h.samples.ensure(std::max<int64_t>(n, 1) * sizeof(pp_sample)));
     PP_CUDA(h.seg.ensure((ns + 1) * sizeof(int64_t)));
-    if (n > 0) PP_CUDA(cudaMemcpyAsync(h.samples.p, samples + base, n * sizeof(pp_sample), cudaMemcpyHostToDevice, cs));
-    PP_CUDA(cudaMemcpyAsync(h.seg.p, ho, (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, cs));
-    PP_CUDA(cudaEventRecord(h.h2d, cs));
+    if (n > 0)
+      PP_CUDA(cudaMemcpyAsync(h.samples.p, samples + base, n * sizeof(pp_sample), cudaMemcpyHostToDevice, h2d_stream));
+    PP_CUDA(cudaMemcpyAsync(h.seg.p, ho, (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, h2d_stream));
+    PP_CUDA(cudaEventRecord(h.h2d, h2d_stream));
     return PP_OK;
   };
   int rc = PP_OK;
-  int q = claim(), set = 0;
-  if (q >= 0 && (rc = stage(set, q))) return rc;
+  // claim + issue under one lock: the shared copy stream carries chunks in
+  // claim order (every worker's first chunk ahead of any prefetch)
+  auto claim_stage = [&](int st_set, int* q) -> int {
+    std::lock_guard<std::mutex> lk(*h2d_mu);
+    *q = claim();
+    return *q >= 0 ? stage(st_set, *q) : PP_OK;
+  };
+  int q = -1, set = 0;
+  if ((rc = claim_stage(set, &q))) return rc;
   while (q >= 0) {
-    const int qn = claim();
-    // prefetch the next chunk's inputs — after this chunk's arrived, so the
-    // first chunks of all workers cross PCIe ahead of any prefetch
-    PP_CUDA(cudaEventSynchronize(sub->hset[set].h2d));
-    if (qn >= 0 && (rc = stage(set ^ 1, qn))) return rc;
+    // prefetch the next chunk's inputs into the other set (its previous
+    // chunk's planning has completed: pp_plan_grid_device is synchronous)
+    int qn = -1;
+    if ((rc = claim_stage(set ^ 1, &qn))) return rc;
     HostSet& h = sub->hset[set];
     const int s0 = cut[q], s1 = cut[q + 1], ns = s1 - s0;
     const int64_t base = seg_offsets[s0], n = seg_offsets[s1] - base;
@@ -1634,9 +1659,14 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
                     int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
                     const pp_dp_options* opts, const pp_plan_out* out, int workers) {
   workers = std::min(workers, (int)n_seg);
-  // two chunks per worker: one is planned while the other's inputs / plans
-  // cross PCIe (plan_host_chunks)
-  std::vector<int> wts(std::min<int>(n_seg, 2 * workers), 1);
+  // >= two chunks per worker: one is planned while the next one's inputs and
+  // the previous one's plans cross PCIe (plan_host_chunks)
+  const int per_worker = ctx->tuning.host_chunks >= 1 ? ctx->tuning.host_chunks : 2;
+  std::vector<int> wts(std::min<int>(n_seg, per_worker * workers), 1);
+  // every chunk's inputs go through ONE in-order copy stream, issued in claim
+  // order, so the first chunk arrives after 1/chunks of the bytes rather than
+  // all workers' first chunks sharing PCIe
+  if (!ctx->h2d_stream) PP_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
   const int chunks = (int)wts.size();
   while ((int)ctx->subs.size() < workers) {
     pp_ctx* sub = nullptr;
@@ -1696,7 +1726,7 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
         S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
       };
       rcs[w] = plan_host_chunks(sub, samples, seg_offsets, cut.data(), presorted, grid, model, opts, out,
-                                claim, done);
+                                claim, done, ctx->h2d_stream, &ctx->h2d_mu);
       acc[w] = S;
     });
   }
@@ -2091,6 +2121,104 @@ int pp_order_search_device(pp_ctx* ctx, const double* d_t_f, const double* d_t_b
   return order_search_run(ctx, d_t_f, d_t_b, d_act_mem, d_mb_offset, h_mb_offset, n_seg, n_stages, limits,
                           n_clusters, comm_latency, d_order, d_makespan, d_bubble_ratio, d_deadlock,
                           d_device_stats, d_status);
+}
+
+
+static const char* parse_msg(int kind) {
+  switch (kind) {
+    case PP_PARSE_MISSING_TAB: return "dataset record missing tab separator";
+    case PP_PARSE_NOT_INTEGERS: return "dataset record is not a pair of integers";
+    case PP_PARSE_INPUT_LT_1: return "dataset record has input_len < 1";
+    default: return "dataset record has target_len < 0";
+  }
+}
+
+int pp_load_records_device(pp_ctx* ctx, const char* d_bytes, int64_t n_bytes, int64_t max_seq_len,
+                           pp_sample* d_out, int64_t capacity, int64_t* n_records, int64_t* err_line,
+                           int64_t* err_byte, int32_t* err_kind) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n_bytes < 0 || (n_bytes > 0 && !d_bytes) || !n_records || !err_line || !err_byte || !err_kind ||
+      capacity < 0)
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  *n_records = 0;
+  *err_line = -1;
+  *err_byte = 0;
+  *err_kind = 0;
+  if (max_seq_len < 1) return fail(ctx, PP_ERR_INVALID, "max_seq_len must be >= 1");  // workload.cpp:110
+  if (n_bytes >= ((int64_t)1 << 31) - 1) return fail(ctx, PP_ERR_INVALID, "record file too large (< 2 GiB)");
+  const size_t need = ingest_scratch_bytes(n_bytes);
+  PP_CUDA(ctx->ing_scratch.ensure(need));
+  int64_t nrec = 0, nlines = 0, el = -1, eb = 0;
+  int32_t ek = 0;
+  PP_CUDA(launch_load_records(reinterpret_cast<const unsigned char*>(d_bytes), n_bytes, max_seq_len,
+                              ctx->ing_scratch.as<char>(), ctx->ing_scratch.cap, d_out, capacity, &nrec, &nlines,
+                              &el, &ek, &eb, ctx->stream));
+  if (el >= 0) {
+    *err_line = el + 1;
+    *err_byte = eb;
+    *err_kind = ek;
+    return fail(ctx, PP_ERR_PARSE, std::string(parse_msg(ek)) + " (line " + std::to_string(el + 1) + ", byte " +
+                                        std::to_string(eb) + ")");
+  }
+  *n_records = nrec;
+  if (nrec == 0) return fail(ctx, PP_ERR_INVALID, "dataset is empty");  // workload.cpp:121
+  if (nrec > capacity) return fail(ctx, PP_ERR_INVALID, "sample capacity too small");
+  PP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PP_OK;
+}
+
+int pp_load_records(pp_ctx* ctx, const char* bytes, int64_t n_bytes, int64_t max_seq_len, pp_sample* out,
+                    int64_t capacity, int64_t* n_records, int64_t* err_line, int64_t* err_byte,
+                    int32_t* err_kind) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n_bytes < 0 || (n_bytes > 0 && !bytes) || capacity < 0) return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  PP_CUDA(ctx->ing_bytes.ensure(std::max<int64_t>(n_bytes, 1)));
+  if (n_bytes > 0)
+    PP_CUDA(cudaMemcpyAsync(ctx->ing_bytes.p, bytes, n_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PP_CUDA(ctx->ing_out.ensure(std::max<int64_t>(capacity, 1) * sizeof(pp_sample)));
+  rc = pp_load_records_device(ctx, ctx->ing_bytes.as<char>(), n_bytes, max_seq_len, ctx->ing_out.as<pp_sample>(),
+                              capacity, n_records, err_line, err_byte, err_kind);
+  if (rc) return rc;
+  if (out && *n_records > 0)
+    PP_CUDA(cudaMemcpyAsync(out, ctx->ing_out.p, *n_records * sizeof(pp_sample), cudaMemcpyDeviceToHost, ctx->stream));
+  PP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PP_OK;
+}
+
+int pp_draw_minibatches_device(pp_ctx* ctx, const pp_sample* d_samples, int64_t n, int64_t token_budget,
+                               int64_t* d_seg_offsets, int64_t* n_seg) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!d_samples || !d_seg_offsets)) || !n_seg) return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  if (token_budget < 1) return fail(ctx, PP_ERR_INVALID, "token_budget must be >= 1");  // workload.cpp:131
+  if (n >= ((int64_t)1 << 31) - 2) return fail(ctx, PP_ERR_INVALID, "too many samples");
+  PP_CUDA(ctx->ing_scratch.ensure(draw_scratch_bytes(n)));
+  PP_CUDA(launch_draw_minibatches(d_samples, n, token_budget, ctx->ing_scratch.as<char>(), ctx->ing_scratch.cap,
+                                  d_seg_offsets, n_seg, ctx->stream));
+  return PP_OK;
+}
+
+int pp_draw_minibatches(pp_ctx* ctx, const pp_sample* samples, int64_t n, int64_t token_budget,
+                        int64_t* seg_offsets, int64_t* n_seg) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!samples || !seg_offsets)) || !n_seg) return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  PP_CUDA(ctx->ing_out.ensure(std::max<int64_t>(n, 1) * sizeof(pp_sample)));
+  PP_CUDA(ctx->ing_off.ensure((n + 1) * sizeof(int64_t)));
+  if (n > 0)
+    PP_CUDA(cudaMemcpyAsync(ctx->ing_out.p, samples, n * sizeof(pp_sample), cudaMemcpyHostToDevice, ctx->stream));
+  rc = pp_draw_minibatches_device(ctx, ctx->ing_out.as<pp_sample>(), n, token_budget, ctx->ing_off.as<int64_t>(),
+                                  n_seg);
+  if (rc) return rc;
+  if (n > 0)
+    PP_CUDA(cudaMemcpyAsync(seg_offsets, ctx->ing_off.p, (*n_seg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  else
+    seg_offsets[0] = 0;
+  PP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PP_OK;
 }
 
 }  // extern "C"

@@ -13,13 +13,14 @@ from paper_2311_10418_b200 import capi  # noqa: E402
 from paper_2311_10418_b200 import workloads as W  # noqa: E402
 
 
-def main(M=888, streams=3, reps=5):
+def main(M=888, streams=3, reps=5, host_chunks=0):
     cfg = W.CONFIGS["C3"]
     s = W.dataset(cfg, M)
     off = W.seg_offsets(cfg, M)
     n = len(s)
     p = capi.Planner(0)
-    p.set_tuning(streams=streams)
+    p.set_tuning(streams=streams, host_chunks=host_chunks)
+    print(f"streams {streams} host_chunks {host_chunks}")
     grid, model = W.grid(), W.model(cfg)
     pin = torch.from_numpy(s).pin_memory()
     pinned = []
