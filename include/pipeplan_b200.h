@@ -129,8 +129,7 @@ typedef struct pp_tuning {
                               dense — the DP passes are issue-bound on a B200, and the
                               record indirection costs more than the bytes it saves */
   int32_t host_chunks;     /* host-buffer calls with streams > 1: chunks per worker (0 =
-                              default 2; 1 = no intra-worker prefetch).  Inputs of all
-                              chunks cross PCIe on one in-order stream, in claim order */
+                              default 2; 1 = no intra-worker prefetch) */
 } pp_tuning;
 
 /* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are

@@ -241,8 +241,6 @@ struct pp_ctx {
   // pipelined host-buffer worker (plan_host_chunks): copy stream + two sets
   cudaStream_t cstream = nullptr;
   HostSet hset[2];
-  cudaStream_t h2d_stream = nullptr;  // shared in-order input stream of plan_host_split
-  std::mutex h2d_mu;
   CostGrid grid_dev{};            // device view of the uploaded grid
   bool grid_valid = false;
   double tau_interval = -1.0;     // interval the device bin thresholds were built for
@@ -668,8 +666,8 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   PP_CUDA(ctx->in_d.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
   PP_CUDA(ctx->tgt_d.ensure(std::max<int64_t>(total, 1) * sizeof(double)));
   if (!table) {
-    PP_CUDA(ctx->range.ensure(6 * sizeof(unsigned long long)));
-    PP_CUDA(ctx->h_range.ensure(6 * sizeof(unsigned long long)));
+    PP_CUDA(ctx->range.ensure(8 * sizeof(unsigned long long)));
+    PP_CUDA(ctx->h_range.ensure(8 * sizeof(unsigned long long)));
     PP_CUDA(ctx->sort_keys.ensure(std::max<int64_t>(total, 1) * 6 * sizeof(unsigned long long)));
     PP_CUDA(ctx->sort_vals.ensure(std::max<int64_t>(total, 1) * 2 * sizeof(uint32_t)));
     if (total > 0)
@@ -1390,10 +1388,6 @@ int pp_ctx_destroy(pp_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  if (ctx->h2d_stream) {
-    cudaStreamSynchronize(ctx->h2d_stream);
-    cudaStreamDestroy(ctx->h2d_stream);
-  }
   if (ctx->cstream) {
     cudaStreamSynchronize(ctx->cstream);
     cudaStreamDestroy(ctx->cstream);
@@ -1556,8 +1550,7 @@ int plan_host(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets,
 template <class Claim, class Done>
 int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_offsets, const int* cut,
                      int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
-                     const pp_dp_options* opts, const pp_plan_out* out, Claim claim, Done done,
-                     cudaStream_t h2d_stream, std::mutex* h2d_mu) {
+                     const pp_dp_options* opts, const pp_plan_out* out, Claim claim, Done done) {
   pp_ctx* ctx = sub;  // (PP_CUDA reports on ctx)
   if (!sub->cstream) PP_CUDA(cudaStreamCreateWithFlags(&sub->cstream, cudaStreamNonBlocking));
   for (HostSet& h : sub->hset) {
@@ -1575,27 +1568,20 @@ int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_o
     for (int s = s0; s <= s1; ++s) ho[s - s0] = seg_offsets[s] - base;
     PP_CUDA(h.samples.ensure(std::max<int64_t>(n, 1) * sizeof(pp_sample)));
     PP_CUDA(h.seg.ensure((ns + 1) * sizeof(int64_t)));
-    if (n > 0)
-      PP_CUDA(cudaMemcpyAsync(h.samples.p, samples + base, n * sizeof(pp_sample), cudaMemcpyHostToDevice, h2d_stream));
-    PP_CUDA(cudaMemcpyAsync(h.seg.p, ho, (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, h2d_stream));
-    PP_CUDA(cudaEventRecord(h.h2d, h2d_stream));
+    if (n > 0) PP_CUDA(cudaMemcpyAsync(h.samples.p, samples + base, n * sizeof(pp_sample), cudaMemcpyHostToDevice, cs));
+    PP_CUDA(cudaMemcpyAsync(h.seg.p, ho, (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, cs));
+    PP_CUDA(cudaEventRecord(h.h2d, cs));
     return PP_OK;
   };
   int rc = PP_OK;
-  // claim + issue under one lock: the shared copy stream carries chunks in
-  // claim order (every worker's first chunk ahead of any prefetch)
-  auto claim_stage = [&](int st_set, int* q) -> int {
-    std::lock_guard<std::mutex> lk(*h2d_mu);
-    *q = claim();
-    return *q >= 0 ? stage(st_set, *q) : PP_OK;
-  };
-  int q = -1, set = 0;
-  if ((rc = claim_stage(set, &q))) return rc;
+  int q = claim(), set = 0;
+  if (q >= 0 && (rc = stage(set, q))) return rc;
   while (q >= 0) {
-    // prefetch the next chunk's inputs into the other set (its previous
-    // chunk's planning has completed: pp_plan_grid_device is synchronous)
-    int qn = -1;
-    if ((rc = claim_stage(set ^ 1, &qn))) return rc;
+    const int qn = claim();
+    // prefetch the next chunk's inputs — after this chunk's arrived, so the
+    // first chunks of all workers cross PCIe ahead of any prefetch
+    PP_CUDA(cudaEventSynchronize(sub->hset[set].h2d));
+    if (qn >= 0 && (rc = stage(set ^ 1, qn))) return rc;
     HostSet& h = sub->hset[set];
     const int s0 = cut[q], s1 = cut[q + 1], ns = s1 - s0;
     const int64_t base = seg_offsets[s0], n = seg_offsets[s1] - base;
@@ -1663,10 +1649,6 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
   // the previous one's plans cross PCIe (plan_host_chunks)
   const int per_worker = ctx->tuning.host_chunks >= 1 ? ctx->tuning.host_chunks : 2;
   std::vector<int> wts(std::min<int>(n_seg, per_worker * workers), 1);
-  // every chunk's inputs go through ONE in-order copy stream, issued in claim
-  // order, so the first chunk arrives after 1/chunks of the bytes rather than
-  // all workers' first chunks sharing PCIe
-  if (!ctx->h2d_stream) PP_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
   const int chunks = (int)wts.size();
   while ((int)ctx->subs.size() < workers) {
     pp_ctx* sub = nullptr;
@@ -1726,7 +1708,7 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
         S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
       };
       rcs[w] = plan_host_chunks(sub, samples, seg_offsets, cut.data(), presorted, grid, model, opts, out,
-                                claim, done, ctx->h2d_stream, &ctx->h2d_mu);
+                                claim, done);
       acc[w] = S;
     });
   }
@@ -1794,8 +1776,8 @@ int pp_order_samples(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_o
   if ((rc = stage_inputs(ctx, samples, seg_offsets, n_seg))) return rc;
   PP_CUDA(ctx->in_d.ensure(total * sizeof(double)));
   PP_CUDA(ctx->tgt_d.ensure(total * sizeof(double)));
-  PP_CUDA(ctx->range.ensure(6 * sizeof(unsigned long long)));
-  PP_CUDA(ctx->h_range.ensure(6 * sizeof(unsigned long long)));
+  PP_CUDA(ctx->range.ensure(8 * sizeof(unsigned long long)));
+  PP_CUDA(ctx->h_range.ensure(8 * sizeof(unsigned long long)));
   PP_CUDA(ctx->sort_keys.ensure(total * 6 * sizeof(unsigned long long)));
   PP_CUDA(ctx->sort_vals.ensure(total * 2 * sizeof(uint32_t)));
   PP_CUDA(launch_segmented_sort(ctx->samples.as<pp_sample>(), ctx->seg_off.as<int64_t>(), seg_offsets,

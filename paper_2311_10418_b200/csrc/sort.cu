@@ -37,12 +37,14 @@ struct FieldRange {
 };
 
 __global__ void field_range_kernel(const pp_sample* __restrict__ s, int64_t n,
-                                   unsigned long long* out /* 6 words, biased */) {
+                                   unsigned long long* out /* 6 words, biased; [6]: ids unordered */) {
   long long mn[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
   long long mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+  int unordered = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     const pp_sample v = s[k];
+    if (k + 1 < n) unordered |= s[k + 1].id <= v.id;
     const long long f[3] = {v.input_len, v.target_len, v.id};
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -65,6 +67,7 @@ __global__ void field_range_kernel(const pp_sample* __restrict__ s, int64_t n,
       atomicMax(&out[3 + q], (unsigned long long)mx[q] ^ 0x8000000000000000ULL);
     }
   }
+  if (__any_sync(0xffffffffu, unordered) && (threadIdx.x & 31) == 0) atomicOr(&out[6], 1ULL);
 }
 
 __device__ __forceinline__ int bit_width(unsigned long long range) {
@@ -102,9 +105,9 @@ __device__ __forceinline__ unsigned long long block_exscan(unsigned long long v,
 }
 
 // One stable LSD pass on `n` items: digit = (key[item*W + w] >> sh) & 3.
-template <int W, bool V = true>
-__device__ void radix_pass(const unsigned long long* __restrict__ kin, const uint32_t* __restrict__ vin,
-                           unsigned long long* __restrict__ kout, uint32_t* __restrict__ vout, int n,
+template <int W, bool V = true, class KT = unsigned long long, class VT = uint32_t>
+__device__ void radix_pass(const KT* __restrict__ kin, const VT* __restrict__ vin,
+                           KT* __restrict__ kout, VT* __restrict__ vout, int n,
                            int w, int sh, unsigned long long* warp_tot, int* bucket) {
   // bucket totals
   if (threadIdx.x < 4) bucket[threadIdx.x] = 0;
@@ -157,11 +160,14 @@ __device__ void radix_pass(const unsigned long long* __restrict__ kin, const uin
 
 // Builds keys for segment `seg`, sorts, and gathers ordered samples + SoA
 // double lengths.  `range` holds the biased field minima/maxima of the call.
-template <int W>
+// KT / VT: key and index types.  uint32 keys + uint16 indices (12 B per
+// item, two 8192-item CTAs per SM) when the launcher certified that every
+// key fits 32 bits (input + target bits <= 32, ids increasing) and n <= 65536.
+template <int W, class KT = unsigned long long, class VT = uint32_t>
 __global__ void __launch_bounds__(kSortThreads)
     seg_sort_kernel(const pp_sample* __restrict__ in, const int64_t* __restrict__ seg_off,
-                    const unsigned long long* __restrict__ range, unsigned long long* gkeys,
-                    uint32_t* gvals, int use_smem, pp_sample* __restrict__ out,
+                    const unsigned long long* __restrict__ range, KT* gkeys,
+                    VT* gvals, int use_smem, pp_sample* __restrict__ out,
                     double* __restrict__ in_d, double* __restrict__ tgt_d, int32_t* __restrict__ perm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long warp_tot[kSortThreads / 32];
@@ -222,12 +228,12 @@ __global__ void __launch_bounds__(kSortThreads)
   }
   if (ids_in_order) bits[2] = 0;
   (void)range;
-  unsigned long long *k0, *k1;
-  uint32_t *v0, *v1;
+  KT *k0, *k1;
+  VT *v0, *v1;
   if (use_smem) {
-    k0 = reinterpret_cast<unsigned long long*>(smem_raw);
+    k0 = reinterpret_cast<KT*>(smem_raw);
     k1 = k0 + (size_t)n * W;
-    v0 = reinterpret_cast<uint32_t*>(k1 + (size_t)n * W);
+    v0 = reinterpret_cast<VT*>(k1 + (size_t)n * W);
     v1 = v0 + n;
   } else {
     k0 = gkeys + (size_t)b * W * 2;
@@ -243,29 +249,29 @@ __global__ void __launch_bounds__(kSortThreads)
     if (W == 1) {
       // caller checked bits[0]+bits[1]+bits[2] <= 64; guard the 64-bit shifts
       const int s1 = bits[1] + bits[2];
-      k0[k] = (s1 < 64 ? (fi << s1) : 0ULL) | (bits[2] < 64 ? (ft << bits[2]) : 0ULL) | fd;
+      k0[k] = (KT)((s1 < 64 ? (fi << s1) : 0ULL) | (bits[2] < 64 ? (ft << bits[2]) : 0ULL) | fd);
     } else {
       k0[(size_t)k * W + 0] = fd;
       k0[(size_t)k * W + 1] = ft;
       k0[(size_t)k * W + 2] = fi;
     }
-    v0[k] = (uint32_t)k;
+    v0[k] = (VT)k;
   }
   __syncthreads();
   if (W == 1) {
     const int total = bits[0] + bits[1] + bits[2];
     for (int sh = 0; sh < total; sh += 2) {
-      radix_pass<1>(k0, v0, k1, v1, n, 0, sh, warp_tot, bucket);
-      unsigned long long* tk = k0; k0 = k1; k1 = tk;
-      uint32_t* tv = v0; v0 = v1; v1 = tv;
+      radix_pass<1, true, KT, VT>(k0, v0, k1, v1, n, 0, sh, warp_tot, bucket);
+      KT* tk = k0; k0 = k1; k1 = tk;
+      VT* tv = v0; v0 = v1; v1 = tv;
     }
   } else {
     const int word_bits[3] = {bits[2], bits[1], bits[0]};
     for (int w = 0; w < 3; ++w)
       for (int sh = 0; sh < word_bits[w]; sh += 2) {
-        radix_pass<W>(k0, v0, k1, v1, n, w, sh, warp_tot, bucket);
-        unsigned long long* tk = k0; k0 = k1; k1 = tk;
-        uint32_t* tv = v0; v0 = v1; v1 = tv;
+        radix_pass<W, true, KT, VT>(k0, v0, k1, v1, n, w, sh, warp_tot, bucket);
+        KT* tk = k0; k0 = k1; k1 = tk;
+        VT* tv = v0; v0 = v1; v1 = tv;
       }
   }
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(kSortThreads)
   const int bits = diff ? 64 - __clzll(diff) : 0;
   int parity = 0;
   for (int sh = 0; sh < bits; sh += 2) {
-    radix_pass<1, false>(k0, nullptr, k1, nullptr, n, 0, sh, warp_tot, bucket);
+    radix_pass<1, false>(k0, (const uint32_t*)nullptr, k1, (uint32_t*)nullptr, n, 0, sh, warp_tot, bucket);
     unsigned long long* tk = k0; k0 = k1; k1 = tk;
     parity ^= 1;
   }
@@ -355,11 +361,11 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
   // Field ranges of the call: they size the sort key and feed the host's
   // monotonicity certificate for the cost passes (capi.cu), so they are
   // computed for presorted calls too.
-  const unsigned long long init[6] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL};
+  const unsigned long long init[7] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL, 0ULL};
   cudaMemcpyAsync(d_range, init, sizeof(init), cudaMemcpyHostToDevice, st);
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
   field_range_kernel<<<blocks, 256, 0, st>>>(d_in, total, d_range);
-  cudaMemcpyAsync(h_range, d_range, sizeof(init), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(h_range, d_range, sizeof(init), cudaMemcpyDeviceToHost, st);  // 7 words
   if (presorted) {
     const int cb = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     copy_soa_kernel<<<cb, 256, 0, st>>>(d_in, total, d_out, d_in_len, d_tgt_len);
@@ -368,15 +374,28 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
   }
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
-  int bits = 0;
+  int bits = 0, fbits[3];
   for (int q = 0; q < 3; ++q) {
     const unsigned long long r = (h_range[3 + q] ^ 0x8000000000000000ULL) -
                                  (h_range[q] ^ 0x8000000000000000ULL);
-    bits += r == 0 ? 0 : 64 - __builtin_clzll(r);
+    fbits[q] = r == 0 ? 0 : 64 - __builtin_clzll(r);
+    bits += fbits[q];
   }
   const int W = bits <= 64 ? 1 : 3;
   int64_t max_n = 0;
   for (int s = 0; s < n_seg; ++s) max_n = std::max<int64_t>(max_n, h_seg_off[s + 1] - h_seg_off[s]);
+  // ids increasing over the call => increasing in every segment, so each
+  // segment's key is (input, target) only: 32-bit keys when those fit
+  const bool key32 = h_range[6] == 0 && fbits[0] + fbits[1] <= 32 && max_n <= 65536;
+  if (key32) {
+    const size_t need = (size_t)max_n * (2 * 4 + 2 * 2);
+    const int sm = need <= 200 * 1024 ? 1 : 0;
+    ensure_dyn_smem((const void*)seg_sort_kernel<1, uint32_t, uint16_t>, sm ? need : 0);
+    seg_sort_kernel<1, uint32_t, uint16_t><<<n_seg, kSortThreads, sm ? need : 0, st>>>(
+        d_in, d_seg_off, d_range, reinterpret_cast<uint32_t*>(d_keys), reinterpret_cast<uint16_t*>(d_vals), sm,
+        d_out, d_in_len, d_tgt_len, d_perm);
+    return cudaGetLastError();
+  }
   const size_t smem_need = (size_t)max_n * (2 * 8 * W + 2 * 4);
   const int use_smem = smem_need <= 200 * 1024 ? 1 : 0;
   const size_t smem = use_smem ? smem_need : 0;
