@@ -913,11 +913,13 @@ __global__ void __launch_bounds__(256)
     // the chain 8 splits per dependent shared-memory load, leaving a
     // checkpoint every 8 splits, and the block expands the checkpoints in
     // parallel (8 dependent loads each)
+    // three n-int buffers (two CTAs per SM at n = 8192): h2 and h8 share
+    // one, and the checkpoints reuse h4's once h8 is built
     int* h1 = chain;
     int* h2 = chain + n;
     int* h4 = chain + 2 * n;
-    int* h8 = chain + 3 * n;
-    int* ck = chain + 4 * n;  // checkpoints: the node before splits 8k .. 8k + 7
+    int* h8 = h2;
+    int* ck = h4;  // checkpoints: the node before splits 8k .. 8k + 7
     for (int q = threadIdx.x; q < n; q += blockDim.x) {
       const int a = h1[q];
       h2[q] = a < n ? h1[a] : n;
@@ -974,7 +976,7 @@ __global__ void __launch_bounds__(256)
   // slice times of the chosen micro-batches, fetched in parallel; staged in
   // shared memory (over the chain, which is no longer needed) when they fit
   double* tsh = chain_in_smem ? reinterpret_cast<double*>(chain) : nullptr;
-  const bool t_in_smem = chain_in_smem && (size_t)m * sizeof(double) <= (size_t)n * sizeof(int) * (chain_in_smem == 2 ? 4 : 1);
+  const bool t_in_smem = chain_in_smem && (size_t)m * sizeof(double) <= (size_t)n * sizeof(int) * (chain_in_smem == 2 ? 3 : 1);
   double mx = 0.0;
   // four micro-batches per thread and step: their band loads are independent
   constexpr int kU = 4;
@@ -1131,8 +1133,8 @@ cudaError_t launch_finalize(const SegDP* dps, const int* best_next, const int64_
                             int32_t* splits,
                             double* mb_times, int32_t* count, double* t_max_used, double* objective,
                             int32_t* status, int64_t* err_id, cudaStream_t st) {
-  // 2: the chain and its three hop tables in shared memory; 1: the chain only
-  const size_t hop_bytes = ((size_t)max_n * 4 + (size_t)max_n / 8 + 2) * sizeof(int);
+  // 2: the chain and its hop tables (three n-int buffers) in shared memory; 1: the chain only
+  const size_t hop_bytes = ((size_t)max_n * 3 + 2) * sizeof(int);
   const int in_smem = hop_bytes <= 200 * 1024 ? 2 : (size_t)max_n * sizeof(int) <= 200 * 1024 ? 1 : 0;
   const size_t smem = in_smem == 2 ? hop_bytes : in_smem ? (size_t)max_n * sizeof(int) : 0;
   ensure_dyn_smem((const void*)finalize_kernel, smem);
