@@ -59,15 +59,36 @@ __global__ void field_range_kernel(const pp_sample* __restrict__ s, int64_t n,
       mx[q] = max(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], o));
     }
   }
-  if ((threadIdx.x & 31) == 0) {
+  // block reduction first: one atomic per block and field (the 7 words are
+  // shared by every block of the call)
+  __shared__ long long wmn[32][3], wmx[32][3];
+  __shared__ int wuo[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int uo = __any_sync(0xffffffffu, unordered);
+  if (lane == 0) {
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      // signed -> order-preserving unsigned
-      atomicMin(&out[q], (unsigned long long)mn[q] ^ 0x8000000000000000ULL);
-      atomicMax(&out[3 + q], (unsigned long long)mx[q] ^ 0x8000000000000000ULL);
+      wmn[wid][q] = mn[q];
+      wmx[wid][q] = mx[q];
     }
+    wuo[wid] = uo;
   }
-  if (__any_sync(0xffffffffu, unordered) && (threadIdx.x & 31) == 0) atomicOr(&out[6], 1ULL);
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int q = threadIdx.x;
+    long long a = wmn[0][q], b = wmx[0][q];
+    for (int w = 1; w < nw; ++w) {
+      a = min(a, wmn[w][q]);
+      b = max(b, wmx[w][q]);
+    }
+    // signed -> order-preserving unsigned
+    atomicMin(&out[q], (unsigned long long)a ^ 0x8000000000000000ULL);
+    atomicMax(&out[3 + q], (unsigned long long)b ^ 0x8000000000000000ULL);
+  } else if (threadIdx.x == 3) {
+    int any = 0;
+    for (int w = 0; w < nw; ++w) any |= wuo[w];
+    if (any) atomicOr(&out[6], 1ULL);
+  }
 }
 
 __device__ __forceinline__ int bit_width(unsigned long long range) {
