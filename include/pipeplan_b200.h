@@ -308,6 +308,35 @@ int pp_draw_minibatches(pp_ctx* ctx, const pp_sample* samples, int64_t n, int64_
 int pp_draw_minibatches_device(pp_ctx* ctx, const pp_sample* d_samples, int64_t n, int64_t token_budget,
                                int64_t* d_seg_offsets, int64_t* n_seg);
 
+/* One row of padding_vs_packing_report (PaddingRow, include/pipeplan/simulate.h:92-100). */
+typedef struct pp_padding_row {
+  int32_t method;            /* 0 DpMicrobatch, 1 Packing, 2 NaivePadding (BatchingMethod) */
+  int32_t reserved;
+  int64_t max_seq_len;
+  double padding_eff_input;
+  double padding_eff_target;
+  int64_t tokens;
+  double sim_time;
+  double throughput_proxy;
+} pp_padding_row;
+
+/* padding_vs_packing_report (src/simulate.cpp:288-406, the second production
+ * caller of dp_partition) on the device: per max_seq_len, truncation, the
+ * token-budgeted draw (pp_draw_minibatches), the DP partition of every
+ * mini-batch in one batched call (order_samples(Sort) -> make_slice_cost(grid,
+ * model, ordered, recompute) -> dp_partition with t_max_interval), first-fit
+ * packing and naive padding, and one zero-noise 1F1B simulate() per mini-batch
+ * and method (schedule_1f1b -> plan_communication -> simulate over
+ * OpCostTable::from_shapes at Recompute::None).  rows receives 3 * n_lens rows
+ * in the reference's order (DP, packing, naive per max_seq_len).  model's
+ * recompute field is ignored (the DP uses `recompute`, the simulations None).
+ * Host buffers; errors as the reference (PP_ERR_INVALID for an empty dataset or
+ * token_budget < 1; the DP's own errors). */
+int pp_padding_report(pp_ctx* ctx, const pp_sample* samples, int64_t n, const int64_t* max_seq_lens,
+                      int32_t n_lens, const pp_grid_desc* grid, const pp_model_desc* model,
+                      int64_t token_budget, double t_max_interval, int32_t max_iterations,
+                      int32_t recompute, pp_padding_row* rows);
+
 /* Diagnostics: measured FP64 add issue rate of `device` (adds/s), the
  * roofline denominator of the FP64-bound cost kernels (calib.cu). */
 int pp_calibrate_fp64(int device, double* dadd_per_s);

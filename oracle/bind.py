@@ -191,6 +191,11 @@ class Oracle:
                            ordered=ordered, n_candidates=int(nc[0]), n_evaluated=int(ne[0]))
 
 
+PADDING_ROW = np.dtype([("method", np.int32), ("reserved", np.int32), ("max_seq_len", np.int64),
+                        ("padding_eff_input", np.float64), ("padding_eff_target", np.float64),
+                        ("tokens", np.int64), ("sim_time", np.float64), ("throughput_proxy", np.float64)])
+
+
 class Reference:
     """The unmodified reference planner (compiled from /root/reference)."""
 
@@ -214,6 +219,9 @@ class Reference:
         L.ref_order_search.restype = dbl
         L.ref_load_record_file.argtypes = [C.c_char_p, i64, vp, i64, vp, vp, vp, vp]
         L.ref_draw_all.argtypes = [vp, i64, i64, vp, vp]
+        L.ref_padding_report.argtypes = [vp, i64, vp, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), i64,
+                                         dbl, i32, i32, vp]
+        L.ref_padding_report.restype = dbl
         self.L = L
 
     def order_samples(self, samples):
@@ -279,6 +287,18 @@ class Reference:
         m = np.zeros(1, np.int64)
         rc = self.L.ref_draw_all(_p(s), len(s), budget, _p(off), _p(m))
         return rc, off[:int(m[0]) + 1].copy()
+
+    def padding_report(self, samples, max_seq_lens, grid, model, token_budget=65536, t_max_interval=5.0,
+                       max_iterations=0, recompute=0):
+        """The reference's padding_vs_packing_report -> (seconds, rows (3L, 8) float64 view)."""
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        lens = np.ascontiguousarray(max_seq_lens, np.int64)
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        rows = np.zeros(3 * len(lens), PADDING_ROW)
+        secs = self.L.ref_padding_report(_p(s), len(s), _p(lens), len(lens), C.byref(g), C.byref(m), token_budget,
+                                         t_max_interval, max_iterations, recompute, rows.ctypes.data)
+        return secs, rows
 
     def synthetic_grid_cells(self, params7, tp, mbs_axis=(), seq_axis=()):
         par = np.asarray(params7, np.float64)

@@ -466,4 +466,36 @@ int ref_draw_all(const pp_sample* s, int64_t n, int64_t budget, int64_t* offsets
   }
 }
 
+
+// padding_vs_packing_report (simulate.cpp:288-406) -> 3 * n_lens rows;
+// returns wall seconds (negative: status).
+double ref_padding_report(const pp_sample* s, int64_t n, const int64_t* lens, int32_t n_lens, const pp_grid_desc* g,
+                          const pp_model_desc* m, int64_t token_budget, double interval, int32_t max_iterations,
+                          int32_t recompute, pp_padding_row* rows) {
+  try {
+    ProfileGrid grid = grid_from_desc(g);
+    ModelConfig cfg = model_from_desc(m);
+    std::vector<Sample> v(n);
+    for (int64_t k = 0; k < n; ++k) v[k] = Sample{s[k].id, s[k].input_len, s[k].target_len};
+    PaddingReportOptions opt;
+    opt.token_budget = token_budget;
+    opt.t_max_interval = interval;
+    opt.max_iterations = max_iterations;
+    opt.recompute = static_cast<Recompute>(recompute);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto out = padding_vs_packing_report(v, std::span<const std::int64_t>(lens, n_lens), grid, cfg, opt);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (std::size_t k = 0; k < out.size(); ++k) {
+      const PaddingRow& r = out[k];
+      rows[k] = pp_padding_row{static_cast<int32_t>(r.method), 0, r.max_seq_len, r.padding_eff_input,
+                               r.padding_eff_target, r.tokens, r.sim_time, r.throughput_proxy};
+    }
+    return secs;
+  } catch (const InfeasibleError&) {
+    return -PP_ERR_INFEASIBLE;
+  } catch (const std::invalid_argument&) {
+    return -PP_ERR_INVALID;
+  }
+}
+
 }  // extern "C"

@@ -33,7 +33,13 @@ EXPORTED = [
     "pp_synthetic_grid", "pp_synthetic_dataset", "pp_slice_cost_host", "pp_calibrate_fp64",
     "pp_op_costs", "pp_plan_op_costs_device", "pp_order_search", "pp_order_search_device",
     "pp_load_records", "pp_load_records_device", "pp_draw_minibatches", "pp_draw_minibatches_device",
+    "pp_padding_report",
 ]
+
+
+PADDING_ROW = np.dtype([("method", np.int32), ("reserved", np.int32), ("max_seq_len", np.int64),
+                        ("padding_eff_input", np.float64), ("padding_eff_target", np.float64),
+                        ("tokens", np.int64), ("sim_time", np.float64), ("throughput_proxy", np.float64)])
 
 
 class PlannerError(RuntimeError):
@@ -151,6 +157,8 @@ def _load():
     lib.pp_load_records_device.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp]
     lib.pp_draw_minibatches.argtypes = [vp, vp, i64, i64, vp, vp]
     lib.pp_draw_minibatches_device.argtypes = [vp, vp, i64, i64, vp, vp]
+    lib.pp_padding_report.argtypes = [vp, vp, i64, vp, i32, C.POINTER(GridDesc), C.POINTER(ModelDesc), i64, dbl,
+                                      i32, i32, vp]
     lib.pp_order_search.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, i32, dbl, vp, vp, vp, vp, vp, vp]
     lib.pp_order_search_device.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, dbl, vp, vp, vp, vp,
                                            vp, vp]
@@ -520,6 +528,19 @@ class Planner:
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())
         return int(m[0])
+
+    def padding_report(self, samples, max_seq_lens, grid: "Grid", model: "Model", token_budget: int = 65536,
+                       t_max_interval: float = 5.0, max_iterations: int = 0, recompute: int = 0) -> np.ndarray:
+        """padding_vs_packing_report on the device -> structured rows (3 per max_seq_len)."""
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        lens = np.ascontiguousarray(max_seq_lens, np.int64)
+        rows = np.zeros(3 * len(lens), PADDING_ROW)
+        rc = lib.pp_padding_report(self._h, _p(s) if len(s) else None, len(s), _p(lens), len(lens),
+                                   C.byref(grid.desc()), C.byref(model.desc()), token_budget, t_max_interval,
+                                   max_iterations, recompute, rows.ctypes.data)
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return rows
 
     def order_search(self, t_f, t_b, act_mem, mb_offset, limits, n_clusters: int = 3,
                      comm_latency: float = 0.0) -> dict:

@@ -111,6 +111,16 @@ cudaError_t launch_load_records(const unsigned char* d_bytes, int64_t n, long lo
                                 int64_t* n_lines_out, int64_t* err_line, int32_t* err_kind, int64_t* err_byte,
                                 cudaStream_t st);
 size_t draw_scratch_bytes(int64_t n);
+cudaError_t launch_sim_1f1b(const double* tf, const double* tb, const double* act, const int64_t* mb_off,
+                            int n_seg, int C, double comm_latency, int64_t max_m, char* scratch,
+                            size_t slot_bytes, int warps, void* items, cudaStream_t st);
+cudaError_t launch_truncate(const pp_sample* in, int64_t n, long long max_len, pp_sample* out, cudaStream_t st);
+cudaError_t launch_minibatch_stats(const pp_sample* s, const int64_t* off, int n_seg, long long max_len,
+                                   long long* bins, long long* st6, pp_padded_shape* naive, cudaStream_t st);
+cudaError_t launch_dp_padded(const pp_padded_shape* sh, const int64_t* mb_off, int n_seg, long long* st6,
+                             cudaStream_t st);
+cudaError_t launch_broadcast_rows(const double* tf1, const double* tb1, const double* ac1, int C, int64_t rows,
+                                  double* tf, double* tb, double* ac, cudaStream_t st);
 cudaError_t launch_draw_minibatches(const pp_sample* d_samples, int64_t n, long long budget, char* scratch,
                                     size_t scratch_bytes, int64_t* d_seg_offsets, int64_t* n_seg, cudaStream_t st);
 cudaError_t launch_order_search(const double* tf, const double* tb, const double* act,
@@ -230,6 +240,9 @@ struct pp_ctx {
       os_items, os_istats, os_order, os_ms, os_bub, os_dl, os_ds, os_status;
   // dataset ingest (ingest.cu)
   DevBuf ing_bytes, ing_scratch, ing_out, ing_off;
+  // padding report (report.cu)
+  DevBuf rp_samples, rp_trunc, rp_off, rp_ordered, rp_splits, rp_times, rp_count, rp_tmax, rp_obj, rp_status,
+      rp_err, rp_tf, rp_tb, rp_act, rp_mboff, rp_st6, rp_bins, rp_naive, rp_items, rp_row;
   // host copy of the uploaded grid (restricted to the recompute strategy)
   // for the monotonicity certificate of cost pass A
   std::vector<double> h_ax, h_cells;
@@ -263,6 +276,9 @@ struct pp_ctx {
             &os_tf, &os_tb, &os_act, &os_off, &os_lim, &os_pred, &os_assign, &os_idx, &os_cloff, &os_clk,
             &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status,
             &ing_bytes, &ing_scratch, &ing_out, &ing_off,
+            &rp_samples, &rp_trunc, &rp_off, &rp_ordered, &rp_splits, &rp_times, &rp_count, &rp_tmax, &rp_obj,
+            &rp_status, &rp_err, &rp_tf, &rp_tb, &rp_act, &rp_mboff, &rp_st6, &rp_bins, &rp_naive, &rp_items,
+            &rp_row,
             &hset[0].samples, &hset[0].seg, &hset[0].ordered, &hset[0].order, &hset[0].splits,
             &hset[0].times, &hset[0].count, &hset[0].tmax, &hset[0].obj, &hset[0].status, &hset[0].err,
             &hset[1].samples, &hset[1].seg, &hset[1].ordered, &hset[1].order, &hset[1].splits,
@@ -2200,6 +2216,205 @@ int pp_draw_minibatches(pp_ctx* ctx, const pp_sample* samples, int64_t n, int64_
   else
     seg_offsets[0] = 0;
   PP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PP_OK;
+}
+
+
+// padding_vs_packing_report, one max_seq_len at a time (simulate.cpp:296-403)
+int pp_padding_report(pp_ctx* ctx, const pp_sample* samples, int64_t n, const int64_t* max_seq_lens,
+                      int32_t n_lens, const pp_grid_desc* grid, const pp_model_desc* model,
+                      int64_t token_budget, double t_max_interval, int32_t max_iterations,
+                      int32_t recompute, pp_padding_row* rows) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n < 1 || !samples) return fail(ctx, PP_ERR_INVALID, "padding report needs a non-empty dataset");  // :293
+  if (n_lens < 0 || (n_lens > 0 && (!max_seq_lens || !rows)) || !grid || !model || model->n_stages < 1 ||
+      model->n_stages > 32)
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  cudaStream_t st = ctx->stream;
+  const int C = model->n_stages;
+  PP_CUDA(ctx->rp_samples.ensure(n * sizeof(pp_sample)));
+  PP_CUDA(ctx->rp_trunc.ensure(n * sizeof(pp_sample)));
+  PP_CUDA(ctx->rp_off.ensure((n + 1) * sizeof(int64_t)));
+  PP_CUDA(cudaMemcpyAsync(ctx->rp_samples.p, samples, n * sizeof(pp_sample), cudaMemcpyHostToDevice, st));
+  pp_model_desc dpm = *model;
+  dpm.recompute = recompute;
+  pp_model_desc nm = *model;
+  nm.recompute = 0;  // run_iteration prices with Recompute::None (:279)
+  std::vector<int32_t> pe(C), pd(C);
+  for (int j = 0; j < C; ++j) {  // packing merges both streams into one sequence (:357-364)
+    pe[j] = model->is_encoder_decoder ? 0 : model->encoder_layers[j];
+    pd[j] = model->is_encoder_decoder ? model->decoder_layers[j] + model->encoder_layers[j] : model->decoder_layers[j];
+  }
+  pp_model_desc pm = nm;
+  pm.encoder_layers = pe.data();
+  pm.decoder_layers = pd.data();
+  pm.is_encoder_decoder = 0;
+  const size_t ib = order_search_item_bytes();
+  for (int L = 0; L < n_lens; ++L) {
+    const int64_t max_len = max_seq_lens[L];
+    PP_CUDA(launch_truncate(ctx->rp_samples.as<pp_sample>(), n, max_len, ctx->rp_trunc.as<pp_sample>(), st));
+    int64_t n_seg64 = 0;
+    if ((rc = pp_draw_minibatches_device(ctx, ctx->rp_trunc.as<pp_sample>(), n, token_budget,
+                                         ctx->rp_off.as<int64_t>(), &n_seg64)))
+      return rc;
+    if (max_iterations > 0) n_seg64 = std::min<int64_t>(n_seg64, max_iterations);
+    const int n_seg = (int)n_seg64;
+    std::vector<int64_t> h_off(n_seg + 1);
+    PP_CUDA(cudaMemcpyAsync(h_off.data(), ctx->rp_off.p, (n_seg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(cudaStreamSynchronize(st));
+    const int64_t total = h_off[n_seg];
+    // ---- DP micro-batching of every mini-batch (:310-326) ----
+    PP_CUDA(ctx->rp_ordered.ensure(total * sizeof(pp_sample)));
+    PP_CUDA(ctx->rp_splits.ensure(total * sizeof(int32_t)));
+    PP_CUDA(ctx->rp_times.ensure(total * sizeof(double)));
+    for (DevBuf* b : {&ctx->rp_count, &ctx->rp_status}) PP_CUDA(b->ensure(n_seg * sizeof(int32_t)));
+    for (DevBuf* b : {&ctx->rp_tmax, &ctx->rp_obj}) PP_CUDA(b->ensure(n_seg * sizeof(double)));
+    PP_CUDA(ctx->rp_err.ensure(n_seg * sizeof(int64_t)));
+    pp_plan_out out{};
+    out.ordered = ctx->rp_ordered.as<pp_sample>();
+    out.splits = ctx->rp_splits.as<int32_t>();
+    out.mb_times = ctx->rp_times.as<double>();
+    out.count = ctx->rp_count.as<int32_t>();
+    out.t_max_used = ctx->rp_tmax.as<double>();
+    out.objective = ctx->rp_obj.as<double>();
+    out.status = ctx->rp_status.as<int32_t>();
+    out.err_sample_id = ctx->rp_err.as<int64_t>();
+    const pp_dp_options opts{C, 1, INFINITY, t_max_interval};
+    if ((rc = pp_plan_grid_device(ctx, ctx->rp_trunc.as<pp_sample>(), ctx->rp_off.as<int64_t>(), h_off.data(), n_seg,
+                                  0, grid, &dpm, &opts, &out)))
+      return rc;
+    std::vector<int32_t> stv(n_seg);
+    PP_CUDA(cudaMemcpyAsync(stv.data(), out.status, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(cudaStreamSynchronize(st));
+    for (int q = 0; q < n_seg; ++q)
+      if (stv[q] != PP_OK) return fail(ctx, stv[q], "dp_partition failed on a mini-batch of the report");
+    // op costs of the DP micro-batches at Recompute::None
+    std::vector<int64_t> mbo(n_seg + 1);
+    for (DevBuf* b : {&ctx->rp_tf, &ctx->rp_tb, &ctx->rp_act}) PP_CUDA(b->ensure(std::max<int64_t>(total, 1) * C * sizeof(double)));
+    if ((rc = pp_plan_op_costs_device(ctx, out.ordered, ctx->rp_off.as<int64_t>(), h_off.data(), n_seg, out.splits,
+                                      out.count, grid, &nm, total, mbo.data(), ctx->rp_tf.as<double>(),
+                                      ctx->rp_tb.as<double>(), ctx->rp_act.as<double>())))
+      return rc;
+    PP_CUDA(ctx->rp_st6.ensure((size_t)n_seg * 6 * sizeof(long long)));
+    PP_CUDA(launch_dp_padded(ctx->shapes.as<pp_padded_shape>(), ctx->mb_off.as<int64_t>(), n_seg,
+                             ctx->rp_st6.as<long long>(), st));
+    // ---- packing / naive integer work (:328-379) ----
+    PP_CUDA(ctx->rp_bins.ensure(std::max<int64_t>(total, 1) * sizeof(long long)));
+    PP_CUDA(ctx->rp_naive.ensure(std::max(n_seg, 1) * sizeof(pp_padded_shape)));
+    PP_CUDA(launch_minibatch_stats(ctx->rp_trunc.as<pp_sample>(), ctx->rp_off.as<int64_t>(), n_seg, max_len,
+                                   ctx->rp_bins.as<long long>(), ctx->rp_st6.as<long long>(),
+                                   ctx->rp_naive.as<pp_padded_shape>(), st));
+    std::vector<long long> st6((size_t)n_seg * 6);
+    PP_CUDA(cudaMemcpyAsync(st6.data(), ctx->rp_st6.p, st6.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(cudaStreamSynchronize(st));
+    // ---- the three table sets, each simulated as one 1F1B iteration per mini-batch ----
+    std::vector<int64_t> pko(n_seg + 1, 0), nvo(n_seg + 1);
+    for (int q = 0; q < n_seg; ++q) pko[q + 1] = pko[q] + st6[6 * q + 3];
+    for (int q = 0; q <= n_seg; ++q) nvo[q] = q;
+    const int64_t n_dp = mbo[n_seg], n_pk = pko[n_seg];
+    const int64_t rows_all = n_dp + n_pk + n_seg;
+    PP_CUDA(ctx->rp_row.ensure(((size_t)rows_all * C * 3 + 3 * C) * sizeof(double)));
+    double* pk_tf = ctx->rp_row.as<double>();
+    double* pk_tb = pk_tf + n_pk * C;
+    double* pk_ac = pk_tb + n_pk * C;
+    double* nv_tf = pk_ac + n_pk * C;
+    double* nv_tb = nv_tf + (int64_t)n_seg * C;
+    double* nv_ac = nv_tb + (int64_t)n_seg * C;
+    double* one = nv_ac + (int64_t)n_seg * C;  // the packed micro-batch's row
+    CostGrid g{};
+    std::vector<double> lay(2 * (size_t)C);
+    // naive: one micro-batch per mini-batch under the model (Recompute::None)
+    if ((rc = upload_grid(ctx, grid, &nm, &g))) return rc;
+    for (int j = 0; j < C; ++j) {
+      lay[j] = nm.encoder_layers[j] > 0 ? (double)nm.encoder_layers[j] : 0.0;
+      lay[C + j] = nm.decoder_layers[j] > 0 ? (double)nm.decoder_layers[j] : 0.0;
+    }
+    PP_CUDA(ctx->stage_lay.ensure(lay.size() * sizeof(double)));
+    PP_CUDA(cudaMemcpyAsync(ctx->stage_lay.p, lay.data(), lay.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    PP_CUDA(launch_op_costs(g, ctx->stage_lay.as<double>(), ctx->stage_lay.as<double>() + C, C,
+                            ctx->rp_naive.as<pp_padded_shape>(), n_seg, nv_tf, nv_tb, nv_ac, st));
+    PP_CUDA(cudaStreamSynchronize(st));  // lay is reused below
+    // packing: every bin is {1, max_len, 0} under the merged-stream model
+    if ((rc = upload_grid(ctx, grid, &pm, &g))) return rc;
+    for (int j = 0; j < C; ++j) {
+      lay[j] = pm.encoder_layers[j] > 0 ? (double)pm.encoder_layers[j] : 0.0;
+      lay[C + j] = pm.decoder_layers[j] > 0 ? (double)pm.decoder_layers[j] : 0.0;
+    }
+    const pp_padded_shape pshape{1, max_len, 0};
+    PP_CUDA(ctx->shapes.ensure(sizeof(pp_padded_shape)));
+    PP_CUDA(cudaMemcpyAsync(ctx->stage_lay.p, lay.data(), lay.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    PP_CUDA(cudaMemcpyAsync(ctx->shapes.p, &pshape, sizeof(pshape), cudaMemcpyHostToDevice, st));
+    PP_CUDA(launch_op_costs(g, ctx->stage_lay.as<double>(), ctx->stage_lay.as<double>() + C, C,
+                            ctx->shapes.as<pp_padded_shape>(), 1, one, one + C, one + 2 * C, st));
+    PP_CUDA(launch_broadcast_rows(one, one + C, one + 2 * C, C, n_pk, pk_tf, pk_tb, pk_ac, st));
+    // offsets of the three sets, one device array
+    PP_CUDA(ctx->rp_mboff.ensure(3 * (size_t)(n_seg + 1) * sizeof(int64_t)));
+    int64_t* d_dpo = ctx->rp_mboff.as<int64_t>();
+    int64_t* d_pko = d_dpo + n_seg + 1;
+    int64_t* d_nvo = d_pko + n_seg + 1;
+    PP_CUDA(cudaMemcpyAsync(d_dpo, mbo.data(), (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    PP_CUDA(cudaMemcpyAsync(d_pko, pko.data(), (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    PP_CUDA(cudaMemcpyAsync(d_nvo, nvo.data(), (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    int64_t max_m = 1;
+    for (int q = 0; q < n_seg; ++q) max_m = std::max({max_m, mbo[q + 1] - mbo[q], pko[q + 1] - pko[q]});
+    const size_t slot = order_search_slot_bytes(max_m, C);
+    size_t free_b = 0, total_b = 0;
+    PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const int warps = order_search_warps(n_seg, C, slot, std::min<size_t>(free_b / 2, (size_t)32 << 30));
+    int G = 1;
+    while (G < C) G *= 2;
+    PP_CUDA(ctx->os_scratch.ensure((size_t)warps * (32 / G) * slot));
+    PP_CUDA(ctx->rp_items.ensure(3 * (size_t)std::max(n_seg, 1) * ib));
+    char* items = ctx->rp_items.as<char>();
+    PP_CUDA(launch_sim_1f1b(ctx->rp_tf.as<double>(), ctx->rp_tb.as<double>(), ctx->rp_act.as<double>(), d_dpo, n_seg, C,
+                            0.0, max_m, ctx->os_scratch.as<char>(), slot, warps, items, st));
+    PP_CUDA(launch_sim_1f1b(pk_tf, pk_tb, pk_ac, d_pko, n_seg, C, 0.0, max_m, ctx->os_scratch.as<char>(), slot,
+                            warps, items + (size_t)n_seg * ib, st));
+    PP_CUDA(launch_sim_1f1b(nv_tf, nv_tb, nv_ac, d_nvo, n_seg, C, 0.0, max_m, ctx->os_scratch.as<char>(), slot,
+                            warps, items + 2 * (size_t)n_seg * ib, st));
+    std::vector<char> hi(3 * (size_t)n_seg * ib);
+    PP_CUDA(cudaMemcpyAsync(hi.data(), items, hi.size(), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(cudaStreamSynchronize(st));
+    // accumulate in iteration order (:319-378), emit (:384-403)
+    struct Acc {
+      long long ai = 0, pi = 0, at = 0, pt = 0;
+      double sim = 0.0;
+    } acc[3];
+    for (int q = 0; q < n_seg; ++q) {
+      const long long* v = st6.data() + 6 * q;
+      double ms[3];
+      for (int m = 0; m < 3; ++m) {
+        const char* it = hi.data() + ((size_t)m * n_seg + q) * ib;
+        std::memcpy(&ms[m], it, sizeof(double));
+        int32_t flags = 0;
+        std::memcpy(&flags, it + 2 * sizeof(double), sizeof(int32_t));
+        if ((flags >> 8) & 0xff) return fail(ctx, PP_ERR_NOT_EXECUTABLE, "1F1B plan not executable");
+      }
+      acc[0].ai += v[0]; acc[0].pi += v[4]; acc[0].at += v[1]; acc[0].pt += v[5]; acc[0].sim += ms[0];
+      acc[1].ai += v[2]; acc[1].pi += v[3] * max_len; acc[1].sim += ms[1];
+      acc[2].ai += v[0]; acc[2].at += v[1]; acc[2].sim += ms[2];
+    }
+    // naive padded sums: count * max lengths, from the naive shapes
+    std::vector<pp_padded_shape> nsh(n_seg);
+    PP_CUDA(cudaMemcpyAsync(nsh.data(), ctx->rp_naive.p, n_seg * sizeof(pp_padded_shape), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(cudaStreamSynchronize(st));
+    for (int q = 0; q < n_seg; ++q) {
+      acc[2].pi += nsh[q].mbs * nsh[q].input_len;
+      acc[2].pt += nsh[q].mbs * nsh[q].target_len;
+    }
+    for (int m = 0; m < 3; ++m) {
+      pp_padding_row& r = rows[3 * L + m];
+      r.method = m;
+      r.reserved = 0;
+      r.max_seq_len = max_len;
+      r.padding_eff_input = acc[m].pi == 0 ? 1.0 : (double)acc[m].ai / (double)acc[m].pi;
+      r.padding_eff_target = acc[m].pt == 0 ? 1.0 : (double)acc[m].at / (double)acc[m].pt;
+      r.tokens = acc[m].ai + acc[m].at;
+      r.sim_time = acc[m].sim;
+      r.throughput_proxy = acc[m].sim > 0 ? (double)r.tokens / acc[m].sim : 0.0;
+    }
+  }
   return PP_OK;
 }
 

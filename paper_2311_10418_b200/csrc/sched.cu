@@ -290,6 +290,10 @@ __device__ __forceinline__ void st_cta(double* p, double v) {
   asm volatile("st.relaxed.cta.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+// F1B: the schedule is schedule_1f1b (schedule.cpp:29-53) of table s (one
+// item per table, no clustering): the simulate() makespan of a fixed 1F1B
+// plan, as padding_vs_packing_report's run_iteration needs (simulate.cpp:277-286).
+template <bool F1B>
 __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
     const double* __restrict__ tf, const double* __restrict__ tb, const double* __restrict__ act,
     const int64_t* __restrict__ mb_off, const double* __restrict__ limits, int C, int G, int k, int kfact,
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
   int* rqn = rqn_s[wib] + grp * 2 * G;
   int* perm = perm_s[wib][grp];
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
-  const double lim = j < C ? limits[j] : 0.0;
+  const double lim = (!F1B && j < C) ? limits[j] : 0.0;
   const int64_t n_items = (int64_t)n_seg * kfact;
 
   for (int64_t ib = gw * IPW; ib < n_items; ib += nw * IPW) {
@@ -318,9 +322,14 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
     if (item < n_items) {
       s = (int)(item / kfact);
       r = (int)(item - (int64_t)s * kfact);
-      kk = cl_k[s];
-      kkf = 1;
-      for (int q = 2; q <= kk; ++q) kkf *= q;
+      if (F1B) {
+        kk = mb_off[s + 1] > mb_off[s] ? 1 : 0;
+        kkf = 1;
+      } else {
+        kk = cl_k[s];
+        kkf = 1;
+        for (int q = 2; q <= kk; ++q) kkf *= q;
+      }
     }
     // (kk == 0: no micro-batch or bad input, status set by cluster_kernel)
     const bool valid = item < n_items && kk > 0 && r < kkf;
@@ -334,10 +343,10 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
 
     // injection order = clusters concatenated in permutation order, written
     // straight into device 0's forward queue
-    if (valid && j == 0) nth_perm(r, kk, perm);
+    if (!F1B && valid && j == 0) nth_perm(r, kk, perm);
     __syncwarp();
     bool ident = true;
-    if (valid) {
+    if (!F1B && valid) {
       const int* idx = cl_idx + base;
       const int* off = cl_off + (int64_t)s * (k + 1);
       int pos = 0;
@@ -356,6 +365,20 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
     __syncwarp();
     int err = 0;  // group-uniform
 
+    // ---- phase 1 (1F1B): stage j runs min(C - j, M) warm-up forwards, then
+    // backward b / forward warmup + b, then drains (schedule.cpp:40-49) ----
+    if (F1B) {
+      if (active) {
+        int* ORD = S.ord + (int64_t)j * M2;
+        const int warm = min(C - j, M);
+        int n_ord = 0;
+        for (int i = 0; i < warm; ++i) ORD[n_ord++] = 2 * i;
+        for (int b2 = 0; b2 < M; ++b2) {
+          ORD[n_ord++] = 2 * b2 + 1;
+          if (warm + b2 < M) ORD[n_ord++] = 2 * (warm + b2);
+        }
+      }
+    } else
     // ---- phase 1: schedule_adaptive (schedule.cpp:55-122) ----
     {
       int n_ord = 0, fh = 0, ft = (j == 0) ? M : 0, bh = 0, bt = 0;
@@ -748,7 +771,7 @@ cudaError_t launch_order_search(const double* tf, const double* tb, const double
   int G = 1;
   while (G < C) G *= 2;
   const int blocks = (warps + 3) / 4;
-  perm_eval_kernel<<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, limits, C, G, k, kfact, comm_latency, n_seg,
+  perm_eval_kernel<false><<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, limits, C, G, k, kfact, comm_latency, n_seg,
                                            cl_idx, cl_off, cl_k, scratch, slot_bytes, max_m,
                                            (ItemOut*)items, item_stats);
   order_select_kernel<<<n_seg, 128, 0, st>>>(mb_off, k, kfact, C, cl_idx, cl_off, cl_k, (const ItemOut*)items,
@@ -757,5 +780,20 @@ cudaError_t launch_order_search(const double* tf, const double* tb, const double
 }
 
 size_t order_search_item_bytes() { return sizeof(ItemOut); }
+
+// simulate() makespans of schedule_1f1b over every table (run_iteration,
+// simulate.cpp:277-286): items[s].makespan, zero noise, comm_latency.
+cudaError_t launch_sim_1f1b(const double* tf, const double* tb, const double* act, const int64_t* mb_off,
+                            int n_seg, int C, double comm_latency, int64_t max_m, char* scratch,
+                            size_t slot_bytes, int warps, void* items, cudaStream_t st) {
+  if (n_seg <= 0) return cudaSuccess;
+  int G = 1;
+  while (G < C) G *= 2;
+  const int blocks = (warps + 3) / 4;
+  perm_eval_kernel<true><<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, nullptr, C, G, 1, 1, comm_latency, n_seg,
+                                                 nullptr, nullptr, nullptr, scratch, slot_bytes, max_m,
+                                                 (ItemOut*)items, nullptr);
+  return cudaGetLastError();
+}
 
 }  // namespace ppb
