@@ -578,44 +578,71 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
         bool prog = false;
         if (active && !gdone)
           while (ip < n_ins) {
-            const int w = INS[ip];
-            const int kind = w & 15, mb = w >> 4;
-            if (kind <= kBwd) {
-              const bool fwd = kind == kFwd;
-              const double dur = fwd ? TF[(int64_t)mb * C + j] : TB[(int64_t)mb * C + j];
-              const double a = AC[(int64_t)mb * C + j];
-              clock = __dadd_rn(clock, dur);
-              busy = __dadd_rn(busy, dur);
-              if (fwd) {
-                mem = __dadd_rn(mem, a);
-                peak = peak < mem ? mem : peak;
-              } else {
-                mem = __dsub_rn(mem, a);
-              }
-            } else if (kind <= kRecvGradStart) {
-              int ch, q;
-              if (kind == kSendActStart) { ch = 2 * j; q = n_sa++; }
-              else if (kind == kSendGradStart) { ch = 2 * (j - 1) + 1; q = n_sg++; }
-              else if (kind == kRecvActStart) { ch = 2 * (j - 1); q = n_ra++; }
-              else { ch = 2 * j + 1; q = n_rg++; }
-              const bool send = kind == kSendActStart || kind == kSendGradStart;
-              (send ? S.sq_mb : S.rq_mb)[(int64_t)ch * M + q] = mb;
-              (send ? S.sq_t : S.rq_t)[(int64_t)ch * M + q] = clock;
-            } else {
-              int ch;
-              if (kind == kWaitSendAct) ch = 2 * j;
-              else if (kind == kWaitRecvAct) ch = 2 * (j - 1);
-              else if (kind == kWaitSendGrad) ch = 2 * (j - 1) + 1;
-              else ch = 2 * j + 1;
-              const double c = ld_cta(S.comp + (int64_t)ch * M + mb);
-              if (c != c) break;  // blocked until the transfer lands
-              if (c > clock) {
-                blocked = __dadd_rn(blocked, __dsub_rn(c, clock));
-                clock = c;
+            // a group of up to 4 instructions: their loads (kind, duration,
+            // act_mem, transfer completion) are issued together, then the
+            // group is executed in order (completions do not change during
+            // the advance half of a round, so the early loads see the same
+            // values the one-by-one walk would)
+            constexpr int kG = 4;
+            const int ng = min(kG, n_ins - ip);
+            int wk[kG];
+            double v0[kG], v1[kG];
+#pragma unroll
+            for (int q = 0; q < kG; ++q) wk[q] = q < ng ? INS[ip + q] : 0;
+#pragma unroll
+            for (int q = 0; q < kG; ++q) {
+              const int kind = wk[q] & 15, mb = wk[q] >> 4;
+              v0[q] = 0.0;
+              v1[q] = 0.0;
+              if (q < ng) {
+                if (kind <= kBwd) {
+                  v0[q] = (kind == kFwd ? TF : TB)[(int64_t)mb * C + j];
+                  v1[q] = AC[(int64_t)mb * C + j];
+                } else if (kind >= kWaitSendAct) {
+                  const int ch = kind == kWaitSendAct ? 2 * j
+                                 : kind == kWaitRecvAct ? 2 * (j - 1)
+                                 : kind == kWaitSendGrad ? 2 * (j - 1) + 1
+                                                         : 2 * j + 1;
+                  v0[q] = ld_cta(S.comp + (int64_t)ch * M + mb);
+                }
               }
             }
-            ++ip;
-            prog = true;
+            bool stop = false;
+#pragma unroll
+            for (int q = 0; q < kG; ++q) {
+              if (q >= ng || stop) break;
+              const int kind = wk[q] & 15, mb = wk[q] >> 4;
+              if (kind <= kBwd) {
+                const double dur = v0[q], a = v1[q];
+                clock = __dadd_rn(clock, dur);
+                busy = __dadd_rn(busy, dur);
+                if (kind == kFwd) {
+                  mem = __dadd_rn(mem, a);
+                  peak = peak < mem ? mem : peak;
+                } else {
+                  mem = __dsub_rn(mem, a);
+                }
+              } else if (kind <= kRecvGradStart) {
+                int ch, qq;
+                if (kind == kSendActStart) { ch = 2 * j; qq = n_sa++; }
+                else if (kind == kSendGradStart) { ch = 2 * (j - 1) + 1; qq = n_sg++; }
+                else if (kind == kRecvActStart) { ch = 2 * (j - 1); qq = n_ra++; }
+                else { ch = 2 * j + 1; qq = n_rg++; }
+                const bool send = kind == kSendActStart || kind == kSendGradStart;
+                (send ? S.sq_mb : S.rq_mb)[(int64_t)ch * M + qq] = mb;
+                (send ? S.sq_t : S.rq_t)[(int64_t)ch * M + qq] = clock;
+              } else {
+                const double c = v0[q];
+                if (c != c) { stop = true; break; }  // blocked until the transfer lands
+                if (c > clock) {
+                  blocked = __dadd_rn(blocked, __dsub_rn(c, clock));
+                  clock = c;
+                }
+              }
+              ++ip;
+              prog = true;
+            }
+            if (stop) break;
           }
         // publish queue lengths, then resolve channels (lane l owns link l)
         if (active && !gdone) {
