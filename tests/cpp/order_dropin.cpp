@@ -19,6 +19,7 @@
 
 #include "pipeplan/comm_plan.h"
 #include "pipeplan/order_search.h"
+#include "pipeplan/padding_report.h"
 #include "pipeplan/planner.h"
 #include "pipeplan/schedule.h"
 #include "pipeplan/simulate.h"
@@ -135,7 +136,39 @@ int main() {
       }
     }
   }
-  // 3. errors: the reference's exception types
+  // 3. padding_vs_packing_report: every row byte-identical
+  int report_rows = 0;
+  for (bool encdec : {false, true}) {
+    ModelConfig cfg = ModelConfig::uniform(encdec ? 4 : 2, 2, 1024, encdec);
+    DatasetSpec spec;
+    spec.synthetic = SyntheticSpec{};
+    spec.synthetic->n = 3000;
+    if (encdec) spec.synthetic->target = LengthDistribution{LengthFamily::Lognormal, 3.5, 1.2, 1, 1, 0.8};
+    spec.max_seq_len = 16384;
+    spec.seed = 31;
+    auto samples = load_dataset(spec);
+    const std::vector<std::int64_t> lens = {512, 4096};
+    PaddingReportOptions ro;
+    ro.token_budget = 32768;
+    ro.t_max_interval = 200.0;
+    ro.max_iterations = 10;
+    b200::PaddingReportOptions bo;
+    bo.token_budget = ro.token_budget;
+    bo.t_max_interval = ro.t_max_interval;
+    bo.max_iterations = ro.max_iterations;
+    const auto ref_rows = padding_vs_packing_report(samples, lens, grid, cfg, ro);
+    const auto got = b200::padding_vs_packing_report(samples, lens, grid, cfg, bo);
+    check(got.size() == ref_rows.size(), "report row count", report_rows);
+    for (std::size_t k = 0; k < std::min(got.size(), ref_rows.size()); ++k, ++report_rows) {
+      const auto& a = got[k];
+      const auto& b = ref_rows[k];
+      check(static_cast<int>(a.method) == static_cast<int>(b.method) && a.max_seq_len == b.max_seq_len &&
+                same(a.padding_eff_input, b.padding_eff_input) && same(a.padding_eff_target, b.padding_eff_target) &&
+                a.tokens == b.tokens && same(a.sim_time, b.sim_time) && same(a.throughput_proxy, b.throughput_proxy),
+            "padding report row", report_rows);
+    }
+  }
+  // 4. errors: the reference's exception types
   bool threw = false;
   try {
     OpCostTable c = OpCostTable::uniform(4, 2, 1.0, 2.0, 5.0);
@@ -145,7 +178,8 @@ int main() {
     threw = std::strstr(e.what(), "converge") != nullptr;
   }
   check(threw, "non-convergence logic_error", -1);
-  std::printf("order dropin: %d random tables, %d planner replicas, %d mismatches\n", cases, planned, failures);
+  std::printf("order dropin: %d random tables, %d planner replicas, %d report rows, %d mismatches\n", cases,
+              planned, report_rows, failures);
   if (failures == 0 && planned > 0) std::printf("order dropin: OK\n");
   return failures == 0 && planned > 0 ? 0 : 1;
 }
