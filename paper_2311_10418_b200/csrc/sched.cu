@@ -441,21 +441,51 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
         bool prog = false;
         if (active && !gdone)
           while (p < M2) {
-            const int o = ORD[p];
-            const int mb = o >> 1;
-            const bool bwd = o & 1;
-            double ready;
-            if (!bwd) ready = j == 0 ? -INF : ld_cta(S.fend + (int64_t)mb * C + j - 1);
-            else ready = j == C - 1 ? ld_cta(S.fend + (int64_t)mb * C + j) : ld_cta(S.bend + (int64_t)mb * C + j + 1);
-            if (ready != ready) break;
-            const double start = dev_free < ready ? ready : dev_free;  // std::max(dev_free, ready)
-            const double end = __dadd_rn(start, bwd ? TB[(int64_t)mb * C + j] : TF[(int64_t)mb * C + j]);
-            ST[p] = start;
-            EN[p] = end;
-            st_cta((bwd ? S.bend : S.fend) + (int64_t)mb * C + j, end);
-            dev_free = end;
-            ++p;
-            prog = true;
+            // four ops at a time: their orders, producer ends and durations are
+            // loaded together; an end still NaN when loaded is re-read when its
+            // op is reached (it may have been written since, e.g. by this lane)
+            constexpr int kG = 4;
+            const int ng = min(kG, M2 - p);
+            int og[kG];
+            double rd[kG], du[kG];
+#pragma unroll
+            for (int q = 0; q < kG; ++q) og[q] = q < ng ? ORD[p + q] : 0;
+            auto ready_ptr = [&](int o) -> const double* {
+              const int mb = o >> 1;
+              if (!(o & 1)) return j == 0 ? nullptr : S.fend + (int64_t)mb * C + j - 1;
+              return j == C - 1 ? S.fend + (int64_t)mb * C + j : S.bend + (int64_t)mb * C + j + 1;
+            };
+#pragma unroll
+            for (int q = 0; q < kG; ++q) {
+              rd[q] = -INF;
+              du[q] = 0.0;
+              if (q < ng) {
+                const double* rp = ready_ptr(og[q]);
+                if (rp) rd[q] = ld_cta(rp);
+                const int mb = og[q] >> 1;
+                du[q] = (og[q] & 1) ? TB[(int64_t)mb * C + j] : TF[(int64_t)mb * C + j];
+              }
+            }
+            bool stop = false;
+#pragma unroll
+            for (int q = 0; q < kG; ++q) {
+              if (q >= ng || stop) break;
+              const int o = og[q];
+              const int mb = o >> 1;
+              const bool bwd = o & 1;
+              double ready = rd[q];
+              if (ready != ready) ready = ld_cta(ready_ptr(o));
+              if (ready != ready) { stop = true; break; }
+              const double start = dev_free < ready ? ready : dev_free;  // std::max(dev_free, ready)
+              const double end = __dadd_rn(start, du[q]);
+              ST[p] = start;
+              EN[p] = end;
+              st_cta((bwd ? S.bend : S.fend) + (int64_t)mb * C + j, end);
+              dev_free = end;
+              ++p;
+              prog = true;
+            }
+            if (stop) break;
           }
         __syncwarp();
         const unsigned pend = __ballot_sync(kFull, active && !gdone && p != M2) & gmask;
