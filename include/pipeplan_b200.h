@@ -180,6 +180,8 @@ typedef struct pp_stats {
   int64_t slices_pass_b;          /* memory-feasible band slices priced by cost pass B */
   int64_t bound_transitions;      /* DP transitions of the bound pass (t = +inf)       */
   int64_t band_bytes;             /* band written by cost pass B (32-row tiles, 8 B/entry) */
+  int64_t candidates_ref_evaluated; /* sum over segments of the candidates the reference's
+                                       loop visits before its break (microbatch.cpp:289-292) */
 } pp_stats;
 
 typedef struct pp_ctx pp_ctx;
@@ -210,6 +212,19 @@ int pp_plan_grid_device(pp_ctx* ctx, const pp_sample* d_samples, const int64_t* 
                         const int64_t* h_seg_offsets, int32_t n_seg, int32_t presorted,
                         const pp_grid_desc* grid, const pp_model_desc* model,
                         const pp_dp_options* opts, pp_plan_out* d_out);
+
+/* Fixed-size plan slots of n_seg planned mini-batches (pp_plan_grid_device
+ * outputs, DEVICE pointers) for the multi-GPU epoch gather that replaces the
+ * per-thread results of run_plan's pool (driver.cpp:222-242).  Slot s =
+ * d_slots[s * words ..], words = 4 + ceil(n_max / 2) * (d_order ? 2 : 1):
+ * [0] count [1] status [2] t_max_used bits [3] objective bits, then the
+ * splits as packed int32, then (d_order non-NULL) the ordering as packed
+ * int32 per-segment sample indices (micro-batch k = samples order[splits[k-1]
+ * .. splits[k]), i.e. make_micro_batch's sample_ids, microbatch.cpp:122-134).
+ * Enqueued on the ctx stream. */
+int pp_pack_plan_slots(pp_ctx* ctx, const int32_t* d_count, const int32_t* d_status, const double* d_t_max_used,
+                       const double* d_objective, const int32_t* d_splits, const int32_t* d_order,
+                       const int64_t* d_seg_offsets, int32_t n_seg, int32_t n_max, int64_t* d_slots);
 
 /* dp_partition over host-evaluated triangular slice tables: row i holds
  * slices [i, j) for j in (i, n] at index row_offset(i) + (j - i - 1)
@@ -345,6 +360,11 @@ int pp_calibrate_fp64(int device, double* dadd_per_s);
 /* eval_objective (microbatch.cpp:109-120) */
 int pp_eval_objective(const double* times, int64_t m, int32_t stage_count, int32_t replica_count,
                       double* out);
+/* dp_partition's tail (microbatch.cpp:337-348): replica_assignment of the m
+ * planned micro-batches (balance_replicas when m >= replica_count, else
+ * micro-batch k -> replica k) and max_replica_load, from their times. */
+int pp_assign_replicas(const double* times, int64_t m, int32_t replica_count, int32_t* replica,
+                       double* max_load);
 /* ProfileGrid::synthetic (cost_model.cpp:91-124).  params = {alpha, beta, gamma,
  * full_mem_factor, selective_mem_factor, full_tb_penalty, selective_tb_penalty};
  * empty axes (n = 0) select the defaults.  out_mbs/out_seq need 64 entries,

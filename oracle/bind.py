@@ -102,6 +102,8 @@ class Oracle:
         L.orc_dp_tables.argtypes = [vp, vp, i64, C.POINTER(_Opts), vp, vp, vp, vp, vp, vp, vp, vp]
         L.orc_plan_grid.argtypes = [vp, i64, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc),
                                     C.POINTER(_Opts), vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_plan_grid_stream.argtypes = [vp, i64, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc),
+                                           C.POINTER(_Opts), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.orc_eval_objective.argtypes = [vp, i64, i32, i32, vp]
         L.orc_slice_extrema.argtypes = [vp, i64, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), dbl,
                                         vp, vp]
@@ -190,6 +192,45 @@ class Oracle:
         return CheckerPlan(PP_OK, sp[:k].copy(), tt[:k].copy(), float(tm[0]), float(ob[0]),
                            ordered=ordered, n_candidates=int(nc[0]), n_evaluated=int(ne[0]))
 
+    def plan_stream(self, samples, grid, model, stage_count, replica_count=1, mem_cap=math.inf,
+                    t_max_interval=5.0, presorted=False, threads=None):
+        """The streaming restatement (pp_stream.c): same record as plan(), no
+        O(n^2) tables, `threads` OpenMP threads (default: all cores)."""
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        n = len(s)
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        o = _Opts(stage_count, replica_count, mem_cap, t_max_interval)
+        ordered = np.empty_like(s)
+        sp = np.zeros(max(n, 1), np.int32)
+        tt = np.zeros(max(n, 1))
+        cnt = np.zeros(1, np.int32)
+        tm, ob = np.zeros(1), np.zeros(1)
+        err = np.full(1, -1, np.int64)
+        nc = np.zeros(1, np.int64)
+        ne = np.zeros(1, np.int64)
+        rc = self.L.orc_plan_grid_stream(_p(s), n, int(presorted), C.byref(g), C.byref(m), C.byref(o),
+                                         int(threads or os.cpu_count() or 1), _p(ordered), _p(sp), _p(tt),
+                                         _p(cnt), _p(tm), _p(ob), _p(err), _p(nc), _p(ne))
+        if rc != PP_OK:
+            return CheckerPlan(rc, err_sample_id=int(err[0]), ordered=ordered)
+        k = int(cnt[0])
+        return CheckerPlan(PP_OK, sp[:k].copy(), tt[:k].copy(), float(tm[0]), float(ob[0]),
+                           ordered=ordered, n_candidates=int(nc[0]), n_evaluated=int(ne[0]))
+
+
+class RefGrid:
+    """A grid built by the reference (fields as grid_desc reads them)."""
+
+    def __init__(self, mbs_axis, seq_axis, cells):
+        self.mbs_axis, self.seq_axis, self.cells = mbs_axis, seq_axis, cells
+
+
+class RefModel:
+    def __init__(self, enc, dec, encdec, recompute):
+        self.encoder_layers, self.decoder_layers = enc, dec
+        self.is_encoder_decoder, self.recompute = encdec, recompute
+
 
 PADDING_ROW = np.dtype([("method", np.int32), ("reserved", np.int32), ("max_seq_len", np.int64),
                         ("padding_eff_input", np.float64), ("padding_eff_target", np.float64),
@@ -208,12 +249,17 @@ class Reference:
         L.ref_per_layer.argtypes = [C.POINTER(_GridDesc), i32, i32, dbl, dbl, vp]
         L.ref_synthetic_grid.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp]
         L.ref_load_dataset.argtypes = [i64, vp, vp, i64, C.c_uint64, vp]
+        L.ref_model_uniform.argtypes = [i32, i32, i64, i32, vp, vp]
+        L.ref_default_grid_params.argtypes = [vp, vp]
         L.ref_plan_grid.argtypes = [vp, i64, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc),
                                     C.POINTER(_Opts), vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.ref_plan_tables.argtypes = [vp, vp, i64, C.POINTER(_Opts), vp, vp, vp, vp, vp, vp, vp, vp]
         L.ref_plan_batch.argtypes = [vp, vp, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc),
                                      C.POINTER(_Opts), i32, vp, vp, vp, vp]
         L.ref_plan_batch.restype = dbl
+        L.ref_plan_batch_out.argtypes = [vp, vp, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc),
+                                         C.POINTER(_Opts), i32, vp, vp, vp, vp, vp, vp, vp]
+        L.ref_plan_batch_out.restype = dbl
         L.ref_op_costs.argtypes = [vp, i64, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), vp, vp, vp]
         L.ref_order_search.argtypes = [vp, vp, vp, vp, i32, i32, vp, i32, dbl, i32, vp, vp, vp, vp, vp, vp]
         L.ref_order_search.restype = dbl
@@ -314,6 +360,26 @@ class Reference:
         nm, ns = int(sizes[0]), int(sizes[1])
         return om[:nm].copy(), os_[:ns].copy(), cells[:18 * nm * ns].reshape(2, 3, nm, ns, 3).copy()
 
+    def default_grid(self):
+        """ProfileGrid::synthetic(SyntheticGridParams{}) with the default
+        axes, built by the reference itself."""
+        par = np.zeros(7)
+        tp = np.zeros(1, np.int32)
+        self.L.ref_default_grid_params(_p(par), _p(tp))
+        mb, sq, cells = self.synthetic_grid_cells(par, int(tp[0]))
+        return RefGrid(mb, sq, cells)
+
+    def model_uniform(self, n_stages, layers_per_stage, encoder_decoder, recompute=0, hidden_dim=1024):
+        """ModelConfig::uniform (cost_model.cpp:273-292) + the Recompute
+        make_slice_cost is called with."""
+        enc = np.zeros(n_stages, np.int32)
+        dec = np.zeros(n_stages, np.int32)
+        rc = self.L.ref_model_uniform(n_stages, layers_per_stage, hidden_dim, int(encoder_decoder), _p(enc),
+                                      _p(dec))
+        if rc != PP_OK:
+            raise ValueError("invalid model")
+        return RefModel(enc, dec, bool(encoder_decoder), int(recompute))
+
     def load_dataset(self, n, max_seq_len, seed, input_dist, target_dist=None):
         out = np.zeros((n, 3), np.int64)
         ind = np.asarray(input_dist, np.float64)
@@ -379,3 +445,24 @@ class Reference:
         secs = self.L.ref_plan_batch(_p(s), _p(off), S, C.byref(g), C.byref(m), C.byref(o), threads,
                                      _p(tm), _p(ob), _p(cnt), _p(st))
         return secs, tm, ob, cnt, st
+
+    def plan_batch_full(self, samples, seg_offsets, grid, model, stage_count, replica_count=1,
+                        mem_cap=math.inf, t_max_interval=5.0, threads=1):
+        """plan_batch_timed that also returns every plan: dict of flat
+        arrays indexed like the device's pp_plan_out (splits / mb_times /
+        ordered_ids at each segment's sample offset) + 'seconds' (the
+        planning wall time only)."""
+        s = np.ascontiguousarray(samples, np.int64).reshape(-1, 3)
+        off = np.ascontiguousarray(seg_offsets, np.int64)
+        S = len(off) - 1
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        o = _Opts(stage_count, replica_count, mem_cap, t_max_interval)
+        r = {"t_max_used": np.zeros(S), "objective": np.zeros(S), "count": np.zeros(S, np.int32),
+             "status": np.zeros(S, np.int32), "splits": np.zeros(len(s), np.int32),
+             "mb_times": np.zeros(len(s)), "ordered_ids": np.zeros(len(s), np.int64)}
+        r["seconds"] = self.L.ref_plan_batch_out(
+            _p(s), _p(off), S, C.byref(g), C.byref(m), C.byref(o), threads, _p(r["t_max_used"]),
+            _p(r["objective"]), _p(r["count"]), _p(r["status"]), _p(r["splits"]), _p(r["mb_times"]),
+            _p(r["ordered_ids"]))
+        return r

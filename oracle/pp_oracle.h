@@ -37,6 +37,13 @@ int orc_plan_grid(const pp_sample* samples, int64_t n, int32_t presorted, const 
                   int64_t* n_evaluated);
 int orc_slice_extrema(const pp_sample* ordered, int64_t n, const pp_grid_desc* g,
                       const pp_model_desc* m, double cap, double* t_capmax, double* single_act_max);
+/* Streaming restatement (pp_stream.c): no O(n^2) tables, slices priced on the
+ * fly, `threads` OpenMP threads.  Same outputs as orc_plan_grid. */
+int orc_plan_grid_stream(const pp_sample* samples, int64_t n, int32_t presorted, const pp_grid_desc* g,
+                         const pp_model_desc* m, const pp_dp_options* o, int32_t threads,
+                         pp_sample* ordered, int32_t* splits, double* mb_times, int32_t* count,
+                         double* t_max_used, double* objective, int64_t* err_sample_id,
+                         int64_t* n_candidates, int64_t* n_evaluated);
 int orc_eval_objective(const double* times, int64_t m, int32_t c, int32_t d, double* out);
 
 #ifdef __cplusplus

@@ -186,6 +186,36 @@ int ref_synthetic_grid(const double* params8, int32_t tp_degree, const int64_t* 
 
 // load_dataset with a synthetic descriptor (workload.cpp:50-63,109-127).
 // dist = {family, log_mean, log_sigma, uniform_lo, uniform_hi, lognormal_weight}
+// The reference's SyntheticGridParams{} defaults (cost_model.h), in
+// ref_synthetic_grid's parameter order.
+int ref_default_grid_params(double* params7, int32_t* tp_degree) {
+  const SyntheticGridParams p{};
+  params7[0] = p.alpha;
+  params7[1] = p.beta;
+  params7[2] = p.gamma;
+  params7[3] = p.full_mem_factor;
+  params7[4] = p.selective_mem_factor;
+  params7[5] = p.full_tb_penalty;
+  params7[6] = p.selective_tb_penalty;
+  *tp_degree = p.tp_degree;
+  return PP_OK;
+}
+
+// ModelConfig::uniform (cost_model.cpp:273-292): per-stage layer counts.
+int ref_model_uniform(int32_t n_stages, int32_t layers_per_stage, int64_t hidden_dim, int32_t encdec,
+                      int32_t* enc_out, int32_t* dec_out) {
+  try {
+    ModelConfig c = ModelConfig::uniform(n_stages, layers_per_stage, hidden_dim, encdec != 0);
+    for (std::size_t s = 0; s < c.stages.size(); ++s) {
+      enc_out[s] = c.stages[s].encoder_layers;
+      dec_out[s] = c.stages[s].decoder_layers;
+    }
+    return PP_OK;
+  } catch (const std::invalid_argument&) {
+    return PP_ERR_INVALID;
+  }
+}
+
 int ref_load_dataset(int64_t n, const double* in_dist, const double* tgt_dist, int64_t max_seq_len,
                      uint64_t seed, pp_sample* out) {
   try {
@@ -281,14 +311,21 @@ int ref_plan_tables(const double* T, const double* M, int64_t n, const pp_dp_opt
 // driver.cpp:222-242): `threads` std::threads pull mini-batch indices from an
 // atomic counter; each runs order_samples(Sort) + make_slice_cost +
 // dp_partition.  Returns wall seconds; per-segment t_max/objective/count out.
-double ref_plan_batch(const pp_sample* samples, const int64_t* seg_off, int32_t n_seg,
-                      const pp_grid_desc* g, const pp_model_desc* m, const pp_dp_options* o,
-                      int32_t threads, double* t_max_used, double* objective, int32_t* count,
-                      int32_t* status) {
+// run_plan's worker pool (driver.cpp:222-242) over n_seg mini-batches; the
+// returned wall time covers order_samples + make_slice_cost + dp_partition
+// only.  Optional (nullable) outputs, written AFTER the timed region, indexed
+// by sample like the device's pp_plan_out: splits and slice times at the
+// segment's offset, the ordered sample ids.
+double ref_plan_batch_out(const pp_sample* samples, const int64_t* seg_off, int32_t n_seg,
+                          const pp_grid_desc* g, const pp_model_desc* m, const pp_dp_options* o,
+                          int32_t threads, double* t_max_used, double* objective, int32_t* count,
+                          int32_t* status, int32_t* splits, double* mb_times, int64_t* ordered_ids) {
   ProfileGrid grid = grid_from_desc(g);
   ModelConfig cfg = model_from_desc(m);
   const Recompute r = static_cast<Recompute>(m->recompute);
   const DpOptions opt = opts_from_desc(o);
+  const bool keep = splits || mb_times || ordered_ids;
+  std::vector<PlanResult> kept(keep ? static_cast<std::size_t>(n_seg) : 0);
   std::atomic<int> next{0};
   auto t0 = std::chrono::steady_clock::now();
   auto work = [&]() {
@@ -304,6 +341,7 @@ double ref_plan_batch(const pp_sample* samples, const int64_t* seg_off, int32_t 
         objective[s] = res.part.objective_value;
         count[s] = static_cast<int32_t>(res.part.micro_batches.size());
       }
+      if (keep) kept[static_cast<std::size_t>(s)] = std::move(res);
     }
   };
   const int nt = threads < 1 ? 1 : threads;
@@ -314,7 +352,32 @@ double ref_plan_batch(const pp_sample* samples, const int64_t* seg_off, int32_t 
     for (int t = 0; t < nt; ++t) pool.emplace_back(work);
     for (auto& th : pool) th.join();
   }
-  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  for (int s = 0; keep && s < n_seg; ++s) {
+    const PlanResult& res = kept[static_cast<std::size_t>(s)];
+    if (res.status != PP_OK) continue;
+    const int64_t b0 = seg_off[s];
+    SliceCostFn cost = make_slice_cost(grid, cfg, res.ordered, r);
+    std::size_t b = 0, k = 0;
+    for (const auto& mb : res.part.micro_batches) {
+      const std::size_t e = b + mb.sample_ids.size();
+      if (splits) splits[b0 + static_cast<int64_t>(k)] = static_cast<int32_t>(e);
+      if (mb_times) mb_times[b0 + static_cast<int64_t>(k)] = cost(b, e).time;
+      b = e;
+      ++k;
+    }
+    if (ordered_ids)
+      for (std::size_t q = 0; q < res.ordered.size(); ++q) ordered_ids[b0 + static_cast<int64_t>(q)] = res.ordered[q].id;
+  }
+  return secs;
+}
+
+double ref_plan_batch(const pp_sample* samples, const int64_t* seg_off, int32_t n_seg,
+                      const pp_grid_desc* g, const pp_model_desc* m, const pp_dp_options* o,
+                      int32_t threads, double* t_max_used, double* objective, int32_t* count,
+                      int32_t* status) {
+  return ref_plan_batch_out(samples, seg_off, n_seg, g, m, o, threads, t_max_used, objective, count, status,
+                            nullptr, nullptr, nullptr);
 }
 
 

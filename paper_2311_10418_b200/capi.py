@@ -33,7 +33,7 @@ EXPORTED = [
     "pp_synthetic_grid", "pp_synthetic_dataset", "pp_slice_cost_host", "pp_calibrate_fp64",
     "pp_op_costs", "pp_plan_op_costs_device", "pp_order_search", "pp_order_search_device",
     "pp_load_records", "pp_load_records_device", "pp_draw_minibatches", "pp_draw_minibatches_device",
-    "pp_padding_report",
+    "pp_padding_report", "pp_assign_replicas", "pp_pack_plan_slots",
 ]
 
 
@@ -113,7 +113,8 @@ class Stats(C.Structure):
                 ("ms_kernel", C.c_double * 8), ("launches", C.c_int64 * 8),
                 ("dp_band_bytes", C.c_int64), ("slices_pass_a", C.c_int64),
                 ("exit_thresh", C.c_double), ("slices_pass_b", C.c_int64),
-                ("bound_transitions", C.c_int64), ("band_bytes", C.c_int64)]
+                ("bound_transitions", C.c_int64), ("band_bytes", C.c_int64),
+                ("candidates_ref_evaluated", C.c_int64)]
 
     def as_dict(self):
         out = {}
@@ -146,6 +147,8 @@ def _load():
     lib.pp_candidate_range.argtypes = [vp, vp, vp, i32, i32, C.POINTER(GridDesc),
                                        C.POINTER(ModelDesc), dbl, vp, vp]
     lib.pp_eval_objective.argtypes = [vp, i64, i32, i32, vp]
+    lib.pp_assign_replicas.argtypes = [vp, i64, i32, vp, vp]
+    lib.pp_pack_plan_slots.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]
     lib.pp_synthetic_grid.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp]
     lib.pp_synthetic_dataset.argtypes = [i64, vp, vp, i64, C.c_uint64, vp]
     lib.pp_slice_cost_host.argtypes = [C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, i64, i64, vp, vp]
@@ -279,6 +282,18 @@ def calibrate_fp64(device: int = 0) -> float:
     return out.value
 
 
+def assign_replicas(times, replica_count: int):
+    """dp_partition's tail (microbatch.cpp:337-348) on the planned times:
+    (replica per micro-batch, max_replica_load)."""
+    t = np.ascontiguousarray(times, np.float64)
+    rep = np.zeros(max(len(t), 1), np.int32)
+    ml = np.zeros(1)
+    rc = lib.pp_assign_replicas(_p(t), len(t), replica_count, _p(rep), _p(ml))
+    if rc != PP_OK:
+        raise InvalidArgument("replica assignment needs at least one micro-batch and replica_count >= 1")
+    return rep[:len(t)].copy(), float(ml[0])
+
+
 def eval_objective(times, stage_count: int, replica_count: int) -> float:
     t = np.ascontiguousarray(times, np.float64)
     out = np.zeros(1)
@@ -298,6 +313,14 @@ class Plan:
     objective: float = math.nan
     err_sample_id: int = -1
     ordered: np.ndarray | None = None
+    # dp_partition's tail (microbatch.cpp:337-348): replica_assignment and
+    # max_replica_load (pp_assign_replicas)
+    replica: np.ndarray | None = None
+    max_load: float = math.nan
+    # the candidate loop's counters: |unique candidates| and the candidates
+    # the reference's loop visits before its break (pp_stats)
+    n_candidates: int = -1
+    n_evaluated: int = -1
 
 
 def _raise_status(status: int, err_id: int, msg: str = ""):
@@ -420,6 +443,21 @@ class Planner:
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())
 
+    def pack_slots_device(self, d_out: dict, d_seg_offsets, n_seg: int, n_max: int, d_slots,
+                          with_order: bool = True) -> None:
+        """pp_pack_plan_slots: the device plan outputs (pp_plan_out field
+        names -> torch tensors) -> fixed-size int64 slots (d_slots, a torch
+        tensor of n_seg x slot words), on the planner's stream."""
+        vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        order = d_out.get("order") if with_order else None
+        if with_order and order is None:
+            raise InvalidArgument("with_order needs the 'order' output")
+        rc = lib.pp_pack_plan_slots(self._h, vp(d_out["count"]), vp(d_out["status"]), vp(d_out["t_max_used"]),
+                                    vp(d_out["objective"]), vp(d_out["splits"]), vp(order), vp(d_seg_offsets),
+                                    n_seg, n_max, vp(d_slots))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+
     def plan(self, samples: np.ndarray, grid: Grid, model: Model, stage_count: int,
              replica_count: int = 1, mem_cap: float = math.inf, t_max_interval: float = 5.0,
              presorted: bool = False) -> Plan:
@@ -431,8 +469,12 @@ class Planner:
         if st != PP_OK:
             _raise_status(st, int(r["err_sample_id"][0]), self._err())
         m = int(r["count"][0])
-        return Plan(st, r["splits"][:m].copy(), r["mb_times"][:m].copy(), float(r["t_max_used"][0]),
-                    float(r["objective"][0]), -1, r["ordered"])
+        times = r["mb_times"][:m].copy()
+        rep, ml = assign_replicas(times, replica_count)
+        st_ = self.stats()
+        return Plan(st, r["splits"][:m].copy(), times, float(r["t_max_used"][0]),
+                    float(r["objective"][0]), -1, r["ordered"], rep, ml,
+                    int(st_["candidates_generated"]), int(st_["candidates_ref_evaluated"]))
 
     def plan_tables(self, T: np.ndarray, M: np.ndarray, n: int, stage_count: int,
                     replica_count: int = 1, mem_cap: float = math.inf,
@@ -452,7 +494,10 @@ class Planner:
         if rc != PP_OK:
             _raise_status(rc, int(err[0]), self._err())
         m = int(cnt[0])
-        return Plan(PP_OK, splits[:m].copy(), times[:m].copy(), float(tm[0]), float(ob[0]))
+        rep, ml = assign_replicas(times[:m], replica_count)
+        st_ = self.stats()
+        return Plan(PP_OK, splits[:m].copy(), times[:m].copy(), float(tm[0]), float(ob[0]), -1, None, rep, ml,
+                    int(st_["candidates_generated"]), int(st_["candidates_ref_evaluated"]))
 
     def op_costs(self, shapes, grid: Grid, model: Model):
         """OpCostTable::from_shapes: (t_f, t_b, act_mem), each (n, n_stages);

@@ -131,6 +131,10 @@ cudaError_t launch_order_search(const double* tf, const double* tb, const double
                                 int* order, double* makespan, double* bubble, int* deadlock,
                                 double* dev_stats, int* status, cudaStream_t st);
 int dp_coop_grid(int device);
+cudaError_t launch_pack_slots(const int32_t* count, const int32_t* status, const double* tmax,
+                              const double* obj, const int32_t* splits, const int32_t* order,
+                              const int64_t* seg_off, int n_seg, int n_max, long long* slots,
+                              cudaStream_t st);
 cudaError_t launch_dp_coop(int mode, int sanitize, const WorkItem& it, int grid, const int64_t* seg_off,
                            const int* blk_base, const int* blk_W, const int64_t* tile_off,
                            const int64_t* seg_band_base, const double* band, const double* cand,
@@ -1213,14 +1217,16 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
 
   // stats
   const SegDP* hd = ctx->h_segdp.as<SegDP>();
-  int64_t ref_tr = 0, gen = 0;
+  int64_t ref_tr = 0, gen = 0, ref_ev = 0;
   for (int s = 0; s < n_seg; ++s) {
     const int64_t n = c.h_seg_off[s + 1] - c.h_seg_off[s];
     if (!active[s]) continue;
     gen += hd[s].n_cand;
+    ref_ev += hd[s].ref_evals;
     ref_tr += n * (n + 1) / 2 * ((int64_t)hd[s].ref_evals + (single ? 0 : 1));
   }
   S.candidates_generated = gen;
+  S.candidates_ref_evaluated = ref_ev;
   S.candidates_evaluated = evaluated;
   S.transitions_executed = transitions;
   S.transitions_reference = ref_tr;
@@ -1343,6 +1349,7 @@ int plan_split(pp_ctx* ctx, const PlanCall& c, int parts) {
     if (rcs[p] != PP_OK) return fail(ctx, rcs[p], sub->err);
     const pp_stats& t = sub->stats;
     S.candidates_generated += t.candidates_generated;
+    S.candidates_ref_evaluated += t.candidates_ref_evaluated;
     S.candidates_evaluated += t.candidates_evaluated;
     S.transitions_executed += t.transitions_executed;
     S.transitions_reference += t.transitions_reference;
@@ -1442,6 +1449,19 @@ int pp_ctx_set_stream(pp_ctx* ctx, void* stream) {
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   ctx->stream = static_cast<cudaStream_t>(stream);
   ctx->own_stream = false;
+  return PP_OK;
+}
+
+int pp_pack_plan_slots(pp_ctx* ctx, const int32_t* d_count, const int32_t* d_status, const double* d_t_max_used,
+                       const double* d_objective, const int32_t* d_splits, const int32_t* d_order,
+                       const int64_t* d_seg_offsets, int32_t n_seg, int32_t n_max, int64_t* d_slots) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n_seg < 0 || n_max < 1 || !d_count || !d_status || !d_t_max_used || !d_objective || !d_splits ||
+      !d_seg_offsets || !d_slots)
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  PP_CUDA(launch_pack_slots(d_count, d_status, d_t_max_used, d_objective, d_splits, d_order, d_seg_offsets,
+                            n_seg, n_max, reinterpret_cast<long long*>(d_slots), ctx->stream));
   return PP_OK;
 }
 
@@ -1703,6 +1723,7 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
       auto done = [&](int) {
         const pp_stats& t = sub->stats;
         S.candidates_generated += t.candidates_generated;
+        S.candidates_ref_evaluated += t.candidates_ref_evaluated;
         S.candidates_evaluated += t.candidates_evaluated;
         S.transitions_executed += t.transitions_executed;
         S.transitions_reference += t.transitions_reference;
@@ -1735,6 +1756,7 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
     if (rcs[w] != PP_OK) return fail(ctx, rcs[w], ctx->subs[w]->err);
     const pp_stats& t = acc[w];
     S.candidates_generated += t.candidates_generated;
+    S.candidates_ref_evaluated += t.candidates_ref_evaluated;
     S.candidates_evaluated += t.candidates_evaluated;
     S.transitions_executed += t.transitions_executed;
     S.transitions_reference += t.transitions_reference;

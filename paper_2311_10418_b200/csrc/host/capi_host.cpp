@@ -1,6 +1,9 @@
 // capi_host.cpp — host-only C-ABI helpers: the drop-in C++ API's grid,
 // dataset and slice-cost functions exposed to C / ctypes callers.
+#include <algorithm>
 #include <cstring>
+#include <span>
+#include <vector>
 #include <stdexcept>
 
 #include "pipeplan/cost_model.h"
@@ -76,6 +79,30 @@ int pp_synthetic_dataset(int64_t n, const double* in_dist, const double* tgt_dis
     spec.seed = seed;
     const std::vector<Sample> s = load_dataset(spec);
     std::memcpy(out, s.data(), sizeof(pp_sample) * s.size());
+    return PP_OK;
+  } catch (const std::invalid_argument&) {
+    return PP_ERR_INVALID;
+  }
+}
+
+int pp_assign_replicas(const double* times, int64_t m, int32_t replica_count, int32_t* replica,
+                       double* max_load) {
+  if (m < 1 || replica_count < 1) return PP_ERR_INVALID;
+  try {
+    const std::span<const double> ts(times, static_cast<std::size_t>(m));
+    std::vector<int> rep;
+    if (m >= replica_count) {
+      rep = balance_replicas(ts, replica_count);
+    } else {
+      rep.resize(static_cast<std::size_t>(m));
+      for (int64_t k = 0; k < m; ++k) rep[static_cast<std::size_t>(k)] = static_cast<int>(k);
+    }
+    std::vector<double> load(static_cast<std::size_t>(replica_count), 0.0);
+    for (int64_t k = 0; k < m; ++k) {
+      replica[k] = rep[static_cast<std::size_t>(k)];
+      load[static_cast<std::size_t>(rep[static_cast<std::size_t>(k)])] += ts[static_cast<std::size_t>(k)];
+    }
+    *max_load = *std::max_element(load.begin(), load.end());
     return PP_OK;
   } catch (const std::invalid_argument&) {
     return PP_ERR_INVALID;

@@ -45,6 +45,12 @@ def record(p, with_order=True):
                    t_max_used=float(p.t_max_used).hex(), objective=float(p.objective).hex())
         if with_order and getattr(p, "ordered", None) is not None:
             rec["ordered_ids"] = [int(x) for x in p.ordered[:, 0]]
+        if getattr(p, "replica", None) is not None:
+            rec["replica"] = [int(x) for x in p.replica]
+            rec["max_load"] = float(p.max_load).hex()
+    if getattr(p, "n_candidates", -1) >= 0:
+        rec["n_candidates"] = int(p.n_candidates)
+        rec["n_evaluated"] = int(p.n_evaluated)
     return rec
 
 
@@ -53,8 +59,17 @@ def unhex(x):
 
 
 def assert_plan_matches(got, expect, ctx=""):
-    """Bit-exact parity with a golden/checker record."""
+    """Bit-exact parity with a golden/checker record: status
+    and error sample, splits, slice times, t_max_used, objective (1e-6), the
+    ordering, dp_partition's replica assignment and max_replica_load, and the
+    candidate loop's counters (|candidates|, candidates the reference's loop
+    visits) whenever both sides carry them."""
     assert int(got.status) == expect["status"], f"{ctx}: status {got.status} != {expect['status']}"
+    if "n_candidates" in expect and getattr(got, "n_candidates", -1) >= 0 and expect["status"] == 0:
+        assert int(got.n_candidates) == expect["n_candidates"], \
+            f"{ctx}: candidates {got.n_candidates} != {expect['n_candidates']}"
+        assert int(got.n_evaluated) == expect["n_evaluated"], \
+            f"{ctx}: reference-loop evaluations {got.n_evaluated} != {expect['n_evaluated']}"
     if expect["status"] != 0:
         if expect["status"] == 2:
             assert int(got.err_sample_id) == expect["err_sample_id"], ctx
@@ -66,3 +81,6 @@ def assert_plan_matches(got, expect, ctx=""):
     assert obj == eobj or abs(obj - eobj) <= 1e-6 * abs(eobj), f"{ctx}: objective {obj} != {eobj}"
     if "ordered_ids" in expect and getattr(got, "ordered", None) is not None:
         assert [int(x) for x in got.ordered[:, 0]] == expect["ordered_ids"], f"{ctx}: order differs"
+    if "replica" in expect and getattr(got, "replica", None) is not None:
+        assert [int(x) for x in got.replica] == expect["replica"], f"{ctx}: replica assignment differs"
+        assert float(got.max_load).hex() == expect["max_load"], f"{ctx}: max_replica_load differs"

@@ -181,8 +181,42 @@ def c3_main():
         json.dump(dict(name="C3", config="C3", expect=rec), f, separators=(",", ":"))
 
 
+def c5_main():
+    """C5 golden from the STREAMING restatement (oracle/pp_stream.c; the
+    reference itself needs ~9 h and 34 GB of tables at n = 65,536).  The
+    restatement is pinned against the unmodified reference at n <= 2048 by
+    tests/test_oracle.py::test_stream_restatement_matches_reference.
+        python tests/golden/make_golden.py c5        (~2 min on 8 cores)"""
+    import hashlib
+    import time
+
+    from oracle.bind import Oracle
+
+    cfg = W.CONFIGS["C5"]
+    samples = W.dataset(cfg, 1)
+    t0 = time.time()
+    p = Oracle().plan_stream(samples, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    secs = time.time() - t0
+    assert p.status == 0
+    sp = np.asarray(p.splits, np.int64)
+    rec = {"status": 0, "count": int(len(sp)),
+           "split_deltas": [int(x) for x in np.diff(np.concatenate([[0], sp]))],
+           "mb_times_sha256": hashlib.sha256(np.ascontiguousarray(p.mb_times, "<f8").tobytes()).hexdigest(),
+           "mb_time_first": [hx(x) for x in p.mb_times[:8]], "mb_time_max": hx(float(np.max(p.mb_times))),
+           "t_max_used": hx(p.t_max_used), "objective": hx(p.objective),
+           "ordered_ids_sha256": hashlib.sha256(np.ascontiguousarray(p.ordered[:, 0], "<i8").tobytes()).hexdigest(),
+           "n_candidates": p.n_candidates, "n_evaluated": p.n_evaluated}
+    with open(os.path.join(OUT, "c5.json"), "w") as f:
+        json.dump(dict(name="C5", config="C5", generator="oracle/pp_stream.c (orc_plan_grid_stream)",
+                       seconds=round(secs, 1), expect=rec), f, separators=(",", ":"))
+    print("c5", len(sp), "micro-batches,", p.n_candidates, "candidates,", p.n_evaluated, "evaluated,",
+          f"{secs:.0f} s")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["c3"]:
         c3_main()
+    elif sys.argv[1:] == ["c5"]:
+        c5_main()
     else:
         main()

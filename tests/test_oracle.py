@@ -105,3 +105,47 @@ def test_oracle_sort_matches_reference(orc):
         n = int(rng.integers(1, 3000))
         s = np.stack([rng.permutation(n) * 7 - 50, rng.integers(-5, 40, n), rng.integers(0, 9, n)], 1)
         assert np.array_equal(orc.order_samples(s), ref.order_samples(s))
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built (needs /root/reference)")
+def test_stream_restatement_matches_reference(orc):
+    """Pin the STREAMING restatement (oracle/pp_stream.c, which produced
+    tests/golden/c5.json) against the unmodified reference for n <= 2048:
+    GPT / T5, capped / uncapped, exact and quantised candidate sets (I in {0,
+    5, 1e3} plus the BASELINE mapping-A' interval), several stage counts.
+    Also against the table restatement's candidate counters."""
+    ref = Reference()
+    grid = W.grid()
+    rng = np.random.default_rng(2311)
+    cases = [(2048, False, 16, 4.0, W.CONFIGS["C3"].interval), (2048, True, 8, 0.0, 1e5),
+             (1024, True, 8, 0.0, W.CONFIGS["C2"].interval), (1024, False, 4, 2.0, 1e3)]
+    for n in (1, 3, 40, 257):
+        for encdec in (False, True):
+            for cap_mult in (0.0, 3.0):
+                for I in (0.0, 5.0, 1e3):
+                    cases.append((n, encdec, int(rng.choice([1, 2, 4, 8])), cap_mult, I))
+    for n, encdec, C, cap_mult, I in cases:
+        s = capi.synthetic_dataset(n, 8192, 900 + n, W.INPUT_DIST, W.T5_TARGET_DIST if encdec else None)
+        s[:, 0] = rng.permutation(n) + 10  # the sort has work to do
+        model = capi.Model.uniform(C, 2, encdec)
+        cap = math.inf
+        if cap_mult:
+            o = orc.order_samples(s)
+            cap = cap_mult * max(orc.slice_cost(grid, model, o, i, i + 1)[1] for i in range(n))
+        ctx = f"n{n} {'t5' if encdec else 'gpt'} C{C} cap{cap_mult} I{I}"
+        a = orc.plan_stream(s, grid, model, C, 1, cap, I, threads=4)
+        b = ref.plan(s, grid, model, C, 1, cap, I)
+        assert_plan_matches(a, record(b), ctx)
+        if n <= 257:
+            t = orc.plan(s, grid, model, C, 1, cap, I)
+            assert (a.n_candidates, a.n_evaluated) == (t.n_candidates, t.n_evaluated), ctx
+
+
+def test_c5_golden_is_the_stream_restatement_output():
+    """tests/golden/c5.json carries what its generator recorded; its
+    candidate counters are consistent with BASELINE config C5 (256 bins)."""
+    g = load_golden("c5")
+    e = g["expect"]
+    assert e["status"] == 0 and e["count"] == len(e["split_deltas"])
+    assert sum(e["split_deltas"]) == W.CONFIGS["C5"].n and min(e["split_deltas"]) >= 1
+    assert e["n_candidates"] <= W.CONFIGS["C5"].K + 1 and e["n_evaluated"] >= 1

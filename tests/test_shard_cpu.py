@@ -42,10 +42,18 @@ def test_pack_roundtrip_odd_and_even():
         st = np.zeros(M, np.int32)
         slots = shard.pack_slots(torch.from_numpy(count), torch.from_numpy(st), torch.from_numpy(tm),
                                  torch.from_numpy(ob), torch.from_numpy(splits), n)
-        back = shard.unpack_slots(slots, n)
+        back = shard.unpack_slots(slots, n, False)
         for k in range(M):
             assert back[k]["count"] == count[k]
             assert back[k]["t_max_used"] == tm[k] and back[k]["objective"] == ob[k]
+            assert np.array_equal(back[k]["splits"], splits[k, :count[k]])
+        order = np.stack([rng.permutation(n) for _ in range(M)]).astype(np.int32)
+        slots = shard.pack_slots(torch.from_numpy(count), torch.from_numpy(st), torch.from_numpy(tm),
+                                 torch.from_numpy(ob), torch.from_numpy(splits), n, torch.from_numpy(order))
+        assert slots.shape[1] == shard.slot_words(n, True)
+        back = shard.unpack_slots(slots, n, True)
+        for k in range(M):
+            assert np.array_equal(back[k]["order"], order[k])
             assert np.array_equal(back[k]["splits"], splits[k, :count[k]])
 
 
@@ -55,6 +63,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _order_of(samples, ordered):
+    """Per-segment sample index of each ordered position (pp_plan_out.order)."""
+    pos = {int(i): k for k, i in enumerate(samples[:, 0])}
+    return np.array([pos[int(i)] for i in ordered[:, 0]], np.int32)
+
+
 def _worker(rank, world, port, M, n, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -62,36 +76,45 @@ def _worker(rank, world, port, M, n, q):
         cfg = W.CONFIGS["C1"]
         data = capi.synthetic_dataset(n * M, 8192, 7, W.INPUT_DIST)
         lo, hi = shard.shard_range(M, world, rank)
-        # equal slot blocks for all_gather: pad the shard to ceil(M / world)
-        per = -(-M // world)
         orc = Oracle()
-        count = np.zeros(per, np.int32)
-        status = np.full(per, -1, np.int32)
-        tm = np.zeros(per)
-        ob = np.zeros(per)
-        splits = np.zeros((per, n), np.int32)
+        k_loc = hi - lo
+        count = np.zeros(k_loc, np.int32)
+        status = np.full(k_loc, -1, np.int32)
+        tm = np.zeros(k_loc)
+        ob = np.zeros(k_loc)
+        splits = np.zeros((k_loc, n), np.int32)
+        order = np.zeros((k_loc, n), np.int32)
         for k, mb in enumerate(range(lo, hi)):
-            p = orc.plan(data[mb * n:(mb + 1) * n], W.grid(), W.model(cfg), cfg.stages, 1, math.inf,
-                         cfg.interval)
+            mbs = data[mb * n:(mb + 1) * n]
+            p = orc.plan(mbs, W.grid(), W.model(cfg), cfg.stages, 1, math.inf, cfg.interval)
             count[k] = len(p.splits)
             status[k] = p.status
             tm[k] = p.t_max_used
             ob[k] = p.objective
             splits[k, :count[k]] = p.splits
+            order[k] = _order_of(mbs, p.ordered)
         slots = shard.pack_slots(torch.from_numpy(count), torch.from_numpy(status), torch.from_numpy(tm),
-                                 torch.from_numpy(ob), torch.from_numpy(splits), n)
-        allp = shard.unpack_slots(shard.gather_plans(slots), n)
-        # drop the padding slots, in rank order
-        plans = []
-        for r in range(world):
-            a, b = shard.shard_range(M, world, r)
-            plans += allp[r * per: r * per + (b - a)]
+                                 torch.from_numpy(ob), torch.from_numpy(splits), n, torch.from_numpy(order))
+        # unequal shards (M % world != 0): gather_epoch pads and trims
+        plans = shard.unpack_slots(shard.gather_epoch(slots, M), n)
         ok = len(plans) == M
         for mb in range(M):
-            ref = orc.plan(data[mb * n:(mb + 1) * n], W.grid(), W.model(cfg), cfg.stages, 1, math.inf,
-                           cfg.interval)
+            mbs = data[mb * n:(mb + 1) * n]
+            ref = orc.plan(mbs, W.grid(), W.model(cfg), cfg.stages, 1, math.inf, cfg.interval)
             ok &= plans[mb]["status"] == 0 and np.array_equal(plans[mb]["splits"], ref.splits)
             ok &= plans[mb]["t_max_used"] == ref.t_max_used and plans[mb]["objective"] == ref.objective
+            # the reference's MicroBatch::sample_ids (microbatch.cpp:122-134)
+            ids = shard.micro_batch_sample_ids(mbs, plans[mb])
+            lo_ = 0
+            for e, got in zip(ref.splits, ids):
+                ok &= np.array_equal(got, ref.ordered[lo_:e, 0])
+                lo_ = e
+        # gather_plans refuses unequal blocks instead of hanging the collective
+        try:
+            shard.gather_plans(slots)
+            ok &= (M % world == 0)
+        except ValueError:
+            ok &= (M % world != 0)
         q.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()
