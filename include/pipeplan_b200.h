@@ -130,6 +130,11 @@ typedef struct pp_tuning {
                               record indirection costs more than the bytes it saves */
   int32_t host_chunks;     /* host-buffer calls with streams > 1: chunks per worker (0 =
                               default 2; 1 = no intra-worker prefetch) */
+  int32_t dp_pricing;      /* 1: on length-sorted single-input mini-batches the DP prices
+                              its slices in-kernel and no band exists in HBM (cost pass B
+                              only marks candidates); 0 (default): pass B writes the band
+                              and the DP streams it — faster on a B200, where the priced
+                              DP is latency-bound at two CTAs per SM */
 } pp_tuning;
 
 /* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are

@@ -61,7 +61,8 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
                              double lo_thresh, int bisect, int sorted_in, int reuse, double* cmin,
-                             short* colbase, int* chunk_nv, int* wrote_cmin, cudaStream_t st);
+                             short* colbase, int* chunk_nv, int* wrote_cmin, int nostore, cudaStream_t st);
+bool band_run_applies(const CostGrid& g, const double* tabT, int reuse, const double* tau, int sorted_in);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
                              int* row_w, int* blk_W, cudaStream_t st);
 cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -92,7 +93,8 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, const double* cmin, double t_margin,
                            unsigned long long* cols_streamed, const short* colbase, const int* chunk_nv,
-                           const int* row_w, ItemResult* res2, cudaStream_t st);
+                           const int* row_w, ItemResult* res2, const DpPrice* price, int price_lay,
+                           cudaStream_t st);
 cudaError_t launch_seg_set_bound(const ItemResult* bound_res, int replicas, SegDP* dp, int n_seg,
                                  cudaStream_t st);
 cudaError_t launch_mb_shapes(const pp_sample* ordered, const int64_t* seg_off, const int32_t* splits,
@@ -153,14 +155,21 @@ cudaError_t launch_finalize(const SegDP* dps, const int* best_next, const int64_
                             const double* band, const SegStats* stats, const short* colbase,
                             const pp_sample* ordered, int stage_count, int replicas, int max_n, int n_seg,
                             int32_t* splits, double* mb_times, int32_t* count, double* t_max_used,
-                            double* objective, int32_t* status, int64_t* err_id, cudaStream_t st);
+                            double* objective, int32_t* status, int64_t* err_id, const DpPrice* price,
+                            int price_lay, cudaStream_t st);
 }  // namespace ppb
 
 using namespace ppb;
 
 namespace {
 
-constexpr size_t kDpSmemLimit = 190 * 1024;  // fixed + state budget before DP state spills to global
+constexpr size_t kDpSmemLimit = 190 * 1024;
+// A DP launch over few, very long mini-batches (C5: 65,536 samples, rows up
+// to n wide) runs each pass as one cooperative kernel over the whole GPU
+// (dp_coop.cu) instead of one CTA per pass.
+constexpr int kCoopMinN = 16384;
+constexpr int kCoopMaxItems = 8;
+  // fixed + state budget before DP state spills to global
 
 // Grow-only device buffer.
 struct DevBuf {
@@ -255,6 +264,9 @@ struct pp_ctx {
   double exit_thresh = INFINITY;  // last call's pass-A row-exit threshold
   double trunc_margin = INFINITY; // candidate-pass truncation margin 2E (+inf: off)
   bool compact = false;           // the band holds compact chunk records (pp_internal.cuh)
+  bool priced = false;            // no band: the DP prices its slices in-kernel (dp.cu PRICE)
+  DpPrice price{};                // its inputs
+  int price_lay = 0;              // its layout class (kLayDec1 / kLayEncDec2)
   // pipelined host-buffer worker (plan_host_chunks): copy stream + two sets
   cudaStream_t cstream = nullptr;
   HostSet hset[2];
@@ -765,7 +777,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                    cap, interval, ctx->row_w.as<int>(), ctx->row_fb.as<int>(), ctx->blk_W.as<int>(),
                                    ctx->stats_d.as<SegStats>(), nullptr, nullptr, nullptr, exit_thresh,
                                    nullptr, nullptr, lo_thresh, bisect, 0, 0, nullptr, nullptr, nullptr,
-                                   nullptr, st));
+                                   nullptr, 0, st));
     PP_TIMED(1, launch_tile_offsets(ctx->blk_W.as<int>(), ctx->blk_base.as<int>(), n_seg,
                                     ctx->tile_off.as<int64_t>(), ctx->stats_d.as<SegStats>(), st));
   }
@@ -779,7 +791,15 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     band_total += hs[s].band;
   }
   ctx->band_total = band_total;
-  PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
+  // In-kernel DP pricing (dp.cu PRICE): pass B takes band_run_kernel (sorted
+  // single-input mini-batches, quantised candidates) and no pass runs
+  // cooperatively (dp_coop.cu streams the band): then the band is never
+  // materialised — pass B only marks candidates, the DP prices its slices.
+  const int64_t coop_n = ctx->tuning.coop_min_n > 0 ? ctx->tuning.coop_min_n : kCoopMinN;
+  const bool price_in_dp = !table && total > 0 && ctx->tuning.dp_pricing && !ctx->tuning.compact_band &&
+                           !c.presorted && band_run_applies(g, nullptr, ctx->tuning.no_slice_reuse ? 0 : 1, tau_d, 1) &&
+                           !(n_seg <= kCoopMaxItems && max_n >= coop_n);
+  if (!price_in_dp) PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
   PP_CUDA(cudaMemcpyAsync(ctx->band_base.p, band_base.data(), n_seg * sizeof(int64_t),
                           cudaMemcpyHostToDevice, st));
   // (no fill: pass B writes every tile entry, NaN where no slice is feasible)
@@ -810,9 +830,43 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                  ctx->band_base.as<int64_t>(), ctx->band.as<double>(), INFINITY, small_bm,
                                  tau_d, -INFINITY, 0, c.presorted ? 0 : 1,
                                  ctx->tuning.no_slice_reuse ? 0 : 1, cmin, colbase, chunk_nv, &wrote_cmin,
-                                 st));
+                                 price_in_dp ? 1 : 0, st));
   ctx->trunc_margin = INFINITY;
   ctx->compact = (wrote_cmin & 2) != 0;
+  ctx->priced = (wrote_cmin & 4) != 0;
+  if (price_in_dp && !ctx->priced) return fail(ctx, PP_ERR_CUDA, "internal: pass B did not take the in-DP pricing path");
+  if (ctx->priced) {
+    DpPrice& p = ctx->price;
+    const int per = g.nm * g.ns;
+    p.P.tt_e = g.tt;
+    p.P.tt_d = g.tt + per;
+    p.P.am_e = g.am;
+    p.P.am_d = g.am + per;
+    p.P.ns = g.ns;
+    p.P.le = g.le;
+    p.P.ld = g.ld;
+    p.P.cap = cap;
+    p.P.need_mem = !(cap == INFINITY);
+    p.cells = per;
+    p.mbp = ctx->mbp.as<AxisPos>();
+    p.pin = ctx->pin.as<AxisPos>();
+    p.in_d = ctx->in_d.as<double>();
+    p.max_n = max_n;
+    // bracket(seq axis, 0.0) (cost_model.cpp:46-53) on the host: the same
+    // IEEE operations as the device's bracket() (band_run_kernel's p0)
+    const double* sx = ctx->h_ax.data() + g.nm;
+    int sg = 0;
+    double tz = 0.0;
+    if (g.ns > 1) {
+      while (sg + 2 < g.ns && 0.0 >= sx[sg + 1]) ++sg;
+      volatile double num = 0.0 - sx[sg], den = sx[sg + 1] - sx[sg];
+      tz = num / den;
+    }
+    p.p0.t = tz;
+    p.p0.seg = sg;
+    p.p0.pad = 0;
+    ctx->price_lay = g.lay_class;
+  }
   if ((wrote_cmin & 1) && !ctx->tuning.no_band_trunc) {
     const unsigned long long* hr = ctx->h_range.as<unsigned long long>();
     double lo[2], hi[2];
@@ -868,15 +922,10 @@ void place_states(std::vector<WorkItem>& items, int mode, size_t& smem_state, in
   }
 }
 
-// A DP launch over few, very long mini-batches (C5: 65,536 samples, rows up
-// to n wide) runs each pass as one cooperative kernel over the whole GPU
-// (dp_coop.cu) instead of one CTA per pass.
-constexpr int kCoopMinN = 16384;
-constexpr int kCoopMaxItems = 8;
 
 bool use_coop(const pp_ctx* ctx, const std::vector<WorkItem>& items, const int64_t* h_seg_off) {
   if (items.empty() || (int)items.size() > kCoopMaxItems) return false;
-  if (ctx->compact) return false;  // the cooperative pass reads the dense band
+  if (ctx->compact || ctx->priced) return false;  // the cooperative pass reads the dense band
   const int64_t min_n = ctx->tuning.coop_min_n > 0 ? ctx->tuning.coop_min_n : kCoopMinN;
   for (const WorkItem& w : items)
     if (h_seg_off[w.seg + 1] - h_seg_off[w.seg] < min_n) return false;
@@ -1004,6 +1053,23 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   // pass C: candidate values from the band (segments pass B did not cover)
   bool need_pass_c = false;
   for (int s = 0; s < n_seg; ++s) need_pass_c |= (mode[s] == 0 || mode[s] == 1);
+  if (ctx->priced && total > 0 && !single && need_pass_c) {
+    // candidate bins past pass B's bitmap: pass C reads them from the band,
+    // so this call materialises it after all (pass B again, storing; its
+    // candidate marks are idempotent) and the DP streams it
+    PP_CUDA(ctx->band.ensure(std::max<int64_t>(ctx->band_total, 1) * sizeof(double)));
+    int wrote = 0;
+    PP_TIMED(3, launch_cost_pass(1, g, nullptr, nullptr, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
+                                 ctx->pin.as<AxisPos>(), ctx->ptg.as<AxisPos>(), c.d_seg_off,
+                                 ctx->blk_base.as<int>(), n_seg, total_blocks, max_n, ctx->mbp.as<AxisPos>(),
+                                 c.opts.per_mb_mem_cap, I, ctx->row_w.as<int>(), ctx->row_fb.as<int>(),
+                                 ctx->blk_W.as<int>(), ctx->stats_d.as<SegStats>(), ctx->tile_off.as<int64_t>(),
+                                 ctx->band_base.as<int64_t>(), ctx->band.as<double>(), INFINITY,
+                                 ctx->small_bm.as<unsigned int>(), ctx->tau.as<double>(), -INFINITY, 0, 1,
+                                 ctx->tuning.no_slice_reuse ? 0 : 1, ctx->cmin.as<double>(), nullptr, nullptr,
+                                 &wrote, 0, st));
+    ctx->priced = false;
+  }
   if (total > 0 && !single && need_pass_c)
     PP_TIMED(6, launch_band_cand(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
                                  ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
@@ -1097,7 +1163,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                    ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
                                    ctx->gstate.as<double>(), 1, nullptr, 0.0, nullptr,
                                    ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                   ctx->row_w.as<int>(), nullptr, st));
+                                   ctx->row_w.as<int>(), nullptr, ctx->priced ? &ctx->price : nullptr,
+                                   ctx->price_lay, st));
       }
       PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
     }
@@ -1169,7 +1236,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                  ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
                                  ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, nullptr, 0.0, nullptr,
                                  ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                 ctx->row_w.as<int>(), ctx->bound_res.as<ItemResult>(), st));
+                                 ctx->row_w.as<int>(), ctx->bound_res.as<ItemResult>(),
+                                 ctx->priced ? &ctx->price : nullptr, ctx->price_lay, st));
       PP_TIMED(7, launch_seg_set_bound(ctx->bound_res.as<ItemResult>(), c.opts.replica_count,
                                        ctx->segdp.as<SegDP>(), n_seg, st));
     } else if (use_coop(ctx, items, c.h_seg_off)) {
@@ -1187,7 +1255,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                  trunc ? ctx->cmin.as<double>() : nullptr, ctx->trunc_margin,
                                  ctx->dp_cols.as<unsigned long long>(),
                                  ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                 ctx->row_w.as<int>(), nullptr, st));
+                                 ctx->row_w.as<int>(), nullptr, ctx->priced ? &ctx->price : nullptr,
+                                 ctx->price_lay, st));
       counted = true;
     }
     PP_TIMED(7, launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
@@ -1207,7 +1276,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                               ctx->stats_d.as<SegStats>(), ctx->compact ? ctx->colbase.as<short>() : nullptr,
                               c.d_ordered, c.opts.stage_count,
                               c.opts.replica_count, std::max(max_n, 1), n_seg, c.d_splits, c.d_times,
-                              c.d_count, c.d_tmax, c.d_obj, c.d_status, c.d_err, st));
+                              c.d_count, c.d_tmax, c.d_obj, c.d_status, c.d_err,
+                              ctx->priced ? &ctx->price : nullptr, ctx->price_lay, st));
   unsigned long long dp_cols = 0;
   if (counted)
     PP_CUDA(cudaMemcpyAsync(&dp_cols, ctx->dp_cols.p, sizeof(dp_cols), cudaMemcpyDeviceToHost, st));
@@ -1240,7 +1310,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     S.launches[ctx->kcat[k]] += 1;
   }
   S.dp_band_bytes = transitions * (int64_t)sizeof(double);
-  S.band_bytes = ctx->band_total * (int64_t)sizeof(double);
+  S.band_bytes = ctx->priced ? 0 : ctx->band_total * (int64_t)sizeof(double);
   S.exit_thresh = ctx->exit_thresh;
   for (int s = 0; s < n_seg; ++s) {
     S.slices_pass_a += (int64_t)hs[s].priced;

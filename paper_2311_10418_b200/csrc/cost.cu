@@ -759,7 +759,10 @@ __global__ void __launch_bounds__(32 * kCostWarps)
 // it (a range-max over the tile's row widths: rows r' with d <= w_r' whose
 // column r' + d lies in the run), so the candidate set is the reference's
 // exactly.  The store stream is the kernel's bound rather than FP64 issue.
-template <int LAY, bool COMPACT>
+// NOSTORE: the band is not written at all — the DP prices its slices itself
+// (dp.cu, PRICE != 0); this pass then only marks the candidate bins, the
+// per-chunk minima and the singleton maximum (no tile, no record).
+template <int LAY, bool COMPACT, bool NOSTORE>
 __global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per SM: more stores in flight
     band_run_kernel(CostArgs a) {
   __shared__ double4 s_tt[kBandCells];
@@ -788,47 +791,14 @@ __global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per 
   const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
   const bool need_mem = !(a.cap == INF);
   constexpr int kTau = kSmallBmWords * 32;
-  const double le = a.g.le, ld = a.g.ld, ival = a.interval, cap = a.cap;
+  const double ival = a.interval;
   AxisPos p0{0.0, 0, 0};
   bracket(a.g.seq_ax, ns, 0.0, p0.seg, p0.t);
-  auto kind_time = [&](int base, int mb, double tm, int sg, double ts, double& tf, double& tb) {
-    const int s1 = min(sg + 1, ns - 1);
-    const double4 c0 = s_tt[base + mb + sg], c1 = s_tt[base + mb + s1];
-    tf = blend_d(tm, ts, c0.x, c0.z, c1.x, c1.z);
-    tb = blend_d(tm, ts, c0.y, c0.w, c1.y, c1.w);
-  };
-  auto kind_mem = [&](int base, int mb, double tm, int sg, double ts) {
-    const int s1 = min(sg + 1, ns - 1);
-    const double2 c0 = s_am[base + mb + sg], c1 = s_am[base + mb + s1];
-    return blend_d(tm, ts, c0.x, c0.y, c1.x, c1.y);
-  };
-  // slice time (band3_kernel's operations)
-  auto price_t = [&](const AxisPos& mb, const AxisPos& pe) {
-    double df, db;
-    kind_time(per, mb.pad, mb.t, pe.seg, pe.t, df, db);
-    const double t2 = __dadd_rn(__dmul_rn(ld, df), __dmul_rn(ld, db));
-    double T = t2;
-    if (LAY != kLayDec1) {
-      double ef, eb;
-      kind_time(0, mb.pad, mb.t, pe.seg, pe.t, ef, eb);
-      const double t1 = __dadd_rn(__dmul_rn(le, ef), __dmul_rn(le, eb));
-      T = (t1 < t2) ? t2 : t1;
-    }
-    return T;
-  };
+  SlicePricer SP{s_tt, s_tt + per, s_am, s_am + per, ns, a.g.le, a.g.ld, a.cap, need_mem};
+  // slice time (band3_kernel's operations) ...
+  auto price_t = [&](const AxisPos& mb, const AxisPos& pe) { return price_time<LAY>(SP, mb, pe); };
   // ... NaN where act_mem exceeds the cap
-  auto price = [&](const AxisPos& mb, const AxisPos& pe) {
-    double T = price_t(mb, pe);
-    if (need_mem) {
-      double M = __dmul_rn(ld, kind_mem(per, mb.pad, mb.t, pe.seg, pe.t));
-      if (LAY != kLayDec1) {
-        const double a1 = __dmul_rn(le, kind_mem(0, mb.pad, mb.t, pe.seg, pe.t));
-        M = (a1 < M) ? M : a1;
-      }
-      T = (M > cap) ? QNAN : T;
-    }
-    return T;
-  };
+  auto price = [&](const AxisPos& mb, const AxisPos& pe) { return price_slice<LAY>(SP, mb, pe); };
   for (int gb = blockIdx.x * kCostWarps + wid; gb < a.total_blocks; gb += warps) {
     const int s = seg_of(a.blk_base, a.n_seg, gb);
     const int64_t b0 = a.seg_off[s];
@@ -954,7 +924,7 @@ __global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per 
               vals[voff + 31 - r] = F;  // window d in [cs - 31, cs]
               if (lane == 0) s_cb[wid][q] = (short)(voff + 31);
               voff += 32;
-            } else {
+            } else if (!NOSTORE) {
               tile[(size_t)cs * kRB + r] = live ? F : QNAN;
             }
             if (live && !isnan(F)) bin(F);
@@ -982,7 +952,7 @@ __global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per 
           for (int idx = lane; idx < L; idx += 32) vals[voff + idx] = ring[(cs - 31 + idx) & 127];
           if (lane <= qe - q) s_cb[wid][q + lane] = (short)(voff + lane + 31);
           voff += L;
-        } else {
+        } else if (!NOSTORE) {
           // column c: lane r stores ring[d = c - r], live iff 1 <= d <= w_r
           double* out = tile + (size_t)cs * kRB + r;
           int d = cs - r;
@@ -1023,7 +993,14 @@ __global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per 
       // the tile's singleton slices [i, i+1) (column r + 1 <= 32, in the dense
       // near tile, written by this lane): their largest feasible time bounds
       // t* from below (dp.cu seg_init_kernel)
-      double v = (r + 1 < W) ? tile[(size_t)(r + 1) * kRB + r] : QNAN;
+      double v;
+      if (NOSTORE) {  // no tile: price the singleton (d = 1, in[i]) directly
+        const double x = rowv ? a.in_d[b0 + i0 + r] : QNAN;
+        const AxisPos px = rowv ? a.pin[b0 + i0 + r] : p0;
+        v = (r + 1 < W) ? price(a.mbp[1], (0.0 < x) ? px : p0) : QNAN;
+      } else {
+        v = (r + 1 < W) ? tile[(size_t)(r + 1) * kRB + r] : QNAN;
+      }
       v = (wr > 0 && !isnan(v)) ? v : -INF;
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
@@ -1552,6 +1529,17 @@ cudaError_t launch_brackets(const CostGrid& g, int max_n, AxisPos* mbp, const do
 }
 
 // pass: 0 = A, 1 = B.  tabT != null selects the table source.
+// Pass B takes band_run_kernel (diagonal reuse) for length-sorted
+// single-input segments with quantised candidates and a grid that fits its
+// static shared memory; only then can the DP price its own slices
+// (band_run_kernel<.., NOSTORE>, dp.cu PRICE).
+bool band_run_applies(const CostGrid& g, const double* tabT, int reuse, const double* tau, int sorted_in) {
+  const GridSmem L = grid_smem_layout(g.nm, g.ns, g.n_lay, tau ? kSmallBmWords * 32 : 0);
+  const int src = tabT ? 2 : (L.bytes <= 160 * 1024 ? 0 : 1);
+  return reuse && tau && src != 2 && 2 * g.nm * g.ns <= kBandCells && sorted_in && !g.is_encdec &&
+         (g.lay_class == kLayDec1 || g.lay_class == kLayEncDec2);
+}
+
 cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, const double* tabM,
                              const double* in_d, const double* tgt_d, const AxisPos* pin,
                              const AxisPos* ptg, const int64_t* seg_off, const int* blk_base, int n_seg,
@@ -1560,7 +1548,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              const int64_t* tile_off, const int64_t* seg_band_base, double* band,
                              double exit_thresh, unsigned int* small_bm, const double* tau,
                              double lo_thresh, int bisect, int sorted_in, int reuse, double* cmin,
-                             short* colbase, int* chunk_nv, int* wrote_cmin, cudaStream_t st) {
+                             short* colbase, int* chunk_nv, int* wrote_cmin, int nostore, cudaStream_t st) {
   CostArgs a{g, tabT, tabM, in_d, tgt_d, pin, ptg, seg_off, blk_base, n_seg, total_blocks, max_n, mbp,
              cap, interval, row_w, row_fb, blk_W, stats, tile_off, seg_band_base, band, exit_thresh,
              small_bm, tau, cmin, colbase, chunk_nv};
@@ -1608,21 +1596,22 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
     }
   } else if (pass == 0) {
     if (src == 0) PP_COST_LAUNCH_L(0, 0); else if (src == 1) PP_COST_LAUNCH_L(0, 1); else PP_COST_LAUNCH(0, 2, 0);
-  } else if (reuse && tau && src != 2 && 2 * g.nm * g.ns <= kBandCells && sorted_in && !g.is_encdec &&
-             (g.lay_class == kLayDec1 || g.lay_class == kLayEncDec2)) {
-    const bool compact = colbase != nullptr;
+  } else if (band_run_applies(g, tabT, reuse, tau, sorted_in)) {
+    const bool compact = colbase != nullptr && !nostore;
     if (!compact) {
       a.colbase = nullptr;
       a.chunk_nv = nullptr;
     }
     if (g.lay_class == kLayDec1) {
-      if (compact) band_run_kernel<kLayDec1, true><<<blocks, 32 * kCostWarps, 0, st>>>(a);
-      else band_run_kernel<kLayDec1, false><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+      if (nostore) band_run_kernel<kLayDec1, false, true><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+      else if (compact) band_run_kernel<kLayDec1, true, false><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+      else band_run_kernel<kLayDec1, false, false><<<blocks, 32 * kCostWarps, 0, st>>>(a);
     } else {
-      if (compact) band_run_kernel<kLayEncDec2, true><<<blocks, 32 * kCostWarps, 0, st>>>(a);
-      else band_run_kernel<kLayEncDec2, false><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+      if (nostore) band_run_kernel<kLayEncDec2, false, true><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+      else if (compact) band_run_kernel<kLayEncDec2, true, false><<<blocks, 32 * kCostWarps, 0, st>>>(a);
+      else band_run_kernel<kLayEncDec2, false, false><<<blocks, 32 * kCostWarps, 0, st>>>(a);
     }
-    if (wrote_cmin) *wrote_cmin = (cmin ? 1 : 0) | (compact ? 2 : 0);
+    if (wrote_cmin) *wrote_cmin = (cmin ? 1 : 0) | (compact && !nostore ? 2 : 0) | (nostore ? 4 : 0);
   } else if (tau && src != 2 && 2 * g.nm * g.ns <= kBandCells &&
              (g.lay_class == kLayDec1 || g.lay_class == kLayEncDec2)) {
 #define PP_BAND3(L, Z, E)                                              \

@@ -137,6 +137,86 @@ __device__ __forceinline__ int far_chunks_needed(int nc, const double* __restric
   return nc;
 }
 
+// ---- in-kernel slice pricing (PRICE != 0) ---------------------------------
+// On length-sorted single-input mini-batches (GPT) the band is never
+// materialised: slice [i, j) depends only on (d = j - i, in[j-1])
+// (pp_internal.cuh SlicePricer), and sorted mini-batches repeat lengths, so
+// along a diagonal the same value recurs for every column of a run of equal
+// lengths.  A warp walks a range of tile columns of the block whose first row
+// is k0; per run it prices the diagonals the run reaches (32 per batch, lane l:
+// d = next + l) into a 128-entry ring indexed by d, and lane r reads its entry
+// of column c at d = c - r; one-column runs are priced in place (lane r: its
+// own slice).  f(c, x, parity) receives lane r's T(k0 + r, k0 + c), NaN when
+// the slice's act_mem exceeds the cap.  Same operations as cost pass B's
+// band_run_kernel, so the values are the band's bit for bit.
+struct WalkScratch {
+  double* ring;   // [128]
+  double* x;      // [32] staged lengths
+  AxisPos* px;    // [32] their sequence brackets
+};
+
+template <int LAY, class F>
+__device__ __forceinline__ void walk_columns(const DpPrice& pr, const SlicePricer& SP, const double* __restrict__ len,
+                                             const AxisPos* __restrict__ pos, int cb, int ce,
+                                             const WalkScratch& ws, int lane, F&& f) {
+  const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
+  double prev_x = QNAN;
+  AxisPos pe = pr.p0;
+  int done = 0;
+  for (int c0 = cb; c0 < ce; c0 += 32) {
+    const int cq = c0 + lane;
+    double xq = QNAN;
+    AxisPos pxq = pr.p0;
+    if (cq < ce && cq > 0) {
+      xq = len[cq];
+      pxq = pos[cq];
+    }
+    ws.x[lane] = xq;
+    ws.px[lane] = pxq;
+    double xn = __shfl_down_sync(0xffffffffu, xq, 1);
+    if (lane == 31) xn = (cq + 1 < ce) ? len[cq + 1] : QNAN;
+    // bit q: column c0 + q ends its run (the next column differs or is past the range)
+    const unsigned int run_end = __ballot_sync(0xffffffffu, !(xn == xq));
+    __syncwarp();
+    const int qend = min(32, ce - c0);
+    for (int q = 0; q < qend;) {
+      const unsigned int e = run_end >> q;
+      const int qe = min(e ? q + __ffs(e) - 1 : 31, qend - 1);
+      const int cs = c0 + q, cend = c0 + qe;
+      const double x = ws.x[q];
+      if (!(x == prev_x)) {  // warp-uniform: column cs starts a run of equal lengths
+        prev_x = x;
+        const AxisPos px = ws.px[q];
+        if (0.0 < x) pe = px; else pe = pr.p0;
+        if (e & 1u) {  // a one-column run: lane r prices its own slice, d = cs - r
+          const int d = cs - lane;
+          f(cs, price_slice<LAY>(SP, pr.mbp[min(max(d, 1), pr.max_n)], pe), 0);
+          q = qe + 1;
+          continue;
+        }
+        done = cs - 32;
+      }
+      // price the run's diagonals (done, cend] (d <= 0 entries are never used)
+      while (done < cend) {
+        const int d = done + 1 + lane;
+        ws.ring[d & 127] = price_slice<LAY>(SP, pr.mbp[min(max(d, 1), pr.max_n)], pe);
+        done += 32;
+      }
+      __syncwarp();
+      int c = cs;
+      for (; c + 1 <= cend; c += 2) {
+        const double x0 = ws.ring[(c - lane) & 127];
+        const double x1 = ws.ring[(c + 1 - lane) & 127];
+        f(c, x0, 0);
+        f(c + 1, x1, 1);
+      }
+      if (c <= cend) f(c, ws.ring[(c - lane) & 127], 0);
+      __syncwarp();
+      q = qe + 1;
+    }
+  }
+}
+
 // (s, c, j) lexmin with lowest-j ties.
 __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int c0, int j0) {
   return s1 < s0 || (s1 == s0 && (c1 < c0 || (c1 == c0 && j1 < j0)));
@@ -164,7 +244,11 @@ __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int
 // finiteness test on the sum is needed: +inf or NaN never compares smaller
 // than the (+inf, 0) identity or any taken value, -inf is taken exactly when
 // the reference takes it.
-template <int MODE, bool SMEM_STATE, bool SANITIZE, bool COMPACT>
+// PRICE (kLayDec1 / kLayEncDec2; 0 = read the band): no band — the workers
+//   price every tile entry themselves (walk_columns above): the near tile of
+//   block b+1 into the dense near buffer and the far-far columns of block b+1
+//   straight into their reductions, during block b; the producer warp idles.
+template <int MODE, bool SMEM_STATE, bool SANITIZE, bool COMPACT, int PRICE>
 __global__ void __launch_bounds__(kDpThreads, 2)
     dp_pass_kernel(const WorkItem* __restrict__ items, const int64_t* __restrict__ seg_off,
                    const int* __restrict__ blk_base, const int* __restrict__ blk_W,
@@ -175,7 +259,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
                    int ring_off, int kRing, const double* __restrict__ cmin, double t_margin,
                    unsigned long long* __restrict__ cols_streamed, const short* __restrict__ colbase,
                    const int* __restrict__ chunk_nv, const int* __restrict__ row_w,
-                   ItemResult* __restrict__ res2) {
+                   ItemResult* __restrict__ res2, DpPrice pr) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* near = reinterpret_cast<double*>(smem + DpSmem::near);
   double* ring = reinterpret_cast<double*>(smem + ring_off);
@@ -276,14 +360,62 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       if (MODE == 1) pm[lane] = INF;
     }
   }
+  // PRICE: the pricer's cells (decoder kind, + encoder kind for kLayEncDec2)
+  // staged in shared memory at ring_off, then per worker warp a diagonal ring
+  // and the staged lengths of its current columns
+  SlicePricer SP{};
+  WalkScratch ws{};
+  if (PRICE) {
+    const int cells = pr.cells;
+    double4* s_tt = reinterpret_cast<double4*>(smem + ring_off);
+    double2* s_am = reinterpret_cast<double2*>(s_tt + (PRICE == kLayEncDec2 ? 2 : 1) * cells);
+    for (int k = threadIdx.x; k < cells; k += blockDim.x) {
+      s_tt[k] = pr.P.tt_d[k];
+      s_am[k] = pr.P.am_d[k];
+      if (PRICE == kLayEncDec2) {
+        s_tt[cells + k] = pr.P.tt_e[k];
+        s_am[cells + k] = pr.P.am_e[k];
+      }
+    }
+    SP = pr.P;
+    SP.tt_d = s_tt;
+    SP.am_d = s_am;
+    SP.tt_e = s_tt + cells;
+    SP.am_e = s_am + cells;
+    double* wbase = reinterpret_cast<double*>(s_am + (PRICE == kLayEncDec2 ? 2 : 1) * cells);
+    const int w = wid < kWorkers ? wid : 0;
+    ws.ring = wbase + w * (128 + 32 + 64);
+    ws.x = ws.ring + 128;
+    ws.px = reinterpret_cast<AxisPos*>(ws.x + 32);
+  }
   __syncthreads();
+  const double* seg_len = PRICE ? pr.in_d + b0 - 1 : nullptr;  // + row i0 + column c: in[i0 + c - 1]
+  const AxisPos* seg_pos = PRICE ? pr.pin + b0 - 1 : nullptr;
+  // PRICE: the dense near tile (columns [0, min(64, W)) of block bb, first
+  // row k0) into near buffer bb % 2; worker w prices columns [8w, 8w + 8)
+  auto price_near = [&](int bb) {
+    const int kk0 = max(0, n - kRB * (bb + 1));
+    const int cmax = min(kNearCols, blk_W[gb0 + bb]);
+    const int c_lo = min(8 * wid, cmax), c_hi = min(8 * wid + 8, cmax);
+    double* dst = near + (size_t)(bb % kNearBufs) * kNearCols * kRB;
+    if (c_lo < c_hi)
+      walk_columns<PRICE ? PRICE : kLayDec1>(pr, SP, seg_len + kk0, seg_pos + kk0, c_lo, c_hi, ws, lane,
+                                            [&](int c, double x, int) { dst[c * kRB + lane] = x; });
+  };
+  if (PRICE) {
+    if (wid == kProducerWarp) return;  // (no band to stream)
+    if (wid == 0 && lane == 0 && cols_streamed && nblk > 0)
+      atomicAdd(cols_streamed, (unsigned long long)min(kNearCols, blk_W[gb0]));
+    if (wid < kWorkers && nblk > 0) price_near(0);
+    named_bar(1, kSyncThreads);
+  }
 
   // ================= producer warp: TMA bulk copies, in consumption order
   // (near tile of block b, then the far-far chunks of block b, which the
   // workers consume during block b-1), each into a buffer its consumers
   // released through the matching "empty" mbarrier.  It never joins the
   // block barrier, so it runs ahead by up to the ring depth.
-  if (wid == kProducerWarp) {
+  if (!PRICE && wid == kProducerWarp) {
     // Issue order = consumption order: near tile of block b (used during
     // block b), then the far-far chunks of block b+1 (used by the workers
     // during block b), so far chunks never queue behind a near-buffer wait.
@@ -365,7 +497,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     if (wid < kWorkers) {
       const int W = blk_W[gb0 + b];
       const int r = lane;
-      mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
+      if (!PRICE) mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
       double s1 = INF, m1 = INF, b1 = INF;
       int c1 = 0, j1 = INT_MAX;
       const int cnf = min(kNearCols, W);
@@ -418,7 +550,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       } else {
         if (MODE == 1) am = pm[pbuf];
       }
-      mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
+      if (!PRICE) mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
     }
     named_bar(3, kSyncThreads);
 
@@ -520,7 +652,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       // release (__syncwarp + mbarrier arrive), and the producer's next TMA
       // write into the buffer waits for it (the TMA pipeline WAR pattern)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);
+      if (!PRICE && lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);
       PP_TRACE(3);
       if (r < nb) {
         const int row = i0 + r;
@@ -563,7 +695,51 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         int ac = 0, aj = INT_MAX, ac2 = 0, aj2 = INT_MAX;
         const int r = lane;
 
-        for (int k = 0; k < nc; ++k) {
+        if (PRICE) {
+          // block b+1's near tile for the chain and phase 1 of the next block ...
+          price_near(bn);
+          // ... and its far-far columns [64, Weff), worker w a contiguous share
+          // of them, priced on the fly into its reductions
+          const int Weff = nc > 0 ? min(Wn, kNearCols + nc * kChunkCols) : min(Wn, kNearCols);
+          const int F = Weff - kNearCols;
+          const int per = F > 0 ? (F + kWorkers - 1) / kWorkers : 0;
+          const int cw0 = kNearCols + min(F, w * per), cw1 = kNearCols + min(F, (w + 1) * per);
+          if (w == 0 && lane == 0 && cols_streamed)
+            atomicAdd(cols_streamed, (unsigned long long)(min(kNearCols, Wn) + max(F, 0)));
+          int ecur = wrap(sk0 + cw0), ccur = cw0;  // state slot of the current column
+          auto upd = [&](int c, double x, int par) {
+            int e = ecur + (c - ccur);
+            if (ring_state && e >= entries) e -= entries;
+            ecur = e;
+            ccur = c;
+            const int j = k0 + c;
+            const double cs = __dadd_rn(x, st_s[e]);
+            double& s_ = par ? as2 : as;
+            int& c_ = par ? ac2 : ac;
+            int& j_ = par ? aj2 : aj;
+            double& m_ = par ? am2 : am;
+            if (BSUM) {
+              double& b_ = par ? ab2 : ab;
+              const double cb = __dadd_rn(x, st_b[e]);
+              b_ = (cb < b_) ? cb : b_;
+            }
+            if (CAND) {
+              const int cn = 1 + st_c[e];
+              const bool u = (x <= t) & ((cs < s_) | ((cs == s_) & (cn < c_)));
+              s_ = u ? cs : s_;
+              c_ = u ? cn : c_;
+              j_ = u ? j : j_;
+            } else {
+              s_ = (cs < s_) ? cs : s_;
+              const double mj = MODE == 1 ? st_m[e] : 0.0;
+              const double v = (x < mj) ? mj : x;
+              if (MODE == 1) m_ = (v < m_) ? v : m_;
+            }
+          };
+          if (cw0 < cw1)
+            walk_columns<PRICE ? PRICE : kLayDec1>(pr, SP, seg_len + k0, seg_pos + k0, cw0, cw1, ws, lane, upd);
+        }
+        for (int k = 0; k < (PRICE ? 0 : nc); ++k) {
           mbar_wait(&ring_full[cslot], cphase);
           const double* ch = ring + (size_t)cslot * kChunkCols * kRB;
           const int c0 = kNearCols + k * kChunkCols;
@@ -868,7 +1044,7 @@ __global__ void __launch_bounds__(256)
                     int replicas, int32_t* __restrict__ splits, double* __restrict__ mb_times,
                     int32_t* __restrict__ count, double* __restrict__ t_max_used,
                     double* __restrict__ objective, int32_t* __restrict__ status,
-                    int64_t* __restrict__ err_id) {
+                    int64_t* __restrict__ err_id, DpPrice pr, int price_lay) {
   extern __shared__ int chain[];
   __shared__ int m_sh;
   const int s = blockIdx.x;
@@ -1002,8 +1178,24 @@ __global__ void __launch_bounds__(256)
       }
     }
     double v[kU];
+    if (price_lay) {  // no band: price the chosen slices like the DP did (walk_columns)
 #pragma unroll
-    for (int u = 0; u < kU; ++u) v[u] = at[u] >= 0 ? __ldg(bseg + at[u]) : 0.0;
+      for (int u = 0; u < kU; ++u) {
+        const int k = kb + u * blockDim.x;
+        v[u] = 0.0;
+        if (k < m) {
+          const int j = sp[k];
+          const int i = k ? sp[k - 1] : 0;
+          const double x = __ldg(pr.in_d + b + j - 1);
+          const AxisPos pe = (0.0 < x) ? pr.pin[b + j - 1] : pr.p0;
+          const AxisPos mb = pr.mbp[j - i];
+          v[u] = price_lay == kLayDec1 ? price_slice<kLayDec1>(pr.P, mb, pe) : price_slice<kLayEncDec2>(pr.P, mb, pe);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = at[u] >= 0 ? __ldg(bseg + at[u]) : 0.0;
+    }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int k = kb + u * blockDim.x;
@@ -1059,6 +1251,17 @@ extern "C" int pp_debug_dp_trace(long long* d_buf) {
 // smem_state = the largest shared-memory DP state of the launch's items
 // (0 with state_global: every item's state then lives in gstate).  The chunk
 // ring gets the rest of `smem_budget` (4..kMaxRing chunks of 8 KB).
+// PRICE shared memory after the fixed part / state: the pricer's cells and
+// per worker a 128-entry diagonal ring + 32 staged lengths and brackets.
+size_t dp_price_smem(int lay, int cells) {
+  return (size_t)(lay == kLayEncDec2 ? 2 : 1) * cells * (sizeof(double4) + sizeof(double2)) +
+         (size_t)kWorkers * (128 + 32 + 64) * sizeof(double);
+}
+
+// smem_state = the largest shared-memory DP state of the launch's items
+// (0 with state_global: every item's state then lives in gstate).  The chunk
+// ring gets the rest of `smem_budget` (4..kMaxRing chunks of 8 KB); with
+// `price` (in-kernel pricing, no band) there is no chunk ring.
 cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t smem_state,
                            int state_global, int sanitize, size_t smem_budget, const int64_t* seg_off,
                            const int* blk_base, const int* blk_W, const int64_t* tile_off,
@@ -1066,26 +1269,37 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, const double* cmin, double t_margin,
                            unsigned long long* cols_streamed, const short* colbase, const int* chunk_nv,
-                           const int* row_w, ItemResult* res2, cudaStream_t st) {
+                           const int* row_w, ItemResult* res2, const DpPrice* price, int price_lay,
+                           cudaStream_t st) {
   if (n_items == 0) return cudaSuccess;
   const size_t ring_off = (DpSmem::state + (state_global ? 0 : smem_state) + 127) / 128 * 128;
-  int ring = (int)std::min<size_t>(kMaxRing, (smem_budget - std::min(smem_budget, ring_off)) / kChunkBytes);
-  ring = std::max(ring, 4);
-  const size_t smem = ring_off + (size_t)ring * kChunkBytes;
+  int ring = 0;
+  size_t smem;
+  DpPrice pr{};
+  if (price) {
+    pr = *price;
+    smem = ring_off + dp_price_smem(price_lay, pr.cells);
+  } else {
+    ring = (int)std::min<size_t>(kMaxRing, (smem_budget - std::min(smem_budget, ring_off)) / kChunkBytes);
+    ring = std::max(ring, 4);
+    smem = ring_off + (size_t)ring * kChunkBytes;
+  }
   const bool compact = colbase != nullptr;
-#define PP_DP_LAUNCH(M, S, Z, C)                                                                      \
+#define PP_DP_LAUNCH(M, S, Z, C, P)                                                                   \
   do {                                                                                                \
-    ensure_dyn_smem((const void*)dp_pass_kernel<M, S, Z, C>, smem);                                   \
-    dp_pass_kernel<M, S, Z, C><<<n_items, kDpThreads, smem, st>>>(                                    \
+    ensure_dyn_smem((const void*)dp_pass_kernel<M, S, Z, C, P>, smem);                                \
+    dp_pass_kernel<M, S, Z, C, P><<<n_items, kDpThreads, smem, st>>>(                                 \
         items, seg_off, blk_base, blk_W, tile_off, seg_band_base, band, cand, cand_off, res, next_buf, \
         gstate, res_by_seg, (int)ring_off, ring, cmin, t_margin, cols_streamed, colbase, chunk_nv,    \
-        row_w, res2);                                                                                 \
+        row_w, res2, pr);                                                                             \
   } while (0)
-#define PP_DP_LAUNCH_Z(M, S)                                   \
-  do {                                                         \
-    if (compact) PP_DP_LAUNCH(M, S, false, true);              \
-    else if (sanitize) PP_DP_LAUNCH(M, S, true, false);        \
-    else PP_DP_LAUNCH(M, S, false, false);                     \
+#define PP_DP_LAUNCH_Z(M, S)                                                 \
+  do {                                                                       \
+    if (price && price_lay == kLayDec1) PP_DP_LAUNCH(M, S, false, false, kLayDec1);        \
+    else if (price) PP_DP_LAUNCH(M, S, false, false, kLayEncDec2);           \
+    else if (compact) PP_DP_LAUNCH(M, S, false, true, 0);                    \
+    else if (sanitize) PP_DP_LAUNCH(M, S, true, false, 0);                   \
+    else PP_DP_LAUNCH(M, S, false, false, 0);                                \
   } while (0)
   if (mode == 0) {
     if (state_global) PP_DP_LAUNCH_Z(0, false); else PP_DP_LAUNCH_Z(0, true);
@@ -1132,7 +1346,8 @@ cudaError_t launch_finalize(const SegDP* dps, const int* best_next, const int64_
                             const pp_sample* ordered, int stage_count, int replicas, int max_n, int n_seg,
                             int32_t* splits,
                             double* mb_times, int32_t* count, double* t_max_used, double* objective,
-                            int32_t* status, int64_t* err_id, cudaStream_t st) {
+                            int32_t* status, int64_t* err_id, const DpPrice* price, int price_lay,
+                            cudaStream_t st) {
   // 2: the chain and its hop tables (three n-int buffers) in shared memory; 1: the chain only
   const size_t hop_bytes = ((size_t)max_n * 3 + 2) * sizeof(int);
   const int in_smem = hop_bytes <= 200 * 1024 ? 2 : (size_t)max_n * sizeof(int) <= 200 * 1024 ? 1 : 0;
@@ -1141,7 +1356,7 @@ cudaError_t launch_finalize(const SegDP* dps, const int* best_next, const int64_
   finalize_kernel<<<n_seg, 256, smem, st>>>(dps, best_next, seg_off, blk_base, tile_off, seg_band_base,
                                             band, stats, colbase, ordered, in_smem, stage_count, replicas,
                                             splits, mb_times, count, t_max_used, objective, status,
-                                            err_id);
+                                            err_id, price ? *price : DpPrice{}, price ? price_lay : 0);
   return cudaGetLastError();
 }
 

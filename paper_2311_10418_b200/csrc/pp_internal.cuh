@@ -238,6 +238,70 @@ __device__ __forceinline__ void slice_cost_lay(const double4* __restrict__ tt,
   }
 }
 
+// Slice pricing of length-sorted single-input segments (GPT; band_run_kernel
+// and the DP's in-kernel pricing, dp.cu): slice [i, j) pads to (d = j - i,
+// in[j-1]), so its value depends on (d, length) only.  price_time is the
+// make_slice_cost time (microbatch.cpp:149-155 over estimate,
+// cost_model.cpp:301-317) with the operations of band3_kernel; price_slice
+// also evaluates act_mem and returns NaN when it exceeds the cap (the
+// reference's `continue` at microbatch.cpp:179).  Cells: per kind the
+// CostGrid tt / am tables with row base mb.pad = mi * ns.
+struct SlicePricer {
+  const double4* tt_e;  // encoder kind (kLayEncDec2 only)
+  const double4* tt_d;  // decoder kind
+  const double2* am_e;
+  const double2* am_d;
+  int ns;
+  double le, ld, cap;
+  bool need_mem;
+};
+
+template <int LAY>
+__device__ __forceinline__ double price_time(const SlicePricer& P, const AxisPos& mb, const AxisPos& pe) {
+  const int s1 = min(pe.seg + 1, P.ns - 1);
+  const double4 c0 = P.tt_d[mb.pad + pe.seg], c1 = P.tt_d[mb.pad + s1];
+  const double df = blend_d(mb.t, pe.t, c0.x, c0.z, c1.x, c1.z);
+  const double db = blend_d(mb.t, pe.t, c0.y, c0.w, c1.y, c1.w);
+  const double t2 = __dadd_rn(__dmul_rn(P.ld, df), __dmul_rn(P.ld, db));
+  if (LAY == kLayDec1) return t2;
+  const double4 e0 = P.tt_e[mb.pad + pe.seg], e1 = P.tt_e[mb.pad + s1];
+  const double ef = blend_d(mb.t, pe.t, e0.x, e0.z, e1.x, e1.z);
+  const double eb = blend_d(mb.t, pe.t, e0.y, e0.w, e1.y, e1.w);
+  const double t1 = __dadd_rn(__dmul_rn(P.le, ef), __dmul_rn(P.le, eb));
+  return (t1 < t2) ? t2 : t1;
+}
+
+template <int LAY>
+__device__ __forceinline__ double price_slice(const SlicePricer& P, const AxisPos& mb, const AxisPos& pe) {
+  double T = price_time<LAY>(P, mb, pe);
+  if (P.need_mem) {
+    const int s1 = min(pe.seg + 1, P.ns - 1);
+    const double2 c0 = P.am_d[mb.pad + pe.seg], c1 = P.am_d[mb.pad + s1];
+    double M = __dmul_rn(P.ld, blend_d(mb.t, pe.t, c0.x, c0.y, c1.x, c1.y));
+    if (LAY != kLayDec1) {
+      const double2 e0 = P.am_e[mb.pad + pe.seg], e1 = P.am_e[mb.pad + s1];
+      const double a1 = __dmul_rn(P.le, blend_d(mb.t, pe.t, e0.x, e0.y, e1.x, e1.y));
+      M = (a1 < M) ? M : a1;
+    }
+    T = (M > P.cap) ? __longlong_as_double(0x7ff8000000000000LL) : T;
+  }
+  return T;
+}
+
+// In-kernel pricing inputs of the DP (dp.cu, PRICE != 0): the pricer's
+// cells live in global memory here and are staged into shared memory by
+// each DP CTA; per micro-batch size the mbs bracket, per ordered sample the
+// sequence bracket of its input length and the length itself.
+struct DpPrice {
+  SlicePricer P;          // global-memory cells
+  int cells;              // cells per kind (nm * ns)
+  const AxisPos* mbp;     // [max_n + 1]
+  const AxisPos* pin;     // [total]
+  const double* in_d;     // [total]
+  int max_n;
+  AxisPos p0;             // bracket of length 0 (padded lengths start at 0)
+};
+
 // Rows per band tile (= rows per DP block).  The band of a segment is stored
 // as one tile per block of 32 rows, top-down (block b holds rows
 // [max(0, n-32(b+1)), n-32b)); tile column c holds the 32 rows' values for

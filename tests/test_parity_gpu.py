@@ -212,6 +212,61 @@ def test_compact_band_matches_dense_band(name):
     b.close()
 
 
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_dp_pricing_matches_band(name):
+    """The DP pricing its own slices (dp.cu PRICE: no band in HBM, pass B
+    only marks candidates) against the band path (pass B writes the band, the
+    DP streams it): identical plans, candidate sets and DP transitions."""
+    cfg = W.CONFIGS[name]
+    M = {"C1": 64, "C3": 6, "C4": 24}[name]
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    a = capi.Planner(0)
+    b = capi.Planner(0)
+    a.set_tuning(dp_pricing=True)
+    ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    sa = a.stats()
+    rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    sb = b.stats()
+    assert sa["band_bytes"] == 0 and sb["band_bytes"] > 0  # the priced path wrote no band
+    for k in ("ordered", "count", "t_max_used", "objective", "status"):
+        assert ra[k].tobytes() == rb[k].tobytes(), k
+    for q in range(M):
+        m = int(ra["count"][q])
+        for k in ("splits", "mb_times"):
+            assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
+    for k in ("candidates_generated", "candidates_evaluated", "candidates_ref_evaluated", "transitions_executed"):
+        assert sa[k] == sb[k], k
+    a.close()
+    b.close()
+
+
+def test_dp_pricing_random_capped_vs_oracle(orc):
+    """In-kernel DP pricing on random GPT mini-batches (binding and
+    non-binding caps, duplicate-heavy and distinct lengths, several
+    intervals and stage counts) against the C restatement."""
+    grid = capi.synthetic_grid()
+    rng = np.random.default_rng(4242)
+    priced = capi.Planner(0)
+    priced.set_tuning(dp_pricing=True)
+    for k in range(40):
+        n = int(rng.integers(1, 700))
+        L = int(rng.choice([8, 64, 1024, 8192]))
+        s = capi.synthetic_dataset(n, L, 3000 + k, W.INPUT_DIST)
+        s[:, 0] = rng.permutation(n) + 7
+        C = int(rng.choice([2, 4, 16]))
+        model = capi.Model.uniform(C, int(rng.integers(1, 4)), False, recompute=int(rng.integers(0, 3)))
+        o = orc.order_samples(s)
+        act = max(orc.slice_cost(grid, model, o, i, i + 1)[1] for i in range(n))
+        cap = float(rng.choice([math.inf, 1.0 * act, 3.0 * act, 40.0 * act]))
+        tot = orc.slice_cost(grid, model, o, 0, n)[0]
+        interval = float(rng.choice([5.0, tot / 7.0, tot / 64.0, tot / 300.0]))
+        a = orc.plan(s, grid, model, C, 1, cap, interval)
+        b = _plan_or_status(lambda: priced.plan(s, grid, model, C, 1, cap, interval))
+        assert_plan_matches(b, record(a), f"priced {k}: n={n} C={C} I={interval} cap={cap}")
+    priced.close()
+
+
 def test_slice_reuse_duplicate_heavy_vs_oracle(planner, orc):
     """Few distinct lengths (long runs), ragged sizes, binding and loose caps,
     fine and coarse intervals: the reuse path against the C restatement."""
