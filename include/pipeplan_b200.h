@@ -135,6 +135,11 @@ typedef struct pp_tuning {
                               only marks candidates); 0 (default): pass B writes the band
                               and the DP streams it — faster on a B200, where the priced
                               DP is latency-bound at two CTAs per SM */
+  int32_t no_slice_table;  /* 1: length-sorted single-input mini-batches get a per-mini-batch
+                              band from cost pass B; 0 (default): ONE slice table per call,
+                              G[length][d] (a slice of such a mini-batch depends on its size
+                              and padded length only), priced once, L2-resident, read by the
+                              DP and the candidate scan — no band (gtab.cu) */
 } pp_tuning;
 
 /* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are

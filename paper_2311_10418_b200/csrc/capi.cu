@@ -63,6 +63,17 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
                              double lo_thresh, int bisect, int sorted_in, int reuse, double* cmin,
                              short* colbase, int* chunk_nv, int* wrote_cmin, int nostore, cudaStream_t st);
 bool band_run_applies(const CostGrid& g, const double* tabT, int reuse, const double* tau, int sorted_in);
+// gtab.cu
+cudaError_t launch_gtab_need(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
+                             const int* blk_W, const double* in_d, int* need, cudaStream_t st);
+cudaError_t launch_gtab_offsets(const int* need, int nK, int64_t* row_off, long long* total, cudaStream_t st);
+cudaError_t launch_gtab_fill(const CostGrid& g, double cap, const AxisPos* mbp, int nK, const int* need,
+                             const int64_t* row_off, double* G, cudaStream_t st);
+cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* row_off, int64_t* gbase,
+                              cudaStream_t st);
+cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int64_t* gbase,
+                             const int* need, const double* G, double interval, const double* tau,
+                             unsigned int* small_bm, SegStats* stats, cudaStream_t st);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
                              int* row_w, int* blk_W, cudaStream_t st);
 cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -265,6 +276,10 @@ struct pp_ctx {
   double trunc_margin = INFINITY; // candidate-pass truncation margin 2E (+inf: off)
   bool compact = false;           // the band holds compact chunk records (pp_internal.cuh)
   bool priced = false;            // no band: the DP prices its slices in-kernel (dp.cu PRICE)
+  bool gtab = false;              // no band: the call's shared slice table (gtab.cu)
+  DevBuf gt_need, gt_off, gt_total, gt_G, gt_base;
+  PinBuf h_gt_total;
+  int64_t gtab_entries = 0;
   DpPrice price{};                // its inputs
   int price_lay = 0;              // its layout class (kLayDec1 / kLayEncDec2)
   // pipelined host-buffer worker (plan_host_chunks): copy stream + two sets
@@ -288,7 +303,7 @@ struct pp_ctx {
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
             &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
             &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act,
-            &cmin, &dp_cols, &colbase, &chunk_nv, &perm,
+            &cmin, &dp_cols, &colbase, &chunk_nv, &perm, &gt_need, &gt_off, &gt_total, &gt_G, &gt_base,
             &os_tf, &os_tb, &os_act, &os_off, &os_lim, &os_pred, &os_assign, &os_idx, &os_cloff, &os_clk,
             &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status,
             &ing_bytes, &ing_scratch, &ing_out, &ing_off,
@@ -796,10 +811,45 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   // cooperatively (dp_coop.cu streams the band): then the band is never
   // materialised — pass B only marks candidates, the DP prices its slices.
   const int64_t coop_n = ctx->tuning.coop_min_n > 0 ? ctx->tuning.coop_min_n : kCoopMinN;
-  const bool price_in_dp = !table && total > 0 && ctx->tuning.dp_pricing && !ctx->tuning.compact_band &&
-                           !c.presorted && band_run_applies(g, nullptr, ctx->tuning.no_slice_reuse ? 0 : 1, tau_d, 1) &&
-                           !(n_seg <= kCoopMaxItems && max_n >= coop_n);
-  if (!price_in_dp) PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
+  const bool sorted_gpt = !table && total > 0 && !ctx->tuning.compact_band && !c.presorted &&
+                          band_run_applies(g, nullptr, ctx->tuning.no_slice_reuse ? 0 : 1, tau_d, 1) &&
+                          !(n_seg <= kCoopMaxItems && max_n >= coop_n);
+  // The call's shared slice table (gtab.cu) instead of a band per
+  // mini-batch: lengths index its rows, so they must be bounded
+  const int64_t max_len = (int64_t)(long long)(ctx->h_range.as<unsigned long long>()[3] ^ 0x8000000000000000ULL);
+  const bool use_gtab = sorted_gpt && !ctx->tuning.no_slice_table && !ctx->tuning.dp_pricing &&
+                        max_len <= (int64_t)1 << 22;
+  const bool price_in_dp = sorted_gpt && !use_gtab && ctx->tuning.dp_pricing;
+  ctx->gtab = false;
+  if (use_gtab) {
+    const int nK = (int)std::max<int64_t>(max_len, 0) + 1;
+    PP_CUDA(ctx->gt_need.ensure((size_t)nK * sizeof(int)));
+    PP_CUDA(ctx->gt_off.ensure((size_t)nK * sizeof(int64_t)));
+    PP_CUDA(ctx->gt_total.ensure(sizeof(long long)));
+    PP_CUDA(ctx->h_gt_total.ensure(sizeof(long long)));
+    PP_CUDA(ctx->gt_base.ensure(std::max<int64_t>(total, 1) * sizeof(int64_t)));
+    PP_CUDA(cudaMemsetAsync(ctx->gt_need.p, 0, (size_t)nK * sizeof(int), st));
+    PP_TIMED(3, launch_gtab_need(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks, ctx->blk_W.as<int>(),
+                                 ctx->in_d.as<double>(), ctx->gt_need.as<int>(), st));
+    PP_TIMED(3, launch_gtab_offsets(ctx->gt_need.as<int>(), nK, ctx->gt_off.as<int64_t>(),
+                                    ctx->gt_total.as<long long>(), st));
+    PP_CUDA(cudaMemcpyAsync(ctx->h_gt_total.p, ctx->gt_total.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(cudaStreamSynchronize(st));
+    const int64_t entries = *ctx->h_gt_total.as<long long>();
+    ctx->gtab_entries = entries;
+    PP_CUDA(ctx->gt_G.ensure((size_t)entries * sizeof(double)));
+    PP_TIMED(3, launch_gtab_fill(g, cap, ctx->mbp.as<AxisPos>(), nK, ctx->gt_need.as<int>(), ctx->gt_off.as<int64_t>(),
+                                 ctx->gt_G.as<double>(), st));
+    PP_TIMED(3, launch_gtab_gbase(ctx->in_d.as<double>(), total, ctx->gt_off.as<int64_t>(),
+                                  ctx->gt_base.as<int64_t>(), st));
+    PP_TIMED(3, launch_gtab_bins(c.d_seg_off, n_seg, ctx->in_d.as<double>(), ctx->gt_base.as<int64_t>(),
+                                 ctx->gt_need.as<int>(), ctx->gt_G.as<double>(), interval, tau_d, small_bm,
+                                 ctx->stats_d.as<SegStats>(), st));
+    ctx->gtab = true;
+    ctx->price = DpPrice{};
+    ctx->price.gbase = ctx->gt_base.as<int64_t>();
+  }
+  if (!price_in_dp && !use_gtab) PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
   PP_CUDA(cudaMemcpyAsync(ctx->band_base.p, band_base.data(), n_seg * sizeof(int64_t),
                           cudaMemcpyHostToDevice, st));
   // (no fill: pass B writes every tile entry, NaN where no slice is feasible)
@@ -821,7 +871,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   }
   int wrote_cmin = 0;
   // Pass B: band + candidate statistics.
-  if (total > 0)
+  if (total > 0 && !use_gtab)
     PP_TIMED(3, launch_cost_pass(1, g, c.d_tabT, c.d_tabM, ctx->in_d.as<double>(), ctx->tgt_d.as<double>(),
                                  ctx->pin.as<AxisPos>(), ctx->ptg.as<AxisPos>(), c.d_seg_off,
                                  ctx->blk_base.as<int>(), n_seg, total_blocks, max_n, ctx->mbp.as<AxisPos>(),
@@ -867,7 +917,9 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     p.p0.pad = 0;
     ctx->price_lay = g.lay_class;
   }
-  if ((wrote_cmin & 1) && !ctx->tuning.no_band_trunc) {
+  if (((wrote_cmin & 1) || use_gtab) && !ctx->tuning.no_band_trunc) {
+    // (the slice-time certificate; the table path records no chunk minima,
+    // so only the bound pass / first wave use it, not the truncation)
     const unsigned long long* hr = ctx->h_range.as<unsigned long long>();
     double lo[2], hi[2];
     for (int q = 0; q < 2; ++q) {
@@ -925,7 +977,7 @@ void place_states(std::vector<WorkItem>& items, int mode, size_t& smem_state, in
 
 bool use_coop(const pp_ctx* ctx, const std::vector<WorkItem>& items, const int64_t* h_seg_off) {
   if (items.empty() || (int)items.size() > kCoopMaxItems) return false;
-  if (ctx->compact || ctx->priced) return false;  // the cooperative pass reads the dense band
+  if (ctx->compact || ctx->priced || ctx->gtab) return false;  // the cooperative pass reads the dense band
   const int64_t min_n = ctx->tuning.coop_min_n > 0 ? ctx->tuning.coop_min_n : kCoopMinN;
   for (const WorkItem& w : items)
     if (h_seg_off[w.seg + 1] - h_seg_off[w.seg] < min_n) return false;
@@ -950,6 +1002,12 @@ int run_coop(pp_ctx* ctx, int mode, int sanitize, const std::vector<WorkItem>& i
   }
   return PP_OK;
 }
+
+// What the DP passes and the assembly read: the band, or (gtab) the call's
+// shared slice table with its per-sample row bases, or (priced) nothing.
+const double* dp_band(const pp_ctx* ctx) { return ctx->gtab ? ctx->gt_G.as<double>() : ctx->band.as<double>(); }
+const DpPrice* dp_price(const pp_ctx* ctx) { return (ctx->gtab || ctx->priced) ? &ctx->price : nullptr; }
+int dp_lay(const pp_ctx* ctx) { return ctx->gtab ? kGtab : ctx->price_lay; }
 
 // The planning pipeline (steps 1-7 above).
 int run_plan(pp_ctx* ctx, const PlanCall& c) {
@@ -1053,7 +1111,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   // pass C: candidate values from the band (segments pass B did not cover)
   bool need_pass_c = false;
   for (int s = 0; s < n_seg; ++s) need_pass_c |= (mode[s] == 0 || mode[s] == 1);
-  if (ctx->priced && total > 0 && !single && need_pass_c) {
+  if ((ctx->priced || ctx->gtab) && total > 0 && !single && need_pass_c) {
     // candidate bins past pass B's bitmap: pass C reads them from the band,
     // so this call materialises it after all (pass B again, storing; its
     // candidate marks are idempotent) and the DP streams it
@@ -1069,6 +1127,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                  ctx->tuning.no_slice_reuse ? 0 : 1, ctx->cmin.as<double>(), nullptr, nullptr,
                                  &wrote, 0, st));
     ctx->priced = false;
+    ctx->gtab = false;
   }
   if (total > 0 && !single && need_pass_c)
     PP_TIMED(6, launch_band_cand(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
@@ -1159,12 +1218,12 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
         PP_TIMED(4, launch_dp_pass(bmode, ctx->bound_items.as<WorkItem>(), (int)bi.size(), smem_state,
                                    state_global, table ? 1 : 0, dp_budget((int)bi.size()), c.d_seg_off,
                                    ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
-                                   ctx->band_base.as<int64_t>(), ctx->band.as<double>(), d_cand, d_cand_off,
+                                   ctx->band_base.as<int64_t>(), dp_band(ctx), d_cand, d_cand_off,
                                    ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
                                    ctx->gstate.as<double>(), 1, nullptr, 0.0, nullptr,
                                    ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                   ctx->row_w.as<int>(), nullptr, ctx->priced ? &ctx->price : nullptr,
-                                   ctx->price_lay, st));
+                                   ctx->row_w.as<int>(), nullptr, dp_price(ctx),
+                                   dp_lay(ctx), st));
       }
       PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
     }
@@ -1233,11 +1292,11 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       PP_TIMED(4, launch_dp_pass(3, ctx->items.as<WorkItem>(), ni, smem_state, state_global, 0, dp_budget(ni),
                                  c.d_seg_off, ctx->blk_base.as<int>(), ctx->blk_W.as<int>(),
                                  ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
-                                 ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
+                                 dp_band(ctx), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
                                  ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, nullptr, 0.0, nullptr,
                                  ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
                                  ctx->row_w.as<int>(), ctx->bound_res.as<ItemResult>(),
-                                 ctx->priced ? &ctx->price : nullptr, ctx->price_lay, st));
+                                 dp_price(ctx), dp_lay(ctx), st));
       PP_TIMED(7, launch_seg_set_bound(ctx->bound_res.as<ItemResult>(), c.opts.replica_count,
                                        ctx->segdp.as<SegDP>(), n_seg, st));
     } else if (use_coop(ctx, items, c.h_seg_off)) {
@@ -1250,13 +1309,13 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       PP_TIMED(5, launch_dp_pass(0, ctx->items.as<WorkItem>(), ni, smem_state, state_global, table ? 1 : 0,
                                  dp_budget(ni), c.d_seg_off, ctx->blk_base.as<int>(),
                                  ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
-                                 ctx->band.as<double>(), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
+                                 dp_band(ctx), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
                                  ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0,
-                                 trunc ? ctx->cmin.as<double>() : nullptr, ctx->trunc_margin,
+                                 (trunc && !ctx->gtab) ? ctx->cmin.as<double>() : nullptr, ctx->trunc_margin,
                                  ctx->dp_cols.as<unsigned long long>(),
                                  ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                 ctx->row_w.as<int>(), nullptr, ctx->priced ? &ctx->price : nullptr,
-                                 ctx->price_lay, st));
+                                 ctx->row_w.as<int>(), nullptr, dp_price(ctx),
+                                 dp_lay(ctx), st));
       counted = true;
     }
     PP_TIMED(7, launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
@@ -1272,12 +1331,12 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   // ---- 7. assembly
   PP_TIMED(7, launch_finalize(ctx->segdp.as<SegDP>(), ctx->best_next.as<int>(), c.d_seg_off,
                               ctx->blk_base.as<int>(), ctx->tile_off.as<int64_t>(),
-                              ctx->band_base.as<int64_t>(), ctx->band.as<double>(),
+                              ctx->band_base.as<int64_t>(), dp_band(ctx),
                               ctx->stats_d.as<SegStats>(), ctx->compact ? ctx->colbase.as<short>() : nullptr,
                               c.d_ordered, c.opts.stage_count,
                               c.opts.replica_count, std::max(max_n, 1), n_seg, c.d_splits, c.d_times,
                               c.d_count, c.d_tmax, c.d_obj, c.d_status, c.d_err,
-                              ctx->priced ? &ctx->price : nullptr, ctx->price_lay, st));
+                              dp_price(ctx), dp_lay(ctx), st));
   unsigned long long dp_cols = 0;
   if (counted)
     PP_CUDA(cudaMemcpyAsync(&dp_cols, ctx->dp_cols.p, sizeof(dp_cols), cudaMemcpyDeviceToHost, st));
@@ -1310,7 +1369,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     S.launches[ctx->kcat[k]] += 1;
   }
   S.dp_band_bytes = transitions * (int64_t)sizeof(double);
-  S.band_bytes = ctx->priced ? 0 : ctx->band_total * (int64_t)sizeof(double);
+  S.band_bytes = (ctx->priced || ctx->gtab) ? 0 : ctx->band_total * (int64_t)sizeof(double);
   S.exit_thresh = ctx->exit_thresh;
   for (int s = 0; s < n_seg; ++s) {
     S.slices_pass_a += (int64_t)hs[s].priced;
@@ -1491,7 +1550,7 @@ int pp_ctx_destroy(pp_ctx* ctx) {
     h.hoff.release();
   }
   for (DevBuf* b : ctx->all_bufs()) b->release();
-  for (PinBuf* b : {&ctx->h_range, &ctx->h_stats, &ctx->h_segdp}) b->release();
+  for (PinBuf* b : {&ctx->h_range, &ctx->h_stats, &ctx->h_segdp, &ctx->h_gt_total}) b->release();
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->kev) cudaEventDestroy(e);

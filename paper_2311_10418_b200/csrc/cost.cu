@@ -770,7 +770,7 @@ __global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per 
   __shared__ double s_tau[kSmallBmWords * 32];
   __shared__ double s_x[kCostWarps][32];
   __shared__ AxisPos s_px[kCostWarps][32];
-  __shared__ double s_ring[kCostWarps][128];
+  __shared__ double s_ring[kCostWarps][160];  // 128 diagonals + a mirror of the first 32 (no wrap on reads)
   __shared__ short s_cb[kCostWarps][32];
   __shared__ int s_rmq[kCostWarps][5][32];
   __shared__ unsigned int s_bm[kCostWarps][kSmallBmWords];
@@ -809,6 +809,10 @@ __global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per 
     const int r = lane;
     const bool rowv = r < i1 - i0;
     const int wr = rowv ? a.row_w[b0 + i0 + r] : 0;  // 0: never live
+    // the last tile column on which every row of the tile is live
+    int minlive = r + wr;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) minlive = min(minlive, __shfl_xor_sync(0xffffffffu, minlive, o));
     // range-max table over the tile's row widths (levels 0..4: windows of 2^L rows)
     {
       int m = wr;
@@ -939,6 +943,7 @@ __global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per 
           const int d = done + 1 + lane;
           const double F = price(a.mbp[min(max(d, 1), a.max_n)], pe);
           ring[d & 127] = F;
+          if ((d & 127) < 32) ring[(d & 127) + 128] = F;
           // live slices carrying (d, run): rows r' in [ca - d, cb - d] with w_r' >= d
           const int lo = max(ca - d, 0), hi = min(cb - d, 31);
           if ((d >= 1) && (lo <= hi) && !isnan(F) && rmq(lo, hi) >= d) bin(F);
@@ -955,13 +960,30 @@ __global__ void __launch_bounds__(32 * kCostWarps, 4)  // 4 CTAs (32 warps) per 
         } else if (!NOSTORE) {
           // column c: lane r stores ring[d = c - r], live iff 1 <= d <= w_r
           double* out = tile + (size_t)cs * kRB + r;
-          int d = cs - r;
+          // the lane's diagonals of the piece sit at ring[b .. b + ce - cs]
+          // without wrapping (the ring's mirrored upper half)
+          const double* src = ring + ((cs - r) & 127);
+          if (cs >= kRB && ce <= minlive) {
+            // every row live on every column of the piece: a plain copy
+            const int L = ce - cs + 1;
+            int k = 0;
+            for (; k + 4 <= L; k += 4) {
+              const double v0 = src[k], v1 = src[k + 1], v2 = src[k + 2], v3 = src[k + 3];
+              out[(size_t)k * kRB] = v0;
+              out[(size_t)(k + 1) * kRB] = v1;
+              out[(size_t)(k + 2) * kRB] = v2;
+              out[(size_t)(k + 3) * kRB] = v3;
+            }
+            for (; k < L; ++k) out[(size_t)k * kRB] = src[k];
+          } else {
+            int d = cs - r;
 #pragma unroll 2
-          for (int c = cs; c <= ce; ++c) {
-            const double v = ring[d & 127];
-            *out = ((unsigned)(d - 1) < (unsigned)wr) ? v : QNAN;
-            out += kRB;
-            ++d;
+            for (int c = cs; c <= ce; ++c) {
+              const double v = *src++;
+              *out = ((unsigned)(d - 1) < (unsigned)wr) ? v : QNAN;
+              out += kRB;
+              ++d;
+            }
           }
         }
         __syncwarp();

@@ -137,6 +137,16 @@ __device__ __forceinline__ int far_chunks_needed(int nc, const double* __restric
   return nc;
 }
 
+// ---- cp.async (8-byte, generic proxy) with mbarrier completion ------------
+__device__ __forceinline__ void cp_async_8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// the mbarrier's phase counts this thread's prior cp.async copies as one of its
+// expected arrivals, delivered when they have all landed
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // ---- in-kernel slice pricing (PRICE != 0) ---------------------------------
 // On length-sorted single-input mini-batches (GPT) the band is never
 // materialised: slice [i, j) depends only on (d = j - i, in[j-1])
@@ -248,6 +258,10 @@ __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int
 //   price every tile entry themselves (walk_columns above): the near tile of
 //   block b+1 into the dense near buffer and the far-far columns of block b+1
 //   straight into their reductions, during block b; the producer warp idles.
+// PRICE == kGtab: the producer streams the tiles from the call's shared
+//   slice table G (gtab.cu: `band` points at G, pr.gbase per sample) with
+//   cp.async, 8 B per lane and one tile column per warp instruction; the
+//   table is L2-resident, the band does not exist.
 template <int MODE, bool SMEM_STATE, bool SANITIZE, bool COMPACT, int PRICE>
 __global__ void __launch_bounds__(kDpThreads, 2)
     dp_pass_kernel(const WorkItem* __restrict__ items, const int64_t* __restrict__ seg_off,
@@ -261,6 +275,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
                    const int* __restrict__ chunk_nv, const int* __restrict__ row_w,
                    ItemResult* __restrict__ res2, DpPrice pr) {
   extern __shared__ __align__(128) unsigned char smem[];
+  constexpr bool INK = PRICE == kLayDec1 || PRICE == kLayEncDec2;  // in-kernel pricing
+  constexpr bool GTAB = PRICE == kGtab;                           // tiles from the shared table
   double* near = reinterpret_cast<double*>(smem + DpSmem::near);
   double* ring = reinterpret_cast<double*>(smem + ring_off);
   double* wps = reinterpret_cast<double*>(smem + DpSmem::wps);
@@ -331,11 +347,11 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   // ---- prologue
   if (threadIdx.x == 0) {
     for (int k = 0; k < kNearBufs; ++k) {
-      mbar_init(&near_full[k], 1);
+      mbar_init(&near_full[k], GTAB ? 32 : 1);  // GTAB: one cp.async arrive per producer lane
       mbar_init(&near_empty[k], 1);   // the chain warp releases a near tile
     }
     for (int k = 0; k < kRing; ++k) {
-      mbar_init(&ring_full[k], 1);
+      mbar_init(&ring_full[k], GTAB ? 32 : 1);
       mbar_init(&ring_empty[k], kWorkers);  // every worker warp releases a chunk
     }
     mbar_fence_init();
@@ -365,7 +381,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   // and the staged lengths of its current columns
   SlicePricer SP{};
   WalkScratch ws{};
-  if (PRICE) {
+  if (INK) {
     const int cells = pr.cells;
     double4* s_tt = reinterpret_cast<double4*>(smem + ring_off);
     double2* s_am = reinterpret_cast<double2*>(s_tt + (PRICE == kLayEncDec2 ? 2 : 1) * cells);
@@ -389,8 +405,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     ws.px = reinterpret_cast<AxisPos*>(ws.x + 32);
   }
   __syncthreads();
-  const double* seg_len = PRICE ? pr.in_d + b0 - 1 : nullptr;  // + row i0 + column c: in[i0 + c - 1]
-  const AxisPos* seg_pos = PRICE ? pr.pin + b0 - 1 : nullptr;
+  const double* seg_len = INK ? pr.in_d + b0 - 1 : nullptr;  // + row i0 + column c: in[i0 + c - 1]
+  const AxisPos* seg_pos = INK ? pr.pin + b0 - 1 : nullptr;
   // PRICE: the dense near tile (columns [0, min(64, W)) of block bb, first
   // row k0) into near buffer bb % 2; worker w prices columns [8w, 8w + 8)
   auto price_near = [&](int bb) {
@@ -399,10 +415,10 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     const int c_lo = min(8 * wid, cmax), c_hi = min(8 * wid + 8, cmax);
     double* dst = near + (size_t)(bb % kNearBufs) * kNearCols * kRB;
     if (c_lo < c_hi)
-      walk_columns<PRICE ? PRICE : kLayDec1>(pr, SP, seg_len + kk0, seg_pos + kk0, c_lo, c_hi, ws, lane,
+      walk_columns<INK ? PRICE : kLayDec1>(pr, SP, seg_len + kk0, seg_pos + kk0, c_lo, c_hi, ws, lane,
                                             [&](int c, double x, int) { dst[c * kRB + lane] = x; });
   };
-  if (PRICE) {
+  if (INK) {
     if (wid == kProducerWarp) return;  // (no band to stream)
     if (wid == 0 && lane == 0 && cols_streamed && nblk > 0)
       atomicAdd(cols_streamed, (unsigned long long)min(kNearCols, blk_W[gb0]));
@@ -415,10 +431,56 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   // workers consume during block b-1), each into a buffer its consumers
   // released through the matching "empty" mbarrier.  It never joins the
   // block barrier, so it runs ahead by up to the ring depth.
-  if (!PRICE && wid == kProducerWarp) {
+  if (!INK && wid == kProducerWarp) {
     // Issue order = consumption order: near tile of block b (used during
     // block b), then the far-far chunks of block b+1 (used by the workers
     // during block b), so far chunks never queue behind a near-buffer wait.
+    if (GTAB) {
+      // tile column c of the block whose first row is ii0: lane r's entry is
+      // G[gbase[sample j - 1] + (c - r)] (d = c - r), column 0 the NaN row
+      const double* G = band;
+      auto issue_cols = [&](double* dst, int ii0, int c0, int cols) {
+        const int c = c0 + lane;
+        const long long bq = lane < cols ? (c == 0 ? 31LL : (long long)pr.gbase[b0 + ii0 + c - 1] + c) : 0LL;
+        for (int q = 0; q < cols; ++q) {
+          const long long base = __shfl_sync(0xffffffffu, bq, q);
+          cp_async_8(dst + q * kRB + lane, G + base - lane);
+        }
+      };
+      int islot = 0, iround = 0;
+      long long ncols_total = 0;
+      for (int b = 0; b < nblk; ++b) {
+        const int gb = gb0 + b;
+        const int W = blk_W[gb];
+        const int nsl = b % kNearBufs;
+        const int ncols = min(kNearCols, W);
+        const int ii0 = max(0, n - kRB * (b + 1));
+        ncols_total += ncols;
+        if (b >= kNearBufs) mbar_wait(&near_empty[nsl], ((b / kNearBufs) - 1) & 1);
+        issue_cols(near + (size_t)nsl * kNearCols * kRB, ii0, 0, min(ncols, 32));
+        if (ncols > 32) issue_cols(near + (size_t)nsl * kNearCols * kRB + 32 * kRB, ii0, 32, ncols - 32);
+        cp_async_arrive_noinc(&near_full[nsl]);
+        if (b + 1 >= nblk) break;
+        const int gn = gb + 1;
+        const int Wn = blk_W[gn];
+        const int k0n = max(0, n - kRB * (b + 2));
+        const int nc = far_nc(gn, Wn);
+        ncols_total += nc > 0 ? min(Wn, kNearCols + nc * kChunkCols) - kNearCols : 0;
+        for (int k = 0; k < nc; ++k) {
+          const int c0 = kNearCols + k * kChunkCols;
+          const int cols = min(kChunkCols, Wn - c0);
+          if (iround > 0) mbar_wait(&ring_empty[islot], (iround - 1) & 1);
+          issue_cols(ring + (size_t)islot * kChunkCols * kRB, k0n, c0, cols);
+          cp_async_arrive_noinc(&ring_full[islot]);
+          if (++islot == kRing) {
+            islot = 0;
+            ++iround;
+          }
+        }
+      }
+      if (lane == 0 && cols_streamed) atomicAdd(cols_streamed, (unsigned long long)ncols_total);
+      return;
+    }
     int islot = 0, iround = 0;
     long long ncols_total = 0;  // tile columns streamed (the transitions this pass visits / 32)
     for (int b = 0; b < nblk; ++b) {
@@ -497,7 +559,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     if (wid < kWorkers) {
       const int W = blk_W[gb0 + b];
       const int r = lane;
-      if (!PRICE) mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
+      if (!INK) mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
       double s1 = INF, m1 = INF, b1 = INF;
       int c1 = 0, j1 = INT_MAX;
       const int cnf = min(kNearCols, W);
@@ -550,7 +612,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       } else {
         if (MODE == 1) am = pm[pbuf];
       }
-      if (!PRICE) mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
+      if (!INK) mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
     }
     named_bar(3, kSyncThreads);
 
@@ -652,7 +714,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       // release (__syncwarp + mbarrier arrive), and the producer's next TMA
       // write into the buffer waits for it (the TMA pipeline WAR pattern)
       __syncwarp();
-      if (!PRICE && lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);
+      if (!INK && lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);
       PP_TRACE(3);
       if (r < nb) {
         const int row = i0 + r;
@@ -695,7 +757,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         int ac = 0, aj = INT_MAX, ac2 = 0, aj2 = INT_MAX;
         const int r = lane;
 
-        if (PRICE) {
+        if (INK) {
           // block b+1's near tile for the chain and phase 1 of the next block ...
           price_near(bn);
           // ... and its far-far columns [64, Weff), worker w a contiguous share
@@ -737,9 +799,9 @@ __global__ void __launch_bounds__(kDpThreads, 2)
             }
           };
           if (cw0 < cw1)
-            walk_columns<PRICE ? PRICE : kLayDec1>(pr, SP, seg_len + k0, seg_pos + k0, cw0, cw1, ws, lane, upd);
+            walk_columns<INK ? PRICE : kLayDec1>(pr, SP, seg_len + k0, seg_pos + k0, cw0, cw1, ws, lane, upd);
         }
-        for (int k = 0; k < (PRICE ? 0 : nc); ++k) {
+        for (int k = 0; k < (INK ? 0 : nc); ++k) {
           mbar_wait(&ring_full[cslot], cphase);
           const double* ch = ring + (size_t)cslot * kChunkCols * kRB;
           const int c0 = kNearCols + k * kChunkCols;
@@ -1178,7 +1240,18 @@ __global__ void __launch_bounds__(256)
       }
     }
     double v[kU];
-    if (price_lay) {  // no band: price the chosen slices like the DP did (walk_columns)
+    if (price_lay == kGtab) {  // the shared slice table (gtab.cu): G[gbase(j - 1) + (j - i)]
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = kb + u * blockDim.x;
+        v[u] = 0.0;
+        if (k < m) {
+          const int j = sp[k];
+          const int i = k ? sp[k - 1] : 0;
+          v[u] = __ldg(band + __ldg(pr.gbase + b + j - 1) + (j - i));
+        }
+      }
+    } else if (price_lay) {  // no band: price the chosen slices like the DP did (walk_columns)
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int k = kb + u * blockDim.x;
@@ -1276,10 +1349,11 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
   int ring = 0;
   size_t smem;
   DpPrice pr{};
-  if (price) {
+  if (price && price_lay != kGtab) {
     pr = *price;
     smem = ring_off + dp_price_smem(price_lay, pr.cells);
   } else {
+    if (price) pr = *price;
     ring = (int)std::min<size_t>(kMaxRing, (smem_budget - std::min(smem_budget, ring_off)) / kChunkBytes);
     ring = std::max(ring, 4);
     smem = ring_off + (size_t)ring * kChunkBytes;
@@ -1295,7 +1369,8 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
   } while (0)
 #define PP_DP_LAUNCH_Z(M, S)                                                 \
   do {                                                                       \
-    if (price && price_lay == kLayDec1) PP_DP_LAUNCH(M, S, false, false, kLayDec1);        \
+    if (price && price_lay == kGtab) PP_DP_LAUNCH(M, S, false, false, kGtab);              \
+    else if (price && price_lay == kLayDec1) PP_DP_LAUNCH(M, S, false, false, kLayDec1);   \
     else if (price) PP_DP_LAUNCH(M, S, false, false, kLayEncDec2);           \
     else if (compact) PP_DP_LAUNCH(M, S, false, true, 0);                    \
     else if (sanitize) PP_DP_LAUNCH(M, S, true, false, 0);                   \

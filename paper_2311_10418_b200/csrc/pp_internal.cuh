@@ -292,6 +292,11 @@ __device__ __forceinline__ double price_slice(const SlicePricer& P, const AxisPo
 // cells live in global memory here and are staged into shared memory by
 // each DP CTA; per micro-batch size the mbs bracket, per ordered sample the
 // sequence bracket of its input length and the length itself.
+// PRICE / price_lay value of the shared-table path (gtab.cu): the DP's tiles
+// come from the call's table G[length][d] instead of the band or in-kernel
+// pricing.
+constexpr int kGtab = 3;
+
 struct DpPrice {
   SlicePricer P;          // global-memory cells
   int cells;              // cells per kind (nm * ns)
@@ -300,6 +305,7 @@ struct DpPrice {
   const double* in_d;     // [total]
   int max_n;
   AxisPos p0;             // bracket of length 0 (padded lengths start at 0)
+  const int64_t* gbase;   // kGtab: per ordered sample, its length's table row at d = 0
 };
 
 // Rows per band tile (= rows per DP block).  The band of a segment is stored

@@ -169,7 +169,8 @@ def test_band_truncation_matches_full_stream(name):
     off = W.seg_offsets(cfg, M)
     a = capi.Planner(0)
     b = capi.Planner(0)
-    b.set_tuning(band_trunc=False)
+    a.set_tuning(slice_table=False)  # the truncation lives on the band path
+    b.set_tuning(band_trunc=False, slice_table=False)
     ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     for k in ("ordered", "count", "t_max_used", "objective", "status"):
@@ -197,6 +198,7 @@ def test_compact_band_matches_dense_band(name):
     a = capi.Planner(0)
     b = capi.Planner(0)
     a.set_tuning(compact_band=True)
+    b.set_tuning(slice_table=False)
     ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     for k in ("ordered", "count", "t_max_used", "objective", "status"):
@@ -213,6 +215,69 @@ def test_compact_band_matches_dense_band(name):
 
 
 @pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_slice_table_matches_band(name):
+    """The call's shared slice table (gtab.cu: G[length][d] priced once, the
+    DP's tiles and the candidate scan read from it) against the per
+    mini-batch band of cost pass B: identical plans, candidate sets,
+    reference-loop counts and bound transitions; no band written."""
+    cfg = W.CONFIGS[name]
+    M = {"C1": 64, "C3": 6, "C4": 24}[name]
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    a = capi.Planner(0)
+    b = capi.Planner(0)
+    b.set_tuning(slice_table=False, band_trunc=False)  # (the table path streams whole tiles)
+    ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    sa = a.stats()
+    rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+    sb = b.stats()
+    assert sa["band_bytes"] == 0 and sb["band_bytes"] > 0
+    for k in ("ordered", "count", "t_max_used", "objective", "status"):
+        assert ra[k].tobytes() == rb[k].tobytes(), k
+    for q in range(M):
+        m = int(ra["count"][q])
+        for k in ("splits", "mb_times"):
+            assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
+    for k in ("candidates_generated", "candidates_ref_evaluated", "bound_transitions"):
+        assert sa[k] == sb[k], k
+    a.close()
+    b.close()
+
+
+def test_slice_table_random_vs_oracle(orc):
+    """The slice-table path on random length-sorted GPT mini-batches
+    (duplicate-heavy and distinct lengths, binding and loose caps, several
+    intervals, stage counts and recompute strategies, several mini-batches
+    per call sharing one table) against the C restatement."""
+    grid = capi.synthetic_grid()
+    rng = np.random.default_rng(777)
+    p = capi.Planner(0)
+    for k in range(30):
+        M = int(rng.integers(1, 5))
+        n = int(rng.integers(1, 600))
+        L = int(rng.choice([8, 64, 1024, 8192, 60000]))
+        s = capi.synthetic_dataset(n * M, L, 5000 + k, W.INPUT_DIST)
+        s[:, 0] = rng.permutation(n * M) + 3
+        C = int(rng.choice([2, 4, 16]))
+        model = capi.Model.uniform(C, int(rng.integers(1, 4)), False, recompute=int(rng.integers(0, 3)))
+        o = orc.order_samples(s[:n])
+        act = max(orc.slice_cost(grid, model, o, i, i + 1)[1] for i in range(n))
+        cap = float(rng.choice([math.inf, 1.0 * act, 3.0 * act, 40.0 * act]))
+        tot = orc.slice_cost(grid, model, o, 0, n)[0]
+        interval = float(rng.choice([5.0, tot / 7.0, tot / 64.0, tot / 300.0]))
+        off = np.arange(M + 1, dtype=np.int64) * n
+        r = p.plan_batch(s, off, grid, model, C, 1, cap, interval)
+        for q in range(M):
+            a = orc.plan(s[off[q]:off[q + 1]], grid, model, C, 1, cap, interval)
+            m = int(r["count"][q])
+            got = capi.Plan(int(r["status"][q]), r["splits"][off[q]:off[q] + m], r["mb_times"][off[q]:off[q] + m],
+                            float(r["t_max_used"][q]), float(r["objective"][q]), int(r["err_sample_id"][q]),
+                            r["ordered"][off[q]:off[q + 1]])
+            assert_plan_matches(got, record(a), f"table {k}.{q}: n={n} C={C} I={interval} cap={cap}")
+    p.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
 def test_dp_pricing_matches_band(name):
     """The DP pricing its own slices (dp.cu PRICE: no band in HBM, pass B
     only marks candidates) against the band path (pass B writes the band, the
@@ -224,6 +289,7 @@ def test_dp_pricing_matches_band(name):
     a = capi.Planner(0)
     b = capi.Planner(0)
     a.set_tuning(dp_pricing=True)
+    b.set_tuning(slice_table=False)
     ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     sa = a.stats()
     rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
