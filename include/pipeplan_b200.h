@@ -123,18 +123,12 @@ typedef struct pp_tuning {
   int32_t no_band_trunc;   /* 1: candidate DP passes stream every tile column; 0 (default):
                               on certified length-sorted tiles they stop at the first
                               32-column chunk whose slices all exceed the candidate */
-  int32_t compact_band;    /* 1: length-sorted single-input mini-batches get compact far
-                              chunk records (the distinct diagonal windows, ~1/4 of the
-                              DP's band traffic) instead of the dense band; 0 (default):
-                              dense — the DP passes are issue-bound on a B200, and the
-                              record indirection costs more than the bytes it saves */
+  int32_t compact_band;    /* retired (ignored): compact far-chunk records were measured slower
+                              than dense tiles; the DP no longer reads them */
   int32_t host_chunks;     /* host-buffer calls with streams > 1: chunks per worker (0 =
                               default 2; 1 = no intra-worker prefetch) */
-  int32_t dp_pricing;      /* 1: on length-sorted single-input mini-batches the DP prices
-                              its slices in-kernel and no band exists in HBM (cost pass B
-                              only marks candidates); 0 (default): pass B writes the band
-                              and the DP streams it — faster on a B200, where the priced
-                              DP is latency-bound at two CTAs per SM */
+  int32_t dp_pricing;      /* retired (ignored): in-DP slice pricing was measured slower than
+                              the shared slice table (no_slice_table = 0) */
   int32_t no_slice_table;  /* 1: length-sorted single-input mini-batches get a per-mini-batch
                               band from cost pass B; 0 (default): ONE slice table per call,
                               G[length][d] (a slice of such a mini-batch depends on its size

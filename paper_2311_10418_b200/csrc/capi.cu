@@ -68,7 +68,7 @@ cudaError_t launch_gtab_need(const int64_t* seg_off, const int* blk_base, int n_
                              const int* blk_W, const double* in_d, int* need, cudaStream_t st);
 cudaError_t launch_gtab_offsets(const int* need, int nK, int64_t* row_off, long long* total, cudaStream_t st);
 cudaError_t launch_gtab_fill(const CostGrid& g, double cap, const AxisPos* mbp, int nK, const int* need,
-                             const int64_t* row_off, double* G, cudaStream_t st);
+                             const int64_t* row_off, double* G, double* G1, cudaStream_t st);
 cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* row_off, int64_t* gbase,
                               cudaStream_t st);
 cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int64_t* gbase,
@@ -103,8 +103,7 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int64_t* seg_band_base, const double* band, const double* cand,
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, const double* cmin, double t_margin,
-                           unsigned long long* cols_streamed, const short* colbase, const int* chunk_nv,
-                           const int* row_w, ItemResult* res2, const DpPrice* price, int price_lay,
+                           unsigned long long* cols_streamed, ItemResult* res2, const int64_t* gbase,
                            cudaStream_t st);
 cudaError_t launch_seg_set_bound(const ItemResult* bound_res, int replicas, SegDP* dp, int n_seg,
                                  cudaStream_t st);
@@ -384,8 +383,9 @@ struct PlanCall {
 int validate_opts(pp_ctx* ctx, const pp_dp_options& o) {
   if (o.stage_count < 1 || o.replica_count < 1)
     return fail(ctx, PP_ERR_INVALID, "stage and replica counts must be >= 1");
-  if (o.t_max_interval < 0 || std::isnan(o.t_max_interval))
-    return fail(ctx, PP_ERR_INVALID, "t_max_interval must be >= 0");
+  // (a NaN interval is not rejected: the reference's `< 0` test passes it and
+  // its `> 0` test then selects the exact candidate set, microbatch.cpp:225,263)
+  if (o.t_max_interval < 0) return fail(ctx, PP_ERR_INVALID, "t_max_interval must be >= 0");
   return PP_OK;
 }
 
@@ -837,9 +837,11 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     PP_CUDA(cudaStreamSynchronize(st));
     const int64_t entries = *ctx->h_gt_total.as<long long>();
     ctx->gtab_entries = entries;
-    PP_CUDA(ctx->gt_G.ensure((size_t)entries * sizeof(double)));
+    // G, then its copy shifted by one entry (starting 16 B aligned)
+    const int64_t g1_at = (entries + 2) & ~(int64_t)1;
+    PP_CUDA(ctx->gt_G.ensure((size_t)(g1_at + entries + 2) * sizeof(double)));
     PP_TIMED(3, launch_gtab_fill(g, cap, ctx->mbp.as<AxisPos>(), nK, ctx->gt_need.as<int>(), ctx->gt_off.as<int64_t>(),
-                                 ctx->gt_G.as<double>(), st));
+                                 ctx->gt_G.as<double>(), ctx->gt_G.as<double>() + g1_at, st));
     PP_TIMED(3, launch_gtab_gbase(ctx->in_d.as<double>(), total, ctx->gt_off.as<int64_t>(),
                                   ctx->gt_base.as<int64_t>(), st));
     PP_TIMED(3, launch_gtab_bins(c.d_seg_off, n_seg, ctx->in_d.as<double>(), ctx->gt_base.as<int64_t>(),
@@ -848,6 +850,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     ctx->gtab = true;
     ctx->price = DpPrice{};
     ctx->price.gbase = ctx->gt_base.as<int64_t>();
+    ctx->price.g_odd = ctx->gt_G.as<double>() + g1_at;
   }
   if (!price_in_dp && !use_gtab) PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
   PP_CUDA(cudaMemcpyAsync(ctx->band_base.p, band_base.data(), n_seg * sizeof(int64_t),
@@ -941,15 +944,12 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
 size_t dp_budget(int n_items) { return n_items <= 148 ? 220 * 1024 : 110 * 1024; }
 
 void state_layout(int mode, int n, int wmax, unsigned& mask, int& entries, size_t& smem) {
-  // a ring of R >= W_max + 64 slots (a multiple of 32; dp.cu indexes it mod R)
-  const int R = (wmax + 64 + 31) / 32 * 32;
-  if (R < n + 1) {
-    mask = (unsigned)(R - 1);  // (any value but ~0: "a ring")
-    entries = R;
-  } else {
-    mask = ~0u;
-    entries = n + 1;
-  }
+  // R slots, a multiple of 32, indexed (j + shift) mod R (dp.cu, shift < 32):
+  // a ring of R >= W_max + 64 (the live states), or the whole row range
+  const int R_ring = (wmax + 64 + 31) / 32 * 32;
+  const int R_full = (n + 32 + 31) / 32 * 32;
+  entries = std::min(R_ring, R_full);
+  mask = entries < R_full ? (unsigned)(entries - 1) : ~0u;  // (informational)
   smem = dp_smem_fixed() + dp_state_bytes(mode, entries);
 }
 
@@ -965,8 +965,8 @@ void place_states(std::vector<WorkItem>& items, int mode, size_t& smem_state, in
     if (dp_smem_fixed() + dp_state_bytes(mode, w.state_entries) > kDpSmemLimit) state_global = 1;
   for (WorkItem& w : items) {
     if (state_global) {
-      w.state_off = goff;
-      goff += (int64_t)((dp_state_bytes(mode, w.state_entries) + 7) / 8);
+      w.state_off = goff;  // (16-byte aligned: the DP's vector state loads)
+      goff += ((int64_t)((dp_state_bytes(mode, w.state_entries) + 7) / 8) + 1) & ~(int64_t)1;
     } else {
       w.state_off = -1;
       smem_state = std::max(smem_state, dp_state_bytes(mode, w.state_entries));
@@ -1008,6 +1008,8 @@ int run_coop(pp_ctx* ctx, int mode, int sanitize, const std::vector<WorkItem>& i
 const double* dp_band(const pp_ctx* ctx) { return ctx->gtab ? ctx->gt_G.as<double>() : ctx->band.as<double>(); }
 const DpPrice* dp_price(const pp_ctx* ctx) { return (ctx->gtab || ctx->priced) ? &ctx->price : nullptr; }
 int dp_lay(const pp_ctx* ctx) { return ctx->gtab ? kGtab : ctx->price_lay; }
+// The DP's per-sample slice-table row bases (slice-table path), or null (band).
+const int64_t* dp_gbase(const pp_ctx* ctx) { return ctx->gtab ? ctx->gt_base.as<int64_t>() : nullptr; }
 
 // The planning pipeline (steps 1-7 above).
 int run_plan(pp_ctx* ctx, const PlanCall& c) {
@@ -1029,7 +1031,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     if (rc) return rc;
   }
   PP_CUDA(cudaEventRecord(ctx->ev[0], st));
-  const double I = c.opts.t_max_interval;
+  // NaN -> 0: exact candidate set, as the reference's `interval > 0` test (microbatch.cpp:263)
+  const double I = c.opts.t_max_interval > 0 ? c.opts.t_max_interval : 0.0;
   const bool table = c.d_tabT != nullptr;
   std::vector<int> blk_base;
   int max_n = 0;
@@ -1220,10 +1223,8 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                    ctx->blk_base.as<int>(), ctx->blk_W.as<int>(), ctx->tile_off.as<int64_t>(),
                                    ctx->band_base.as<int64_t>(), dp_band(ctx), d_cand, d_cand_off,
                                    ctx->bound_res.as<ItemResult>(), ctx->next_buf.as<int>(),
-                                   ctx->gstate.as<double>(), 1, nullptr, 0.0, nullptr,
-                                   ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                   ctx->row_w.as<int>(), nullptr, dp_price(ctx),
-                                   dp_lay(ctx), st));
+                                   ctx->gstate.as<double>(), 1, nullptr, 0.0, nullptr, nullptr,
+                                   dp_gbase(ctx), st));
       }
       PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
     }
@@ -1294,9 +1295,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                  ctx->tile_off.as<int64_t>(), ctx->band_base.as<int64_t>(),
                                  dp_band(ctx), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
                                  ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0, nullptr, 0.0, nullptr,
-                                 ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                 ctx->row_w.as<int>(), ctx->bound_res.as<ItemResult>(),
-                                 dp_price(ctx), dp_lay(ctx), st));
+                                 ctx->bound_res.as<ItemResult>(), dp_gbase(ctx), st));
       PP_TIMED(7, launch_seg_set_bound(ctx->bound_res.as<ItemResult>(), c.opts.replica_count,
                                        ctx->segdp.as<SegDP>(), n_seg, st));
     } else if (use_coop(ctx, items, c.h_seg_off)) {
@@ -1312,10 +1311,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                  dp_band(ctx), d_cand, d_cand_off, ctx->results.as<ItemResult>(),
                                  ctx->next_buf.as<int>(), ctx->gstate.as<double>(), 0,
                                  (trunc && !ctx->gtab) ? ctx->cmin.as<double>() : nullptr, ctx->trunc_margin,
-                                 ctx->dp_cols.as<unsigned long long>(),
-                                 ctx->compact ? ctx->colbase.as<short>() : nullptr, ctx->chunk_nv.as<int>(),
-                                 ctx->row_w.as<int>(), nullptr, dp_price(ctx),
-                                 dp_lay(ctx), st));
+                                 ctx->dp_cols.as<unsigned long long>(), nullptr, dp_gbase(ctx), st));
       counted = true;
     }
     PP_TIMED(7, launch_select(ctx->items.as<WorkItem>(), ctx->results.as<ItemResult>(),
@@ -1564,6 +1560,11 @@ const char* pp_ctx_last_error(const pp_ctx* ctx) { return ctx ? ctx->err.c_str()
 int pp_ctx_set_tuning(pp_ctx* ctx, const pp_tuning* t) {
   if (!ctx || !t || t->first_wave < 1 || t->streams < 0 || t->streams > 16) return PP_ERR_INVALID;
   ctx->tuning = *t;
+  // retired knobs (the DP reads dense tiles or the slice table only): the
+  // compact band records and the in-DP pricing were measured slower
+  // and the DP kernel no longer has those variants
+  ctx->tuning.compact_band = 0;
+  ctx->tuning.dp_pricing = 0;
   return PP_OK;
 }
 

@@ -18,38 +18,50 @@
 // yields the reference's state bit-for-bit.
 //
 // CTA schedule (never changes results).  Rows are processed top-down in
-// 32-row blocks; the band of a block is one tile (cost.cu): column c holds
-// T[i0 + r, i0 + c] for the 32 rows r.  For block b:
-//   * warp 0 (the chain warp) takes the folded far-far partial, the near-far
-//     columns [nb, 64) (four interleaved accumulators) and then runs the
-//     in-block triangle serially: lane r owns row i0 + r; walking
-//     jj = nb-1 .. 0, lane jj's row is final and is broadcast with shuffles,
-//     the lanes below fold T[i0 + r, i0 + jj] + state into their
-//     accumulators with predicated selects (no divergence, no stores until
-//     the block ends);
-//   * warps 1..8 (workers) meanwhile reduce the far-far columns [64, W) of
-//     block b+1, whose states (j >= i1(b)) are already final, and fold their
-//     eight partials into one per row off the chain's critical path;
-//   * the near tile (columns [0, 64)) of each block and the far-far columns in
-//     32-column chunks are streamed global -> shared by TMA bulk copies
-//     (cp.async.bulk, mbarrier completion), issued by one worker thread ahead
-//     of use through a ring of chunk buffers, so the serial chain never waits
-//     on global memory.
-// DP state lives in shared memory, as a ring of R >= W_max + 64 entries when
-// the memory cap bounds the row widths.
+// 32-row blocks; block b's tile (cost.cu band, or the call's slice table G,
+// gtab.cu) has column c = T[i0 + r, i0 + c] for its 32 rows r.  Columns split
+// into the triangle [0, nb) (in-block j), the near-far columns [nb, nb + 32)
+// (j = the previous block's rows), and the far-far columns [64, W).
+//   * workers (warps 0..7) reduce the far-far columns of block b+1 while the
+//     chain runs block b (their states are final), four contiguous columns per
+//     warp and 32-column chunk, and fold their eight partials into one;
+//   * the chain warp (warp 9) runs block b's triangle.  Its critical path is
+//     the row-to-row dependency state[k] <- T[k, k+1] + state[k+1]: instead of
+//     broadcasting each newly final row with a shuffle (a shuffle round trip
+//     per row), EVERY lane recomputes state[k] itself from
+//       H_k = lane k's accumulator over columns >= k+2 (shuffled one row ahead,
+//             off the critical path) and the tile entry T[k, k+1] (a
+//             broadcast shared load),
+//     with exactly lane k's own operations, so the copies are bit-identical
+//     to what lane k stores.  As each state[k] appears, lane l folds
+//     T[l, k] + state[k] into its own row (l < k) AND T'[l, nb' + k] into row
+//     l of the NEXT block — the next block's near-far columns are reduced on
+//     the fly, so no separate near-far phase or partial fold sits between
+//     blocks;
+//   * the producer warp (warp 8) stages, per block, a 64-column "unit" (the
+//     triangle of block u and the near-far columns of block u+1) and, on the
+//     band path, the far-far chunks through a ring, with TMA bulk copies and
+//     mbarriers; on the slice-table path it fills the units with coalesced
+//     loads of G and the workers read their far-far entries from G directly
+//     (L2/L1-resident, no ring).
+// DP state lives in shared memory (or an L2-resident global array), indexed
+// slot(j) = (j + shift) mod R with shift = -n mod 32, so every far-far chunk
+// starts at a 32-aligned slot and a worker's four columns load with 16-byte
+// vector loads.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 
 #include "pp_internal.cuh"
 
 namespace ppb {
 
 constexpr int kWorkers = 8;
-constexpr int kDpThreads = 32 * (2 + kWorkers);      // chain + workers + producer warp
-constexpr int kSyncThreads = 32 * (1 + kWorkers);    // chain + workers (block barrier)
+constexpr int kDpThreads = 32 * (2 + kWorkers);      // workers + producer + chain
+constexpr int kSyncThreads = 32 * (1 + kWorkers);    // workers + chain (block barrier)
 // Warp roles.  The SM sub-partition scheduler picks the highest warp id
 // first among eligible warps, so the serial chain warp gets the highest id:
 // it is the critical path and must never lose an issue slot to a worker.
@@ -67,50 +79,42 @@ __device__ long long* g_dp_trace = nullptr;  // [block][16] clock64 stamps of CT
   do {                 \
   } while (0)
 #endif
-constexpr int kNearCols = 64;
+constexpr int kUnitCols = 64;   // unit u: triangle of block u [0, 32) + near-far of block u+1 [32, 64)
+constexpr int kNearCols = 64;   // a tile's far-far columns start here
 constexpr int kChunkCols = 32;
 constexpr int kMaxRing = 24;
-constexpr int kNearBufs = 2;  // near tile of block b in use, b+1 in flight
 constexpr uint32_t kColBytes = kRB * sizeof(double);  // 256 B
 constexpr size_t kChunkBytes = (size_t)kChunkCols * kColBytes;  // 8 KB
 
 // Shared-memory layout of dp_pass_kernel (offsets in bytes): fixed part,
-// then the DP state (when it lives in shared memory), then the ring of far
-// chunk buffers, whose depth the launcher sizes to the remaining space.
+// then the DP state (when it lives in shared memory), then (band path) the
+// ring of far chunk buffers, whose depth the launcher sizes to what is left.
+// "x" is the second double of a state: the bound sum (MODE 3) or the
+// minimax (MODE 1).
 struct DpSmem {
-  static constexpr size_t near = 0;                                   // [3][64][32] double
-  static constexpr size_t wps = near + kNearBufs * kNearCols * kColBytes;  // [8][32] double worker partials
-  static constexpr size_t wpx = wps + kWorkers * kRB * 8;             // [8][32] double / int
-  static constexpr size_t wpj = wpx + kWorkers * kRB * 8;             // [8][32] int
-  static constexpr size_t ps = wpj + kWorkers * kRB * 4;              // [2][32] double  folded partial
-  static constexpr size_t px = ps + 2 * kRB * 8;                      // [2][32] double / int
-  static constexpr size_t pj = px + 2 * kRB * 8;                      // [2][32] int
-  static constexpr size_t nps = pj + 2 * kRB * 4;                     // [8][32] double  near-far partials
-  static constexpr size_t npx = nps + kWorkers * kRB * 8;             // [8][32] double / int
-  static constexpr size_t npj = npx + kWorkers * kRB * 8;             // [8][32] int
-  // MODE 3 (fused bound + candidate): the bound sums' partials
-  static constexpr size_t npb = npj + kWorkers * kRB * 4;             // [8][32] double  near-far
-  static constexpr size_t wpb = npb + kWorkers * kRB * 8;             // [8][32] double  worker
-  static constexpr size_t pb = wpb + kWorkers * kRB * 8;              // [2][32] double  folded
-  static constexpr size_t row0 = pb + 2 * kRB * 8;                    // raw state[0] (sum, aux, bound)
-  // compact band: column -> window index tables of the near tiles and the
-  // ring chunks (int16), and the row widths of the current / next block
-  static constexpr size_t cbn = (row0 + 32 + 15) / 16 * 16;           // [2][64] short
-  static constexpr size_t cbr = cbn + kNearBufs * kNearCols * 2;      // [kMaxRing][32] short
-  static constexpr size_t wrs = cbr + kMaxRing * kChunkCols * 2;      // [2][32] int
-  static constexpr size_t bars = (wrs + 2 * kRB * 4 + 15) / 16 * 16;  // mbarriers: near full/empty
-  static constexpr size_t state = (bars + 8 * (2 * kNearBufs + 2 * kMaxRing) + 127) / 128 * 128;  // + ring
+  static constexpr size_t unit = 0;                                   // [2][64][32] double
+  static constexpr size_t wps = unit + 2 * kUnitCols * kColBytes;     // [8][32] double  worker partials
+  static constexpr size_t wpx = wps + kWorkers * kRB * 8;             // [8][32] double
+  static constexpr size_t wpc = wpx + kWorkers * kRB * 8;             // [8][32] int
+  static constexpr size_t wpj = wpc + kWorkers * kRB * 4;             // [8][32] int
+  static constexpr size_t ps = wpj + kWorkers * kRB * 4;              // [2][32] double  folded far partial
+  static constexpr size_t px = ps + 2 * kRB * 8;                      // [2][32] double
+  static constexpr size_t pc = px + 2 * kRB * 8;                      // [2][32] int
+  static constexpr size_t pj = pc + 2 * kRB * 4;                      // [2][32] int
+  static constexpr size_t row0 = pj + 2 * kRB * 4;                    // state[0]: sum, aux, x
+  static constexpr size_t bars = (row0 + 32 + 15) / 16 * 16;          // unit full/empty, ring full/empty
+  static constexpr size_t state = (bars + 8 * (4 + 2 * kMaxRing) + 127) / 128 * 128;
 };
 
 size_t dp_smem_fixed() { return DpSmem::state; }
-// DP state arrays (sum; count or minimax) of E = entries + kStatePad slots:
-// a ring (R = mask + 1 entries) mirrors its first kStatePad entries after its
-// end, so the far-far loop reads a chunk's 32 states at base + q with no
-// per-column wrap or clamp; a full array (mask = ~0) just gets the slack.
+// DP state: arrays of SE = entries + kStatePad slots (entries a multiple of
+// 32): sum (double), x (double: MODE 1 / 3), count (int: MODE 0 / 3).  The
+// first kStatePad slots are mirrored after the end, so a chunk's 32 states
+// read at base + q with no wrap.
 constexpr int kStatePad = 32;
 int dp_state_stride(int entries) { return entries + kStatePad; }
 size_t dp_state_bytes(int mode, int entries) {
-  return (size_t)(entries + kStatePad) * (mode == 0 ? 12 : mode == 3 ? 20 : 16);
+  return (size_t)(entries + kStatePad) * (mode == 0 ? 12 : mode == 1 ? 16 : mode == 2 ? 8 : 20);
 }
 size_t dp_chunk_bytes() { return kChunkBytes; }
 int dp_max_ring() { return kMaxRing; }
@@ -137,99 +141,63 @@ __device__ __forceinline__ int far_chunks_needed(int nc, const double* __restric
   return nc;
 }
 
-// ---- cp.async (8-byte, generic proxy) with mbarrier completion ------------
-__device__ __forceinline__ void cp_async_8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-// the mbarrier's phase counts this thread's prior cp.async copies as one of its
-// expected arrivals, delivered when they have all landed
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// ---- in-kernel slice pricing (PRICE != 0) ---------------------------------
-// On length-sorted single-input mini-batches (GPT) the band is never
-// materialised: slice [i, j) depends only on (d = j - i, in[j-1])
-// (pp_internal.cuh SlicePricer), and sorted mini-batches repeat lengths, so
-// along a diagonal the same value recurs for every column of a run of equal
-// lengths.  A warp walks a range of tile columns of the block whose first row
-// is k0; per run it prices the diagonals the run reaches (32 per batch, lane l:
-// d = next + l) into a 128-entry ring indexed by d, and lane r reads its entry
-// of column c at d = c - r; one-column runs are priced in place (lane r: its
-// own slice).  f(c, x, parity) receives lane r's T(k0 + r, k0 + c), NaN when
-// the slice's act_mem exceeds the cap.  Same operations as cost pass B's
-// band_run_kernel, so the values are the band's bit for bit.
-struct WalkScratch {
-  double* ring;   // [128]
-  double* x;      // [32] staged lengths
-  AxisPos* px;    // [32] their sequence brackets
+// One row's running state: sum s, second value x (bound sum / minimax),
+// count c and argmin j (CAND modes).
+struct Acc {
+  double s, x;
+  int c, j;
 };
 
-template <int LAY, class F>
-__device__ __forceinline__ void walk_columns(const DpPrice& pr, const SlicePricer& SP, const double* __restrict__ len,
-                                             const AxisPos* __restrict__ pos, int cb, int ce,
-                                             const WalkScratch& ws, int lane, F&& f) {
-  const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
-  double prev_x = QNAN;
-  AxisPos pe = pr.p0;
-  int done = 0;
-  for (int c0 = cb; c0 < ce; c0 += 32) {
-    const int cq = c0 + lane;
-    double xq = QNAN;
-    AxisPos pxq = pr.p0;
-    if (cq < ce && cq > 0) {
-      xq = len[cq];
-      pxq = pos[cq];
-    }
-    ws.x[lane] = xq;
-    ws.px[lane] = pxq;
-    double xn = __shfl_down_sync(0xffffffffu, xq, 1);
-    if (lane == 31) xn = (cq + 1 < ce) ? len[cq + 1] : QNAN;
-    // bit q: column c0 + q ends its run (the next column differs or is past the range)
-    const unsigned int run_end = __ballot_sync(0xffffffffu, !(xn == xq));
-    __syncwarp();
-    const int qend = min(32, ce - c0);
-    for (int q = 0; q < qend;) {
-      const unsigned int e = run_end >> q;
-      const int qe = min(e ? q + __ffs(e) - 1 : 31, qend - 1);
-      const int cs = c0 + q, cend = c0 + qe;
-      const double x = ws.x[q];
-      if (!(x == prev_x)) {  // warp-uniform: column cs starts a run of equal lengths
-        prev_x = x;
-        const AxisPos px = ws.px[q];
-        if (0.0 < x) pe = px; else pe = pr.p0;
-        if (e & 1u) {  // a one-column run: lane r prices its own slice, d = cs - r
-          const int d = cs - lane;
-          f(cs, price_slice<LAY>(SP, pr.mbp[min(max(d, 1), pr.max_n)], pe), 0);
-          q = qe + 1;
-          continue;
-        }
-        done = cs - 32;
-      }
-      // price the run's diagonals (done, cend] (d <= 0 entries are never used)
-      while (done < cend) {
-        const int d = done + 1 + lane;
-        ws.ring[d & 127] = price_slice<LAY>(SP, pr.mbp[min(max(d, 1), pr.max_n)], pe);
-        done += 32;
-      }
-      __syncwarp();
-      int c = cs;
-      for (; c + 1 <= cend; c += 2) {
-        const double x0 = ws.ring[(c - lane) & 127];
-        const double x1 = ws.ring[(c + 1 - lane) & 127];
-        f(c, x0, 0);
-        f(c + 1, x1, 1);
-      }
-      if (c <= cend) f(c, ws.ring[(c - lane) & 127], 0);
-      __syncwarp();
-      q = qe + 1;
-    }
+// The DP transition of one tile entry into a row accumulator, for the mode's
+// recurrences (microbatch.cpp:176-186; the bound pass :274-279).  `ss`, `sx`,
+// `sc` are state[j]; DESC: columns arrive in descending j, so an equal
+// (sum, count) takes the new (lower) j; otherwise ascending j keeps the old.
+//   CAND (MODE 0 / 3): (x + S, 1 + C) when x <= t and it is lexicographically
+//     smaller.  NaN entries (infeasible slices) and +inf states fail every
+//     compare against the (+inf, 0) identity or any taken value.
+//   MODE 3 also: bound sum min(x + B);  MODE 1: min sum and min over
+//     max(x, M) (the minimax t*);  MODE 2: min sum.
+template <int MODE, bool DESC>
+__device__ __forceinline__ void fold(Acc& a, double xv, double ss, double sx, int sc, int j, bool okb,
+                                     double t) {
+  constexpr bool CAND = MODE == 0 || MODE == 3;
+  const double cs = __dadd_rn(xv, ss);
+  if (CAND) {
+    const int cn = 1 + sc;
+    const bool tie = DESC ? (cn <= a.c) : (cn < a.c);
+    const bool upd = okb & (xv <= t) & ((cs < a.s) | ((cs == a.s) & tie));
+    a.s = upd ? cs : a.s;
+    a.c = upd ? cn : a.c;
+    a.j = upd ? j : a.j;
+  } else {
+    a.s = (okb & (cs < a.s)) ? cs : a.s;
+  }
+  if (MODE == 3) {
+    const double cb = __dadd_rn(xv, sx);
+    a.x = (okb & (cb < a.x)) ? cb : a.x;
+  } else if (MODE == 1) {
+    const double v = (xv < sx) ? sx : xv;
+    a.x = (okb & (v < a.x)) ? v : a.x;
   }
 }
 
 // (s, c, j) lexmin with lowest-j ties.
 __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int c0, int j0) {
   return s1 < s0 || (s1 == s0 && (c1 < c0 || (c1 == c0 && j1 < j0)));
+}
+// Combine two partial accumulators over disjoint column sets (associative).
+template <int MODE>
+__device__ __forceinline__ void combine(Acc& a, const Acc& o) {
+  constexpr bool CAND = MODE == 0 || MODE == 3;
+  if (CAND) {
+    const bool tk = better(o.s, o.c, o.j, a.s, a.c, a.j);
+    a.s = tk ? o.s : a.s;
+    a.c = tk ? o.c : a.c;
+    a.j = tk ? o.j : a.j;
+  } else {
+    a.s = (o.s < a.s) ? o.s : a.s;
+  }
+  if (MODE == 1 || MODE == 3) a.x = (o.x < a.x) ? o.x : a.x;
 }
 
 // MODE 0: DP pass of one t_max candidate: (sum, count, next) per row.
@@ -239,30 +207,17 @@ __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int
 //         t* comes from the singleton slices instead (seg_init_kernel).
 // MODE 3: MODE 2 fused with the first candidate pass (MODE 0): that candidate
 //         (the first >= the singleton bound) is known before the bound, so
-//         one pass streams the band once and runs both recurrences — two
-//         independent chains interleaved in the same triangle steps.  The
+//         one pass streams the tiles once and runs both recurrences.  The
 //         candidate result goes to res[item], the bound to res2[segment].
-// SMEM_STATE: DP state in shared memory (else an L2-resident global ring).
+// SMEM_STATE: DP state in shared memory (else an L2-resident global array).
 // SANITIZE: slice times may be -inf (generic SliceCostFn tables).  The
-//   reference skips non-finite state[j] (microbatch.cpp:180); states are stored
-//   with non-finite sums as +inf, which can never improve a row (x + inf is
-//   +inf or NaN), so the hot loops need no finiteness test.  Grid-priced
-//   times are >= 0 and never -inf, so only the table path pays for this.
-//
-// Update rule (microbatch.cpp:183-184): take (x + S[j], 1 + C[j]) when it is
-// lexicographically smaller; equal (sum, count) keeps the lowest j.  No
-// finiteness test on the sum is needed: +inf or NaN never compares smaller
-// than the (+inf, 0) identity or any taken value, -inf is taken exactly when
-// the reference takes it.
-// PRICE (kLayDec1 / kLayEncDec2; 0 = read the band): no band — the workers
-//   price every tile entry themselves (walk_columns above): the near tile of
-//   block b+1 into the dense near buffer and the far-far columns of block b+1
-//   straight into their reductions, during block b; the producer warp idles.
-// PRICE == kGtab: the producer streams the tiles from the call's shared
-//   slice table G (gtab.cu: `band` points at G, pr.gbase per sample) with
-//   cp.async, 8 B per lane and one tile column per warp instruction; the
-//   table is L2-resident, the band does not exist.
-template <int MODE, bool SMEM_STATE, bool SANITIZE, bool COMPACT, int PRICE>
+//   reference skips non-finite state[j] (microbatch.cpp:180); states are used
+//   and stored with non-finite sums as +inf, which can never improve a row
+//   (x + inf is +inf or NaN), so the hot loops need no finiteness test.
+// GTAB: the tiles are views of the call's shared slice table G (gtab.cu:
+//   `band` points at G, pr.gbase per ordered sample): column c of the block
+//   whose first row is i0 is G[gbase[i0 + c - 1] + c - r] for row r.
+template <int MODE, bool SMEM_STATE, bool SANITIZE, bool GTAB>
 __global__ void __launch_bounds__(kDpThreads, 2)
     dp_pass_kernel(const WorkItem* __restrict__ items, const int64_t* __restrict__ seg_off,
                    const int* __restrict__ blk_base, const int* __restrict__ blk_W,
@@ -271,36 +226,25 @@ __global__ void __launch_bounds__(kDpThreads, 2)
                    const int64_t* __restrict__ cand_off, ItemResult* __restrict__ res,
                    int* __restrict__ next_buf, double* __restrict__ gstate, int res_by_seg,
                    int ring_off, int kRing, const double* __restrict__ cmin, double t_margin,
-                   unsigned long long* __restrict__ cols_streamed, const short* __restrict__ colbase,
-                   const int* __restrict__ chunk_nv, const int* __restrict__ row_w,
-                   ItemResult* __restrict__ res2, DpPrice pr) {
+                   unsigned long long* __restrict__ cols_streamed, ItemResult* __restrict__ res2,
+                   const int64_t* __restrict__ gbase) {
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr bool INK = PRICE == kLayDec1 || PRICE == kLayEncDec2;  // in-kernel pricing
-  constexpr bool GTAB = PRICE == kGtab;                           // tiles from the shared table
-  double* near = reinterpret_cast<double*>(smem + DpSmem::near);
+  constexpr bool CAND = MODE == 0 || MODE == 3;
+  constexpr bool X2 = MODE == 1 || MODE == 3;
+  double* unit = reinterpret_cast<double*>(smem + DpSmem::unit);
   double* ring = reinterpret_cast<double*>(smem + ring_off);
   double* wps = reinterpret_cast<double*>(smem + DpSmem::wps);
-  int* wpc = reinterpret_cast<int*>(smem + DpSmem::wpx);        // MODE 0
-  double* wpm = reinterpret_cast<double*>(smem + DpSmem::wpx);  // MODE 1
+  double* wpx = reinterpret_cast<double*>(smem + DpSmem::wpx);
+  int* wpc = reinterpret_cast<int*>(smem + DpSmem::wpc);
   int* wpj = reinterpret_cast<int*>(smem + DpSmem::wpj);
   double* ps = reinterpret_cast<double*>(smem + DpSmem::ps);
-  int* pc = reinterpret_cast<int*>(smem + DpSmem::px);          // MODE 0
-  double* pm = reinterpret_cast<double*>(smem + DpSmem::px);    // MODE 1
+  double* px = reinterpret_cast<double*>(smem + DpSmem::px);
+  int* pc = reinterpret_cast<int*>(smem + DpSmem::pc);
   int* pj = reinterpret_cast<int*>(smem + DpSmem::pj);
-  double* nps = reinterpret_cast<double*>(smem + DpSmem::nps);
-  int* npc = reinterpret_cast<int*>(smem + DpSmem::npx);        // MODE 0
-  double* npm = reinterpret_cast<double*>(smem + DpSmem::npx);  // MODE 1
-  int* npj = reinterpret_cast<int*>(smem + DpSmem::npj);
-  double* npb = reinterpret_cast<double*>(smem + DpSmem::npb);  // MODE 3
-  double* wpb = reinterpret_cast<double*>(smem + DpSmem::wpb);  // MODE 3
-  double* pb = reinterpret_cast<double*>(smem + DpSmem::pb);    // MODE 3
   double* row0 = reinterpret_cast<double*>(smem + DpSmem::row0);
-  short* cbn = reinterpret_cast<short*>(smem + DpSmem::cbn);
-  short* cbr = reinterpret_cast<short*>(smem + DpSmem::cbr);
-  int* wrs = reinterpret_cast<int*>(smem + DpSmem::wrs);
-  uint64_t* near_full = reinterpret_cast<uint64_t*>(smem + DpSmem::bars);
-  uint64_t* near_empty = near_full + kNearBufs;
-  uint64_t* ring_full = near_full + 2 * kNearBufs;
+  uint64_t* unit_full = reinterpret_cast<uint64_t*>(smem + DpSmem::bars);
+  uint64_t* unit_empty = unit_full + 2;
+  uint64_t* ring_full = unit_full + 4;
   uint64_t* ring_empty = ring_full + kMaxRing;
 
   const WorkItem it = items[blockIdx.x];
@@ -310,10 +254,11 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   const int gb0 = blk_base[s];
   const int nblk = blk_base[s + 1] - gb0;
   const double t = item_t(it, cand, cand_off);
-  const double* bseg = band + seg_band_base[s];
+  const double* bseg = GTAB ? band : band + seg_band_base[s];
+  const int64_t* gb_seg = GTAB ? gbase + b0 : nullptr;  // per ordered sample of the segment
   // candidate passes on certified tiles stream only the far chunks that can
   // hold a slice time <= t (thr = +inf or cmin == null: all of them)
-  const bool trunc = MODE == 0 && cmin != nullptr;
+  const bool trunc = MODE == 0 && !GTAB && cmin != nullptr;
   const double thr = trunc ? __dadd_ru(t, t_margin) : __longlong_as_double(0x7ff0000000000000LL);
   auto far_nc = [&](int gb, int W) {
     const int nc = n_chunks(W);
@@ -324,43 +269,44 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
-  // CAND: the candidate recurrence (lexmin of (sum, count, j) over T <= t);
-  // BSUM: MODE 3's extra bound recurrence (min sum, t = +inf)
-  constexpr bool CAND = MODE == 0 || MODE == 3;
-  constexpr bool BSUM = MODE == 3;
+  const Acc kIdent{INF, INF, 0, INT_MAX};
 
-  // state: ring of R = mask + 1 entries (mask = ~0 when not a ring)
-  const unsigned mask = it.state_mask;
-  const int entries = it.state_entries;
+  // state slots: slot(j) = (j + shift) mod R, R = entries (a multiple of 32)
+  const int R = it.state_entries;
+  const int SE = R + kStatePad;
+  const int shift = (32 - (n & 31)) & 31;
   double* st_s = SMEM_STATE ? reinterpret_cast<double*>(smem + DpSmem::state) : gstate + it.state_off;
-  int* st_c = reinterpret_cast<int*>(st_s + (BSUM ? 2 : 1) * (entries + kStatePad));  // CAND
-  double* st_m = st_s + entries + kStatePad;                                         // MODE 1
-  double* st_b = st_s + entries + kStatePad;                                         // MODE 3
-  const bool ring_state = mask != ~0u;
-  // state slot of row j: j mod R on a ring of R = entries slots (R is only a
-  // multiple of 32 sized to the widest tile, not a power of two): one modulo
-  // per block and role; offsets below R from a block's base wrap once
-  auto slot = [&](int j) { return ring_state ? j % entries : j; };
-  auto wrap = [&](int e) { return (ring_state && e >= entries) ? e - entries : e; };
+  double* st_x = st_s + SE;                                                   // X2
+  int* st_c = reinterpret_cast<int*>(st_s + (X2 ? 2 : 1) * SE);               // CAND
+  auto slot = [&](int j) {
+    const int e = j + shift;
+    return e >= R ? e % R : e;
+  };
   int* nxt = next_buf + it.next_off;
+  // tile column base of column c of the block whose first row is i0 (GTAB):
+  // row r's entry is G[colbase - r]
+  auto gcol = [&](int i0, int c) -> int64_t { return c == 0 ? 31 : gb_seg[i0 + c - 1] + c; };
 
   // ---- prologue
   if (threadIdx.x == 0) {
-    for (int k = 0; k < kNearBufs; ++k) {
-      mbar_init(&near_full[k], GTAB ? 32 : 1);  // GTAB: one cp.async arrive per producer lane
-      mbar_init(&near_empty[k], 1);   // the chain warp releases a near tile
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&unit_full[k], GTAB ? 32 : 1);  // GTAB: every producer lane arrives after its stores
+      mbar_init(&unit_empty[k], 1);             // the chain warp releases a unit
     }
     for (int k = 0; k < kRing; ++k) {
-      mbar_init(&ring_full[k], GTAB ? 32 : 1);
+      mbar_init(&ring_full[k], 1);
       mbar_init(&ring_empty[k], kWorkers);  // every worker warp releases a chunk
     }
     mbar_fence_init();
-    // state[n] = {0.0, 0} (microbatch.cpp:174), and its ring mirror
-    for (int e = slot(n); ; e += entries) {
-      st_s[e] = 0.0;
-      if (CAND) st_c[e] = 0; else if (MODE == 1) st_m[e] = -INF;
-      if (BSUM) st_b[e] = 0.0;
-      if (!(ring_state && e < kStatePad)) break;
+    // state[n] = {0.0, 0} (microbatch.cpp:174), and its mirror
+    const int e = slot(n);
+    for (int q = 0; q < 2; ++q) {
+      const int ee = q ? e + R : e;
+      if (q && e >= kStatePad) break;
+      st_s[ee] = 0.0;
+      if (CAND) st_c[ee] = 0;
+      if (MODE == 1) st_x[ee] = -INF;
+      if (MODE == 3) st_x[ee] = 0.0;
     }
     row0[0] = INF;
     row0[1] = CAND ? 0.0 : INF;
@@ -368,164 +314,91 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   }
   if (wid == 0) {  // block 0 has no far-far columns (j <= n < i0 + 64)
     ps[lane] = INF;
-    if (BSUM) pb[lane] = INF;
-    if (CAND) {
-      pc[lane] = 0;
-      pj[lane] = INT_MAX;
-    } else {
-      if (MODE == 1) pm[lane] = INF;
-    }
-  }
-  // PRICE: the pricer's cells (decoder kind, + encoder kind for kLayEncDec2)
-  // staged in shared memory at ring_off, then per worker warp a diagonal ring
-  // and the staged lengths of its current columns
-  SlicePricer SP{};
-  WalkScratch ws{};
-  if (INK) {
-    const int cells = pr.cells;
-    double4* s_tt = reinterpret_cast<double4*>(smem + ring_off);
-    double2* s_am = reinterpret_cast<double2*>(s_tt + (PRICE == kLayEncDec2 ? 2 : 1) * cells);
-    for (int k = threadIdx.x; k < cells; k += blockDim.x) {
-      s_tt[k] = pr.P.tt_d[k];
-      s_am[k] = pr.P.am_d[k];
-      if (PRICE == kLayEncDec2) {
-        s_tt[cells + k] = pr.P.tt_e[k];
-        s_am[cells + k] = pr.P.am_e[k];
-      }
-    }
-    SP = pr.P;
-    SP.tt_d = s_tt;
-    SP.am_d = s_am;
-    SP.tt_e = s_tt + cells;
-    SP.am_e = s_am + cells;
-    double* wbase = reinterpret_cast<double*>(s_am + (PRICE == kLayEncDec2 ? 2 : 1) * cells);
-    const int w = wid < kWorkers ? wid : 0;
-    ws.ring = wbase + w * (128 + 32 + 64);
-    ws.x = ws.ring + 128;
-    ws.px = reinterpret_cast<AxisPos*>(ws.x + 32);
+    px[lane] = INF;
+    pc[lane] = 0;
+    pj[lane] = INT_MAX;
   }
   __syncthreads();
-  const double* seg_len = INK ? pr.in_d + b0 - 1 : nullptr;  // + row i0 + column c: in[i0 + c - 1]
-  const AxisPos* seg_pos = INK ? pr.pin + b0 - 1 : nullptr;
-  // PRICE: the dense near tile (columns [0, min(64, W)) of block bb, first
-  // row k0) into near buffer bb % 2; worker w prices columns [8w, 8w + 8)
-  auto price_near = [&](int bb) {
-    const int kk0 = max(0, n - kRB * (bb + 1));
-    const int cmax = min(kNearCols, blk_W[gb0 + bb]);
-    const int c_lo = min(8 * wid, cmax), c_hi = min(8 * wid + 8, cmax);
-    double* dst = near + (size_t)(bb % kNearBufs) * kNearCols * kRB;
-    if (c_lo < c_hi)
-      walk_columns<INK ? PRICE : kLayDec1>(pr, SP, seg_len + kk0, seg_pos + kk0, c_lo, c_hi, ws, lane,
-                                            [&](int c, double x, int) { dst[c * kRB + lane] = x; });
-  };
-  if (INK) {
-    if (wid == kProducerWarp) return;  // (no band to stream)
-    if (wid == 0 && lane == 0 && cols_streamed && nblk > 0)
-      atomicAdd(cols_streamed, (unsigned long long)min(kNearCols, blk_W[gb0]));
-    if (wid < kWorkers && nblk > 0) price_near(0);
-    named_bar(1, kSyncThreads);
-  }
 
-  // ================= producer warp: TMA bulk copies, in consumption order
-  // (near tile of block b, then the far-far chunks of block b, which the
-  // workers consume during block b-1), each into a buffer its consumers
-  // released through the matching "empty" mbarrier.  It never joins the
-  // block barrier, so it runs ahead by up to the ring depth.
-  if (!INK && wid == kProducerWarp) {
-    // Issue order = consumption order: near tile of block b (used during
-    // block b), then the far-far chunks of block b+1 (used by the workers
-    // during block b), so far chunks never queue behind a near-buffer wait.
-    if (GTAB) {
-      // tile column c of the block whose first row is ii0: lane r's entry is
-      // G[gbase[sample j - 1] + (c - r)] (d = c - r), column 0 the NaN row
-      const double* G = band;
-      auto issue_cols = [&](double* dst, int ii0, int c0, int cols) {
-        const int c = c0 + lane;
-        const long long bq = lane < cols ? (c == 0 ? 31LL : (long long)pr.gbase[b0 + ii0 + c - 1] + c) : 0LL;
-        for (int q = 0; q < cols; ++q) {
-          const long long base = __shfl_sync(0xffffffffu, bq, q);
-          cp_async_8(dst + q * kRB + lane, G + base - lane);
-        }
-      };
-      int islot = 0, iround = 0;
-      long long ncols_total = 0;
-      for (int b = 0; b < nblk; ++b) {
-        const int gb = gb0 + b;
-        const int W = blk_W[gb];
-        const int nsl = b % kNearBufs;
-        const int ncols = min(kNearCols, W);
-        const int ii0 = max(0, n - kRB * (b + 1));
-        ncols_total += ncols;
-        if (b >= kNearBufs) mbar_wait(&near_empty[nsl], ((b / kNearBufs) - 1) & 1);
-        issue_cols(near + (size_t)nsl * kNearCols * kRB, ii0, 0, min(ncols, 32));
-        if (ncols > 32) issue_cols(near + (size_t)nsl * kNearCols * kRB + 32 * kRB, ii0, 32, ncols - 32);
-        cp_async_arrive_noinc(&near_full[nsl]);
-        if (b + 1 >= nblk) break;
-        const int gn = gb + 1;
-        const int Wn = blk_W[gn];
-        const int k0n = max(0, n - kRB * (b + 2));
-        const int nc = far_nc(gn, Wn);
-        ncols_total += nc > 0 ? min(Wn, kNearCols + nc * kChunkCols) - kNearCols : 0;
-        for (int k = 0; k < nc; ++k) {
-          const int c0 = kNearCols + k * kChunkCols;
-          const int cols = min(kChunkCols, Wn - c0);
-          if (iround > 0) mbar_wait(&ring_empty[islot], (iround - 1) & 1);
-          issue_cols(ring + (size_t)islot * kChunkCols * kRB, k0n, c0, cols);
-          cp_async_arrive_noinc(&ring_full[islot]);
-          if (++islot == kRing) {
-            islot = 0;
-            ++iround;
+  // ================= producer warp: the units (and, band path, the far-far
+  // ring) in consumption order.  Unit u goes to buffer (u + 1) & 1; unit -1
+  // holds only block 0's near-far columns.  It never joins the block barrier.
+  if (wid == kProducerWarp) {
+    long long ncols_total = 0;  // tile columns visited (transitions / 32)
+    auto unit_geom = [&](int u, int& i0, int& nb, int& W) {
+      const int i1 = n - kRB * u;
+      i0 = max(0, i1 - kRB);
+      nb = i1 - i0;
+      W = blk_W[gb0 + u];
+    };
+    auto load_unit = [&](int u) {
+      const int k = (u + 1) & 1;
+      double* U = unit + (size_t)k * kUnitCols * kRB;
+      int ct = 0, cn = 0, i0 = 0, nb = 0, W = 0, i0n = 0, nbn = 0, Wn = 0;
+      if (u >= 0) {
+        unit_geom(u, i0, nb, W);
+        ct = min(nb, W);
+      }
+      if (u + 1 < nblk) {
+        unit_geom(u + 1, i0n, nbn, Wn);
+        cn = max(0, min(kRB, Wn - nbn));
+      }
+      if (GTAB) {
+        // lane q holds the column bases of triangle column q and near-far column q
+        const int64_t gt = lane < ct ? gcol(i0, lane) : 0;
+        const int64_t gn = lane < cn ? gcol(i0n, nbn + lane) : 0;
+        for (int c0 = 0; c0 < ct; c0 += 8) {
+          double v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int64_t g = __shfl_sync(0xffffffffu, gt, (c0 + q) & 31);
+            v[q] = c0 + q < ct ? __ldg(band + g - lane) : QNAN;
           }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c0 + q < ct) U[(c0 + q) * kRB + lane] = v[q];
+        }
+        for (int c0 = 0; c0 < cn; c0 += 8) {
+          double v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int64_t g = __shfl_sync(0xffffffffu, gn, (c0 + q) & 31);
+            v[q] = c0 + q < cn ? __ldg(band + g - lane) : QNAN;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c0 + q < cn) U[(kRB + c0 + q) * kRB + lane] = v[q];
+        }
+        mbar_arrive(&unit_full[k]);  // (each lane, after its own stores)
+      } else {
+        if (lane == 0) {
+          mbar_expect_tx(&unit_full[k], (uint32_t)(ct + cn) * kColBytes);
+          if (ct > 0) tma_load_1d(U, bseg + tile_off[gb0 + u], ct * kColBytes, &unit_full[k]);
+          if (cn > 0)
+            tma_load_1d(U + kRB * kRB, bseg + tile_off[gb0 + u + 1] + (size_t)nbn * kRB, cn * kColBytes,
+                        &unit_full[k]);
         }
       }
-      if (lane == 0 && cols_streamed) atomicAdd(cols_streamed, (unsigned long long)ncols_total);
-      return;
-    }
+    };
+    load_unit(-1);
+    if (nblk > 0) load_unit(0);
     int islot = 0, iround = 0;
-    long long ncols_total = 0;  // tile columns streamed (the transitions this pass visits / 32)
     for (int b = 0; b < nblk; ++b) {
-      const int gb = gb0 + b;
-      const int W = blk_W[gb];
-      const int nsl = b % kNearBufs;
-      const int ncols = min(kNearCols, W);
-      ncols_total += ncols;
-      if (lane == 0) {
-        if (b >= kNearBufs) mbar_wait(&near_empty[nsl], ((b / kNearBufs) - 1) & 1);
-        mbar_expect_tx(&near_full[nsl], ncols * kColBytes);
-        tma_load_1d(near + (size_t)nsl * kNearCols * kRB, bseg + tile_off[gb], ncols * kColBytes,
-                    &near_full[nsl]);
-      }
+      const int W = blk_W[gb0 + b];
+      ncols_total += min(kNearCols, W);
       if (b + 1 >= nblk) break;
-      const int gn = gb + 1;
+      // unit b+1 into the buffer of unit b-1, once the chain released it
+      const int u = b + 1, k = (u + 1) & 1, f = (u + 1) >> 1;
+      mbar_wait(&unit_empty[k], (f - 1) & 1);
+      load_unit(u);
+      // far-far chunks of block b+1 (the workers reduce them during block b)
+      const int gn = gb0 + b + 1;
       const int Wn = blk_W[gn];
-      // (the whole warp: far_nc is warp-cooperative; lane 0 issues)
-      const int nc = far_nc(gn, Wn);
+      const int nc = GTAB ? n_chunks(Wn) : far_nc(gn, Wn);
       ncols_total += nc > 0 ? min(Wn, kNearCols + nc * kChunkCols) - kNearCols : 0;
-      if (COMPACT) {
-        // far chunks kk = 2 .. nc + 1 are records (pp_internal.cuh); their
-        // sizes are read 32 at a time by the whole warp
-        const int64_t cid = chunk_id0(seg_band_base[s] + tile_off[gn], gn) + kNearCols / kChunkCols;
-        const double* tb = bseg + tile_off[gn] + (size_t)kNearCols * kRB;
-        int mynv = 0;
-        for (int k = 0; k < nc; ++k) {
-          if ((k & 31) == 0) mynv = k + lane < nc ? chunk_nv[cid + k + lane] : 0;
-          const int nv = __shfl_sync(0xffffffffu, mynv, k & 31);
-          const uint32_t vbytes = (uint32_t)((nv + 1) & ~1) * 8u;  // a multiple of 16 B
-          if (lane == 0) {
-            if (iround > 0) mbar_wait(&ring_empty[islot], (iround - 1) & 1);
-            mbar_expect_tx(&ring_full[islot], vbytes + 64u);
-            tma_load_1d(ring + (size_t)islot * kChunkCols * kRB, tb + (size_t)k * kChunkCols * kRB, vbytes,
-                        &ring_full[islot]);
-            tma_load_1d(cbr + islot * kChunkCols, colbase + (cid + k) * kChunkCols, 64u, &ring_full[islot]);
-          }
-          if (++islot == kRing) {
-            islot = 0;
-            ++iround;
-          }
-        }
-      } else if (lane == 0) {
-        for (int k = 0; k < nc; ++k) {
-          const int c0 = kNearCols + k * kChunkCols;
+      if (!GTAB && lane == 0) {
+        for (int q = 0; q < nc; ++q) {
+          const int c0 = kNearCols + q * kChunkCols;
           const int cols = min(kChunkCols, Wn - c0);
           if (iround > 0) mbar_wait(&ring_empty[islot], (iround - 1) & 1);
           mbar_expect_tx(&ring_full[islot], cols * kColBytes);
@@ -541,389 +414,285 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     if (lane == 0 && cols_streamed) atomicAdd(cols_streamed, (unsigned long long)ncols_total);
     return;
   }
-  int cslot = 0;
-  uint32_t cphase = 0;
 
-  for (int b = 0; b < nblk; ++b) {
-    const int i1 = n - kRB * b;
-    const int i0 = max(0, i1 - kRB);
-    const int nb = i1 - i0;
-
-    // ---- phase 1 (workers): near-far columns [nb, min(64, W)) of block b;
-    // their states (rows of blocks b-1, b-2 and state[n]) are final.  Worker
-    // w takes columns nb + w, nb + w + 8, ...; the chain folds the eight
-    // partials.  A few hundred cycles instead of a serial 32-column loop on
-    // the chain.
-    const double* nt = near + (size_t)(b % kNearBufs) * kNearCols * kRB;
-    const int si0 = slot(i0);  // state slot of the block's first row
-    if (wid < kWorkers) {
-      const int W = blk_W[gb0 + b];
-      const int r = lane;
-      if (!INK) mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
-      double s1 = INF, m1 = INF, b1 = INF;
-      int c1 = 0, j1 = INT_MAX;
-      const int cnf = min(kNearCols, W);
-      for (int c = nb + wid; c < cnf; c += kWorkers) {
-        const double x = nt[c * kRB + r];
-        const int j = i0 + c;
-        const int sj = wrap(si0 + c);  // (c < 64 < R)
-        const double cs = __dadd_rn(x, st_s[sj]);
-        if (BSUM) {
-          const double cb = __dadd_rn(x, st_b[sj]);
-          b1 = (cb < b1) ? cb : b1;
-        }
-        if (CAND) {
-          const int cn = 1 + st_c[sj];
-          const bool upd = (x <= t) & ((cs < s1) | ((cs == s1) & (cn < c1)));
-          s1 = upd ? cs : s1;
-          c1 = upd ? cn : c1;
-          j1 = upd ? j : j1;
-        } else {
-          // (NaN / +inf entries never pass the compares: see the far-far loop)
-          s1 = (cs < s1) ? cs : s1;
-          const double mj = MODE == 1 ? st_m[sj] : 0.0;
-          const double v = (x < mj) ? mj : x;
-          if (MODE == 1) m1 = (v < m1) ? v : m1;
-        }
-      }
-      const int o = wid * kRB + r;
-      nps[o] = s1;
-      if (BSUM) npb[o] = b1;
-      if (CAND) {
-        npc[o] = c1;
-        npj[o] = j1;
-      } else {
-        if (MODE == 1) npm[o] = m1;
-      }
-    }
-    // ---- the chain warp meanwhile loads its far-far partial, waits for its tile
-    const int W = blk_W[gb0 + b];
+  // ================= chain warp
+  if (wid == kChainWarp) {
     const int r = lane;
-    double as = INF, am = INF, ab = INF;
-    int ac = 0, aj = INT_MAX;
-    if (wid == kChainWarp) {
-      PP_TRACE(0);
-      const int pbuf = (b & 1) * kRB + r;
-      as = ps[pbuf];
-      if (BSUM) ab = pb[pbuf];
-      if (CAND) {
-        ac = pc[pbuf];
-        aj = pj[pbuf];
-      } else {
-        if (MODE == 1) am = pm[pbuf];
+    Acc N = kIdent;  // this lane's row of the NEXT block: its near-far columns so far
+    // block 0's near-far columns (unit -1: j = n, ...), from the stored states
+    if (nblk > 0) {
+      mbar_wait(&unit_full[0], 0);
+      const int nb0 = n - max(0, n - kRB);
+      const int cnf = max(0, min(kRB, blk_W[gb0] - nb0));
+      const double* U = unit;
+      for (int k = cnf - 1; k >= 0; --k) {
+        const int j = n - kRB * 0 + k;  // i1 of block 0 is n
+        const int e = slot(j);
+        fold<MODE, true>(N, U[(kRB + k) * kRB + r], st_s[e], X2 ? st_x[e] : 0.0, CAND ? st_c[e] : 0, j, true,
+                         t);
       }
-      if (!INK) mbar_wait(&near_full[b % kNearBufs], (b / kNearBufs) & 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&unit_empty[0]);
     }
-    named_bar(3, kSyncThreads);
-
-    if (wid == kChainWarp) {
-      // ================= chain warp: block b =================
-      PP_TRACE(1);
-      // fold the 8 near-far partials: a pairwise tree (ILP), lexmin with j
-      // ties is associative
+    for (int b = 0; b < nblk; ++b) {
+      PP_TRACE(0);
+      const int i1 = n - kRB * b;
+      const int i0 = max(0, i1 - kRB);
+      const int nb = i1 - i0;
+      const int W = blk_W[gb0 + b];
+      const bool has_next = b + 1 < nblk;
+      const int i0n = max(0, i0 - kRB);
+      const int nbn = i0 - i0n;
+      const int cnx = has_next ? max(0, min(kRB, blk_W[gb0 + b + 1] - nbn)) : 0;  // valid next near-far cols
+      const int ub = (b + 1) & 1;
+      const double* U = unit + (size_t)ub * kUnitCols * kRB;
+      // this row's accumulator: the near-far columns (folded during the
+      // previous block) and the workers' far-far partial
+      Acc A = N;
       {
-        double s8[kWorkers], m8[kWorkers], b8[kWorkers];
-        int c8[kWorkers], j8[kWorkers];
-#pragma unroll
-        for (int v = 0; v < kWorkers; ++v) {
-          const int o = v * kRB + r;
-          s8[v] = nps[o];
-          b8[v] = BSUM ? npb[o] : INF;
-          if (CAND) {
-            c8[v] = npc[o];
-            j8[v] = npj[o];
-          } else {
-            m8[v] = MODE == 1 ? npm[o] : INF;
-          }
-        }
-#pragma unroll
-        for (int h = kWorkers / 2; h >= 1; h /= 2) {
-#pragma unroll
-          for (int v = 0; v < h; ++v) {
-            if (BSUM) b8[v] = (b8[v + h] < b8[v]) ? b8[v + h] : b8[v];
-            if (CAND) {
-              const bool tk = better(s8[v + h], c8[v + h], j8[v + h], s8[v], c8[v], j8[v]);
-              s8[v] = tk ? s8[v + h] : s8[v];
-              c8[v] = tk ? c8[v + h] : c8[v];
-              j8[v] = tk ? j8[v + h] : j8[v];
-            } else {
-              s8[v] = (s8[v + h] < s8[v]) ? s8[v + h] : s8[v];
-              if (MODE == 1) m8[v] = (m8[v + h] < m8[v]) ? m8[v + h] : m8[v];
-            }
-          }
-        }
-        if (BSUM) ab = (b8[0] < ab) ? b8[0] : ab;
-        if (CAND) {
-          const bool tk = better(s8[0], c8[0], j8[0], as, ac, aj);
-          as = tk ? s8[0] : as;
-          ac = tk ? c8[0] : ac;
-          aj = tk ? j8[0] : aj;
-        } else {
-          as = (s8[0] < as) ? s8[0] : as;
-          if (MODE == 1) am = (m8[0] < am) ? m8[0] : am;
+        const int p = (b & 1) * kRB + r;
+        Acc P{ps[p], X2 ? px[p] : INF, CAND ? pc[p] : 0, CAND ? pj[p] : INT_MAX};
+        combine<MODE>(A, P);
+      }
+      // the last block of a segment whose n is not a multiple of 32 has
+      // near-far columns past the previous block's rows: fold them from the
+      // tile in global memory and the stored states (once per pass)
+      if (nb < kRB && b > 0) {
+        const int chi = min(kNearCols, W);
+        for (int c = chi - 1; c >= nb + kRB; --c) {
+          const int j = i0 + c;
+          const double xv = GTAB ? __ldg(band + gcol(i0, c) - r) : __ldg(bseg + tile_off[gb0 + b] + (size_t)c * kRB + r);
+          const int e = slot(j);
+          fold<MODE, true>(A, xv, st_s[e], X2 ? st_x[e] : 0.0, CAND ? st_c[e] : 0, j, true, t);
         }
       }
+      if (r >= nb) A = kIdent;
+      N = kIdent;
+      mbar_wait(&unit_full[ub], ((b + 1) >> 1) & 1);
+      PP_TRACE(1);
       PP_TRACE(2);
-      if (r >= nb) {
-        as = INF;
-        ac = 0;
-        am = INF;
-        ab = INF;
-      }
-      // Step jj: lane jj's row is final; broadcast it, the lanes below absorb
-      // T[i0 + r, i0 + jj] + state.  Descending j: equal (sum, count) takes
-      // the lower j.  Rows >= nb hold (+inf, 0), which can never be taken, so
-      // a full block runs all 32 steps unconditionally.
-      // the triangle's tile column jj is read from shared memory inside its
-      // step (independent of the chain, so its latency hides under the
-      // shuffle) — 32 doubles fewer live registers
-      auto tri_step = [&](int jj) {
-        const double x = lds_f64(nt + jj * kRB + r);
-        double sj = __shfl_sync(0xffffffffu, as, jj);
-        if (SANITIZE) sj = isfinite(sj) ? sj : INF;
-        const double cs = __dadd_rn(x, sj);
-        const bool okb = (jj < W) & (r < jj);
-        const bool ok = okb & (CAND ? (x <= t) : true);  // (NaN: fails the `<`s)
-        if (BSUM) {  // the bound chain, independent of the candidate chain
-          const double bj = __shfl_sync(0xffffffffu, ab, jj);
-          const double cb = __dadd_rn(x, bj);
-          ab = (okb & (cb < ab)) ? cb : ab;
-        }
-        if (CAND) {
-          const int cn = 1 + __shfl_sync(0xffffffffu, ac, jj);
-          const bool upd = ok & ((cs < as) | ((cs == as) & (cn <= ac)));
-          as = upd ? cs : as;
-          ac = upd ? cn : ac;
-          aj = upd ? i0 + jj : aj;
-        } else {
-          const double mj = MODE == 1 ? __shfl_sync(0xffffffffu, am, jj) : 0.0;
-          as = (ok & (cs < as)) ? cs : as;
-          const double v = (x < mj) ? mj : x;
-          if (MODE == 1) am = (ok & (v < am)) ? v : am;
+      // ---- the triangle.  Iteration k: every lane computes state[k] from
+      // H_k (lane k's accumulator over columns >= k+2) and T[k, k+1] exactly
+      // as lane k folds it, then lane l < k folds T[l, k] + state[k] and every
+      // lane folds the next block's T'[l, nbn + k] + state[k]; lane k-2's
+      // accumulator (now over columns >= k) is shuffled for iteration k-2.
+      auto shfl_acc = [&](const Acc& a, int src) {
+        Acc h;
+        h.s = __shfl_sync(0xffffffffu, a.s, src);
+        h.x = X2 ? __shfl_sync(0xffffffffu, a.x, src) : INF;
+        h.c = CAND ? __shfl_sync(0xffffffffu, a.c, src) : 0;
+        h.j = 0;
+        return h;
+      };
+      auto triangle = [&](auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        Acc H1 = shfl_acc(A, nb - 1);
+        Acc H2 = shfl_acc(A, max(nb - 2, 0));
+        double Ss = 0.0, Sx = 0.0;  // state[k+1] as every lane knows it
+        int Sc = 0;
+#pragma unroll
+        for (int k = kRB - 1; k >= 0; --k) {
+          if (FULL || k < nb) {
+            // state[k]
+            Acc h = H1;
+            if (FULL ? (k + 1 < kRB) : (k + 1 < nb)) {
+              const double x1 = lds_f64(U + (k + 1) * kRB + k);
+              fold<MODE, true>(h, x1, Ss, Sx, Sc, 0, k + 1 < W, t);
+            }
+            double ns = h.s, nx = h.x;
+            if (SANITIZE) {
+              ns = isfinite(ns) ? ns : INF;
+              if (MODE == 3) nx = isfinite(nx) ? nx : INF;
+            }
+            // this lane's row (l < k) and its row of the next block
+            const double xo = lds_f64(U + k * kRB + r);
+            fold<MODE, true>(A, xo, ns, nx, h.c, i0 + k, (r < k) & (k < W), t);
+            if (has_next) {
+              const double xn = lds_f64(U + (kRB + k) * kRB + r);
+              fold<MODE, true>(N, xn, ns, nx, h.c, i0 + k, k < cnx, t);
+            }
+            Ss = ns;
+            Sx = nx;
+            Sc = h.c;
+            H1 = H2;
+            if (k >= 2) H2 = shfl_acc(A, k - 2);
+          }
         }
       };
-      if (nb == kRB) {  // every block but the top one of a segment
-#pragma unroll
-        for (int jj = kRB - 1; jj >= 0; --jj) tri_step(jj);
-      } else {
-#pragma unroll
-        for (int jj = kRB - 1; jj >= 0; --jj)
-          if (jj < nb) tri_step(jj);
-      }
-      // near tile of block b consumed: the warp's reads are ordered before the
-      // release (__syncwarp + mbarrier arrive), and the producer's next TMA
-      // write into the buffer waits for it (the TMA pipeline WAR pattern)
+      if (nb == kRB) triangle(std::true_type{}); else triangle(std::false_type{});
+      // unit b consumed: the warp's reads are ordered before the release
+      // (__syncwarp + mbarrier arrive), and the producer's next write into the
+      // buffer waits for it
       __syncwarp();
-      if (!INK && lane == 0) mbar_arrive(&near_empty[b % kNearBufs]);
+      if (lane == 0) mbar_arrive(&unit_empty[ub]);
       PP_TRACE(3);
       if (r < nb) {
         const int row = i0 + r;
-        const bool f = isfinite(as);
-        const int e = wrap(si0 + r);
-        const int em = (ring_state && e < kStatePad) ? e + entries : e;  // the ring mirror
-        const double sv = (SANITIZE && !f) ? INF : as;
-        st_s[e] = sv;
-        st_s[em] = sv;
-        if (BSUM) {
-          st_b[e] = ab;
-          st_b[em] = ab;
+        const bool f = isfinite(A.s);
+        const int e = slot(row);
+        const double sv = (SANITIZE && !f) ? INF : A.s;
+        const double xv = (SANITIZE && MODE == 3 && !isfinite(A.x)) ? INF : A.x;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q && e >= kStatePad) break;
+          const int ee = q ? e + R : e;  // the mirror
+          st_s[ee] = sv;
+          if (X2) st_x[ee] = xv;
+          if (CAND) st_c[ee] = f ? A.c : 0;
         }
-        if (CAND) {
-          st_c[e] = f ? ac : 0;
-          st_c[em] = f ? ac : 0;
-          nxt[row] = f ? aj : -1;
-        } else {
-          if (MODE == 1) st_m[e] = am;
-          if (MODE == 1) st_m[em] = am;
-        }
+        if (CAND) nxt[row] = f ? A.j : -1;
         if (row == 0) {
-          row0[0] = as;
-          row0[1] = CAND ? (double)ac : am;
-          row0[2] = ab;
+          row0[0] = A.s;
+          row0[1] = CAND ? (double)A.c : A.x;
+          row0[2] = A.x;
         }
       }
-    } else {
-      // ================= workers: far-far of block b+1 =================
-      const int w = wid;
+      PP_TRACE(4);
+      named_bar(1, kSyncThreads);  // chain + workers: block b's states and block b+1's partial
+      PP_TRACE(5);
+    }
+  } else {
+    // ================= workers: far-far columns of block b+1 during block b
+    const int w = wid;
+    int cslot = 0;
+    uint32_t cphase = 0;
+    for (int b = 0; b < nblk; ++b) {
       const int bn = b + 1;
       if (w == 0) PP_TRACE(8);
       if (bn < nblk) {
         const int j1 = n - kRB * bn;
         const int k0 = max(0, j1 - kRB);  // i0 of block b+1
         const int Wn = blk_W[gb0 + bn];
-        const int nc = far_nc(gb0 + bn, Wn);
-        const int sk0 = slot(k0);  // state slot of block b+1's first row
-        double as = INF, am = INF, as2 = INF, am2 = INF, ab = INF, ab2 = INF;
-        int ac = 0, aj = INT_MAX, ac2 = 0, aj2 = INT_MAX;
-        const int r = lane;
-
-        if (INK) {
-          // block b+1's near tile for the chain and phase 1 of the next block ...
-          price_near(bn);
-          // ... and its far-far columns [64, Weff), worker w a contiguous share
-          // of them, priced on the fly into its reductions
-          const int Weff = nc > 0 ? min(Wn, kNearCols + nc * kChunkCols) : min(Wn, kNearCols);
-          const int F = Weff - kNearCols;
-          const int per = F > 0 ? (F + kWorkers - 1) / kWorkers : 0;
-          const int cw0 = kNearCols + min(F, w * per), cw1 = kNearCols + min(F, (w + 1) * per);
-          if (w == 0 && lane == 0 && cols_streamed)
-            atomicAdd(cols_streamed, (unsigned long long)(min(kNearCols, Wn) + max(F, 0)));
-          int ecur = wrap(sk0 + cw0), ccur = cw0;  // state slot of the current column
-          auto upd = [&](int c, double x, int par) {
-            int e = ecur + (c - ccur);
-            if (ring_state && e >= entries) e -= entries;
-            ecur = e;
-            ccur = c;
-            const int j = k0 + c;
-            const double cs = __dadd_rn(x, st_s[e]);
-            double& s_ = par ? as2 : as;
-            int& c_ = par ? ac2 : ac;
-            int& j_ = par ? aj2 : aj;
-            double& m_ = par ? am2 : am;
-            if (BSUM) {
-              double& b_ = par ? ab2 : ab;
-              const double cb = __dadd_rn(x, st_b[e]);
-              b_ = (cb < b_) ? cb : b_;
-            }
-            if (CAND) {
-              const int cn = 1 + st_c[e];
-              const bool u = (x <= t) & ((cs < s_) | ((cs == s_) & (cn < c_)));
-              s_ = u ? cs : s_;
-              c_ = u ? cn : c_;
-              j_ = u ? j : j_;
-            } else {
-              s_ = (cs < s_) ? cs : s_;
-              const double mj = MODE == 1 ? st_m[e] : 0.0;
-              const double v = (x < mj) ? mj : x;
-              if (MODE == 1) m_ = (v < m_) ? v : m_;
-            }
-          };
-          if (cw0 < cw1)
-            walk_columns<INK ? PRICE : kLayDec1>(pr, SP, seg_len + k0, seg_pos + k0, cw0, cw1, ws, lane, upd);
-        }
-        for (int k = 0; k < (INK ? 0 : nc); ++k) {
-          mbar_wait(&ring_full[cslot], cphase);
-          const double* ch = ring + (size_t)cslot * kChunkCols * kRB;
-          const int c0 = kNearCols + k * kChunkCols;
-          const int cols = min(kChunkCols, Wn - c0);
-          // the chunk's states: slots jb .. jb + 31 (ring mirror / slack: no wrap)
-          const int jb = wrap(sk0 + c0) + w;  // (c0 < W <= R - 63)
-          const double* ss = st_s + jb;
-          const int* sc = st_c + jb;
-          const double* sm = st_m + jb;
-          const double* sb = st_b + jb;
+        const int nc = GTAB ? n_chunks(Wn) : far_nc(gb0 + bn, Wn);
+        Acc a0 = kIdent, a1 = kIdent;
+        // a multiple of 32 (k0 + 64 == n mod 32) except on the last block of a
+        // segment whose n is not a multiple of 32: then scalar state loads
+        int sb = slot(k0 + kNearCols);
+        const bool vec = (sb & 3) == 0;
+        const int q0 = 4 * w;
+        // GTAB: column bases and entries of the next chunk are loaded one
+        // chunk ahead of their use
+        int64_t gnext[4];
+        double xnext[4];
+        auto load_g = [&](int k, int64_t* g) {
+          const int c0 = kNearCols + k * kChunkCols + q0;
 #pragma unroll
-          for (int q0 = 0; q0 < kChunkCols; q0 += kWorkers) {
-            const int q = q0 + w;
-            const int j = k0 + c0 + q;
-            // columns past the chunk are masked (NaN never passes x <= t)
-            double x;
-            if (COMPACT) {  // record of a far chunk (pp_internal.cuh: no masking needed)
-              x = (q < cols) ? ch[cbr[cslot * kChunkCols + q] - r] : QNAN;
-            } else {
-              x = (q < cols) ? ch[q * kRB + r] : QNAN;
+          for (int i = 0; i < 4; ++i) g[i] = (k < nc && c0 + i < Wn) ? gb_seg[k0 + c0 + i - 1] + c0 + i : -1;
+        };
+        auto load_x = [&](const int64_t* g, double* x) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) x[i] = g[i] >= 0 ? __ldg(band + g[i] - lane) : QNAN;
+        };
+        if (GTAB) {
+          int64_t g0[4];
+          load_g(0, g0);
+          load_x(g0, xnext);
+          load_g(1, gnext);
+        }
+        for (int k = 0; k < nc; ++k) {
+          const int c0 = kNearCols + k * kChunkCols;
+          double x[4];
+          if (GTAB) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = xnext[i];
+            load_x(gnext, xnext);
+            load_g(k + 2, gnext);
+          } else {
+            mbar_wait(&ring_full[cslot], cphase);
+            const double* ch = ring + (size_t)cslot * kChunkCols * kRB;
+            const int cols = min(kChunkCols, Wn - c0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (q0 + i < cols) ? ch[(q0 + i) * kRB + lane] : QNAN;
+          }
+          // states of the four columns: 16-byte vector loads (sb + q0 is a
+          // multiple of 4; the mirror covers sb + 31 >= R)
+          double2 s01, s23, x01{0.0, 0.0}, x23{0.0, 0.0};
+          int4 cc{0, 0, 0, 0};
+          const int e = sb + q0;
+          if (vec) {
+            s01 = *reinterpret_cast<const double2*>(st_s + e);
+            s23 = *reinterpret_cast<const double2*>(st_s + e + 2);
+            if (X2) {
+              x01 = *reinterpret_cast<const double2*>(st_x + e);
+              x23 = *reinterpret_cast<const double2*>(st_x + e + 2);
             }
-            const double cs = __dadd_rn(x, ss[q0]);
-            // two accumulators (even / odd q0 step) for ILP; ascending j in each
-            double& s_ = (q0 / kWorkers) & 1 ? as2 : as;
-            int& c_ = (q0 / kWorkers) & 1 ? ac2 : ac;
-            int& j_ = (q0 / kWorkers) & 1 ? aj2 : aj;
-            double& m_ = (q0 / kWorkers) & 1 ? am2 : am;
-            if (BSUM) {
-              double& b_ = (q0 / kWorkers) & 1 ? ab2 : ab;
-              const double cb = __dadd_rn(x, sb[q0]);
-              b_ = (cb < b_) ? cb : b_;
+            if (CAND) cc = *reinterpret_cast<const int4*>(st_c + e);
+          } else {
+            s01 = double2{st_s[e], st_s[e + 1]};
+            s23 = double2{st_s[e + 2], st_s[e + 3]};
+            if (X2) {
+              x01 = double2{st_x[e], st_x[e + 1]};
+              x23 = double2{st_x[e + 2], st_x[e + 3]};
             }
-            if (CAND) {
-              const int cn = 1 + sc[q0];
-              const bool upd = (x <= t) & ((cs < s_) | ((cs == s_) & (cn < c_)));
-              s_ = upd ? cs : s_;
-              c_ = upd ? cn : c_;
-              j_ = upd ? j : j_;
-            } else {
-              // an infeasible entry (x NaN) gives cs = NaN and v = NaN, which
-              // fail every `<`; x = +inf or state = +inf gives v = +inf, which
-              // never beats the running minimum (<= +inf): no separate tests
-              s_ = (cs < s_) ? cs : s_;
-              const double mj = MODE == 1 ? sm[q0] : 0.0;
-              const double v = (x < mj) ? mj : x;
-              if (MODE == 1) m_ = (v < m_) ? v : m_;
+            if (CAND) cc = int4{st_c[e], st_c[e + 1], st_c[e + 2], st_c[e + 3]};
+          }
+          const int j = k0 + c0 + q0;
+          // two accumulators (even / odd column) for ILP, ascending j in each
+          fold<MODE, false>(a0, x[0], s01.x, x01.x, cc.x, j, true, t);
+          fold<MODE, false>(a1, x[1], s01.y, x01.y, cc.y, j + 1, true, t);
+          fold<MODE, false>(a0, x[2], s23.x, x23.x, cc.z, j + 2, true, t);
+          fold<MODE, false>(a1, x[3], s23.y, x23.y, cc.w, j + 3, true, t);
+          if (!GTAB) {
+            __syncwarp();  // the warp's reads of the slot, then its release
+            if (lane == 0) mbar_arrive(&ring_empty[cslot]);
+            if (++cslot == kRing) {
+              cslot = 0;
+              cphase ^= 1u;
             }
           }
-          __syncwarp();  // the warp's reads of the slot, then its release
-          if (lane == 0) mbar_arrive(&ring_empty[cslot]);  // this warp is done with the chunk
-          if (++cslot == kRing) {
-            cslot = 0;
-            cphase ^= 1u;
-          }
+          sb += kChunkCols;
+          if (sb >= R) sb -= R;
         }
-        if (BSUM) ab = (ab2 < ab) ? ab2 : ab;
-        if (CAND) {
-          const bool tk = better(as2, ac2, aj2, as, ac, aj);
-          as = tk ? as2 : as;
-          ac = tk ? ac2 : ac;
-          aj = tk ? aj2 : aj;
-        } else {
-          as = (as2 < as) ? as2 : as;
-          if (MODE == 1) am = (am2 < am) ? am2 : am;
-        }
+        combine<MODE>(a0, a1);
         if (w == 0) PP_TRACE(9);
-        const int o = w * kRB + r;
-        wps[o] = as;
-        if (BSUM) wpb[o] = ab;
+        const int o = w * kRB + lane;
+        wps[o] = a0.s;
+        if (X2) wpx[o] = a0.x;
         if (CAND) {
-          wpc[o] = ac;
-          wpj[o] = aj;
-        } else {
-          if (MODE == 1) wpm[o] = am;
+          wpc[o] = a0.c;
+          wpj[o] = a0.j;
         }
         named_bar(2, 32 * kWorkers);
-        if (w == 0) {  // fold the 8 worker partials for the chain
+        if (w == 0) {  // fold the 8 worker partials for the chain: a pairwise tree
+          Acc v[kWorkers];
 #pragma unroll
-          for (int v = 1; v < kWorkers; ++v) {
-            const int p = v * kRB + r;
-            if (BSUM) ab = (wpb[p] < ab) ? wpb[p] : ab;
-            if (CAND) {
-              if (better(wps[p], wpc[p], wpj[p], as, ac, aj)) {
-                as = wps[p];
-                ac = wpc[p];
-                aj = wpj[p];
-              }
-            } else {
-              as = (wps[p] < as) ? wps[p] : as;
-              if (MODE == 1) am = (wpm[p] < am) ? wpm[p] : am;
-            }
+          for (int q = 0; q < kWorkers; ++q) {
+            const int p = q * kRB + lane;
+            v[q].s = wps[p];
+            v[q].x = X2 ? wpx[p] : INF;
+            v[q].c = CAND ? wpc[p] : 0;
+            v[q].j = CAND ? wpj[p] : INT_MAX;
           }
-          const int pb2 = (bn & 1) * kRB + r;
-          ps[pb2] = as;
-          if (BSUM) pb[pb2] = ab;
+#pragma unroll
+          for (int h = kWorkers / 2; h >= 1; h /= 2)
+#pragma unroll
+            for (int q = 0; q < h; ++q) combine<MODE>(v[q], v[q + h]);
+          const int p2 = (bn & 1) * kRB + lane;
+          ps[p2] = v[0].s;
+          if (X2) px[p2] = v[0].x;
           if (CAND) {
-            pc[pb2] = ac;
-            pj[pb2] = aj;
-          } else {
-            if (MODE == 1) pm[pb2] = am;
+            pc[p2] = v[0].c;
+            pj[p2] = v[0].j;
           }
         }
+        if (w == 0) PP_TRACE(10);
       }
+      named_bar(1, kSyncThreads);  // chain + workers: block b's states and block b+1's partial
     }
-    if (wid == kChainWarp) PP_TRACE(4);
-    if (wid == 0) PP_TRACE(10);
-    named_bar(1, kSyncThreads);  // chain + workers: block b's states and block b+1's partials
-    if (wid == kChainWarp) PP_TRACE(5);
   }
-  if (threadIdx.x == 0) {  // after the last block barrier: row0 is final
+  if (threadIdx.x == 0) {  // (worker 0) after the last block barrier: row0 is final
     ItemResult rr;
     rr.sum0 = row0[0];
     rr.count0 = CAND ? (int)row0[1] : 0;
     rr.feasible = isfinite(row0[0]) ? 1 : 0;
-    rr.aux = MODE == 1 ? row0[1] : -__longlong_as_double(0x7ff0000000000000LL);  // (MODE 2: no t*)
+    rr.aux = MODE == 1 ? row0[1] : -INF;  // (MODE 2: no t*)
     res[res_by_seg ? s : blockIdx.x] = rr;
-    if (BSUM) {  // the fused bound pass's result, by segment
+    if (MODE == 3) {  // the fused bound pass's result, by segment
       ItemResult rb;
       rb.sum0 = row0[2];
       rb.count0 = 0;
       rb.feasible = isfinite(row0[2]) ? 1 : 0;
-      rb.aux = -__longlong_as_double(0x7ff0000000000000LL);
+      rb.aux = -INF;
       res2[s] = rb;
     }
   }
@@ -1322,59 +1091,38 @@ extern "C" int pp_debug_dp_trace(long long* d_buf) {
 }
 #endif
 // smem_state = the largest shared-memory DP state of the launch's items
-// (0 with state_global: every item's state then lives in gstate).  The chunk
-// ring gets the rest of `smem_budget` (4..kMaxRing chunks of 8 KB).
-// PRICE shared memory after the fixed part / state: the pricer's cells and
-// per worker a 128-entry diagonal ring + 32 staged lengths and brackets.
-size_t dp_price_smem(int lay, int cells) {
-  return (size_t)(lay == kLayEncDec2 ? 2 : 1) * cells * (sizeof(double4) + sizeof(double2)) +
-         (size_t)kWorkers * (128 + 32 + 64) * sizeof(double);
-}
-
-// smem_state = the largest shared-memory DP state of the launch's items
-// (0 with state_global: every item's state then lives in gstate).  The chunk
-// ring gets the rest of `smem_budget` (4..kMaxRing chunks of 8 KB); with
-// `price` (in-kernel pricing, no band) there is no chunk ring.
+// (0 with state_global: every item's state then lives in gstate).  Band path:
+// the chunk ring gets the rest of `smem_budget` (4..kMaxRing chunks of 8 KB);
+// slice-table path (gbase != null): no ring, the workers read G directly.
 cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t smem_state,
                            int state_global, int sanitize, size_t smem_budget, const int64_t* seg_off,
                            const int* blk_base, const int* blk_W, const int64_t* tile_off,
                            const int64_t* seg_band_base, const double* band, const double* cand,
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, const double* cmin, double t_margin,
-                           unsigned long long* cols_streamed, const short* colbase, const int* chunk_nv,
-                           const int* row_w, ItemResult* res2, const DpPrice* price, int price_lay,
+                           unsigned long long* cols_streamed, ItemResult* res2, const int64_t* gbase,
                            cudaStream_t st) {
   if (n_items == 0) return cudaSuccess;
   const size_t ring_off = (DpSmem::state + (state_global ? 0 : smem_state) + 127) / 128 * 128;
   int ring = 0;
-  size_t smem;
-  DpPrice pr{};
-  if (price && price_lay != kGtab) {
-    pr = *price;
-    smem = ring_off + dp_price_smem(price_lay, pr.cells);
-  } else {
-    if (price) pr = *price;
+  size_t smem = ring_off;
+  if (!gbase) {
     ring = (int)std::min<size_t>(kMaxRing, (smem_budget - std::min(smem_budget, ring_off)) / kChunkBytes);
     ring = std::max(ring, 4);
     smem = ring_off + (size_t)ring * kChunkBytes;
   }
-  const bool compact = colbase != nullptr;
-#define PP_DP_LAUNCH(M, S, Z, C, P)                                                                   \
+#define PP_DP_LAUNCH(M, S, Z, G)                                                                      \
   do {                                                                                                \
-    ensure_dyn_smem((const void*)dp_pass_kernel<M, S, Z, C, P>, smem);                                \
-    dp_pass_kernel<M, S, Z, C, P><<<n_items, kDpThreads, smem, st>>>(                                 \
+    ensure_dyn_smem((const void*)dp_pass_kernel<M, S, Z, G>, smem);                                   \
+    dp_pass_kernel<M, S, Z, G><<<n_items, kDpThreads, smem, st>>>(                                    \
         items, seg_off, blk_base, blk_W, tile_off, seg_band_base, band, cand, cand_off, res, next_buf, \
-        gstate, res_by_seg, (int)ring_off, ring, cmin, t_margin, cols_streamed, colbase, chunk_nv,    \
-        row_w, res2, pr);                                                                             \
+        gstate, res_by_seg, (int)ring_off, ring, cmin, t_margin, cols_streamed, res2, gbase);         \
   } while (0)
-#define PP_DP_LAUNCH_Z(M, S)                                                 \
-  do {                                                                       \
-    if (price && price_lay == kGtab) PP_DP_LAUNCH(M, S, false, false, kGtab);              \
-    else if (price && price_lay == kLayDec1) PP_DP_LAUNCH(M, S, false, false, kLayDec1);   \
-    else if (price) PP_DP_LAUNCH(M, S, false, false, kLayEncDec2);           \
-    else if (compact) PP_DP_LAUNCH(M, S, false, true, 0);                    \
-    else if (sanitize) PP_DP_LAUNCH(M, S, true, false, 0);                   \
-    else PP_DP_LAUNCH(M, S, false, false, 0);                                \
+#define PP_DP_LAUNCH_Z(M, S)                          \
+  do {                                                \
+    if (gbase) PP_DP_LAUNCH(M, S, false, true);       \
+    else if (sanitize) PP_DP_LAUNCH(M, S, true, false); \
+    else PP_DP_LAUNCH(M, S, false, false);            \
   } while (0)
   if (mode == 0) {
     if (state_global) PP_DP_LAUNCH_Z(0, false); else PP_DP_LAUNCH_Z(0, true);

@@ -28,6 +28,9 @@
 //
 // Values are priced with price_slice (pp_internal.cuh), the operations of
 // cost pass B's band_run_kernel, so G holds the band's values bit for bit.
+// A second copy shifted by one entry (G1[k + 1] = G[k]) makes every tile
+// column's 32-entry window start 16 B aligned in one of the two, so the DP's
+// producer moves each column with ONE 256 B cp.async.bulk (TMA) copy.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -113,7 +116,7 @@ template <int LAY>
 __global__ void __launch_bounds__(32 * kGWarps) gtab_fill_kernel(CostGrid g, double cap, const AxisPos* __restrict__ mbp,
                                                                  int nK, const int* __restrict__ need,
                                                                  const int64_t* __restrict__ row_off,
-                                                                 double* __restrict__ G) {
+                                                                 double* __restrict__ G, double* __restrict__ G1) {
   __shared__ double4 s_tt[kGCells];
   __shared__ double2 s_am[kGCells];
   const int nm = g.nm, ns = g.ns, per = nm * ns;
@@ -123,7 +126,10 @@ __global__ void __launch_bounds__(32 * kGWarps) gtab_fill_kernel(CostGrid g, dou
   }
   __syncthreads();
   const double QNAN = __longlong_as_double(0x7ff8000000000000LL);
-  if (blockIdx.x == 0 && threadIdx.x < 32) G[threadIdx.x] = QNAN;  // the NaN row
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // the NaN row, in both copies
+    G[threadIdx.x] = QNAN;
+    G1[threadIdx.x + 1] = QNAN;
+  }
   const SlicePricer SP{s_tt, s_tt + per, s_am, s_am + per, ns, g.le, g.ld, cap,
                        !(cap == __longlong_as_double(0x7ff0000000000000LL))};
   const int lane = threadIdx.x & 31;
@@ -137,9 +143,12 @@ __global__ void __launch_bounds__(32 * kGWarps) gtab_fill_kernel(CostGrid g, dou
     pe.pad = 0;
     bracket(g.seq_ax, ns, (double)K, pe.seg, pe.t);
     double* row = G + row_off[K];
+    double* row1 = G1 + row_off[K] + 1;
     for (int e = lane; e < D + 32; e += 32) {
       const int d = e - 31;
-      row[e] = d >= 1 ? price_slice<LAY>(SP, mbp[d], pe) : QNAN;
+      const double v = d >= 1 ? price_slice<LAY>(SP, mbp[d], pe) : QNAN;
+      row[e] = v;
+      row1[e] = v;
     }
   }
 }
@@ -276,12 +285,12 @@ cudaError_t launch_gtab_offsets(const int* need, int nK, int64_t* row_off, long 
 }
 
 cudaError_t launch_gtab_fill(const CostGrid& g, double cap, const AxisPos* mbp, int nK, const int* need,
-                             const int64_t* row_off, double* G, cudaStream_t st) {
+                             const int64_t* row_off, double* G, double* G1, cudaStream_t st) {
   const int blocks = std::max(1, std::min((nK + kGWarps - 1) / kGWarps, 148 * 8));
   if (g.lay_class == kLayDec1)
-    gtab_fill_kernel<kLayDec1><<<blocks, 32 * kGWarps, 0, st>>>(g, cap, mbp, nK, need, row_off, G);
+    gtab_fill_kernel<kLayDec1><<<blocks, 32 * kGWarps, 0, st>>>(g, cap, mbp, nK, need, row_off, G, G1);
   else
-    gtab_fill_kernel<kLayEncDec2><<<blocks, 32 * kGWarps, 0, st>>>(g, cap, mbp, nK, need, row_off, G);
+    gtab_fill_kernel<kLayEncDec2><<<blocks, 32 * kGWarps, 0, st>>>(g, cap, mbp, nK, need, row_off, G, G1);
   return cudaGetLastError();
 }
 

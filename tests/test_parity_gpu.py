@@ -141,7 +141,8 @@ def test_slice_reuse_matches_per_slice_pricing(name):
     off = W.seg_offsets(cfg, M)
     a = capi.Planner(0)
     b = capi.Planner(0)
-    b.set_tuning(slice_reuse=False)
+    a.set_tuning(slice_table=False)  # the diagonal reuse lives on the band path
+    b.set_tuning(slice_reuse=False, slice_table=False)
     ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     for k in ("ordered", "count", "t_max_used", "objective", "status"):
@@ -182,34 +183,6 @@ def test_band_truncation_matches_full_stream(name):
     sa, sb = a.stats(), b.stats()
     assert sa["candidates_evaluated"] == sb["candidates_evaluated"]
     assert sa["transitions_executed"] < sb["transitions_executed"]
-    a.close()
-    b.close()
-
-
-@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
-def test_compact_band_matches_dense_band(name):
-    """DP passes and assembly reading compact chunk records (the distinct
-    diagonal windows of each 32-column chunk) against the dense band:
-    identical plans and candidate sets."""
-    cfg = W.CONFIGS[name]
-    M = {"C1": 64, "C3": 6, "C4": 24}[name]
-    s = W.dataset(cfg, M)
-    off = W.seg_offsets(cfg, M)
-    a = capi.Planner(0)
-    b = capi.Planner(0)
-    a.set_tuning(compact_band=True)
-    b.set_tuning(slice_table=False)
-    ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
-    rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
-    for k in ("ordered", "count", "t_max_used", "objective", "status"):
-        assert ra[k].tobytes() == rb[k].tobytes(), k
-    for q in range(M):
-        m = int(ra["count"][q])
-        for k in ("splits", "mb_times"):
-            assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
-    sa, sb = a.stats(), b.stats()
-    for k in ("candidates_generated", "candidates_evaluated", "transitions_executed"):
-        assert sa[k] == sb[k], k
     a.close()
     b.close()
 
@@ -277,44 +250,15 @@ def test_slice_table_random_vs_oracle(orc):
     p.close()
 
 
-@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
-def test_dp_pricing_matches_band(name):
-    """The DP pricing its own slices (dp.cu PRICE: no band in HBM, pass B
-    only marks candidates) against the band path (pass B writes the band, the
-    DP streams it): identical plans, candidate sets and DP transitions."""
-    cfg = W.CONFIGS[name]
-    M = {"C1": 64, "C3": 6, "C4": 24}[name]
-    s = W.dataset(cfg, M)
-    off = W.seg_offsets(cfg, M)
-    a = capi.Planner(0)
-    b = capi.Planner(0)
-    a.set_tuning(dp_pricing=True)
-    b.set_tuning(slice_table=False)
-    ra = a.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
-    sa = a.stats()
-    rb = b.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
-    sb = b.stats()
-    assert sa["band_bytes"] == 0 and sb["band_bytes"] > 0  # the priced path wrote no band
-    for k in ("ordered", "count", "t_max_used", "objective", "status"):
-        assert ra[k].tobytes() == rb[k].tobytes(), k
-    for q in range(M):
-        m = int(ra["count"][q])
-        for k in ("splits", "mb_times"):
-            assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
-    for k in ("candidates_generated", "candidates_evaluated", "candidates_ref_evaluated", "transitions_executed"):
-        assert sa[k] == sb[k], k
-    a.close()
-    b.close()
-
-
-def test_dp_pricing_random_capped_vs_oracle(orc):
-    """In-kernel DP pricing on random GPT mini-batches (binding and
-    non-binding caps, duplicate-heavy and distinct lengths, several
+def test_band_path_random_capped_vs_oracle(orc):
+    """The band path (cost pass B writes per mini-batch tiles, the DP streams
+    them with TMA) on random GPT mini-batches (binding and non-binding caps,
+    duplicate-heavy and distinct lengths, ragged last blocks, several
     intervals and stage counts) against the C restatement."""
     grid = capi.synthetic_grid()
     rng = np.random.default_rng(4242)
     priced = capi.Planner(0)
-    priced.set_tuning(dp_pricing=True)
+    priced.set_tuning(slice_table=False)
     for k in range(40):
         n = int(rng.integers(1, 700))
         L = int(rng.choice([8, 64, 1024, 8192]))
@@ -329,8 +273,28 @@ def test_dp_pricing_random_capped_vs_oracle(orc):
         interval = float(rng.choice([5.0, tot / 7.0, tot / 64.0, tot / 300.0]))
         a = orc.plan(s, grid, model, C, 1, cap, interval)
         b = _plan_or_status(lambda: priced.plan(s, grid, model, C, 1, cap, interval))
-        assert_plan_matches(b, record(a), f"priced {k}: n={n} C={C} I={interval} cap={cap}")
+        assert_plan_matches(b, record(a), f"band {k}: n={n} C={C} I={interval} cap={cap}")
     priced.close()
+
+
+@pytest.mark.parametrize("slice_table", [True, False])
+def test_global_state_dp_vs_streaming_oracle(orc, slice_table):
+    """Uncapped 10,000-sample GPT mini-batches: the DP state (20 B x ~10k
+    rows) no longer fits shared memory, so the passes keep it in an
+    L2-resident global array — on the slice-table and the band path —
+    against the streaming C restatement (O(n) memory)."""
+    grid = capi.synthetic_grid()
+    p = capi.Planner(0)
+    p.set_tuning(slice_table=slice_table)
+    for k, n in enumerate((10000, 9985)):  # (a ragged last block)
+        s = capi.synthetic_dataset(n, 8192, 900 + k, W.INPUT_DIST)
+        model = capi.Model.uniform(4, 2, False)
+        tot = orc.slice_cost(grid, model, orc.order_samples(s), 0, n)[0]
+        interval = tot / 40.0
+        a = orc.plan_stream(s, grid, model, 4, 1, math.inf, interval)
+        b = p.plan(s, grid, model, 4, 1, math.inf, interval)
+        assert_plan_matches(b, record(a), f"global state n={n} table={slice_table}")
+    p.close()
 
 
 def test_slice_reuse_duplicate_heavy_vs_oracle(planner, orc):
@@ -435,6 +399,22 @@ def test_random_vs_reference(planner):
         a = ref.plan(s, grid, model, 4, 1, math.inf, 5000.0)
         b = planner.plan(s, grid, model, 4, 1, math.inf, 5000.0)
         assert_plan_matches(b, record(a), f"ref {k}")
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not shipped")
+def test_nan_interval_plans_like_the_reference(planner):
+    """A NaN t_max_interval is accepted by the reference (microbatch.cpp:225
+    tests `< 0`) and selects the exact candidate set (`> 0` at :263)."""
+    ref = Reference()
+    grid = capi.synthetic_grid()
+    for encdec in (False, True):
+        s = capi.synthetic_dataset(300, 8192, 77, W.INPUT_DIST, W.T5_TARGET_DIST if encdec else None)
+        model = capi.Model.uniform(4, 2, encdec)
+        a = ref.plan(s, grid, model, 4, 1, math.inf, math.nan)
+        b = planner.plan(s, grid, model, 4, 1, math.inf, math.nan)
+        assert_plan_matches(b, record(a), f"nan interval encdec={encdec}")
+        c = planner.plan(s, grid, model, 4, 1, math.inf, 0.0)
+        assert c.splits.tobytes() == b.splits.tobytes() and c.t_max_used == b.t_max_used
 
 
 def _monotone_grid(rng, nm=5, ns=6, jitter=False):

@@ -28,6 +28,9 @@ def main():
     capi.lib.pp_debug_dp_trace.argtypes = [ctypes.c_void_p]
     assert capi.lib.pp_debug_dp_trace(ctypes.c_void_p(buf.data_ptr())) == 0
     p = capi.Planner(0)
+    # QB_TUNE="slice_table=0": A/B switches, as in tools/quick_bench.py
+    tune = {k: bool(int(v)) for k, v in (kv.split("=") for kv in os.environ.get("QB_TUNE", "").split(",") if kv)}
+    p.set_tuning(**tune)
     s = W.dataset(cfg, 1)
     for _ in range(2):
         p.plan(s, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
@@ -36,7 +39,7 @@ def main():
     ok = t[:, 0] > 0
     t = t[ok]
     d = lambda a, b: t[:, b] - t[:, a]  # noqa: E731
-    rows = [("chain: fold partials", 0, 1), ("chain: tile loads", 1, 2),
+    rows = [("chain: A prep (partials)", 0, 1), ("chain: unit wait", 1, 2),
             ("chain: triangle", 2, 3), ("chain: store states", 3, 4), ("chain: block barrier", 4, 5),
             ("worker0: far-far chunks", 8, 9), ("worker0: fold", 9, 10), ("worker0: to barrier", 10, 5)]
     print(f"{name}: {len(t)} blocks traced; cycles per block (median / mean)")
