@@ -69,9 +69,9 @@ cudaError_t launch_gtab_need(const int64_t* seg_off, const int* blk_base, int n_
 cudaError_t launch_gtab_offsets(const int* need, int nK, int64_t* row_off, long long* total, cudaStream_t st);
 cudaError_t launch_gtab_fill(const CostGrid& g, double cap, const AxisPos* mbp, int nK, const int* need,
                              const int64_t* row_off, double* G, double* G1, cudaStream_t st);
-cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* row_off, int64_t* gbase,
+cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* row_off, int* gbase,
                               cudaStream_t st);
-cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int64_t* gbase,
+cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int* gbase,
                              const int* need, const double* G, double interval, const double* tau,
                              unsigned int* small_bm, SegStats* stats, cudaStream_t st);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -103,7 +103,7 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int64_t* seg_band_base, const double* band, const double* cand,
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, const double* cmin, double t_margin,
-                           unsigned long long* cols_streamed, ItemResult* res2, const int64_t* gbase,
+                           unsigned long long* cols_streamed, ItemResult* res2, const int* gbase,
                            cudaStream_t st);
 cudaError_t launch_seg_set_bound(const ItemResult* bound_res, int replicas, SegDP* dp, int n_seg,
                                  cudaStream_t st);
@@ -817,8 +817,8 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   // The call's shared slice table (gtab.cu) instead of a band per
   // mini-batch: lengths index its rows, so they must be bounded
   const int64_t max_len = (int64_t)(long long)(ctx->h_range.as<unsigned long long>()[3] ^ 0x8000000000000000ULL);
-  const bool use_gtab = sorted_gpt && !ctx->tuning.no_slice_table && !ctx->tuning.dp_pricing &&
-                        max_len <= (int64_t)1 << 22;
+  bool use_gtab = sorted_gpt && !ctx->tuning.no_slice_table && !ctx->tuning.dp_pricing &&
+                  max_len <= (int64_t)1 << 22;
   const bool price_in_dp = sorted_gpt && !use_gtab && ctx->tuning.dp_pricing;
   ctx->gtab = false;
   if (use_gtab) {
@@ -827,7 +827,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     PP_CUDA(ctx->gt_off.ensure((size_t)nK * sizeof(int64_t)));
     PP_CUDA(ctx->gt_total.ensure(sizeof(long long)));
     PP_CUDA(ctx->h_gt_total.ensure(sizeof(long long)));
-    PP_CUDA(ctx->gt_base.ensure(std::max<int64_t>(total, 1) * sizeof(int64_t)));
+    PP_CUDA(ctx->gt_base.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
     PP_CUDA(cudaMemsetAsync(ctx->gt_need.p, 0, (size_t)nK * sizeof(int), st));
     PP_TIMED(3, launch_gtab_need(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks, ctx->blk_W.as<int>(),
                                  ctx->in_d.as<double>(), ctx->gt_need.as<int>(), st));
@@ -837,19 +837,25 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     PP_CUDA(cudaStreamSynchronize(st));
     const int64_t entries = *ctx->h_gt_total.as<long long>();
     ctx->gtab_entries = entries;
+    // row bases are int32 (dp.cu reads G[base - r]): a larger table takes the band
+    if (entries + 64 >= (int64_t)INT_MAX) use_gtab = false;
+  }
+  if (use_gtab) {
+    const int nK = (int)std::max<int64_t>(max_len, 0) + 1;
+    const int64_t entries = ctx->gtab_entries;
     // G, then its copy shifted by one entry (starting 16 B aligned)
     const int64_t g1_at = (entries + 2) & ~(int64_t)1;
     PP_CUDA(ctx->gt_G.ensure((size_t)(g1_at + entries + 2) * sizeof(double)));
     PP_TIMED(3, launch_gtab_fill(g, cap, ctx->mbp.as<AxisPos>(), nK, ctx->gt_need.as<int>(), ctx->gt_off.as<int64_t>(),
                                  ctx->gt_G.as<double>(), ctx->gt_G.as<double>() + g1_at, st));
     PP_TIMED(3, launch_gtab_gbase(ctx->in_d.as<double>(), total, ctx->gt_off.as<int64_t>(),
-                                  ctx->gt_base.as<int64_t>(), st));
-    PP_TIMED(3, launch_gtab_bins(c.d_seg_off, n_seg, ctx->in_d.as<double>(), ctx->gt_base.as<int64_t>(),
+                                  ctx->gt_base.as<int>(), st));
+    PP_TIMED(3, launch_gtab_bins(c.d_seg_off, n_seg, ctx->in_d.as<double>(), ctx->gt_base.as<int>(),
                                  ctx->gt_need.as<int>(), ctx->gt_G.as<double>(), interval, tau_d, small_bm,
                                  ctx->stats_d.as<SegStats>(), st));
     ctx->gtab = true;
     ctx->price = DpPrice{};
-    ctx->price.gbase = ctx->gt_base.as<int64_t>();
+    ctx->price.gbase = ctx->gt_base.as<int>();
     ctx->price.g_odd = ctx->gt_G.as<double>() + g1_at;
   }
   if (!price_in_dp && !use_gtab) PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
@@ -1009,7 +1015,7 @@ const double* dp_band(const pp_ctx* ctx) { return ctx->gtab ? ctx->gt_G.as<doubl
 const DpPrice* dp_price(const pp_ctx* ctx) { return (ctx->gtab || ctx->priced) ? &ctx->price : nullptr; }
 int dp_lay(const pp_ctx* ctx) { return ctx->gtab ? kGtab : ctx->price_lay; }
 // The DP's per-sample slice-table row bases (slice-table path), or null (band).
-const int64_t* dp_gbase(const pp_ctx* ctx) { return ctx->gtab ? ctx->gt_base.as<int64_t>() : nullptr; }
+const int* dp_gbase(const pp_ctx* ctx) { return ctx->gtab ? ctx->gt_base.as<int>() : nullptr; }
 
 // The planning pipeline (steps 1-7 above).
 int run_plan(pp_ctx* ctx, const PlanCall& c) {

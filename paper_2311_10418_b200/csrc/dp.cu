@@ -157,13 +157,14 @@ struct Acc {
 //     compare against the (+inf, 0) identity or any taken value.
 //   MODE 3 also: bound sum min(x + B);  MODE 1: min sum and min over
 //     max(x, M) (the minimax t*);  MODE 2: min sum.
+// fold_c takes the count through j already incremented (cn = 1 + C): the
+// DP state arrays store 1 + count, so the far-far loop adds nothing.
 template <int MODE, bool DESC>
-__device__ __forceinline__ void fold(Acc& a, double xv, double ss, double sx, int sc, int j, bool okb,
-                                     double t) {
+__device__ __forceinline__ void fold_c(Acc& a, double xv, double ss, double sx, int cn, int j, bool okb,
+                                       double t) {
   constexpr bool CAND = MODE == 0 || MODE == 3;
   const double cs = __dadd_rn(xv, ss);
   if (CAND) {
-    const int cn = 1 + sc;
     const bool tie = DESC ? (cn <= a.c) : (cn < a.c);
     const bool upd = okb & (xv <= t) & ((cs < a.s) | ((cs == a.s) & tie));
     a.s = upd ? cs : a.s;
@@ -179,6 +180,11 @@ __device__ __forceinline__ void fold(Acc& a, double xv, double ss, double sx, in
     const double v = (xv < sx) ? sx : xv;
     a.x = (okb & (v < a.x)) ? v : a.x;
   }
+}
+template <int MODE, bool DESC>
+__device__ __forceinline__ void fold(Acc& a, double xv, double ss, double sx, int sc, int j, bool okb,
+                                     double t) {
+  fold_c<MODE, DESC>(a, xv, ss, sx, 1 + sc, j, okb, t);
 }
 
 // (s, c, j) lexmin with lowest-j ties.
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
                    int* __restrict__ next_buf, double* __restrict__ gstate, int res_by_seg,
                    int ring_off, int kRing, const double* __restrict__ cmin, double t_margin,
                    unsigned long long* __restrict__ cols_streamed, ItemResult* __restrict__ res2,
-                   const int64_t* __restrict__ gbase) {
+                   const int* __restrict__ gbase) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr bool CAND = MODE == 0 || MODE == 3;
   constexpr bool X2 = MODE == 1 || MODE == 3;
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   const int nblk = blk_base[s + 1] - gb0;
   const double t = item_t(it, cand, cand_off);
   const double* bseg = GTAB ? band : band + seg_band_base[s];
-  const int64_t* gb_seg = GTAB ? gbase + b0 : nullptr;  // per ordered sample of the segment
+  const int* gb_seg = GTAB ? gbase + b0 : nullptr;  // per ordered sample of the segment
   // candidate passes on certified tiles stream only the far chunks that can
   // hold a slice time <= t (thr = +inf or cmin == null: all of them)
   const bool trunc = MODE == 0 && !GTAB && cmin != nullptr;
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   const int shift = (32 - (n & 31)) & 31;
   double* st_s = SMEM_STATE ? reinterpret_cast<double*>(smem + DpSmem::state) : gstate + it.state_off;
   double* st_x = st_s + SE;                                                   // X2
-  int* st_c = reinterpret_cast<int*>(st_s + (X2 ? 2 : 1) * SE);               // CAND
+  int* st_c = reinterpret_cast<int*>(st_s + (X2 ? 2 : 1) * SE);               // CAND: 1 + count
   auto slot = [&](int j) {
     const int e = j + shift;
     return e >= R ? e % R : e;
@@ -285,7 +291,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   int* nxt = next_buf + it.next_off;
   // tile column base of column c of the block whose first row is i0 (GTAB):
   // row r's entry is G[colbase - r]
-  auto gcol = [&](int i0, int c) -> int64_t { return c == 0 ? 31 : gb_seg[i0 + c - 1] + c; };
+  auto gcol = [&](int i0, int c) -> int { return c == 0 ? 31 : __ldg(gb_seg + i0 + c - 1) + c; };
 
   // ---- prologue
   if (threadIdx.x == 0) {
@@ -304,7 +310,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       const int ee = q ? e + R : e;
       if (q && e >= kStatePad) break;
       st_s[ee] = 0.0;
-      if (CAND) st_c[ee] = 0;
+      if (CAND) st_c[ee] = 1;
       if (MODE == 1) st_x[ee] = -INF;
       if (MODE == 3) st_x[ee] = 0.0;
     }
@@ -345,13 +351,13 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       }
       if (GTAB) {
         // lane q holds the column bases of triangle column q and near-far column q
-        const int64_t gt = lane < ct ? gcol(i0, lane) : 0;
-        const int64_t gn = lane < cn ? gcol(i0n, nbn + lane) : 0;
+        const int gt = lane < ct ? gcol(i0, lane) : 0;
+        const int gn = lane < cn ? gcol(i0n, nbn + lane) : 0;
         for (int c0 = 0; c0 < ct; c0 += 8) {
           double v[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const int64_t g = __shfl_sync(0xffffffffu, gt, (c0 + q) & 31);
+            const int g = __shfl_sync(0xffffffffu, gt, (c0 + q) & 31);
             v[q] = c0 + q < ct ? __ldg(band + g - lane) : QNAN;
           }
 #pragma unroll
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           double v[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const int64_t g = __shfl_sync(0xffffffffu, gn, (c0 + q) & 31);
+            const int g = __shfl_sync(0xffffffffu, gn, (c0 + q) & 31);
             v[q] = c0 + q < cn ? __ldg(band + g - lane) : QNAN;
           }
 #pragma unroll
@@ -428,7 +434,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       for (int k = cnf - 1; k >= 0; --k) {
         const int j = n - kRB * 0 + k;  // i1 of block 0 is n
         const int e = slot(j);
-        fold<MODE, true>(N, U[(kRB + k) * kRB + r], st_s[e], X2 ? st_x[e] : 0.0, CAND ? st_c[e] : 0, j, true,
+        fold_c<MODE, true>(N, U[(kRB + k) * kRB + r], st_s[e], X2 ? st_x[e] : 0.0, CAND ? st_c[e] : 1, j, true,
                          t);
       }
       __syncwarp();
@@ -463,7 +469,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           const int j = i0 + c;
           const double xv = GTAB ? __ldg(band + gcol(i0, c) - r) : __ldg(bseg + tile_off[gb0 + b] + (size_t)c * kRB + r);
           const int e = slot(j);
-          fold<MODE, true>(A, xv, st_s[e], X2 ? st_x[e] : 0.0, CAND ? st_c[e] : 0, j, true, t);
+          fold_c<MODE, true>(A, xv, st_s[e], X2 ? st_x[e] : 0.0, CAND ? st_c[e] : 1, j, true, t);
         }
       }
       if (r >= nb) A = kIdent;
@@ -538,7 +544,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           const int ee = q ? e + R : e;  // the mirror
           st_s[ee] = sv;
           if (X2) st_x[ee] = xv;
-          if (CAND) st_c[ee] = f ? A.c : 0;
+          if (CAND) st_c[ee] = f ? A.c + 1 : 1;
         }
         if (CAND) nxt[row] = f ? A.j : -1;
         if (row == 0) {
@@ -567,49 +573,19 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         Acc a0 = kIdent, a1 = kIdent;
         // a multiple of 32 (k0 + 64 == n mod 32) except on the last block of a
         // segment whose n is not a multiple of 32: then scalar state loads
-        int sb = slot(k0 + kNearCols);
-        const bool vec = (sb & 3) == 0;
+        const int sb0 = slot(k0 + kNearCols);
         const int q0 = 4 * w;
-        // GTAB: column bases and entries of the next chunk are loaded one
-        // chunk ahead of their use
-        int64_t gnext[4];
-        double xnext[4];
-        auto load_g = [&](int k, int64_t* g) {
-          const int c0 = kNearCols + k * kChunkCols + q0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) g[i] = (k < nc && c0 + i < Wn) ? gb_seg[k0 + c0 + i - 1] + c0 + i : -1;
-        };
-        auto load_x = [&](const int64_t* g, double* x) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) x[i] = g[i] >= 0 ? __ldg(band + g[i] - lane) : QNAN;
-        };
-        if (GTAB) {
-          int64_t g0[4];
-          load_g(0, g0);
-          load_x(g0, xnext);
-          load_g(1, gnext);
-        }
-        for (int k = 0; k < nc; ++k) {
-          const int c0 = kNearCols + k * kChunkCols;
-          double x[4];
-          if (GTAB) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) x[i] = xnext[i];
-            load_x(gnext, xnext);
-            load_g(k + 2, gnext);
-          } else {
-            mbar_wait(&ring_full[cslot], cphase);
-            const double* ch = ring + (size_t)cslot * kChunkCols * kRB;
-            const int cols = min(kChunkCols, Wn - c0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) x[i] = (q0 + i < cols) ? ch[(q0 + i) * kRB + lane] : QNAN;
-          }
-          // states of the four columns: 16-byte vector loads (sb + q0 is a
-          // multiple of 4; the mirror covers sb + 31 >= R)
+        // one chunk step: the four columns' states (sb = the chunk's first
+        // slot) and entries x folded into the two accumulators (even / odd
+        // column, ascending j in each).  VEC: 16-byte state loads (sb + q0 is
+        // a multiple of 4; the mirror covers sb + 31 >= R).  The stored count
+        // is already 1 + count (fold_c).
+        auto reduce4 = [&](auto vec_tag, int sb, int j, const double* x) {
+          constexpr bool VEC = decltype(vec_tag)::value;
           double2 s01, s23, x01{0.0, 0.0}, x23{0.0, 0.0};
-          int4 cc{0, 0, 0, 0};
+          int4 cc{1, 1, 1, 1};
           const int e = sb + q0;
-          if (vec) {
+          if (VEC) {
             s01 = *reinterpret_cast<const double2*>(st_s + e);
             s23 = *reinterpret_cast<const double2*>(st_s + e + 2);
             if (X2) {
@@ -626,22 +602,74 @@ __global__ void __launch_bounds__(kDpThreads, 2)
             }
             if (CAND) cc = int4{st_c[e], st_c[e + 1], st_c[e + 2], st_c[e + 3]};
           }
-          const int j = k0 + c0 + q0;
-          // two accumulators (even / odd column) for ILP, ascending j in each
-          fold<MODE, false>(a0, x[0], s01.x, x01.x, cc.x, j, true, t);
-          fold<MODE, false>(a1, x[1], s01.y, x01.y, cc.y, j + 1, true, t);
-          fold<MODE, false>(a0, x[2], s23.x, x23.x, cc.z, j + 2, true, t);
-          fold<MODE, false>(a1, x[3], s23.y, x23.y, cc.w, j + 3, true, t);
-          if (!GTAB) {
+          fold_c<MODE, false>(a0, x[0], s01.x, x01.x, cc.x, j, true, t);
+          fold_c<MODE, false>(a1, x[1], s01.y, x01.y, cc.y, j + 1, true, t);
+          fold_c<MODE, false>(a0, x[2], s23.x, x23.x, cc.z, j + 2, true, t);
+          fold_c<MODE, false>(a1, x[3], s23.y, x23.y, cc.w, j + 3, true, t);
+        };
+        auto next_sb = [&](int sb) {
+          sb += kChunkCols;
+          return sb >= R ? sb - R : sb;
+        };
+        if (GTAB) {
+          // lane q holds the table base of column 64 + 32k + q of chunk k (one
+          // coalesced int32 load per chunk; 31 = the NaN row past the tile),
+          // a worker takes its four columns' bases by shuffles.  Bases run
+          // two chunks and entries one chunk ahead of their use; the loop is
+          // unrolled by two chunks so the prefetched entries never move.
+          const int* gp = gb_seg + k0 - 1 + kNearCols + lane;  // column 64 + lane of chunk 0
+          int cw = kNearCols + lane;                             // this lane's column
+          auto colb = [&]() -> int {
+            const int v = cw < Wn ? __ldg(gp) + cw : 31;
+            gp += kChunkCols;
+            cw += kChunkCols;
+            return v;
+          };
+          auto load_x = [&](int lb, double* x) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = __ldg(band + (__shfl_sync(0xffffffffu, lb, q0 + i) - lane));
+          };
+          auto loop = [&](auto vec_tag) {
+            double xa[4], xb[4];
+            int sb = sb0, j = k0 + kNearCols + q0;
+            load_x(colb(), xa);
+            int lb = colb();
+            int k = 0;
+            for (; k + 2 <= nc; k += 2) {
+              load_x(lb, xb);
+              lb = colb();
+              reduce4(vec_tag, sb, j, xa);
+              sb = next_sb(sb);
+              j += kChunkCols;
+              load_x(lb, xa);
+              lb = colb();
+              reduce4(vec_tag, sb, j, xb);
+              sb = next_sb(sb);
+              j += kChunkCols;
+            }
+            if (k < nc) reduce4(vec_tag, sb, j, xa);
+          };
+          if ((sb0 & 3) == 0) loop(std::true_type{}); else loop(std::false_type{});
+        } else {
+          int sb = sb0;
+          for (int k = 0; k < nc; ++k) {
+            const int c0 = kNearCols + k * kChunkCols;
+            double x[4];
+            mbar_wait(&ring_full[cslot], cphase);
+            const double* ch = ring + (size_t)cslot * kChunkCols * kRB;
+            const int cols = min(kChunkCols, Wn - c0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = (q0 + i < cols) ? ch[(q0 + i) * kRB + lane] : QNAN;
+            if ((sb0 & 3) == 0) reduce4(std::true_type{}, sb, k0 + c0 + q0, x);
+            else reduce4(std::false_type{}, sb, k0 + c0 + q0, x);
             __syncwarp();  // the warp's reads of the slot, then its release
             if (lane == 0) mbar_arrive(&ring_empty[cslot]);
             if (++cslot == kRing) {
               cslot = 0;
               cphase ^= 1u;
             }
+            sb = next_sb(sb);
           }
-          sb += kChunkCols;
-          if (sb >= R) sb -= R;
         }
         combine<MODE>(a0, a1);
         if (w == 0) PP_TRACE(9);
@@ -1100,7 +1128,7 @@ cudaError_t launch_dp_pass(int mode, const WorkItem* items, int n_items, size_t 
                            const int64_t* seg_band_base, const double* band, const double* cand,
                            const int64_t* cand_off, ItemResult* res, int* next_buf, double* gstate,
                            int res_by_seg, const double* cmin, double t_margin,
-                           unsigned long long* cols_streamed, ItemResult* res2, const int64_t* gbase,
+                           unsigned long long* cols_streamed, ItemResult* res2, const int* gbase,
                            cudaStream_t st) {
   if (n_items == 0) return cudaSuccess;
   const size_t ring_off = (DpSmem::state + (state_global ? 0 : smem_state) + 127) / 128 * 128;

@@ -155,9 +155,9 @@ __global__ void __launch_bounds__(32 * kGWarps) gtab_fill_kernel(CostGrid g, dou
 
 // Per ordered sample: the offset of its length's row at d = 0.
 __global__ void gtab_gbase_kernel(const double* __restrict__ in_d, int64_t total, const int64_t* __restrict__ row_off,
-                                  int64_t* __restrict__ gbase) {
+                                  int* __restrict__ gbase) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x)
-    gbase[k] = row_off[len_key(in_d[k])] + 31;
+    gbase[k] = (int)(row_off[len_key(in_d[k])] + 31);
 }
 
 // Candidate bins and statistics of each mini-batch from the table (the part
@@ -169,7 +169,7 @@ __global__ void gtab_gbase_kernel(const double* __restrict__ in_d, int64_t total
 // range of out-of-bitmap bins (then the call falls back to the band).
 __global__ void __launch_bounds__(256) gtab_bins_kernel(const int64_t* __restrict__ seg_off,
                                                         const double* __restrict__ in_d,
-                                                        const int64_t* __restrict__ gbase,
+                                                        const int* __restrict__ gbase,
                                                         const int* __restrict__ need,
                                                         const double* __restrict__ G, double ival,
                                                         const double* __restrict__ tau,
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256) gtab_bins_kernel(const int64_t* __restric
       ends &= ends - 1;
       const int j = p0 + q + 1;  // the run's last slice end
       const double xq = __shfl_sync(0xffffffffu, x, q);
-      const int64_t gb = gbase[b0 + j - 1];
+      const int gb = gbase[b0 + j - 1];
       const int D = min(j, need[len_key(xq)]);
       const double* row = G + gb;
       if (lane == 0) {
@@ -294,14 +294,14 @@ cudaError_t launch_gtab_fill(const CostGrid& g, double cap, const AxisPos* mbp, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* row_off, int64_t* gbase,
+cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* row_off, int* gbase,
                               cudaStream_t st) {
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
   gtab_gbase_kernel<<<blocks, 256, 0, st>>>(in_d, total, row_off, gbase);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int64_t* gbase,
+cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int* gbase,
                              const int* need, const double* G, double interval, const double* tau,
                              unsigned int* small_bm, SegStats* stats, cudaStream_t st) {
   if (n_seg > 0)

@@ -305,7 +305,8 @@ struct DpPrice {
   const double* in_d;     // [total]
   int max_n;
   AxisPos p0;             // bracket of length 0 (padded lengths start at 0)
-  const int64_t* gbase;   // kGtab: per ordered sample, its length's table row at d = 0
+  const int* gbase;       // kGtab: per ordered sample, its length's table row at d = 0
+                          // (int32: the call keeps G below 2^31 entries)
   const double* g_odd;    // kGtab: the table shifted by one entry (g_odd[k + 1] = G[k]), so
                           // every 32-entry window starts 16 B aligned in one of the copies
 };
