@@ -437,6 +437,8 @@ def run_ours(args, rank, world, local):
 
 def report(args, cfg, W, capi, planner, stats, solo_stats, M, M_total, world, steps, warm, ms_max, value, clk,
            e2e_value, e2e_api, h2d, d2h, status_ok, gathered_ok, mine, local):
+    import torch
+
     pk, pk_kind = peaks()
     names = capi.KERNEL_NAMES
 
@@ -465,14 +467,30 @@ def report(args, cfg, W, capi, planner, stats, solo_stats, M, M_total, world, st
     reuse = not cfg.encdec
 
     # algorithmic work per kernel category
+    table = s_agg["band_b"] == 0 and reuse  # the call's slice table (gtab.cu): no band in HBM
+    samples = len(solo_stats) * M * cfg.n
+    props = torch.cuda.get_device_properties(local)
+    clk_sum = clk.summary()
+    sm_mhz = clk_sum["sm_mhz"] or clk_sum["sm_max_mhz"] or pk.get("sm_max_mhz", 1965.0)
+
     def work_of(a):
-        return {
+        w = {
+            0: ("hbm", samples * 68, "68 B per sample: 24 B record in, 24 B ordered record + 16 B SoA lengths "
+                                     "+ 4 B order out (sort.cu)"),
             2: ("fp64", a["sl_a"] * 11 * kl, "11 FP64 ops per act_mem pricing per (layout, kind)"),
             3: (("hbm", a["band_b"], "8 B per band entry written (32-row tiles incl. masked entries)")
                 if reuse else ("fp64", a["sl_b"] * 17 * kl, f"{17 * kl} FP64 ops per band slice")),
-            4: ("hbm", a["bound_tr"] * 8, "8 B band entry per transition"),
-            5: ("hbm", (a["tr"] - a["bound_tr"]) * 8, "8 B band entry per transition"),
         }
+        if table:
+            # DP transitions read the L2-resident slice table: the bound is the
+            # SM issue rate; SURVEY §8(d) prices a transition at ~7 thread
+            # instructions (one add + compares + select)
+            w[4] = ("issue", a["bound_tr"] * 7 / 32, "7 thread-instructions per DP transition (SURVEY §8d)")
+            w[5] = ("issue", (a["tr"] - a["bound_tr"]) * 7 / 32, "7 thread-instructions per DP transition")
+        else:
+            w[4] = ("hbm", a["bound_tr"] * 8, "8 B band entry per transition")
+            w[5] = ("hbm", (a["tr"] - a["bound_tr"]) * 8, "8 B band entry per transition")
+        return w
 
     work = work_of(s_agg)
 
@@ -482,6 +500,11 @@ def report(args, cfg, W, capi, planner, stats, solo_stats, M, M_total, world, st
         if bound == "fp64":
             ach, peak, unit = units / secs / 1e12, fp64_peak, "TFLOP/s"
             src = "fp64 add rate measured in-run (pp_calibrate_fp64)"
+        elif bound == "issue":
+            ach, unit = units / secs / 1e9, "G warp-instr/s"
+            peak = 4 * props.multi_processor_count * sm_mhz / 1e3
+            src = (f"4 warp-instructions per cycle per SM x {props.multi_processor_count} SMs x "
+                   f"{sm_mhz:.0f} MHz (SM clock measured over the timed region)")
         else:
             ach, peak, unit = units / secs / 1e9, pk["hbm_gbs"], "GB/s"
             src = f"MEASURED_PEAKS.json hbm_gbs ({pk_kind}, burst)"
@@ -490,18 +513,28 @@ def report(args, cfg, W, capi, planner, stats, solo_stats, M, M_total, world, st
                 "avg_launch_ms": s_kern[cat] / max(int(s_launch[cat]), 1),
                 "share_of_step": s_kern[cat] / max(s_kern.sum(), 1e-9)}
 
-    cats = [c for c in work if s_kern[c] > 0]
-    dom = max(cats, key=lambda c: s_kern[c])
+    # (slice table: category 3 is the table build + candidate scan, no band bytes to price)
+    cats = [c for c in work if s_kern[c] > 0 and not (table and c == 3)]
+    dom = max((c for c in cats if c != 0), key=lambda c: s_kern[c])
     roof = roof_of(dom)
     roof["timing"] = (f"per-launch durations from {len(solo_stats)} untimed one-stream steps of {M} mini-batches "
                       "(CUDA events on the launching stream, each kernel alone on the GPU)")
     tr = traffic_record(cfg.name)
     if tr and names[dom] in tr["kernels"]:
-        per_plan = tr["kernels"][names[dom]]["dram_bytes_per_plan"]
+        rec = tr["kernels"][names[dom]]
+        per_plan = rec["dram_bytes_per_plan"]
         roof["traffic"] = per_plan * M
         roof["traffic_source"] = tr["source"]
         if work[dom][0] == "hbm":
             roof["traffic_vs_algorithmic"] = per_plan * M * len(solo_stats) / max(work[dom][1], 1)
+        for k in ("ncu_issue_active_pct", "ncu_warp_instr_per_transition", "ncu_ipc", "ncu_l2_hit_pct"):
+            if k in rec:
+                roof[k] = rec[k]
+    if 0 in cats:
+        roof["sort"] = {k: roof_of(0)[k] for k in ("bound", "achieved", "peak", "unit", "frac", "algorithmic",
+                                                   "avg_launch_ms")}
+        if tr and names[0] in tr["kernels"]:
+            roof["sort"]["traffic"] = tr["kernels"][names[0]]["dram_bytes_per_plan"] * M
     roof["all"] = {names[c]: {k: roof_of(c)[k] for k in ("bound", "achieved", "unit", "frac", "avg_launch_ms",
                                                          "share_of_step")} for c in cats}
     cpu = parity = None

@@ -134,6 +134,9 @@ typedef struct pp_tuning {
                               G[length][d] (a slice of such a mini-batch depends on its size
                               and padded length only), priced once, L2-resident, read by the
                               DP and the candidate scan — no band (gtab.cu) */
+  int32_t no_bin_intervals; /* 1: the slice-table candidate scan reads every table entry a
+                              mini-batch reaches; 0 (default): rows whose bins form an
+                              interval for every prefix are marked from two entries */
 } pp_tuning;
 
 /* Per-call result arrays, all caller-owned.  Arrays sized [total samples] are

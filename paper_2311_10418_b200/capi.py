@@ -92,7 +92,7 @@ class Tuning(C.Structure):
     _fields_ = [("first_wave", C.c_int32), ("max_wave", C.c_int32), ("streams", C.c_int32),
                 ("coop_min_n", C.c_int32), ("no_slice_reuse", C.c_int32), ("no_band_trunc", C.c_int32),
                 ("compact_band", C.c_int32), ("host_chunks", C.c_int32), ("dp_pricing", C.c_int32),
-                ("no_slice_table", C.c_int32)]
+                ("no_slice_table", C.c_int32), ("no_bin_intervals", C.c_int32)]
 
 
 class PlanOut(C.Structure):
@@ -363,10 +363,11 @@ class Planner:
 
     def set_tuning(self, first_wave: int = 1, max_wave: int = 16, streams: int = 1, coop_min_n: int = 0,
                    slice_reuse: bool = True, band_trunc: bool = True, compact_band: bool = False,
-                   host_chunks: int = 0, dp_pricing: bool = False, slice_table: bool = True):
+                   host_chunks: int = 0, dp_pricing: bool = False, slice_table: bool = True,
+                   bin_intervals: bool = True):
         t = Tuning(first_wave, max_wave, streams, coop_min_n, 0 if slice_reuse else 1, 0 if band_trunc else 1,
                    1 if compact_band else 0, host_chunks, 1 if dp_pricing else 0,
-                   0 if slice_table else 1)
+                   0 if slice_table else 1, 0 if bin_intervals else 1)
         rc = lib.pp_ctx_set_tuning(self._h, C.byref(t))
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())

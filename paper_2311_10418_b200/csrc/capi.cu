@@ -65,7 +65,7 @@ cudaError_t launch_cost_pass(int pass, const CostGrid& g, const double* tabT, co
 bool band_run_applies(const CostGrid& g, const double* tabT, int reuse, const double* tau, int sorted_in);
 // gtab.cu
 cudaError_t launch_gtab_need(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
-                             const int* blk_W, const double* in_d, int* need, cudaStream_t st);
+                             int max_blocks, const int* blk_W, const double* in_d, int* need, cudaStream_t st);
 cudaError_t launch_gtab_offsets(const int* need, int nK, int64_t* row_off, long long* total, cudaStream_t st);
 cudaError_t launch_gtab_fill(const CostGrid& g, double cap, const AxisPos* mbp, int nK, const int* need,
                              const int64_t* row_off, double* G, double* G1, cudaStream_t st);
@@ -73,7 +73,8 @@ cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* 
                               cudaStream_t st);
 cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int* gbase,
                              const int* need, const double* G, double interval, const double* tau,
-                             unsigned int* small_bm, SegStats* stats, cudaStream_t st);
+                             unsigned int* small_bm, SegStats* stats, int nK, const int64_t* row_off, int* rf,
+                             double* rlo, cudaStream_t st);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
                              int* row_w, int* blk_W, cudaStream_t st);
 cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -276,7 +277,7 @@ struct pp_ctx {
   bool compact = false;           // the band holds compact chunk records (pp_internal.cuh)
   bool priced = false;            // no band: the DP prices its slices in-kernel (dp.cu PRICE)
   bool gtab = false;              // no band: the call's shared slice table (gtab.cu)
-  DevBuf gt_need, gt_off, gt_total, gt_G, gt_base;
+  DevBuf gt_need, gt_off, gt_total, gt_G, gt_base, gt_rf, gt_rlo;
   PinBuf h_gt_total;
   int64_t gtab_entries = 0;
   DpPrice price{};                // its inputs
@@ -302,7 +303,7 @@ struct pp_ctx {
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
             &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
             &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act,
-            &cmin, &dp_cols, &colbase, &chunk_nv, &perm, &gt_need, &gt_off, &gt_total, &gt_G, &gt_base,
+            &cmin, &dp_cols, &colbase, &chunk_nv, &perm, &gt_need, &gt_off, &gt_total, &gt_G, &gt_base, &gt_rf, &gt_rlo,
             &os_tf, &os_tb, &os_act, &os_off, &os_lim, &os_pred, &os_assign, &os_idx, &os_cloff, &os_clk,
             &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status,
             &ing_bytes, &ing_scratch, &ing_out, &ing_off,
@@ -828,8 +829,11 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     PP_CUDA(ctx->gt_total.ensure(sizeof(long long)));
     PP_CUDA(ctx->h_gt_total.ensure(sizeof(long long)));
     PP_CUDA(ctx->gt_base.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
+    PP_CUDA(ctx->gt_rf.ensure((size_t)nK * sizeof(int)));
+    PP_CUDA(ctx->gt_rlo.ensure((size_t)nK * sizeof(double)));
     PP_CUDA(cudaMemsetAsync(ctx->gt_need.p, 0, (size_t)nK * sizeof(int), st));
-    PP_TIMED(3, launch_gtab_need(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks, ctx->blk_W.as<int>(),
+    PP_TIMED(3, launch_gtab_need(c.d_seg_off, ctx->blk_base.as<int>(), n_seg, total_blocks,
+                                 (int)((max_n + kRB - 1) / kRB), ctx->blk_W.as<int>(),
                                  ctx->in_d.as<double>(), ctx->gt_need.as<int>(), st));
     PP_TIMED(3, launch_gtab_offsets(ctx->gt_need.as<int>(), nK, ctx->gt_off.as<int64_t>(),
                                     ctx->gt_total.as<long long>(), st));
@@ -852,7 +856,9 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                   ctx->gt_base.as<int>(), st));
     PP_TIMED(3, launch_gtab_bins(c.d_seg_off, n_seg, ctx->in_d.as<double>(), ctx->gt_base.as<int>(),
                                  ctx->gt_need.as<int>(), ctx->gt_G.as<double>(), interval, tau_d, small_bm,
-                                 ctx->stats_d.as<SegStats>(), st));
+                                 ctx->stats_d.as<SegStats>(), nK, ctx->gt_off.as<int64_t>(),
+                                 ctx->tuning.no_bin_intervals ? nullptr : ctx->gt_rf.as<int>(),
+                                 ctx->gt_rlo.as<double>(), st));
     ctx->gtab = true;
     ctx->price = DpPrice{};
     ctx->price.gbase = ctx->gt_base.as<int>();

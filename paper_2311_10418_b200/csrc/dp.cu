@@ -157,6 +157,30 @@ struct Acc {
 //     compare against the (+inf, 0) identity or any taken value.
 //   MODE 3 also: bound sum min(x + B);  MODE 1: min sum and min over
 //     max(x, M) (the minimax t*);  MODE 2: min sum.
+// Lexicographic (sum, count) select of a descending-column fold: (hs, hc)
+// <- (cs, cn) when pre and (cs < hs or cs == hs and cn <= hc); returns the
+// decision.  Written in PTX so both compares of cs hang off the add in
+// parallel and one predicate OR feeds the selects — ptxas otherwise chains
+// the compares, pre and the count tie one after another behind the add,
+// which is the chain warp's critical path (the triangle's state step).
+__device__ __forceinline__ unsigned lex_select_desc(double cs, int cn, unsigned pre, double& hs, int& hc) {
+  unsigned u;
+  asm("{\n\t"
+      ".reg .pred pp, pt, pl, pe;\n\t"
+      "setp.ne.u32 pp, %5, 0;\n\t"
+      "setp.le.and.s32 pt, %4, %2, pp;\n\t"
+      "setp.lt.and.f64 pl, %3, %1, pp;\n\t"
+      "setp.eq.and.f64 pe, %3, %1, pt;\n\t"
+      "or.pred pl, pl, pe;\n\t"
+      "selp.f64 %1, %3, %1, pl;\n\t"
+      "selp.s32 %2, %4, %2, pl;\n\t"
+      "selp.u32 %0, 1, 0, pl;\n\t"
+      "}"
+      : "=r"(u), "+d"(hs), "+r"(hc)
+      : "d"(cs), "r"(cn), "r"(pre));
+  return u;
+}
+
 // fold_c takes the count through j already incremented (cn = 1 + C): the
 // DP state arrays store 1 + count, so the far-far loop adds nothing.
 template <int MODE, bool DESC>
@@ -164,7 +188,11 @@ __device__ __forceinline__ void fold_c(Acc& a, double xv, double ss, double sx, 
                                        double t) {
   constexpr bool CAND = MODE == 0 || MODE == 3;
   const double cs = __dadd_rn(xv, ss);
-  if (CAND) {
+  if (CAND && DESC) {
+    const unsigned pre = (okb & (xv <= t)) ? 1u : 0u;
+    const unsigned u = lex_select_desc(cs, cn, pre, a.s, a.c);
+    a.j = u ? j : a.j;
+  } else if (CAND) {
     const bool tie = DESC ? (cn <= a.c) : (cn < a.c);
     const bool upd = okb & (xv <= t) & ((cs < a.s) | ((cs == a.s) & tie));
     a.s = upd ? cs : a.s;
@@ -496,14 +524,39 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         Acc H2 = shfl_acc(A, max(nb - 2, 0));
         double Ss = 0.0, Sx = 0.0;  // state[k+1] as every lane knows it
         int Sc = 0;
+        // the step's tile entries, loaded one step ahead
+        auto ld1 = [&](int k) { return (FULL ? (k + 1 < kRB) : (k + 1 < nb)) ? lds_f64(U + (k + 1) * kRB + k) : 0.0; };
+        auto ldo = [&](int k) { return lds_f64(U + k * kRB + r); };
+        auto ldn = [&](int k) { return has_next ? lds_f64(U + (kRB + k) * kRB + r) : 0.0; };
+        const int kst = FULL ? kRB - 1 : nb - 1;  // the first step
+        double x1n = ld1(kst), xon = ldo(kst), xnn = ldn(kst);
 #pragma unroll
         for (int k = kRB - 1; k >= 0; --k) {
           if (FULL || k < nb) {
+            const double x1 = x1n, xo = xon, xn = xnn;
+            if (k > 0) {
+              x1n = ld1(k - 1);
+              xon = ldo(k - 1);
+              xnn = ldn(k - 1);
+            }
             // state[k]
             Acc h = H1;
             if (FULL ? (k + 1 < kRB) : (k + 1 < nb)) {
-              const double x1 = lds_f64(U + (k + 1) * kRB + k);
-              fold<MODE, true>(h, x1, Ss, Sx, Sc, 0, k + 1 < W, t);
+              if (CAND) {
+                // the critical path: cs -> {lt, eq} -> upd -> select; the
+                // slice's own tests (x1 <= t, in the tile) and the count
+                // tie are settled off it
+                const unsigned pre = ((k + 1 < W) & (x1 <= t)) ? 1u : 0u;
+                const double cs = __dadd_rn(x1, Ss);
+                const int cn = 1 + Sc;
+                lex_select_desc(cs, cn, pre, h.s, h.c);
+                if (MODE == 3) {
+                  const double cb = __dadd_rn(x1, Sx);
+                  h.x = ((k + 1 < W) & (cb < h.x)) ? cb : h.x;
+                }
+              } else {
+                fold<MODE, true>(h, x1, Ss, Sx, Sc, 0, k + 1 < W, t);
+              }
             }
             double ns = h.s, nx = h.x;
             if (SANITIZE) {
@@ -511,12 +564,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
               if (MODE == 3) nx = isfinite(nx) ? nx : INF;
             }
             // this lane's row (l < k) and its row of the next block
-            const double xo = lds_f64(U + k * kRB + r);
             fold<MODE, true>(A, xo, ns, nx, h.c, i0 + k, (r < k) & (k < W), t);
-            if (has_next) {
-              const double xn = lds_f64(U + (kRB + k) * kRB + r);
-              fold<MODE, true>(N, xn, ns, nx, h.c, i0 + k, k < cnx, t);
-            }
+            if (has_next) fold<MODE, true>(N, xn, ns, nx, h.c, i0 + k, k < cnx, t);
             Ss = ns;
             Sx = nx;
             Sc = h.c;

@@ -72,6 +72,81 @@ __global__ void gtab_need_kernel(const int64_t* __restrict__ seg_off, const int*
   }
 }
 
+// need[K] by runs (one CTA per segment; the same values as gtab_need_kernel
+// with one atomic per run instead of one per tile column that ends a run).
+// Block bl's tile covers slice ends j in [i0 + 1, E], E = i0 + W - 1, and a
+// run of equal lengths on positions [ps, pe] (slice ends [ps + 1, pe + 1])
+// meets it in its last column min(pe + 1, E) - i0 when i0 <= pe and
+// E >= max(ps, i0) + 1.  Over the blocks in ascending i0, the first one
+// that can meet the run is found by bisection on the prefix maximum of E;
+// the walk stops at the first block with E >= pe + 1 (every later block has
+// a larger i0, hence a smaller column).  No monotonicity is assumed.
+constexpr int kNeedMaxBlocks = 4096;
+__global__ void __launch_bounds__(256) gtab_need_runs_kernel(const int64_t* __restrict__ seg_off,
+                                                             const int* __restrict__ blk_base,
+                                                             const int* __restrict__ blk_W,
+                                                             const double* __restrict__ in_d,
+                                                             int* __restrict__ need) {
+  extern __shared__ int s_need[];
+  const int s = blockIdx.x;
+  const int64_t b0 = seg_off[s];
+  const int n = (int)(seg_off[s + 1] - b0);
+  const int gb0 = blk_base[s];
+  const int nblk = blk_base[s + 1] - gb0;
+  int* s_i0 = s_need;             // ascending block a: i0
+  int* s_E = s_i0 + nblk;         // its tile's last slice end (i0 - 1 + W)
+  int* s_pm = s_E + nblk;         // prefix max of s_E
+  for (int a = threadIdx.x; a < nblk; a += blockDim.x) {
+    const int bl = nblk - 1 - a;
+    const int i0 = max(0, n - kRB * (bl + 1));
+    s_i0[a] = i0;
+    s_E[a] = i0 + blk_W[gb0 + bl] - 1;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    int carry = INT_MIN;
+    for (int a0 = 0; a0 < nblk; a0 += 32) {
+      int v = a0 + lane < nblk ? s_E[a0 + lane] : INT_MIN;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = max(v, y);
+      }
+      v = max(v, carry);
+      if (a0 + lane < nblk) s_pm[a0 + lane] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  const double* in = in_d + b0;
+  for (int pe = threadIdx.x; pe < n; pe += blockDim.x) {
+    const double x = in[pe];
+    if (pe + 1 < n && in[pe + 1] == x) continue;  // not the run's last position
+    // ps = the run's first position (the segment is sorted ascending)
+    int lo = 0, hi = pe;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (in[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    const int ps = lo;
+    // first ascending block whose prefix-max end reaches ps + 1
+    int a = 0, ah = nblk;
+    while (a < ah) {
+      const int mid = (a + ah) >> 1;
+      if (s_pm[mid] < ps + 1) a = mid + 1; else ah = mid;
+    }
+    int best = 0;
+    for (; a < nblk; ++a) {
+      const int i0 = s_i0[a], E = s_E[a];
+      if (i0 > pe) break;
+      if (E >= max(ps, i0) + 1) best = max(best, min(pe + 1, E) - i0);
+      if (E >= pe + 1) break;
+    }
+    if (best > 0) atomicMax(&need[len_key(x)], best);
+  }
+}
+
 // Row offsets: rows of lengths with need > 0, each need + 32 entries
 // (d in [-31, need]); a 32-entry NaN row at offset 0 serves column 0 of the
 // top tiles (never a slice).  One CTA.
@@ -160,6 +235,56 @@ __global__ void gtab_gbase_kernel(const double* __restrict__ in_d, int64_t total
     gbase[k] = (int)(row_off[len_key(in_d[k])] + 31);
 }
 
+// Per table row K (after the fill): when the row's candidate bins are an
+// interval for every prefix — ival > 0, the non-NaN entries of d in
+// [1, need] are a prefix [1, f] of finite values whose bins q(d) =
+// ceil(G[K][d] / I) (microbatch.cpp:264) are finite and step by 0 or +1 —
+// then the bins of any prefix [1, D] are exactly [q(1), q(min(D, f))], and
+// gtab_bins_kernel marks them without scanning the row: rf[K] = f, rlo[K] =
+// q(1).  Otherwise rf[K] = -1 and the row is scanned entry by entry.
+__global__ void __launch_bounds__(32 * kGWarps) gtab_rowinfo_kernel(int nK, const int* __restrict__ need,
+                                                                    const int64_t* __restrict__ row_off,
+                                                                    const double* __restrict__ G, double ival,
+                                                                    int* __restrict__ rf, double* __restrict__ rlo) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * kGWarps;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  for (int K = blockIdx.x * kGWarps + (threadIdx.x >> 5); K < nK; K += warps) {
+    const int D = need[K];
+    if (D <= 0) continue;
+    const double* row = G + row_off[K] + 31;  // row[d]
+    int first_nan = D + 1, last_ok = 0;
+    bool bad = !(ival > 0.0);
+    for (int d = 1 + lane; d <= D && !bad; d += 32) {
+      const double T = row[d];
+      if (isnan(T)) {
+        first_nan = min(first_nan, d);
+        continue;
+      }
+      last_ok = max(last_ok, d);
+      const double q = ceil(__ddiv_rn(T, ival));
+      if (!(q < INF) || !(T < INF)) bad = true;
+      if (d < D) {
+        const double T2 = row[d + 1];
+        if (!isnan(T2)) {
+          const double q2 = ceil(__ddiv_rn(T2, ival));
+          if (!(q2 >= q && q2 <= q + 1.0)) bad = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      first_nan = min(first_nan, __shfl_xor_sync(0xffffffffu, first_nan, o));
+      last_ok = max(last_ok, __shfl_xor_sync(0xffffffffu, last_ok, o));
+    }
+    bad = __any_sync(0xffffffffu, bad) || last_ok > first_nan;
+    if (lane == 0) {
+      rf[K] = bad ? -1 : last_ok;
+      rlo[K] = (!bad && last_ok >= 1) ? ceil(__ddiv_rn(row[1], ival)) : 0.0;
+    }
+  }
+}
+
 // Candidate bins and statistics of each mini-batch from the table (the part
 // of cost pass B's band_run_kernel that the DP needs before its passes):
 // per run of equal lengths ending at position j (1-based slice end), the
@@ -174,7 +299,9 @@ __global__ void __launch_bounds__(256) gtab_bins_kernel(const int64_t* __restric
                                                         const double* __restrict__ G, double ival,
                                                         const double* __restrict__ tau,
                                                         unsigned int* __restrict__ small_bm,
-                                                        SegStats* __restrict__ stats) {
+                                                        SegStats* __restrict__ stats,
+                                                        const int* __restrict__ rf,
+                                                        const double* __restrict__ rlo) {
   constexpr int kTau = kSmallBmWords * 32;
   __shared__ double s_tau[kTau];
   __shared__ unsigned int s_bm[kSmallBmWords];
@@ -197,7 +324,38 @@ __global__ void __launch_bounds__(256) gtab_bins_kernel(const int64_t* __restric
   for (int p0 = wid * 32; p0 < n; p0 += nw * 32) {
     const int p = p0 + lane;
     const double x = p < n ? in_d[b0 + p] : 0.0;
-    const bool end = p < n && (p + 1 == n || !(in_d[b0 + p + 1] == x));
+    bool end = p < n && (p + 1 == n || !(in_d[b0 + p + 1] == x));
+    if (end && rf != nullptr) {
+      // interval rows (gtab_rowinfo_kernel): this lane marks its run alone
+      const int K = len_key(x);
+      const int f = rf[K];
+      if (f >= 0) {
+        end = false;
+        const int Dp = min(min(p + 1, need[K]), f);
+        if (Dp >= 1) {
+          const double* row = G + gbase[b0 + p];
+          const double t1 = row[1];  // the singleton of the run's samples
+          tsing = (tsing < t1) ? t1 : tsing;
+          scanned += (unsigned long long)Dp;
+          const double lo = rlo[K];
+          const double hi = ceil(__ddiv_rn(row[Dp], ival));
+          if (lo < (double)kTau) {
+            const int k0 = (int)lo, k1 = hi < (double)kTau ? (int)hi : kTau - 1;
+            any_binned = true;
+            for (int wd = k0 >> 5; wd <= (k1 >> 5); ++wd) {
+              const int a0 = max(k0, wd * 32) - wd * 32, a1 = min(k1, wd * 32 + 31) - wd * 32;
+              const unsigned int m = (a1 == 31 ? 0xffffffffu : ((1u << (a1 + 1)) - 1u)) & ~((1u << a0) - 1u);
+              atomicOr(&s_bm[wd], m);
+            }
+          }
+          if (!(hi < (double)kTau)) {
+            const double kl = (lo < (double)kTau) ? (double)kTau : lo;
+            kmn = (kl < kmn) ? kl : kmn;
+            kmx = (kmx < hi) ? hi : kmx;
+          }
+        }
+      }
+    }
     unsigned int ends = __ballot_sync(0xffffffffu, end);
     while (ends) {
       const int q = __ffs(ends) - 1;
@@ -273,7 +431,14 @@ __global__ void __launch_bounds__(256) gtab_bins_kernel(const int64_t* __restric
 }  // namespace
 
 cudaError_t launch_gtab_need(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
-                             const int* blk_W, const double* in_d, int* need, cudaStream_t st) {
+                             int max_blocks, const int* blk_W, const double* in_d, int* need, cudaStream_t st) {
+  if (n_seg > 0 && max_blocks <= kNeedMaxBlocks) {
+    const size_t smem = (size_t)3 * max_blocks * sizeof(int);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(gtab_need_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    gtab_need_runs_kernel<<<n_seg, 256, smem, st>>>(seg_off, blk_base, blk_W, in_d, need);
+    return cudaGetLastError();
+  }
   const int blocks = std::max(1, std::min((total_blocks + 7) / 8, 148 * 16));
   gtab_need_kernel<<<blocks, 256, 0, st>>>(seg_off, blk_base, n_seg, total_blocks, blk_W, in_d, need);
   return cudaGetLastError();
@@ -303,9 +468,15 @@ cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* 
 
 cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int* gbase,
                              const int* need, const double* G, double interval, const double* tau,
-                             unsigned int* small_bm, SegStats* stats, cudaStream_t st) {
+                             unsigned int* small_bm, SegStats* stats, int nK, const int64_t* row_off, int* rf,
+                             double* rlo, cudaStream_t st) {
+  if (rf) {
+    const int blocks = std::max(1, std::min((nK + kGWarps - 1) / kGWarps, 148 * 8));
+    gtab_rowinfo_kernel<<<blocks, 32 * kGWarps, 0, st>>>(nK, need, row_off, G, interval, rf, rlo);
+  }
   if (n_seg > 0)
-    gtab_bins_kernel<<<n_seg, 256, 0, st>>>(seg_off, in_d, gbase, need, G, interval, tau, small_bm, stats);
+    gtab_bins_kernel<<<n_seg, 256, 0, st>>>(seg_off, in_d, gbase, need, G, interval, tau, small_bm, stats, rf,
+                                            rlo);
   return cudaGetLastError();
 }
 

@@ -217,6 +217,54 @@ def test_slice_table_matches_band(name):
     b.close()
 
 
+@pytest.mark.parametrize("name", ["C1", "C3", "C4", "random"])
+def test_bin_intervals_match_row_scan(name):
+    """The candidate bins of interval rows (gtab_rowinfo_kernel: two table
+    entries per run) against the entry-by-entry scan of the same rows:
+    identical plans, candidate sets, reference-loop counts and scanned-entry
+    counts (BASELINE configs, and random grids with fine intervals where the
+    bins step by more than one and rows fall back to the scan)."""
+    cases = []
+    if name == "random":
+        rng = np.random.default_rng(99)
+        for k in range(12):
+            M, n = int(rng.integers(1, 6)), int(rng.integers(2, 900))
+            s = capi.synthetic_dataset(n * M, int(rng.choice([64, 1024, 8192])), 900 + k, W.INPUT_DIST)
+            s[:, 0] = rng.permutation(n * M) + 1
+            C = int(rng.choice([2, 4, 16]))
+            model = capi.Model.uniform(C, 2, False)
+            tot = 1e5 * n
+            cases.append((s, np.arange(M + 1, dtype=np.int64) * n, capi.synthetic_grid(), model, C,
+                          float(rng.choice([math.inf, 50.0, 400.0])), float(rng.choice([5.0, tot / 64, tot / 4096]))))
+    else:
+        cfg = W.CONFIGS[name]
+        M = {"C1": 64, "C3": 6, "C4": 24}[name]
+        cases.append((W.dataset(cfg, M), W.seg_offsets(cfg, M), W.grid(), W.model(cfg), cfg.stages, cfg.mem_cap,
+                      cfg.interval))
+    a = capi.Planner(0)
+    b = capi.Planner(0)
+    b.set_tuning(bin_intervals=False)
+    for s, off, grid, model, C, cap, interval in cases:
+        ra = a.plan_batch(s, off, grid, model, C, 1, cap, interval)
+        sa = a.stats()
+        rb = b.plan_batch(s, off, grid, model, C, 1, cap, interval)
+        sb = b.stats()
+        for k in ("ordered", "status", "err_sample_id"):
+            assert ra[k].tobytes() == rb[k].tobytes(), k
+        for q in range(len(off) - 1):
+            if ra["status"][q] != 0:
+                continue
+            m = int(ra["count"][q])
+            for k in ("count", "t_max_used", "objective"):
+                assert ra[k][q] == rb[k][q] or (ra[k][q] != ra[k][q] and rb[k][q] != rb[k][q]), (k, q)
+            for k in ("splits", "mb_times"):
+                assert ra[k][off[q]:off[q] + m].tobytes() == rb[k][off[q]:off[q] + m].tobytes(), (k, q)
+        for k in ("candidates_generated", "candidates_ref_evaluated", "slices_pass_b", "bound_transitions"):
+            assert sa[k] == sb[k], (k, sa[k], sb[k])
+    a.close()
+    b.close()
+
+
 def test_slice_table_random_vs_oracle(orc):
     """The slice-table path on random length-sorted GPT mini-batches
     (duplicate-heavy and distinct lengths, binding and loose caps, several
