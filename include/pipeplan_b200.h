@@ -269,6 +269,35 @@ int pp_plan_op_costs_device(pp_ctx* ctx, const pp_sample* d_ordered, const int64
                             const pp_model_desc* model, int64_t capacity, int64_t* mb_offset,
                             double* d_t_f, double* d_t_b, double* d_act_mem);
 
+/* select_recomputation (src/schedule.cpp:319-364, include/pipeplan/
+ * schedule.h:114-120; called per replica at planner.cpp:83-84), batched over
+ * n_seg partitions: for each, the first strategy of {None, Selective, Full}
+ * (in that order) whose bit is set in strategies_mask (1 << Recompute) and
+ * whose OpCostTable::from_shapes has every act_mem(mb, j) < limits[j]
+ * (limits: n_stages host doubles).  Per partition: strategy (the Recompute
+ * value, or -1 when none fits — the reference's InfeasibleError) and
+ * violating_stage (-1, or the lowest stage violated by the LAST strategy
+ * tried: the exception's stage); rows mb_offset[s]..mb_offset[s+1] of the
+ * t_f / t_b / act_mem tables hold the chosen strategy's costs.
+ * PP_ERR_INVALID "no recompute strategies to try" for an empty mask
+ * (schedule.cpp:323).  The reference's RecomputeSelection::schedule
+ * (schedule_adaptive over the identity order) is not returned: plan_iteration
+ * never reads it, and the order search evaluates the identity order itself.
+ * Host buffers: shapes as pp_op_costs, mb_offset n_seg + 1 entries. */
+int pp_select_recomputation(pp_ctx* ctx, const pp_padded_shape* shapes, const int64_t* mb_offset, int32_t n_seg,
+                            const pp_grid_desc* grid, const pp_model_desc* model, int32_t strategies_mask,
+                            const double* limits, double* t_f, double* t_b, double* act_mem, int32_t* strategy,
+                            int32_t* violating_stage);
+/* The same for plans already on the device (pp_plan_grid_device outputs),
+ * like pp_plan_op_costs_device: mb_offset (host) is filled, the d_* outputs
+ * are device arrays (tables of capacity x n_stages doubles, n_seg int32s). */
+int pp_select_recomputation_device(pp_ctx* ctx, const pp_sample* d_ordered, const int64_t* d_seg_offsets,
+                                   const int64_t* h_seg_offsets, int32_t n_seg, const int32_t* d_splits,
+                                   const int32_t* d_count, const pp_grid_desc* grid, const pp_model_desc* model,
+                                   int32_t strategies_mask, const double* limits, int64_t capacity,
+                                   int64_t* mb_offset, double* d_t_f, double* d_t_b, double* d_act_mem,
+                                   int32_t* d_strategy, int32_t* d_violating_stage);
+
 /* Injection-order search of the per-replica planner:
  * order_microbatches(predicted, costs, limits, n_clusters, evaluator)
  * (src/schedule.cpp:277-317, include/pipeplan/schedule.h:101-108) with the

@@ -261,6 +261,8 @@ class Reference:
                                          C.POINTER(_Opts), i32, vp, vp, vp, vp, vp, vp, vp]
         L.ref_plan_batch_out.restype = dbl
         L.ref_op_costs.argtypes = [vp, i64, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), vp, vp, vp]
+        L.ref_select_recomputation.argtypes = [vp, vp, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), i32, vp,
+                                               vp, vp, vp, vp, vp]
         L.ref_order_search.argtypes = [vp, vp, vp, vp, i32, i32, vp, i32, dbl, i32, vp, vp, vp, vp, vp, vp]
         L.ref_order_search.restype = dbl
         L.ref_load_record_file.argtypes = [C.c_char_p, i64, vp, i64, vp, vp, vp, vp]
@@ -295,6 +297,25 @@ class Reference:
         if rc != PP_OK:
             raise ValueError(f"reference from_shapes failed: {rc}")
         return tf, tb, act
+
+    def select_recomputation(self, shapes, mb_offset, grid, model, strategies=(0, 1, 2), limits=None):
+        """The reference's select_recomputation per partition of shapes ->
+        dict like capi.Planner.select_recomputation."""
+        sh = np.ascontiguousarray(shapes, np.int64).reshape(-1, 3)
+        off = np.ascontiguousarray(mb_offset, np.int64)
+        g, k1 = grid_desc(grid)
+        m, k2 = model_desc(model)
+        S, C_ = len(off) - 1, len(model.encoder_layers)
+        lim = np.ascontiguousarray(limits, np.float64)
+        mask = sum(1 << int(r) for r in strategies)
+        tf, tb, act = (np.zeros((max(len(sh), 1), C_)) for _ in range(3))
+        st, vs = np.zeros(S, np.int32), np.zeros(S, np.int32)
+        rc = self.L.ref_select_recomputation(_p(sh), _p(off), S, C.byref(g), C.byref(m), mask, _p(lim), _p(tf),
+                                             _p(tb), _p(act), _p(st), _p(vs))
+        if rc != PP_OK:
+            raise ValueError(f"reference select_recomputation failed: {rc}")
+        n = len(sh)
+        return {"strategy": st, "violating_stage": vs, "t_f": tf[:n], "t_b": tb[:n], "act_mem": act[:n]}
 
     def order_search(self, t_f, t_b, act_mem, mb_offset, limits, n_clusters=3, comm_latency=0.0,
                      threads=1):

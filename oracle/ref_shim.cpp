@@ -407,6 +407,51 @@ int ref_op_costs(const pp_padded_shape* shapes, int64_t n, const pp_grid_desc* g
 }
 
 
+// select_recomputation (src/schedule.cpp:319-364) per partition, on
+// micro-batches carrying the given padded shapes; strategy -1 and the
+// InfeasibleError's stage when none fits.  Tables as ref_op_costs.
+int ref_select_recomputation(const pp_padded_shape* shapes, const int64_t* mb_off, int32_t n_seg,
+                             const pp_grid_desc* g, const pp_model_desc* m, int32_t mask, const double* limits,
+                             double* t_f, double* t_b, double* act, int32_t* strategy, int32_t* violating) {
+  try {
+    ProfileGrid grid = grid_from_desc(g);
+    ModelConfig cfg = model_from_desc(m);
+    const int C = cfg.stage_count();
+    std::vector<Recompute> allowed;
+    for (int r = 0; r < 3; ++r)
+      if (mask & (1 << r)) allowed.push_back(static_cast<Recompute>(r));
+    std::vector<double> lim(limits, limits + C);
+    for (int s = 0; s < n_seg; ++s) {
+      MicroBatchPartition part;
+      for (int64_t k = mb_off[s]; k < mb_off[s + 1]; ++k) {
+        MicroBatch mb;
+        mb.padded_mbs = shapes[k].mbs;
+        mb.padded_input_len = shapes[k].input_len;
+        mb.padded_target_len = shapes[k].target_len;
+        part.micro_batches.push_back(mb);
+      }
+      try {
+        RecomputeSelection sel = select_recomputation(grid, cfg, part, lim, allowed);
+        strategy[s] = static_cast<int32_t>(sel.strategy);
+        violating[s] = -1;
+        const std::size_t o = static_cast<std::size_t>(mb_off[s]) * C;
+        std::memcpy(t_f + o, sel.costs.t_f.data(), sel.costs.t_f.size() * sizeof(double));
+        std::memcpy(t_b + o, sel.costs.t_b.data(), sel.costs.t_b.size() * sizeof(double));
+        std::memcpy(act + o, sel.costs.act_mem.data(), sel.costs.act_mem.size() * sizeof(double));
+      } catch (const InfeasibleError& e) {
+        strategy[s] = -1;
+        violating[s] = e.stage();
+      }
+    }
+    return PP_OK;
+  } catch (const std::invalid_argument&) {
+    return PP_ERR_INVALID;
+  } catch (const std::logic_error&) {
+    return PP_ERR_NOT_CONVERGED;
+  }
+}
+
+
 // order_microbatches with plan_iteration's evaluator (planner.cpp:94-108)
 // over n_seg op-cost tables, then the chosen order's schedule_adaptive ->
 // plan_communication -> simulate report, exactly as plan_iteration builds

@@ -33,7 +33,8 @@ EXPORTED = [
     "pp_synthetic_grid", "pp_synthetic_dataset", "pp_slice_cost_host", "pp_calibrate_fp64",
     "pp_op_costs", "pp_plan_op_costs_device", "pp_order_search", "pp_order_search_device",
     "pp_load_records", "pp_load_records_device", "pp_draw_minibatches", "pp_draw_minibatches_device",
-    "pp_padding_report", "pp_assign_replicas", "pp_pack_plan_slots",
+    "pp_padding_report", "pp_assign_replicas", "pp_pack_plan_slots", "pp_select_recomputation",
+    "pp_select_recomputation_device",
 ]
 
 
@@ -155,6 +156,10 @@ def _load():
     lib.pp_slice_cost_host.argtypes = [C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, i64, i64, vp, vp]
     lib.pp_calibrate_fp64.argtypes = [C.c_int, C.POINTER(dbl)]
     lib.pp_op_costs.argtypes = [vp, vp, i64, C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, vp, vp]
+    lib.pp_select_recomputation.argtypes = [vp, vp, vp, i32, C.POINTER(GridDesc), C.POINTER(ModelDesc), i32, vp,
+                                            vp, vp, vp, vp, vp]
+    lib.pp_select_recomputation_device.argtypes = [vp, vp, vp, vp, i32, vp, vp, C.POINTER(GridDesc),
+                                                   C.POINTER(ModelDesc), i32, vp, i64, vp, vp, vp, vp, vp, vp]
     lib.pp_plan_op_costs_device.argtypes = [vp, vp, vp, vp, i32, vp, vp, C.POINTER(GridDesc),
                                             C.POINTER(ModelDesc), i64, vp, vp, vp, vp]
     lib.pp_load_records.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp]
@@ -513,6 +518,46 @@ class Planner:
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())
         return tf, tb, act
+
+    def select_recomputation(self, shapes, mb_offset, grid: Grid, model: Model, strategies=(0, 1, 2),
+                             limits=None) -> dict:
+        """select_recomputation per partition (rows mb_offset[s]..[s+1] of
+        shapes): {"strategy": (S,) Recompute or -1, "violating_stage": (S,),
+        "t_f"/"t_b"/"act_mem": (rows, n_stages) of the chosen strategy}."""
+        sh = np.ascontiguousarray(shapes, np.int64).reshape(-1, 3)
+        off = np.ascontiguousarray(mb_offset, np.int64)
+        S, C_ = len(off) - 1, len(model.encoder_layers)
+        lim = np.ascontiguousarray(limits, np.float64)
+        mask = sum(1 << int(r) for r in strategies)
+        tf, tb, act = (np.zeros((max(len(sh), 1), C_)) for _ in range(3))
+        st, vs = np.zeros(S, np.int32), np.zeros(S, np.int32)
+        rc = lib.pp_select_recomputation(self._h, _p(sh), _p(off), S, C.byref(grid.desc()), C.byref(model.desc()),
+                                         mask, _p(lim), _p(tf), _p(tb), _p(act), _p(st), _p(vs))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        n = len(sh)
+        return {"strategy": st, "violating_stage": vs, "t_f": tf[:n], "t_b": tb[:n], "act_mem": act[:n]}
+
+    def select_recomputation_device(self, d_ordered, d_seg_offsets, h_seg_offsets, d_splits, d_count,
+                                    grid: Grid, model: Model, limits, d_tf, d_tb, d_act, d_strategy,
+                                    d_violating, strategies=(0, 1, 2)) -> np.ndarray:
+        """select_recomputation for every plan already on the device; returns
+        mb_offset (host); tables / strategy / violating stage into the d_* tensors."""
+        h_off = np.ascontiguousarray(h_seg_offsets, np.int64)
+        S = len(h_off) - 1
+        mb_off = np.zeros(S + 1, np.int64)
+        cap = d_tf.numel() // len(model.encoder_layers)
+        lim = np.ascontiguousarray(limits, np.float64)
+        mask = sum(1 << int(r) for r in strategies)
+        rc = lib.pp_select_recomputation_device(
+            self._h, C.c_void_p(d_ordered.data_ptr()), C.c_void_p(d_seg_offsets.data_ptr()), _p(h_off), S,
+            C.c_void_p(d_splits.data_ptr()), C.c_void_p(d_count.data_ptr()), C.byref(grid.desc()),
+            C.byref(model.desc()), mask, _p(lim), cap, _p(mb_off), C.c_void_p(d_tf.data_ptr()),
+            C.c_void_p(d_tb.data_ptr()), C.c_void_p(d_act.data_ptr()), C.c_void_p(d_strategy.data_ptr()),
+            C.c_void_p(d_violating.data_ptr()))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        return mb_off
 
     def plan_op_costs_device(self, d_ordered, d_seg_offsets, h_seg_offsets, d_splits, d_count,
                              grid: Grid, model: Model, d_tf, d_tb, d_act) -> np.ndarray:

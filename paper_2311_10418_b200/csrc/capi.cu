@@ -114,6 +114,10 @@ cudaError_t launch_mb_shapes(const pp_sample* ordered, const int64_t* seg_off, c
 cudaError_t launch_op_costs(const CostGrid& g, const double* le_st, const double* ld_st, int stages,
                             const pp_padded_shape* shapes, int64_t n, double* t_f, double* t_b,
                             double* act, cudaStream_t st);
+cudaError_t launch_recompute_select(const int64_t* mb_off, int n_seg, int C, int n_tries, const int* tries,
+                                    int64_t n_mb, const double* tf_all, const double* tb_all,
+                                    const double* act_all, const double* limits, int32_t* strategy,
+                                    int32_t* violating, double* t_f, double* t_b, double* act, cudaStream_t st);
 size_t dp_coop_parts_bytes(int grid);
 size_t order_search_slot_bytes(int64_t max_m, int C);
 int order_search_warps(int64_t n_items, int C, size_t slot_bytes, size_t budget);
@@ -278,6 +282,7 @@ struct pp_ctx {
   bool priced = false;            // no band: the DP prices its slices in-kernel (dp.cu PRICE)
   bool gtab = false;              // no band: the call's shared slice table (gtab.cu)
   DevBuf gt_need, gt_off, gt_total, gt_G, gt_base, gt_rf, gt_rlo;
+  DevBuf rc_tab, rc_lim, rc_out;  // select_recomputation
   PinBuf h_gt_total;
   int64_t gtab_entries = 0;
   DpPrice price{};                // its inputs
@@ -291,6 +296,7 @@ struct pp_ctx {
   // concurrent sub-batch contexts (pp_tuning::streams), created on demand
   std::vector<pp_ctx*> subs;
   cudaEvent_t ev_in = nullptr;
+  cudaEvent_t ev_done = nullptr;  // (sub-context) its stream's work of a plan_split part
   // per-launch event pairs for kernel timing (pp_stats::ms_kernel)
   std::vector<cudaEvent_t> kev;
   std::vector<int> kcat;
@@ -303,7 +309,7 @@ struct pp_ctx {
             &gstate, &seg_item_start, &seg_item_cnt, &segdp, &best_next, &bound_items, &bound_res,
             &out_splits, &out_times, &out_count, &out_tmax, &out_obj, &out_status, &out_err,
             &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act,
-            &cmin, &dp_cols, &colbase, &chunk_nv, &perm, &gt_need, &gt_off, &gt_total, &gt_G, &gt_base, &gt_rf, &gt_rlo,
+            &cmin, &dp_cols, &colbase, &chunk_nv, &perm, &gt_need, &gt_off, &gt_total, &gt_G, &gt_base, &gt_rf, &gt_rlo, &rc_tab, &rc_lim, &rc_out,
             &os_tf, &os_tb, &os_act, &os_off, &os_lim, &os_pred, &os_assign, &os_idx, &os_cloff, &os_clk,
             &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status,
             &ing_bytes, &ing_scratch, &ing_out, &ing_off,
@@ -1473,12 +1479,19 @@ int plan_split(pp_ctx* ctx, const PlanCall& c, int parts) {
         cc.d_obj = c.d_obj ? c.d_obj + s0 : nullptr;
         cc.d_status = c.d_status ? c.d_status + s0 : nullptr;
         cc.d_err = c.d_err ? c.d_err + s0 : nullptr;
-        rc = run_plan(sub, cc);  // synchronises its stream before returning
+        rc = run_plan(sub, cc);
       }
+      // the sub-stream's completion, for the caller's stream below (run_plan
+      // happens to synchronise its stream today; the event keeps the
+      // single-stream semantics if it stops doing so)
+      if (!sub->ev_done) cu(cudaEventCreateWithFlags(&sub->ev_done, cudaEventDisableTiming));
+      cu(cudaEventRecord(sub->ev_done, sub->stream));
       rcs[p] = rc;
     });
   }
   for (auto& t : th) t.join();
+  for (int p = 0; p < parts; ++p)
+    if (ctx->subs[p]->ev_done) PP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->subs[p]->ev_done, 0));
   pp_stats S{};
   S.exit_thresh = INFINITY;
   for (int p = 0; p < parts; ++p) {
@@ -1547,6 +1560,7 @@ int pp_ctx_destroy(pp_ctx* ctx) {
   ctx->subs.clear();
   cudaSetDevice(ctx->device);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->cstream) {
     cudaStreamSynchronize(ctx->cstream);
@@ -2145,6 +2159,131 @@ int pp_plan_op_costs_device(pp_ctx* ctx, const pp_sample* d_ordered, const int64
   PP_CUDA(launch_op_costs(g, ctx->stage_lay.as<double>(), ctx->stage_lay.as<double>() + C, C,
                           ctx->shapes.as<pp_padded_shape>(), n_mb, d_t_f, d_t_b, d_act_mem, st));
   PP_CUDA(cudaStreamSynchronize(st));  // lay and the offsets die here
+  return PP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// select_recomputation over device-resident shapes (ctx->shapes, n_mb rows,
+// ctx->mb_off per table): one op-cost table per allowed strategy, then the
+// per-table choice (opcost.cu recompute_select_kernel).
+int select_recompute_run(pp_ctx* ctx, const pp_grid_desc* grid, const pp_model_desc* model, int32_t mask,
+                         const double* limits, int32_t n_seg, int64_t n_mb, double* d_t_f, double* d_t_b,
+                         double* d_act, int32_t* d_strategy, int32_t* d_violating) {
+  cudaStream_t st = ctx->stream;
+  int tries[3], n_tries = 0;
+  for (int r = 0; r < 3; ++r)  // the reference's canonical order (schedule.cpp:332-336)
+    if (mask & (1 << r)) tries[n_tries++] = r;
+  const int C = model->n_stages;
+  std::vector<double> lay(2 * (size_t)C);
+  for (int j = 0; j < C; ++j) {
+    lay[j] = model->encoder_layers[j] > 0 ? (double)model->encoder_layers[j] : 0.0;
+    lay[C + j] = model->decoder_layers[j] > 0 ? (double)model->decoder_layers[j] : 0.0;
+  }
+  const size_t tab = (size_t)std::max<int64_t>(n_mb, 1) * C;
+  PP_CUDA(ctx->stage_lay.ensure(lay.size() * sizeof(double)));
+  PP_CUDA(ctx->rc_tab.ensure(3 * (size_t)n_tries * tab * sizeof(double)));
+  PP_CUDA(ctx->rc_lim.ensure((size_t)C * sizeof(double)));
+  PP_CUDA(cudaMemcpyAsync(ctx->stage_lay.p, lay.data(), lay.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->rc_lim.p, limits, (size_t)C * sizeof(double), cudaMemcpyHostToDevice, st));
+  double* tf_all = ctx->rc_tab.as<double>();
+  double* tb_all = tf_all + (size_t)n_tries * tab;
+  double* act_all = tb_all + (size_t)n_tries * tab;
+  for (int q = 0; q < n_tries; ++q) {
+    pp_model_desc m = *model;
+    m.recompute = tries[q];
+    CostGrid g{};
+    int rc = upload_grid(ctx, grid, &m, &g);
+    if (rc) return rc;
+    PP_CUDA(launch_op_costs(g, ctx->stage_lay.as<double>(), ctx->stage_lay.as<double>() + C, C,
+                            ctx->shapes.as<pp_padded_shape>(), n_mb, tf_all + q * tab, tb_all + q * tab,
+                            act_all + q * tab, st));
+  }
+  PP_CUDA(launch_recompute_select(ctx->mb_off.as<int64_t>(), n_seg, C, n_tries, tries, n_mb, tf_all, tb_all,
+                                  act_all, ctx->rc_lim.as<double>(), d_strategy, d_violating, d_t_f, d_t_b,
+                                  d_act, st));
+  return PP_OK;
+}
+
+int select_recompute_check(pp_ctx* ctx, int32_t n_seg, const pp_model_desc* model, int32_t mask,
+                           const double* limits) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n_seg < 1 || !model || !limits) return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  if ((mask & 7) == 0) return fail(ctx, PP_ERR_INVALID, "no recompute strategies to try");  // schedule.cpp:323
+  if (model->n_stages < 1) return fail(ctx, PP_ERR_INVALID, "stage and layer counts must be >= 1");
+  return PP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pp_select_recomputation(pp_ctx* ctx, const pp_padded_shape* shapes, const int64_t* mb_offset, int32_t n_seg,
+                            const pp_grid_desc* grid, const pp_model_desc* model, int32_t strategies_mask,
+                            const double* limits, double* t_f, double* t_b, double* act_mem, int32_t* strategy,
+                            int32_t* violating_stage) {
+  int rc = select_recompute_check(ctx, n_seg, model, strategies_mask, limits);
+  if (rc) return rc;
+  if (!mb_offset || !strategy || !violating_stage || (mb_offset[n_seg] > 0 && (!shapes || !t_f || !t_b || !act_mem)))
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  cudaStream_t st = ctx->stream;
+  const int64_t n_mb = mb_offset[n_seg];
+  const int C = model->n_stages;
+  PP_CUDA(ctx->shapes.ensure(std::max<int64_t>(n_mb, 1) * sizeof(pp_padded_shape)));
+  PP_CUDA(ctx->mb_off.ensure((n_seg + 1) * sizeof(int64_t)));
+  PP_CUDA(ctx->oc_tf.ensure(std::max<int64_t>(n_mb, 1) * C * sizeof(double)));
+  PP_CUDA(ctx->oc_tb.ensure(std::max<int64_t>(n_mb, 1) * C * sizeof(double)));
+  PP_CUDA(ctx->oc_act.ensure(std::max<int64_t>(n_mb, 1) * C * sizeof(double)));
+  PP_CUDA(ctx->rc_out.ensure(2 * (size_t)n_seg * sizeof(int32_t)));
+  if (n_mb > 0)
+    PP_CUDA(cudaMemcpyAsync(ctx->shapes.p, shapes, n_mb * sizeof(pp_padded_shape), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->mb_off.p, mb_offset, (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  int32_t* d_sv = ctx->rc_out.as<int32_t>();
+  if ((rc = select_recompute_run(ctx, grid, model, strategies_mask, limits, n_seg, n_mb, ctx->oc_tf.as<double>(),
+                                 ctx->oc_tb.as<double>(), ctx->oc_act.as<double>(), d_sv, d_sv + n_seg)))
+    return rc;
+  if (n_mb > 0) {
+    PP_CUDA(cudaMemcpyAsync(t_f, ctx->oc_tf.p, n_mb * C * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(cudaMemcpyAsync(t_b, ctx->oc_tb.p, n_mb * C * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(cudaMemcpyAsync(act_mem, ctx->oc_act.p, n_mb * C * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  PP_CUDA(cudaMemcpyAsync(strategy, d_sv, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaMemcpyAsync(violating_stage, d_sv + n_seg, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaStreamSynchronize(st));
+  return PP_OK;
+}
+
+int pp_select_recomputation_device(pp_ctx* ctx, const pp_sample* d_ordered, const int64_t* d_seg_offsets,
+                                   const int64_t* h_seg_offsets, int32_t n_seg, const int32_t* d_splits,
+                                   const int32_t* d_count, const pp_grid_desc* grid, const pp_model_desc* model,
+                                   int32_t strategies_mask, const double* limits, int64_t capacity,
+                                   int64_t* mb_offset, double* d_t_f, double* d_t_b, double* d_act_mem,
+                                   int32_t* d_strategy, int32_t* d_violating_stage) {
+  int rc = select_recompute_check(ctx, n_seg, model, strategies_mask, limits);
+  if (rc) return rc;
+  if (!d_ordered || !d_seg_offsets || !h_seg_offsets || !d_splits || !d_count || !mb_offset || !d_strategy ||
+      !d_violating_stage)
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  cudaStream_t st = ctx->stream;
+  std::vector<int32_t> cnt(n_seg);
+  PP_CUDA(cudaMemcpyAsync(cnt.data(), d_count, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaStreamSynchronize(st));
+  mb_offset[0] = 0;
+  for (int s = 0; s < n_seg; ++s) mb_offset[s + 1] = mb_offset[s] + std::max(cnt[s], 0);
+  const int64_t n_mb = mb_offset[n_seg];
+  if (n_mb > capacity) return fail(ctx, PP_ERR_INVALID, "op-cost table capacity too small");
+  PP_CUDA(ctx->mb_off.ensure((n_seg + 1) * sizeof(int64_t)));
+  PP_CUDA(ctx->shapes.ensure(std::max<int64_t>(n_mb, 1) * sizeof(pp_padded_shape)));
+  PP_CUDA(cudaMemcpyAsync(ctx->mb_off.p, mb_offset, (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  PP_CUDA(launch_mb_shapes(d_ordered, d_seg_offsets, d_splits, ctx->mb_off.as<int64_t>(), n_seg, n_mb,
+                           ctx->shapes.as<pp_padded_shape>(), st));
+  if ((rc = select_recompute_run(ctx, grid, model, strategies_mask, limits, n_seg, n_mb, d_t_f, d_t_b, d_act_mem,
+                                 d_strategy, d_violating_stage)))
+    return rc;
+  PP_CUDA(cudaStreamSynchronize(st));  // the host offsets and limits die here
   return PP_OK;
 }
 

@@ -56,8 +56,11 @@ std::vector<InjectionOrder> search_injection_orders(std::span<const OpCostTable>
         throw std::logic_error("adaptive scheduler failed to converge; invariant violated");
       case PP_ERR_NOT_EXECUTABLE:
         throw std::logic_error("schedule is not executable: circular dependency between devices");
+      case PP_ERR_INVALID:  // a device limit (order_search.h), not a reference error
+        throw std::invalid_argument("op durations must be non-negative and not NaN (device order search)");
       default:
-        throw std::invalid_argument("op durations must be non-negative (device order search)");
+        throw std::runtime_error("pipeplan_b200 device order search: status " +
+                                 std::to_string(st[static_cast<std::size_t>(s)]));
     }
     InjectionOrder& r = out[static_cast<std::size_t>(s)];
     const std::int64_t b = off[static_cast<std::size_t>(s)], m = off[static_cast<std::size_t>(s) + 1] - b;

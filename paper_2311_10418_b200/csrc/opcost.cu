@@ -85,7 +85,67 @@ __global__ void op_cost_kernel(CostGrid g, const double* __restrict__ le_st, con
   }
 }
 
+// select_recomputation (src/schedule.cpp:319-364) over n_seg op-cost
+// tables at once, one CTA per table: the first allowed strategy, in the
+// reference's cheapest-compute-first order (None, Selective, Full), whose
+// every act_mem(mb, j) < limits[j]; the violating stage of a strategy that
+// does not fit is the smallest j holding an act >= limit (the reference's
+// j-major scan with its break), and a table that fits no strategy reports
+// the LAST tried strategy's stage (InfeasibleError's stage).  The chosen
+// strategy's rows are copied to the output tables.
+__global__ void __launch_bounds__(256) recompute_select_kernel(
+    const int64_t* __restrict__ mb_off, int C, int n_tries, int3 tries, int64_t n_mb,
+    const double* __restrict__ tf_all, const double* __restrict__ tb_all, const double* __restrict__ act_all,
+    const double* __restrict__ limits, int32_t* __restrict__ strategy, int32_t* __restrict__ violating,
+    double* __restrict__ t_f, double* __restrict__ t_b, double* __restrict__ act) {
+  __shared__ int s_min;
+  const int s = blockIdx.x;
+  const int64_t r0 = mb_off[s] * C, r1 = mb_off[s + 1] * C;
+  int chosen = -1, viol = -1;
+  for (int q = 0; q < n_tries; ++q) {
+    if (threadIdx.x == 0) s_min = C;
+    __syncthreads();
+    const double* a = act_all + (size_t)q * n_mb * C;
+    int m = C;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      const int j = (int)(i % C);
+      if (a[i] >= limits[j]) m = min(m, j);
+    }
+    if (m < C) atomicMin(&s_min, m);
+    __syncthreads();
+    const int vj = s_min;
+    __syncthreads();
+    if (vj == C) {
+      chosen = q;
+      break;
+    }
+    viol = vj;
+  }
+  if (threadIdx.x == 0) {
+    strategy[s] = chosen < 0 ? -1 : (chosen == 0 ? tries.x : chosen == 1 ? tries.y : tries.z);
+    violating[s] = chosen < 0 ? viol : -1;
+  }
+  if (chosen < 0) return;
+  const size_t o = (size_t)chosen * n_mb * C;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    t_f[i] = tf_all[o + i];
+    t_b[i] = tb_all[o + i];
+    act[i] = act_all[o + i];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_recompute_select(const int64_t* mb_off, int n_seg, int C, int n_tries, const int* tries,
+                                    int64_t n_mb, const double* tf_all, const double* tb_all,
+                                    const double* act_all, const double* limits, int32_t* strategy,
+                                    int32_t* violating, double* t_f, double* t_b, double* act, cudaStream_t st) {
+  if (n_seg <= 0) return cudaSuccess;
+  const int3 tr = make_int3(tries[0], n_tries > 1 ? tries[1] : -1, n_tries > 2 ? tries[2] : -1);
+  recompute_select_kernel<<<n_seg, 256, 0, st>>>(mb_off, C, n_tries, tr, n_mb, tf_all, tb_all, act_all, limits,
+                                                 strategy, violating, t_f, t_b, act);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_mb_shapes(const pp_sample* ordered, const int64_t* seg_off, const int32_t* splits,
                              const int64_t* mb_off, int n_seg, int64_t n_mb, pp_padded_shape* shapes,

@@ -860,6 +860,124 @@ def test_plan_op_costs_device_match_reference_shapes(planner):
         assert ref[0].tobytes() == host[0].tobytes() and ref[2].tobytes() == host[2].tobytes()
 
 
+def _recompute_cases(rng, grid, model, orc_act):
+    """(shapes, mb_offset, limits, strategies) cases around the strategies'
+    activation maxima: every strategy fits, only Selective / Full fit, none
+    fits, limits on the boundary (act == limit violates), empty partitions,
+    restricted strategy sets."""
+    cases = []
+    for k in range(16):
+        S = int(rng.integers(1, 7))
+        counts = rng.integers(0 if k % 5 == 0 else 1, 40, S)
+        off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        n = int(off[-1])
+        sh = np.stack([rng.integers(1, 300, n), rng.integers(0, 9000, n), rng.integers(0, 700, n)], 1).astype(np.int64)
+        acts = [orc_act(sh, r) for r in range(3)]  # per strategy (n, C) tables
+        C_ = len(model.encoder_layers)
+        mx = [a.max(0) if len(a) else np.zeros(C_) for a in acts]
+        pick = k % 4
+        if pick == 0:
+            lim = mx[0] * 1.01 + 1.0           # everything fits: None
+        elif pick == 1:
+            lim = (mx[0] + mx[1]) / 2          # None violates somewhere, Selective may fit
+        elif pick == 2:
+            lim = np.minimum(mx[2], mx[1]) * 0.5  # nothing fits: the last strategy's stage
+        else:
+            lim = mx[1].copy()                 # boundary: act == limit violates
+        strategies = [(0, 1, 2), (2,), (1, 2), (0, 2)][k % 4]
+        cases.append((sh, off, np.ascontiguousarray(lim, np.float64), strategies))
+    return cases
+
+
+def test_select_recomputation_matches_reference(planner):
+    """pp_select_recomputation (schedule.cpp:319-364)
+    against the reference's select_recomputation on the same shapes: chosen
+    strategy, InfeasibleError stage, and the chosen tables bit for bit
+    (GPT and T5, 4 and 8 stages)."""
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    ref = Reference()
+    rng = np.random.default_rng(31)
+    grid = W.grid()
+    for C_, encdec in ((4, False), (8, True)):
+        model = capi.Model.uniform(C_, 2, encdec)
+
+        def orc_act(sh, r):
+            m = capi.Model.uniform(C_, 2, encdec, recompute=r)
+            return planner.op_costs(sh, grid, m)[2] if len(sh) else np.zeros((0, C_))
+
+        for sh, off, lim, strat in _recompute_cases(rng, grid, model, orc_act):
+            got = planner.select_recomputation(sh, off, grid, model, strat, lim)
+            exp = ref.select_recomputation(sh, off, grid, model, strat, lim)
+            assert got["strategy"].tolist() == exp["strategy"].tolist(), (strat, got["strategy"], exp["strategy"])
+            assert got["violating_stage"].tolist() == exp["violating_stage"].tolist()
+            for q in range(len(off) - 1):
+                if exp["strategy"][q] < 0:
+                    continue
+                a, b = off[q], off[q + 1]
+                for k in ("t_f", "t_b", "act_mem"):
+                    assert got[k][a:b].tobytes() == exp[k][a:b].tobytes(), (k, q)
+    with pytest.raises(capi.InvalidArgument):
+        planner.select_recomputation(sh, off, grid, model, (), lim)
+
+
+def test_select_recomputation_device_plans(planner):
+    """select_recomputation over device-resident C1 plans (the padded shape of
+    each planned micro-batch) equals the host entry point on those shapes;
+    limits make some mini-batches take Selective / Full."""
+    import torch
+
+    cfg = W.CONFIGS["C1"]
+    M = 48
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    d_s, d_off = torch.from_numpy(s).cuda(), torch.from_numpy(off).cuda()
+    tot = M * cfg.n
+    out = {"ordered": torch.empty((tot, 3), dtype=torch.int64, device="cuda"),
+           "splits": torch.empty(tot, dtype=torch.int32, device="cuda"),
+           "mb_times": torch.empty(tot, dtype=torch.float64, device="cuda"),
+           "count": torch.empty(M, dtype=torch.int32, device="cuda"),
+           "t_max_used": torch.empty(M, dtype=torch.float64, device="cuda"),
+           "objective": torch.empty(M, dtype=torch.float64, device="cuda"),
+           "status": torch.empty(M, dtype=torch.int32, device="cuda"),
+           "err_sample_id": torch.empty(M, dtype=torch.int64, device="cuda")}
+    planner.plan_batch_device(d_s, d_off, off, out, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap,
+                              cfg.interval)
+    C_ = cfg.stages
+    model = W.model(cfg)
+    ordered, splits, count = (out[k].cpu().numpy() for k in ("ordered", "splits", "count"))
+    shapes, mbo = [], [0]
+    for q in range(M):
+        lo = 0
+        for e in splits[off[q]:off[q] + count[q]]:
+            blk = ordered[off[q] + lo:off[q] + e]
+            shapes.append((e - lo, max(0, blk[:, 1].max()), max(0, blk[:, 2].max())))
+            lo = e
+        mbo.append(len(shapes))
+    shapes = np.array(shapes, np.int64)
+    act0 = planner.op_costs(shapes, W.grid(), model)[2]
+    lim = np.quantile(act0, 0.9, axis=0)  # the heaviest mini-batches must recompute
+    tf, tb, act = (torch.empty(len(shapes) * C_, dtype=torch.float64, device="cuda") for _ in range(3))
+    st, vs = (torch.empty(M, dtype=torch.int32, device="cuda") for _ in range(2))
+    mb_off = planner.select_recomputation_device(out["ordered"], d_off, off, out["splits"], out["count"],
+                                                 W.grid(), model, lim, tf, tb, act, st, vs)
+    assert mb_off.tolist() == mbo
+    host = planner.select_recomputation(shapes, np.array(mbo), W.grid(), model, (0, 1, 2), lim)
+    assert st.cpu().numpy().tolist() == host["strategy"].tolist()
+    assert vs.cpu().numpy().tolist() == host["violating_stage"].tolist()
+    assert len(set(host["strategy"].tolist())) > 1  # the limits really split the strategies
+    n = len(shapes)
+    for q in range(M):
+        if host["strategy"][q] < 0:
+            continue
+        a, b = mbo[q] * C_, mbo[q + 1] * C_
+        for k, d in (("t_f", tf), ("t_b", tb), ("act_mem", act)):
+            assert host[k].reshape(-1)[a:b].tobytes() == d[a:b].cpu().numpy().tobytes(), (k, q)
+    if reference_available():
+        exp = Reference().select_recomputation(shapes, np.array(mbo), W.grid(), model, (0, 1, 2), lim)
+        assert exp["strategy"].tolist() == host["strategy"].tolist()
+
+
 def test_pack_plan_slots_kernel_matches_host_packing(planner):
     """pp_pack_plan_slots (csrc/slots.cu) packs device plans into exactly the
     slots shard.pack_slots builds on the host, order included; unpacked
