@@ -56,6 +56,7 @@
 #include <type_traits>
 
 #include "pp_internal.cuh"
+#include "dp_fold.cuh"
 
 namespace ppb {
 
@@ -70,6 +71,7 @@ constexpr int kChainWarp = kWorkers + 1;     // warp 9
 
 #ifdef PP_DP_TRACE
 __device__ long long* g_dp_trace = nullptr;  // [block][16] clock64 stamps of CTA 0
+__device__ int g_dp_flags = 0;               // bit 0: workers skip the far-far columns (timing only)
 #define PP_TRACE(slot)                                                           \
   do {                                                                            \
     if (g_dp_trace && blockIdx.x == 0 && lane == 0) g_dp_trace[b * 16 + (slot)] = clock64(); \
@@ -139,99 +141,6 @@ __device__ __forceinline__ int far_chunks_needed(int nc, const double* __restric
     if (m) return base + __ffs(m) - 1;
   }
   return nc;
-}
-
-// One row's running state: sum s, second value x (bound sum / minimax),
-// count c and argmin j (CAND modes).
-struct Acc {
-  double s, x;
-  int c, j;
-};
-
-// The DP transition of one tile entry into a row accumulator, for the mode's
-// recurrences (microbatch.cpp:176-186; the bound pass :274-279).  `ss`, `sx`,
-// `sc` are state[j]; DESC: columns arrive in descending j, so an equal
-// (sum, count) takes the new (lower) j; otherwise ascending j keeps the old.
-//   CAND (MODE 0 / 3): (x + S, 1 + C) when x <= t and it is lexicographically
-//     smaller.  NaN entries (infeasible slices) and +inf states fail every
-//     compare against the (+inf, 0) identity or any taken value.
-//   MODE 3 also: bound sum min(x + B);  MODE 1: min sum and min over
-//     max(x, M) (the minimax t*);  MODE 2: min sum.
-// Lexicographic (sum, count) select of a descending-column fold: (hs, hc)
-// <- (cs, cn) when pre and (cs < hs or cs == hs and cn <= hc); returns the
-// decision.  Written in PTX so both compares of cs hang off the add in
-// parallel and one predicate OR feeds the selects — ptxas otherwise chains
-// the compares, pre and the count tie one after another behind the add,
-// which is the chain warp's critical path (the triangle's state step).
-__device__ __forceinline__ unsigned lex_select_desc(double cs, int cn, unsigned pre, double& hs, int& hc) {
-  unsigned u;
-  asm("{\n\t"
-      ".reg .pred pp, pt, pl, pe;\n\t"
-      "setp.ne.u32 pp, %5, 0;\n\t"
-      "setp.le.and.s32 pt, %4, %2, pp;\n\t"
-      "setp.lt.and.f64 pl, %3, %1, pp;\n\t"
-      "setp.eq.and.f64 pe, %3, %1, pt;\n\t"
-      "or.pred pl, pl, pe;\n\t"
-      "selp.f64 %1, %3, %1, pl;\n\t"
-      "selp.s32 %2, %4, %2, pl;\n\t"
-      "selp.u32 %0, 1, 0, pl;\n\t"
-      "}"
-      : "=r"(u), "+d"(hs), "+r"(hc)
-      : "d"(cs), "r"(cn), "r"(pre));
-  return u;
-}
-
-// fold_c takes the count through j already incremented (cn = 1 + C): the
-// DP state arrays store 1 + count, so the far-far loop adds nothing.
-template <int MODE, bool DESC>
-__device__ __forceinline__ void fold_c(Acc& a, double xv, double ss, double sx, int cn, int j, bool okb,
-                                       double t) {
-  constexpr bool CAND = MODE == 0 || MODE == 3;
-  const double cs = __dadd_rn(xv, ss);
-  if (CAND && DESC) {
-    const unsigned pre = (okb & (xv <= t)) ? 1u : 0u;
-    const unsigned u = lex_select_desc(cs, cn, pre, a.s, a.c);
-    a.j = u ? j : a.j;
-  } else if (CAND) {
-    const bool tie = DESC ? (cn <= a.c) : (cn < a.c);
-    const bool upd = okb & (xv <= t) & ((cs < a.s) | ((cs == a.s) & tie));
-    a.s = upd ? cs : a.s;
-    a.c = upd ? cn : a.c;
-    a.j = upd ? j : a.j;
-  } else {
-    a.s = (okb & (cs < a.s)) ? cs : a.s;
-  }
-  if (MODE == 3) {
-    const double cb = __dadd_rn(xv, sx);
-    a.x = (okb & (cb < a.x)) ? cb : a.x;
-  } else if (MODE == 1) {
-    const double v = (xv < sx) ? sx : xv;
-    a.x = (okb & (v < a.x)) ? v : a.x;
-  }
-}
-template <int MODE, bool DESC>
-__device__ __forceinline__ void fold(Acc& a, double xv, double ss, double sx, int sc, int j, bool okb,
-                                     double t) {
-  fold_c<MODE, DESC>(a, xv, ss, sx, 1 + sc, j, okb, t);
-}
-
-// (s, c, j) lexmin with lowest-j ties.
-__device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int c0, int j0) {
-  return s1 < s0 || (s1 == s0 && (c1 < c0 || (c1 == c0 && j1 < j0)));
-}
-// Combine two partial accumulators over disjoint column sets (associative).
-template <int MODE>
-__device__ __forceinline__ void combine(Acc& a, const Acc& o) {
-  constexpr bool CAND = MODE == 0 || MODE == 3;
-  if (CAND) {
-    const bool tk = better(o.s, o.c, o.j, a.s, a.c, a.j);
-    a.s = tk ? o.s : a.s;
-    a.c = tk ? o.c : a.c;
-    a.j = tk ? o.j : a.j;
-  } else {
-    a.s = (o.s < a.s) ? o.s : a.s;
-  }
-  if (MODE == 1 || MODE == 3) a.x = (o.x < a.x) ? o.x : a.x;
 }
 
 // MODE 0: DP pass of one t_max candidate: (sum, count, next) per row.
@@ -505,72 +414,44 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       mbar_wait(&unit_full[ub], ((b + 1) >> 1) & 1);
       PP_TRACE(1);
       PP_TRACE(2);
-      // ---- the triangle.  Iteration k: every lane computes state[k] from
-      // H_k (lane k's accumulator over columns >= k+2) and T[k, k+1] exactly
-      // as lane k folds it, then lane l < k folds T[l, k] + state[k] and every
-      // lane folds the next block's T'[l, nbn + k] + state[k]; lane k-2's
-      // accumulator (now over columns >= k) is shuffled for iteration k-2.
-      auto shfl_acc = [&](const Acc& a, int src) {
-        Acc h;
-        h.s = __shfl_sync(0xffffffffu, a.s, src);
-        h.x = X2 ? __shfl_sync(0xffffffffu, a.x, src) : INF;
-        h.c = CAND ? __shfl_sync(0xffffffffu, a.c, src) : 0;
-        h.j = 0;
-        return h;
-      };
+      // ---- the triangle.  Iteration k: every lane l <= k folds the slice
+      // (l, k+1) with state[k+1] (lane k's row is then complete: state[k]),
+      // lane k's accumulator is shuffled to every lane, and every lane folds
+      // state[k] into its row of the NEXT block (near-far column k).  The
+      // serial path per row is one fold and one shuffle round trip
+      // (tools/chain_probe.cu: ~64 cycles per row alone on an SM, against
+      // ~110 for recomputing each state redundantly from accumulators
+      // shuffled two rows ahead).
       auto triangle = [&](auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
-        Acc H1 = shfl_acc(A, nb - 1);
-        Acc H2 = shfl_acc(A, max(nb - 2, 0));
-        double Ss = 0.0, Sx = 0.0;  // state[k+1] as every lane knows it
+        double Ss = 0.0, Sx = 0.0;  // state[k+1] (every lane)
         int Sc = 0;
-        // the step's tile entries, loaded one step ahead
-        auto ld1 = [&](int k) { return (FULL ? (k + 1 < kRB) : (k + 1 < nb)) ? lds_f64(U + (k + 1) * kRB + k) : 0.0; };
-        auto ldo = [&](int k) { return lds_f64(U + k * kRB + r); };
-        auto ldn = [&](int k) { return has_next ? lds_f64(U + (kRB + k) * kRB + r) : 0.0; };
+        auto lda = [&](int k) { return (FULL ? (k + 1 < kRB) : (k + 1 < nb)) ? lds_f64(U + (k + 1) * kRB + r) : 0.0; };
+        auto ldn = [&](int k) { return lds_f64(U + (kRB + k) * kRB + r); };
         const int kst = FULL ? kRB - 1 : nb - 1;  // the first step
-        double x1n = ld1(kst), xon = ldo(kst), xnn = ldn(kst);
+        double xan = lda(kst), xnn = ldn(kst);
 #pragma unroll
         for (int k = kRB - 1; k >= 0; --k) {
           if (FULL || k < nb) {
-            const double x1 = x1n, xo = xon, xn = xnn;
-            if (k > 0) {
-              x1n = ld1(k - 1);
-              xon = ldo(k - 1);
+            const double xa = xan, xn = xnn;
+            if (k > 0) {  // the next step's entries, one step ahead
+              xan = lda(k - 1);
               xnn = ldn(k - 1);
             }
-            // state[k]
-            Acc h = H1;
-            if (FULL ? (k + 1 < kRB) : (k + 1 < nb)) {
-              if (CAND) {
-                // the critical path: cs -> {lt, eq} -> upd -> select; the
-                // slice's own tests (x1 <= t, in the tile) and the count
-                // tie are settled off it
-                const unsigned pre = ((k + 1 < W) & (x1 <= t)) ? 1u : 0u;
-                const double cs = __dadd_rn(x1, Ss);
-                const int cn = 1 + Sc;
-                lex_select_desc(cs, cn, pre, h.s, h.c);
-                if (MODE == 3) {
-                  const double cb = __dadd_rn(x1, Sx);
-                  h.x = ((k + 1 < W) & (cb < h.x)) ? cb : h.x;
-                }
-              } else {
-                fold<MODE, true>(h, x1, Ss, Sx, Sc, 0, k + 1 < W, t);
-              }
-            }
-            double ns = h.s, nx = h.x;
+            if (FULL ? (k + 1 < kRB) : (k + 1 < nb))
+              fold<MODE, true>(A, xa, Ss, Sx, Sc, i0 + k + 1, (r <= k) & (k + 1 < W), t);
+            double ns = shfl_f64(A.s, k);
+            double nx = X2 ? shfl_f64(A.x, k) : INF;
+            const int nc = CAND ? shfl_i32(A.c, k) : 0;
             if (SANITIZE) {
               ns = isfinite(ns) ? ns : INF;
               if (MODE == 3) nx = isfinite(nx) ? nx : INF;
             }
-            // this lane's row (l < k) and its row of the next block
-            fold<MODE, true>(A, xo, ns, nx, h.c, i0 + k, (r < k) & (k < W), t);
-            if (has_next) fold<MODE, true>(N, xn, ns, nx, h.c, i0 + k, k < cnx, t);
+            // (k < cnx is false without a next block; ldn then reads the idle buffer half)
+            fold<MODE, true>(N, xn, ns, nx, nc, i0 + k, k < cnx, t);
             Ss = ns;
             Sx = nx;
-            Sc = h.c;
-            H1 = H2;
-            if (k >= 2) H2 = shfl_acc(A, k - 2);
+            Sc = nc;
           }
         }
       };
@@ -618,7 +499,11 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         const int j1 = n - kRB * bn;
         const int k0 = max(0, j1 - kRB);  // i0 of block b+1
         const int Wn = blk_W[gb0 + bn];
+#ifdef PP_DP_TRACE
+        const int nc = (g_dp_flags & 1) ? 0 : (GTAB ? n_chunks(Wn) : far_nc(gb0 + bn, Wn));
+#else
         const int nc = GTAB ? n_chunks(Wn) : far_nc(gb0 + bn, Wn);
+#endif
         Acc a0 = kIdent, a1 = kIdent;
         // a multiple of 32 (k0 + 64 == n mod 32) except on the last block of a
         // segment whose n is not a multiple of 32: then scalar state loads
@@ -1165,6 +1050,9 @@ __global__ void __launch_bounds__(256)
 #ifdef PP_DP_TRACE
 extern "C" int pp_debug_dp_trace(long long* d_buf) {
   return cudaMemcpyToSymbol(g_dp_trace, &d_buf, sizeof(d_buf)) == cudaSuccess ? 0 : 4;
+}
+extern "C" int pp_debug_dp_flags(int flags) {
+  return cudaMemcpyToSymbol(g_dp_flags, &flags, sizeof(flags)) == cudaSuccess ? 0 : 4;
 }
 #endif
 // smem_state = the largest shared-memory DP state of the launch's items

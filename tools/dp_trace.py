@@ -27,13 +27,17 @@ def main():
     buf = torch.zeros(nblk * 16, dtype=torch.int64, device="cuda")
     capi.lib.pp_debug_dp_trace.argtypes = [ctypes.c_void_p]
     assert capi.lib.pp_debug_dp_trace(ctypes.c_void_p(buf.data_ptr())) == 0
+    # DP_FLAGS=1: the workers skip the far-far columns (wrong plans; isolates the chain's timing)
+    assert capi.lib.pp_debug_dp_flags(int(os.environ.get("DP_FLAGS", "0"))) == 0
     p = capi.Planner(0)
     # QB_TUNE="slice_table=0": A/B switches, as in tools/quick_bench.py
     tune = {k: bool(int(v)) for k, v in (kv.split("=") for kv in os.environ.get("QB_TUNE", "").split(",") if kv)}
     p.set_tuning(**tune)
-    s = W.dataset(cfg, 1)
+    M = int(os.environ.get("DP_M", "1"))  # mini-batches planned together (CTA 0 is traced)
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
     for _ in range(2):
-        p.plan(s, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+        p.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
     torch.cuda.synchronize()
     t = buf.view(nblk, 16).cpu().numpy().astype(np.int64)
     ok = t[:, 0] > 0

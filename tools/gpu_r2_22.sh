@@ -1,0 +1,6 @@
+# straight-line triangle steps (inline shfl.sync, unconditional next-block fold)
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_parity_gpu.py -x -q > gpurun_out/r2_22_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2_22_pytest.log
+timeout 600 python tools/ab_bench.py C3 296 "slice_table=1" 2>&1 | tee gpurun_out/r2_22_ab_c3.log
+timeout 600 python tools/ab_bench.py C4 512 "slice_table=1" 2>&1 | tee gpurun_out/r2_22_ab_c4.log
+PIPEPLAN_B200_LIB=build/trace/libpipeplan_b200_trace.so timeout 300 python tools/dp_trace.py C3 2>&1 | tee gpurun_out/r2_22_trace.log | tail -12
