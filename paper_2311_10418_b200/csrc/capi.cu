@@ -28,6 +28,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <string>
@@ -231,6 +232,41 @@ struct PinBuf {
   }
 };
 
+// Small transfers of the planning path (offsets, work lists, per-segment
+// statistics, read-backs) run as a one-CTA copy kernel through mapped pinned
+// memory (UVA: a cudaMallocHost pointer is valid on the device), never on a
+// copy engine: a host-buffer call keeps the engines busy with tens of MB of
+// samples and plans, and a small cudaMemcpyAsync — pageable or not — can
+// queue behind them for milliseconds while the planning stream waits on it.
+__global__ void small_copy_kernel(const unsigned int* __restrict__ src, unsigned int* __restrict__ dst, size_t words) {
+  for (size_t k = threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
+}
+cudaError_t small_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  small_copy_kernel<<<1, 256, 0, st>>>(static_cast<const unsigned int*>(src), static_cast<unsigned int*>(dst),
+                                       (bytes + 3) / 4);
+  return cudaGetLastError();
+}
+
+// Pinned staging arena for small_copy uploads: bump-allocated within a
+// planning call (every call ends with its stream synchronised, so the next
+// call starts over); a request that does not fit waits for the stream.
+struct PinArena {
+  PinBuf buf;
+  size_t off = 0;
+  void* take(size_t bytes, cudaStream_t st) {
+    bytes = (bytes + 15) / 16 * 16;
+    if (off + bytes > buf.cap) {
+      if (cudaStreamSynchronize(st) != cudaSuccess) return nullptr;
+      off = 0;
+      if (bytes > buf.cap && buf.ensure(std::max<size_t>(bytes, (size_t)1 << 20)) != cudaSuccess) return nullptr;
+    }
+    void* p = static_cast<char*>(buf.p) + off;
+    off += bytes;
+    return p;
+  }
+};
+
 // One staging set of a pipelined host-buffer worker (plan_host_chunks):
 // device inputs and outputs of one chunk, the pinned segment offsets, and the
 // events that order its copies against the compute stream.
@@ -289,6 +325,11 @@ struct pp_ctx {
   int price_lay = 0;              // its layout class (kLayDec1 / kLayEncDec2)
   // pipelined host-buffer worker (plan_host_chunks): copy stream + two sets
   cudaStream_t cstream = nullptr;
+  cudaStream_t ostream = nullptr;             // plan_host_pieces: device->host copies
+  PinArena arena;                             // small_copy uploads of the planning path
+  PinBuf h_word;                              // small_copy read-back scratch
+  std::vector<cudaEvent_t> piece_ev;          // plan_host_pieces: inputs in / part planned
+  PinBuf piece_off;                           // plan_host_pieces: part-relative offsets (pinned)
   HostSet hset[2];
   CostGrid grid_dev{};            // device view of the uploaded grid
   bool grid_valid = false;
@@ -358,9 +399,34 @@ cudaError_t timed_end(pp_ctx* ctx) { return cudaEventRecord(ctx->kev[ctx->kused+
     PP_CUDA(timed_end(ctx));        \
   } while (0)
 
+// PP_E2E_TRACE=1: host timestamps (µs since the first mark) of planning
+// phases, to stderr (development aid).
+void trace_mark(const char* what) {
+  static const bool on = std::getenv("PP_E2E_TRACE") != nullptr;
+  if (!on) return;
+  static const auto t0 = std::chrono::steady_clock::now();
+  const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  std::fprintf(stderr, "phase %9.1f us  %s\n", us, what);
+}
+
 int fail(pp_ctx* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
   return code;
+}
+
+// Upload `bytes` of host memory to device memory on the ctx stream through
+// the pinned arena and small_copy (see small_copy_kernel).
+cudaError_t up(pp_ctx* ctx, void* d_dst, const void* h_src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  void* stage = ctx->arena.take(bytes, ctx->stream);
+  if (!stage) return cudaErrorMemoryAllocation;
+  std::memcpy(stage, h_src, bytes);
+  return small_copy(d_dst, stage, bytes, ctx->stream);
+}
+// Device memory into PINNED host memory (a PinBuf) on the ctx stream; the
+// caller synchronises the stream before reading it.
+cudaError_t down(pp_ctx* ctx, void* h_pinned, const void* d_src, size_t bytes) {
+  return small_copy(h_pinned, d_src, bytes, ctx->stream);
 }
 
 // Everything one planning call needs, all device pointers unless h_*.
@@ -749,9 +815,8 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
   PP_CUDA(ctx->band_base.ensure(n_seg * sizeof(int64_t)));
   SegStats* hs = ctx->h_stats.as<SegStats>();
   for (int s = 0; s < n_seg; ++s) hs[s] = SegStats{~0ULL, 0ULL, 0ULL, INT_MAX, 0, 0, 0, 0, 0ULL, 0ULL, 0ULL};
-  PP_CUDA(cudaMemcpyAsync(ctx->stats_d.p, hs, n_seg * sizeof(SegStats), cudaMemcpyHostToDevice, st));
-  PP_CUDA(cudaMemcpyAsync(ctx->blk_base.p, blk_base.data(), (n_seg + 1) * sizeof(int),
-                          cudaMemcpyHostToDevice, st));
+  PP_CUDA(up(ctx, ctx->stats_d.p, hs, n_seg * sizeof(SegStats)));
+  PP_CUDA(up(ctx, ctx->blk_base.p, blk_base.data(), (n_seg + 1) * sizeof(int)));
   const double cap = c.opts.per_mb_mem_cap;
   // Pass A (or its closed form when every slice is memory-feasible).
   const bool full_rows = !table && cap == INFINITY;
@@ -782,8 +847,9 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
       std::vector<double> tau;
       bin_thresholds(interval, tau);
       PP_CUDA(ctx->tau.ensure(tau.size() * sizeof(double)));
-      PP_CUDA(cudaMemcpyAsync(ctx->tau.p, tau.data(), tau.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+      PP_CUDA(up(ctx, ctx->tau.p, tau.data(), tau.size() * sizeof(double)));
       PP_CUDA(cudaStreamSynchronize(st));  // tau dies at scope exit
+      trace_mark("passA tau sync");
       ctx->tau_interval = interval;
     }
     tau_d = ctx->tau.as<double>();
@@ -803,8 +869,9 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     PP_TIMED(1, launch_tile_offsets(ctx->blk_W.as<int>(), ctx->blk_base.as<int>(), n_seg,
                                     ctx->tile_off.as<int64_t>(), ctx->stats_d.as<SegStats>(), st));
   }
-  PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(down(ctx, hs, ctx->stats_d.p, n_seg * sizeof(SegStats)));
   PP_CUDA(cudaStreamSynchronize(st));
+  trace_mark("passA stats sync");
   // Band allocation (tiles are NaN-filled: masked / unused entries).
   std::vector<int64_t> band_base(n_seg);
   int64_t band_total = 0;
@@ -843,8 +910,9 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                  ctx->in_d.as<double>(), ctx->gt_need.as<int>(), st));
     PP_TIMED(3, launch_gtab_offsets(ctx->gt_need.as<int>(), nK, ctx->gt_off.as<int64_t>(),
                                     ctx->gt_total.as<long long>(), st));
-    PP_CUDA(cudaMemcpyAsync(ctx->h_gt_total.p, ctx->gt_total.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(down(ctx, ctx->h_gt_total.p, ctx->gt_total.p, sizeof(long long)));
     PP_CUDA(cudaStreamSynchronize(st));
+    trace_mark("gtab total sync");
     const int64_t entries = *ctx->h_gt_total.as<long long>();
     ctx->gtab_entries = entries;
     // row bases are int32 (dp.cu reads G[base - r]): a larger table takes the band
@@ -871,8 +939,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     ctx->price.g_odd = ctx->gt_G.as<double>() + g1_at;
   }
   if (!price_in_dp && !use_gtab) PP_CUDA(ctx->band.ensure(std::max<int64_t>(band_total, 1) * sizeof(double)));
-  PP_CUDA(cudaMemcpyAsync(ctx->band_base.p, band_base.data(), n_seg * sizeof(int64_t),
-                          cudaMemcpyHostToDevice, st));
+  PP_CUDA(up(ctx, ctx->band_base.p, band_base.data(), n_seg * sizeof(int64_t)));
   // (no fill: pass B writes every tile entry, NaN where no slice is feasible)
   // Per-chunk minimum slice times for the candidate passes' truncation (dp.cu):
   // one slot per 1024 band entries plus one per block bounds every tile's chunks.
@@ -949,8 +1016,9 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
     }
     ctx->trunc_margin = time_trunc_margin(ctx, max_n, lo, hi);
   }
-  PP_CUDA(cudaMemcpyAsync(hs, ctx->stats_d.p, n_seg * sizeof(SegStats), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(down(ctx, hs, ctx->stats_d.p, n_seg * sizeof(SegStats)));
   PP_CUDA(cudaStreamSynchronize(st));
+  trace_mark("passB stats sync");
   return PP_OK;
 }
 
@@ -1031,6 +1099,7 @@ const int* dp_gbase(const pp_ctx* ctx) { return ctx->gtab ? ctx->gt_base.as<int>
 
 // The planning pipeline (steps 1-7 above).
 int run_plan(pp_ctx* ctx, const PlanCall& c) {
+  ctx->arena.off = 0;  // (the previous call ended with its stream synchronised)
   cudaStream_t st = ctx->stream;
   const int n_seg = c.n_seg;
   if (c.h_seg_off[0] != 0) return fail(ctx, PP_ERR_INVALID, "seg_offsets[0] must be 0");
@@ -1119,11 +1188,11 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   PP_CUDA(ctx->cand_off.ensure((n_seg + 1) * sizeof(int64_t)));
   PP_CUDA(ctx->cand.ensure(std::max<int64_t>(cand_off[n_seg], 1) * sizeof(double)));
   PP_CUDA(ctx->cand_n.ensure(n_seg * sizeof(int)));
-  PP_CUDA(cudaMemcpyAsync(ctx->bitmap_off.p, bm_off.data(), (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  PP_CUDA(cudaMemcpyAsync(ctx->seg_mode.p, mode.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
-  PP_CUDA(cudaMemcpyAsync(ctx->active.p, active.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
-  PP_CUDA(cudaMemcpyAsync(ctx->raw_off.p, raw_off.data(), (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  PP_CUDA(cudaMemcpyAsync(ctx->cand_off.p, cand_off.data(), (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  PP_CUDA(up(ctx, ctx->bitmap_off.p, bm_off.data(), (n_seg + 1) * sizeof(int64_t)));
+  PP_CUDA(up(ctx, ctx->seg_mode.p, mode.data(), n_seg * sizeof(int)));
+  PP_CUDA(up(ctx, ctx->active.p, active.data(), n_seg * sizeof(int)));
+  PP_CUDA(up(ctx, ctx->raw_off.p, raw_off.data(), (n_seg + 1) * sizeof(int64_t)));
+  PP_CUDA(up(ctx, ctx->cand_off.p, cand_off.data(), (n_seg + 1) * sizeof(int64_t)));
   if (bm_off[n_seg] > 0) PP_CUDA(cudaMemsetAsync(ctx->bitmap.p, 0, bm_off[n_seg] * sizeof(unsigned int), st));
   PP_CUDA(cudaMemsetAsync(ctx->raw_cnt.p, 0, n_seg * sizeof(unsigned long long), st));
   PP_CUDA(cudaMemsetAsync(ctx->raw_in_tmp.p, 0, n_seg * sizeof(int), st));
@@ -1163,9 +1232,10 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   if (single) {
     std::vector<double> infs(cand_off[n_seg], INFINITY);
     std::vector<int> ones(n_seg, 1);
-    PP_CUDA(cudaMemcpyAsync(ctx->cand.p, infs.data(), infs.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-    PP_CUDA(cudaMemcpyAsync(ctx->cand_n.p, ones.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
+    PP_CUDA(up(ctx, ctx->cand.p, infs.data(), infs.size() * sizeof(double)));
+    PP_CUDA(up(ctx, ctx->cand_n.p, ones.data(), n_seg * sizeof(int)));
     PP_CUDA(cudaStreamSynchronize(st));  // host vectors die here
+    trace_mark("dp setup sync");
   } else {
     PP_TIMED(6, launch_cand_bitmap(ctx->bitmap.as<unsigned int>(), ctx->bitmap_off.as<int64_t>(),
                                    ctx->stats_d.as<SegStats>(), ctx->seg_mode.as<int>(), n_seg,
@@ -1221,8 +1291,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
       PP_CUDA(ctx->bound_items.ensure(bi.size() * sizeof(WorkItem)));
       PP_CUDA(ctx->gstate.ensure(std::max<int64_t>(goff, 1) * sizeof(double)));
       PP_CUDA(ctx->next_buf.ensure(std::max<int64_t>(total, 1) * sizeof(int)));
-      PP_CUDA(cudaMemcpyAsync(ctx->bound_items.p, bi.data(), bi.size() * sizeof(WorkItem),
-                              cudaMemcpyHostToDevice, st));
+      PP_CUDA(up(ctx, ctx->bound_items.p, bi.data(), bi.size() * sizeof(WorkItem)));
       const bool coop = use_coop(ctx, bi, c.h_seg_off);
       // (pass B recorded the largest singleton time per segment, SegStats::tsingle)
       const int bmode = std::isfinite(ctx->trunc_margin) && !table ? 2 : 1;
@@ -1245,6 +1314,7 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                                    dp_gbase(ctx), st));
       }
       PP_CUDA(cudaStreamSynchronize(st));  // bi dies here
+      trace_mark("wave sync");
     }
   }
   PP_TIMED(7, launch_seg_init(ctx->bound_res.as<ItemResult>(), single ? 0 : fused ? 2 : 1, c.opts.replica_count,
@@ -1265,8 +1335,9 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
   std::vector<WorkItem> items;
   std::vector<int> item_start(n_seg), item_cnt(n_seg);
   for (;;) {
-    PP_CUDA(cudaMemcpyAsync(ctx->h_segdp.p, ctx->segdp.p, n_seg * sizeof(SegDP), cudaMemcpyDeviceToHost, st));
+    PP_CUDA(down(ctx, ctx->h_segdp.p, ctx->segdp.p, n_seg * sizeof(SegDP)));
     PP_CUDA(cudaStreamSynchronize(st));
+    trace_mark("wave end sync");
     const SegDP* hd = ctx->h_segdp.as<SegDP>();
     items.clear();
     int64_t noff = 0, goff = 0;
@@ -1302,9 +1373,9 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
     PP_CUDA(ctx->gstate.ensure(std::max<int64_t>(goff, 1) * sizeof(double)));
     PP_CUDA(ctx->seg_item_start.ensure(n_seg * sizeof(int)));
     PP_CUDA(ctx->seg_item_cnt.ensure(n_seg * sizeof(int)));
-    PP_CUDA(cudaMemcpyAsync(ctx->items.p, items.data(), ni * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
-    PP_CUDA(cudaMemcpyAsync(ctx->seg_item_start.p, item_start.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
-    PP_CUDA(cudaMemcpyAsync(ctx->seg_item_cnt.p, item_cnt.data(), n_seg * sizeof(int), cudaMemcpyHostToDevice, st));
+    PP_CUDA(up(ctx, ctx->items.p, items.data(), ni * sizeof(WorkItem)));
+    PP_CUDA(up(ctx, ctx->seg_item_start.p, item_start.data(), n_seg * sizeof(int)));
+    PP_CUDA(up(ctx, ctx->seg_item_cnt.p, item_cnt.data(), n_seg * sizeof(int)));
     if (fused) {
       // the bound pass and the first wave in one band stream (MODE 3): the
       // candidate results per item, the bounds per segment
@@ -1352,9 +1423,13 @@ int run_plan(pp_ctx* ctx, const PlanCall& c) {
                               c.d_count, c.d_tmax, c.d_obj, c.d_status, c.d_err,
                               dp_price(ctx), dp_lay(ctx), st));
   unsigned long long dp_cols = 0;
-  if (counted)
-    PP_CUDA(cudaMemcpyAsync(&dp_cols, ctx->dp_cols.p, sizeof(dp_cols), cudaMemcpyDeviceToHost, st));
+  if (counted) {
+    PP_CUDA(ctx->h_word.ensure(sizeof(dp_cols)));
+    PP_CUDA(down(ctx, ctx->h_word.p, ctx->dp_cols.p, sizeof(dp_cols)));
+  }
   PP_CUDA(cudaStreamSynchronize(st));
+  trace_mark("run_plan end sync");
+  if (counted) dp_cols = *ctx->h_word.as<unsigned long long>();
   PP_CUDA(cudaGetLastError());
   transitions += (int64_t)dp_cols * kRB;
 
@@ -1562,6 +1637,11 @@ int pp_ctx_destroy(pp_ctx* ctx) {
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->ostream) {
+    cudaStreamSynchronize(ctx->ostream);
+    cudaStreamDestroy(ctx->ostream);
+  }
+  for (cudaEvent_t e : ctx->piece_ev) cudaEventDestroy(e);
   if (ctx->cstream) {
     cudaStreamSynchronize(ctx->cstream);
     cudaStreamDestroy(ctx->cstream);
@@ -1572,7 +1652,8 @@ int pp_ctx_destroy(pp_ctx* ctx) {
     h.hoff.release();
   }
   for (DevBuf* b : ctx->all_bufs()) b->release();
-  for (PinBuf* b : {&ctx->h_range, &ctx->h_stats, &ctx->h_segdp, &ctx->h_gt_total}) b->release();
+  for (PinBuf* b : {&ctx->h_range, &ctx->h_stats, &ctx->h_segdp, &ctx->h_gt_total, &ctx->arena.buf, &ctx->h_word})
+    b->release();
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->kev) cudaEventDestroy(e);
@@ -1739,10 +1820,37 @@ int plan_host(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets,
 // outputs are reused only after their device->host copy completed).
 // `claim` hands out chunk indices (-1: none left); chunk q covers segments
 // [cut[q], cut[q + 1]).
+// PP_E2E_TRACE=1: host timestamps of the host-buffer pipeline's phases,
+// printed to stderr per call (development aid; no effect otherwise).
+struct E2eTrace {
+  bool on = std::getenv("PP_E2E_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(int worker, int chunk, const char* what) const {
+    if (!on) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "e2e %9.1f us  w%d c%d %s\n", us, worker, chunk, what);
+  }
+};
+
+// Large host<->device copies of the host-buffer pipeline go out in pieces of
+// at most 4 MB, so the planning calls' small staging copies and read-backs on
+// the other streams interleave with them in the copy engines instead of
+// queueing behind tens of MB.
+cudaError_t copy_pieces(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+  constexpr size_t kPiece = (size_t)4 << 20;
+  for (size_t o = 0; o < bytes; o += kPiece) {
+    const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                                          std::min(kPiece, bytes - o), kind, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 template <class Claim, class Done>
 int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_offsets, const int* cut,
                      int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
-                     const pp_dp_options* opts, const pp_plan_out* out, Claim claim, Done done) {
+                     const pp_dp_options* opts, const pp_plan_out* out, Claim claim, Done done,
+                     const E2eTrace& tr, int wid) {
   pp_ctx* ctx = sub;  // (PP_CUDA reports on ctx)
   if (!sub->cstream) PP_CUDA(cudaStreamCreateWithFlags(&sub->cstream, cudaStreamNonBlocking));
   for (HostSet& h : sub->hset) {
@@ -1760,7 +1868,7 @@ int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_o
     for (int s = s0; s <= s1; ++s) ho[s - s0] = seg_offsets[s] - base;
     PP_CUDA(h.samples.ensure(std::max<int64_t>(n, 1) * sizeof(pp_sample)));
     PP_CUDA(h.seg.ensure((ns + 1) * sizeof(int64_t)));
-    if (n > 0) PP_CUDA(cudaMemcpyAsync(h.samples.p, samples + base, n * sizeof(pp_sample), cudaMemcpyHostToDevice, cs));
+    if (n > 0) PP_CUDA(copy_pieces(h.samples.p, samples + base, n * sizeof(pp_sample), cudaMemcpyHostToDevice, cs));
     PP_CUDA(cudaMemcpyAsync(h.seg.p, ho, (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, cs));
     PP_CUDA(cudaEventRecord(h.h2d, cs));
     return PP_OK;
@@ -1768,11 +1876,13 @@ int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_o
   int rc = PP_OK;
   int q = claim(), set = 0;
   if (q >= 0 && (rc = stage(set, q))) return rc;
+  tr.mark(wid, q, "staged");
   while (q >= 0) {
     const int qn = claim();
     // prefetch the next chunk's inputs — after this chunk's arrived, so the
     // first chunks of all workers cross PCIe ahead of any prefetch
     PP_CUDA(cudaEventSynchronize(sub->hset[set].h2d));
+    tr.mark(wid, q, "h2d done");
     if (qn >= 0 && (rc = stage(set ^ 1, qn))) return rc;
     HostSet& h = sub->hset[set];
     const int s0 = cut[q], s1 = cut[q + 1], ns = s1 - s0;
@@ -1805,6 +1915,7 @@ int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_o
     d.err_sample_id = h.err.as<int64_t>();
     rc = pp_plan_grid_device(sub, h.samples.as<pp_sample>(), h.seg.as<int64_t>(), h.hoff.as<int64_t>(), ns,
                              presorted, grid, model, opts, &d);
+    tr.mark(wid, q, "planned");
     if (rc) {
       cudaStreamSynchronize(cs);  // no copy into the caller's buffers after the call
       return rc;
@@ -1813,7 +1924,7 @@ int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_o
     // drain this chunk's plans on the copy stream (the compute stream is idle:
     // the planning call synchronised it)
     auto d2h = [&](void* dst, const void* src, size_t bytes) {
-      return dst && bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs) : cudaSuccess;
+      return dst && bytes ? copy_pieces(dst, src, bytes, cudaMemcpyDeviceToHost, cs) : cudaSuccess;
     };
     PP_CUDA(d2h(out->ordered ? out->ordered + base : nullptr, d.ordered, n * sizeof(pp_sample)));
     PP_CUDA(d2h(out->order ? out->order + base : nullptr, d.order, n * sizeof(int32_t)));
@@ -1830,6 +1941,202 @@ int plan_host_chunks(pp_ctx* sub, const pp_sample* samples, const int64_t* seg_o
     set ^= 1;
   }
   PP_CUDA(cudaStreamSynchronize(cs));
+  tr.mark(wid, -1, "drained");
+  return PP_OK;
+}
+
+// Host buffers, cut into `parts` parts by sample count: every part's
+// samples go out at once, in part order, on one copy stream (one event per
+// part), and `workers` host threads (sub-contexts with their own stream and
+// scratch) plan parts w, w + workers, ... each as soon as its samples are in,
+// then send its plans back on the worker's own copy stream while the worker
+// plans its next part.  What stays exposed is the first part's upload and
+// the last parts' download.  All small transfers inside a planning call are
+// copy kernels through mapped pinned memory (small_copy), so they never wait
+// behind these bulk copies in the copy engines.
+int plan_host_pieces(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets, int32_t n_seg,
+                     int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
+                     const pp_dp_options* opts, const pp_plan_out* out, int parts, int workers) {
+  parts = std::max(1, std::min(parts, (int)n_seg));
+  workers = std::max(1, std::min(workers, parts));
+  const int64_t total = seg_offsets[n_seg];
+  std::vector<int> cut(parts + 1, 0);
+  cut[parts] = n_seg;
+  for (int p = 1; p < parts; ++p) {
+    const int64_t target = total * p / parts;
+    int s = cut[p - 1] + 1;
+    while (s < n_seg - (parts - p) && seg_offsets[s] < target) ++s;
+    cut[p] = s;
+  }
+  while ((int)ctx->subs.size() < workers) {
+    pp_ctx* sub = nullptr;
+    const int rc = pp_ctx_create(ctx->device, &sub);
+    if (rc != PP_OK) return fail(ctx, rc, "cannot create a sub-context");
+    ctx->subs.push_back(sub);
+  }
+  if (!ctx->cstream) PP_CUDA(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+  while ((int)ctx->piece_ev.size() < parts) {
+    cudaEvent_t e;
+    PP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->piece_ev.push_back(e);
+  }
+  const size_t nn = (size_t)std::max<int64_t>(total, 1);
+  PP_CUDA(ctx->samples.ensure(nn * sizeof(pp_sample)));
+  PP_CUDA(ctx->ordered.ensure(nn * sizeof(pp_sample)));
+  PP_CUDA(ctx->seg_off.ensure((n_seg + parts) * sizeof(int64_t)));
+  PP_CUDA(ctx->piece_off.ensure((n_seg + parts) * sizeof(int64_t)));
+  PP_CUDA(ctx->out_splits.ensure(nn * sizeof(int32_t)));
+  PP_CUDA(ctx->out_times.ensure(nn * sizeof(double)));
+  PP_CUDA(ctx->out_count.ensure(n_seg * sizeof(int32_t)));
+  PP_CUDA(ctx->out_tmax.ensure(n_seg * sizeof(double)));
+  PP_CUDA(ctx->out_obj.ensure(n_seg * sizeof(double)));
+  PP_CUDA(ctx->out_status.ensure(n_seg * sizeof(int32_t)));
+  PP_CUDA(ctx->out_err.ensure(n_seg * sizeof(int64_t)));
+  if (out->order) PP_CUDA(ctx->perm.ensure(nn * sizeof(int32_t)));
+  // part-relative segment offsets, part p at [cut[p] + p, cut[p + 1] + p]
+  int64_t* ho = ctx->piece_off.as<int64_t>();
+  for (int p = 0; p < parts; ++p)
+    for (int s = cut[p]; s <= cut[p + 1]; ++s) ho[s + p] = seg_offsets[s] - seg_offsets[cut[p]];
+  cudaStream_t ci = ctx->cstream;
+  for (int p = 0; p < parts; ++p) {
+    const int64_t base = seg_offsets[cut[p]], n = seg_offsets[cut[p + 1]] - base;
+    PP_CUDA(cudaMemcpyAsync(ctx->seg_off.as<int64_t>() + cut[p] + p, ho + cut[p] + p,
+                            (cut[p + 1] - cut[p] + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ci));
+    if (n > 0)
+      PP_CUDA(copy_pieces(ctx->samples.as<pp_sample>() + base, samples + base, n * sizeof(pp_sample),
+                          cudaMemcpyHostToDevice, ci));
+    PP_CUDA(cudaEventRecord(ctx->piece_ev[p], ci));
+  }
+  const E2eTrace tr;
+  std::vector<int> rcs(workers, PP_OK);
+  std::vector<pp_stats> acc(workers);
+  std::vector<std::thread> th;
+  for (int w = 0; w < workers; ++w) {
+    th.emplace_back([&, w]() {
+      pp_ctx* sub = ctx->subs[w];
+      cudaSetDevice(sub->device);
+      sub->tuning = ctx->tuning;
+      sub->tuning.streams = 1;
+      pp_stats S{};
+      S.exit_thresh = INFINITY;
+      int rc = PP_OK;
+      auto cu = [&](cudaError_t e) {
+        if (e != cudaSuccess && rc == PP_OK) {
+          sub->err = cudaGetErrorString(e);
+          rc = PP_ERR_CUDA;
+        }
+      };
+      if (!sub->ostream) cu(cudaStreamCreateWithFlags(&sub->ostream, cudaStreamNonBlocking));
+      while (rc == PP_OK && (int)sub->piece_ev.size() < 1) {
+        cudaEvent_t e;
+        cu(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        sub->piece_ev.push_back(e);
+      }
+      for (int p = w; p < parts && rc == PP_OK; p += workers) {
+        const int s0 = cut[p], s1 = cut[p + 1];
+        const int64_t base = seg_offsets[s0], n = seg_offsets[s1] - base;
+        cu(cudaStreamWaitEvent(sub->stream, ctx->piece_ev[p], 0));
+        if (tr.on) {
+          cudaEventSynchronize(ctx->piece_ev[p]);
+          tr.mark(w, p, "in");
+        }
+        PlanCall c;
+        c.d_samples = ctx->samples.as<pp_sample>() + base;
+        c.d_seg_off = ctx->seg_off.as<int64_t>() + s0 + p;
+        c.h_seg_off = ho + s0 + p;
+        c.n_seg = s1 - s0;
+        c.presorted = presorted;
+        c.grid = grid;
+        c.model = model;
+        c.opts = *opts;
+        c.d_ordered = ctx->ordered.as<pp_sample>() + base;
+        c.d_order = out->order ? ctx->perm.as<int32_t>() + base : nullptr;
+        c.d_splits = ctx->out_splits.as<int32_t>() + base;
+        c.d_times = ctx->out_times.as<double>() + base;
+        c.d_count = ctx->out_count.as<int32_t>() + s0;
+        c.d_tmax = ctx->out_tmax.as<double>() + s0;
+        c.d_obj = ctx->out_obj.as<double>() + s0;
+        c.d_status = ctx->out_status.as<int32_t>() + s0;
+        c.d_err = ctx->out_err.as<int64_t>() + s0;
+        if (rc == PP_OK) rc = run_plan(sub, c);
+        tr.mark(w, p, "planned");
+        if (rc != PP_OK) break;
+        const pp_stats& t = sub->stats;
+        S.candidates_generated += t.candidates_generated;
+        S.candidates_ref_evaluated += t.candidates_ref_evaluated;
+        S.candidates_evaluated += t.candidates_evaluated;
+        S.transitions_executed += t.transitions_executed;
+        S.transitions_reference += t.transitions_reference;
+        S.slices_costed += t.slices_costed;
+        S.waves = std::max(S.waves, t.waves);
+        S.ms_sort += t.ms_sort;
+        S.ms_cost += t.ms_cost;
+        S.ms_dp += t.ms_dp;
+        S.ms_total += t.ms_total;
+        for (int q = 0; q < 8; ++q) {
+          S.ms_kernel[q] += t.ms_kernel[q];
+          S.launches[q] += t.launches[q];
+        }
+        S.dp_band_bytes += t.dp_band_bytes;
+        S.slices_pass_a += t.slices_pass_a;
+        S.slices_pass_b += t.slices_pass_b;
+        S.band_bytes += t.band_bytes;
+        S.bound_transitions += t.bound_transitions;
+        S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
+        // this part's plans back to the caller while the worker plans its next part
+        cudaStream_t co = sub->ostream;
+        cu(cudaEventRecord(sub->piece_ev[0], sub->stream));
+        cu(cudaStreamWaitEvent(co, sub->piece_ev[0], 0));
+        auto d2h = [&](void* dst, const void* src, size_t bytes) {
+          if (dst && bytes) cu(copy_pieces(dst, src, bytes, cudaMemcpyDeviceToHost, co));
+        };
+        d2h(out->ordered ? out->ordered + base : nullptr, c.d_ordered, n * sizeof(pp_sample));
+        d2h(out->order ? out->order + base : nullptr, c.d_order, n * sizeof(int32_t));
+        d2h(out->splits ? out->splits + base : nullptr, c.d_splits, n * sizeof(int32_t));
+        d2h(out->mb_times ? out->mb_times + base : nullptr, c.d_times, n * sizeof(double));
+        d2h(out->count ? out->count + s0 : nullptr, c.d_count, (s1 - s0) * sizeof(int32_t));
+        d2h(out->t_max_used ? out->t_max_used + s0 : nullptr, c.d_tmax, (s1 - s0) * sizeof(double));
+        d2h(out->objective ? out->objective + s0 : nullptr, c.d_obj, (s1 - s0) * sizeof(double));
+        d2h(out->status ? out->status + s0 : nullptr, c.d_status, (s1 - s0) * sizeof(int32_t));
+        d2h(out->err_sample_id ? out->err_sample_id + s0 : nullptr, c.d_err, (s1 - s0) * sizeof(int64_t));
+      }
+      // no copy into the caller's buffers after the call, failed or not
+      if (sub->ostream) cudaStreamSynchronize(sub->ostream);
+      tr.mark(w, -1, "drained");
+      rcs[w] = rc;
+      acc[w] = S;
+    });
+  }
+  for (auto& t : th) t.join();
+  cudaStreamSynchronize(ci);
+  pp_stats S{};
+  S.exit_thresh = INFINITY;
+  for (int w = 0; w < workers; ++w) {
+    if (rcs[w] != PP_OK) return fail(ctx, rcs[w], ctx->subs[w]->err);
+    const pp_stats& t = acc[w];
+    S.candidates_generated += t.candidates_generated;
+    S.candidates_ref_evaluated += t.candidates_ref_evaluated;
+    S.candidates_evaluated += t.candidates_evaluated;
+    S.transitions_executed += t.transitions_executed;
+    S.transitions_reference += t.transitions_reference;
+    S.slices_costed += t.slices_costed;
+    S.waves = std::max(S.waves, t.waves);
+    S.ms_sort = std::max(S.ms_sort, t.ms_sort);
+    S.ms_cost = std::max(S.ms_cost, t.ms_cost);
+    S.ms_dp = std::max(S.ms_dp, t.ms_dp);
+    S.ms_total = std::max(S.ms_total, t.ms_total);
+    for (int q = 0; q < 8; ++q) {
+      S.ms_kernel[q] += t.ms_kernel[q];
+      S.launches[q] += t.launches[q];
+    }
+    S.dp_band_bytes += t.dp_band_bytes;
+    S.slices_pass_a += t.slices_pass_a;
+    S.slices_pass_b += t.slices_pass_b;
+    S.band_bytes += t.band_bytes;
+    S.bound_transitions += t.bound_transitions;
+    S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
+  }
+  ctx->stats = S;
   return PP_OK;
 }
 
@@ -1839,7 +2146,7 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
   workers = std::min(workers, (int)n_seg);
   // >= two chunks per worker: one is planned while the next one's inputs and
   // the previous one's plans cross PCIe (plan_host_chunks)
-  const int per_worker = ctx->tuning.host_chunks >= 1 ? ctx->tuning.host_chunks : 2;
+  const int per_worker = -ctx->tuning.host_chunks >= 1 ? -ctx->tuning.host_chunks : 2;
   std::vector<int> wts(std::min<int>(n_seg, per_worker * workers), 1);
   const int chunks = (int)wts.size();
   while ((int)ctx->subs.size() < workers) {
@@ -1860,10 +2167,10 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
     while (s < n_seg - (chunks - p) && seg_offsets[s] < target) ++s;
     cut[p] = s;
   }
-  std::atomic<int> next{0};
   std::vector<int> rcs(workers, PP_OK);
   std::vector<pp_stats> acc(workers);
   std::vector<std::thread> th;
+  const E2eTrace tr;
   for (int w = 0; w < workers; ++w) {
     th.emplace_back([&, w]() {
       pp_ctx* sub = ctx->subs[w];
@@ -1872,8 +2179,14 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
       sub->tuning.streams = 1;
       pp_stats S{};
       S.exit_thresh = INFINITY;
+      // chunks w, w + workers, w + 2 workers, ... (static round robin: a
+      // worker claims its next chunk early, to prefetch its inputs, so a
+      // shared queue would let the first workers take chunks an idle worker
+      // could have started on)
+      int mine = w;
       auto claim = [&]() {
-        const int k = next++;
+        const int k = mine;
+        mine += workers;
         return k < chunks ? k : -1;
       };
       auto done = [&](int) {
@@ -1901,7 +2214,7 @@ int plan_host_split(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_of
         S.exit_thresh = std::min(S.exit_thresh, t.exit_thresh);
       };
       rcs[w] = plan_host_chunks(sub, samples, seg_offsets, cut.data(), presorted, grid, model, opts, out,
-                                claim, done);
+                                claim, done, tr, w);
       acc[w] = S;
     });
   }
@@ -1952,9 +2265,16 @@ int pp_plan_grid(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offse
   if (seg_offsets[0] != 0) return fail(ctx, PP_ERR_INVALID, "seg_offsets[0] must be 0");
   for (int s = 0; s < n_seg; ++s)
     if (seg_offsets[s + 1] < seg_offsets[s]) return fail(ctx, PP_ERR_INVALID, "seg_offsets must be non-decreasing");
-  if (ctx->tuning.streams > 1 && n_seg > 1)
-    return plan_host_split(ctx, samples, seg_offsets, n_seg, presorted, grid, model, opts, out,
-                           ctx->tuning.streams);
+  if (ctx->tuning.streams > 1 && n_seg > 1) {
+    if (ctx->tuning.host_chunks < 0)  // the concurrent-worker pipeline (A/B)
+      return plan_host_split(ctx, samples, seg_offsets, n_seg, presorted, grid, model, opts, out,
+                             ctx->tuning.streams);
+    // parts: host_chunks per worker (default 1: smaller parts plan less
+    // efficiently than the upload they hide, profiles/r02/e2e), workers: streams
+    const int per = ctx->tuning.host_chunks > 0 ? ctx->tuning.host_chunks : 1;
+    return plan_host_pieces(ctx, samples, seg_offsets, n_seg, presorted, grid, model, opts, out,
+                            per * ctx->tuning.streams, ctx->tuning.streams);
+  }
   return plan_host(ctx, samples, seg_offsets, n_seg, presorted, grid, model, opts, out);
 }
 

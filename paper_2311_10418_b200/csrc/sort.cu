@@ -36,6 +36,13 @@ struct FieldRange {
   long long mx[3];
 };
 
+__global__ void range_init_kernel(unsigned long long* r) {
+  if (threadIdx.x < 7) r[threadIdx.x] = threadIdx.x < 3 ? ~0ULL : 0ULL;
+}
+__global__ void range_out_kernel(const unsigned long long* r, unsigned long long* h) {
+  if (threadIdx.x < 7) h[threadIdx.x] = r[threadIdx.x];
+}
+
 __global__ void field_range_kernel(const pp_sample* __restrict__ s, int64_t n,
                                    unsigned long long* out /* 6 words, biased; [6]: ids unordered */) {
   long long mn[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
@@ -382,11 +389,12 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
   // Field ranges of the call: they size the sort key and feed the host's
   // monotonicity certificate for the cost passes (capi.cu), so they are
   // computed for presorted calls too.
-  const unsigned long long init[7] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL, 0ULL};
-  cudaMemcpyAsync(d_range, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  // (initialised and read back by one-thread kernels, h_range being pinned:
+  // no copy-engine transfer on the planning stream, capi.cu small_copy)
+  range_init_kernel<<<1, 32, 0, st>>>(d_range);
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
   field_range_kernel<<<blocks, 256, 0, st>>>(d_in, total, d_range);
-  cudaMemcpyAsync(h_range, d_range, sizeof(init), cudaMemcpyDeviceToHost, st);  // 7 words
+  range_out_kernel<<<1, 32, 0, st>>>(d_range, h_range);  // 7 words
   if (presorted) {
     const int cb = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     copy_soa_kernel<<<cb, 256, 0, st>>>(d_in, total, d_out, d_in_len, d_tgt_len);
