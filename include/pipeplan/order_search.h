@@ -44,7 +44,7 @@ struct InjectionOrder {
 /// std::invalid_argument (schedule.cpp:281-284, 62-66) or std::logic_error
 /// (schedule.cpp:81-82, 155-156) for the first failing table, like a loop
 /// over the reference would.  Device limits (std::invalid_argument where
-/// the reference would return an order): stages <= 32, n_clusters <= 8, and
+/// the reference would return an order): stages <= 32, n_clusters <= 12, and
 /// op durations >= 0 and not NaN (the Start lists are merged from per-device
 /// sorted op ends).
 std::vector<InjectionOrder> search_injection_orders(std::span<const OpCostTable> tables,

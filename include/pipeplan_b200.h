@@ -320,7 +320,8 @@ int pp_select_recomputation_device(pp_ctx* ctx, const pp_sample* d_ordered, cons
  * [s][stage][5] = busy, idle, blocked, peak_mem, final_mem: DeviceStats,
  * simulate.h:30-36), status (PP_ERR_INVALID: no micro-batch or a negative /
  * NaN duration; PP_ERR_NOT_CONVERGED / PP_ERR_NOT_EXECUTABLE: the
- * reference's logic_errors).  Device limits: n_stages <= 32, n_clusters <= 8.
+ * reference's logic_errors).  Device limits: n_stages <= 32, n_clusters <= 12 (permutations beyond 8 clusters are
+ * evaluated in windows folded into a running best).
  * Host buffers. */
 int pp_order_search(pp_ctx* ctx, const double* t_f, const double* t_b, const double* act_mem,
                     const int64_t* mb_offset, int32_t n_seg, int32_t n_stages, const double* limits,

@@ -36,6 +36,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "pp_internal.cuh"
 
 namespace ppb {
@@ -123,6 +125,7 @@ size_t dp_coop_parts_bytes(int grid);
 size_t order_search_slot_bytes(int64_t max_m, int C);
 int order_search_warps(int64_t n_items, int C, size_t slot_bytes, size_t budget);
 size_t order_search_item_bytes();
+size_t order_search_best_bytes();
 size_t ingest_scratch_bytes(int64_t n_bytes);
 cudaError_t launch_load_records(const unsigned char* d_bytes, int64_t n, long long max_seq_len, char* scratch,
                                 size_t scratch_bytes, pp_sample* d_out, int64_t capacity, int64_t* n_records,
@@ -147,7 +150,7 @@ cudaError_t launch_order_search(const double* tf, const double* tb, const double
                                 int* assign, int* cl_idx, int* cl_off, int* cl_k, char* scratch,
                                 size_t slot_bytes, int warps, void* items, double* item_stats,
                                 int* order, double* makespan, double* bubble, int* deadlock,
-                                double* dev_stats, int* status, cudaStream_t st);
+                                double* dev_stats, int* status, int rwin, void* best, double* best_stats, cudaStream_t st);
 int dp_coop_grid(int device);
 cudaError_t launch_pack_slots(const int32_t* count, const int32_t* status, const double* tmax,
                               const double* obj, const int32_t* splits, const int32_t* order,
@@ -301,7 +304,7 @@ struct pp_ctx {
       colbase, chunk_nv, perm;
   // injection-order search (sched.cu)
   DevBuf os_tf, os_tb, os_act, os_off, os_lim, os_pred, os_assign, os_idx, os_cloff, os_clk, os_scratch,
-      os_items, os_istats, os_order, os_ms, os_bub, os_dl, os_ds, os_status;
+      os_items, os_istats, os_order, os_ms, os_bub, os_dl, os_ds, os_status, os_best, os_bstats;
   // dataset ingest (ingest.cu)
   DevBuf ing_bytes, ing_scratch, ing_out, ing_off;
   // padding report (report.cu)
@@ -352,7 +355,7 @@ struct pp_ctx {
             &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act,
             &cmin, &dp_cols, &colbase, &chunk_nv, &perm, &gt_need, &gt_off, &gt_total, &gt_G, &gt_base, &gt_rf, &gt_rlo, &rc_tab, &rc_lim, &rc_out,
             &os_tf, &os_tb, &os_act, &os_off, &os_lim, &os_pred, &os_assign, &os_idx, &os_cloff, &os_clk,
-            &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status,
+            &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status, &os_best, &os_bstats,
             &ing_bytes, &ing_scratch, &ing_out, &ing_off,
             &rp_samples, &rp_trunc, &rp_off, &rp_ordered, &rp_splits, &rp_times, &rp_count, &rp_tmax, &rp_obj,
             &rp_status, &rp_err, &rp_tf, &rp_tb, &rp_act, &rp_mboff, &rp_st6, &rp_bins, &rp_naive, &rp_items,
@@ -392,8 +395,22 @@ cudaError_t timed_begin(pp_ctx* ctx, int cat) {
 }
 cudaError_t timed_end(pp_ctx* ctx) { return cudaEventRecord(ctx->kev[ctx->kused++], ctx->stream); }
 
+// NVTX ranges (header-only NVTX v3: free without a profiler attached): one
+// per planning call / part / run_plan phase, and one per kernel launch named
+// by its pp_stats category, so an Nsight Systems timeline shows the phases.
+const char* const kNvtxCat[8] = {"pp sort", "pp cost setup", "pp cost pass A", "pp slice table / pass B",
+                                 "pp DP bound (+first candidate)", "pp DP candidates", "pp candidate compaction",
+                                 "pp selection / assembly"};
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 #define PP_TIMED(cat, x)            \
   do {                              \
+    NvtxRange nvtx_(kNvtxCat[cat]); \
     PP_CUDA(timed_begin(ctx, cat)); \
     PP_CUDA(x);                     \
     PP_CUDA(timed_end(ctx));        \
@@ -1099,6 +1116,7 @@ const int* dp_gbase(const pp_ctx* ctx) { return ctx->gtab ? ctx->gt_base.as<int>
 
 // The planning pipeline (steps 1-7 above).
 int run_plan(pp_ctx* ctx, const PlanCall& c) {
+  NvtxRange nvtx("pp run_plan");
   ctx->arena.off = 0;  // (the previous call ended with its stream synchronised)
   cudaStream_t st = ctx->stream;
   const int n_seg = c.n_seg;
@@ -1719,6 +1737,7 @@ int pp_plan_grid_device(pp_ctx* ctx, const pp_sample* d_samples, const int64_t* 
                         const int64_t* h_seg_offsets, int32_t n_seg, int32_t presorted,
                         const pp_grid_desc* grid, const pp_model_desc* model,
                         const pp_dp_options* opts, pp_plan_out* d_out) {
+  NvtxRange nvtx("pp_plan_grid_device");
   int rc = check_ctx(ctx);
   if (rc) return rc;
   if (!opts || !d_out || n_seg < 1 || !h_seg_offsets || !d_seg_offsets)
@@ -2058,7 +2077,10 @@ int plan_host_pieces(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_o
         c.d_obj = ctx->out_obj.as<double>() + s0;
         c.d_status = ctx->out_status.as<int32_t>() + s0;
         c.d_err = ctx->out_err.as<int64_t>() + s0;
-        if (rc == PP_OK) rc = run_plan(sub, c);
+        if (rc == PP_OK) {
+          NvtxRange nvtx("pp host part");
+          rc = run_plan(sub, c);
+        }
         tr.mark(w, p, "planned");
         if (rc != PP_OK) break;
         const pp_stats& t = sub->stats;
@@ -2257,6 +2279,7 @@ extern "C" {
 int pp_plan_grid(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offsets, int32_t n_seg,
                  int32_t presorted, const pp_grid_desc* grid, const pp_model_desc* model,
                  const pp_dp_options* opts, pp_plan_out* out) {
+  NvtxRange nvtx("pp_plan_grid");
   int rc = check_ctx(ctx);
   if (rc) return rc;
   if (!samples || !seg_offsets || n_seg < 1 || !opts || !out)
@@ -2629,7 +2652,13 @@ int order_search_run(pp_ctx* ctx, const double* d_tf, const double* d_tb, const 
   int kfact = 1;
   for (int q = 2; q <= k; ++q) kfact *= q;
   const int64_t n_mb = h_off[n_seg] - h_off[0];
-  const int64_t n_items = (int64_t)n_seg * kfact;
+  // permutations per launch: all of them, or windows of at most ~4 M
+  // (table, permutation) evaluations whose results fold into a running best
+  constexpr int64_t kWindowItems = (int64_t)1 << 22;
+  const int rwin = (int64_t)n_seg * kfact <= kWindowItems
+                       ? kfact
+                       : (int)std::max<int64_t>(1, kWindowItems / std::max<int32_t>(n_seg, 1));
+  const int64_t n_items = (int64_t)n_seg * rwin;
   const size_t slot = order_search_slot_bytes(max_m, C);
   // scratch budget: half the free memory, at most 32 GB (one slot per
   // resident (mini-batch, permutation) evaluation; L2-resident when small)
@@ -2648,6 +2677,10 @@ int order_search_run(pp_ctx* ctx, const double* d_tf, const double* d_tb, const 
   PP_CUDA(ctx->os_scratch.ensure((size_t)warps * (32 / G) * slot));
   PP_CUDA(ctx->os_items.ensure(n_items * order_search_item_bytes()));
   PP_CUDA(ctx->os_istats.ensure(n_items * 5 * C * sizeof(double)));
+  if (rwin < kfact) {
+    PP_CUDA(ctx->os_best.ensure((size_t)n_seg * order_search_best_bytes()));
+    PP_CUDA(ctx->os_bstats.ensure((size_t)n_seg * 5 * C * sizeof(double)));
+  }
   PP_CUDA(cudaMemcpyAsync(ctx->os_lim.p, limits, C * sizeof(double), cudaMemcpyHostToDevice, st));
   PP_CUDA(cudaMemcpyAsync(d_status, stat.data(), n_seg * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   // tables with no micro-batch are skipped by the kernels (cl_k = 0)
@@ -2658,7 +2691,7 @@ int order_search_run(pp_ctx* ctx, const double* d_tf, const double* d_tb, const 
                               ctx->os_idx.as<int>(), ctx->os_cloff.as<int>(), ctx->os_clk.as<int>(),
                               ctx->os_scratch.as<char>(), slot, warps, ctx->os_items.p,
                               d_ds ? ctx->os_istats.as<double>() : nullptr, d_order, d_ms, d_bub, d_dl, d_ds,
-                              d_status, st));
+                              d_status, rwin, ctx->os_best.p, d_ds ? ctx->os_bstats.as<double>() : nullptr, st));
   PP_CUDA(cudaStreamSynchronize(st));  // stat / limits die here
   return PP_OK;
 }
@@ -2668,7 +2701,7 @@ int order_search_check(pp_ctx* ctx, const int64_t* h_off, int32_t n_seg, int32_t
   if (n_seg < 0 || (n_seg > 0 && (!h_off || !limits))) return fail(ctx, PP_ERR_INVALID, "bad arguments");
   if (C < 1 || C > 32) return fail(ctx, PP_ERR_INVALID, "the device order search supports 1..32 stages");
   if (k < 1) return fail(ctx, PP_ERR_INVALID, "n_clusters must be >= 1");  // schedule.cpp:284
-  if (k > 8) return fail(ctx, PP_ERR_INVALID, "the device order search supports n_clusters <= 8");
+  if (k > 12) return fail(ctx, PP_ERR_INVALID, "the device order search supports n_clusters <= 12");
   for (int s = 0; s < n_seg; ++s)
     if (h_off[s + 1] < h_off[s]) return fail(ctx, PP_ERR_INVALID, "mb_offset must be non-decreasing");
   return PP_OK;

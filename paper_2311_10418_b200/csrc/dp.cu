@@ -68,6 +68,14 @@ constexpr int kSyncThreads = 32 * (1 + kWorkers);    // workers + chain (block b
 // it is the critical path and must never lose an issue slot to a worker.
 constexpr int kProducerWarp = kWorkers;      // warp 8
 constexpr int kChainWarp = kWorkers + 1;     // warp 9
+// Named barriers: 1 = block barrier (chain + workers), 2 = worker partials,
+// and on the slice-table path the unit hand-off between the producer and the
+// chain warp (64 threads): full[k] = 3 + k (producer arrives after its
+// stores, the chain syncs), empty[k] = 5 + k (the chain arrives after its
+// reads, the producer syncs before refilling buffer k).  Generic-proxy
+// stores ordered by bar.arrive / bar.sync: nothing for racecheck to flag,
+// unlike TMA writes ordered through an mbarrier (the band path).
+constexpr int kBarUnitFull = 3, kBarUnitEmpty = 5;
 
 #ifdef PP_DP_TRACE
 __device__ long long* g_dp_trace = nullptr;  // [block][16] clock64 stamps of CTA 0
@@ -233,7 +241,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   // ---- prologue
   if (threadIdx.x == 0) {
     for (int k = 0; k < 2; ++k) {
-      mbar_init(&unit_full[k], GTAB ? 32 : 1);  // GTAB: every producer lane arrives after its stores
+      mbar_init(&unit_full[k], 1);  // (band path; the slice-table path hands units over by named barriers)
       mbar_init(&unit_empty[k], 1);             // the chain warp releases a unit
     }
     for (int k = 0; k < kRing; ++k) {
@@ -312,7 +320,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           for (int q = 0; q < 8; ++q)
             if (c0 + q < cn) U[(kRB + c0 + q) * kRB + lane] = v[q];
         }
-        mbar_arrive(&unit_full[k]);  // (each lane, after its own stores)
+        named_bar_arrive(kBarUnitFull + k, 64);  // (the chain's named_bar completes it)
       } else {
         if (lane == 0) {
           mbar_expect_tx(&unit_full[k], (uint32_t)(ct + cn) * kColBytes);
@@ -323,6 +331,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         }
       }
     };
+    if (GTAB && nblk == 0) return;  // (no unit is ever consumed)
     load_unit(-1);
     if (nblk > 0) load_unit(0);
     int islot = 0, iround = 0;
@@ -332,7 +341,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       if (b + 1 >= nblk) break;
       // unit b+1 into the buffer of unit b-1, once the chain released it
       const int u = b + 1, k = (u + 1) & 1, f = (u + 1) >> 1;
-      mbar_wait(&unit_empty[k], (f - 1) & 1);
+      if (GTAB) named_bar(kBarUnitEmpty + k, 64);
+      else mbar_wait(&unit_empty[k], (f - 1) & 1);
       load_unit(u);
       // far-far chunks of block b+1 (the workers reduce them during block b)
       const int gn = gb0 + b + 1;
@@ -355,6 +365,10 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       }
     }
     if (lane == 0 && cols_streamed) atomicAdd(cols_streamed, (unsigned long long)ncols_total);
+    if (GTAB) {  // the releases of the last unit in each buffer (never refilled)
+      named_bar(kBarUnitEmpty + (nblk & 1), 64);
+      named_bar(kBarUnitEmpty + ((nblk - 1) & 1), 64);
+    }
     return;
   }
 
@@ -364,7 +378,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     Acc N = kIdent;  // this lane's row of the NEXT block: its near-far columns so far
     // block 0's near-far columns (unit -1: j = n, ...), from the stored states
     if (nblk > 0) {
-      mbar_wait(&unit_full[0], 0);
+      if (GTAB) named_bar(kBarUnitFull + 0, 64);
+      else mbar_wait(&unit_full[0], 0);
       const int nb0 = n - max(0, n - kRB);
       const int cnf = max(0, min(kRB, blk_W[gb0] - nb0));
       const double* U = unit;
@@ -375,7 +390,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
                          t);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&unit_empty[0]);
+      if (GTAB) named_bar_arrive(kBarUnitEmpty + 0, 64);
+      else if (lane == 0) mbar_arrive(&unit_empty[0]);
     }
     for (int b = 0; b < nblk; ++b) {
       PP_TRACE(0);
@@ -411,7 +427,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       }
       if (r >= nb) A = kIdent;
       N = kIdent;
-      mbar_wait(&unit_full[ub], ((b + 1) >> 1) & 1);
+      if (GTAB) named_bar(kBarUnitFull + ub, 64);
+      else mbar_wait(&unit_full[ub], ((b + 1) >> 1) & 1);
       PP_TRACE(1);
       PP_TRACE(2);
       // ---- the triangle.  Iteration k: every lane l <= k folds the slice
@@ -460,7 +477,8 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       // (__syncwarp + mbarrier arrive), and the producer's next write into the
       // buffer waits for it
       __syncwarp();
-      if (lane == 0) mbar_arrive(&unit_empty[ub]);
+      if (GTAB) named_bar_arrive(kBarUnitEmpty + ub, 64);
+      else if (lane == 0) mbar_arrive(&unit_empty[ub]);
       PP_TRACE(3);
       if (r < nb) {
         const int row = i0 + r;
@@ -484,6 +502,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         }
       }
       PP_TRACE(4);
+      __syncwarp();  // (reconverge: lanes >= nb skipped the stores)
       named_bar(1, kSyncThreads);  // chain + workers: block b's states and block b+1's partial
       PP_TRACE(5);
     }
@@ -614,6 +633,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
           wpc[o] = a0.c;
           wpj[o] = a0.j;
         }
+        __syncwarp();
         named_bar(2, 32 * kWorkers);
         if (w == 0) {  // fold the 8 worker partials for the chain: a pairwise tree
           Acc v[kWorkers];
@@ -639,6 +659,7 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         }
         if (w == 0) PP_TRACE(10);
       }
+      __syncwarp();
       named_bar(1, kSyncThreads);  // chain + workers: block b's states and block b+1's partial
     }
   }

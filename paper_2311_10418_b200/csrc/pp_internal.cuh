@@ -429,6 +429,11 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+// Producer side of a named-barrier hand-off (release; the consumer's
+// named_bar on the same id and count completes it).
+__device__ __forceinline__ void named_bar_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 // One DP pass: (mini-batch, t_max candidate).
 struct WorkItem {

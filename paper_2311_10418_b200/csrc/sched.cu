@@ -45,6 +45,11 @@
 
 namespace ppb {
 
+// Largest n_clusters the device search takes: 12! = 479,001,600 permutations
+// still index with int; beyond 8 clusters the permutations are evaluated in
+// windows whose results fold into a running best per table (order_merge_kernel).
+constexpr int kMaxClusters = 12;
+
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(256) cluster_kernel(
 
 // r-th permutation of 0..k-1 in lexicographic (std::next_permutation) order
 __device__ inline void nth_perm(int r, int k, int* perm) {
-  int pool[16];
+  int pool[kMaxClusters];
   for (int i = 0; i < k; ++i) pool[i] = i;
   for (int i = 0; i < k; ++i) {
     int f = 1;  // (k - 1 - i)!
@@ -299,9 +304,9 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
     const int64_t* __restrict__ mb_off, const double* __restrict__ limits, int C, int G, int k, int kfact,
     double comm_latency, int n_seg, const int* __restrict__ cl_idx, const int* __restrict__ cl_off,
     const int* __restrict__ cl_k, char* __restrict__ scratch, size_t slot_bytes, int64_t Mcap,
-    ItemOut* __restrict__ items, double* __restrict__ dev_stats) {
+    ItemOut* __restrict__ items, double* __restrict__ dev_stats, int r0, int rwin) {
   __shared__ int sqn_s[4][64], rqn_s[4][64];
-  __shared__ int perm_s[4][32][8];
+  __shared__ int perm_s[4][32][kMaxClusters];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int IPW = 32 / G;                 // items per warp
   const int grp = lane / G, j = lane % G;  // item slot in the warp, device
@@ -314,14 +319,16 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
   int* perm = perm_s[wib][grp];
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   const double lim = (!F1B && j < C) ? limits[j] : 0.0;
-  const int64_t n_items = (int64_t)n_seg * kfact;
+  // this launch evaluates permutations [r0, r0 + rwin) of every table; item
+  // = s * rwin + (r - r0), the window-local output slot
+  const int64_t n_items = (int64_t)n_seg * rwin;
 
   for (int64_t ib = gw * IPW; ib < n_items; ib += nw * IPW) {
     const int64_t item = ib + grp;
     int s = 0, r = 0, kk = 0, kkf = 0;
     if (item < n_items) {
-      s = (int)(item / kfact);
-      r = (int)(item - (int64_t)s * kfact);
+      s = (int)(item / rwin);
+      r = r0 + (int)(item - (int64_t)s * rwin);
       if (F1B) {
         kk = mb_off[s + 1] > mb_off[s] ? 1 : 0;
         kkf = 1;
@@ -747,7 +754,7 @@ __global__ void order_select_kernel(const int64_t* __restrict__ mb_off, int k, i
                                     double* __restrict__ makespan, double* __restrict__ bubble,
                                     int* __restrict__ deadlock, double* __restrict__ dev_stats,
                                     int* __restrict__ status) {
-  __shared__ int best_s, perm[16];
+  __shared__ int best_s, perm[kMaxClusters];
   const int s = blockIdx.x;
   const int64_t base = mb_off[s];
   const int M = (int)(mb_off[s + 1] - base);
@@ -803,6 +810,101 @@ __global__ void order_select_kernel(const int64_t* __restrict__ mb_off, int k, i
   }
 }
 
+// Windowed selection (n_clusters > 8 or too many items for one launch): the
+// reference's rule (schedule.cpp:297-316: smaller makespan, the identity
+// order on a tie; the first failing evaluation throws) applied to each
+// window of permutations in order, against a running best per table.
+struct OrderBest {
+  double makespan, bubble;
+  int r, flags, err, pad;
+};
+
+__global__ void order_merge_kernel(int n_seg, int C, int r0, int rwin, const int* __restrict__ cl_k,
+                                   const ItemOut* __restrict__ items, const double* __restrict__ item_stats,
+                                   OrderBest* __restrict__ best, double* __restrict__ best_stats,
+                                   const int* __restrict__ status) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_seg) return;
+  OrderBest b = best[s];
+  const int kk = cl_k[s];
+  if (kk <= 0 || status[s] != PP_OK || b.err) return;
+  int nf = 1;
+  for (int q = 2; q <= kk; ++q) nf *= q;
+  int won = -1;
+  for (int r = r0; r < r0 + rwin && r < nf; ++r) {
+    const ItemOut it = items[(int64_t)s * rwin + (r - r0)];
+    const int e = (it.flags >> 8) & 0xff;
+    if (e) {
+      b.err = e;
+      break;
+    }
+    const bool id = it.flags & 1;
+    const bool bid = b.r >= 0 && (b.flags & 1);
+    if (it.makespan < b.makespan || (it.makespan == b.makespan && id && !bid)) {
+      b.makespan = it.makespan;
+      b.bubble = it.bubble;
+      b.flags = it.flags;
+      b.r = r;
+      won = r - r0;
+    }
+  }
+  if (won >= 0 && item_stats)
+    for (int q = 0; q < 5 * C; ++q) best_stats[(int64_t)s * 5 * C + q] = item_stats[((int64_t)s * rwin + won) * 5 * C + q];
+  best[s] = b;
+}
+
+__global__ void order_final_kernel(const int64_t* __restrict__ mb_off, int k, int C, const int* __restrict__ cl_idx,
+                                   const int* __restrict__ cl_off, const int* __restrict__ cl_k,
+                                   const OrderBest* __restrict__ bestv, const double* __restrict__ best_stats,
+                                   int* __restrict__ order, double* __restrict__ makespan, double* __restrict__ bubble,
+                                   int* __restrict__ deadlock, double* __restrict__ dev_stats,
+                                   int* __restrict__ status) {
+  __shared__ int perm[kMaxClusters];
+  const int s = blockIdx.x;
+  const int64_t base = mb_off[s];
+  const int M = (int)(mb_off[s + 1] - base);
+  const int kk = cl_k[s];
+  const OrderBest b = bestv[s];
+  int best = (kk > 0 && status[s] == PP_OK) ? b.r : -1;
+  if (kk > 0 && status[s] == PP_OK && b.err) best = -1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (kk > 0 && status[s] == PP_OK && b.err) status[s] = b.err == 3 ? PP_ERR_NOT_CONVERGED : PP_ERR_NOT_EXECUTABLE;
+    if (best >= 0) {
+      makespan[s] = b.makespan;
+      if (bubble) bubble[s] = b.bubble;
+      if (deadlock) deadlock[s] = (b.flags >> 1) & 1;
+      nth_perm(best, kk, perm);
+    } else {
+      makespan[s] = __longlong_as_double(0x7ff8000000000000LL);
+      if (bubble) bubble[s] = 0.0;
+      if (deadlock) deadlock[s] = 0;
+    }
+  }
+  __syncthreads();
+  if (best < 0) {
+    for (int i = threadIdx.x; i < M; i += blockDim.x) order[base + i] = -1;
+    return;
+  }
+  if (dev_stats && best_stats)
+    for (int q = threadIdx.x; q < 5 * C; q += blockDim.x) dev_stats[s * 5 * C + q] = best_stats[(int64_t)s * 5 * C + q];
+  const int* off = cl_off + (int64_t)s * (k + 1);
+  int pos = 0;
+  for (int q = 0; q < kk; ++q) {
+    const int c = perm[q];
+    const int a = off[c], n = off[c + 1] - off[c];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) order[base + pos + t] = cl_idx[base + a + t];
+    pos += n;
+  }
+}
+
+__global__ void order_best_init_kernel(int n_seg, OrderBest* best) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n_seg) best[s] = OrderBest{__longlong_as_double(0x7ff0000000000000LL), 0.0, -1, 0, 0, 0};
+}
+
+size_t order_search_best_bytes() { return sizeof(OrderBest); }
+
 size_t order_search_slot_bytes(int64_t max_m, int C) { return sched_slot_bytes(max_m, C); }
 
 // warps for the evaluation grid; the scratch holds warps * (32 / G) slots
@@ -822,17 +924,33 @@ cudaError_t launch_order_search(const double* tf, const double* tb, const double
                                 int* assign, int* cl_idx, int* cl_off, int* cl_k, char* scratch,
                                 size_t slot_bytes, int warps, void* items, double* item_stats,
                                 int* order, double* makespan, double* bubble, int* deadlock,
-                                double* dev_stats, int* status, cudaStream_t st) {
+                                double* dev_stats, int* status, int rwin, void* best, double* best_stats,
+                                cudaStream_t st) {
   if (n_seg <= 0) return cudaSuccess;
   cluster_kernel<<<n_seg, 256, 0, st>>>(tf, tb, mb_off, C, k, pred, assign, cl_idx, cl_off, cl_k, status);
   int G = 1;
   while (G < C) G *= 2;
   const int blocks = (warps + 3) / 4;
-  perm_eval_kernel<false><<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, limits, C, G, k, kfact, comm_latency, n_seg,
-                                           cl_idx, cl_off, cl_k, scratch, slot_bytes, max_m,
-                                           (ItemOut*)items, item_stats);
-  order_select_kernel<<<n_seg, 128, 0, st>>>(mb_off, k, kfact, C, cl_idx, cl_off, cl_k, (const ItemOut*)items,
-                                             item_stats, order, makespan, bubble, deadlock, dev_stats, status);
+  if (rwin >= kfact) {  // every permutation in one launch
+    perm_eval_kernel<false><<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, limits, C, G, k, kfact, comm_latency, n_seg,
+                                                    cl_idx, cl_off, cl_k, scratch, slot_bytes, max_m,
+                                                    (ItemOut*)items, item_stats, 0, kfact);
+    order_select_kernel<<<n_seg, 128, 0, st>>>(mb_off, k, kfact, C, cl_idx, cl_off, cl_k, (const ItemOut*)items,
+                                               item_stats, order, makespan, bubble, deadlock, dev_stats, status);
+    return cudaGetLastError();
+  }
+  OrderBest* bv = static_cast<OrderBest*>(best);
+  order_best_init_kernel<<<(n_seg + 127) / 128, 128, 0, st>>>(n_seg, bv);
+  for (int r0 = 0; r0 < kfact; r0 += rwin) {
+    const int w = std::min(rwin, kfact - r0);
+    perm_eval_kernel<false><<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, limits, C, G, k, kfact, comm_latency, n_seg,
+                                                    cl_idx, cl_off, cl_k, scratch, slot_bytes, max_m,
+                                                    (ItemOut*)items, item_stats, r0, w);
+    order_merge_kernel<<<(n_seg + 127) / 128, 128, 0, st>>>(n_seg, C, r0, w, cl_k, (const ItemOut*)items, item_stats,
+                                                            bv, best_stats, status);
+  }
+  order_final_kernel<<<n_seg, 128, 0, st>>>(mb_off, k, C, cl_idx, cl_off, cl_k, bv, best_stats, order, makespan,
+                                            bubble, deadlock, dev_stats, status);
   return cudaGetLastError();
 }
 
@@ -849,7 +967,7 @@ cudaError_t launch_sim_1f1b(const double* tf, const double* tb, const double* ac
   const int blocks = (warps + 3) / 4;
   perm_eval_kernel<true><<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, nullptr, C, G, 1, 1, comm_latency, n_seg,
                                                  nullptr, nullptr, nullptr, scratch, slot_bytes, max_m,
-                                                 (ItemOut*)items, nullptr);
+                                                 (ItemOut*)items, nullptr, 0, 1);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,7 @@ import pytest
 
 from conftest import load_golden
 from oracle.bind import Reference, reference_available
-from order_cases import cases, nonconvergent
+from order_cases import cases, nonconvergent, random_tables
 from paper_2311_10418_b200 import capi
 from paper_2311_10418_b200 import workloads as W
 
@@ -137,6 +137,25 @@ def test_planner_tables_vs_reference(planner):
         planner.order_search_device(*(torch.from_numpy(x).to(dev) for x in (tf, tb, act)),
                                     torch.tensor(mb_off, dtype=torch.int64, device=dev), mb_off, lim, d, k, 0.0)
         assert_same({key: v.cpu().numpy() for key, v in d.items()}, exp, f"device C={C}")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("k, n_tab", [(9, 2), (9, 12), (10, 1)])
+def test_more_than_eight_clusters_vs_reference(planner, k, n_tab):
+    """n_clusters 9 and 10 (9! = 362,880 / 10! = 3,628,800 evaluations per
+    table, as the reference's std::next_permutation loop): one launch for 2
+    tables, permutation windows folded into a running best for 12 tables
+    (> 4 M evaluations) and for 10 clusters; order, makespan, bubble ratio
+    and device stats against the reference's order_microbatches."""
+    rng = np.random.default_rng(900 + k + n_tab)
+    # (distinct durations for 9 clusters: k-means keeps all k clusters, so
+    # every table really has 9! permutations; lattice durations for 10)
+    tf, tb, act, off = random_tables(rng, n_tab, k + 2, k + 6, 3, lattice=k > 9)
+    lim = 3.0 * act.max(axis=0)
+    got = planner.order_search(tf, tb, act, off, lim, k, 0.0)
+    _, exp = Reference().order_search(tf, tb, act, off, lim, k, 0.0, threads=16)
+    assert_same(got, exp, f"k={k} tables={n_tab}")
 
 
 @pytest.mark.gpu
