@@ -337,6 +337,45 @@ int pp_order_search_device(pp_ctx* ctx, const double* d_t_f, const double* d_t_b
                            int32_t* d_order, double* d_makespan, double* d_bubble_ratio,
                            int32_t* d_deadlock, double* d_device_stats, int32_t* d_status);
 
+/* The chosen plan of every replica, emitted on the device: for each table
+ * s (op costs as pp_order_search) and its GIVEN injection order (order, n_s
+ * entries at mb_offset[s]; e.g. pp_order_search's output), the
+ * ExecutionPlan instruction lists of plan_communication(schedule_adaptive(
+ * costs, limits, order)) (src/comm_plan.cpp:115-233, schedule.cpp:55-122) —
+ * or of schedule_1f1b(n_s, C) when one_f_one_b (schedule.cpp:29-53; order
+ * and limits unused) — with the zero-noise SimReport summary of that plan
+ * (simulate.cpp:78-213) as pp_order_search reports it.  Device j's list of
+ * table s is instructions[10 C mb_offset[s] + 10 n_s j ..] (capacity 10 x
+ * n_stages x rows ints), n_instructions[s * n_stages + j] entries, each
+ * (micro_batch << 4) | InstrKind with the reference's InstrKind numbering
+ * (comm_plan.h:28-39: ForwardPass 0 ... WaitRecvGrad 9); the peer of a
+ * transfer is the neighbouring stage (SendAct / WaitSendAct / RecvGrad /
+ * WaitRecvGrad: j + 1, the others j - 1) and its shape boundary_shape() of
+ * the micro-batch (comm_plan.cpp:104-113), so the plan file (save_plan,
+ * comm_plan.cpp:313-342) is a formatting of these lists.  status:
+ * PP_ERR_INVALID (no micro-batch, a negative / NaN duration, an order that
+ * is not a permutation), PP_ERR_NOT_CONVERGED / PP_ERR_NOT_EXECUTABLE (the
+ * reference's logic_errors).  Host buffers. */
+int pp_emit_plans(pp_ctx* ctx, const double* t_f, const double* t_b, const double* act_mem, const int64_t* mb_offset,
+                  int32_t n_seg, int32_t n_stages, const double* limits, double comm_latency, int32_t one_f_one_b,
+                  const int32_t* order, int32_t* instructions, int32_t* n_instructions, double* makespan,
+                  double* bubble_ratio, int32_t* deadlock, double* device_stats, int32_t* status);
+/* save_plan's text (src/comm_plan.cpp:313-342) of ONE table of a
+ * pp_emit_plans result: instructions / n_instructions of that table (device
+ * j's list at instructions[10 * micro_batches * j]), the micro-batches'
+ * padded shapes, the model's stage layouts and recompute strategy, and the
+ * PlanMeta fields (src/planner.cpp:86-95); into out (cap bytes, NUL
+ * terminated), *len = the full text length.  Host code (plan_file.cpp). */
+int pp_format_plan(const int32_t* instructions, const int32_t* n_instructions, int32_t n_stages,
+                   int32_t micro_batches, const pp_padded_shape* shapes, const pp_model_desc* model,
+                   int64_t iteration, int32_t replica, int64_t hidden_dim, char* out, int64_t cap, int64_t* len);
+/* The same on device-resident tables, orders and outputs (ctx stream). */
+int pp_emit_plans_device(pp_ctx* ctx, const double* d_t_f, const double* d_t_b, const double* d_act_mem,
+                         const int64_t* d_mb_offset, const int64_t* h_mb_offset, int32_t n_seg, int32_t n_stages,
+                         const double* limits, double comm_latency, int32_t one_f_one_b, const int32_t* d_order,
+                         int32_t* d_instructions, int32_t* d_n_instructions, double* d_makespan,
+                         double* d_bubble_ratio, int32_t* d_deadlock, double* d_device_stats, int32_t* d_status);
+
 /* Dataset ingest on the device: load_dataset over a
  * record file (src/workload.cpp:65-103 load_record_file + :109-127
  * truncation to max_seq_len), given the file's bytes.  out receives the

@@ -261,6 +261,8 @@ class Reference:
                                          C.POINTER(_Opts), i32, vp, vp, vp, vp, vp, vp, vp]
         L.ref_plan_batch_out.restype = dbl
         L.ref_op_costs.argtypes = [vp, i64, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), vp, vp, vp]
+        L.ref_emit_plans.argtypes = [vp, vp, vp, vp, i32, i32, vp, dbl, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                     vp, C.POINTER(_ModelDesc), i64, i32, i64, C.c_char_p, i64]
         L.ref_select_recomputation.argtypes = [vp, vp, i32, C.POINTER(_GridDesc), C.POINTER(_ModelDesc), i32, vp,
                                                vp, vp, vp, vp, vp]
         L.ref_order_search.argtypes = [vp, vp, vp, vp, i32, i32, vp, i32, dbl, i32, vp, vp, vp, vp, vp, vp]
@@ -297,6 +299,53 @@ class Reference:
         if rc != PP_OK:
             raise ValueError(f"reference from_shapes failed: {rc}")
         return tf, tb, act
+
+    def emit_plans(self, t_f, t_b, act_mem, mb_offset, limits=None, order=None, comm_latency=0.0,
+                   one_f_one_b=False, shapes=None, model=None, iteration=0, replica=0, hidden=1024):
+        """The reference's plan per table for the given order (or 1F1B):
+        dict like capi.Planner.emit_plans plus "peers" and, with shapes and
+        model, "plan_text" = save_plan of table 0."""
+        tf = np.ascontiguousarray(t_f, np.float64)
+        C_ = tf.shape[1]
+        tb = np.ascontiguousarray(t_b, np.float64)
+        ac = np.ascontiguousarray(act_mem, np.float64)
+        off = np.ascontiguousarray(mb_offset, np.int64)
+        S = len(off) - 1
+        rows = int(off[-1])
+        ins = np.zeros(max(rows, 1) * 10 * C_, np.int32)
+        peer = np.zeros_like(ins)
+        nins = np.zeros((S, C_), np.int32)
+        ms, bub = np.zeros(S), np.zeros(S)
+        dl, st = np.zeros(S, np.int32), np.zeros(S, np.int32)
+        ds = np.zeros((S, C_, 5))
+        lim = np.ascontiguousarray(limits if limits is not None else np.zeros(C_), np.float64)
+        od = np.ascontiguousarray(order if order is not None else np.zeros(max(rows, 1)), np.int32)
+        sh = np.ascontiguousarray(shapes if shapes is not None else np.zeros((1, 3)), np.int64)
+        text = C.create_string_buffer(1 << 24)
+        mdesc = None
+        if model is not None:
+            mdesc, _keep = model_desc(model)
+        rc = self.L.ref_emit_plans(_p(tf), _p(tb), _p(ac), _p(off), S, C_, _p(lim), comm_latency,
+                                   1 if one_f_one_b else 0, _p(od) if order is not None else None, _p(ins), _p(peer),
+                                   _p(nins), _p(ms), _p(bub), _p(dl), _p(ds), _p(st),
+                                   _p(sh) if shapes is not None else None,
+                                   C.byref(mdesc) if mdesc is not None else None, iteration, replica, hidden, text,
+                                   len(text))
+        if rc != PP_OK:
+            raise ValueError(f"reference emit failed: {rc}")
+        lists, peers = [], []
+        for s in range(S):
+            m = int(off[s + 1] - off[s])
+            per, pp_ = [], []
+            for j in range(C_):
+                o = 10 * C_ * off[s] + 10 * m * j
+                a = ins[o:o + nins[s, j]]
+                per.append(np.stack([a & 15, a >> 4], 1).astype(np.int32))
+                pp_.append(peer[o:o + nins[s, j]].copy())
+            lists.append(per)
+            peers.append(pp_)
+        return {"instructions": lists, "peers": peers, "makespan": ms, "bubble_ratio": bub, "deadlock": dl,
+                "device_stats": ds, "status": st, "plan_text": text.value.decode()}
 
     def select_recomputation(self, shapes, mb_offset, grid, model, strategies=(0, 1, 2), limits=None):
         """The reference's select_recomputation per partition of shapes ->

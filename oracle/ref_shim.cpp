@@ -524,6 +524,82 @@ double ref_order_search(const double* t_f, const double* t_b, const double* act,
 }
 
 
+// The reference's plan of each table for a GIVEN injection order (or the
+// 1F1B schedule): plan_communication(schedule_adaptive(costs, limits, order))
+// instruction lists packed like pp_emit_plans ((mb << 4) | kind, peers in
+// `peer`), the zero-noise SimReport, and (when meta != null) save_plan's text
+// of table 0 with that plan metadata into text (cap bytes).
+int ref_emit_plans(const double* t_f, const double* t_b, const double* act, const int64_t* mb_off, int32_t n_seg,
+                   int32_t C, const double* limits, double comm_latency, int32_t f1b, const int32_t* order,
+                   int32_t* ins, int32_t* peer, int32_t* nins, double* makespan, double* bubble, int32_t* deadlock,
+                   double* dev_stats, int32_t* status, const pp_padded_shape* shapes, const pp_model_desc* m,
+                   int64_t iteration, int32_t replica, int64_t hidden, char* text, int64_t cap) {
+  std::vector<double> lim(limits ? limits : act, (limits ? limits : act) + C);
+  for (int s = 0; s < n_seg; ++s) {
+    const int64_t b = mb_off[s], M = mb_off[s + 1] - b;
+    for (int j = 0; j < C; ++j) nins[s * C + j] = 0;
+    try {
+      OpCostTable costs;
+      costs.micro_batches = static_cast<int>(M);
+      costs.stages = C;
+      costs.t_f.assign(t_f + b * C, t_f + (b + M) * C);
+      costs.t_b.assign(t_b + b * C, t_b + (b + M) * C);
+      costs.act_mem.assign(act + b * C, act + (b + M) * C);
+      PlanMeta meta;
+      if (shapes && m) {
+        ModelConfig cfg = model_from_desc(m);
+        meta.iteration = iteration;
+        meta.replica = replica;
+        meta.hidden_dim = hidden;
+        meta.encoder_decoder = cfg.is_encoder_decoder;
+        meta.recompute = static_cast<Recompute>(m->recompute);
+        meta.stage_layers = cfg.stages;
+        for (int64_t i = 0; i < M; ++i)
+          meta.shape_table.push_back({shapes[b + i].mbs, shapes[b + i].input_len, shapes[b + i].target_len});
+      } else {
+        meta.shape_table.assign(static_cast<std::size_t>(M), MbShapeEntry{1, 1, 0});
+      }
+      std::vector<int> ord(order ? order + b : nullptr, order ? order + b + M : nullptr);
+      PipelineSchedule sched = f1b ? schedule_1f1b(static_cast<int>(M), C) : schedule_adaptive(costs, lim, ord);
+      ExecutionPlan plan = plan_communication(sched, costs, meta);
+      SimConfig zero_noise;
+      zero_noise.comm_latency = comm_latency;
+      SimReport rep = simulate(plan, costs, zero_noise);
+      for (int j = 0; j < C; ++j) {
+        const auto& L = plan.devices[static_cast<std::size_t>(j)];
+        nins[s * C + j] = static_cast<int32_t>(L.size());
+        int32_t* o = ins + 10 * C * b + 10 * M * j;
+        int32_t* pe = peer + 10 * C * b + 10 * M * j;
+        for (std::size_t q = 0; q < L.size(); ++q) {
+          o[q] = (L[q].microbatch << 4) | static_cast<int>(L[q].kind);
+          pe[q] = L[q].peer;
+        }
+        const DeviceStats& d = rep.devices[static_cast<std::size_t>(j)];
+        double* ds = dev_stats + (static_cast<int64_t>(s) * C + j) * 5;
+        ds[0] = d.busy; ds[1] = d.idle; ds[2] = d.blocked; ds[3] = d.peak_mem; ds[4] = d.final_mem;
+      }
+      makespan[s] = rep.makespan;
+      bubble[s] = rep.bubble_ratio;
+      deadlock[s] = rep.deadlock ? 1 : 0;
+      status[s] = PP_OK;
+      if (s == 0 && text && cap > 0) {
+        std::ostringstream os;
+        save_plan(plan, os);
+        const std::string t = os.str();
+        const std::size_t nbytes = std::min<std::size_t>(t.size(), static_cast<std::size_t>(cap - 1));
+        std::memcpy(text, t.data(), nbytes);
+        text[nbytes] = 0;
+      }
+    } catch (const std::invalid_argument&) {
+      status[s] = PP_ERR_INVALID;
+    } catch (const std::logic_error& e) {
+      status[s] = std::strstr(e.what(), "converge") ? PP_ERR_NOT_CONVERGED : PP_ERR_NOT_EXECUTABLE;
+    }
+  }
+  return PP_OK;
+}
+
+
 // load_dataset over a record file (workload.cpp:65-127): samples out (up to
 // cap), *n set; PP_ERR_PARSE with line / byte / message kind, PP_ERR_INVALID.
 int ref_load_record_file(const char* path, int64_t max_seq_len, pp_sample* out, int64_t cap, int64_t* n,

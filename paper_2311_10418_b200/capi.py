@@ -34,7 +34,7 @@ EXPORTED = [
     "pp_op_costs", "pp_plan_op_costs_device", "pp_order_search", "pp_order_search_device",
     "pp_load_records", "pp_load_records_device", "pp_draw_minibatches", "pp_draw_minibatches_device",
     "pp_padding_report", "pp_assign_replicas", "pp_pack_plan_slots", "pp_select_recomputation",
-    "pp_select_recomputation_device",
+    "pp_select_recomputation_device", "pp_emit_plans", "pp_emit_plans_device", "pp_format_plan",
 ]
 
 
@@ -156,6 +156,8 @@ def _load():
     lib.pp_slice_cost_host.argtypes = [C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, i64, i64, vp, vp]
     lib.pp_calibrate_fp64.argtypes = [C.c_int, C.POINTER(dbl)]
     lib.pp_op_costs.argtypes = [vp, vp, i64, C.POINTER(GridDesc), C.POINTER(ModelDesc), vp, vp, vp]
+    lib.pp_format_plan.argtypes = [vp, vp, i32, i32, vp, C.POINTER(ModelDesc), i64, i32, i64, C.c_char_p, i64, vp]
+    lib.pp_emit_plans.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, C.c_double, i32, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.pp_select_recomputation.argtypes = [vp, vp, vp, i32, C.POINTER(GridDesc), C.POINTER(ModelDesc), i32, vp,
                                             vp, vp, vp, vp, vp]
     lib.pp_select_recomputation_device.argtypes = [vp, vp, vp, vp, i32, vp, vp, C.POINTER(GridDesc),
@@ -558,6 +560,63 @@ class Planner:
         if rc != PP_OK:
             _raise_status(rc, -1, self._err())
         return mb_off
+
+    def emit_plans(self, t_f, t_b, act_mem, mb_offset, limits=None, order=None, comm_latency=0.0,
+                   one_f_one_b=False) -> dict:
+        """The chosen plan per table: {"instructions": list (table) of lists
+        (stage) of (InstrKind, micro_batch) int32 arrays, "makespan",
+        "bubble_ratio", "deadlock", "device_stats" (S, C, 5), "status"}."""
+        tf = np.ascontiguousarray(t_f, np.float64)
+        C_ = tf.shape[1]
+        tb = np.ascontiguousarray(t_b, np.float64)
+        ac = np.ascontiguousarray(act_mem, np.float64)
+        off = np.ascontiguousarray(mb_offset, np.int64)
+        S = len(off) - 1
+        rows = int(off[-1])
+        ins = np.zeros(max(rows, 1) * 10 * C_, np.int32)
+        nins = np.zeros((S, C_), np.int32)
+        ms, bub = np.zeros(S), np.zeros(S)
+        dl, st = np.zeros(S, np.int32), np.zeros(S, np.int32)
+        ds = np.zeros((S, C_, 5))
+        lim = np.ascontiguousarray(limits if limits is not None else np.zeros(C_), np.float64)
+        od = np.ascontiguousarray(order if order is not None else np.zeros(max(rows, 1)), np.int32)
+        rc = lib.pp_emit_plans(self._h, _p(tf), _p(tb), _p(ac), _p(off), S, C_, _p(lim), comm_latency,
+                               1 if one_f_one_b else 0, _p(od), _p(ins), _p(nins), _p(ms), _p(bub), _p(dl),
+                               _p(ds), _p(st))
+        if rc != PP_OK:
+            _raise_status(rc, -1, self._err())
+        lists = []
+        for s in range(S):
+            m = int(off[s + 1] - off[s])
+            per = []
+            for j in range(C_):
+                a = ins[10 * C_ * off[s] + 10 * m * j: 10 * C_ * off[s] + 10 * m * j + nins[s, j]]
+                per.append(np.stack([a & 15, a >> 4], 1).astype(np.int32))
+            lists.append(per)
+        return {"instructions": lists, "makespan": ms, "bubble_ratio": bub, "deadlock": dl, "device_stats": ds,
+                "status": st}
+
+    @staticmethod
+    def format_plan(instructions, shapes, model: "Model", iteration=0, replica=0, hidden_dim=1024) -> str:
+        """save_plan's text of one emitted plan: instructions = emit_plans(...)
+        ["instructions"][s] (per stage (kind, micro_batch) rows)."""
+        C_ = len(instructions)
+        sh = np.ascontiguousarray(shapes, np.int64).reshape(-1, 3)
+        M = len(sh)
+        ins = np.zeros(max(M, 1) * 10 * C_, np.int32)
+        nins = np.zeros(C_, np.int32)
+        for j, a in enumerate(instructions):
+            packed = (np.asarray(a)[:, 1] << 4) | np.asarray(a)[:, 0] if len(a) else np.zeros(0, np.int32)
+            ins[10 * M * j:10 * M * j + len(packed)] = packed
+            nins[j] = len(packed)
+        n = np.zeros(1, np.int64)
+        md = model.desc()
+        buf = C.create_string_buffer(1 << 22)
+        rc = lib.pp_format_plan(_p(ins), _p(nins), C_, M, _p(sh), C.byref(md), iteration, replica, hidden_dim, buf,
+                                len(buf), _p(n))
+        if rc != PP_OK:
+            raise InvalidArgument("bad plan")
+        return buf.value.decode()
 
     def plan_op_costs_device(self, d_ordered, d_seg_offsets, h_seg_offsets, d_splits, d_count,
                              grid: Grid, model: Model, d_tf, d_tb, d_act) -> np.ndarray:

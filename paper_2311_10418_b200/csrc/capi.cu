@@ -125,6 +125,11 @@ size_t dp_coop_parts_bytes(int grid);
 size_t order_search_slot_bytes(int64_t max_m, int C);
 int order_search_warps(int64_t n_items, int C, size_t slot_bytes, size_t budget);
 size_t order_search_item_bytes();
+cudaError_t launch_emit_plans(const double* tf, const double* tb, const double* act, const int64_t* mb_off, int n_seg,
+                              int C, const double* limits, double comm_latency, int64_t max_m, const int* order,
+                              int f1b, char* scratch, size_t slot_bytes, int warps, void* items, int* ok, int* seen,
+                              int* out_ins, int* out_nins, double* makespan, double* bubble, int* deadlock,
+                              double* dev_stats, int* status, cudaStream_t st);
 size_t order_search_best_bytes();
 size_t ingest_scratch_bytes(int64_t n_bytes);
 cudaError_t launch_load_records(const unsigned char* d_bytes, int64_t n, long long max_seq_len, char* scratch,
@@ -304,7 +309,7 @@ struct pp_ctx {
       colbase, chunk_nv, perm;
   // injection-order search (sched.cu)
   DevBuf os_tf, os_tb, os_act, os_off, os_lim, os_pred, os_assign, os_idx, os_cloff, os_clk, os_scratch,
-      os_items, os_istats, os_order, os_ms, os_bub, os_dl, os_ds, os_status, os_best, os_bstats;
+      os_items, os_istats, os_order, os_ms, os_bub, os_dl, os_ds, os_status, os_best, os_bstats, em_ins, em_nins;
   // dataset ingest (ingest.cu)
   DevBuf ing_bytes, ing_scratch, ing_out, ing_off;
   // padding report (report.cu)
@@ -355,7 +360,7 @@ struct pp_ctx {
             &small_bm, &coop_state, &coop_parts, &shapes, &stage_lay, &mb_off, &oc_tf, &oc_tb, &oc_act,
             &cmin, &dp_cols, &colbase, &chunk_nv, &perm, &gt_need, &gt_off, &gt_total, &gt_G, &gt_base, &gt_rf, &gt_rlo, &rc_tab, &rc_lim, &rc_out,
             &os_tf, &os_tb, &os_act, &os_off, &os_lim, &os_pred, &os_assign, &os_idx, &os_cloff, &os_clk,
-            &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status, &os_best, &os_bstats,
+            &os_scratch, &os_items, &os_istats, &os_order, &os_ms, &os_bub, &os_dl, &os_ds, &os_status, &os_best, &os_bstats, &em_ins, &em_nins,
             &ing_bytes, &ing_scratch, &ing_out, &ing_off,
             &rp_samples, &rp_trunc, &rp_off, &rp_ordered, &rp_splits, &rp_times, &rp_count, &rp_tmax, &rp_obj,
             &rp_status, &rp_err, &rp_tf, &rp_tb, &rp_act, &rp_mboff, &rp_st6, &rp_bins, &rp_naive, &rp_items,
@@ -2777,6 +2782,125 @@ int pp_order_search_device(pp_ctx* ctx, const double* d_t_f, const double* d_t_b
                           d_device_stats, d_status);
 }
 
+
+}  // extern "C"
+
+namespace {
+
+// Emission of the chosen plans (device tables, orders and outputs).
+int emit_plans_run(pp_ctx* ctx, const double* d_tf, const double* d_tb, const double* d_act, const int64_t* d_off,
+                   const int64_t* h_off, int32_t n_seg, int32_t C, const double* limits, double comm_latency,
+                   int32_t f1b, const int32_t* d_order, int32_t* d_ins, int32_t* d_nins, double* d_ms, double* d_bub,
+                   int32_t* d_dl, double* d_ds, int32_t* d_status) {
+  cudaStream_t st = ctx->stream;
+  int64_t max_m = 1;
+  for (int s = 0; s < n_seg; ++s) {
+    const int64_t m = h_off[s + 1] - h_off[s];
+    if (m >= (int64_t)1 << 26) return fail(ctx, PP_ERR_INVALID, "micro-batch count too large");
+    max_m = std::max(max_m, m);
+  }
+  const int64_t rows = h_off[n_seg] - h_off[0];
+  const size_t slot = order_search_slot_bytes(max_m, C);
+  size_t free_b = 0, total_b = 0;
+  PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const int warps = order_search_warps(n_seg, C, slot, std::min<size_t>(free_b / 2, (size_t)32 << 30));
+  int G = 1;
+  while (G < C) G *= 2;
+  PP_CUDA(ctx->os_lim.ensure(C * sizeof(double)));
+  PP_CUDA(ctx->os_scratch.ensure((size_t)warps * (32 / G) * slot));
+  PP_CUDA(ctx->os_items.ensure((size_t)n_seg * order_search_item_bytes()));
+  PP_CUDA(ctx->os_idx.ensure(std::max<int64_t>(rows + h_off[0], 1) * sizeof(int)));
+  PP_CUDA(ctx->os_clk.ensure(n_seg * sizeof(int)));
+  if (!f1b) PP_CUDA(up(ctx, ctx->os_lim.p, limits, C * sizeof(double)));
+  PP_CUDA(launch_emit_plans(d_tf, d_tb, d_act, d_off, n_seg, C, ctx->os_lim.as<double>(), comm_latency, max_m,
+                            d_order, f1b, ctx->os_scratch.as<char>(), slot, warps, ctx->os_items.p,
+                            ctx->os_clk.as<int>(), ctx->os_idx.as<int>(), d_ins, d_nins, d_ms, d_bub, d_dl, d_ds,
+                            d_status, st));
+  PP_CUDA(cudaStreamSynchronize(st));
+  return PP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pp_emit_plans(pp_ctx* ctx, const double* t_f, const double* t_b, const double* act_mem, const int64_t* mb_offset,
+                  int32_t n_seg, int32_t n_stages, const double* limits, double comm_latency, int32_t one_f_one_b,
+                  const int32_t* order, int32_t* instructions, int32_t* n_instructions, double* makespan,
+                  double* bubble_ratio, int32_t* deadlock, double* device_stats, int32_t* status) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n_seg < 0 || n_stages < 1 || n_stages > 32 || (n_seg > 0 && !mb_offset))
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  if (n_seg == 0) return PP_OK;
+  if (!t_f || !t_b || !act_mem || (!one_f_one_b && (!order || !limits)) || !instructions || !n_instructions ||
+      !makespan || !status)
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  for (int s = 0; s < n_seg; ++s)
+    if (mb_offset[s + 1] < mb_offset[s]) return fail(ctx, PP_ERR_INVALID, "mb_offset must be non-decreasing");
+  const int C = n_stages;
+  const int64_t o0 = mb_offset[0], n_mb = mb_offset[n_seg] - o0;
+  std::vector<int64_t> off(n_seg + 1);
+  for (int s = 0; s <= n_seg; ++s) off[s] = mb_offset[s] - o0;
+  cudaStream_t st = ctx->stream;
+  const size_t tb_bytes = std::max<int64_t>(n_mb, 1) * C * sizeof(double);
+  PP_CUDA(ctx->os_tf.ensure(tb_bytes));
+  PP_CUDA(ctx->os_tb.ensure(tb_bytes));
+  PP_CUDA(ctx->os_act.ensure(tb_bytes));
+  PP_CUDA(ctx->mb_off.ensure((n_seg + 1) * sizeof(int64_t)));
+  PP_CUDA(ctx->os_order.ensure(std::max<int64_t>(n_mb, 1) * sizeof(int32_t)));
+  PP_CUDA(ctx->em_ins.ensure(std::max<int64_t>(n_mb, 1) * 10 * C * sizeof(int32_t)));
+  PP_CUDA(ctx->em_nins.ensure((size_t)n_seg * C * sizeof(int32_t)));
+  PP_CUDA(ctx->os_ms.ensure(n_seg * sizeof(double)));
+  PP_CUDA(ctx->os_bub.ensure(n_seg * sizeof(double)));
+  PP_CUDA(ctx->os_dl.ensure(n_seg * sizeof(int32_t)));
+  PP_CUDA(ctx->os_ds.ensure((size_t)n_seg * 5 * C * sizeof(double)));
+  PP_CUDA(ctx->os_status.ensure(n_seg * sizeof(int32_t)));
+  PP_CUDA(cudaMemcpyAsync(ctx->os_tf.p, t_f + o0 * C, n_mb * C * sizeof(double), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->os_tb.p, t_b + o0 * C, n_mb * C * sizeof(double), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->os_act.p, act_mem + o0 * C, n_mb * C * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (!one_f_one_b)
+    PP_CUDA(cudaMemcpyAsync(ctx->os_order.p, order + o0, n_mb * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  PP_CUDA(cudaMemcpyAsync(ctx->mb_off.p, off.data(), (n_seg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if ((rc = emit_plans_run(ctx, ctx->os_tf.as<double>(), ctx->os_tb.as<double>(), ctx->os_act.as<double>(),
+                           ctx->mb_off.as<int64_t>(), off.data(), n_seg, C, limits, comm_latency, one_f_one_b,
+                           ctx->os_order.as<int32_t>(), ctx->em_ins.as<int32_t>(), ctx->em_nins.as<int32_t>(),
+                           ctx->os_ms.as<double>(), ctx->os_bub.as<double>(), ctx->os_dl.as<int32_t>(),
+                           ctx->os_ds.as<double>(), ctx->os_status.as<int32_t>())))
+    return rc;
+  PP_CUDA(cudaMemcpyAsync(instructions + o0 * 10 * C, ctx->em_ins.p, n_mb * 10 * C * sizeof(int32_t),
+                          cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaMemcpyAsync(n_instructions, ctx->em_nins.p, (size_t)n_seg * C * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                          st));
+  PP_CUDA(cudaMemcpyAsync(makespan, ctx->os_ms.p, n_seg * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (bubble_ratio)
+    PP_CUDA(cudaMemcpyAsync(bubble_ratio, ctx->os_bub.p, n_seg * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (deadlock) PP_CUDA(cudaMemcpyAsync(deadlock, ctx->os_dl.p, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (device_stats)
+    PP_CUDA(cudaMemcpyAsync(device_stats, ctx->os_ds.p, (size_t)n_seg * 5 * C * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaMemcpyAsync(status, ctx->os_status.p, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  PP_CUDA(cudaStreamSynchronize(st));
+  return PP_OK;
+}
+
+int pp_emit_plans_device(pp_ctx* ctx, const double* d_t_f, const double* d_t_b, const double* d_act_mem,
+                         const int64_t* d_mb_offset, const int64_t* h_mb_offset, int32_t n_seg, int32_t n_stages,
+                         const double* limits, double comm_latency, int32_t one_f_one_b, const int32_t* d_order,
+                         int32_t* d_instructions, int32_t* d_n_instructions, double* d_makespan,
+                         double* d_bubble_ratio, int32_t* d_deadlock, double* d_device_stats, int32_t* d_status) {
+  int rc = check_ctx(ctx);
+  if (rc) return rc;
+  if (n_seg < 0 || n_stages < 1 || n_stages > 32 || (n_seg > 0 && !h_mb_offset))
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  if (n_seg == 0) return PP_OK;
+  if (!d_t_f || !d_t_b || !d_act_mem || !d_mb_offset || (!one_f_one_b && (!d_order || !limits)) || !d_instructions ||
+      !d_n_instructions || !d_makespan || !d_status)
+    return fail(ctx, PP_ERR_INVALID, "bad arguments");
+  return emit_plans_run(ctx, d_t_f, d_t_b, d_act_mem, d_mb_offset, h_mb_offset, n_seg, n_stages, limits,
+                        comm_latency, one_f_one_b, d_order, d_instructions, d_n_instructions, d_makespan,
+                        d_bubble_ratio, d_deadlock, d_device_stats, d_status);
+}
 
 static const char* parse_msg(int kind) {
   switch (kind) {

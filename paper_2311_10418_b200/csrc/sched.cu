@@ -298,13 +298,21 @@ __device__ __forceinline__ void st_cta(double* p, double v) {
 // F1B: the schedule is schedule_1f1b (schedule.cpp:29-53) of table s (one
 // item per table, no clustering): the simulate() makespan of a fixed 1F1B
 // plan, as padding_vs_packing_report's run_iteration needs (simulate.cpp:277-286).
-template <bool F1B>
+// EMIT: one item per table with its injection order GIVEN (`given`, M_s
+// entries at mb_off[s]; ignored with F1B, whose order is the identity): the
+// plan_communication instruction lists of that schedule (comm_plan.cpp:115-233)
+// are copied out — device j's at out_ins[10 C mb_off[s] + 10 M_s j], packed
+// (mb << 4 | InstrKind), their count at out_nins[s C + j] — next to the
+// SimReport summary, so the chosen plan of every replica comes off the device.
+template <bool F1B, bool EMIT = false>
 __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
     const double* __restrict__ tf, const double* __restrict__ tb, const double* __restrict__ act,
     const int64_t* __restrict__ mb_off, const double* __restrict__ limits, int C, int G, int k, int kfact,
     double comm_latency, int n_seg, const int* __restrict__ cl_idx, const int* __restrict__ cl_off,
     const int* __restrict__ cl_k, char* __restrict__ scratch, size_t slot_bytes, int64_t Mcap,
-    ItemOut* __restrict__ items, double* __restrict__ dev_stats, int r0, int rwin) {
+    ItemOut* __restrict__ items, double* __restrict__ dev_stats, int r0, int rwin,
+    const int* __restrict__ given = nullptr, int* __restrict__ out_ins = nullptr,
+    int* __restrict__ out_nins = nullptr) {
   __shared__ int sqn_s[4][64], rqn_s[4][64];
   __shared__ int perm_s[4][32][kMaxClusters];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -329,8 +337,8 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
     if (item < n_items) {
       s = (int)(item / rwin);
       r = r0 + (int)(item - (int64_t)s * rwin);
-      if (F1B) {
-        kk = mb_off[s + 1] > mb_off[s] ? 1 : 0;
+      if (F1B || EMIT) {
+        kk = (mb_off[s + 1] > mb_off[s] && (!EMIT || cl_k[s] > 0)) ? 1 : 0;  // EMIT: cl_k = the table's check
         kkf = 1;
       } else {
         kk = cl_k[s];
@@ -350,10 +358,16 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
 
     // injection order = clusters concatenated in permutation order, written
     // straight into device 0's forward queue
-    if (!F1B && valid && j == 0) nth_perm(r, kk, perm);
+    if (!F1B && !EMIT && valid && j == 0) nth_perm(r, kk, perm);
     __syncwarp();
     bool ident = true;
-    if (!F1B && valid) {
+    if (EMIT && !F1B && valid) {  // the given injection order
+      for (int t = j; t < M; t += G) {
+        const int mb = given[base + t];
+        S.fq[t] = mb;
+        ident &= (mb == t);
+      }
+    } else if (!F1B && valid) {
       const int* idx = cl_idx + base;
       const int* off = cl_off + (int64_t)s * (k + 1);
       int pos = 0;
@@ -590,7 +604,12 @@ __global__ void __launch_bounds__(128, 6) perm_eval_kernel(
         emit(a ? kWaitSendAct : kWaitSendGrad, pend_mb[1 - a]);
       } else if (pend[0]) emit(kWaitSendAct, pend_mb[0]);
       else if (pend[1]) emit(kWaitSendGrad, pend_mb[1]);
+      if (EMIT) {
+        int* dst = out_ins + (int64_t)10 * C * base + (int64_t)10 * M * j;
+        for (int q = 0; q < n_ins; ++q) dst[q] = INS[q];
+      }
     }
+    if (EMIT && active) out_nins[(int64_t)s * C + j] = err ? 0 : n_ins;
     __syncwarp();
 
     // ---- phase 4: simulate at zero noise (simulate.cpp:78-213) ----
@@ -955,6 +974,83 @@ cudaError_t launch_order_search(const double* tf, const double* tb, const double
 }
 
 size_t order_search_item_bytes() { return sizeof(ItemOut); }
+
+// Emission inputs per table: at least one micro-batch, durations >= 0 and
+// not NaN (the emission merge), and (adaptive) an injection order that is a
+// permutation of 0..M-1 (schedule_adaptive's precondition, schedule.cpp:62-66).
+__global__ void __launch_bounds__(256) emit_check_kernel(const double* __restrict__ tf, const double* __restrict__ tb,
+                                                         const int64_t* __restrict__ mb_off, int C,
+                                                         const int* __restrict__ order, int f1b, int* __restrict__ ok,
+                                                         int* __restrict__ seen, int* __restrict__ status,
+                                                         int* __restrict__ out_nins) {
+  __shared__ int bad;
+  const int s = blockIdx.x;
+  const int64_t base = mb_off[s];
+  const int M = (int)(mb_off[s + 1] - base);
+  if (threadIdx.x == 0) bad = M < 1;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) seen[base + i] = 0;
+  for (int j = threadIdx.x; j < C; j += blockDim.x) out_nins[(int64_t)s * C + j] = 0;
+  __syncthreads();
+  for (int64_t q = threadIdx.x; q < (int64_t)M * C; q += blockDim.x)
+    if (!(tf[base * C + q] >= 0.0) || !(tb[base * C + q] >= 0.0)) bad = 1;
+  if (!f1b)
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+      const int mb = order[base + i];
+      if (mb < 0 || mb >= M || atomicExch(&seen[base + mb], 1)) bad = 1;
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ok[s] = bad ? 0 : 1;
+    status[s] = bad ? PP_ERR_INVALID : PP_OK;
+  }
+}
+
+__global__ void emit_final_kernel(int n_seg, const int* __restrict__ ok, const ItemOut* __restrict__ items,
+                                  double* __restrict__ makespan, double* __restrict__ bubble, int* __restrict__ deadlock,
+                                  int* __restrict__ status) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_seg) return;
+  if (!ok[s]) {
+    makespan[s] = __longlong_as_double(0x7ff8000000000000LL);
+    if (bubble) bubble[s] = 0.0;
+    if (deadlock) deadlock[s] = 0;
+    return;
+  }
+  const ItemOut it = items[s];
+  const int e = (it.flags >> 8) & 0xff;
+  status[s] = e ? (e == 3 ? PP_ERR_NOT_CONVERGED : PP_ERR_NOT_EXECUTABLE) : PP_OK;
+  makespan[s] = it.makespan;
+  if (bubble) bubble[s] = it.bubble;
+  if (deadlock) deadlock[s] = (it.flags >> 1) & 1;
+}
+
+// plan_communication of each table's schedule_adaptive(costs, limits, order)
+// (or schedule_1f1b with f1b) for GIVEN injection orders: instruction lists,
+// counts, and the SimReport summary (makespan, bubble, deadlock, device
+// stats [s][C][5]); status PP_ERR_INVALID / NOT_CONVERGED / NOT_EXECUTABLE.
+cudaError_t launch_emit_plans(const double* tf, const double* tb, const double* act, const int64_t* mb_off, int n_seg,
+                              int C, const double* limits, double comm_latency, int64_t max_m, const int* order,
+                              int f1b, char* scratch, size_t slot_bytes, int warps, void* items, int* ok, int* seen,
+                              int* out_ins, int* out_nins, double* makespan, double* bubble, int* deadlock,
+                              double* dev_stats, int* status, cudaStream_t st) {
+  if (n_seg <= 0) return cudaSuccess;
+  int G = 1;
+  while (G < C) G *= 2;
+  const int blocks = (warps + 3) / 4;
+  emit_check_kernel<<<n_seg, 256, 0, st>>>(tf, tb, mb_off, C, order, f1b, ok, seen, status, out_nins);
+  if (f1b)
+    perm_eval_kernel<true, true><<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, limits, C, G, 1, 1, comm_latency,
+                                                         n_seg, nullptr, nullptr, ok, scratch, slot_bytes, max_m,
+                                                         (ItemOut*)items, dev_stats, 0, 1, order, out_ins, out_nins);
+  else
+    perm_eval_kernel<false, true><<<blocks, 128, 0, st>>>(tf, tb, act, mb_off, limits, C, G, 1, 1, comm_latency,
+                                                          n_seg, nullptr, nullptr, ok, scratch, slot_bytes,
+                                                          max_m, (ItemOut*)items, dev_stats, 0, 1, order, out_ins,
+                                                          out_nins);
+  emit_final_kernel<<<(n_seg + 127) / 128, 128, 0, st>>>(n_seg, ok, (const ItemOut*)items, makespan, bubble, deadlock,
+                                                          status);
+  return cudaGetLastError();
+}
 
 // simulate() makespans of schedule_1f1b over every table (run_iteration,
 // simulate.cpp:277-286): items[s].makespan, zero noise, comm_latency.

@@ -158,6 +158,62 @@ def test_more_than_eight_clusters_vs_reference(planner, k, n_tab):
     assert_same(got, exp, f"k={k} tables={n_tab}")
 
 
+def _peer(kind, j):
+    return j + 1 if kind in (2, 5, 6, 9) else j - 1
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("one_f_one_b", [False, True])
+def test_emit_plans_vs_reference(planner, one_f_one_b):
+    """pp_emit_plans: the instruction lists of plan_communication(schedule_
+    adaptive(costs, limits, order)) (or of the 1F1B schedule) for the orders
+    the device search chose, against the reference's plan_communication on
+    the same order — kinds, micro-batches, peers — plus the SimReport
+    summary, and save_plan's text (pp_format_plan) for a T5 and a GPT model."""
+    R = Reference()
+    for name, tf, tb, act, off, lim, k, lat in cases(seed=5150):
+        if name == "uniform" or tf.shape[1] > 16:
+            continue
+        found = planner.order_search(tf, tb, act, off, lim, k, lat)
+        order = found["order"]
+        ok = found["status"] == 0
+        got = planner.emit_plans(tf, tb, act, off, lim, order, lat, one_f_one_b)
+        exp = R.emit_plans(tf, tb, act, off, lim, order, lat, one_f_one_b)
+        for s in range(len(off) - 1):
+            if not one_f_one_b and (not ok[s] or order[off[s]] < 0):
+                continue
+            assert got["status"][s] == exp["status"][s], (name, s)
+            if exp["status"][s] != 0:
+                continue
+            C_ = tf.shape[1]
+            for j in range(C_):
+                a, b = got["instructions"][s][j], exp["instructions"][s][j]
+                assert a.tobytes() == b.tobytes(), (name, s, j)
+                assert [_peer(int(x), j) for x in a[:, 0] if x >= 2] == [int(p) for p, x in
+                                                                         zip(exp["peers"][s][j], b[:, 0]) if x >= 2]
+            for key in ("makespan", "bubble_ratio", "deadlock"):
+                assert got[key][s] == exp[key][s] or (got[key][s] != got[key][s] and exp[key][s] != exp[key][s]), key
+            assert got["device_stats"][s].tobytes() == exp["device_stats"][s].tobytes()
+            if not one_f_one_b:  # the adaptive plan reproduces the search's report
+                assert got["makespan"][s] == found["makespan"][s]
+    # plan text: shapes / model metadata from a real planner table
+    rng = np.random.default_rng(3)
+    for encdec, C_ in ((True, 4), (False, 3)):
+        M = 9
+        tf, tb, act, off = random_tables(rng, 1, M, M, C_, lattice=False)
+        shapes = np.stack([rng.integers(1, 64, M), rng.integers(1, 4096, M),
+                           rng.integers(0, 512, M) if encdec else np.zeros(M, np.int64)], 1).astype(np.int64)
+        model = capi.Model.uniform(C_, 2, encdec, recompute=int(rng.integers(0, 3)))
+        lim = 3.0 * act.max(axis=0)
+        order = planner.order_search(tf, tb, act, off, lim, 3, 0.0)["order"]
+        got = planner.emit_plans(tf, tb, act, off, lim, order, 0.0, one_f_one_b)
+        text = capi.Planner.format_plan(got["instructions"][0], shapes, model, iteration=7, replica=1, hidden_dim=2048)
+        exp = R.emit_plans(tf, tb, act, off, lim, order, 0.0, one_f_one_b, shapes=shapes, model=model, iteration=7,
+                           replica=1, hidden=2048)
+        assert text == exp["plan_text"], (encdec, text[:200], exp["plan_text"][:200])
+
+
 @pytest.mark.gpu
 def test_errors(planner):
     tf, tb, act, off, lim = nonconvergent()
