@@ -28,7 +28,7 @@ if TRACE:
     LIB = os.path.join(BUILD, "libpipeplan_b200_trace.so")
 
 CU = ["sort.cu", "cost.cu", "dp.cu", "dp_coop.cu", "opcost.cu", "sched.cu", "ingest.cu", "report.cu", "slots.cu", "gtab.cu", "capi.cu", "calib.cu"]
-CPP = ["host/workload.cpp", "host/cost_model.cpp", "host/microbatch.cpp", "host/order_search.cpp", "host/padding_report.cpp", "host/capi_host.cpp", "host/plan_file.cpp"]
+CPP = ["host/workload.cpp", "host/cost_model.cpp", "host/microbatch.cpp", "host/order_search.cpp", "host/padding_report.cpp", "host/capi_host.cpp", "host/plan_file.cpp", "host/epoch.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -68,3 +68,20 @@ def test_injection_order_search_matches_reference_planner(tmp_path):
     r = subprocess.run([ORD], capture_output=True, text=True, timeout=600, cwd=tmp_path)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     assert "order dropin: OK" in r.stdout, r.stdout
+
+
+EPO = os.path.join(ROOT, "oracle", "_ref", "epoch_dropin")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(EPO), reason="epoch_dropin not built")
+def test_epoch_planning_files_match_reference_run_plan(tmp_path):
+    """tests/cpp/epoch_dropin.cpp: pipeplan::b200::plan_epoch (draw, plans,
+    select_recomputation, injection-order search, emitted plans — all on the
+    device) writes the same plans_index.csv and .plan files, byte for byte,
+    as the reference's run_plan (GPT / T5, 1 and 2 replicas, adaptive and
+    1F1B policies, restricted strategy sets, limits tight enough to make
+    iterations infeasible)."""
+    r = subprocess.run([EPO, str(tmp_path)], capture_output=True, text=True, timeout=900, cwd=tmp_path)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert r.stdout.strip().endswith("OK"), r.stdout
