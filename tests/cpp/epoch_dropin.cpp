@@ -5,6 +5,7 @@
 // acceptance_dropin setup).  For each configuration both write
 // plans_index.csv and every iter_<i>_replica_<d>.plan; the files must be
 // identical byte for byte.  Test infrastructure (tests/test_dropin.py).
+#include <chrono>
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
@@ -63,7 +64,7 @@ int main(int argc, char** argv) {
     cfg.t_max_interval = c.interval;
     cfg.n_clusters = c.clusters;
     cfg.policy = c.adaptive ? SchedulePolicy::Adaptive : SchedulePolicy::OneFOneB;
-    cfg.workers = 4;
+    cfg.workers = 16;  // run_plan's pool on every host core of the box
     // limits: a multiple of the largest single-sample act_mem of the grid
     const ProfileGrid grid = make_grid(cfg);
     const ModelConfig model = make_model(cfg);
@@ -73,7 +74,9 @@ int main(int argc, char** argv) {
     for (double& l : cfg.device_limits) l = c.limit * amax * 8.0;
     cfg.output_dir = (root / c.name / "reference").string();
     std::ostringstream log;
+    const auto r0 = std::chrono::steady_clock::now();
     run_plan(cfg, log);
+    const double ref_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
 
     b200::EpochConfig ec;
     ec.token_budget = cfg.token_budget;
@@ -100,8 +103,8 @@ int main(int argc, char** argv) {
     for (const auto& e : fs::directory_iterator(ec.output_dir)) { (void)e; ++ours; }
     if (ours != files) ++bad;
     std::cout << c.name << ": " << sum.iterations << " iterations (" << sum.feasible << " feasible), " << files
-              << " reference files, " << ours << " device files, " << bad << " mismatches, device epoch "
-              << sum.total_ms << " ms\n";
+              << " reference files, " << ours << " device files, " << bad << " mismatches; epoch wall: reference run_plan "
+              << ref_ms << " ms (16 threads), device plan_epoch " << sum.total_ms << " ms\n";
     failures += bad;
   }
   std::cout << (failures ? "FAIL" : "OK") << "\n";
