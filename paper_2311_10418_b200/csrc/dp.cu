@@ -341,9 +341,12 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       if (b + 1 >= nblk) break;
       // unit b+1 into the buffer of unit b-1, once the chain released it
       const int u = b + 1, k = (u + 1) & 1, f = (u + 1) >> 1;
+      PP_TRACE(11);
       if (GTAB) named_bar(kBarUnitEmpty + k, 64);
       else mbar_wait(&unit_empty[k], (f - 1) & 1);
+      PP_TRACE(12);
       load_unit(u);
+      PP_TRACE(13);
       // far-far chunks of block b+1 (the workers reduce them during block b)
       const int gn = gb0 + b + 1;
       const int Wn = blk_W[gn];

@@ -45,7 +45,8 @@ def main():
     d = lambda a, b: t[:, b] - t[:, a]  # noqa: E731
     rows = [("chain: A prep (partials)", 0, 1), ("chain: unit wait", 1, 2),
             ("chain: triangle", 2, 3), ("chain: store states", 3, 4), ("chain: block barrier", 4, 5),
-            ("worker0: far-far chunks", 8, 9), ("worker0: fold", 9, 10), ("worker0: to barrier", 10, 5)]
+            ("worker0: far-far chunks", 8, 9), ("worker0: fold", 9, 10), ("worker0: to barrier", 10, 5),
+            ("producer: wait for a free unit", 11, 12), ("producer: unit fill", 12, 13)]
     print(f"{name}: {len(t)} blocks traced; cycles per block (median / mean)")
     for lbl, a, b in rows:
         x = d(a, b)
