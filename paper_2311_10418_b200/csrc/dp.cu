@@ -68,7 +68,7 @@ constexpr int kSyncThreads = 32 * (1 + kWorkers);    // workers + chain (block b
 // it is the critical path and must never lose an issue slot to a worker.
 constexpr int kProducerWarp = kWorkers;      // warp 8
 constexpr int kChainWarp = kWorkers + 1;     // warp 9
-// Named barriers: 1 = block barrier (chain + workers), 2 = worker partials,
+// Named barriers: 1 = block barrier (chain + workers),
 // and on the slice-table path the unit hand-off between the producer and the
 // chain warp (64 threads): full[k] = 3 + k (producer arrives after its
 // stores, the chain syncs), empty[k] = 5 + k (the chain arrives after its
@@ -76,6 +76,8 @@ constexpr int kChainWarp = kWorkers + 1;     // warp 9
 // stores ordered by bar.arrive / bar.sync: nothing for racecheck to flag,
 // unlike TMA writes ordered through an mbarrier (the band path).
 constexpr int kBarUnitFull = 3, kBarUnitEmpty = 5;
+// 7 + w (w < 4): worker w + 4 hands its far-far partial to worker w.
+constexpr int kBarPair = 7;
 
 #ifdef PP_DP_TRACE
 __device__ long long* g_dp_trace = nullptr;  // [block][16] clock64 stamps of CTA 0
@@ -103,15 +105,13 @@ constexpr size_t kChunkBytes = (size_t)kChunkCols * kColBytes;  // 8 KB
 // minimax (MODE 1).
 struct DpSmem {
   static constexpr size_t unit = 0;                                   // [2][64][32] double
-  static constexpr size_t wps = unit + 2 * kUnitCols * kColBytes;     // [8][32] double  worker partials
-  static constexpr size_t wpx = wps + kWorkers * kRB * 8;             // [8][32] double
-  static constexpr size_t wpc = wpx + kWorkers * kRB * 8;             // [8][32] int
-  static constexpr size_t wpj = wpc + kWorkers * kRB * 4;             // [8][32] int
-  static constexpr size_t ps = wpj + kWorkers * kRB * 4;              // [2][32] double  folded far partial
-  static constexpr size_t px = ps + 2 * kRB * 8;                      // [2][32] double
-  static constexpr size_t pc = px + 2 * kRB * 8;                      // [2][32] int
-  static constexpr size_t pj = pc + 2 * kRB * 4;                      // [2][32] int
-  static constexpr size_t row0 = pj + 2 * kRB * 4;                    // state[0]: sum, aux, x
+  // worker partials of a block's far-far columns, double-buffered by block
+  // parity: [2][8][32] each (the chain folds a block's eight partials)
+  static constexpr size_t wps = unit + 2 * kUnitCols * kColBytes;     // double sum
+  static constexpr size_t wpx = wps + 2 * kWorkers * kRB * 8;         // double x
+  static constexpr size_t wpc = wpx + 2 * kWorkers * kRB * 8;         // int count
+  static constexpr size_t wpj = wpc + 2 * kWorkers * kRB * 4;         // int argmin
+  static constexpr size_t row0 = wpj + 2 * kWorkers * kRB * 4;        // state[0]: sum, aux, x
   static constexpr size_t bars = (row0 + 32 + 15) / 16 * 16;          // unit full/empty, ring full/empty
   static constexpr size_t state = (bars + 8 * (4 + 2 * kMaxRing) + 127) / 128 * 128;
 };
@@ -188,10 +188,6 @@ __global__ void __launch_bounds__(kDpThreads, 2)
   double* wpx = reinterpret_cast<double*>(smem + DpSmem::wpx);
   int* wpc = reinterpret_cast<int*>(smem + DpSmem::wpc);
   int* wpj = reinterpret_cast<int*>(smem + DpSmem::wpj);
-  double* ps = reinterpret_cast<double*>(smem + DpSmem::ps);
-  double* px = reinterpret_cast<double*>(smem + DpSmem::px);
-  int* pc = reinterpret_cast<int*>(smem + DpSmem::pc);
-  int* pj = reinterpret_cast<int*>(smem + DpSmem::pj);
   double* row0 = reinterpret_cast<double*>(smem + DpSmem::row0);
   uint64_t* unit_full = reinterpret_cast<uint64_t*>(smem + DpSmem::bars);
   uint64_t* unit_empty = unit_full + 2;
@@ -263,11 +259,12 @@ __global__ void __launch_bounds__(kDpThreads, 2)
     row0[1] = CAND ? 0.0 : INF;
     row0[2] = INF;
   }
-  if (wid == 0) {  // block 0 has no far-far columns (j <= n < i0 + 64)
-    ps[lane] = INF;
-    px[lane] = INF;
-    pc[lane] = 0;
-    pj[lane] = INT_MAX;
+  if (wid < kWorkers) {  // block 0 has no far-far columns (j <= n < i0 + 64): identity partials
+    const int o = wid * kRB + lane;
+    wps[o] = INF;
+    wpx[o] = INF;
+    wpc[o] = 0;
+    wpj[o] = INT_MAX;
   }
   __syncthreads();
 
@@ -295,31 +292,17 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         cn = max(0, min(kRB, Wn - nbn));
       }
       if (GTAB) {
-        // lane q holds the column bases of triangle column q and near-far column q
+        // lane q holds the column bases of triangle column q and near-far
+        // column q; every lane copies its row of every column with cp.async
+        // (a unit's 64 x 32 entries in flight at once: ~1 L2 round trip
+        // instead of eight dependent batches of register loads)
         const int gt = lane < ct ? gcol(i0, lane) : 0;
         const int gn = lane < cn ? gcol(i0n, nbn + lane) : 0;
-        for (int c0 = 0; c0 < ct; c0 += 8) {
-          double v[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int g = __shfl_sync(0xffffffffu, gt, (c0 + q) & 31);
-            v[q] = c0 + q < ct ? __ldg(band + g - lane) : QNAN;
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (c0 + q < ct) U[(c0 + q) * kRB + lane] = v[q];
-        }
-        for (int c0 = 0; c0 < cn; c0 += 8) {
-          double v[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int g = __shfl_sync(0xffffffffu, gn, (c0 + q) & 31);
-            v[q] = c0 + q < cn ? __ldg(band + g - lane) : QNAN;
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (c0 + q < cn) U[(kRB + c0 + q) * kRB + lane] = v[q];
-        }
+        for (int c = 0; c < ct; ++c)
+          cp_async8(U + c * kRB + lane, band + (__shfl_sync(0xffffffffu, gt, c) - lane));
+        for (int c = 0; c < cn; ++c)
+          cp_async8(U + (kRB + c) * kRB + lane, band + (__shfl_sync(0xffffffffu, gn, c) - lane));
+        cp_async_wait_all();
         named_bar_arrive(kBarUnitFull + k, 64);  // (the chain's named_bar completes it)
       } else {
         if (lane == 0) {
@@ -411,10 +394,23 @@ __global__ void __launch_bounds__(kDpThreads, 2)
       // this row's accumulator: the near-far columns (folded during the
       // previous block) and the workers' far-far partial
       Acc A = N;
-      {
-        const int p = (b & 1) * kRB + r;
-        Acc P{ps[p], X2 ? px[p] : INF, CAND ? pc[p] : 0, CAND ? pj[p] : INT_MAX};
-        combine<MODE>(A, P);
+      {  // the worker partials of this block's far-far columns (four: workers
+         // 0-3 folded in 4-7's), a pairwise tree
+        constexpr int kParts = kWorkers / 2;
+        Acc v[kParts];
+#pragma unroll
+        for (int q = 0; q < kParts; ++q) {
+          const int p = ((b & 1) * kWorkers + q) * kRB + r;
+          v[q].s = wps[p];
+          v[q].x = X2 ? wpx[p] : INF;
+          v[q].c = CAND ? wpc[p] : 0;
+          v[q].j = CAND ? wpj[p] : INT_MAX;
+        }
+#pragma unroll
+        for (int h = kParts / 2; h >= 1; h /= 2)
+#pragma unroll
+          for (int q = 0; q < h; ++q) combine<MODE>(v[q], v[q + h]);
+        combine<MODE>(A, v[0]);
       }
       // the last block of a segment whose n is not a multiple of 32 has
       // near-far columns past the previous block's rows: fold them from the
@@ -629,36 +625,30 @@ __global__ void __launch_bounds__(kDpThreads, 2)
         }
         combine<MODE>(a0, a1);
         if (w == 0) PP_TRACE(9);
-        const int o = w * kRB + lane;
-        wps[o] = a0.s;
-        if (X2) wpx[o] = a0.x;
-        if (CAND) {
-          wpc[o] = a0.c;
-          wpj[o] = a0.j;
-        }
-        __syncwarp();
-        named_bar(2, 32 * kWorkers);
-        if (w == 0) {  // fold the 8 worker partials for the chain: a pairwise tree
-          Acc v[kWorkers];
-#pragma unroll
-          for (int q = 0; q < kWorkers; ++q) {
-            const int p = q * kRB + lane;
-            v[q].s = wps[p];
-            v[q].x = X2 ? wpx[p] : INF;
-            v[q].c = CAND ? wpc[p] : 0;
-            v[q].j = CAND ? wpj[p] : INT_MAX;
-          }
-#pragma unroll
-          for (int h = kWorkers / 2; h >= 1; h /= 2)
-#pragma unroll
-            for (int q = 0; q < h; ++q) combine<MODE>(v[q], v[q + h]);
-          const int p2 = (bn & 1) * kRB + lane;
-          ps[p2] = v[0].s;
-          if (X2) px[p2] = v[0].x;
+        // this worker's partial of block b+1, for the chain to fold when it
+        // starts that block (slot parity bn: the chain is reading block b's).
+        // Workers w + 4 hand theirs to worker w (a named barrier per pair),
+        // which folds it in: the chain folds four partials, not eight.
+        const int half = kWorkers / 2;
+        auto put = [&](int slot, const Acc& a) {
+          const int o = ((bn & 1) * kWorkers + slot) * kRB + lane;
+          wps[o] = a.s;
+          if (X2) wpx[o] = a.x;
           if (CAND) {
-            pc[p2] = v[0].c;
-            pj[p2] = v[0].j;
+            wpc[o] = a.c;
+            wpj[o] = a.j;
           }
+        };
+        if (w >= half) {
+          put(w, a0);
+          __syncwarp();
+          named_bar_arrive(kBarPair + (w - half), 64);
+        } else {
+          named_bar(kBarPair + w, 64);
+          const int o = ((bn & 1) * kWorkers + w + half) * kRB + lane;
+          Acc p{wps[o], X2 ? wpx[o] : INF, CAND ? wpc[o] : 0, CAND ? wpj[o] : INT_MAX};
+          combine<MODE>(a0, p);
+          put(w, a0);
         }
         if (w == 0) PP_TRACE(10);
       }

@@ -429,6 +429,15 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+// 8-byte asynchronous global -> shared copy (LDGSTS): no register staging,
+// so one warp keeps a whole unit's loads in flight; cp_async_wait_all makes
+// the calling thread's copies complete (and visible to it) before it arrives
+// on the consumers' barrier.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Producer side of a named-barrier hand-off (release; the consumer's
 // named_bar on the same id and count completes it).
 __device__ __forceinline__ void named_bar_arrive(int id, int threads) {
