@@ -410,6 +410,9 @@ def run_ours(args, rank, world, local):
                                cfg.interval, out=host_out)
         e2e_value = M * steps / (time.perf_counter() - t0)
         e2e_api = "pp_plan_grid (host buffers; pinned samples in, plans out)"
+        # pinned outputs: splits / mb_times come back as each segment's valid
+        # prefix (count[s] entries, prefix_out_kernel), the order in full
+        d2h = tot * 4 + int(host_out["count"].astype(np.int64).sum()) * (4 + 8) + M * (4 + 8 + 8 + 4 + 8)
 
     # ---- isolated kernel durations: the timed region runs `streams` concurrent
     # sub-batches, so per-kernel event spans there overlap and are NOT

@@ -97,6 +97,30 @@ __device__ __forceinline__ void fold(Acc& a, double xv, double ss, double sx, in
   fold_c<MODE, DESC>(a, xv, ss, sx, 1 + sc, j, okb, t);
 }
 
+// Keyed form for the slice-table far-far loop: the state's count and column
+// travel as one key ((1 + C) << 16 | j, dp.cu kKeyShift; n <= kKeyMaxN), so
+// (sum, count) lexicographic order with lowest-j ties is (sum, key) order
+// with a strict key compare in either column order, and a.c carries the key
+// (a.j unused): one select fewer per transition.
+template <int MODE>
+__device__ __forceinline__ void fold_k(Acc& a, double xv, double ss, double sx, int key, double t) {
+  const double cs = __dadd_rn(xv, ss);
+  const bool upd = (xv <= t) & ((cs < a.s) | ((cs == a.s) & (key < a.c)));
+  a.s = upd ? cs : a.s;
+  a.c = upd ? key : a.c;
+  if (MODE == 3) {
+    const double cb = __dadd_rn(xv, sx);
+    a.x = (cb < a.x) ? cb : a.x;
+  }
+}
+template <int MODE>
+__device__ __forceinline__ void combine_k(Acc& a, const Acc& o) {
+  const bool tk = o.s < a.s || (o.s == a.s && o.c < a.c);
+  a.s = tk ? o.s : a.s;
+  a.c = tk ? o.c : a.c;
+  if (MODE == 3) a.x = (o.x < a.x) ? o.x : a.x;
+}
+
 // (s, c, j) lexmin with lowest-j ties.
 __device__ __forceinline__ bool better(double s1, int c1, int j1, double s0, int c0, int j0) {
   return s1 < s0 || (s1 == s0 && (c1 < c0 || (c1 == c0 && j1 < j0)));

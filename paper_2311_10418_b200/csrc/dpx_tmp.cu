@@ -175,7 +175,7 @@ __device__ __forceinline__ int far_chunks_needed(int nc, const double* __restric
 //   `band` points at G, pr.gbase per ordered sample): column c of the block
 //   whose first row is i0 is G[gbase[i0 + c - 1] + c - r] for row r.
 template <int MODE, bool SMEM_STATE, bool SANITIZE, bool GTAB>
-__global__ void __launch_bounds__(dp_threads<GTAB>(), 2)
+__global__ void __launch_bounds__(dp_threads<GTAB>(), 2, 1)
     dp_pass_kernel(const WorkItem* __restrict__ items, const int64_t* __restrict__ seg_off,
                    const int* __restrict__ blk_base, const int* __restrict__ blk_W,
                    const int64_t* __restrict__ tile_off, const int64_t* __restrict__ seg_band_base,

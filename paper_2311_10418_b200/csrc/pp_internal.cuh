@@ -316,6 +316,11 @@ struct DpPrice {
 // [max(0, n-32(b+1)), n-32b)); tile column c holds the 32 rows' values for
 // slice end j = i0 + c, contiguous (256 B per column).
 constexpr int kRB = 32;
+// Slice-table DP state key (dp.cu KEYED): (1 + count) << kKeyShift | column,
+// a positive int32 while the column and 1 + count stay below 2^16 and 2^15:
+// the slice table serves mini-batches of at most kGtabMaxN samples.
+constexpr int kKeyShift = 16;
+constexpr int kGtabMaxN = 32766;
 
 // Compact band (length-sorted single-input mini-batches: cost.cu
 // band_run_kernel<.., true> writes it, dp.cu dp_pass_kernel<.., .., .., true>

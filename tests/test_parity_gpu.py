@@ -636,6 +636,49 @@ def test_order_output_matches_ordered_samples(planner):
         p.close()
 
 
+def test_pinned_outputs_match_pageable(planner):
+    """Pinned output buffers take the valid prefix of splits / mb_times
+    through their device alias (prefix_out_kernel) instead of full-length
+    copies: same plans as pageable buffers on every host-buffer path
+    (single call, part pipeline with 1 and 2 parts per worker, the
+    concurrent-worker pipeline), and nothing past count[s] is written."""
+    import torch
+
+    def pinned_alloc(shape, dtype):
+        t = torch.full(shape if isinstance(shape, tuple) else (shape,), -7,
+                       dtype={np.int64: torch.int64, np.int32: torch.int32, np.float64: torch.float64}[dtype])
+        return t.pin_memory().numpy()
+
+    cfg = W.CONFIGS["C3"]
+    M = 7
+    s = W.dataset(cfg, M)
+    off = W.seg_offsets(cfg, M)
+    for streams, chunks in ((1, 0), (3, 0), (3, 2), (3, -1)):
+        p = capi.Planner(0)
+        p.set_tuning(streams=streams, host_chunks=chunks)
+        a = p.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval)
+        keep = []
+
+        def alloc(shape, dtype):
+            x = pinned_alloc(shape, dtype)
+            keep.append(x)
+            return x
+
+        b = p.plan_batch(s, off, W.grid(), W.model(cfg), cfg.stages, 1, cfg.mem_cap, cfg.interval,
+                         out=capi.Planner.plan_buffers(len(s), M, alloc, order_only=True))
+        for k in ("count", "status", "t_max_used", "objective"):
+            assert np.array_equal(a[k].view(np.int64) if a[k].dtype == np.float64 else a[k],
+                                  b[k].view(np.int64) if b[k].dtype == np.float64 else b[k]), (streams, chunks, k)
+        for q in range(M):
+            m = int(a["count"][q])
+            lo, hi = off[q], off[q + 1]
+            assert np.array_equal(a["splits"][lo:lo + m], b["splits"][lo:lo + m]), (streams, chunks, q)
+            assert np.array_equal(a["mb_times"][lo:lo + m].view(np.int64), b["mb_times"][lo:lo + m].view(np.int64))
+            if streams > 1:  # the prefix writes leave the rest of the caller's buffer alone
+                assert (b["splits"][lo + m:hi] == -7).all(), (streams, chunks, q)
+        p.close()
+
+
 def test_presorted_arbitrary_order_matches_oracle(planner, orc):
     """dp_partition(span) on the caller's order (no sort): running maxima of
     the padded lengths over unsorted spans, certified scan (no bisection)."""

@@ -1,0 +1,11 @@
+# refresh at 47ab8b0: full bench set, GPU tests, ncu capture + launch list of C3
+mkdir -p gpurun_out/r2_41
+timeout 900 python bench.py > gpurun_out/r2_41/bench_c3.json 2> gpurun_out/r2_41/bench_c3.err; echo "c3 rc=$?"; head -c 900 gpurun_out/r2_41/bench_c3.json; echo
+for c in C1 C2 C4; do timeout 900 python bench.py --config $c > gpurun_out/r2_41/bench_$c.json 2> gpurun_out/r2_41/bench_$c.err; echo "$c rc=$?"; head -c 300 gpurun_out/r2_41/bench_$c.json; echo; done
+timeout 900 python bench.py --config C4 --epoch --steps 5 --warmup 3 > gpurun_out/r2_41/bench_C4_epoch.json 2> gpurun_out/r2_41/bench_C4_epoch.err; echo "C4 epoch rc=$?"; head -c 300 gpurun_out/r2_41/bench_C4_epoch.json; echo
+timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/r2_41/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2_41/pytest_gpu.log
+timeout 1200 ncu --set full --clock-control none --import-source on \
+    -k regex:"dp_pass_kernel|seg_sort_kernel|gtab_bins_kernel" -c 3 -o gpurun_out/r2_41/c3 -f \
+    python tools/quick_bench.py C3:296 > gpurun_out/r2_41/ncu.log 2>&1; echo "ncu rc=$?"; tail -2 gpurun_out/r2_41/ncu.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_41/launches_c3.csv \
+    python bench.py --steps 2 --warmup 3 > gpurun_out/r2_41/launch.log 2>&1; echo "launches rc=$?"
