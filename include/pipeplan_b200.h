@@ -125,10 +125,11 @@ typedef struct pp_tuning {
                               32-column chunk whose slices all exceed the candidate */
   int32_t compact_band;    /* retired (ignored): compact far-chunk records were measured slower
                               than dense tiles; the DP no longer reads them */
-  int32_t host_chunks;     /* host-buffer calls with streams > 1: parts per worker (0 = default
-                              1); the call's samples are uploaded part by part on one copy
-                              stream while `streams` workers plan parts as they arrive and
-                              send plans back on their own copy streams.  Negative values
+  int32_t host_chunks;     /* host-buffer calls with streams > 1: the call's samples are
+                              uploaded part by part on one copy stream while workers plan
+                              parts as they arrive and send plans back on their own copy
+                              streams.  0 (default): 2 x streams workers, one part each;
+                              k > 0: `streams` workers, k parts each.  Negative values
                               select the earlier concurrent-worker pipeline with -host_chunks
                               chunks per worker (A/B only) */
   int32_t dp_pricing;      /* retired (ignored): in-DP slice pricing was measured slower than

@@ -246,13 +246,38 @@ struct PinBuf {
 // copy engine: a host-buffer call keeps the engines busy with tens of MB of
 // samples and plans, and a small cudaMemcpyAsync — pageable or not — can
 // queue behind them for milliseconds while the planning stream waits on it.
-__global__ void small_copy_kernel(const unsigned int* __restrict__ src, unsigned int* __restrict__ dst, size_t words) {
-  for (size_t k = threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
+// Every thread issues its (up to four) 16-byte loads before any store, so a
+// copy of up to 64 KB costs one PCIe round trip, not one per 1 KB.
+__global__ void __launch_bounds__(1024) small_copy_kernel(const unsigned int* __restrict__ src,
+                                                          unsigned int* __restrict__ dst, size_t words) {
+  size_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const size_t nv = words / 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (size_t k = threadIdx.x; k < nv; k += 4 * (size_t)blockDim.x) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t q = k + (size_t)u * blockDim.x;
+        if (q < nv) v[u] = s4[q];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t q = k + (size_t)u * blockDim.x;
+        if (q < nv) d4[q] = v[u];
+      }
+    }
+    done = nv * 4;
+  }
+  for (size_t k = done + threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
 }
 cudaError_t small_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (bytes == 0) return cudaSuccess;
-  small_copy_kernel<<<1, 256, 0, st>>>(static_cast<const unsigned int*>(src), static_cast<unsigned int*>(dst),
-                                       (bytes + 3) / 4);
+  const size_t words = (bytes + 3) / 4;
+  const unsigned threads = words >= 4096 ? 1024u : words >= 512 ? 256u : 64u;
+  small_copy_kernel<<<1, threads, 0, st>>>(static_cast<const unsigned int*>(src), static_cast<unsigned int*>(dst),
+                                           words);
   return cudaGetLastError();
 }
 
@@ -2348,9 +2373,15 @@ int pp_plan_grid(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_offse
                              ctx->tuning.streams);
     // parts: host_chunks per worker (default 1: smaller parts plan less
     // efficiently than the upload they hide, profiles/r02/e2e), workers: streams
-    const int per = ctx->tuning.host_chunks > 0 ? ctx->tuning.host_chunks : 1;
+    // default: 2 x streams workers with one part each — the parts start
+    // staggered by their uploads, and more, smaller concurrent parts keep
+    // the GPU busier at both ends of the call (C3, 888 mini-batches,
+    // streams 3: 8.95 ms with 3 workers, 8.30 ms with 6; profiles/r02/e2e)
+    if (ctx->tuning.host_chunks > 0)
+      return plan_host_pieces(ctx, samples, seg_offsets, n_seg, presorted, grid, model, opts, out,
+                              ctx->tuning.host_chunks * ctx->tuning.streams, ctx->tuning.streams);
     return plan_host_pieces(ctx, samples, seg_offsets, n_seg, presorted, grid, model, opts, out,
-                            per * ctx->tuning.streams, ctx->tuning.streams);
+                            2 * ctx->tuning.streams, 2 * ctx->tuning.streams);
   }
   return plan_host(ctx, samples, seg_offsets, n_seg, presorted, grid, model, opts, out);
 }
