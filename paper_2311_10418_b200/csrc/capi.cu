@@ -316,6 +316,7 @@ struct pp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t pstream = nullptr;             // plan_host_pieces: this worker's prioritised stream
   std::string err;
   pp_tuning tuning{};
   pp_stats stats{};
@@ -1705,6 +1706,7 @@ int pp_ctx_destroy(pp_ctx* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->kev) cudaEventDestroy(e);
+  if (ctx->pstream) cudaStreamDestroy(ctx->pstream);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PP_OK;
@@ -2064,6 +2066,22 @@ int plan_host_pieces(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_o
     if (rc != PP_OK) return fail(ctx, rc, "cannot create a sub-context");
     ctx->subs.push_back(sub);
   }
+  // later parts plan on higher-priority streams: their samples arrive last,
+  // so their kernels go ahead of earlier parts' when both are ready and the
+  // call's tail (the last part's planning + download) shrinks
+  static const bool prio_on = std::getenv("PP_HOST_NO_PRIO") == nullptr;
+  int p_least = 0, p_greatest = 0;
+  if (prio_on) PP_CUDA(cudaDeviceGetStreamPriorityRange(&p_least, &p_greatest));
+  std::vector<cudaStream_t> wstream(workers);
+  for (int w = 0; w < workers; ++w) {
+    pp_ctx* sub = ctx->subs[w];
+    if (prio_on && !sub->pstream) {
+      const int span = p_least - p_greatest;  // (priorities count down)
+      const int prio = p_least - (workers > 1 ? w * span / (workers - 1) : 0);
+      PP_CUDA(cudaStreamCreateWithPriority(&sub->pstream, cudaStreamNonBlocking, prio));
+    }
+    wstream[w] = prio_on ? sub->pstream : sub->stream;
+  }
   if (!ctx->cstream) PP_CUDA(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
   while ((int)ctx->piece_ev.size() < parts) {
     cudaEvent_t e;
@@ -2109,6 +2127,12 @@ int plan_host_pieces(pp_ctx* ctx, const pp_sample* samples, const int64_t* seg_o
       cudaSetDevice(sub->device);
       sub->tuning = ctx->tuning;
       sub->tuning.streams = 1;
+      struct Restore {  // the sub-context's own stream back after the call
+        pp_ctx* c;
+        cudaStream_t s;
+        ~Restore() { c->stream = s; }
+      } restore{sub, sub->stream};
+      sub->stream = wstream[w];
       pp_stats S{};
       S.exit_thresh = INFINITY;
       int rc = PP_OK;

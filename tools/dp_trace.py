@@ -54,6 +54,19 @@ def main():
     per = np.diff(t[:, 0])
     print(f"  {'block period':32s} {np.median(per):8.0f} {per.mean():8.0f}")
     print(f"  total {t[-1, 5] - t[0, 0]} cycles")
+    # the two halves per block: chain (partials, triangle, stores) vs worker 0
+    # (far-far + its fold; blocks whose worker stamps were written)
+    w_ok = (t[:, 8] > 0) & (t[:, 10] >= t[:, 8])
+    ch = d(0, 4)
+    wk = np.where(w_ok, t[:, 10] - t[:, 8], 0)
+    print(f"  sum chain path {ch.sum()}  sum worker path {wk.sum()}  sum max {np.maximum(ch, wk).sum()}"
+          f"  sum period {per.sum()}")
+    q = max(1, len(t) // 8)
+    print("  per eighth of the blocks (mean chain / worker / period):")
+    for a in range(0, len(t), q):
+        sl = slice(a, min(a + q, len(t)))
+        pp = per[a:min(a + q, len(per))]
+        print(f"    blocks {a:4d}+: {ch[sl].mean():7.0f} {wk[sl].mean():7.0f} {pp.mean() if len(pp) else 0:7.0f}")
 
 
 if __name__ == "__main__":
