@@ -186,6 +186,73 @@ __device__ void radix_pass(const KT* __restrict__ kin, const VT* __restrict__ vi
   __syncthreads();
 }
 
+// One stable LSD pass with a 7-bit digit (one key word): warp w owns the
+// contiguous item range [w * per, (w + 1) * per) and ranks its items 32 at a
+// time with __match_any_sync (peers with the same digit; rank = peers below
+// this lane) against warp-private counters in shared memory; an exclusive
+// scan over (digit, warp) in digit-major order turns the counts into
+// starting positions, and a second sweep scatters.  Items keep their order
+// within a digit (warps own contiguous ranges, ranks follow lane order), so
+// the pass is stable: two passes sort a 14-bit key where 2-bit passes took
+// seven block scans each.  cnt: [warps][kDig7] ints.
+constexpr int kDig7 = 128;
+template <class KT, class VT>
+__device__ void radix_pass7(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restrict__ kout,
+                            VT* __restrict__ vout, int n, int sh, int* cnt, unsigned long long* warp_tot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int per = (n + nw - 1) / nw;
+  const int wb = min(n, wid * per), we = min(n, wb + per);
+  int* my = cnt + wid * kDig7;
+  for (int d = lane; d < kDig7; d += 32) my[d] = 0;
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int k0 = wb; k0 < we; k0 += 32) {
+    const int k = k0 + lane;
+    const unsigned d = k < we ? (unsigned)((kin[k] >> sh) & (kDig7 - 1)) : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (d != 0xffffffffu && (peers & lt) == 0) my[d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive scan over entries e = d * nw + w (digit-major), 4 per thread
+  {
+    const int total = kDig7 * nw;
+    const int e0 = threadIdx.x * 4;
+    int v[4], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = e0 + q;
+      v[q] = e < total ? cnt[(e % nw) * kDig7 + e / nw] : 0;
+      sum += v[q];
+    }
+    unsigned long long tot;
+    int run = (int)block_exscan((unsigned long long)sum, warp_tot, tot);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = e0 + q;
+      if (e < total) cnt[(e % nw) * kDig7 + e / nw] = run;
+      run += v[q];
+    }
+  }
+  __syncthreads();
+  for (int k0 = wb; k0 < we; k0 += 32) {
+    const int k = k0 + lane;
+    const bool ok = k < we;
+    const unsigned d = ok ? (unsigned)((kin[k] >> sh) & (kDig7 - 1)) : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    int pos = 0;
+    if (ok) pos = my[d] + __popc(peers & lt);
+    __syncwarp();
+    if (ok) {
+      kout[pos] = kin[k];
+      vout[pos] = vin[k];
+      if ((peers & lt) == 0) my[d] += __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
 // Builds keys for segment `seg`, sorts, and gathers ordered samples + SoA
 // double lengths.  `range` holds the biased field minima/maxima of the call.
 // KT / VT: key and index types.  uint32 keys + uint16 indices (12 B per
@@ -200,6 +267,7 @@ __global__ void __launch_bounds__(kSortThreads)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long warp_tot[kSortThreads / 32];
   __shared__ int bucket[4];
+  __shared__ int dig_cnt[W == 1 ? (kSortThreads / 32) * kDig7 : 1];
   const int s = blockIdx.x;
   const int64_t b = seg_off[s];
   const int n = (int)(seg_off[s + 1] - b);
@@ -247,7 +315,7 @@ __global__ void __launch_bounds__(kSortThreads)
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     long long lo = s_rng[0][q], hi = s_rng[0][3 + q];
-    for (int w = 1; w < kSortThreads / 32; ++w) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
       lo = min(lo, s_rng[w][q]);
       hi = max(hi, s_rng[w][3 + q]);
     }
@@ -288,8 +356,8 @@ __global__ void __launch_bounds__(kSortThreads)
   __syncthreads();
   if (W == 1) {
     const int total = bits[0] + bits[1] + bits[2];
-    for (int sh = 0; sh < total; sh += 2) {
-      radix_pass<1, true, KT, VT>(k0, v0, k1, v1, n, 0, sh, warp_tot, bucket);
+    for (int sh = 0; sh < total; sh += 7) {
+      radix_pass7<KT, VT>(k0, v0, k1, v1, n, sh, dig_cnt, warp_tot);
       KT* tk = k0; k0 = k1; k1 = tk;
       VT* tv = v0; v0 = v1; v1 = tv;
     }
@@ -416,11 +484,14 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
   // ids increasing over the call => increasing in every segment, so each
   // segment's key is (input, target) only: 32-bit keys when those fit
   const bool key32 = h_range[6] == 0 && fbits[0] + fbits[1] <= 32 && max_n <= 65536;
+  // one-word keys (radix_pass7, any warp count): small segments take
+  // smaller CTAs, more of them per SM (C1: 256 samples per segment)
+  const int t1 = max_n <= 1024 ? 128 : max_n <= 4096 ? 256 : kSortThreads;
   if (key32) {
     const size_t need = (size_t)max_n * (2 * 4 + 2 * 2);
     const int sm = need <= 200 * 1024 ? 1 : 0;
     ensure_dyn_smem((const void*)seg_sort_kernel<1, uint32_t, uint16_t>, sm ? need : 0);
-    seg_sort_kernel<1, uint32_t, uint16_t><<<n_seg, kSortThreads, sm ? need : 0, st>>>(
+    seg_sort_kernel<1, uint32_t, uint16_t><<<n_seg, t1, sm ? need : 0, st>>>(
         d_in, d_seg_off, d_range, reinterpret_cast<uint32_t*>(d_keys), reinterpret_cast<uint16_t*>(d_vals), sm,
         d_out, d_in_len, d_tgt_len, d_perm);
     return cudaGetLastError();
@@ -430,7 +501,7 @@ cudaError_t launch_segmented_sort(const pp_sample* d_in, const int64_t* d_seg_of
   const size_t smem = use_smem ? smem_need : 0;
   if (W == 1) {
     ensure_dyn_smem((const void*)seg_sort_kernel<1>, smem);
-    seg_sort_kernel<1><<<n_seg, kSortThreads, smem, st>>>(d_in, d_seg_off, d_range, d_keys, d_vals,
+    seg_sort_kernel<1><<<n_seg, t1, smem, st>>>(d_in, d_seg_off, d_range, d_keys, d_vals,
                                                           use_smem, d_out, d_in_len, d_tgt_len, d_perm);
   } else {
     ensure_dyn_smem((const void*)seg_sort_kernel<3>, smem);
