@@ -401,6 +401,8 @@ def run_ours(args, rank, world, local):
         host_out = capi.Planner.plan_buffers(tot, M, pinned_alloc, order_only=True)
         h2d = tot * 24 + seg.nbytes
         d2h = tot * (4 + 4 + 8) + M * (4 + 8 + 8 + 4 + 8)
+        e2e_streams = args.e2e_streams or args.streams
+        planner.set_tuning(streams=e2e_streams)
         for g in range(warm):
             planner.plan_batch(pin_np[g * tot:(g + 1) * tot], seg, grid, model, cfg.stages, 1, cfg.mem_cap,
                                cfg.interval, out=host_out)
@@ -419,7 +421,7 @@ def run_ours(args, rank, world, local):
             # call's uploads and downloads overlap another's planning
             plans = [planner] + [capi.Planner(local) for _ in range(callers - 1)]
             for pl in plans[1:]:
-                pl.set_tuning(streams=args.streams)
+                pl.set_tuning(streams=e2e_streams)
             outs = [host_out] + [capi.Planner.plan_buffers(tot, M, pinned_alloc, order_only=True)
                                  for _ in range(callers - 1)]
             for c in range(1, callers):  # (warm-up of the extra contexts)
@@ -634,6 +636,7 @@ def main():
     ap.add_argument("--cpu-plans", type=int, default=0, help="cpu_baseline / parity sample (0: cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=3, help="concurrent sub-batches per GPU")
+    ap.add_argument("--e2e-streams", type=int, default=0, help="streams of the e2e calls (0: --streams)")
     ap.add_argument("--e2e-callers", type=int, default=2,
                     help="host threads issuing the e2e pp_plan_grid calls (alternate steps)")
     ap.add_argument("--chunk", type=int, default=0, help="mini-batches per planning call (0: all; epoch: 1024)")
