@@ -401,8 +401,9 @@ def run_ours(args, rank, world, local):
         host_out = capi.Planner.plan_buffers(tot, M, pinned_alloc, order_only=True)
         h2d = tot * 24 + seg.nbytes
         d2h = tot * (4 + 4 + 8) + M * (4 + 8 + 8 + 4 + 8)
-        e2e_streams = args.e2e_streams or args.streams
-        planner.set_tuning(streams=e2e_streams)
+        # one caller: the library's own host pipeline (--streams workers);
+        # several callers: --e2e-streams each (default 1: the callers are the pipeline)
+        e2e_streams = args.e2e_streams or 1
         for g in range(warm):
             planner.plan_batch(pin_np[g * tot:(g + 1) * tot], seg, grid, model, cfg.stages, 1, cfg.mem_cap,
                                cfg.interval, out=host_out)
@@ -420,11 +421,11 @@ def run_ours(args, rank, world, local):
             # c, c + C, ... through its own context and pinned buffers, so one
             # call's uploads and downloads overlap another's planning
             plans = [planner] + [capi.Planner(local) for _ in range(callers - 1)]
-            for pl in plans[1:]:
+            for pl in plans:
                 pl.set_tuning(streams=e2e_streams)
             outs = [host_out] + [capi.Planner.plan_buffers(tot, M, pinned_alloc, order_only=True)
                                  for _ in range(callers - 1)]
-            for c in range(1, callers):  # (warm-up of the extra contexts)
+            for c in range(callers):  # (warm-up of every context at this tuning)
                 plans[c].plan_batch(pin_np[:tot], seg, grid, model, cfg.stages, 1, cfg.mem_cap, cfg.interval,
                                     out=outs[c])
             errs = []
@@ -449,8 +450,10 @@ def run_ours(args, rank, world, local):
             for pl in plans[1:]:
                 pl.close()
             e2e_api = {"api": f"pp_plan_grid (host buffers; pinned samples in, plans out) from {callers} "
-                              "concurrent host threads, one context each, alternate steps (run_plan's pool pattern)",
-                       "callers": callers, "single_caller_value": e2e_single}
+                              f"concurrent host threads (one context each, streams={e2e_streams}), step g on "
+                              "thread g mod callers: run_plan's pool pattern",
+                       "callers": callers, "single_caller_value": e2e_single,
+                       "single_caller_streams": args.streams}
         # pinned outputs: splits / mb_times come back as each segment's valid
         # prefix (count[s] entries, prefix_out_kernel), the order in full
         d2h = tot * 4 + int(host_out["count"].astype(np.int64).sum()) * (4 + 8) + M * (4 + 8 + 8 + 4 + 8)
@@ -636,8 +639,8 @@ def main():
     ap.add_argument("--cpu-plans", type=int, default=0, help="cpu_baseline / parity sample (0: cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=3, help="concurrent sub-batches per GPU")
-    ap.add_argument("--e2e-streams", type=int, default=0, help="streams of the e2e calls (0: --streams)")
-    ap.add_argument("--e2e-callers", type=int, default=2,
+    ap.add_argument("--e2e-streams", type=int, default=1, help="streams of each concurrent e2e caller")
+    ap.add_argument("--e2e-callers", type=int, default=8,
                     help="host threads issuing the e2e pp_plan_grid calls (alternate steps)")
     ap.add_argument("--chunk", type=int, default=0, help="mini-batches per planning call (0: all; epoch: 1024)")
     args = ap.parse_args()
