@@ -304,24 +304,44 @@ def run_ours(args, rank, world, local):
     d_seg_c = torch.from_numpy(seg_c).to(dev)
     per_sample = ("ordered", "order", "splits", "mb_times")
 
-    def plan_into(src):
+    # concurrent callers (one GPU, no collective): caller c has its own
+    # context, stream and output buffers and plans steps c, c + C, ... from
+    # its own host thread — run_plan's pool pattern; caller 0 is `planner`
+    callers = max(1, args.callers) if (world == 1 and not epoch) else 1
+    args.callers_used = callers
+    cplans, cstreams, couts, cslots = [planner], [stream], [out], [slots]
+    for _ in range(callers - 1):
+        pl = capi.Planner(local)
+        st_c = torch.cuda.Stream(device=dev)
+        pl.set_stream(st_c.cuda_stream)
+        cplans.append(pl)
+        cstreams.append(st_c)
+        couts.append({k: torch.empty_like(v) for k, v in out.items()})
+        cslots.append(torch.empty_like(slots))
+    for pl in cplans:
+        pl.set_tuning(streams=args.caller_streams if callers > 1 else args.streams)
+
+    def plan_into(src, c=0):
+        pl, o_all, sl_all = cplans[c], couts[c], cslots[c]
         for c0 in range(0, M, chunk):
             mc = min(chunk, M - c0)
-            o = {k: (v[c0 * n:(c0 + mc) * n] if k in per_sample else v[c0:c0 + mc]) for k, v in out.items()}
-            shard.plan_shard_device(planner, src[c0 * n:(c0 + mc) * n], n, mc, grid, model, cfg.stages, 1,
+            o = {k: (v[c0 * n:(c0 + mc) * n] if k in per_sample else v[c0:c0 + mc]) for k, v in o_all.items()}
+            shard.plan_shard_device(pl, src[c0 * n:(c0 + mc) * n], n, mc, grid, model, cfg.stages, 1,
                                     cfg.mem_cap, cfg.interval, o, d_seg_c[:mc + 1], seg_c[:mc + 1],
-                                    slots[c0:c0 + mc])
-        return slots
+                                    sl_all[c0:c0 + mc])
+        return sl_all
 
-    def step(g):
+    def step(g, c=0):
         base = (g % groups) * tot
-        with torch.cuda.stream(stream):
-            sl = plan_into(d_samples[base:base + tot])
+        with torch.cuda.stream(cstreams[c]):
+            sl = plan_into(d_samples[base:base + tot], c)
             if world > 1:  # the only collective: one all_gather of the plans per step
                 gathered["slots"] = (shard.gather_epoch(sl, M_total) if epoch else shard.gather_plans(sl))
 
     for g in range(warm):
         step(g)
+    for c in range(1, callers):
+        step(c, c)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -331,9 +351,33 @@ def run_ours(args, rank, world, local):
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
-        for g in range(warm, warm + steps):
-            step(g)
-            stats.append(planner.stats())
+        if callers == 1:
+            for g in range(warm, warm + steps):
+                step(g)
+                stats.append(planner.stats())
+        else:
+            per = [[] for _ in range(callers)]
+            errs = []
+
+            def run(c):
+                try:
+                    cstreams[c].wait_event(ev0)
+                    for g in range(warm + c, warm + steps, callers):
+                        step(g, c)
+                        per[c].append(cplans[c].stats())
+                except BaseException as e:  # noqa: BLE001 - re-raised below
+                    errs.append(e)
+
+            ths = [threading.Thread(target=run, args=(c,)) for c in range(callers)]
+            for th in ths:
+                th.start()
+            for th in ths:
+                th.join()
+            if errs:
+                raise errs[0]
+            for c in range(1, callers):
+                stream.wait_stream(cstreams[c])
+            stats = [x for p_ in per for x in p_]
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -404,6 +448,7 @@ def run_ours(args, rank, world, local):
         # one caller: the library's own host pipeline (--streams workers);
         # several callers: --e2e-streams each (default 1: the callers are the pipeline)
         e2e_streams = args.e2e_streams or 1
+        planner.set_tuning(streams=args.streams)
         for g in range(warm):
             planner.plan_batch(pin_np[g * tot:(g + 1) * tot], seg, grid, model, cfg.stages, 1, cfg.mem_cap,
                                cfg.interval, out=host_out)
@@ -607,7 +652,10 @@ def report(args, cfg, W, capi, planner, stats, solo_stats, M, M_total, world, st
         "setup": {"minibatches_per_gpu_per_step": M, "minibatches_per_step": M_total,
                   "parallelism": (f"epoch sharded x{world} (shard_range), one NCCL all_gather of plan slots"
                                   if args.epoch else f"mini-batch sharding x{world}, NCCL plan gather"),
-                  "concurrent_sub_batches": args.streams},
+                  "concurrent_sub_batches": args.streams,
+                  "device_callers": getattr(args, "callers_used", 1),
+                  "device_caller_streams": args.caller_streams if getattr(args, "callers_used", 1) > 1
+                  else args.streams},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 **(e2e_api if isinstance(e2e_api, dict) else {"api": e2e_api})},
         "gpu_launches": int(launches.sum()) + int(launches[0]),  # + one slot-pack kernel per planning call
@@ -638,7 +686,10 @@ def main():
     ap.add_argument("--per-gpu", type=int, default=0, help="mini-batches per GPU per step (weak mode)")
     ap.add_argument("--cpu-plans", type=int, default=0, help="cpu_baseline / parity sample (0: cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=3, help="concurrent sub-batches per GPU")
+    ap.add_argument("--streams", type=int, default=3, help="concurrent sub-batches per planning call")
+    ap.add_argument("--callers", type=int, default=8,
+                    help="device-resident measurement: host threads issuing planning calls (alternate steps)")
+    ap.add_argument("--caller-streams", type=int, default=1, help="streams per call with --callers > 1")
     ap.add_argument("--e2e-streams", type=int, default=1, help="streams of each concurrent e2e caller")
     ap.add_argument("--e2e-callers", type=int, default=8,
                     help="host threads issuing the e2e pp_plan_grid calls (alternate steps)")
