@@ -307,7 +307,9 @@ def run_ours(args, rank, world, local):
     # concurrent callers (one GPU, no collective): caller c has its own
     # context, stream and output buffers and plans steps c, c + C, ... from
     # its own host thread — run_plan's pool pattern; caller 0 is `planner`
-    callers = max(1, args.callers) if (world == 1 and not epoch) else 1
+    # (one caller for very long mini-batches: each pass is already a
+    # whole-GPU cooperative kernel, and a context holds a multi-GB band)
+    callers = max(1, args.callers) if (world == 1 and not epoch and cfg.n < 16384) else 1
     args.callers_used = callers
     cplans, cstreams, couts, cslots = [planner], [stream], [out], [slots]
     for _ in range(callers - 1):
@@ -459,7 +461,7 @@ def run_ours(args, rank, world, local):
         e2e_single = M * steps / (time.perf_counter() - t0)
         e2e_value = e2e_single
         e2e_api = "pp_plan_grid (host buffers; pinned samples in, plans out)"
-        callers = max(1, args.e2e_callers)
+        callers = max(1, args.e2e_callers) if cfg.n < 16384 else 1
         if callers > 1:
             # concurrent callers, as the reference's run_plan drives
             # plan_iteration from a thread pool: caller c plans steps
