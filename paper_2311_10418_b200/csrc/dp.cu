@@ -72,17 +72,12 @@ constexpr int kSyncThreads = 32 * (1 + kWorkers);    // workers + chain (block b
 // Warp roles.  The SM sub-partition scheduler picks the highest warp id
 // first among eligible warps, so the serial chain warp gets the highest id:
 // it is the critical path and must never lose an issue slot to a worker.
-constexpr int kProducerWarp = kWorkers;      // warp 8
-constexpr int kChainWarp = kWorkers + 1;     // warp 9
-// Named barriers: 1 = block barrier (chain + workers),
-// and on the slice-table path the unit hand-off between the producer and the
-// chain warp (64 threads): full[k] = 3 + k (producer arrives after its
-// stores, the chain syncs), empty[k] = 5 + k (the chain arrives after its
-// reads, the producer syncs before refilling buffer k).  Generic-proxy
-// stores ordered by bar.arrive / bar.sync: nothing for racecheck to flag,
-// unlike TMA writes ordered through an mbarrier (the band path).
-constexpr int kBarUnitFull = 3, kBarUnitEmpty = 5;
-// 7 + w (w < 4): worker w + 4 hands its far-far partial to worker w.
+constexpr int kProducerWarp = kWorkers;      // warp 8 (band path)
+constexpr int kChainWarp = kWorkers + 1;     // warp 9 (band path; warp 8 on the slice-table path)
+// Named barriers: 1 = block barrier (chain + workers; on the slice-table path
+// it also hands the chain the unit the workers copied with cp.async);
+// 7 + w (w < 4): worker w + 4 hands its far-far partial to worker w.  The
+// band path orders its TMA unit and chunk copies through mbarriers.
 constexpr int kBarPair = 7;
 
 #ifdef PP_DP_TRACE
