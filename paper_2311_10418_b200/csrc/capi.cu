@@ -77,7 +77,7 @@ cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* 
 cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int* gbase,
                              const int* need, const double* G, double interval, const double* tau,
                              unsigned int* small_bm, SegStats* stats, int nK, const int64_t* row_off, int* rf,
-                             double* rlo, cudaStream_t st);
+                             double* rlo, int max_n, cudaStream_t st);
 cudaError_t launch_full_rows(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
                              int* row_w, int* blk_W, cudaStream_t st);
 cudaError_t launch_band_cand(const int64_t* seg_off, const int* blk_base, int n_seg, int total_blocks,
@@ -980,7 +980,7 @@ int cost_pass_a(pp_ctx* ctx, const PlanCall& c, const CostGrid& g, double interv
                                  ctx->gt_need.as<int>(), ctx->gt_G.as<double>(), interval, tau_d, small_bm,
                                  ctx->stats_d.as<SegStats>(), nK, ctx->gt_off.as<int64_t>(),
                                  ctx->tuning.no_bin_intervals ? nullptr : ctx->gt_rf.as<int>(),
-                                 ctx->gt_rlo.as<double>(), st));
+                                 ctx->gt_rlo.as<double>(), max_n, st));
     ctx->gtab = true;
     ctx->price = DpPrice{};
     ctx->price.gbase = ctx->gt_base.as<int>();

@@ -292,7 +292,11 @@ __global__ void __launch_bounds__(32 * kGWarps) gtab_rowinfo_kernel(int nK, cons
 // non-NaN ones (one division per bin change of a lane, thresholds tau), the
 // largest singleton time (SegStats::tsingle, dp.cu seg_init_kernel), the
 // range of out-of-bitmap bins (then the call falls back to the band).
-__global__ void __launch_bounds__(256) gtab_bins_kernel(const int64_t* __restrict__ seg_off,
+// One CTA per segment, up to 32 warps: the row loop is a chain of dependent
+// loads (length, run key, table base, row entries), so occupancy hides it
+// (8 warps per CTA left the SMs at a quarter of their warp slots on C3).
+constexpr int kBinsThreads = 1024;
+__global__ void __launch_bounds__(kBinsThreads) gtab_bins_kernel(const int64_t* __restrict__ seg_off,
                                                         const double* __restrict__ in_d,
                                                         const int* __restrict__ gbase,
                                                         const int* __restrict__ need,
@@ -469,14 +473,16 @@ cudaError_t launch_gtab_gbase(const double* in_d, int64_t total, const int64_t* 
 cudaError_t launch_gtab_bins(const int64_t* seg_off, int n_seg, const double* in_d, const int* gbase,
                              const int* need, const double* G, double interval, const double* tau,
                              unsigned int* small_bm, SegStats* stats, int nK, const int64_t* row_off, int* rf,
-                             double* rlo, cudaStream_t st) {
+                             double* rlo, int max_n, cudaStream_t st) {
   if (rf) {
     const int blocks = std::max(1, std::min((nK + kGWarps - 1) / kGWarps, 148 * 8));
     gtab_rowinfo_kernel<<<blocks, 32 * kGWarps, 0, st>>>(nK, need, row_off, G, interval, rf, rlo);
   }
+  // long segments take 32 warps (C3: 0.15 -> 0.11 ms per 296); short ones 8
+  // (C1's 256-sample segments were slower at 32)
   if (n_seg > 0)
-    gtab_bins_kernel<<<n_seg, 256, 0, st>>>(seg_off, in_d, gbase, need, G, interval, tau, small_bm, stats, rf,
-                                            rlo);
+    gtab_bins_kernel<<<n_seg, max_n >= 4096 ? kBinsThreads : 256, 0, st>>>(seg_off, in_d, gbase, need, G, interval,
+                                                                           tau, small_bm, stats, rf, rlo);
   return cudaGetLastError();
 }
 

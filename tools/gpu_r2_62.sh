@@ -1,0 +1,5 @@
+# candidate-bin kernel at 32 warps per CTA
+mkdir -p gpurun_out/r2_62
+timeout 1500 python -m pytest tests/test_parity_gpu.py -x -q > gpurun_out/r2_62/pytest.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/r2_62/pytest.log
+for c in "C3 296" "C4 512" "C1 2048"; do timeout 600 python tools/ab_bench.py $c "slice_table=1" 2>&1; done | tee gpurun_out/r2_62/ab.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gtab_bins --csv python tools/quick_bench.py C3:296 2>/dev/null | grep gtab_bins | tail -2
