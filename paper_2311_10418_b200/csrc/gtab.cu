@@ -82,7 +82,7 @@ __global__ void gtab_need_kernel(const int64_t* __restrict__ seg_off, const int*
 // the walk stops at the first block with E >= pe + 1 (every later block has
 // a larger i0, hence a smaller column).  No monotonicity is assumed.
 constexpr int kNeedMaxBlocks = 4096;
-__global__ void __launch_bounds__(256) gtab_need_runs_kernel(const int64_t* __restrict__ seg_off,
+__global__ void __launch_bounds__(1024) gtab_need_runs_kernel(const int64_t* __restrict__ seg_off,
                                                              const int* __restrict__ blk_base,
                                                              const int* __restrict__ blk_W,
                                                              const double* __restrict__ in_d,
@@ -440,7 +440,8 @@ cudaError_t launch_gtab_need(const int64_t* seg_off, const int* blk_base, int n_
     const size_t smem = (size_t)3 * max_blocks * sizeof(int);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(gtab_need_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gtab_need_runs_kernel<<<n_seg, 256, smem, st>>>(seg_off, blk_base, blk_W, in_d, need);
+    // (long segments: 32 warps to hide the dependent bisection loads, as gtab_bins_kernel)
+    gtab_need_runs_kernel<<<n_seg, max_blocks >= 128 ? 1024 : 256, smem, st>>>(seg_off, blk_base, blk_W, in_d, need);
     return cudaGetLastError();
   }
   const int blocks = std::max(1, std::min((total_blocks + 7) / 8, 148 * 16));
