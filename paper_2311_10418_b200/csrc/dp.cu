@@ -79,6 +79,8 @@ constexpr int kChainWarp = kWorkers + 1;     // warp 9 (band path; warp 8 on the
 // 7 + w (w < 4): worker w + 4 hands its far-far partial to worker w.  The
 // band path orders its TMA unit and chunk copies through mbarriers.
 constexpr int kBarPair = 7;
+// 11 + w (w < 2): worker w + 2 hands its (already paired) partial to worker w.
+constexpr int kBarPair2 = 11;
 
 #ifdef PP_DP_TRACE
 __device__ long long* g_dp_trace = nullptr;  // [block][16] clock64 stamps of CTA 0
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(dp_threads<GTAB>(), 2)
       Acc A = N;
       {  // the worker partials of this block's far-far columns (four: workers
          // 0-3 folded in 4-7's), a pairwise tree
-        constexpr int kParts = kWorkers / 2;
+        constexpr int kParts = kWorkers / 4;
         Acc v[kParts];
 #pragma unroll
         for (int q = 0; q < kParts; ++q) {
@@ -720,11 +722,23 @@ __global__ void __launch_bounds__(dp_threads<GTAB>(), 2)
           named_bar_arrive(kBarPair + (w - half), 64);
         } else {
           named_bar(kBarPair + w, 64);
-          const int o = ((bn & 1) * kWorkers + w + half) * kRB + lane;
-          Acc p{wps[o], X2 ? wpx[o] : INF, CAND ? wpc[o] : 0, CAND && !KEYED ? wpj[o] : INT_MAX};
-          if (KEYED) combine_k<MODE>(a0, p);
-          else combine<MODE>(a0, p);
-          put(w, a0);
+          auto take = [&](int from) {
+            const int o = ((bn & 1) * kWorkers + from) * kRB + lane;
+            Acc p{wps[o], X2 ? wpx[o] : INF, CAND ? wpc[o] : 0, CAND && !KEYED ? wpj[o] : INT_MAX};
+            if (KEYED) combine_k<MODE>(a0, p);
+            else combine<MODE>(a0, p);
+          };
+          take(w + half);
+          // a second level: workers 2-3 hand theirs to 0-1, the chain folds two
+          if (w >= 2) {
+            put(w, a0);
+            __syncwarp();
+            named_bar_arrive(kBarPair2 + (w - 2), 64);
+          } else {
+            named_bar(kBarPair2 + w, 64);
+            take(w + 2);
+            put(w, a0);
+          }
         }
         if (w == 0) PP_TRACE(10);
       }
